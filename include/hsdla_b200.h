@@ -1,0 +1,156 @@
+/* hsdla_b200 — B200-native (sm_100a) HSDLA Hamiltonian/Overlap construction.
+ *
+ * The C-ABI drop-in boundary for the reference's hot path
+ *   hsdla::pipeline::build_hs_refined(const ProblemInstance&, const PipelineConfig&) -> HSResult
+ *   (/root/reference/proj/include/hsdla/pipeline.hpp:55, src/pipeline.cpp:281-329)
+ * Plain pointers and sizes only; no exceptions cross it.  Status codes map onto
+ * the reference exception taxonomy (proj/include/hsdla/errors.hpp:9-26); the
+ * message of the last failure on the calling thread is hsdla_b200_last_error().
+ *
+ * Storage contract (proj/include/hsdla/complex_matrix.hpp:11-31, problem.hpp:16-27):
+ *   complex numbers are interleaved (re, im) doubles (std::complex<double>);
+ *   A, B      : (n_atoms*n_l) x n_g, column-major, ld = n_atoms*n_l, atom blocks
+ *               stacked rowwise (block a = rows [a*n_l, (a+1)*n_l));
+ *   T_AA/T_AB/T_BB : n_atoms contiguous n_l x n_l column-major blocks; T_AA and
+ *               T_BB are read from their LOWER triangles only (kernels.cpp:152-167);
+ *               T^[BA] is never stored, it is T_AB^H (problem.hpp:15);
+ *   U         : n_atoms*n_l reals (atom-major), S uses (U B)^H (U B) (pipeline.cpp:298-300);
+ *   H, S      : n_g x n_g column-major; ONLY i >= j is written (lower triangle
+ *               authoritative, complex_matrix.hpp:48-49), the strict upper
+ *               triangle is never read or written, diagonal imaginary parts are
+ *               exactly 0 (kernels.cpp:112,130,145).
+ */
+#ifndef HSDLA_B200_H
+#define HSDLA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (errors.hpp:9-26) ---------------------------------- */
+#define HSDLA_B200_OK 0
+#define HSDLA_B200_DIMENSION_ERROR 1 /* hsdla::DimensionError */
+#define HSDLA_B200_SIZING_ERROR 2    /* hsdla::SizingError (incl. device out of memory) */
+#define HSDLA_B200_CONFIG_ERROR 3    /* hsdla::ConfigError */
+#define HSDLA_B200_IO_ERROR 4        /* hsdla::IoError */
+#define HSDLA_B200_CUDA_ERROR 5      /* CUDA runtime / launch failure */
+#define HSDLA_B200_NCCL_ERROR 6      /* NCCL failure */
+
+/* ---- algorithms ------------------------------------------------------- */
+/* Reference phase order s, z_loop, her2k, hemm_loop, herkx; five launches of the
+ * contraction engine, executed flops == the reference ledger. */
+#define HSDLA_B200_ALGO_REFINED 1
+/* Same products; her2k and herkx run as ONE lower-triangular contraction over
+ * the stacked inner dimension [Z;B;A]^H [B;Z;X] (default).  Executed flops ==
+ * ledger; the herkx phase reports 0 s (fused into her2k). */
+#define HSDLA_B200_ALGO_REFINED_FUSED 0
+
+/* Problem (ProblemInstance, problem.hpp:16-27). */
+typedef struct hsdla_b200_problem {
+  uint64_t n_atoms, n_l, n_g;
+  const double* A;    /* 2 * n_atoms*n_l * n_g doubles */
+  const double* B;    /* same */
+  const double* T_AA; /* 2 * n_atoms * n_l*n_l doubles */
+  const double* T_AB;
+  const double* T_BB;
+  const double* U;    /* n_atoms * n_l doubles */
+} hsdla_b200_problem;
+
+/* Options (PipelineConfig, pipeline.hpp:22-30, with the B200 strategy fields). */
+typedef struct hsdla_b200_options {
+  int n_gpus;             /* 0 or 1: one GPU; >1: atoms sharded, NCCL reduce to device_ids[0] */
+  const int* device_ids;  /* NULL: devices 0..n_gpus-1 */
+  int algo;               /* HSDLA_B200_ALGO_* */
+  int flags;              /* reserved, 0 */
+} hsdla_b200_options;
+
+/* Phase index order = the reference's phase names (test_pipeline.cpp:167-176). */
+#define HSDLA_B200_PHASE_S 0
+#define HSDLA_B200_PHASE_Z_LOOP 1
+#define HSDLA_B200_PHASE_HER2K 2
+#define HSDLA_B200_PHASE_HEMM_LOOP 3
+#define HSDLA_B200_PHASE_HERKX 4
+
+/* Ledger key order: gemm, hemm, her2k, herk, scaling, herkx, potrf, trmm, total
+ * (flop_ledger.hpp; values == pipeline::flop_model, pipeline.cpp:336-364). */
+typedef struct hsdla_b200_stats {
+  double phase_seconds[5];   /* device (CUDA-event) time per phase, max over GPUs */
+  double h2d_seconds;        /* host->device upload of A, B, T, U */
+  double device_seconds;     /* first phase start .. H,S reduced on the root GPU */
+  double reduce_seconds;     /* NCCL reduce tail after the last contraction (0 on 1 GPU) */
+  double d2h_seconds;        /* packed-triangle download + unpack into H, S */
+  double total_seconds;      /* wall time of the call */
+  uint64_t ledger[9];
+  uint64_t executed_flops;   /* algorithmic flops of the kernels actually run */
+  uint64_t peak_device_bytes;/* device bytes held by the largest shard */
+  uint64_t peak_temp_bytes;  /* device temporaries (the X/Z stacks), cf. HSResult::peak_temp_bytes */
+  int n_gpus;
+  int kernel_launches;       /* launches of this library's kernels in the build */
+} hsdla_b200_stats;
+
+/* ---- the drop-in --------------------------------------------------------
+ * build_hs_refined (pipeline.cpp:281-329) on the GPU(s).  Writes the lower
+ * triangles of the caller-allocated H and S (n_g*n_g complex each, col-major).
+ * Engines (device buffers) are cached per (device, shape) across calls; host
+ * buffers registered with hsdla_b200_host_register() upload at full PCIe rate. */
+int hsdla_b200_build_hs(const hsdla_b200_problem* p, const hsdla_b200_options* opts, double* H,
+                        double* S, hsdla_b200_stats* stats);
+
+/* pipeline::flop_model (pipeline.cpp:336-364). variant: 0 original, 1 refined. */
+int hsdla_b200_flop_model(int variant, uint64_t n_atoms, uint64_t n_l, uint64_t n_g, uint64_t n_hpd,
+                          uint64_t ledger[9]);
+
+/* generate_problem (problem.cpp:79-142), bit-identical to the reference
+ * (std::mt19937_64 + the reference's double mapping).  Output layouts as above;
+ * hpd: n_atoms bytes (hpd_flags). */
+int hsdla_b200_generate_problem(uint64_t n_atoms, uint64_t n_l, uint64_t n_g, uint64_t seed,
+                                uint64_t n_not_hpd, double* A, double* B, double* T_AA, double* T_AB,
+                                double* T_BB, double* U, uint8_t* hpd);
+
+const char* hsdla_b200_last_error(void);
+int hsdla_b200_device_count(int* count);
+int hsdla_b200_host_register(void* ptr, size_t bytes);   /* cudaHostRegister (portable) */
+int hsdla_b200_host_unregister(void* ptr);
+int hsdla_b200_release_cache(void);                      /* free cached engines */
+
+/* ---- device-resident engine (one per GPU / per rank) ---------------------
+ * An engine owns the device copy of one atom shard [atom_begin, atom_end) of a
+ * problem with n_atoms_total atoms, its temporaries and packed-lower partial
+ * H and S.  build() runs the whole hot path on device-resident inputs (the
+ * bench's `value`); download() returns the lower triangles. */
+typedef struct hsdla_b200_engine hsdla_b200_engine;
+
+int hsdla_b200_engine_create(int device, uint64_t n_atoms_local, uint64_t n_l, uint64_t n_g,
+                             hsdla_b200_engine** out);
+int hsdla_b200_engine_destroy(hsdla_b200_engine* e);
+/* H2D of atoms [atom_begin, atom_begin + n_atoms_local) of p (p->n_atoms total). */
+int hsdla_b200_engine_upload(hsdla_b200_engine* e, const hsdla_b200_problem* p, uint64_t atom_begin);
+/* Enqueue the full build (all phases) on the engine stream; asynchronous. */
+int hsdla_b200_engine_build(hsdla_b200_engine* e, int algo);
+/* NCCL sum-reduce of the packed partial H and S to rank `root` (no-op without comm). */
+int hsdla_b200_engine_reduce(hsdla_b200_engine* e, int root);
+/* Wait for the engine's streams; fills phase/device timings of the last build. */
+int hsdla_b200_engine_sync(hsdla_b200_engine* e, hsdla_b200_stats* stats);
+/* D2H of the packed triangles, unpacked into the lower triangles of H, S
+ * (either may be NULL). Synchronous. */
+int hsdla_b200_engine_download(hsdla_b200_engine* e, double* H, double* S);
+/* Packed lower (LAPACK 'L' packed, column-major) device pointers of H and S. */
+int hsdla_b200_engine_device_results(hsdla_b200_engine* e, void** Hp, void** Sp);
+/* The cudaStream_t the engine launches on. */
+int hsdla_b200_engine_stream(hsdla_b200_engine* e, void** stream);
+/* NCCL: one communicator per engine (one rank per GPU; id from rank 0). */
+int hsdla_b200_nccl_unique_id(void* id128);
+int hsdla_b200_engine_set_comm(hsdla_b200_engine* e, const void* id128, int nranks, int rank);
+
+/* Contraction-kernel timing for the roofline: mean device time (ms) of the
+ * last build's S and H contraction launches and their algorithmic flops. */
+int hsdla_b200_engine_kernel_times(hsdla_b200_engine* e, double* ms_s, double* ms_h,
+                                   uint64_t* flops_s, uint64_t* flops_h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HSDLA_B200_H */

@@ -1,0 +1,61 @@
+/* TEST INFRASTRUCTURE ONLY — the CPU oracle for the HSDLA H/S construction.
+ *
+ * Plain-C restatement of the reference algorithm (arXiv 1712.07206, refined
+ * pipeline, /root/reference/proj).  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline leg may load it, as the CHECKER.  The product path
+ * (paper_1712_07206_b200/) never links or calls it.
+ *
+ * Parity pinned: tests/test_oracle.py checks every function here BIT-FOR-BIT
+ * against golden vectors produced by the unmodified reference library
+ * (tests/golden/make_golden.py over oracle/_ref/libhsdla_ref.so).
+ *
+ * Storage: complex numbers are interleaved (re, im) doubles; matrices are
+ * column-major (proj/include/hsdla/complex_matrix.hpp:11-31).  Per-atom N_L x N_L
+ * operator blocks are contiguous, atom-major.
+ */
+#ifndef HSDLA_ORACLE_H
+#define HSDLA_ORACLE_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* proj/src/problem.cpp:79-142 */
+int orc_generate_problem(uint64_t na, uint64_t nl, uint64_t ng, uint64_t seed, uint64_t n_not_hpd,
+                         double* A, double* B, double* T_AA, double* T_AB, double* T_BB, double* U,
+                         uint8_t* hpd);
+
+/* proj/src/pipeline.cpp:281-329 with the kernels of proj/src/kernels.cpp
+ * (Variant::Reference order).  H, S: n_g x n_g column-major; the caller zeroes
+ * them (HermitianView(ng) is zero-initialised, pipeline.cpp:287-288).  ledger[9]
+ * in the key order gemm, hemm, her2k, herk, scaling, herkx, potrf, trmm, total. */
+int orc_build_hs_refined(uint64_t na, uint64_t nl, uint64_t ng, const double* A, const double* B,
+                         const double* T_AA, const double* T_AB, const double* T_BB,
+                         const double* U, double* H, double* S, uint64_t* ledger);
+
+/* proj/src/pipeline.cpp:336-364 */
+void orc_flop_model(int variant, uint64_t na, uint64_t nl, uint64_t ng, uint64_t n_hpd,
+                    uint64_t* ledger);
+
+/* proj/src/oracle.cpp:72-126 (which: 0 direct_H, 1 direct_S, 2 direct_H_grouped);
+ * out: full n_g x n_g.  Refuses n_g > 512 (oracle.hpp:9) with return 3. */
+int orc_direct(int which, uint64_t na, uint64_t nl, uint64_t ng, const double* A, const double* B,
+               const double* T_AA, const double* T_AB, const double* T_BB, const double* U,
+               double* out);
+
+/* Principal-submatrix sampling (SURVEY §7 hard part 3): H[J,J], S[J,J] for the
+ * column subset J (|J| = nj) by the refined pipeline on the J-sliced problem.
+ * Hs, Ss: nj x nj column-major (lower authoritative). */
+int orc_build_hs_sampled(uint64_t na, uint64_t nl, uint64_t ng, const double* A, const double* B,
+                         const double* T_AA, const double* T_AB, const double* T_BB,
+                         const double* U, const uint64_t* J, uint64_t nj, double* Hs, double* Ss);
+
+/* proj/src/complex_matrix.cpp:106-118 */
+double orc_rel_frobenius_error_lower(uint64_t n, const double* x, const double* y);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,843 @@
+// hsdla_b200: C-ABI + device engine for the HSDLA refined H/S construction on B200.
+//
+// Drop-in for hsdla::pipeline::build_hs_refined (reference pipeline.cpp:281-329).
+// Device data layout (one engine per GPU / atom shard, all HBM-resident):
+//   A, B    K x N_G complex, column-major, ld = K (= the reference stacking,
+//           problem.hpp:20-21; uploaded with one strided 2-D copy per matrix)
+//   X1      K x N_G: first U*B (phase s, diag_scale kernels.cpp:438-450), then
+//           T_AA A (hemm_loop, pipeline.cpp:314-321)
+//   X2      K x N_G: Z = T_AB^H A + 1/2 T_BB B (z_loop, pipeline.cpp:302-307)
+//   Tab     raw per-atom T_AB blocks (used as-is: Z = T_AB^H A is a CTN product)
+//   Pbb,Paa 1/2 full(T_BB), full(T_AA) expanded from the LOWER triangles only
+//   Hp, Sp  packed-lower N_G(N_G+1)/2 complex (halves D2H and NCCL bytes)
+// Phases run in the reference order on one stream, CUDA-event timed.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <tuple>
+#include <vector>
+
+#include "../../include/hsdla_b200.h"
+#include "ctn_contract.cuh"
+
+namespace hsdla_b200 {
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+thread_local std::string g_last_error;
+
+struct Status {
+  int code;
+  std::string msg;
+};
+
+struct Fail {
+  int code;
+  std::string msg;
+};
+
+#define HS_CUDA(x)                                                                              \
+  do {                                                                                          \
+    cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess) {                                                                    \
+      (void)cudaGetLastError();                                                                 \
+      throw Fail{e_ == cudaErrorMemoryAllocation ? HSDLA_B200_SIZING_ERROR : HSDLA_B200_CUDA_ERROR, \
+                 std::string(#x) + ": " + cudaGetErrorString(e_)};                              \
+    }                                                                                           \
+  } while (0)
+
+#define HS_NCCL(x)                                                                   \
+  do {                                                                               \
+    ncclResult_t r_ = (x);                                                           \
+    if (r_ != ncclSuccess)                                                           \
+      throw Fail{HSDLA_B200_NCCL_ERROR, std::string(#x) + ": " + ncclGetErrorString(r_)}; \
+  } while (0)
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return HSDLA_B200_OK;
+  } catch (const Fail& e) {
+    g_last_error = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return HSDLA_B200_SIZING_ERROR;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return HSDLA_B200_CUDA_ERROR;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// elementwise kernels (HBM-bound)
+// ---------------------------------------------------------------------------
+
+// X = diag(u) B  (kernels.cpp:438-450); columns strided over blockIdx.y.
+__global__ void diag_scale_kernel(const double2* __restrict__ B, const double* __restrict__ u,
+                                  double2* __restrict__ X, uint64_t K, uint64_t ng) {
+  const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  const double s = u[k];
+  for (uint64_t j = blockIdx.y; j < ng; j += gridDim.y) {
+    const double2 b = B[k + j * K];
+    X[k + j * K] = make_double2(s * b.x, s * b.y);
+  }
+}
+
+// Hermitian expansion from the LOWER triangle (kernels.cpp:152-167 reads only
+// h[l*ldh+i] for l <= i and conj(h[i*ldh+l]) above):
+//   Pbb[a](k,i) = 1/2 * T_BB[a](k,i),  Paa[a](k,i) = T_AA[a](k,i)  (full Hermitian)
+__global__ void expand_hermitian_kernel(const double2* __restrict__ taa, const double2* __restrict__ tbb,
+                                        double2* __restrict__ paa, double2* __restrict__ pbb, int nl,
+                                        uint64_t total) {
+  const uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const uint64_t blk = static_cast<uint64_t>(nl) * nl;
+  const uint64_t a = idx / blk;
+  const int r = static_cast<int>(idx - a * blk);
+  const int k = r % nl, i = r / nl;  // element (k, i) of the column-major block
+  const uint64_t lo = a * blk + (k >= i ? (k + static_cast<uint64_t>(i) * nl) : (i + static_cast<uint64_t>(k) * nl));
+  double2 vaa = taa[lo], vbb = tbb[lo];
+  if (k < i) {
+    vaa.y = -vaa.y;
+    vbb.y = -vbb.y;
+  }
+  paa[idx] = vaa;
+  pbb[idx] = make_double2(0.5 * vbb.x, 0.5 * vbb.y);
+}
+
+// ---------------------------------------------------------------------------
+// tensor maps
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  if (!fn) throw Fail{HSDLA_B200_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable"};
+  return fn;
+}
+
+// 3-D FP64 tensor map; dims/strides in elements (doubles), box rows of 16 doubles
+// (128 B) with the 128-byte swizzle the consumer's LDS.128 pattern expects.
+static void make_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
+                     uint64_t s2, uint32_t b1, uint32_t b2) {
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {s1 * 8, s2 * 8};
+  cuuint32_t box[3] = {16, b1, b2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw Fail{HSDLA_B200_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")"};
+}
+
+// kernel shapes
+constexpr int kTriBM = 64, kTriStages = 6;
+using TriCfg = CtnCfg<kTri, kTriBM, kTriBM, 2, 2, kTriStages>;
+constexpr int kBatBM = 32, kBatBN = 128, kBatStages = 4;
+using BatCfg = CtnCfg<kBatch, kBatBM, kBatBN, 1, 4, kBatStages>;
+
+static auto tri_kernel = ctn_contract_kernel<kTri, kTriBM, kTriBM, 2, 2, kTriStages>;
+static auto bat_kernel = ctn_contract_kernel<kBatch, kBatBM, kBatBN, 1, 4, kBatStages>;
+
+// ---------------------------------------------------------------------------
+// engine
+// ---------------------------------------------------------------------------
+enum Ev { EV_START, EV_S_BEGIN, EV_S_END, EV_Z_END, EV_HER2K_BEGIN, EV_HER2K_END, EV_HEMM_END, EV_HERKX_BEGIN,
+          EV_END, EV_REDUCE_END, EV_COUNT };
+
+}  // namespace hsdla_b200
+
+struct hsdla_b200_engine {
+  int device = 0;
+  uint64_t na = 0, nl = 0, ng = 0, K = 0, npk = 0;
+  cudaStream_t stream = nullptr, comm_stream = nullptr;
+  double2 *A = nullptr, *B = nullptr, *X1 = nullptr, *X2 = nullptr;
+  double2 *Tab = nullptr, *Taa = nullptr, *Tbb = nullptr, *Paa = nullptr, *Pbb = nullptr;
+  double* U = nullptr;
+  double2 *Hp = nullptr, *Sp = nullptr;
+  double2* host_stage = nullptr;  // pinned, 2 * npk
+  cudaEvent_t ev[hsdla_b200::EV_COUNT] = {};
+  cudaEvent_t ev_s_done = nullptr;
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  int last_algo = 0;
+  bool reduced = false;
+  int launches = 0;
+  uint64_t device_bytes = 0, temp_bytes = 0;
+  hsdla_b200::CtnParams p_s, p_z, p_x, p_h, p_h2k, p_hkx;
+  dim3 grid_tri, grid_bat;
+};
+
+namespace hsdla_b200 {
+
+static void check_dims(uint64_t na, uint64_t nl, uint64_t ng) {
+  if (na < 1 || nl < 1 || ng < 1) throw Fail{HSDLA_B200_DIMENSION_ERROR, "all dims must be >= 1"};
+  const uint64_t max = UINT64_MAX / 16 / 4;
+  if (na > max / nl) throw Fail{HSDLA_B200_SIZING_ERROR, "n_atoms * n_l overflows"};
+  if (na * nl > max / ng) throw Fail{HSDLA_B200_SIZING_ERROR, "problem allocation overflows"};
+  if (ng > (1u << 31) - 1 || na * nl > (1u << 30))
+    throw Fail{HSDLA_B200_SIZING_ERROR, "dimension exceeds the 32-bit tile coordinate range"};
+}
+
+template <class T>
+static void dalloc(hsdla_b200_engine* e, T** p, uint64_t count) {
+  const uint64_t bytes = std::max<uint64_t>(count * sizeof(T), 16);
+  HS_CUDA(cudaMalloc(reinterpret_cast<void**>(p), bytes));
+  e->device_bytes += bytes;
+}
+
+static void engine_free(hsdla_b200_engine* e) {
+  cudaSetDevice(e->device);
+  for (void* p : {(void*)e->A, (void*)e->B, (void*)e->X1, (void*)e->X2, (void*)e->Tab, (void*)e->Taa,
+                  (void*)e->Tbb, (void*)e->Paa, (void*)e->Pbb, (void*)e->U, (void*)e->Hp, (void*)e->Sp})
+    if (p) cudaFree(p);
+  if (e->host_stage) cudaFreeHost(e->host_stage);
+  for (auto& ev : e->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (e->ev_s_done) cudaEventDestroy(e->ev_s_done);
+  if (e->comm) ncclCommDestroy(e->comm);
+  if (e->stream) cudaStreamDestroy(e->stream);
+  if (e->comm_stream) cudaStreamDestroy(e->comm_stream);
+}
+
+static int chunks(uint64_t kcomplex) { return static_cast<int>((kcomplex + kChunkC - 1) / kChunkC); }
+
+static void set_tri_seg(CtnParams& P, int s, const CUtensorMap& L, const CUtensorMap& R, uint64_t K) {
+  P.L[s] = L;
+  P.R[s] = R;
+  P.kchunks[s] = chunks(K);
+  P.l_row_z[s] = 0;
+  P.r_row_z[s] = 0;
+}
+
+static void build_params(hsdla_b200_engine* e) {
+  const uint64_t K = e->K, ng = e->ng, nl = e->nl, na = e->na;
+  // 2-D K x N_G stacks as 3-D {2K, N_G, 1}
+  CUtensorMap mA, mB, mX1, mX2;
+  make_map(&mA, e->A, 2 * K, ng, 1, 2 * K, 2 * K * ng, kTriBM, 1);
+  make_map(&mB, e->B, 2 * K, ng, 1, 2 * K, 2 * K * ng, kTriBM, 1);
+  make_map(&mX1, e->X1, 2 * K, ng, 1, 2 * K, 2 * K * ng, kTriBM, 1);
+  make_map(&mX2, e->X2, 2 * K, ng, 1, 2 * K, 2 * K * ng, kTriBM, 1);
+  const int tiles = static_cast<int>((ng + kTriBM - 1) / kTriBM);
+  auto tri_base = [&](CtnParams& P, double2* out, double beta) {
+    std::memset(&P, 0, sizeof(P));
+    P.n = static_cast<int>(ng);
+    P.tiles = tiles;
+    P.out = out;
+    P.alpha_re = 1.0;
+    P.alpha_im = 0.0;
+    P.beta = beta;
+  };
+  // phase s: S = A^H A + (U B)^H (U B)   (pipeline.cpp:298-300)
+  tri_base(e->p_s, e->Sp, 0.0);
+  set_tri_seg(e->p_s, 0, mA, mA, K);
+  set_tri_seg(e->p_s, 1, mX1, mX1, K);
+  e->p_s.nseg = 2;
+  // fused H = Z^H B + B^H Z + A^H X   (pipeline.cpp:311 + :324)
+  tri_base(e->p_h, e->Hp, 0.0);
+  set_tri_seg(e->p_h, 0, mX2, mB, K);
+  set_tri_seg(e->p_h, 1, mB, mX2, K);
+  set_tri_seg(e->p_h, 2, mA, mX1, K);
+  e->p_h.nseg = 3;
+  // reference-order her2k (beta 0) and herkx (beta 1)
+  tri_base(e->p_h2k, e->Hp, 0.0);
+  set_tri_seg(e->p_h2k, 0, mX2, mB, K);
+  set_tri_seg(e->p_h2k, 1, mB, mX2, K);
+  e->p_h2k.nseg = 2;
+  tri_base(e->p_hkx, e->Hp, 1.0);
+  set_tri_seg(e->p_hkx, 0, mA, mX1, K);
+  e->p_hkx.nseg = 1;
+  e->grid_tri = dim3(static_cast<unsigned>(static_cast<uint64_t>(tiles) * (tiles + 1) / 2));
+
+  // batched per-atom products: operators {2nl, nl, na} (row i in dim 1, atom in dim 2),
+  // coefficient views {2nl, na, ng} (atom in dim 1, G row in dim 2).
+  CUtensorMap mTab, mPbb, mPaa, vA, vB;
+  make_map(&mTab, e->Tab, 2 * nl, nl, na, 2 * nl, 2 * nl * nl, kBatBM, 1);
+  make_map(&mPbb, e->Pbb, 2 * nl, nl, na, 2 * nl, 2 * nl * nl, kBatBM, 1);
+  make_map(&mPaa, e->Paa, 2 * nl, nl, na, 2 * nl, 2 * nl * nl, kBatBM, 1);
+  make_map(&vA, e->A, 2 * nl, na, ng, 2 * nl, 2 * K, 1, kBatBN);
+  make_map(&vB, e->B, 2 * nl, na, ng, 2 * nl, 2 * K, 1, kBatBN);
+  auto bat_base = [&](CtnParams& P, double2* out) {
+    std::memset(&P, 0, sizeof(P));
+    P.n = static_cast<int>(ng);
+    P.m_valid = static_cast<int>(nl);
+    P.out = out;
+    P.ldo = K;
+    P.alpha_re = 1.0;
+  };
+  // Z_a = T_AB^H A_a + (1/2 T_BB) B_a   (compute_z, pipeline.cpp:176-185)
+  bat_base(e->p_z, e->X2);
+  e->p_z.L[0] = mTab;
+  e->p_z.R[0] = vA;
+  e->p_z.L[1] = mPbb;
+  e->p_z.R[1] = vB;
+  e->p_z.kchunks[0] = e->p_z.kchunks[1] = chunks(nl);
+  e->p_z.r_row_z[0] = e->p_z.r_row_z[1] = 1;
+  e->p_z.nseg = 2;
+  // X_a = T_AA A_a   (hemm_loop, pipeline.cpp:314-321)
+  bat_base(e->p_x, e->X1);
+  e->p_x.L[0] = mPaa;
+  e->p_x.R[0] = vA;
+  e->p_x.kchunks[0] = chunks(nl);
+  e->p_x.r_row_z[0] = 1;
+  e->p_x.nseg = 1;
+  e->grid_bat = dim3(static_cast<unsigned>((ng + kBatBN - 1) / kBatBN), static_cast<unsigned>((nl + kBatBM - 1) / kBatBM),
+                     static_cast<unsigned>(na));
+}
+
+static void init_kernel_attrs() {
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] {
+    err = cudaFuncSetAttribute(tri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TriCfg::kSmemBytes);
+    if (err == cudaSuccess)
+      err = cudaFuncSetAttribute(bat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BatCfg::kSmemBytes);
+  });
+  HS_CUDA(err);
+}
+
+static hsdla_b200_engine* engine_create(int device, uint64_t na, uint64_t nl, uint64_t ng) {
+  check_dims(na, nl, ng);
+  auto e = std::make_unique<hsdla_b200_engine>();
+  e->device = device;
+  e->na = na;
+  e->nl = nl;
+  e->ng = ng;
+  e->K = na * nl;
+  e->npk = ng * (ng + 1) / 2;
+  try {
+    HS_CUDA(cudaSetDevice(device));
+    // Attributes are per-device for the current context: set them on every device.
+    HS_CUDA(cudaFuncSetAttribute(tri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TriCfg::kSmemBytes));
+    HS_CUDA(cudaFuncSetAttribute(bat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BatCfg::kSmemBytes));
+    HS_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    HS_CUDA(cudaStreamCreateWithFlags(&e->comm_stream, cudaStreamNonBlocking));
+    for (auto& ev : e->ev) HS_CUDA(cudaEventCreate(&ev));
+    HS_CUDA(cudaEventCreateWithFlags(&e->ev_s_done, cudaEventDisableTiming));
+    const uint64_t KG = e->K * ng;
+    dalloc(e.get(), &e->A, KG);
+    dalloc(e.get(), &e->B, KG);
+    dalloc(e.get(), &e->X1, KG);
+    dalloc(e.get(), &e->X2, KG);
+    e->temp_bytes = 2 * KG * sizeof(double2);
+    dalloc(e.get(), &e->Tab, na * nl * nl);
+    dalloc(e.get(), &e->Taa, na * nl * nl);
+    dalloc(e.get(), &e->Tbb, na * nl * nl);
+    dalloc(e.get(), &e->Paa, na * nl * nl);
+    dalloc(e.get(), &e->Pbb, na * nl * nl);
+    dalloc(e.get(), &e->U, e->K);
+    dalloc(e.get(), &e->Hp, e->npk);
+    dalloc(e.get(), &e->Sp, e->npk);
+    build_params(e.get());
+  } catch (...) {
+    engine_free(e.get());
+    throw;
+  }
+  return e.release();
+}
+
+static void engine_upload(hsdla_b200_engine* e, const hsdla_b200_problem* p, uint64_t a0) {
+  if (!p || !p->A || !p->B || !p->T_AA || !p->T_AB || !p->T_BB || !p->U)
+    throw Fail{HSDLA_B200_DIMENSION_ERROR, "null problem pointer"};
+  if (p->n_l != e->nl || p->n_g != e->ng || a0 + e->na > p->n_atoms)
+    throw Fail{HSDLA_B200_DIMENSION_ERROR, "problem shape does not match the engine shard"};
+  HS_CUDA(cudaSetDevice(e->device));
+  const uint64_t Kg = p->n_atoms * p->n_l;  // global ld
+  const uint64_t r0 = a0 * e->nl;
+  const size_t width = e->K * sizeof(double2);
+  const size_t spitch = Kg * sizeof(double2);
+  HS_CUDA(cudaMemcpy2DAsync(e->A, width, reinterpret_cast<const double2*>(p->A) + r0, spitch, width, e->ng,
+                            cudaMemcpyHostToDevice, e->stream));
+  HS_CUDA(cudaMemcpy2DAsync(e->B, width, reinterpret_cast<const double2*>(p->B) + r0, spitch, width, e->ng,
+                            cudaMemcpyHostToDevice, e->stream));
+  const uint64_t blk = e->nl * e->nl;
+  const size_t tbytes = e->na * blk * sizeof(double2);
+  HS_CUDA(cudaMemcpyAsync(e->Taa, reinterpret_cast<const double2*>(p->T_AA) + a0 * blk, tbytes,
+                          cudaMemcpyHostToDevice, e->stream));
+  HS_CUDA(cudaMemcpyAsync(e->Tab, reinterpret_cast<const double2*>(p->T_AB) + a0 * blk, tbytes,
+                          cudaMemcpyHostToDevice, e->stream));
+  HS_CUDA(cudaMemcpyAsync(e->Tbb, reinterpret_cast<const double2*>(p->T_BB) + a0 * blk, tbytes,
+                          cudaMemcpyHostToDevice, e->stream));
+  HS_CUDA(cudaMemcpyAsync(e->U, p->U + r0, e->K * sizeof(double), cudaMemcpyHostToDevice, e->stream));
+}
+
+static void launch_tri(hsdla_b200_engine* e, const CtnParams& P) {
+  tri_kernel<<<e->grid_tri, TriCfg::kThreads, TriCfg::kSmemBytes, e->stream>>>(P);
+  HS_CUDA(cudaGetLastError());
+  ++e->launches;
+}
+static void launch_bat(hsdla_b200_engine* e, const CtnParams& P) {
+  bat_kernel<<<e->grid_bat, BatCfg::kThreads, BatCfg::kSmemBytes, e->stream>>>(P);
+  HS_CUDA(cudaGetLastError());
+  ++e->launches;
+}
+
+static void engine_build(hsdla_b200_engine* e, int algo) {
+  if (algo != HSDLA_B200_ALGO_REFINED && algo != HSDLA_B200_ALGO_REFINED_FUSED)
+    throw Fail{HSDLA_B200_CONFIG_ERROR, "unknown algo " + std::to_string(algo)};
+  HS_CUDA(cudaSetDevice(e->device));
+  cudaStream_t s = e->stream;
+  e->launches = 0;
+  e->last_algo = algo;
+  e->reduced = false;
+  const uint64_t K = e->K, ng = e->ng;
+  HS_CUDA(cudaEventRecord(e->ev[EV_START], s));
+  // operator expansion (lower triangles of T_AA, T_BB only)
+  {
+    const uint64_t total = e->na * e->nl * e->nl;
+    expand_hermitian_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(e->Taa, e->Tbb, e->Paa, e->Pbb,
+                                                                                        static_cast<int>(e->nl), total);
+    HS_CUDA(cudaGetLastError());
+    ++e->launches;
+  }
+  // ---- phase s ----
+  HS_CUDA(cudaEventRecord(e->ev[EV_S_BEGIN], s));
+  diag_scale_kernel<<<dim3(static_cast<unsigned>((K + 255) / 256), static_cast<unsigned>(std::min<uint64_t>(ng, 2048))), 256, 0,
+                      s>>>(e->B, e->U, e->X1, K, ng);
+  HS_CUDA(cudaGetLastError());
+  ++e->launches;
+  launch_tri(e, e->p_s);
+  HS_CUDA(cudaEventRecord(e->ev[EV_S_END], s));
+  if (e->comm) {  // overlap S's reduce with the H phases
+    HS_CUDA(cudaEventRecord(e->ev_s_done, s));
+  }
+  // ---- phase z_loop ----
+  launch_bat(e, e->p_z);
+  HS_CUDA(cudaEventRecord(e->ev[EV_Z_END], s));
+  if (algo == HSDLA_B200_ALGO_REFINED) {
+    // ---- her2k ----
+    HS_CUDA(cudaEventRecord(e->ev[EV_HER2K_BEGIN], s));
+    launch_tri(e, e->p_h2k);
+    HS_CUDA(cudaEventRecord(e->ev[EV_HER2K_END], s));
+    // ---- hemm_loop ----
+    launch_bat(e, e->p_x);
+    HS_CUDA(cudaEventRecord(e->ev[EV_HEMM_END], s));
+    // ---- herkx ----
+    HS_CUDA(cudaEventRecord(e->ev[EV_HERKX_BEGIN], s));
+    launch_tri(e, e->p_hkx);
+    HS_CUDA(cudaEventRecord(e->ev[EV_END], s));
+  } else {
+    // ---- hemm_loop (X = T_AA A), then one fused her2k+herkx contraction ----
+    launch_bat(e, e->p_x);
+    HS_CUDA(cudaEventRecord(e->ev[EV_HEMM_END], s));
+    HS_CUDA(cudaEventRecord(e->ev[EV_HER2K_BEGIN], s));
+    launch_tri(e, e->p_h);
+    HS_CUDA(cudaEventRecord(e->ev[EV_HER2K_END], s));
+    HS_CUDA(cudaEventRecord(e->ev[EV_END], s));
+  }
+}
+
+// NCCL sum-reduce of the packed partials to `root`, split so S's reduce overlaps the
+// H phases (it only waits for phase s).  Single-process multi-GPU calls wrap each
+// step in an NCCL group across engines.
+static void reduce_s(hsdla_b200_engine* e, int root) {
+  HS_CUDA(cudaSetDevice(e->device));
+  HS_CUDA(cudaStreamWaitEvent(e->comm_stream, e->ev_s_done, 0));
+  HS_NCCL(ncclReduce(e->Sp, e->Sp, 2 * e->npk, ncclFloat64, ncclSum, root, e->comm, e->comm_stream));
+}
+static void reduce_h(hsdla_b200_engine* e, int root) {
+  HS_CUDA(cudaSetDevice(e->device));
+  HS_CUDA(cudaStreamWaitEvent(e->comm_stream, e->ev[EV_END], 0));
+  HS_NCCL(ncclReduce(e->Hp, e->Hp, 2 * e->npk, ncclFloat64, ncclSum, root, e->comm, e->comm_stream));
+}
+static void reduce_finish(hsdla_b200_engine* e) {
+  HS_CUDA(cudaSetDevice(e->device));
+  HS_CUDA(cudaEventRecord(e->ev[EV_REDUCE_END], e->comm_stream));
+  HS_CUDA(cudaStreamWaitEvent(e->stream, e->ev[EV_REDUCE_END], 0));
+  e->reduced = true;
+}
+static void engine_reduce(hsdla_b200_engine* e, int root) {
+  if (!e->comm) return;
+  reduce_s(e, root);
+  reduce_h(e, root);
+  reduce_finish(e);
+}
+
+static float ev_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  HS_CUDA(cudaEventElapsedTime(&ms, a, b));
+  return ms;
+}
+
+static void engine_sync(hsdla_b200_engine* e, hsdla_b200_stats* st) {
+  HS_CUDA(cudaSetDevice(e->device));
+  HS_CUDA(cudaStreamSynchronize(e->stream));
+  HS_CUDA(cudaStreamSynchronize(e->comm_stream));
+  if (!st) return;
+  std::memset(st->phase_seconds, 0, sizeof(st->phase_seconds));
+  st->phase_seconds[HSDLA_B200_PHASE_S] = ev_ms(e->ev[EV_START], e->ev[EV_S_END]) * 1e-3;
+  st->phase_seconds[HSDLA_B200_PHASE_Z_LOOP] = ev_ms(e->ev[EV_S_END], e->ev[EV_Z_END]) * 1e-3;
+  if (e->last_algo == HSDLA_B200_ALGO_REFINED) {
+    st->phase_seconds[HSDLA_B200_PHASE_HER2K] = ev_ms(e->ev[EV_Z_END], e->ev[EV_HER2K_END]) * 1e-3;
+    st->phase_seconds[HSDLA_B200_PHASE_HEMM_LOOP] = ev_ms(e->ev[EV_HER2K_END], e->ev[EV_HEMM_END]) * 1e-3;
+    st->phase_seconds[HSDLA_B200_PHASE_HERKX] = ev_ms(e->ev[EV_HEMM_END], e->ev[EV_END]) * 1e-3;
+  } else {
+    st->phase_seconds[HSDLA_B200_PHASE_HEMM_LOOP] = ev_ms(e->ev[EV_Z_END], e->ev[EV_HEMM_END]) * 1e-3;
+    st->phase_seconds[HSDLA_B200_PHASE_HER2K] = ev_ms(e->ev[EV_HEMM_END], e->ev[EV_END]) * 1e-3;
+    st->phase_seconds[HSDLA_B200_PHASE_HERKX] = 0.0;  // fused into her2k
+  }
+  const cudaEvent_t last = e->reduced ? e->ev[EV_REDUCE_END] : e->ev[EV_END];
+  st->device_seconds = ev_ms(e->ev[EV_START], last) * 1e-3;
+  st->reduce_seconds = e->reduced ? ev_ms(e->ev[EV_END], e->ev[EV_REDUCE_END]) * 1e-3 : 0.0;
+  st->kernel_launches = e->launches;
+  st->peak_device_bytes = e->device_bytes;
+  st->peak_temp_bytes = e->temp_bytes;
+  st->n_gpus = e->nranks;
+}
+
+// Unpack column-major packed lower into the lower triangle of an n x n matrix.
+static void unpack_lower(const double2* pk, double2* full, uint64_t n) {
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const uint64_t total = n * (n + 1) / 2;
+  const unsigned nt = total < (1u << 20) ? 1u : hw;
+  auto work = [&](uint64_t j0, uint64_t j1) {
+    for (uint64_t j = j0; j < j1; ++j)
+      std::memcpy(full + j * n + j, pk + j * (2 * n - j + 1) / 2, (n - j) * sizeof(double2));
+  };
+  if (nt == 1) {
+    work(0, n);
+    return;
+  }
+  // split columns into nt ranges of equal element count
+  std::vector<std::thread> th;
+  uint64_t j = 0;
+  for (unsigned t = 0; t < nt && j < n; ++t) {
+    const uint64_t target = total * (t + 1) / nt;
+    uint64_t j1 = j;
+    while (j1 < n && j1 * (2 * n - j1 + 1) / 2 < target) ++j1;
+    if (t == nt - 1) j1 = n;
+    th.emplace_back(work, j, j1);
+    j = j1;
+  }
+  for (auto& t : th) t.join();
+}
+
+static void engine_download(hsdla_b200_engine* e, double* H, double* S) {
+  HS_CUDA(cudaSetDevice(e->device));
+  if (!e->host_stage) HS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&e->host_stage), 2 * e->npk * sizeof(double2)));
+  const size_t bytes = e->npk * sizeof(double2);
+  if (H) HS_CUDA(cudaMemcpyAsync(e->host_stage, e->Hp, bytes, cudaMemcpyDeviceToHost, e->stream));
+  if (S) HS_CUDA(cudaMemcpyAsync(e->host_stage + e->npk, e->Sp, bytes, cudaMemcpyDeviceToHost, e->stream));
+  HS_CUDA(cudaStreamSynchronize(e->stream));
+  if (H) unpack_lower(e->host_stage, reinterpret_cast<double2*>(H), e->ng);
+  if (S) unpack_lower(e->host_stage + e->npk, reinterpret_cast<double2*>(S), e->ng);
+}
+
+// ---------------------------------------------------------------------------
+// the one-shot drop-in: cached engines, atom sharding, NCCL reduce
+// ---------------------------------------------------------------------------
+struct EngineSet {
+  std::vector<hsdla_b200_engine*> engines;
+  std::vector<uint64_t> atom0;
+  ~EngineSet() {
+    for (auto* e : engines) {
+      engine_free(e);
+      delete e;
+    }
+  }
+};
+
+static std::mutex g_cache_mu;
+static std::map<std::tuple<std::vector<int>, uint64_t, uint64_t, uint64_t>, std::unique_ptr<EngineSet>> g_cache;
+
+// Contiguous, count-balanced atom ranges.
+static std::vector<uint64_t> shard_atoms(uint64_t na, int parts) {
+  std::vector<uint64_t> b(parts + 1);
+  for (int r = 0; r <= parts; ++r) b[r] = na * r / parts;
+  return b;
+}
+
+static EngineSet* get_engines(const std::vector<int>& devs, uint64_t na, uint64_t nl, uint64_t ng) {
+  auto key = std::make_tuple(devs, na, nl, ng);
+  auto it = g_cache.find(key);
+  if (it != g_cache.end()) return it->second.get();
+  // one shape at a time keeps HBM free for the caller
+  g_cache.clear();
+  auto set = std::make_unique<EngineSet>();
+  const int P = static_cast<int>(devs.size());
+  const auto b = shard_atoms(na, P);
+  for (int r = 0; r < P; ++r) {
+    if (b[r + 1] == b[r]) throw Fail{HSDLA_B200_CONFIG_ERROR, "more GPUs than atoms"};
+    set->engines.push_back(engine_create(devs[r], b[r + 1] - b[r], nl, ng));
+    set->engines.back()->rank = r;
+    set->engines.back()->nranks = P;
+    set->atom0.push_back(b[r]);
+  }
+  if (P > 1) {
+    std::vector<ncclComm_t> comms(P);
+    HS_NCCL(ncclCommInitAll(comms.data(), P, devs.data()));
+    for (int r = 0; r < P; ++r) set->engines[r]->comm = comms[r];
+  }
+  EngineSet* raw = set.get();
+  g_cache.emplace(key, std::move(set));
+  return raw;
+}
+
+static void flop_model(int variant, uint64_t na, uint64_t nl, uint64_t ng, uint64_t n_hpd, uint64_t* l) {
+  // pipeline.cpp:336-364
+  const uint64_t n_fail = na - std::min(n_hpd, na);
+  std::memset(l, 0, 9 * sizeof(uint64_t));
+  l[0] = 8 * na * nl * nl * ng;
+  l[1] = 8 * na * nl * nl * ng;
+  l[2] = 8 * na * nl * ng * ng;
+  l[3] = 8 * na * nl * ng * ng;
+  l[4] = 2 * na * nl * ng;
+  if (variant == 0) {
+    l[6] = na * (4 * nl * nl * nl / 3);
+    if (n_hpd > 0) {
+      l[7] = 4 * n_hpd * nl * nl * ng;
+      l[3] += 4 * n_hpd * nl * ng * ng;
+    }
+    if (n_fail > 0) {
+      l[1] += 8 * n_fail * nl * nl * ng;
+      l[0] += 8 * n_fail * nl * ng * ng;
+    }
+  } else {
+    l[1] += 8 * na * nl * nl * ng;
+    l[5] = 4 * na * nl * ng * ng;
+  }
+  for (int i = 0; i < 8; ++i) l[8] += l[i];
+}
+
+}  // namespace hsdla_b200
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+using namespace hsdla_b200;
+
+extern "C" {
+
+const char* hsdla_b200_last_error(void) { return g_last_error.c_str(); }
+
+int hsdla_b200_device_count(int* count) {
+  return guarded([&] {
+    if (!count) throw Fail{HSDLA_B200_DIMENSION_ERROR, "null count"};
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      n = 0;
+    }
+    *count = n;
+  });
+}
+
+int hsdla_b200_flop_model(int variant, uint64_t na, uint64_t nl, uint64_t ng, uint64_t n_hpd, uint64_t ledger[9]) {
+  return guarded([&] {
+    if (!ledger) throw Fail{HSDLA_B200_DIMENSION_ERROR, "null ledger"};
+    flop_model(variant, na, nl, ng, n_hpd, ledger);
+  });
+}
+
+int hsdla_b200_host_register(void* ptr, size_t bytes) {
+  return guarded([&] { HS_CUDA(cudaHostRegister(ptr, bytes, cudaHostRegisterPortable)); });
+}
+int hsdla_b200_host_unregister(void* ptr) {
+  return guarded([&] { HS_CUDA(cudaHostUnregister(ptr)); });
+}
+int hsdla_b200_release_cache(void) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    g_cache.clear();
+  });
+}
+
+int hsdla_b200_engine_create(int device, uint64_t na, uint64_t nl, uint64_t ng, hsdla_b200_engine** out) {
+  return guarded([&] {
+    if (!out) throw Fail{HSDLA_B200_DIMENSION_ERROR, "null out"};
+    *out = engine_create(device, na, nl, ng);
+  });
+}
+int hsdla_b200_engine_destroy(hsdla_b200_engine* e) {
+  return guarded([&] {
+    if (!e) return;
+    engine_free(e);
+    delete e;
+  });
+}
+int hsdla_b200_engine_upload(hsdla_b200_engine* e, const hsdla_b200_problem* p, uint64_t a0) {
+  return guarded([&] {
+    if (!e) throw Fail{HSDLA_B200_CONFIG_ERROR, "null engine"};
+    engine_upload(e, p, a0);
+  });
+}
+int hsdla_b200_engine_build(hsdla_b200_engine* e, int algo) {
+  return guarded([&] {
+    if (!e) throw Fail{HSDLA_B200_CONFIG_ERROR, "null engine"};
+    engine_build(e, algo);
+  });
+}
+int hsdla_b200_engine_reduce(hsdla_b200_engine* e, int root) {
+  return guarded([&] {
+    if (!e) throw Fail{HSDLA_B200_CONFIG_ERROR, "null engine"};
+    engine_reduce(e, root);
+  });
+}
+int hsdla_b200_engine_sync(hsdla_b200_engine* e, hsdla_b200_stats* st) {
+  return guarded([&] {
+    if (!e) throw Fail{HSDLA_B200_CONFIG_ERROR, "null engine"};
+    engine_sync(e, st);
+  });
+}
+int hsdla_b200_engine_download(hsdla_b200_engine* e, double* H, double* S) {
+  return guarded([&] {
+    if (!e) throw Fail{HSDLA_B200_CONFIG_ERROR, "null engine"};
+    engine_download(e, H, S);
+  });
+}
+int hsdla_b200_engine_device_results(hsdla_b200_engine* e, void** Hp, void** Sp) {
+  return guarded([&] {
+    if (!e) throw Fail{HSDLA_B200_CONFIG_ERROR, "null engine"};
+    if (Hp) *Hp = e->Hp;
+    if (Sp) *Sp = e->Sp;
+  });
+}
+int hsdla_b200_engine_stream(hsdla_b200_engine* e, void** stream) {
+  return guarded([&] {
+    if (!e || !stream) throw Fail{HSDLA_B200_CONFIG_ERROR, "null engine"};
+    *stream = e->stream;
+  });
+}
+int hsdla_b200_nccl_unique_id(void* id128) {
+  return guarded([&] {
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    HS_NCCL(ncclGetUniqueId(&id));
+    std::memcpy(id128, &id, sizeof(id));
+  });
+}
+int hsdla_b200_engine_set_comm(hsdla_b200_engine* e, const void* id128, int nranks, int rank) {
+  return guarded([&] {
+    if (!e) throw Fail{HSDLA_B200_CONFIG_ERROR, "null engine"};
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw Fail{HSDLA_B200_CONFIG_ERROR, "bad rank"};
+    HS_CUDA(cudaSetDevice(e->device));
+    if (e->comm) {
+      ncclCommDestroy(e->comm);
+      e->comm = nullptr;
+    }
+    e->nranks = nranks;
+    e->rank = rank;
+    if (nranks == 1) return;
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    HS_NCCL(ncclCommInitRank(&e->comm, nranks, id, rank));
+  });
+}
+int hsdla_b200_engine_kernel_times(hsdla_b200_engine* e, double* ms_s, double* ms_h, uint64_t* flops_s,
+                                   uint64_t* flops_h) {
+  return guarded([&] {
+    if (!e) throw Fail{HSDLA_B200_CONFIG_ERROR, "null engine"};
+    HS_CUDA(cudaStreamSynchronize(e->stream));
+    // S contraction: herk + herk (8 K N_G^2 ledger flops); diag_scale is in the window too (HBM-bound, <1%).
+    if (ms_s) *ms_s = ev_ms(e->ev[EV_S_BEGIN], e->ev[EV_S_END]);
+    if (ms_h) *ms_h = ev_ms(e->ev[EV_HER2K_BEGIN], e->ev[EV_HER2K_END]);
+    const uint64_t KN2 = e->K * e->ng * e->ng;
+    if (flops_s) *flops_s = 8 * KN2;
+    if (flops_h) *flops_h = (e->last_algo == HSDLA_B200_ALGO_REFINED ? 8 : 12) * KN2;
+  });
+}
+
+int hsdla_b200_build_hs(const hsdla_b200_problem* p, const hsdla_b200_options* o, double* H, double* S,
+                        hsdla_b200_stats* st) {
+  return guarded([&] {
+    const auto t0 = std::chrono::steady_clock::now();
+    if (!p) throw Fail{HSDLA_B200_DIMENSION_ERROR, "null problem"};
+    check_dims(p->n_atoms, p->n_l, p->n_g);
+    if (!H || !S) throw Fail{HSDLA_B200_DIMENSION_ERROR, "null H or S"};
+    const int algo = o ? o->algo : HSDLA_B200_ALGO_REFINED_FUSED;
+    int P = o && o->n_gpus > 1 ? o->n_gpus : 1;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+      (void)cudaGetLastError();
+      throw Fail{HSDLA_B200_CONFIG_ERROR, "no CUDA device visible (the B200 path has no CPU fallback)"};
+    }
+    std::vector<int> devs(P);
+    for (int r = 0; r < P; ++r) devs[r] = (o && o->device_ids) ? o->device_ids[r] : r;
+    for (int d : devs)
+      if (d < 0 || d >= ndev) throw Fail{HSDLA_B200_CONFIG_ERROR, "device id out of range"};
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    EngineSet* set = get_engines(devs, p->n_atoms, p->n_l, p->n_g);
+    // upload + build per GPU (host threads so pageable uploads proceed in parallel)
+    const auto t_up = std::chrono::steady_clock::now();
+    std::vector<std::thread> th;
+    std::vector<Status> errs(P, Status{0, ""});
+    for (int r = 0; r < P; ++r) {
+      th.emplace_back([&, r] {
+        errs[r].code = guarded([&] {
+          hsdla_b200_engine* e = set->engines[r];
+          engine_upload(e, p, set->atom0[r]);
+          HS_CUDA(cudaStreamSynchronize(e->stream));
+        });
+        if (errs[r].code) errs[r].msg = g_last_error;
+      });
+    }
+    for (auto& t : th) t.join();
+    for (auto& er : errs)
+      if (er.code) throw Fail{er.code, er.msg};
+    const double h2d = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_up).count();
+    for (int r = 0; r < P; ++r) engine_build(set->engines[r], algo);
+    if (P > 1) {
+      HS_NCCL(ncclGroupStart());
+      for (int r = 0; r < P; ++r) reduce_s(set->engines[r], 0);
+      HS_NCCL(ncclGroupEnd());
+      HS_NCCL(ncclGroupStart());
+      for (int r = 0; r < P; ++r) reduce_h(set->engines[r], 0);
+      HS_NCCL(ncclGroupEnd());
+      for (int r = 0; r < P; ++r) reduce_finish(set->engines[r]);
+    }
+    hsdla_b200_stats local{};
+    double maxph[5] = {0, 0, 0, 0, 0};
+    double dev_s = 0, red_s = 0;
+    int launches = 0;
+    for (int r = 0; r < P; ++r) {
+      engine_sync(set->engines[r], &local);
+      for (int i = 0; i < 5; ++i) maxph[i] = std::max(maxph[i], local.phase_seconds[i]);
+      dev_s = std::max(dev_s, local.device_seconds);
+      red_s = std::max(red_s, local.reduce_seconds);
+      launches += local.kernel_launches;
+    }
+    const auto t_d = std::chrono::steady_clock::now();
+    engine_download(set->engines[0], H, S);
+    const double d2h = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_d).count();
+    if (st) {
+      std::memcpy(st->phase_seconds, maxph, sizeof(maxph));
+      st->h2d_seconds = h2d;
+      st->device_seconds = dev_s;
+      st->reduce_seconds = red_s;
+      st->d2h_seconds = d2h;
+      flop_model(1, p->n_atoms, p->n_l, p->n_g, p->n_atoms, st->ledger);
+      st->executed_flops = st->ledger[8];
+      st->peak_device_bytes = local.peak_device_bytes;
+      st->peak_temp_bytes = local.peak_temp_bytes;
+      st->n_gpus = P;
+      st->kernel_launches = launches;
+      st->total_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,269 @@
+"""Host-side mirror of the reference pipeline API for the B200 strategy.
+
+Reference interface mirrored (names, argument meaning, error behaviour):
+  hsdla::pipeline::build_hs_refined / build_hs / flop_model      pipeline.hpp:55-62
+  PipelineConfig / HSResult / PhaseTime / FlopLedger              pipeline.hpp:22-44, flop_ledger.hpp
+  HermitianView::mirror, rel_frobenius_error_lower               complex_matrix.hpp:62-94
+All arithmetic runs in libhsdla_b200.so on the GPU; nothing here computes H or S.
+"""
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from .errors import ConfigError, DimensionError, check
+
+VARIANTS = ("original", "refined")
+STRATEGIES = ("b200",)
+ALGOS = {"fused": _lib.ALGO_REFINED_FUSED, "refined": _lib.ALGO_REFINED}
+
+
+def parse_variant(s):
+    if s not in VARIANTS:
+        raise ConfigError(f"unknown variant: {s}")
+    return s
+
+
+def parse_strategy(s):
+    """The B200 build provides one strategy.  The reference's cpu/static/dynamic
+    strategies (pipeline.hpp:15) are host-CPU paths and are not part of it."""
+    if s not in STRATEGIES:
+        raise ConfigError(f"unknown strategy: {s} (the B200 build implements: {', '.join(STRATEGIES)})")
+    return s
+
+
+@dataclass
+class PipelineConfig:
+    variant: str = "refined"
+    strategy: str = "b200"
+    n_gpus: int = 1
+    device_ids: Optional[Sequence[int]] = None
+    algo: str = "fused"  # "fused" (her2k+herkx in one contraction) | "refined" (reference phase order)
+
+
+@dataclass
+class PhaseTime:
+    name: str
+    seconds: float
+
+
+class FlopLedger:
+    """Per-kernel integer real-flop counts, complex MAC = 8 (flop_ledger.hpp:9-35)."""
+
+    def __init__(self, counts=None):
+        self._counts = {k: int(v) for k, v in (counts or {}).items() if int(v) != 0}
+
+    @classmethod
+    def from_array(cls, arr):
+        return cls({k: int(v) for k, v in zip(_lib.LEDGER_KEYS, list(arr)[:8])})
+
+    def add(self, kernel, flops):
+        self._counts[kernel] = self._counts.get(kernel, 0) + int(flops)
+
+    def total(self):
+        return sum(self._counts.values())
+
+    def count(self, kernel):
+        return self._counts.get(kernel, 0)
+
+    def counts(self):
+        return dict(sorted(self._counts.items()))
+
+    def __eq__(self, other):
+        return isinstance(other, FlopLedger) and self.counts() == other.counts()
+
+    def __repr__(self):
+        return f"FlopLedger({self.counts()}, total={self.total()})"
+
+
+@dataclass
+class HSResult:
+    H: np.ndarray  # (n_g, n_g) complex128, Fortran order; lower triangle authoritative, upper exactly 0
+    S: np.ndarray
+    ledger: FlopLedger
+    peak_temp_bytes: int = 0
+    phases: List[PhaseTime] = field(default_factory=list)
+    warnings: List[str] = field(default_factory=list)
+    stats: dict = field(default_factory=dict)
+
+
+def _options(cfg):
+    ids = None
+    if cfg.device_ids is not None:
+        if len(cfg.device_ids) < cfg.n_gpus:
+            raise ConfigError("device_ids shorter than n_gpus")
+        ids = (C.c_int * len(cfg.device_ids))(*cfg.device_ids)
+    if cfg.algo not in ALGOS:
+        raise ConfigError(f"unknown algo: {cfg.algo}")
+    if cfg.n_gpus < 1:
+        raise ConfigError("n_gpus must be >= 1")
+    return _lib.Options(int(cfg.n_gpus), ids, ALGOS[cfg.algo], 0), ids
+
+
+def stats_dict(st):
+    return {
+        "phase_seconds": dict(zip(_lib.PHASE_NAMES, list(st.phase_seconds))),
+        "h2d_seconds": st.h2d_seconds, "device_seconds": st.device_seconds, "reduce_seconds": st.reduce_seconds,
+        "d2h_seconds": st.d2h_seconds, "total_seconds": st.total_seconds,
+        "ledger_total": int(st.ledger[8]), "executed_flops": int(st.executed_flops),
+        "peak_device_bytes": int(st.peak_device_bytes), "peak_temp_bytes": int(st.peak_temp_bytes),
+        "n_gpus": st.n_gpus, "kernel_launches": st.kernel_launches,
+    }
+
+
+def build_hs_refined(p, cfg: Optional[PipelineConfig] = None, H=None, S=None) -> HSResult:
+    """build_hs_refined (pipeline.cpp:281-329) on B200.  ``H``/``S`` may be passed
+    preallocated (n_g x n_g complex128, Fortran order); only their lower triangles
+    are written.  Fresh outputs have exactly-zero upper triangles."""
+    cfg = cfg or PipelineConfig()
+    parse_strategy(cfg.strategy)
+    if parse_variant(cfg.variant) != "refined":
+        raise ConfigError("the B200 strategy implements the refined variant (Algorithm 3)")
+    prob = p.c_struct()
+    n = p.n_g
+    if H is None:
+        H = np.zeros((n, n), np.complex128, order="F")
+    if S is None:
+        S = np.zeros((n, n), np.complex128, order="F")
+    for name, M in (("H", H), ("S", S)):
+        if M.shape != (n, n) or M.dtype != np.complex128 or not M.flags.f_contiguous:
+            raise DimensionError(f"{name} must be a ({n}, {n}) complex128 Fortran array")
+    opts, _keep = _options(cfg)
+    st = _lib.Stats()
+    check(_lib.lib().hsdla_b200_build_hs(C.byref(prob), C.byref(opts), H.ctypes.data_as(C.c_void_p),
+                                         S.ctypes.data_as(C.c_void_p), C.byref(st)), "build_hs")
+    phases = [PhaseTime(nm, float(sec)) for nm, sec in zip(_lib.PHASE_NAMES, st.phase_seconds)]
+    warnings = []
+    if cfg.algo == "fused":
+        warnings.append("herkx fused into the her2k contraction (phase time 0)")
+    return HSResult(H, S, FlopLedger.from_array(st.ledger), int(st.peak_temp_bytes), phases, warnings,
+                    stats_dict(st))
+
+
+def build_hs(p, cfg: PipelineConfig) -> HSResult:
+    """build_hs (pipeline.cpp:331-334)."""
+    parse_variant(cfg.variant)
+    if cfg.variant == "original":
+        raise ConfigError("variant 'original' (Algorithm 1) is not provided by the B200 strategy")
+    return build_hs_refined(p, cfg)
+
+
+def flop_model(p, variant="refined") -> FlopLedger:
+    """Closed-form ledger (pipeline.cpp:336-364)."""
+    parse_variant(variant)
+    n_hpd = p.n_atoms if getattr(p, "hpd_flags", None) is None else int(np.sum(np.asarray(p.hpd_flags, bool)))
+    out = (C.c_uint64 * 9)()
+    check(_lib.lib().hsdla_b200_flop_model(C.c_int(0 if variant == "original" else 1), C.c_uint64(p.n_atoms),
+                                           C.c_uint64(p.n_l), C.c_uint64(p.n_g), C.c_uint64(n_hpd), out),
+          "flop_model")
+    return FlopLedger.from_array(out)
+
+
+def mirror(M):
+    """HermitianView::mirror (complex_matrix.cpp:39-45), in place."""
+    n = M.shape[0]
+    iu = np.triu_indices(n, 1)
+    M[iu] = np.conj(M.T[iu])
+    M[np.diag_indices(n)] = M.diagonal().real
+    return M
+
+
+def rel_frobenius_error_lower(x, y):
+    """complex_matrix.cpp:106-118."""
+    if x.shape != y.shape or x.shape[0] != x.shape[1]:
+        raise DimensionError("rel_frobenius_error_lower: shape mismatch")
+    il = np.tril_indices(x.shape[0])
+    d = np.linalg.norm((x - y)[il])
+    r = np.linalg.norm(y[il])
+    return float(d / max(r, 1e-300))
+
+
+class Engine:
+    """Device-resident engine for one atom shard on one GPU (C-ABI hsdla_b200_engine_*)."""
+
+    def __init__(self, device, n_atoms_local, n_l, n_g):
+        h = C.c_void_p()
+        check(_lib.lib().hsdla_b200_engine_create(C.c_int(device), C.c_uint64(n_atoms_local), C.c_uint64(n_l),
+                                                  C.c_uint64(n_g), C.byref(h)), "engine_create")
+        self.h = h
+        self.n_g = n_g
+        self.device = device
+
+    def close(self):
+        if self.h:
+            _lib.lib().hsdla_b200_engine_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def upload(self, p, atom_begin=0):
+        prob = p.c_struct()
+        check(_lib.lib().hsdla_b200_engine_upload(self.h, C.byref(prob), C.c_uint64(atom_begin)), "engine_upload")
+
+    def build(self, algo="fused"):
+        check(_lib.lib().hsdla_b200_engine_build(self.h, C.c_int(ALGOS[algo])), "engine_build")
+
+    def reduce(self, root=0):
+        check(_lib.lib().hsdla_b200_engine_reduce(self.h, C.c_int(root)), "engine_reduce")
+
+    def sync(self):
+        st = _lib.Stats()
+        check(_lib.lib().hsdla_b200_engine_sync(self.h, C.byref(st)), "engine_sync")
+        return stats_dict(st)
+
+    def download(self, H=None, S=None):
+        n = self.n_g
+        if H is None:
+            H = np.zeros((n, n), np.complex128, order="F")
+        if S is None:
+            S = np.zeros((n, n), np.complex128, order="F")
+        check(_lib.lib().hsdla_b200_engine_download(self.h, H.ctypes.data_as(C.c_void_p),
+                                                    S.ctypes.data_as(C.c_void_p)), "engine_download")
+        return H, S
+
+    def set_comm(self, uid: bytes, nranks, rank):
+        buf = C.create_string_buffer(uid, 128)
+        check(_lib.lib().hsdla_b200_engine_set_comm(self.h, buf, C.c_int(nranks), C.c_int(rank)), "set_comm")
+
+    def stream(self):
+        s = C.c_void_p()
+        check(_lib.lib().hsdla_b200_engine_stream(self.h, C.byref(s)), "engine_stream")
+        return s.value
+
+    def kernel_times(self):
+        ms_s, ms_h = C.c_double(), C.c_double()
+        fs, fh = C.c_uint64(), C.c_uint64()
+        check(_lib.lib().hsdla_b200_engine_kernel_times(self.h, C.byref(ms_s), C.byref(ms_h), C.byref(fs),
+                                                        C.byref(fh)), "kernel_times")
+        return {"s_ms": ms_s.value, "h_ms": ms_h.value, "s_flops": fs.value, "h_flops": fh.value}
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(_lib.lib().hsdla_b200_nccl_unique_id(buf), "nccl_unique_id")
+    return buf.raw
+
+
+def device_count():
+    n = C.c_int(0)
+    check(_lib.lib().hsdla_b200_device_count(C.byref(n)), "device_count")
+    return n.value
+
+
+def host_register(arr):
+    check(_lib.lib().hsdla_b200_host_register(arr.ctypes.data_as(C.c_void_p), C.c_size_t(arr.nbytes)),
+          "host_register")
+
+
+def host_unregister(arr):
+    check(_lib.lib().hsdla_b200_host_unregister(arr.ctypes.data_as(C.c_void_p)), "host_unregister")
+
+
+def release_cache():
+    check(_lib.lib().hsdla_b200_release_cache(), "release_cache")

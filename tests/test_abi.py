@@ -1,0 +1,43 @@
+"""The C-ABI library loads and exports every symbol include/hsdla_b200.h declares
+(no compute calls: this runs without a GPU)."""
+import ctypes as C
+import os
+import re
+
+import paper_1712_07206_b200 as hb
+from paper_1712_07206_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "hsdla_b200.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(hsdla_b200_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = C.CDLL(_lib.LIB_PATH)
+    syms = declared_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(L, s), s
+    assert set(syms) == set(_lib.EXPORTS)
+
+
+def test_library_is_sm100a_only():
+    blob = open(_lib.LIB_PATH, "rb").read()
+    assert b"sm_100a" in blob
+
+
+def test_status_codes_and_last_error():
+    L = _lib.lib()
+    rc = L.hsdla_b200_flop_model(C.c_int(1), C.c_uint64(1), C.c_uint64(1), C.c_uint64(1), C.c_uint64(1), None)
+    assert rc == _lib.DIMENSION_ERROR
+    assert "null" in _lib.last_error()
+    n = C.c_int(-1)
+    assert L.hsdla_b200_device_count(C.byref(n)) == 0 and n.value >= 0
+    h = C.c_void_p()
+    assert L.hsdla_b200_engine_create(C.c_int(0), C.c_uint64(0), C.c_uint64(1), C.c_uint64(1), C.byref(h)) == \
+        _lib.DIMENSION_ERROR
+    assert hb.flop_model(hb.empty_problem(2, 3, 4)).total() > 0

@@ -1,0 +1,98 @@
+"""The CPU oracle (oracle/hsdla_oracle.c) pinned against the reference.
+
+Golden vectors come from the UNMODIFIED reference library (tests/golden/make_golden.py);
+the restatement must reproduce them BIT FOR BIT (it replays the reference's
+operation order), and the reference's own known-answer tests:
+  hand unit problem H=[[6]], S=[[2]]           test_oracle.cpp:11-47
+  flop model at unit dims totals 46            test_pipeline.cpp:75-85
+  NaCl her2k = 1,021,490,233,344               test_pipeline.cpp:87-95
+  ledger == flop_model, closed-form delta       test_pipeline.cpp:97-113
+  grouped == ungrouped (<= 1e-13)              test_oracle.cpp:76-83
+  refined vs direct oracle <= 1e-10 sqrt(N_G)  test_pipeline.cpp:42-52
+"""
+import numpy as np
+import pytest
+
+from conftest import golden_cases, load_case
+from oracle.oracle import LEDGER_KEYS, Reference, Restatement, alloc_problem
+
+
+@pytest.mark.parametrize("path", golden_cases(), ids=lambda p: p.split("/")[-1][:-4])
+def test_restatement_bitwise_vs_reference_golden(path, restatement):
+    dims, d = load_case(path)
+    na, nl, ng, seed, nnh = dims
+    p = restatement.generate_problem(na, nl, ng, seed, nnh)
+    for k in ("A", "B", "T_AA", "T_AB", "T_BB", "U"):
+        assert np.array_equal(getattr(p, k), d[k]), k
+    assert np.array_equal(p.hpd_flags, d["hpd"])
+    H, S, led = restatement.build_hs_refined(p)
+    assert np.array_equal(H, d["H"]) and np.array_equal(S, d["S"])
+    assert [led.get(k, 0) for k in LEDGER_KEYS] + [led["total"]] == d["ledger"].tolist()
+    if ng <= 512:
+        assert np.array_equal(restatement.direct_H(p), d["Hd"])
+        assert np.array_equal(restatement.direct_S(p), d["Sd"])
+        tol = 1e-10 * np.sqrt(ng)
+        assert restatement.rel_frobenius_error_lower(H, d["Hd"]) < tol
+        assert restatement.rel_frobenius_error_lower(S, d["Sd"]) < tol
+    if "Hg" in d:
+        assert np.array_equal(restatement.direct_H_grouped(p), d["Hg"])
+        assert restatement.rel_frobenius_error_lower(d["Hg"], d["Hd"]) < 1e-13
+    # the refined pipeline never touches the upper triangles (test_pipeline.cpp:136-147)
+    iu = np.triu_indices(ng, 1)
+    assert np.all(H[iu] == 0) and np.all(S[iu] == 0)
+    assert np.all(np.diag(H).imag == 0) and np.all(np.diag(S).imag == 0)
+
+
+def test_hand_unit_problem(restatement):
+    p = alloc_problem(1, 1, 1)
+    p.A[0, 0] = 1.0
+    p.B[0, 0] = 1j
+    p.T_AA[0, 0, 0] = 2.0
+    p.T_AB[0, 0, 0] = 1.0
+    p.T_BB[0, 0, 0] = 4.0
+    p.U[0, 0] = 1.0
+    assert restatement.direct_H(p)[0, 0] == pytest.approx(6.0, abs=1e-14)
+    assert restatement.direct_S(p)[0, 0] == pytest.approx(2.0, abs=1e-14)
+    H, S, _ = restatement.build_hs_refined(p)
+    assert H[0, 0] == pytest.approx(6.0, abs=1e-14) and S[0, 0] == pytest.approx(2.0, abs=1e-14)
+
+
+def test_flop_model_known_answers(restatement):
+    m = restatement.flop_model(1, 1, 1)
+    assert m == {"gemm": 8, "hemm": 16, "her2k": 8, "herk": 8, "scaling": 2, "herkx": 4, "total": 46}
+    assert restatement.flop_model(512, 49, 2256)["her2k"] == 1021490233344
+    # original vs refined closed-form delta (test_pipeline.cpp:97-113)
+    for nnh in (0, 2, 4):
+        na, nl, ng = 4, 6, 40
+        o = restatement.flop_model(na, nl, ng, "original", n_hpd=na - nnh)
+        r = restatement.flop_model(na, nl, ng, "refined")
+        delta = 4 * nnh * nl * ng * ng + na * (4 * nl ** 3 // 3) - 4 * (na - nnh) * nl * nl * ng
+        assert o["total"] - r["total"] == delta
+
+
+def test_sampled_principal_submatrix(restatement):
+    p = restatement.generate_problem(3, 7, 40, 4, 0)
+    H, S, _ = restatement.build_hs_refined(p)
+    J = np.array([0, 3, 5, 17, 18, 39], np.uint64)
+    Hs, Ss = restatement.build_hs_sampled(p, J)
+    Ji = J.astype(int)
+    il = np.tril_indices(len(J))
+    assert np.array_equal(Hs[il], H[np.ix_(Ji, Ji)][il])
+    assert np.array_equal(Ss[il], S[np.ix_(Ji, Ji)][il])
+
+
+def test_direct_oracle_refuses_oversized(restatement):
+    p = alloc_problem(1, 1, 513)
+    with pytest.raises(ValueError):
+        restatement.direct_H(p)
+
+
+@pytest.mark.skipif(not Reference.available(), reason="oracle/_ref not built (needs /root/reference at build time)")
+def test_compiled_reference_matches_golden():
+    ref = Reference()
+    path = golden_cases()[3]
+    dims, d = load_case(path)
+    p = ref.generate_problem(*dims)
+    r = ref.build_hs(p, "refined", threads=2, blocked=True)
+    assert np.array_equal(r["H"], d["H"]) and np.array_equal(r["S"], d["S"])
+    assert [ph[0] for ph in r["phases"]] == ["s", "z_loop", "her2k", "hemm_loop", "herkx"]
