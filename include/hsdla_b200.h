@@ -145,10 +145,18 @@ int hsdla_b200_engine_stream(hsdla_b200_engine* e, void** stream);
 int hsdla_b200_nccl_unique_id(void* id128);
 int hsdla_b200_engine_set_comm(hsdla_b200_engine* e, const void* id128, int nranks, int rank);
 
-/* Contraction-kernel timing for the roofline: mean device time (ms) of the
- * last build's S and H contraction launches and their algorithmic flops. */
-int hsdla_b200_engine_kernel_times(hsdla_b200_engine* e, double* ms_s, double* ms_h,
-                                   uint64_t* flops_s, uint64_t* flops_h);
+/* Contraction-kernel timing for the roofline: mean CUDA-event duration (ms) of
+ * the S contraction (herk+herk, 8 K N_G^2 flops) and the H contraction launch
+ * (fused: 12 K N_G^2; refined algo: the her2k launch, 8 K N_G^2) over every
+ * build since the last reset, recorded on the engine stream without per-build
+ * host syncs.  reset != 0 clears the accumulators after reading. */
+int hsdla_b200_engine_kernel_times(hsdla_b200_engine* e, int reset, double* ms_s, double* ms_h,
+                                   uint64_t* flops_s, uint64_t* flops_h, uint64_t* n_builds);
+
+/* Roofline denominator: runs a DMMA (mma.sync m8n8k4 f64) throughput loop on
+ * `device` for about `seconds` and returns the achieved FP64 TFLOP/s.  A
+ * measurement probe, not part of the H/S path. */
+int hsdla_b200_fp64_peak(int device, double seconds, double* tflops);
 
 #ifdef __cplusplus
 }

@@ -188,6 +188,17 @@ struct hsdla_b200_engine {
   int launches = 0;
   uint64_t device_bytes = 0, temp_bytes = 0;
   hsdla_b200::CtnParams p_s, p_z, p_x, p_h, p_h2k, p_hkx;
+  // per-build CUDA events around the S and H contraction launches (roofline timing
+  // over a whole timed region without per-step host syncs)
+  static constexpr int kRing = 64;
+  struct KTimer {
+    cudaEvent_t s0 = nullptr, s1 = nullptr, h0 = nullptr, h1 = nullptr;
+    bool pending = false;
+    uint64_t flops_h = 0;
+  } ring[kRing];
+  uint64_t builds = 0;
+  double sum_s_ms = 0, sum_h_ms = 0;
+  uint64_t sum_flops_h = 0, timed_builds = 0;
   dim3 grid_tri, grid_bat;
 };
 
@@ -218,6 +229,9 @@ static void engine_free(hsdla_b200_engine* e) {
   for (auto& ev : e->ev)
     if (ev) cudaEventDestroy(ev);
   if (e->ev_s_done) cudaEventDestroy(e->ev_s_done);
+  for (auto& t : e->ring)
+    for (cudaEvent_t ev : {t.s0, t.s1, t.h0, t.h1})
+      if (ev) cudaEventDestroy(ev);
   if (e->comm) ncclCommDestroy(e->comm);
   if (e->stream) cudaStreamDestroy(e->stream);
   if (e->comm_stream) cudaStreamDestroy(e->comm_stream);
@@ -337,6 +351,8 @@ static hsdla_b200_engine* engine_create(int device, uint64_t na, uint64_t nl, ui
     HS_CUDA(cudaStreamCreateWithFlags(&e->comm_stream, cudaStreamNonBlocking));
     for (auto& ev : e->ev) HS_CUDA(cudaEventCreate(&ev));
     HS_CUDA(cudaEventCreateWithFlags(&e->ev_s_done, cudaEventDisableTiming));
+    for (auto& t : e->ring)
+      for (cudaEvent_t* ev : {&t.s0, &t.s1, &t.h0, &t.h1}) HS_CUDA(cudaEventCreate(ev));
     const uint64_t KG = e->K * ng;
     dalloc(e.get(), &e->A, KG);
     dalloc(e.get(), &e->B, KG);
@@ -395,6 +411,18 @@ static void launch_bat(hsdla_b200_engine* e, const CtnParams& P) {
   ++e->launches;
 }
 
+static float ev_ms(cudaEvent_t a, cudaEvent_t b);
+
+static void harvest(hsdla_b200_engine* e, hsdla_b200_engine::KTimer& t) {
+  if (!t.pending) return;
+  HS_CUDA(cudaEventSynchronize(t.h1));
+  e->sum_s_ms += ev_ms(t.s0, t.s1);
+  e->sum_h_ms += ev_ms(t.h0, t.h1);
+  e->sum_flops_h += t.flops_h;
+  ++e->timed_builds;
+  t.pending = false;
+}
+
 static void engine_build(hsdla_b200_engine* e, int algo) {
   if (algo != HSDLA_B200_ALGO_REFINED && algo != HSDLA_B200_ALGO_REFINED_FUSED)
     throw Fail{HSDLA_B200_CONFIG_ERROR, "unknown algo " + std::to_string(algo)};
@@ -404,6 +432,9 @@ static void engine_build(hsdla_b200_engine* e, int algo) {
   e->last_algo = algo;
   e->reduced = false;
   const uint64_t K = e->K, ng = e->ng;
+  auto& kt = e->ring[e->builds++ % hsdla_b200_engine::kRing];
+  harvest(e, kt);
+  kt.flops_h = (algo == HSDLA_B200_ALGO_REFINED ? 8 : 12) * K * ng * ng;
   HS_CUDA(cudaEventRecord(e->ev[EV_START], s));
   // operator expansion (lower triangles of T_AA, T_BB only)
   {
@@ -419,7 +450,9 @@ static void engine_build(hsdla_b200_engine* e, int algo) {
                       s>>>(e->B, e->U, e->X1, K, ng);
   HS_CUDA(cudaGetLastError());
   ++e->launches;
+  HS_CUDA(cudaEventRecord(kt.s0, s));
   launch_tri(e, e->p_s);
+  HS_CUDA(cudaEventRecord(kt.s1, s));
   HS_CUDA(cudaEventRecord(e->ev[EV_S_END], s));
   if (e->comm) {  // overlap S's reduce with the H phases
     HS_CUDA(cudaEventRecord(e->ev_s_done, s));
@@ -430,7 +463,9 @@ static void engine_build(hsdla_b200_engine* e, int algo) {
   if (algo == HSDLA_B200_ALGO_REFINED) {
     // ---- her2k ----
     HS_CUDA(cudaEventRecord(e->ev[EV_HER2K_BEGIN], s));
+    HS_CUDA(cudaEventRecord(kt.h0, s));
     launch_tri(e, e->p_h2k);
+    HS_CUDA(cudaEventRecord(kt.h1, s));
     HS_CUDA(cudaEventRecord(e->ev[EV_HER2K_END], s));
     // ---- hemm_loop ----
     launch_bat(e, e->p_x);
@@ -444,10 +479,13 @@ static void engine_build(hsdla_b200_engine* e, int algo) {
     launch_bat(e, e->p_x);
     HS_CUDA(cudaEventRecord(e->ev[EV_HEMM_END], s));
     HS_CUDA(cudaEventRecord(e->ev[EV_HER2K_BEGIN], s));
+    HS_CUDA(cudaEventRecord(kt.h0, s));
     launch_tri(e, e->p_h);
+    HS_CUDA(cudaEventRecord(kt.h1, s));
     HS_CUDA(cudaEventRecord(e->ev[EV_HER2K_END], s));
     HS_CUDA(cudaEventRecord(e->ev[EV_END], s));
   }
+  kt.pending = true;
 }
 
 // NCCL sum-reduce of the packed partials to `root`, split so S's reduce overlaps the
@@ -486,6 +524,7 @@ static void engine_sync(hsdla_b200_engine* e, hsdla_b200_stats* st) {
   HS_CUDA(cudaSetDevice(e->device));
   HS_CUDA(cudaStreamSynchronize(e->stream));
   HS_CUDA(cudaStreamSynchronize(e->comm_stream));
+  for (auto& t : e->ring) harvest(e, t);
   if (!st) return;
   std::memset(st->phase_seconds, 0, sizeof(st->phase_seconds));
   st->phase_seconds[HSDLA_B200_PHASE_S] = ev_ms(e->ev[EV_START], e->ev[EV_S_END]) * 1e-3;
@@ -747,17 +786,23 @@ int hsdla_b200_engine_set_comm(hsdla_b200_engine* e, const void* id128, int nran
     HS_NCCL(ncclCommInitRank(&e->comm, nranks, id, rank));
   });
 }
-int hsdla_b200_engine_kernel_times(hsdla_b200_engine* e, double* ms_s, double* ms_h, uint64_t* flops_s,
-                                   uint64_t* flops_h) {
+int hsdla_b200_engine_kernel_times(hsdla_b200_engine* e, int reset, double* ms_s, double* ms_h,
+                                   uint64_t* flops_s, uint64_t* flops_h, uint64_t* n_builds) {
   return guarded([&] {
     if (!e) throw Fail{HSDLA_B200_CONFIG_ERROR, "null engine"};
+    HS_CUDA(cudaSetDevice(e->device));
     HS_CUDA(cudaStreamSynchronize(e->stream));
-    // S contraction: herk + herk (8 K N_G^2 ledger flops); diag_scale is in the window too (HBM-bound, <1%).
-    if (ms_s) *ms_s = ev_ms(e->ev[EV_S_BEGIN], e->ev[EV_S_END]);
-    if (ms_h) *ms_h = ev_ms(e->ev[EV_HER2K_BEGIN], e->ev[EV_HER2K_END]);
-    const uint64_t KN2 = e->K * e->ng * e->ng;
-    if (flops_s) *flops_s = 8 * KN2;
-    if (flops_h) *flops_h = (e->last_algo == HSDLA_B200_ALGO_REFINED ? 8 : 12) * KN2;
+    for (auto& t : e->ring) harvest(e, t);
+    const double n = static_cast<double>(std::max<uint64_t>(e->timed_builds, 1));
+    if (ms_s) *ms_s = e->sum_s_ms / n;
+    if (ms_h) *ms_h = e->sum_h_ms / n;
+    if (flops_s) *flops_s = 8 * e->K * e->ng * e->ng;  // herk(A) + herk(UB), ledger 2 x 4 K N_G^2
+    if (flops_h) *flops_h = static_cast<uint64_t>(static_cast<double>(e->sum_flops_h) / n);
+    if (n_builds) *n_builds = e->timed_builds;
+    if (reset) {
+      e->sum_s_ms = e->sum_h_ms = 0;
+      e->sum_flops_h = e->timed_builds = 0;
+    }
   });
 }
 

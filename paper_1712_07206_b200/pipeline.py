@@ -236,12 +236,23 @@ class Engine:
         check(_lib.lib().hsdla_b200_engine_stream(self.h, C.byref(s)), "engine_stream")
         return s.value
 
-    def kernel_times(self):
+    def kernel_times(self, reset=False):
+        """Mean CUDA-event duration of the S and H contraction launches over all
+        builds since the last reset (recorded on the engine stream)."""
         ms_s, ms_h = C.c_double(), C.c_double()
-        fs, fh = C.c_uint64(), C.c_uint64()
-        check(_lib.lib().hsdla_b200_engine_kernel_times(self.h, C.byref(ms_s), C.byref(ms_h), C.byref(fs),
-                                                        C.byref(fh)), "kernel_times")
-        return {"s_ms": ms_s.value, "h_ms": ms_h.value, "s_flops": fs.value, "h_flops": fh.value}
+        fs, fh, nb = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        check(_lib.lib().hsdla_b200_engine_kernel_times(self.h, C.c_int(1 if reset else 0), C.byref(ms_s),
+                                                        C.byref(ms_h), C.byref(fs), C.byref(fh), C.byref(nb)),
+              "kernel_times")
+        return {"s_ms": ms_s.value, "h_ms": ms_h.value, "s_flops": fs.value, "h_flops": fh.value,
+                "builds": nb.value}
+
+
+def fp64_peak(device=0, seconds=0.5):
+    """Measured FP64 DMMA throughput (TFLOP/s) — the roofline denominator."""
+    tf = C.c_double()
+    check(_lib.lib().hsdla_b200_fp64_peak(C.c_int(device), C.c_double(seconds), C.byref(tf)), "fp64_peak")
+    return tf.value
 
 
 def nccl_unique_id() -> bytes:
