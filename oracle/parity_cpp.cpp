@@ -1,0 +1,70 @@
+// TEST INFRASTRUCTURE ONLY — C++ drop-in parity driver.
+//
+// Links the UNMODIFIED reference library (oracle/_ref/libhsdla_ref.so, built from
+// /root/reference/proj/src) and libhsdla_b200.so, and drives BOTH through the
+// reference's own C++ types: hsdla::generate_problem -> hsdla::pipeline::build_hs_refined
+// (CPU) vs hsdla_b200::build_hs_refined (include/hsdla_b200/pipeline.hpp, GPU).
+// Exit code = number of failed checks (the acceptance.cpp convention).
+//   parity_cpp <n_atoms> <n_l> <n_g> <seed> <n_not_hpd> [threads]
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+
+#include "hsdla/pipeline.hpp"
+#include "hsdla/problem.hpp"
+#include "hsdla_b200/pipeline.hpp"
+
+int main(int argc, char** argv) {
+  if (argc < 6) {
+    std::fprintf(stderr, "usage: %s n_atoms n_l n_g seed n_not_hpd [threads]\n", argv[0]);
+    return 64;
+  }
+  const std::size_t na = std::atoll(argv[1]), nl = std::atoll(argv[2]), ng = std::atoll(argv[3]);
+  const std::uint64_t seed = std::atoll(argv[4]);
+  const std::size_t nnh = std::atoll(argv[5]);
+  const int threads = argc > 6 ? std::atoi(argv[6]) : 0;
+  const hsdla::ProblemInstance p = hsdla::generate_problem(na, nl, ng, seed, nnh);
+  hsdla::pipeline::PipelineConfig cfg;
+  cfg.kernel = {hsdla::kernels::Variant::BlockedParallel, 128, threads};
+  const hsdla::pipeline::HSResult cpu = hsdla::pipeline::build_hs_refined(p, cfg);
+  int fails = 0;
+  auto check = [&](bool ok, const char* what, double v) {
+    std::printf("%-44s %s (%.3e)\n", what, ok ? "PASS" : "FAIL", v);
+    if (!ok) ++fails;
+  };
+  for (int algo : {HSDLA_B200_ALGO_REFINED_FUSED, HSDLA_B200_ALGO_REFINED}) {
+    hsdla_b200::Options opt;
+    opt.algo = algo;
+    const hsdla::pipeline::HSResult gpu = hsdla_b200::build_hs_refined(p, cfg, opt);
+    const double eh = hsdla::rel_frobenius_error_lower(gpu.H.matrix(), cpu.H.matrix());
+    const double es = hsdla::rel_frobenius_error_lower(gpu.S.matrix(), cpu.S.matrix());
+    std::printf("algo %d\n", algo);
+    check(eh <= 1e-11, "  H rel Frobenius (lower) <= 1e-11", eh);
+    check(es <= 1e-11, "  S rel Frobenius (lower) <= 1e-11", es);
+    check(gpu.ledger == hsdla::pipeline::flop_model(p, hsdla::pipeline::Variant::Refined),
+          "  ledger == flop_model(p, Refined)", double(gpu.ledger.total()));
+    check(gpu.ledger == cpu.ledger, "  ledger == reference CPU ledger", double(cpu.ledger.total()));
+    bool upper0 = true, diag0 = true;
+    for (std::size_t j = 0; j < ng; ++j) {
+      diag0 = diag0 && gpu.H(j, j).imag() == 0.0 && gpu.S(j, j).imag() == 0.0;
+      for (std::size_t i = 0; i < j; ++i)
+        upper0 = upper0 && gpu.H(i, j) == hsdla::cplx(0.0) && gpu.S(i, j) == hsdla::cplx(0.0);
+    }
+    check(upper0, "  upper triangles exactly 0", 0.0);
+    check(diag0, "  diagonal imaginary parts exactly 0", 0.0);
+    bool names = gpu.phases.size() == 5;
+    for (std::size_t i = 0; names && i < 5; ++i) names = gpu.phases[i].name == cpu.phases[i].name;
+    check(names, "  phase names == reference", double(gpu.phases.size()));
+  }
+  // error mapping: the original variant is not provided -> hsdla::ConfigError
+  try {
+    hsdla::pipeline::PipelineConfig bad = cfg;
+    bad.variant = hsdla::pipeline::Variant::Original;
+    hsdla_b200::build_hs(p, bad);
+    check(false, "original variant -> ConfigError", 0);
+  } catch (const hsdla::ConfigError&) {
+    check(true, "original variant -> ConfigError", 0);
+  }
+  std::printf("%d failure(s)\n", fails);
+  return fails;
+}

@@ -127,8 +127,8 @@ struct CtnCfg {
   static constexpr int kSmemBytes = STAGES * kStageBytes + 1024 /*align*/ + 2 * STAGES * 8 + 64;
 };
 
-template <int MODE, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES>
-__global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>::kThreads, 1)
+template <int MODE, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, int MINB = 1>
+__global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>::kThreads, MINB)
     ctn_contract_kernel(const __grid_constant__ CtnParams P) {
   using Cfg = CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>;
   constexpr int MB = Cfg::kMB, NB = Cfg::kNB;

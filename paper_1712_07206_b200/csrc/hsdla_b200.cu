@@ -155,11 +155,11 @@ static void make_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1,
 
 // kernel shapes
 constexpr int kTriBM = 64, kTriStages = 6;
-using TriCfg = CtnCfg<kTri, kTriBM, kTriBM, 2, 2, kTriStages>;
+using TriCfg = CtnCfg<kTri, kTriBM, kTriBM, 2, 4, kTriStages>;
 constexpr int kBatBM = 32, kBatBN = 128, kBatStages = 4;
 using BatCfg = CtnCfg<kBatch, kBatBM, kBatBN, 1, 4, kBatStages>;
 
-static auto tri_kernel = ctn_contract_kernel<kTri, kTriBM, kTriBM, 2, 2, kTriStages>;
+static auto tri_kernel = ctn_contract_kernel<kTri, kTriBM, kTriBM, 2, 4, kTriStages>;
 static auto bat_kernel = ctn_contract_kernel<kBatch, kBatBM, kBatBN, 1, 4, kBatStages>;
 
 // ---------------------------------------------------------------------------
@@ -526,6 +526,11 @@ static void engine_sync(hsdla_b200_engine* e, hsdla_b200_stats* st) {
   HS_CUDA(cudaStreamSynchronize(e->comm_stream));
   for (auto& t : e->ring) harvest(e, t);
   if (!st) return;
+  std::memset(st, 0, sizeof(*st));
+  st->peak_device_bytes = e->device_bytes;
+  st->peak_temp_bytes = e->temp_bytes;
+  st->n_gpus = e->nranks;
+  if (e->builds == 0) return;  // nothing timed yet
   std::memset(st->phase_seconds, 0, sizeof(st->phase_seconds));
   st->phase_seconds[HSDLA_B200_PHASE_S] = ev_ms(e->ev[EV_START], e->ev[EV_S_END]) * 1e-3;
   st->phase_seconds[HSDLA_B200_PHASE_Z_LOOP] = ev_ms(e->ev[EV_S_END], e->ev[EV_Z_END]) * 1e-3;

@@ -1,0 +1,96 @@
+// Development harness: times TRI-mode contraction configs on a C2-sized S product
+// (2 segments, K = 5184, N_G = 3000) with random data.  Not part of the product.
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include <cudaTypedefs.h>
+#include "../paper_1712_07206_b200/csrc/ctn_contract.cuh"
+using namespace hsdla_b200;
+
+static PFN_cuTensorMapEncodeTiled_v12000 enc;
+static void make_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
+                     uint64_t s2, uint32_t b1, uint32_t b2) {
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {s1 * 8, s2 * 8};
+  cuuint32_t box[3] = {16, b1, b2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r) { printf("encode failed %d\n", r); exit(1); }
+}
+
+__global__ void fill(double* p, size_t n, unsigned seed) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    unsigned x = (unsigned)i * 2654435761u ^ seed;
+    x ^= x >> 13; x *= 0x5bd1e995; x ^= x >> 15;
+    p[i] = (x & 0xffffff) / 16777216.0 - 0.5;
+  }
+}
+
+template <int BM, int WM, int WN, int ST, int MINB>
+void run(const char* name, double2* A, double2* B, double2* out, uint64_t K, uint64_t ng, int nseg) {
+  using Cfg = CtnCfg<kTri, BM, BM, WM, WN, ST>;
+  auto kern = ctn_contract_kernel<kTri, BM, BM, WM, WN, ST, MINB>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
+  CtnParams P;
+  memset(&P, 0, sizeof(P));
+  CUtensorMap mA, mB;
+  make_map(&mA, A, 2 * K, ng, 1, 2 * K, 2 * K * ng, BM, 1);
+  make_map(&mB, B, 2 * K, ng, 1, 2 * K, 2 * K * ng, BM, 1);
+  for (int s = 0; s < nseg; ++s) {
+    P.L[s] = (s & 1) ? mB : mA;
+    P.R[s] = (s & 1) ? mA : mB;
+    P.kchunks[s] = (int)((K + 7) / 8);
+  }
+  P.nseg = nseg;
+  P.n = (int)ng;
+  int tiles = (int)((ng + BM - 1) / BM);
+  P.tiles = tiles;
+  P.out = out;
+  P.alpha_re = 1.0;
+  int grid = tiles * (tiles + 1) / 2;
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::kThreads, Cfg::kSmemBytes);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes>>>(P);
+  cudaDeviceSynchronize();
+  float best = 1e9;
+  for (int r = 0; r < 5; ++r) {
+    cudaEventRecord(e0);
+    kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes>>>(P);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    best = ms < best ? ms : best;
+  }
+  cudaError_t err = cudaGetLastError();
+  double flops = 4.0 * nseg * K * (double)ng * ng;
+  printf("%-34s occ %d grid %6d  %8.3f ms  %6.2f TF/s  %s\n", name, occ, grid, best, flops / best / 1e9,
+         err ? cudaGetErrorString(err) : "");
+}
+
+int main(int argc, char** argv) {
+  cudaDriverEntryPointQueryResult q;
+  cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q);
+  uint64_t K = argc > 1 ? atoll(argv[1]) : 5184, ng = argc > 2 ? atoll(argv[2]) : 3000;
+  int nseg = argc > 3 ? atoi(argv[3]) : 2;
+  double2 *A, *B, *out;
+  cudaMalloc(&A, K * ng * 16); cudaMalloc(&B, K * ng * 16); cudaMalloc(&out, ng * (ng + 1) / 2 * 16);
+  fill<<<1024, 256>>>((double*)A, 2 * K * ng, 1);
+  fill<<<1024, 256>>>((double*)B, 2 * K * ng, 2);
+  printf("K %lu N_G %lu nseg %d\n", K, ng, nseg);
+  run<64, 2, 2, 6, 1>("64 2x2 (32x32) st6 minb1", A, B, out, K, ng, nseg);
+  run<64, 2, 2, 4, 1>("64 2x2 (32x32) st4 minb1", A, B, out, K, ng, nseg);
+  run<64, 2, 2, 6, 2>("64 2x2 (32x32) st6 minb2", A, B, out, K, ng, nseg);
+  run<64, 2, 4, 6, 1>("64 2x4 (32x16) st6 minb1", A, B, out, K, ng, nseg);
+  run<64, 2, 4, 6, 2>("64 2x4 (32x16) st6 minb2", A, B, out, K, ng, nseg);
+  run<64, 4, 2, 6, 2>("64 4x2 (16x32) st6 minb2", A, B, out, K, ng, nseg);
+  run<64, 4, 4, 6, 2>("64 4x4 (16x16) st6 minb2", A, B, out, K, ng, nseg);
+  run<64, 2, 4, 4, 2>("64 2x4 (32x16) st4 minb2", A, B, out, K, ng, nseg);
+  run<128, 4, 4, 4, 1>("128 4x4 (32x32) st4 minb1", A, B, out, K, ng, nseg);
+  run<128, 4, 8, 4, 1>("128 4x8 (32x16) st4 minb1", A, B, out, K, ng, nseg);
+  run<32, 1, 2, 8, 3>("32 1x2 (32x16) st8 minb3", A, B, out, K, ng, nseg);
+  return 0;
+}
