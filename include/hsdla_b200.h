@@ -110,6 +110,10 @@ int hsdla_b200_generate_problem(uint64_t n_atoms, uint64_t n_l, uint64_t n_g, ui
                                 uint64_t n_not_hpd, double* A, double* B, double* T_AA, double* T_AB,
                                 double* T_BB, double* U, uint8_t* hpd);
 
+/* Contiguous, count-balanced atom ranges for `parts` GPUs:
+ * bounds[r] .. bounds[r+1] is shard r; bounds has parts+1 entries. */
+int hsdla_b200_shard_atoms(uint64_t n_atoms, int parts, uint64_t* bounds);
+
 const char* hsdla_b200_last_error(void);
 int hsdla_b200_device_count(int* count);
 int hsdla_b200_host_register(void* ptr, size_t bytes);   /* cudaHostRegister (portable) */

@@ -22,7 +22,7 @@ EXPORTS = (
     "hsdla_b200_engine_upload", "hsdla_b200_engine_build", "hsdla_b200_engine_reduce",
     "hsdla_b200_engine_sync", "hsdla_b200_engine_download", "hsdla_b200_engine_device_results",
     "hsdla_b200_engine_stream", "hsdla_b200_nccl_unique_id", "hsdla_b200_engine_set_comm",
-    "hsdla_b200_engine_kernel_times", "hsdla_b200_fp64_peak",
+    "hsdla_b200_engine_kernel_times", "hsdla_b200_fp64_peak", "hsdla_b200_shard_atoms",
 )
 
 

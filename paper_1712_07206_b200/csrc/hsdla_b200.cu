@@ -697,6 +697,15 @@ int hsdla_b200_flop_model(int variant, uint64_t na, uint64_t nl, uint64_t ng, ui
   });
 }
 
+int hsdla_b200_shard_atoms(uint64_t n_atoms, int parts, uint64_t* bounds) {
+  return guarded([&] {
+    if (!bounds || parts < 1) throw Fail{HSDLA_B200_CONFIG_ERROR, "shard_atoms: parts must be >= 1"};
+    if (static_cast<uint64_t>(parts) > n_atoms) throw Fail{HSDLA_B200_CONFIG_ERROR, "more GPUs than atoms"};
+    const auto b = shard_atoms(n_atoms, parts);
+    std::copy(b.begin(), b.end(), bounds);
+  });
+}
+
 int hsdla_b200_host_register(void* ptr, size_t bytes) {
   return guarded([&] { HS_CUDA(cudaHostRegister(ptr, bytes, cudaHostRegisterPortable)); });
 }

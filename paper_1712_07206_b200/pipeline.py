@@ -261,6 +261,13 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def shard_atoms(n_atoms, parts):
+    """Contiguous count-balanced atom ranges (the engine's multi-GPU partition)."""
+    out = (C.c_uint64 * (parts + 1))()
+    check(_lib.lib().hsdla_b200_shard_atoms(C.c_uint64(n_atoms), C.c_int(parts), out), "shard_atoms")
+    return [int(x) for x in out]
+
+
 def device_count():
     n = C.c_int(0)
     check(_lib.lib().hsdla_b200_device_count(C.byref(n)), "device_count")
