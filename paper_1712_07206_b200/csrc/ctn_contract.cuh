@@ -50,7 +50,11 @@ struct alignas(64) CtnParams {
   int n;                   // TRI: order N_G.  BATCH: number of output columns (N_G)
   int m_valid;             // BATCH: valid output rows per atom (N_L)
   int tiles;               // TRI: tiles per dimension
+  int tiles_total;         // TRI: lower tiles t(t+1)/2
   double2* out;            // TRI: packed lower.  BATCH: column-major stacked buffer
+  double* sk_ws;           // TRI stream-K: per-CTA partial-accumulator slots
+  uint32_t* sk_flags;      // TRI stream-K: per-CTA publish flags (== epoch when the slot is ready)
+  uint32_t epoch;          // TRI stream-K: unique per launch
   uint64_t ldo;            // BATCH: output leading dimension (complex elements)
   double alpha_re, alpha_im;
   double beta;             // real; 0 => C is never read
@@ -127,11 +131,75 @@ struct CtnCfg {
   static constexpr int kSmemBytes = STAGES * kStageBytes + 1024 /*align*/ + 2 * STAGES * 8 + 64;
 };
 
+// ---------------------------------------------------------------------------
+// Work decomposition.  BATCH: one whole tile per CTA (grid = tiles x atoms).
+// TRI: persistent CTAs (grid = #SMs) with a data-parallel + stream-K split:
+// all full waves but the last are whole tiles (tile b, b+G, ...); the remaining
+// tiles' k-iterations are divided evenly over the G CTAs, so the last wave has no
+// idle SMs.  A tile cut between CTAs is finished by its OWNER (the CTA holding its
+// k = 0 piece, processed LAST in that CTA's range); the other contributors process
+// their piece FIRST, park the partial accumulators in a workspace slot and publish
+// a per-CTA flag (release/acquire).  The owner adds partials in a fixed order,
+// so the result is bitwise deterministic run to run.
+// ---------------------------------------------------------------------------
+struct Piece {
+  int tile, k0, k1;
+  int kind;  // 0 whole tile, 1 owner (k0 == 0, k1 < I), 2 contributor (k0 > 0)
+};
+
+struct TriSched {
+  int G, b, I, dp_tiles, dp_next;
+  long long sk_total, sk_pos, sk_end;
+  __device__ TriSched(int tiles, int iters, int grid, int block) : G(grid), b(block), I(iters) {
+    dp_tiles = (tiles % grid == 0) ? tiles : max(0, tiles / grid - 1) * grid;
+    sk_total = static_cast<long long>(tiles - dp_tiles) * iters;
+    sk_pos = start(block);
+    sk_end = start(block + 1);
+    dp_next = block;
+  }
+  __device__ long long start(int cta) const { return sk_total * cta / G; }
+  __device__ bool next(Piece& p) {
+    if (dp_next < dp_tiles) {
+      p.tile = dp_next;
+      p.k0 = 0;
+      p.k1 = I;
+      p.kind = 0;
+      dp_next += G;
+      return true;
+    }
+    if (sk_pos < sk_end) {
+      const int t = static_cast<int>(sk_pos / I);
+      p.k0 = static_cast<int>(sk_pos - static_cast<long long>(t) * I);
+      const long long rem = sk_end - sk_pos;
+      p.k1 = static_cast<int>(p.k0 + rem < I ? p.k0 + rem : I);
+      p.tile = dp_tiles + t;
+      p.kind = (p.k0 == 0 && p.k1 == I) ? 0 : (p.k0 == 0 ? 1 : 2);
+      sk_pos += p.k1 - p.k0;
+      return true;
+    }
+    return false;
+  }
+};
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void consumer_bar(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
 template <int MODE, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, int MINB = 1>
 __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>::kThreads, MINB)
     ctn_contract_kernel(const __grid_constant__ CtnParams P) {
   using Cfg = CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>;
   constexpr int MB = Cfg::kMB, NB = Cfg::kNB;
+  constexpr int NCT = Cfg::kConsumerWarps * 32;  // consumer threads
+  constexpr int NACC = MB * NB * 4;              // accumulator doubles per consumer thread
   static_assert(BM % (8 * WARPS_M) == 0 && BN % (8 * WARPS_N) == 0, "tile shape");
 
   extern __shared__ uint8_t smem_raw[];
@@ -142,20 +210,6 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
-  // ---- which output tile --------------------------------------------------
-  int row0, col0, atom;
-  if (MODE == kTri) {
-    int ti, tj;
-    tri_tile(blockIdx.x, ti, tj);
-    row0 = ti * BM;
-    col0 = tj * BN;
-    atom = 0;
-  } else {
-    col0 = blockIdx.x * BN;
-    row0 = blockIdx.y * BM;
-    atom = blockIdx.z;
-  }
-
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -165,10 +219,25 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>
   }
   __syncthreads();
 
-  int total = 0;
+  int iters = 0;
 #pragma unroll
   for (int s = 0; s < kMaxSeg; ++s)
-    if (s < P.nseg) total += P.kchunks[s];
+    if (s < P.nseg) iters += P.kchunks[s];
+
+  // tile coordinates of a piece
+  auto tile_origin = [&](int tile, int& row0, int& col0, int& atom) {
+    if (MODE == kTri) {
+      int ti, tj;
+      tri_tile(tile, ti, tj);
+      row0 = ti * BM;
+      col0 = tj * BN;
+      atom = 0;
+    } else {
+      col0 = blockIdx.x * BN;
+      row0 = blockIdx.y * BM;
+      atom = blockIdx.z;
+    }
+  };
 
   if (warp == Cfg::kConsumerWarps) {
     // ===================== TMA producer (one lane) =========================
@@ -177,34 +246,45 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>
         prefetch_map(&P.L[s]);
         prefetch_map(&P.R[s]);
       }
-      int seg = 0, kc = 0;
-      for (int c = 0; c < total; ++c) {
-        while (kc >= P.kchunks[seg]) {
-          kc = 0;
-          ++seg;
+      TriSched sched(P.tiles_total, iters, gridDim.x, blockIdx.x);
+      Piece pc;
+      bool have = MODE == kTri ? sched.next(pc) : true;
+      if (MODE != kTri) pc = Piece{0, 0, iters, 0};
+      int it = 0;
+      while (have) {
+        int row0, col0, atom;
+        tile_origin(pc.tile, row0, col0, atom);
+        int seg = 0, kc = pc.k0;
+        while (seg < P.nseg - 1 && kc >= P.kchunks[seg]) kc -= P.kchunks[seg++];
+        for (int c = pc.k0; c < pc.k1; ++c, ++it) {
+          while (kc >= P.kchunks[seg]) {
+            kc = 0;
+            ++seg;
+          }
+          const int slot = it % STAGES;
+          mbar_wait(&empty[slot], ((it / STAGES) & 1) ^ 1);
+          uint8_t* sL = smem + slot * Cfg::kStageBytes;
+          uint8_t* sR = sL + Cfg::kStageL;
+          mbar_arrive_expect_tx(&full[slot], Cfg::kStageBytes);
+          const int x = kc * 2 * kChunkC;
+          if (P.l_row_z[seg])
+            tma_load_3d(sL, &P.L[seg], x, atom, row0, &full[slot]);
+          else
+            tma_load_3d(sL, &P.L[seg], x, row0, atom, &full[slot]);
+          if (P.r_row_z[seg])
+            tma_load_3d(sR, &P.R[seg], x, atom, col0, &full[slot]);
+          else
+            tma_load_3d(sR, &P.R[seg], x, col0, atom, &full[slot]);
+          ++kc;
         }
-        const int slot = c % STAGES;
-        const uint32_t par = ((c / STAGES) & 1) ^ 1;
-        mbar_wait(&empty[slot], par);
-        uint8_t* sL = smem + slot * Cfg::kStageBytes;
-        uint8_t* sR = sL + Cfg::kStageL;
-        mbar_arrive_expect_tx(&full[slot], Cfg::kStageBytes);
-        const int x = kc * 2 * kChunkC;
-        if (P.l_row_z[seg])
-          tma_load_3d(sL, &P.L[seg], x, atom, row0, &full[slot]);
-        else
-          tma_load_3d(sL, &P.L[seg], x, row0, atom, &full[slot]);
-        if (P.r_row_z[seg])
-          tma_load_3d(sR, &P.R[seg], x, atom, col0, &full[slot]);
-        else
-          tma_load_3d(sR, &P.R[seg], x, col0, atom, &full[slot]);
-        ++kc;
+        have = MODE == kTri ? sched.next(pc) : false;
       }
     }
     return;
   }
 
   // ======================= DMMA consumers =================================
+  const int ctid = threadIdx.x;  // 0 .. NCT-1
   const int wm = warp % WARPS_M;
   const int wn = warp / WARPS_M;
   const int g = lane >> 2;
@@ -219,89 +299,135 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>
 #pragma unroll
   for (int kk = 0; kk < 2; ++kk) offK[kk] = ((4 * kk + q) ^ pg) << 4;
 
-  double cre[MB][NB][2], cim[MB][NB][2];
+  TriSched sched(P.tiles_total, iters, gridDim.x, blockIdx.x);
+  Piece pc;
+  bool have = MODE == kTri ? sched.next(pc) : true;
+  if (MODE != kTri) pc = Piece{0, 0, iters, 0};
+  int it = 0;
+  while (have) {
+    double acc[MB][NB][2][2];  // [mb][nb][e][re/im]
 #pragma unroll
-  for (int mb = 0; mb < MB; ++mb)
+    for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
-    for (int nb = 0; nb < NB; ++nb) {
-      cre[mb][nb][0] = cre[mb][nb][1] = 0.0;
-      cim[mb][nb][0] = cim[mb][nb][1] = 0.0;
-    }
+      for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) acc[mb][nb][e][0] = acc[mb][nb][e][1] = 0.0;
 
-  for (int c = 0; c < total; ++c) {
-    const int slot = c % STAGES;
-    mbar_wait(&full[slot], (c / STAGES) & 1);
-    const uint8_t* st = smem + slot * Cfg::kStageBytes;
+    for (int c = pc.k0; c < pc.k1; ++c, ++it) {
+      const int slot = it % STAGES;
+      mbar_wait(&full[slot], (it / STAGES) & 1);
+      const uint8_t* st = smem + slot * Cfg::kStageBytes;
 #pragma unroll
-    for (int kk = 0; kk < 2; ++kk) {
-      double2 a[MB], b[NB];
-      double nbr[NB];
+      for (int kk = 0; kk < 2; ++kk) {
+        double2 a[MB], b[NB];
+        double nbr[NB];
 #pragma unroll
-      for (int mb = 0; mb < MB; ++mb) a[mb] = *reinterpret_cast<const double2*>(st + offL[mb] + offK[kk]);
+        for (int mb = 0; mb < MB; ++mb) a[mb] = *reinterpret_cast<const double2*>(st + offL[mb] + offK[kk]);
 #pragma unroll
-      for (int nb = 0; nb < NB; ++nb) {
-        b[nb] = *reinterpret_cast<const double2*>(st + offR[nb] + offK[kk]);
-        nbr[nb] = -b[nb].x;
+        for (int nb = 0; nb < NB; ++nb) {
+          b[nb] = *reinterpret_cast<const double2*>(st + offR[nb] + offK[kk]);
+          nbr[nb] = -b[nb].x;
+        }
+        // Four independent sweeps so consecutive DMMAs never share an accumulator.
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb) dmma(acc[mb][nb][0][0], acc[mb][nb][1][0], a[mb].x, b[nb].x);
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb) dmma(acc[mb][nb][0][1], acc[mb][nb][1][1], a[mb].x, b[nb].y);
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb) dmma(acc[mb][nb][0][0], acc[mb][nb][1][0], a[mb].y, b[nb].y);
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb) dmma(acc[mb][nb][0][1], acc[mb][nb][1][1], a[mb].y, nbr[nb]);
       }
-      // Four independent sweeps so consecutive DMMAs never share an accumulator.
-#pragma unroll
-      for (int mb = 0; mb < MB; ++mb)
-#pragma unroll
-        for (int nb = 0; nb < NB; ++nb) dmma(cre[mb][nb][0], cre[mb][nb][1], a[mb].x, b[nb].x);
-#pragma unroll
-      for (int mb = 0; mb < MB; ++mb)
-#pragma unroll
-        for (int nb = 0; nb < NB; ++nb) dmma(cim[mb][nb][0], cim[mb][nb][1], a[mb].x, b[nb].y);
-#pragma unroll
-      for (int mb = 0; mb < MB; ++mb)
-#pragma unroll
-        for (int nb = 0; nb < NB; ++nb) dmma(cre[mb][nb][0], cre[mb][nb][1], a[mb].y, b[nb].y);
-#pragma unroll
-      for (int mb = 0; mb < MB; ++mb)
-#pragma unroll
-        for (int nb = 0; nb < NB; ++nb) dmma(cim[mb][nb][0], cim[mb][nb][1], a[mb].y, nbr[nb]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[slot]);
-  }
 
-  // ---- epilogue -------------------------------------------------------------
-  const double ar = P.alpha_re, ai = P.alpha_im, beta = P.beta;
+    if (MODE == kTri && pc.kind == 2) {
+      // contributor: park the partial, publish the flag
+      double* ws = P.sk_ws + static_cast<size_t>(blockIdx.x) * NACC * NCT;
 #pragma unroll
-  for (int mb = 0; mb < MB; ++mb) {
-    const int i = row0 + wm * Cfg::kWM + 8 * mb + pg;
+      for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
-    for (int nb = 0; nb < NB; ++nb) {
+        for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int j = col0 + wn * Cfg::kWN + 8 * nb + (e ? 4 + q : q);
-        const double xr = cre[mb][nb][e], xi = cim[mb][nb][e];
-        double vr = ar * xr - ai * xi;
-        double vi = ar * xi + ai * xr;
-        if (MODE == kTri) {
-          if (i < P.n && j < P.n && i >= j) {
-            if (i == j) vi = 0.0;
-            double2* dst = P.out + packed_index(P.n, i, j);
-            if (beta != 0.0) {
-              const double2 o = *dst;
-              vr += beta * o.x;
-              vi += beta * o.y;
+          for (int e = 0; e < 2; ++e)
+#pragma unroll
+            for (int r = 0; r < 2; ++r) __stcg(ws + ((((mb * NB + nb) * 2 + e) * 2 + r) * NCT + ctid), acc[mb][nb][e][r]);
+      __threadfence();
+      consumer_bar(NCT);
+      if (ctid == 0) st_release_u32(P.sk_flags + blockIdx.x, P.epoch);
+    } else {
+      if (MODE == kTri && pc.kind == 1) {
+        // owner: add the later pieces of this tile, in CTA order (deterministic)
+        const long long tile_end = static_cast<long long>(pc.tile - sched.dp_tiles + 1) * sched.I;
+        for (int b2 = blockIdx.x + 1; b2 < static_cast<int>(gridDim.x) && sched.start(b2) < tile_end; ++b2) {
+          if (sched.start(b2 + 1) == sched.start(b2)) continue;  // empty range
+          if (ctid == 0)
+            while (ld_acquire_u32(P.sk_flags + b2) != P.epoch) __nanosleep(64);
+          consumer_bar(NCT);
+          const double* ws = P.sk_ws + static_cast<size_t>(b2) * NACC * NCT;
+#pragma unroll
+          for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+              for (int e = 0; e < 2; ++e)
+#pragma unroll
+                for (int r = 0; r < 2; ++r)
+                  acc[mb][nb][e][r] += __ldcg(ws + ((((mb * NB + nb) * 2 + e) * 2 + r) * NCT + ctid));
+        }
+      }
+      // ---- epilogue ---------------------------------------------------------
+      int row0, col0, atom;
+      tile_origin(pc.tile, row0, col0, atom);
+      const double ar = P.alpha_re, ai = P.alpha_im, beta = P.beta;
+#pragma unroll
+      for (int mb = 0; mb < MB; ++mb) {
+        const int i = row0 + wm * Cfg::kWM + 8 * mb + pg;
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int j = col0 + wn * Cfg::kWN + 8 * nb + (e ? 4 + q : q);
+            const double xr = acc[mb][nb][e][0], xi = acc[mb][nb][e][1];
+            double vr = ar * xr - ai * xi;
+            double vi = ar * xi + ai * xr;
+            if (MODE == kTri) {
+              if (i < P.n && j < P.n && i >= j) {
+                if (i == j) vi = 0.0;
+                double2* dst = P.out + packed_index(P.n, i, j);
+                if (beta != 0.0) {
+                  const double2 o = *dst;
+                  vr += beta * o.x;
+                  vi += beta * o.y;
+                }
+                *dst = make_double2(vr, vi);
+              }
+            } else {
+              if (i < P.m_valid && j < P.n) {
+                double2* dst =
+                    P.out + (static_cast<uint64_t>(atom) * P.m_valid + i) + static_cast<uint64_t>(j) * P.ldo;
+                if (beta != 0.0) {
+                  const double2 o = *dst;
+                  vr += beta * o.x;
+                  vi += beta * o.y;
+                }
+                *dst = make_double2(vr, vi);
+              }
             }
-            *dst = make_double2(vr, vi);
-          }
-        } else {
-          if (i < P.m_valid && j < P.n) {
-            double2* dst = P.out + (static_cast<uint64_t>(atom) * P.m_valid + i) + static_cast<uint64_t>(j) * P.ldo;
-            if (beta != 0.0) {
-              const double2 o = *dst;
-              vr += beta * o.x;
-              vi += beta * o.y;
-            }
-            *dst = make_double2(vr, vi);
           }
         }
       }
     }
+    have = MODE == kTri ? sched.next(pc) : false;
   }
 }
 

@@ -187,6 +187,10 @@ struct hsdla_b200_engine {
   bool reduced = false;
   int launches = 0;
   uint64_t device_bytes = 0, temp_bytes = 0;
+  int sms = 148;             // persistent TRI grid
+  double* sk_ws = nullptr;   // stream-K workspace (sms slots x 64x64 complex)
+  uint32_t* sk_flags = nullptr;
+  uint32_t epoch = 0;
   hsdla_b200::CtnParams p_s, p_z, p_x, p_h, p_h2k, p_hkx;
   // per-build CUDA events around the S and H contraction launches (roofline timing
   // over a whole timed region without per-step host syncs)
@@ -222,7 +226,7 @@ static void dalloc(hsdla_b200_engine* e, T** p, uint64_t count) {
 
 static void engine_free(hsdla_b200_engine* e) {
   cudaSetDevice(e->device);
-  for (void* p : {(void*)e->A, (void*)e->B, (void*)e->X1, (void*)e->X2, (void*)e->Tab, (void*)e->Taa,
+  for (void* p : {(void*)e->sk_ws, (void*)e->sk_flags, (void*)e->A, (void*)e->B, (void*)e->X1, (void*)e->X2, (void*)e->Tab, (void*)e->Taa,
                   (void*)e->Tbb, (void*)e->Paa, (void*)e->Pbb, (void*)e->U, (void*)e->Hp, (void*)e->Sp})
     if (p) cudaFree(p);
   if (e->host_stage) cudaFreeHost(e->host_stage);
@@ -260,7 +264,10 @@ static void build_params(hsdla_b200_engine* e) {
     std::memset(&P, 0, sizeof(P));
     P.n = static_cast<int>(ng);
     P.tiles = tiles;
+    P.tiles_total = tiles * (tiles + 1) / 2;
     P.out = out;
+    P.sk_ws = e->sk_ws;
+    P.sk_flags = e->sk_flags;
     P.alpha_re = 1.0;
     P.alpha_im = 0.0;
     P.beta = beta;
@@ -284,7 +291,9 @@ static void build_params(hsdla_b200_engine* e) {
   tri_base(e->p_hkx, e->Hp, 1.0);
   set_tri_seg(e->p_hkx, 0, mA, mX1, K);
   e->p_hkx.nseg = 1;
-  e->grid_tri = dim3(static_cast<unsigned>(static_cast<uint64_t>(tiles) * (tiles + 1) / 2));
+  // persistent stream-K grid: one CTA per SM, never more CTAs than k-iterations
+  const uint64_t tri_tiles = static_cast<uint64_t>(tiles) * (tiles + 1) / 2;
+  e->grid_tri = dim3(static_cast<unsigned>(std::min<uint64_t>(e->sms, tri_tiles * chunks(K))));
 
   // batched per-atom products: operators {2nl, nl, na} (row i in dim 1, atom in dim 2),
   // coefficient views {2nl, na, ng} (atom in dim 1, G row in dim 2).
@@ -367,6 +376,10 @@ static hsdla_b200_engine* engine_create(int device, uint64_t na, uint64_t nl, ui
     dalloc(e.get(), &e->U, e->K);
     dalloc(e.get(), &e->Hp, e->npk);
     dalloc(e.get(), &e->Sp, e->npk);
+    HS_CUDA(cudaDeviceGetAttribute(&e->sms, cudaDevAttrMultiProcessorCount, device));
+    dalloc(e.get(), &e->sk_ws, static_cast<uint64_t>(e->sms) * kTriBM * kTriBM * 2);
+    dalloc(e.get(), &e->sk_flags, static_cast<uint64_t>(e->sms));
+    HS_CUDA(cudaMemset(e->sk_flags, 0, e->sms * sizeof(uint32_t)));
     build_params(e.get());
   } catch (...) {
     engine_free(e.get());
@@ -400,7 +413,8 @@ static void engine_upload(hsdla_b200_engine* e, const hsdla_b200_problem* p, uin
   HS_CUDA(cudaMemcpyAsync(e->U, p->U + r0, e->K * sizeof(double), cudaMemcpyHostToDevice, e->stream));
 }
 
-static void launch_tri(hsdla_b200_engine* e, const CtnParams& P) {
+static void launch_tri(hsdla_b200_engine* e, CtnParams& P) {
+  P.epoch = ++e->epoch;  // fresh stream-K flag generation per launch
   tri_kernel<<<e->grid_tri, TriCfg::kThreads, TriCfg::kSmemBytes, e->stream>>>(P);
   HS_CUDA(cudaGetLastError());
   ++e->launches;
