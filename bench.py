@@ -328,8 +328,7 @@ def run_e2e(args, hb, d, p, eng, na_total, nl, ng):
             hb.release_cache()
         else:
             def one():
-                eng.upload(p, 0)
-                eng.build(args.algo)
+                eng.build_streamed(p, 0, args.algo)
                 eng.reduce(0)
                 if d.rank == 0:
                     eng.download(H, S)

@@ -134,6 +134,12 @@ int hsdla_b200_engine_destroy(hsdla_b200_engine* e);
 int hsdla_b200_engine_upload(hsdla_b200_engine* e, const hsdla_b200_problem* p, uint64_t atom_begin);
 /* Enqueue the full build (all phases) on the engine stream; asynchronous. */
 int hsdla_b200_engine_build(hsdla_b200_engine* e, int algo);
+/* Streamed build from HOST memory: uploads shard `atom_begin` of p in atom chunks on
+ * a copy stream, each chunk's phases start as soon as its bytes land, H and S
+ * accumulate over chunks.  Asynchronous w.r.t. the host for pinned p; follow with
+ * reduce / sync / download as for engine_build. */
+int hsdla_b200_engine_build_streamed(hsdla_b200_engine* e, const hsdla_b200_problem* p, uint64_t atom_begin,
+                                     int algo);
 /* NCCL sum-reduce of the packed partial H and S to rank `root` (no-op without comm). */
 int hsdla_b200_engine_reduce(hsdla_b200_engine* e, int root);
 /* Wait for the engine's streams; fills phase/device timings of the last build. */

@@ -19,7 +19,7 @@ EXPORTS = (
     "hsdla_b200_build_hs", "hsdla_b200_flop_model", "hsdla_b200_generate_problem", "hsdla_b200_last_error",
     "hsdla_b200_device_count", "hsdla_b200_host_register", "hsdla_b200_host_unregister",
     "hsdla_b200_release_cache", "hsdla_b200_engine_create", "hsdla_b200_engine_destroy",
-    "hsdla_b200_engine_upload", "hsdla_b200_engine_build", "hsdla_b200_engine_reduce",
+    "hsdla_b200_engine_upload", "hsdla_b200_engine_build", "hsdla_b200_engine_build_streamed", "hsdla_b200_engine_reduce",
     "hsdla_b200_engine_sync", "hsdla_b200_engine_download", "hsdla_b200_engine_device_results",
     "hsdla_b200_engine_stream", "hsdla_b200_nccl_unique_id", "hsdla_b200_engine_set_comm",
     "hsdla_b200_engine_kernel_times", "hsdla_b200_fp64_peak", "hsdla_b200_shard_atoms",

@@ -97,6 +97,12 @@ __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 
+__device__ __forceinline__ double2 lds128(uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
       : "+d"(c0), "+d"(c1)
@@ -313,41 +319,59 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>
 #pragma unroll
         for (int e = 0; e < 2; ++e) acc[mb][nb][e][0] = acc[mb][nb][e][1] = 0.0;
 
-    for (int c = pc.k0; c < pc.k1; ++c, ++it) {
-      const int slot = it % STAGES;
-      mbar_wait(&full[slot], (it / STAGES) & 1);
-      const uint8_t* st = smem + slot * Cfg::kStageBytes;
+    // Software-pipelined main loop: the fragments of step s+1 (next kk, or the next
+    // stage's first kk) are loaded before the 32 DMMAs of step s issue, so LDS latency
+    // and the stage-full wait hide behind the tensor pipe.
+    struct Frag {
+      double2 a[MB], b[NB];
+    };
+    auto load_frag = [&](Frag& f, const uint8_t* st, int kk) {
+      const uint32_t base = smem_u32(st) + offK[kk];
 #pragma unroll
-      for (int kk = 0; kk < 2; ++kk) {
-        double2 a[MB], b[NB];
-        double nbr[NB];
+      for (int mb = 0; mb < MB; ++mb) f.a[mb] = lds128(base + offL[mb]);
 #pragma unroll
-        for (int mb = 0; mb < MB; ++mb) a[mb] = *reinterpret_cast<const double2*>(st + offL[mb] + offK[kk]);
+      for (int nb = 0; nb < NB; ++nb) f.b[nb] = lds128(base + offR[nb]);
+    };
+    auto mma_frag = [&](const Frag& f) {
+      // Four independent sweeps so consecutive DMMAs never share an accumulator.
 #pragma unroll
-        for (int nb = 0; nb < NB; ++nb) {
-          b[nb] = *reinterpret_cast<const double2*>(st + offR[nb] + offK[kk]);
-          nbr[nb] = -b[nb].x;
-        }
-        // Four independent sweeps so consecutive DMMAs never share an accumulator.
+      for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
-        for (int mb = 0; mb < MB; ++mb)
+        for (int nb = 0; nb < NB; ++nb) dmma(acc[mb][nb][0][0], acc[mb][nb][1][0], f.a[mb].x, f.b[nb].x);
 #pragma unroll
-          for (int nb = 0; nb < NB; ++nb) dmma(acc[mb][nb][0][0], acc[mb][nb][1][0], a[mb].x, b[nb].x);
+      for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
-        for (int mb = 0; mb < MB; ++mb)
+        for (int nb = 0; nb < NB; ++nb) dmma(acc[mb][nb][0][1], acc[mb][nb][1][1], f.a[mb].x, f.b[nb].y);
 #pragma unroll
-          for (int nb = 0; nb < NB; ++nb) dmma(acc[mb][nb][0][1], acc[mb][nb][1][1], a[mb].x, b[nb].y);
+      for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
-        for (int mb = 0; mb < MB; ++mb)
+        for (int nb = 0; nb < NB; ++nb) dmma(acc[mb][nb][0][0], acc[mb][nb][1][0], f.a[mb].y, f.b[nb].y);
 #pragma unroll
-          for (int nb = 0; nb < NB; ++nb) dmma(acc[mb][nb][0][0], acc[mb][nb][1][0], a[mb].y, b[nb].y);
+      for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
-        for (int mb = 0; mb < MB; ++mb)
-#pragma unroll
-          for (int nb = 0; nb < NB; ++nb) dmma(acc[mb][nb][0][1], acc[mb][nb][1][1], a[mb].y, nbr[nb]);
+        for (int nb = 0; nb < NB; ++nb) dmma(acc[mb][nb][0][1], acc[mb][nb][1][1], f.a[mb].y, -f.b[nb].x);
+    };
+    if (pc.k1 > pc.k0) {
+      Frag f0, f1;
+      {
+        const int slot = it % STAGES;
+        mbar_wait(&full[slot], (it / STAGES) & 1);
+        load_frag(f0, smem + slot * Cfg::kStageBytes, 0);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
+      for (int c = pc.k0; c < pc.k1; ++c, ++it) {
+        const int slot = it % STAGES;
+        const uint8_t* st = smem + slot * Cfg::kStageBytes;
+        load_frag(f1, st, 1);
+        mma_frag(f0);
+        if (c + 1 < pc.k1) {
+          const int nslot = (it + 1) % STAGES;
+          mbar_wait(&full[nslot], ((it + 1) / STAGES) & 1);
+          load_frag(f0, smem + nslot * Cfg::kStageBytes, 0);
+        }
+        mma_frag(f1);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+      }
     }
 
     if (MODE == kTri && pc.kind == 2) {

@@ -3,14 +3,20 @@
 // Drop-in for hsdla::pipeline::build_hs_refined (reference pipeline.cpp:281-329).
 // Device data layout (one engine per GPU / atom shard, all HBM-resident):
 //   A, B    K x N_G complex, column-major, ld = K (= the reference stacking,
-//           problem.hpp:20-21; uploaded with one strided 2-D copy per matrix)
+//           problem.hpp:20-21; uploaded with strided 2-D copies from the caller)
 //   X1      K x N_G: first U*B (phase s, diag_scale kernels.cpp:438-450), then
 //           T_AA A (hemm_loop, pipeline.cpp:314-321)
 //   X2      K x N_G: Z = T_AB^H A + 1/2 T_BB B (z_loop, pipeline.cpp:302-307)
 //   Tab     raw per-atom T_AB blocks (used as-is: Z = T_AB^H A is a CTN product)
 //   Pbb,Paa 1/2 full(T_BB), full(T_AA) expanded from the LOWER triangles only
 //   Hp, Sp  packed-lower N_G(N_G+1)/2 complex (halves D2H and NCCL bytes)
-// Phases run in the reference order on one stream, CUDA-event timed.
+//
+// A build is a list of atom CHUNKS.  The device-resident build is one chunk over
+// all atoms.  The streamed build (the one-shot drop-in with host buffers) splits
+// the atoms into chunks: chunk c+1 is copied host->device on the copy stream while
+// chunk c's phases run, and every contraction accumulates into H, S (beta = 1 after
+// the first chunk) — H and S are sums over atoms, so any chunking is exact up to
+// FP64 rounding order.  S is downloaded and unpacked on the host while H computes.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -39,31 +45,26 @@ namespace hsdla_b200 {
 // ---------------------------------------------------------------------------
 thread_local std::string g_last_error;
 
-struct Status {
-  int code;
-  std::string msg;
-};
-
 struct Fail {
   int code;
   std::string msg;
 };
 
-#define HS_CUDA(x)                                                                              \
-  do {                                                                                          \
-    cudaError_t e_ = (x);                                                                       \
-    if (e_ != cudaSuccess) {                                                                    \
-      (void)cudaGetLastError();                                                                 \
+#define HS_CUDA(x)                                                                                 \
+  do {                                                                                             \
+    cudaError_t e_ = (x);                                                                          \
+    if (e_ != cudaSuccess) {                                                                       \
+      (void)cudaGetLastError();                                                                    \
       throw Fail{e_ == cudaErrorMemoryAllocation ? HSDLA_B200_SIZING_ERROR : HSDLA_B200_CUDA_ERROR, \
-                 std::string(#x) + ": " + cudaGetErrorString(e_)};                              \
-    }                                                                                           \
+                 std::string(#x) + ": " + cudaGetErrorString(e_)};                                 \
+    }                                                                                              \
   } while (0)
 
-#define HS_NCCL(x)                                                                   \
-  do {                                                                               \
-    ncclResult_t r_ = (x);                                                           \
-    if (r_ != ncclSuccess)                                                           \
-      throw Fail{HSDLA_B200_NCCL_ERROR, std::string(#x) + ": " + ncclGetErrorString(r_)}; \
+#define HS_NCCL(x)                                                                            \
+  do {                                                                                        \
+    ncclResult_t r_ = (x);                                                                    \
+    if (r_ != ncclSuccess)                                                                    \
+      throw Fail{HSDLA_B200_NCCL_ERROR, std::string(#x) + ": " + ncclGetErrorString(r_)};     \
   } while (0)
 
 template <class F>
@@ -87,15 +88,16 @@ int guarded(F&& f) {
 // elementwise kernels (HBM-bound)
 // ---------------------------------------------------------------------------
 
-// X = diag(u) B  (kernels.cpp:438-450); columns strided over blockIdx.y.
+// X = diag(u) B for rows [0, Kc) of a K-strided stack (kernels.cpp:438-450);
+// coalesced along K, columns strided over blockIdx.y.
 __global__ void diag_scale_kernel(const double2* __restrict__ B, const double* __restrict__ u,
-                                  double2* __restrict__ X, uint64_t K, uint64_t ng) {
+                                  double2* __restrict__ X, uint64_t Kc, uint64_t ld, uint64_t ng) {
   const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= K) return;
+  if (k >= Kc) return;
   const double s = u[k];
   for (uint64_t j = blockIdx.y; j < ng; j += gridDim.y) {
-    const double2 b = B[k + j * K];
-    X[k + j * K] = make_double2(s * b.x, s * b.y);
+    const double2 b = B[k + j * ld];
+    X[k + j * ld] = make_double2(s * b.x, s * b.y);
   }
 }
 
@@ -111,7 +113,8 @@ __global__ void expand_hermitian_kernel(const double2* __restrict__ taa, const d
   const uint64_t a = idx / blk;
   const int r = static_cast<int>(idx - a * blk);
   const int k = r % nl, i = r / nl;  // element (k, i) of the column-major block
-  const uint64_t lo = a * blk + (k >= i ? (k + static_cast<uint64_t>(i) * nl) : (i + static_cast<uint64_t>(k) * nl));
+  const uint64_t lo =
+      a * blk + (k >= i ? (k + static_cast<uint64_t>(i) * nl) : (i + static_cast<uint64_t>(k) * nl));
   double2 vaa = taa[lo], vbb = tbb[lo];
   if (k < i) {
     vaa.y = -vaa.y;
@@ -150,50 +153,65 @@ static void make_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1,
                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
-    throw Fail{HSDLA_B200_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")"};
+    throw Fail{HSDLA_B200_CUDA_ERROR,
+               "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")"};
 }
 
-// kernel shapes
+// kernel shapes (tools/tune_tri.cu sweep): TRI 64x64 tiles, 8 consumer warps of
+// 32x16; BATCH 32x128 tiles, 8 consumer warps of 32x16.
 constexpr int kTriBM = 64, kTriStages = 6;
 using TriCfg = CtnCfg<kTri, kTriBM, kTriBM, 2, 4, kTriStages>;
 constexpr int kBatBM = 32, kBatBN = 128, kBatStages = 4;
-using BatCfg = CtnCfg<kBatch, kBatBM, kBatBN, 1, 4, kBatStages>;
+using BatCfg = CtnCfg<kBatch, kBatBM, kBatBN, 1, 8, kBatStages>;
 
 static auto tri_kernel = ctn_contract_kernel<kTri, kTriBM, kTriBM, 2, 4, kTriStages>;
-static auto bat_kernel = ctn_contract_kernel<kBatch, kBatBM, kBatBN, 1, 4, kBatStages>;
+static auto bat_kernel = ctn_contract_kernel<kBatch, kBatBM, kBatBN, 1, 8, kBatStages>;
 
-// ---------------------------------------------------------------------------
-// engine
-// ---------------------------------------------------------------------------
-enum Ev { EV_START, EV_S_BEGIN, EV_S_END, EV_Z_END, EV_HER2K_BEGIN, EV_HER2K_END, EV_HEMM_END, EV_HERKX_BEGIN,
-          EV_END, EV_REDUCE_END, EV_COUNT };
+static int chunks_of(uint64_t kcomplex) { return static_cast<int>((kcomplex + kChunkC - 1) / kChunkC); }
+
+// One atom chunk [a0, a1) of a build: the parameter blocks of every launch.
+struct ChunkPlan {
+  uint64_t a0 = 0, a1 = 0;
+  CtnParams s, z, x, h, h2k, hkx;  // h = fused her2k+herkx
+  dim3 grid_tri, grid_bat;
+};
+
+struct OpTime {
+  int phase;
+  cudaEvent_t b, e;
+};
 
 }  // namespace hsdla_b200
 
 struct hsdla_b200_engine {
   int device = 0;
   uint64_t na = 0, nl = 0, ng = 0, K = 0, npk = 0;
-  cudaStream_t stream = nullptr, comm_stream = nullptr;
+  cudaStream_t stream = nullptr, copy_stream = nullptr, comm_stream = nullptr;
   double2 *A = nullptr, *B = nullptr, *X1 = nullptr, *X2 = nullptr;
   double2 *Tab = nullptr, *Taa = nullptr, *Tbb = nullptr, *Paa = nullptr, *Pbb = nullptr;
   double* U = nullptr;
   double2 *Hp = nullptr, *Sp = nullptr;
   double2* host_stage = nullptr;  // pinned, 2 * npk
-  cudaEvent_t ev[hsdla_b200::EV_COUNT] = {};
-  cudaEvent_t ev_s_done = nullptr;
-  ncclComm_t comm = nullptr;
-  int nranks = 1, rank = 0;
-  int last_algo = 0;
-  bool reduced = false;
-  int launches = 0;
-  uint64_t device_bytes = 0, temp_bytes = 0;
-  int sms = 148;             // persistent TRI grid
-  double* sk_ws = nullptr;   // stream-K workspace (sms slots x 64x64 complex)
+  int sms = 148;                  // persistent TRI grid
+  double* sk_ws = nullptr;        // stream-K workspace (sms slots x 64x64 complex)
   uint32_t* sk_flags = nullptr;
   uint32_t epoch = 0;
-  hsdla_b200::CtnParams p_s, p_z, p_x, p_h, p_h2k, p_hkx;
-  // per-build CUDA events around the S and H contraction launches (roofline timing
-  // over a whole timed region without per-step host syncs)
+  uint64_t device_bytes = 0, temp_bytes = 0;
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+
+  std::vector<hsdla_b200::ChunkPlan> whole, streamed;
+  // per-build timing
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<hsdla_b200::OpTime> ops;
+  cudaEvent_t ev_begin = nullptr, ev_end = nullptr, ev_s_done = nullptr, ev_s_red = nullptr,
+              ev_reduce_end = nullptr, ev_up0 = nullptr, ev_up1 = nullptr, ev_s_d2h = nullptr,
+              ev_h_d2h = nullptr;
+  std::vector<cudaEvent_t> ev_chunk_up;
+  int last_algo = 0, launches = 0;
+  bool built = false, reduced = false, uploaded_streamed = false;
+  // roofline: events around the whole-build S and H contraction launches, harvested lazily
   static constexpr int kRing = 64;
   struct KTimer {
     cudaEvent_t s0 = nullptr, s1 = nullptr, h0 = nullptr, h1 = nullptr;
@@ -203,7 +221,6 @@ struct hsdla_b200_engine {
   uint64_t builds = 0;
   double sum_s_ms = 0, sum_h_ms = 0;
   uint64_t sum_flops_h = 0, timed_builds = 0;
-  dim3 grid_tri, grid_bat;
 };
 
 namespace hsdla_b200 {
@@ -213,8 +230,8 @@ static void check_dims(uint64_t na, uint64_t nl, uint64_t ng) {
   const uint64_t max = UINT64_MAX / 16 / 4;
   if (na > max / nl) throw Fail{HSDLA_B200_SIZING_ERROR, "n_atoms * n_l overflows"};
   if (na * nl > max / ng) throw Fail{HSDLA_B200_SIZING_ERROR, "problem allocation overflows"};
-  if (ng > (1u << 31) - 1 || na * nl > (1u << 30))
-    throw Fail{HSDLA_B200_SIZING_ERROR, "dimension exceeds the 32-bit tile coordinate range"};
+  if (ng > (1u << 31) - 1 || na * nl > (1u << 30) || nl > 4096)
+    throw Fail{HSDLA_B200_SIZING_ERROR, "dimension exceeds the supported coordinate range"};
 }
 
 template <class T>
@@ -226,40 +243,47 @@ static void dalloc(hsdla_b200_engine* e, T** p, uint64_t count) {
 
 static void engine_free(hsdla_b200_engine* e) {
   cudaSetDevice(e->device);
-  for (void* p : {(void*)e->sk_ws, (void*)e->sk_flags, (void*)e->A, (void*)e->B, (void*)e->X1, (void*)e->X2, (void*)e->Tab, (void*)e->Taa,
-                  (void*)e->Tbb, (void*)e->Paa, (void*)e->Pbb, (void*)e->U, (void*)e->Hp, (void*)e->Sp})
+  for (void* p : {(void*)e->sk_ws, (void*)e->sk_flags, (void*)e->A, (void*)e->B, (void*)e->X1, (void*)e->X2,
+                  (void*)e->Tab, (void*)e->Taa, (void*)e->Tbb, (void*)e->Paa, (void*)e->Pbb, (void*)e->U,
+                  (void*)e->Hp, (void*)e->Sp})
     if (p) cudaFree(p);
   if (e->host_stage) cudaFreeHost(e->host_stage);
-  for (auto& ev : e->ev)
+  for (cudaEvent_t ev : e->ev_pool) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : e->ev_chunk_up) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : {e->ev_begin, e->ev_end, e->ev_s_done, e->ev_s_red, e->ev_reduce_end, e->ev_up0, e->ev_up1,
+                         e->ev_s_d2h, e->ev_h_d2h})
     if (ev) cudaEventDestroy(ev);
-  if (e->ev_s_done) cudaEventDestroy(e->ev_s_done);
   for (auto& t : e->ring)
     for (cudaEvent_t ev : {t.s0, t.s1, t.h0, t.h1})
       if (ev) cudaEventDestroy(ev);
   if (e->comm) ncclCommDestroy(e->comm);
-  if (e->stream) cudaStreamDestroy(e->stream);
-  if (e->comm_stream) cudaStreamDestroy(e->comm_stream);
+  for (cudaStream_t s : {e->stream, e->copy_stream, e->comm_stream})
+    if (s) cudaStreamDestroy(s);
 }
 
-static int chunks(uint64_t kcomplex) { return static_cast<int>((kcomplex + kChunkC - 1) / kChunkC); }
-
-static void set_tri_seg(CtnParams& P, int s, const CUtensorMap& L, const CUtensorMap& R, uint64_t K) {
+static void set_seg(CtnParams& P, int s, const CUtensorMap& L, const CUtensorMap& R, uint64_t Kc) {
   P.L[s] = L;
   P.R[s] = R;
-  P.kchunks[s] = chunks(K);
+  P.kchunks[s] = chunks_of(Kc);
   P.l_row_z[s] = 0;
   P.r_row_z[s] = 0;
 }
 
-static void build_params(hsdla_b200_engine* e) {
-  const uint64_t K = e->K, ng = e->ng, nl = e->nl, na = e->na;
-  // 2-D K x N_G stacks as 3-D {2K, N_G, 1}
+// Parameter blocks for atoms [a0, a1).  `first` = the chunk that starts H and S
+// (beta 0); later chunks accumulate (beta 1).
+static void make_chunk(hsdla_b200_engine* e, uint64_t a0, uint64_t a1, bool first, ChunkPlan& cp) {
+  const uint64_t K = e->K, ng = e->ng, nl = e->nl;
+  const uint64_t r0 = a0 * nl, Kc = (a1 - a0) * nl, nac = a1 - a0;
+  cp.a0 = a0;
+  cp.a1 = a1;
+  // K-stacked buffers restricted to rows [r0, r0+Kc): {2Kc, N_G, 1}, column stride 2K
   CUtensorMap mA, mB, mX1, mX2;
-  make_map(&mA, e->A, 2 * K, ng, 1, 2 * K, 2 * K * ng, kTriBM, 1);
-  make_map(&mB, e->B, 2 * K, ng, 1, 2 * K, 2 * K * ng, kTriBM, 1);
-  make_map(&mX1, e->X1, 2 * K, ng, 1, 2 * K, 2 * K * ng, kTriBM, 1);
-  make_map(&mX2, e->X2, 2 * K, ng, 1, 2 * K, 2 * K * ng, kTriBM, 1);
+  make_map(&mA, e->A + r0, 2 * Kc, ng, 1, 2 * K, 2 * K * ng, kTriBM, 1);
+  make_map(&mB, e->B + r0, 2 * Kc, ng, 1, 2 * K, 2 * K * ng, kTriBM, 1);
+  make_map(&mX1, e->X1 + r0, 2 * Kc, ng, 1, 2 * K, 2 * K * ng, kTriBM, 1);
+  make_map(&mX2, e->X2 + r0, 2 * Kc, ng, 1, 2 * K, 2 * K * ng, kTriBM, 1);
   const int tiles = static_cast<int>((ng + kTriBM - 1) / kTriBM);
+  const double beta0 = first ? 0.0 : 1.0;
   auto tri_base = [&](CtnParams& P, double2* out, double beta) {
     std::memset(&P, 0, sizeof(P));
     P.n = static_cast<int>(ng);
@@ -273,36 +297,37 @@ static void build_params(hsdla_b200_engine* e) {
     P.beta = beta;
   };
   // phase s: S = A^H A + (U B)^H (U B)   (pipeline.cpp:298-300)
-  tri_base(e->p_s, e->Sp, 0.0);
-  set_tri_seg(e->p_s, 0, mA, mA, K);
-  set_tri_seg(e->p_s, 1, mX1, mX1, K);
-  e->p_s.nseg = 2;
+  tri_base(cp.s, e->Sp, beta0);
+  set_seg(cp.s, 0, mA, mA, Kc);
+  set_seg(cp.s, 1, mX1, mX1, Kc);
+  cp.s.nseg = 2;
   // fused H = Z^H B + B^H Z + A^H X   (pipeline.cpp:311 + :324)
-  tri_base(e->p_h, e->Hp, 0.0);
-  set_tri_seg(e->p_h, 0, mX2, mB, K);
-  set_tri_seg(e->p_h, 1, mB, mX2, K);
-  set_tri_seg(e->p_h, 2, mA, mX1, K);
-  e->p_h.nseg = 3;
-  // reference-order her2k (beta 0) and herkx (beta 1)
-  tri_base(e->p_h2k, e->Hp, 0.0);
-  set_tri_seg(e->p_h2k, 0, mX2, mB, K);
-  set_tri_seg(e->p_h2k, 1, mB, mX2, K);
-  e->p_h2k.nseg = 2;
-  tri_base(e->p_hkx, e->Hp, 1.0);
-  set_tri_seg(e->p_hkx, 0, mA, mX1, K);
-  e->p_hkx.nseg = 1;
+  tri_base(cp.h, e->Hp, beta0);
+  set_seg(cp.h, 0, mX2, mB, Kc);
+  set_seg(cp.h, 1, mB, mX2, Kc);
+  set_seg(cp.h, 2, mA, mX1, Kc);
+  cp.h.nseg = 3;
+  // reference-order her2k (beta 0 on the first chunk) and herkx (always accumulates)
+  tri_base(cp.h2k, e->Hp, beta0);
+  set_seg(cp.h2k, 0, mX2, mB, Kc);
+  set_seg(cp.h2k, 1, mB, mX2, Kc);
+  cp.h2k.nseg = 2;
+  tri_base(cp.hkx, e->Hp, 1.0);
+  set_seg(cp.hkx, 0, mA, mX1, Kc);
+  cp.hkx.nseg = 1;
   // persistent stream-K grid: one CTA per SM, never more CTAs than k-iterations
   const uint64_t tri_tiles = static_cast<uint64_t>(tiles) * (tiles + 1) / 2;
-  e->grid_tri = dim3(static_cast<unsigned>(std::min<uint64_t>(e->sms, tri_tiles * chunks(K))));
+  cp.grid_tri = dim3(static_cast<unsigned>(std::min<uint64_t>(e->sms, tri_tiles * chunks_of(Kc))));
 
-  // batched per-atom products: operators {2nl, nl, na} (row i in dim 1, atom in dim 2),
-  // coefficient views {2nl, na, ng} (atom in dim 1, G row in dim 2).
+  // batched per-atom products: operators {2nl, nl, nac} (row i in dim 1, atom in dim 2),
+  // coefficient views {2nl, nac, ng} (atom in dim 1, G row in dim 2).
+  const uint64_t blk = nl * nl;
   CUtensorMap mTab, mPbb, mPaa, vA, vB;
-  make_map(&mTab, e->Tab, 2 * nl, nl, na, 2 * nl, 2 * nl * nl, kBatBM, 1);
-  make_map(&mPbb, e->Pbb, 2 * nl, nl, na, 2 * nl, 2 * nl * nl, kBatBM, 1);
-  make_map(&mPaa, e->Paa, 2 * nl, nl, na, 2 * nl, 2 * nl * nl, kBatBM, 1);
-  make_map(&vA, e->A, 2 * nl, na, ng, 2 * nl, 2 * K, 1, kBatBN);
-  make_map(&vB, e->B, 2 * nl, na, ng, 2 * nl, 2 * K, 1, kBatBN);
+  make_map(&mTab, e->Tab + a0 * blk, 2 * nl, nl, nac, 2 * nl, 2 * blk, kBatBM, 1);
+  make_map(&mPbb, e->Pbb + a0 * blk, 2 * nl, nl, nac, 2 * nl, 2 * blk, kBatBM, 1);
+  make_map(&mPaa, e->Paa + a0 * blk, 2 * nl, nl, nac, 2 * nl, 2 * blk, kBatBM, 1);
+  make_map(&vA, e->A + r0, 2 * nl, nac, ng, 2 * nl, 2 * K, 1, kBatBN);
+  make_map(&vB, e->B + r0, 2 * nl, nac, ng, 2 * nl, 2 * K, 1, kBatBN);
   auto bat_base = [&](CtnParams& P, double2* out) {
     std::memset(&P, 0, sizeof(P));
     P.n = static_cast<int>(ng);
@@ -312,34 +337,33 @@ static void build_params(hsdla_b200_engine* e) {
     P.alpha_re = 1.0;
   };
   // Z_a = T_AB^H A_a + (1/2 T_BB) B_a   (compute_z, pipeline.cpp:176-185)
-  bat_base(e->p_z, e->X2);
-  e->p_z.L[0] = mTab;
-  e->p_z.R[0] = vA;
-  e->p_z.L[1] = mPbb;
-  e->p_z.R[1] = vB;
-  e->p_z.kchunks[0] = e->p_z.kchunks[1] = chunks(nl);
-  e->p_z.r_row_z[0] = e->p_z.r_row_z[1] = 1;
-  e->p_z.nseg = 2;
+  bat_base(cp.z, e->X2 + r0);
+  cp.z.L[0] = mTab;
+  cp.z.R[0] = vA;
+  cp.z.L[1] = mPbb;
+  cp.z.R[1] = vB;
+  cp.z.kchunks[0] = cp.z.kchunks[1] = chunks_of(nl);
+  cp.z.r_row_z[0] = cp.z.r_row_z[1] = 1;
+  cp.z.nseg = 2;
   // X_a = T_AA A_a   (hemm_loop, pipeline.cpp:314-321)
-  bat_base(e->p_x, e->X1);
-  e->p_x.L[0] = mPaa;
-  e->p_x.R[0] = vA;
-  e->p_x.kchunks[0] = chunks(nl);
-  e->p_x.r_row_z[0] = 1;
-  e->p_x.nseg = 1;
-  e->grid_bat = dim3(static_cast<unsigned>((ng + kBatBN - 1) / kBatBN), static_cast<unsigned>((nl + kBatBM - 1) / kBatBM),
-                     static_cast<unsigned>(na));
+  bat_base(cp.x, e->X1 + r0);
+  cp.x.L[0] = mPaa;
+  cp.x.R[0] = vA;
+  cp.x.kchunks[0] = chunks_of(nl);
+  cp.x.r_row_z[0] = 1;
+  cp.x.nseg = 1;
+  cp.grid_bat = dim3(static_cast<unsigned>((ng + kBatBN - 1) / kBatBN),
+                     static_cast<unsigned>((nl + kBatBM - 1) / kBatBM), static_cast<unsigned>(nac));
 }
 
-static void init_kernel_attrs() {
-  static std::once_flag once;
-  static cudaError_t err = cudaSuccess;
-  std::call_once(once, [] {
-    err = cudaFuncSetAttribute(tri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TriCfg::kSmemBytes);
-    if (err == cudaSuccess)
-      err = cudaFuncSetAttribute(bat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BatCfg::kSmemBytes);
-  });
-  HS_CUDA(err);
+// Streamed chunking: ~8 chunks of whole atoms, each >= 2 atoms (small problems: 1 chunk).
+static std::vector<uint64_t> stream_bounds(uint64_t na, uint64_t nl, uint64_t ng) {
+  uint64_t n = std::min<uint64_t>(8, na / 2);
+  if (na * nl * ng < (uint64_t(1) << 22)) n = 1;  // < 64 MB of A+B: nothing to overlap
+  n = std::max<uint64_t>(n, 1);
+  std::vector<uint64_t> b(n + 1);
+  for (uint64_t c = 0; c <= n; ++c) b[c] = na * c / n;
+  return b;
 }
 
 static hsdla_b200_engine* engine_create(int device, uint64_t na, uint64_t nl, uint64_t ng) {
@@ -357,9 +381,12 @@ static hsdla_b200_engine* engine_create(int device, uint64_t na, uint64_t nl, ui
     HS_CUDA(cudaFuncSetAttribute(tri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TriCfg::kSmemBytes));
     HS_CUDA(cudaFuncSetAttribute(bat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BatCfg::kSmemBytes));
     HS_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    HS_CUDA(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
     HS_CUDA(cudaStreamCreateWithFlags(&e->comm_stream, cudaStreamNonBlocking));
-    for (auto& ev : e->ev) HS_CUDA(cudaEventCreate(&ev));
-    HS_CUDA(cudaEventCreateWithFlags(&e->ev_s_done, cudaEventDisableTiming));
+    for (cudaEvent_t* ev : {&e->ev_begin, &e->ev_end, &e->ev_reduce_end, &e->ev_up0, &e->ev_up1})
+      HS_CUDA(cudaEventCreate(ev));
+    for (cudaEvent_t* ev : {&e->ev_s_done, &e->ev_s_red, &e->ev_s_d2h, &e->ev_h_d2h})
+      HS_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     for (auto& t : e->ring)
       for (cudaEvent_t* ev : {&t.s0, &t.s1, &t.h0, &t.h1}) HS_CUDA(cudaEventCreate(ev));
     const uint64_t KG = e->K * ng;
@@ -380,7 +407,13 @@ static hsdla_b200_engine* engine_create(int device, uint64_t na, uint64_t nl, ui
     dalloc(e.get(), &e->sk_ws, static_cast<uint64_t>(e->sms) * kTriBM * kTriBM * 2);
     dalloc(e.get(), &e->sk_flags, static_cast<uint64_t>(e->sms));
     HS_CUDA(cudaMemset(e->sk_flags, 0, e->sms * sizeof(uint32_t)));
-    build_params(e.get());
+    e->whole.resize(1);
+    make_chunk(e.get(), 0, na, true, e->whole[0]);
+    const auto b = stream_bounds(na, nl, ng);
+    e->streamed.resize(b.size() - 1);
+    for (size_t c = 0; c + 1 < b.size(); ++c) make_chunk(e.get(), b[c], b[c + 1], c == 0, e->streamed[c]);
+    e->ev_chunk_up.resize(e->streamed.size());
+    for (auto& ev : e->ev_chunk_up) HS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   } catch (...) {
     engine_free(e.get());
     throw;
@@ -388,44 +421,78 @@ static hsdla_b200_engine* engine_create(int device, uint64_t na, uint64_t nl, ui
   return e.release();
 }
 
-static void engine_upload(hsdla_b200_engine* e, const hsdla_b200_problem* p, uint64_t a0) {
+static void check_problem(const hsdla_b200_engine* e, const hsdla_b200_problem* p, uint64_t a0) {
   if (!p || !p->A || !p->B || !p->T_AA || !p->T_AB || !p->T_BB || !p->U)
     throw Fail{HSDLA_B200_DIMENSION_ERROR, "null problem pointer"};
   if (p->n_l != e->nl || p->n_g != e->ng || a0 + e->na > p->n_atoms)
     throw Fail{HSDLA_B200_DIMENSION_ERROR, "problem shape does not match the engine shard"};
+}
+
+// H2D of local atoms [b0, b1) (engine-local indices) of shard a0 of p, on stream s.
+static void upload_atoms(hsdla_b200_engine* e, const hsdla_b200_problem* p, uint64_t a0, uint64_t b0, uint64_t b1,
+                         cudaStream_t s) {
+  const uint64_t Kg = p->n_atoms * p->n_l;  // caller's leading dimension
+  const uint64_t nl = e->nl, r0 = b0 * nl, rows = (b1 - b0) * nl, g0 = (a0 + b0) * nl;
+  const size_t width = rows * sizeof(double2);
+  HS_CUDA(cudaMemcpy2DAsync(e->A + r0, e->K * sizeof(double2), reinterpret_cast<const double2*>(p->A) + g0,
+                            Kg * sizeof(double2), width, e->ng, cudaMemcpyHostToDevice, s));
+  HS_CUDA(cudaMemcpy2DAsync(e->B + r0, e->K * sizeof(double2), reinterpret_cast<const double2*>(p->B) + g0,
+                            Kg * sizeof(double2), width, e->ng, cudaMemcpyHostToDevice, s));
+  const uint64_t blk = nl * nl;
+  const size_t tbytes = (b1 - b0) * blk * sizeof(double2);
+  const uint64_t t0 = (a0 + b0) * blk;
+  HS_CUDA(cudaMemcpyAsync(e->Taa + b0 * blk, reinterpret_cast<const double2*>(p->T_AA) + t0, tbytes,
+                          cudaMemcpyHostToDevice, s));
+  HS_CUDA(cudaMemcpyAsync(e->Tab + b0 * blk, reinterpret_cast<const double2*>(p->T_AB) + t0, tbytes,
+                          cudaMemcpyHostToDevice, s));
+  HS_CUDA(cudaMemcpyAsync(e->Tbb + b0 * blk, reinterpret_cast<const double2*>(p->T_BB) + t0, tbytes,
+                          cudaMemcpyHostToDevice, s));
+  HS_CUDA(cudaMemcpyAsync(e->U + r0, p->U + g0, rows * sizeof(double), cudaMemcpyHostToDevice, s));
+}
+
+static void engine_upload(hsdla_b200_engine* e, const hsdla_b200_problem* p, uint64_t a0) {
+  check_problem(e, p, a0);
   HS_CUDA(cudaSetDevice(e->device));
-  const uint64_t Kg = p->n_atoms * p->n_l;  // global ld
-  const uint64_t r0 = a0 * e->nl;
-  const size_t width = e->K * sizeof(double2);
-  const size_t spitch = Kg * sizeof(double2);
-  HS_CUDA(cudaMemcpy2DAsync(e->A, width, reinterpret_cast<const double2*>(p->A) + r0, spitch, width, e->ng,
-                            cudaMemcpyHostToDevice, e->stream));
-  HS_CUDA(cudaMemcpy2DAsync(e->B, width, reinterpret_cast<const double2*>(p->B) + r0, spitch, width, e->ng,
-                            cudaMemcpyHostToDevice, e->stream));
-  const uint64_t blk = e->nl * e->nl;
-  const size_t tbytes = e->na * blk * sizeof(double2);
-  HS_CUDA(cudaMemcpyAsync(e->Taa, reinterpret_cast<const double2*>(p->T_AA) + a0 * blk, tbytes,
-                          cudaMemcpyHostToDevice, e->stream));
-  HS_CUDA(cudaMemcpyAsync(e->Tab, reinterpret_cast<const double2*>(p->T_AB) + a0 * blk, tbytes,
-                          cudaMemcpyHostToDevice, e->stream));
-  HS_CUDA(cudaMemcpyAsync(e->Tbb, reinterpret_cast<const double2*>(p->T_BB) + a0 * blk, tbytes,
-                          cudaMemcpyHostToDevice, e->stream));
-  HS_CUDA(cudaMemcpyAsync(e->U, p->U + r0, e->K * sizeof(double), cudaMemcpyHostToDevice, e->stream));
+  upload_atoms(e, p, a0, 0, e->na, e->stream);
 }
 
-static void launch_tri(hsdla_b200_engine* e, CtnParams& P) {
+// ---- launches ---------------------------------------------------------------
+static cudaEvent_t next_event(hsdla_b200_engine* e) {
+  if (e->ev_used == e->ev_pool.size()) {
+    cudaEvent_t ev;
+    HS_CUDA(cudaEventCreate(&ev));
+    e->ev_pool.push_back(ev);
+  }
+  return e->ev_pool[e->ev_used++];
+}
+
+// CUDA-event bracket of one phase op on the compute stream.
+template <class F>
+static void timed_op(hsdla_b200_engine* e, int phase, F&& body) {
+  cudaEvent_t b = next_event(e), end = next_event(e);
+  HS_CUDA(cudaEventRecord(b, e->stream));
+  body();
+  HS_CUDA(cudaEventRecord(end, e->stream));
+  e->ops.push_back({phase, b, end});
+}
+
+static void launch_tri(hsdla_b200_engine* e, CtnParams& P, const dim3& grid) {
   P.epoch = ++e->epoch;  // fresh stream-K flag generation per launch
-  tri_kernel<<<e->grid_tri, TriCfg::kThreads, TriCfg::kSmemBytes, e->stream>>>(P);
+  tri_kernel<<<grid, TriCfg::kThreads, TriCfg::kSmemBytes, e->stream>>>(P);
   HS_CUDA(cudaGetLastError());
   ++e->launches;
 }
-static void launch_bat(hsdla_b200_engine* e, const CtnParams& P) {
-  bat_kernel<<<e->grid_bat, BatCfg::kThreads, BatCfg::kSmemBytes, e->stream>>>(P);
+static void launch_bat(hsdla_b200_engine* e, const CtnParams& P, const dim3& grid) {
+  bat_kernel<<<grid, BatCfg::kThreads, BatCfg::kSmemBytes, e->stream>>>(P);
   HS_CUDA(cudaGetLastError());
   ++e->launches;
 }
 
-static float ev_ms(cudaEvent_t a, cudaEvent_t b);
+static float ev_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  HS_CUDA(cudaEventElapsedTime(&ms, a, b));
+  return ms;
+}
 
 static void harvest(hsdla_b200_engine* e, hsdla_b200_engine::KTimer& t) {
   if (!t.pending) return;
@@ -437,69 +504,89 @@ static void harvest(hsdla_b200_engine* e, hsdla_b200_engine::KTimer& t) {
   t.pending = false;
 }
 
-static void engine_build(hsdla_b200_engine* e, int algo) {
+// All phases of one chunk on the compute stream, in the reference phase order.
+static void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool last,
+                          hsdla_b200_engine::KTimer* kt) {
+  cudaStream_t s = e->stream;
+  const uint64_t nac = cp.a1 - cp.a0, nl = e->nl, r0 = cp.a0 * nl, Kc = nac * nl, ng = e->ng;
+  timed_op(e, HSDLA_B200_PHASE_S, [&] {
+    // operator expansion (lower triangles of T_AA, T_BB only) for this chunk's atoms
+    const uint64_t total = nac * nl * nl, off = cp.a0 * nl * nl;
+    expand_hermitian_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
+        e->Taa + off, e->Tbb + off, e->Paa + off, e->Pbb + off, static_cast<int>(nl), total);
+    HS_CUDA(cudaGetLastError());
+    const dim3 g(static_cast<unsigned>((Kc + 255) / 256), static_cast<unsigned>(std::min<uint64_t>(ng, 2048)));
+    diag_scale_kernel<<<g, 256, 0, s>>>(e->B + r0, e->U + r0, e->X1 + r0, Kc, e->K, ng);
+    HS_CUDA(cudaGetLastError());
+    e->launches += 2;
+    if (kt) HS_CUDA(cudaEventRecord(kt->s0, s));
+    launch_tri(e, cp.s, cp.grid_tri);
+    if (kt) HS_CUDA(cudaEventRecord(kt->s1, s));
+  });
+  if (last) HS_CUDA(cudaEventRecord(e->ev_s_done, s));
+  timed_op(e, HSDLA_B200_PHASE_Z_LOOP, [&] { launch_bat(e, cp.z, cp.grid_bat); });
+  if (algo == HSDLA_B200_ALGO_REFINED) {
+    timed_op(e, HSDLA_B200_PHASE_HER2K, [&] {
+      if (kt) HS_CUDA(cudaEventRecord(kt->h0, s));
+      launch_tri(e, cp.h2k, cp.grid_tri);
+      if (kt) HS_CUDA(cudaEventRecord(kt->h1, s));
+    });
+    timed_op(e, HSDLA_B200_PHASE_HEMM_LOOP, [&] { launch_bat(e, cp.x, cp.grid_bat); });
+    timed_op(e, HSDLA_B200_PHASE_HERKX, [&] { launch_tri(e, cp.hkx, cp.grid_tri); });
+  } else {
+    timed_op(e, HSDLA_B200_PHASE_HEMM_LOOP, [&] { launch_bat(e, cp.x, cp.grid_bat); });
+    timed_op(e, HSDLA_B200_PHASE_HER2K, [&] {  // her2k + herkx fused
+      if (kt) HS_CUDA(cudaEventRecord(kt->h0, s));
+      launch_tri(e, cp.h, cp.grid_tri);
+      if (kt) HS_CUDA(cudaEventRecord(kt->h1, s));
+    });
+  }
+}
+
+static void begin_build(hsdla_b200_engine* e, int algo) {
   if (algo != HSDLA_B200_ALGO_REFINED && algo != HSDLA_B200_ALGO_REFINED_FUSED)
     throw Fail{HSDLA_B200_CONFIG_ERROR, "unknown algo " + std::to_string(algo)};
   HS_CUDA(cudaSetDevice(e->device));
-  cudaStream_t s = e->stream;
   e->launches = 0;
   e->last_algo = algo;
   e->reduced = false;
-  const uint64_t K = e->K, ng = e->ng;
+  e->uploaded_streamed = false;
+  e->ev_used = 0;
+  e->ops.clear();
+  e->built = true;
+}
+
+// Device-resident build: one chunk over all atoms (the bench's `value`).
+static void engine_build(hsdla_b200_engine* e, int algo) {
+  begin_build(e, algo);
   auto& kt = e->ring[e->builds++ % hsdla_b200_engine::kRing];
   harvest(e, kt);
-  kt.flops_h = (algo == HSDLA_B200_ALGO_REFINED ? 8 : 12) * K * ng * ng;
-  HS_CUDA(cudaEventRecord(e->ev[EV_START], s));
-  // operator expansion (lower triangles of T_AA, T_BB only)
-  {
-    const uint64_t total = e->na * e->nl * e->nl;
-    expand_hermitian_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(e->Taa, e->Tbb, e->Paa, e->Pbb,
-                                                                                        static_cast<int>(e->nl), total);
-    HS_CUDA(cudaGetLastError());
-    ++e->launches;
-  }
-  // ---- phase s ----
-  HS_CUDA(cudaEventRecord(e->ev[EV_S_BEGIN], s));
-  diag_scale_kernel<<<dim3(static_cast<unsigned>((K + 255) / 256), static_cast<unsigned>(std::min<uint64_t>(ng, 2048))), 256, 0,
-                      s>>>(e->B, e->U, e->X1, K, ng);
-  HS_CUDA(cudaGetLastError());
-  ++e->launches;
-  HS_CUDA(cudaEventRecord(kt.s0, s));
-  launch_tri(e, e->p_s);
-  HS_CUDA(cudaEventRecord(kt.s1, s));
-  HS_CUDA(cudaEventRecord(e->ev[EV_S_END], s));
-  if (e->comm) {  // overlap S's reduce with the H phases
-    HS_CUDA(cudaEventRecord(e->ev_s_done, s));
-  }
-  // ---- phase z_loop ----
-  launch_bat(e, e->p_z);
-  HS_CUDA(cudaEventRecord(e->ev[EV_Z_END], s));
-  if (algo == HSDLA_B200_ALGO_REFINED) {
-    // ---- her2k ----
-    HS_CUDA(cudaEventRecord(e->ev[EV_HER2K_BEGIN], s));
-    HS_CUDA(cudaEventRecord(kt.h0, s));
-    launch_tri(e, e->p_h2k);
-    HS_CUDA(cudaEventRecord(kt.h1, s));
-    HS_CUDA(cudaEventRecord(e->ev[EV_HER2K_END], s));
-    // ---- hemm_loop ----
-    launch_bat(e, e->p_x);
-    HS_CUDA(cudaEventRecord(e->ev[EV_HEMM_END], s));
-    // ---- herkx ----
-    HS_CUDA(cudaEventRecord(e->ev[EV_HERKX_BEGIN], s));
-    launch_tri(e, e->p_hkx);
-    HS_CUDA(cudaEventRecord(e->ev[EV_END], s));
-  } else {
-    // ---- hemm_loop (X = T_AA A), then one fused her2k+herkx contraction ----
-    launch_bat(e, e->p_x);
-    HS_CUDA(cudaEventRecord(e->ev[EV_HEMM_END], s));
-    HS_CUDA(cudaEventRecord(e->ev[EV_HER2K_BEGIN], s));
-    HS_CUDA(cudaEventRecord(kt.h0, s));
-    launch_tri(e, e->p_h);
-    HS_CUDA(cudaEventRecord(kt.h1, s));
-    HS_CUDA(cudaEventRecord(e->ev[EV_HER2K_END], s));
-    HS_CUDA(cudaEventRecord(e->ev[EV_END], s));
-  }
+  kt.flops_h = (algo == HSDLA_B200_ALGO_REFINED ? 8 : 12) * e->K * e->ng * e->ng;
+  HS_CUDA(cudaEventRecord(e->ev_begin, e->stream));
+  enqueue_chunk(e, e->whole[0], algo, true, &kt);
+  HS_CUDA(cudaEventRecord(e->ev_end, e->stream));
   kt.pending = true;
+}
+
+// Streamed build from host memory: chunk c+1's H2D overlaps chunk c's phases.
+static void engine_build_streamed(hsdla_b200_engine* e, const hsdla_b200_problem* p, uint64_t a0, int algo) {
+  check_problem(e, p, a0);
+  begin_build(e, algo);
+  // the copy stream may only overwrite A/B/T/U once the previous build has consumed them
+  HS_CUDA(cudaStreamWaitEvent(e->copy_stream, e->ev_end, 0));
+  HS_CUDA(cudaEventRecord(e->ev_up0, e->copy_stream));
+  for (size_t c = 0; c < e->streamed.size(); ++c) {
+    upload_atoms(e, p, a0, e->streamed[c].a0, e->streamed[c].a1, e->copy_stream);
+    HS_CUDA(cudaEventRecord(e->ev_chunk_up[c], e->copy_stream));
+  }
+  HS_CUDA(cudaEventRecord(e->ev_up1, e->copy_stream));
+  for (size_t c = 0; c < e->streamed.size(); ++c) {
+    HS_CUDA(cudaStreamWaitEvent(e->stream, e->ev_chunk_up[c], 0));
+    if (c == 0) HS_CUDA(cudaEventRecord(e->ev_begin, e->stream));
+    enqueue_chunk(e, e->streamed[c], algo, c + 1 == e->streamed.size(), nullptr);
+  }
+  HS_CUDA(cudaEventRecord(e->ev_end, e->stream));
+  e->uploaded_streamed = true;
 }
 
 // NCCL sum-reduce of the packed partials to `root`, split so S's reduce overlaps the
@@ -512,13 +599,14 @@ static void reduce_s(hsdla_b200_engine* e, int root) {
 }
 static void reduce_h(hsdla_b200_engine* e, int root) {
   HS_CUDA(cudaSetDevice(e->device));
-  HS_CUDA(cudaStreamWaitEvent(e->comm_stream, e->ev[EV_END], 0));
+  HS_CUDA(cudaEventRecord(e->ev_s_red, e->comm_stream));
+  HS_CUDA(cudaStreamWaitEvent(e->comm_stream, e->ev_end, 0));
   HS_NCCL(ncclReduce(e->Hp, e->Hp, 2 * e->npk, ncclFloat64, ncclSum, root, e->comm, e->comm_stream));
 }
 static void reduce_finish(hsdla_b200_engine* e) {
   HS_CUDA(cudaSetDevice(e->device));
-  HS_CUDA(cudaEventRecord(e->ev[EV_REDUCE_END], e->comm_stream));
-  HS_CUDA(cudaStreamWaitEvent(e->stream, e->ev[EV_REDUCE_END], 0));
+  HS_CUDA(cudaEventRecord(e->ev_reduce_end, e->comm_stream));
+  HS_CUDA(cudaStreamWaitEvent(e->stream, e->ev_reduce_end, 0));
   e->reduced = true;
 }
 static void engine_reduce(hsdla_b200_engine* e, int root) {
@@ -528,15 +616,10 @@ static void engine_reduce(hsdla_b200_engine* e, int root) {
   reduce_finish(e);
 }
 
-static float ev_ms(cudaEvent_t a, cudaEvent_t b) {
-  float ms = 0.f;
-  HS_CUDA(cudaEventElapsedTime(&ms, a, b));
-  return ms;
-}
-
 static void engine_sync(hsdla_b200_engine* e, hsdla_b200_stats* st) {
   HS_CUDA(cudaSetDevice(e->device));
   HS_CUDA(cudaStreamSynchronize(e->stream));
+  HS_CUDA(cudaStreamSynchronize(e->copy_stream));
   HS_CUDA(cudaStreamSynchronize(e->comm_stream));
   for (auto& t : e->ring) harvest(e, t);
   if (!st) return;
@@ -544,33 +627,20 @@ static void engine_sync(hsdla_b200_engine* e, hsdla_b200_stats* st) {
   st->peak_device_bytes = e->device_bytes;
   st->peak_temp_bytes = e->temp_bytes;
   st->n_gpus = e->nranks;
-  if (e->builds == 0) return;  // nothing timed yet
-  std::memset(st->phase_seconds, 0, sizeof(st->phase_seconds));
-  st->phase_seconds[HSDLA_B200_PHASE_S] = ev_ms(e->ev[EV_START], e->ev[EV_S_END]) * 1e-3;
-  st->phase_seconds[HSDLA_B200_PHASE_Z_LOOP] = ev_ms(e->ev[EV_S_END], e->ev[EV_Z_END]) * 1e-3;
-  if (e->last_algo == HSDLA_B200_ALGO_REFINED) {
-    st->phase_seconds[HSDLA_B200_PHASE_HER2K] = ev_ms(e->ev[EV_Z_END], e->ev[EV_HER2K_END]) * 1e-3;
-    st->phase_seconds[HSDLA_B200_PHASE_HEMM_LOOP] = ev_ms(e->ev[EV_HER2K_END], e->ev[EV_HEMM_END]) * 1e-3;
-    st->phase_seconds[HSDLA_B200_PHASE_HERKX] = ev_ms(e->ev[EV_HEMM_END], e->ev[EV_END]) * 1e-3;
-  } else {
-    st->phase_seconds[HSDLA_B200_PHASE_HEMM_LOOP] = ev_ms(e->ev[EV_Z_END], e->ev[EV_HEMM_END]) * 1e-3;
-    st->phase_seconds[HSDLA_B200_PHASE_HER2K] = ev_ms(e->ev[EV_HEMM_END], e->ev[EV_END]) * 1e-3;
-    st->phase_seconds[HSDLA_B200_PHASE_HERKX] = 0.0;  // fused into her2k
-  }
-  const cudaEvent_t last = e->reduced ? e->ev[EV_REDUCE_END] : e->ev[EV_END];
-  st->device_seconds = ev_ms(e->ev[EV_START], last) * 1e-3;
-  st->reduce_seconds = e->reduced ? ev_ms(e->ev[EV_END], e->ev[EV_REDUCE_END]) * 1e-3 : 0.0;
+  if (!e->built) return;  // nothing timed yet
+  for (const OpTime& op : e->ops) st->phase_seconds[op.phase] += ev_ms(op.b, op.e) * 1e-3;
+  const cudaEvent_t last = e->reduced ? e->ev_reduce_end : e->ev_end;
+  st->device_seconds = ev_ms(e->ev_begin, last) * 1e-3;
+  st->reduce_seconds = e->reduced ? ev_ms(e->ev_end, e->ev_reduce_end) * 1e-3 : 0.0;
+  if (e->uploaded_streamed) st->h2d_seconds = ev_ms(e->ev_up0, e->ev_up1) * 1e-3;
   st->kernel_launches = e->launches;
-  st->peak_device_bytes = e->device_bytes;
-  st->peak_temp_bytes = e->temp_bytes;
-  st->n_gpus = e->nranks;
 }
 
 // Unpack column-major packed lower into the lower triangle of an n x n matrix.
 static void unpack_lower(const double2* pk, double2* full, uint64_t n) {
   const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
   const uint64_t total = n * (n + 1) / 2;
-  const unsigned nt = total < (1u << 20) ? 1u : hw;
+  const unsigned nt = total < (1u << 18) ? 1u : hw;
   auto work = [&](uint64_t j0, uint64_t j1) {
     for (uint64_t j = j0; j < j1; ++j)
       std::memcpy(full + j * n + j, pk + j * (2 * n - j + 1) / 2, (n - j) * sizeof(double2));
@@ -579,8 +649,7 @@ static void unpack_lower(const double2* pk, double2* full, uint64_t n) {
     work(0, n);
     return;
   }
-  // split columns into nt ranges of equal element count
-  std::vector<std::thread> th;
+  std::vector<std::thread> th;  // nt column ranges of equal element count
   uint64_t j = 0;
   for (unsigned t = 0; t < nt && j < n; ++t) {
     const uint64_t target = total * (t + 1) / nt;
@@ -593,15 +662,37 @@ static void unpack_lower(const double2* pk, double2* full, uint64_t n) {
   for (auto& t : th) t.join();
 }
 
+static void ensure_stage(hsdla_b200_engine* e) {
+  if (!e->host_stage)
+    HS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&e->host_stage), 2 * e->npk * sizeof(double2)));
+}
+
+// Enqueue the packed-triangle D2H of S (after phase s / its reduce) and H (after
+// the build / its reduce) on the copy stream.
+static void enqueue_download(hsdla_b200_engine* e) {
+  ensure_stage(e);
+  const size_t bytes = e->npk * sizeof(double2);
+  HS_CUDA(cudaStreamWaitEvent(e->copy_stream, e->reduced ? e->ev_s_red : e->ev_s_done, 0));
+  HS_CUDA(cudaMemcpyAsync(e->host_stage + e->npk, e->Sp, bytes, cudaMemcpyDeviceToHost, e->copy_stream));
+  HS_CUDA(cudaEventRecord(e->ev_s_d2h, e->copy_stream));
+  HS_CUDA(cudaStreamWaitEvent(e->copy_stream, e->reduced ? e->ev_reduce_end : e->ev_end, 0));
+  HS_CUDA(cudaMemcpyAsync(e->host_stage, e->Hp, bytes, cudaMemcpyDeviceToHost, e->copy_stream));
+  HS_CUDA(cudaEventRecord(e->ev_h_d2h, e->copy_stream));
+}
+
+// Unpack S as soon as its bytes land (H may still be computing), then H.
+static void finish_download(hsdla_b200_engine* e, double* H, double* S) {
+  HS_CUDA(cudaEventSynchronize(e->ev_s_d2h));
+  if (S) unpack_lower(e->host_stage + e->npk, reinterpret_cast<double2*>(S), e->ng);
+  HS_CUDA(cudaEventSynchronize(e->ev_h_d2h));
+  if (H) unpack_lower(e->host_stage, reinterpret_cast<double2*>(H), e->ng);
+}
+
 static void engine_download(hsdla_b200_engine* e, double* H, double* S) {
   HS_CUDA(cudaSetDevice(e->device));
-  if (!e->host_stage) HS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&e->host_stage), 2 * e->npk * sizeof(double2)));
-  const size_t bytes = e->npk * sizeof(double2);
-  if (H) HS_CUDA(cudaMemcpyAsync(e->host_stage, e->Hp, bytes, cudaMemcpyDeviceToHost, e->stream));
-  if (S) HS_CUDA(cudaMemcpyAsync(e->host_stage + e->npk, e->Sp, bytes, cudaMemcpyDeviceToHost, e->stream));
-  HS_CUDA(cudaStreamSynchronize(e->stream));
-  if (H) unpack_lower(e->host_stage, reinterpret_cast<double2*>(H), e->ng);
-  if (S) unpack_lower(e->host_stage + e->npk, reinterpret_cast<double2*>(S), e->ng);
+  if (!e->built) throw Fail{HSDLA_B200_CONFIG_ERROR, "download before build"};
+  enqueue_download(e);
+  finish_download(e, H, S);
 }
 
 // ---------------------------------------------------------------------------
@@ -632,13 +723,12 @@ static EngineSet* get_engines(const std::vector<int>& devs, uint64_t na, uint64_
   auto key = std::make_tuple(devs, na, nl, ng);
   auto it = g_cache.find(key);
   if (it != g_cache.end()) return it->second.get();
-  // one shape at a time keeps HBM free for the caller
-  g_cache.clear();
+  g_cache.clear();  // one shape at a time keeps HBM free for the caller
   auto set = std::make_unique<EngineSet>();
   const int P = static_cast<int>(devs.size());
+  if (static_cast<uint64_t>(P) > na) throw Fail{HSDLA_B200_CONFIG_ERROR, "more GPUs than atoms"};
   const auto b = shard_atoms(na, P);
   for (int r = 0; r < P; ++r) {
-    if (b[r + 1] == b[r]) throw Fail{HSDLA_B200_CONFIG_ERROR, "more GPUs than atoms"};
     set->engines.push_back(engine_create(devs[r], b[r + 1] - b[r], nl, ng));
     set->engines.back()->rank = r;
     set->engines.back()->nranks = P;
@@ -695,8 +785,7 @@ int hsdla_b200_device_count(int* count) {
   return guarded([&] {
     if (!count) throw Fail{HSDLA_B200_DIMENSION_ERROR, "null count"};
     int n = 0;
-    cudaError_t e = cudaGetDeviceCount(&n);
-    if (e != cudaSuccess) {
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
       (void)cudaGetLastError();
       n = 0;
     }
@@ -758,6 +847,12 @@ int hsdla_b200_engine_build(hsdla_b200_engine* e, int algo) {
     engine_build(e, algo);
   });
 }
+int hsdla_b200_engine_build_streamed(hsdla_b200_engine* e, const hsdla_b200_problem* p, uint64_t a0, int algo) {
+  return guarded([&] {
+    if (!e) throw Fail{HSDLA_B200_CONFIG_ERROR, "null engine"};
+    engine_build_streamed(e, p, a0, algo);
+  });
+}
 int hsdla_b200_engine_reduce(hsdla_b200_engine* e, int root) {
   return guarded([&] {
     if (!e) throw Fail{HSDLA_B200_CONFIG_ERROR, "null engine"};
@@ -792,6 +887,7 @@ int hsdla_b200_engine_stream(hsdla_b200_engine* e, void** stream) {
 int hsdla_b200_nccl_unique_id(void* id128) {
   return guarded([&] {
     static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    if (!id128) throw Fail{HSDLA_B200_DIMENSION_ERROR, "null id"};
     ncclUniqueId id;
     HS_NCCL(ncclGetUniqueId(&id));
     std::memcpy(id128, &id, sizeof(id));
@@ -814,8 +910,8 @@ int hsdla_b200_engine_set_comm(hsdla_b200_engine* e, const void* id128, int nran
     HS_NCCL(ncclCommInitRank(&e->comm, nranks, id, rank));
   });
 }
-int hsdla_b200_engine_kernel_times(hsdla_b200_engine* e, int reset, double* ms_s, double* ms_h,
-                                   uint64_t* flops_s, uint64_t* flops_h, uint64_t* n_builds) {
+int hsdla_b200_engine_kernel_times(hsdla_b200_engine* e, int reset, double* ms_s, double* ms_h, uint64_t* flops_s,
+                                   uint64_t* flops_h, uint64_t* n_builds) {
   return guarded([&] {
     if (!e) throw Fail{HSDLA_B200_CONFIG_ERROR, "null engine"};
     HS_CUDA(cudaSetDevice(e->device));
@@ -841,8 +937,12 @@ int hsdla_b200_build_hs(const hsdla_b200_problem* p, const hsdla_b200_options* o
     if (!p) throw Fail{HSDLA_B200_DIMENSION_ERROR, "null problem"};
     check_dims(p->n_atoms, p->n_l, p->n_g);
     if (!H || !S) throw Fail{HSDLA_B200_DIMENSION_ERROR, "null H or S"};
+    if (!p->A || !p->B || !p->T_AA || !p->T_AB || !p->T_BB || !p->U)
+      throw Fail{HSDLA_B200_DIMENSION_ERROR, "null problem pointer"};
     const int algo = o ? o->algo : HSDLA_B200_ALGO_REFINED_FUSED;
-    int P = o && o->n_gpus > 1 ? o->n_gpus : 1;
+    if (algo != HSDLA_B200_ALGO_REFINED && algo != HSDLA_B200_ALGO_REFINED_FUSED)
+      throw Fail{HSDLA_B200_CONFIG_ERROR, "unknown algo " + std::to_string(algo)};
+    const int P = o && o->n_gpus > 1 ? o->n_gpus : 1;
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
       (void)cudaGetLastError();
@@ -854,25 +954,8 @@ int hsdla_b200_build_hs(const hsdla_b200_problem* p, const hsdla_b200_options* o
       if (d < 0 || d >= ndev) throw Fail{HSDLA_B200_CONFIG_ERROR, "device id out of range"};
     std::lock_guard<std::mutex> lk(g_cache_mu);
     EngineSet* set = get_engines(devs, p->n_atoms, p->n_l, p->n_g);
-    // upload + build per GPU (host threads so pageable uploads proceed in parallel)
-    const auto t_up = std::chrono::steady_clock::now();
-    std::vector<std::thread> th;
-    std::vector<Status> errs(P, Status{0, ""});
-    for (int r = 0; r < P; ++r) {
-      th.emplace_back([&, r] {
-        errs[r].code = guarded([&] {
-          hsdla_b200_engine* e = set->engines[r];
-          engine_upload(e, p, set->atom0[r]);
-          HS_CUDA(cudaStreamSynchronize(e->stream));
-        });
-        if (errs[r].code) errs[r].msg = g_last_error;
-      });
-    }
-    for (auto& t : th) t.join();
-    for (auto& er : errs)
-      if (er.code) throw Fail{er.code, er.msg};
-    const double h2d = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_up).count();
-    for (int r = 0; r < P; ++r) engine_build(set->engines[r], algo);
+    // streamed upload + build per GPU
+    for (int r = 0; r < P; ++r) engine_build_streamed(set->engines[r], p, set->atom0[r], algo);
     if (P > 1) {
       HS_NCCL(ncclGroupStart());
       for (int r = 0; r < P; ++r) reduce_s(set->engines[r], 0);
@@ -882,20 +965,24 @@ int hsdla_b200_build_hs(const hsdla_b200_problem* p, const hsdla_b200_options* o
       HS_NCCL(ncclGroupEnd());
       for (int r = 0; r < P; ++r) reduce_finish(set->engines[r]);
     }
+    hsdla_b200_engine* root = set->engines[0];
+    HS_CUDA(cudaSetDevice(root->device));
+    enqueue_download(root);
+    const auto t_d = std::chrono::steady_clock::now();
+    finish_download(root, H, S);
+    const double d2h = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_d).count();
     hsdla_b200_stats local{};
     double maxph[5] = {0, 0, 0, 0, 0};
-    double dev_s = 0, red_s = 0;
+    double dev_s = 0, red_s = 0, h2d = 0;
     int launches = 0;
     for (int r = 0; r < P; ++r) {
       engine_sync(set->engines[r], &local);
       for (int i = 0; i < 5; ++i) maxph[i] = std::max(maxph[i], local.phase_seconds[i]);
       dev_s = std::max(dev_s, local.device_seconds);
       red_s = std::max(red_s, local.reduce_seconds);
+      h2d = std::max(h2d, local.h2d_seconds);
       launches += local.kernel_launches;
     }
-    const auto t_d = std::chrono::steady_clock::now();
-    engine_download(set->engines[0], H, S);
-    const double d2h = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_d).count();
     if (st) {
       std::memcpy(st->phase_seconds, maxph, sizeof(maxph));
       st->h2d_seconds = h2d;

@@ -209,6 +209,12 @@ class Engine:
     def build(self, algo="fused"):
         check(_lib.lib().hsdla_b200_engine_build(self.h, C.c_int(ALGOS[algo])), "engine_build")
 
+    def build_streamed(self, p, atom_begin=0, algo="fused"):
+        """Upload shard `atom_begin` of host problem p in atom chunks overlapped with the build."""
+        self._prob = p.c_struct()  # keep the struct alive while the copies are in flight
+        check(_lib.lib().hsdla_b200_engine_build_streamed(self.h, C.byref(self._prob), C.c_uint64(atom_begin),
+                                                          C.c_int(ALGOS[algo])), "engine_build_streamed")
+
     def reduce(self, root=0):
         check(_lib.lib().hsdla_b200_engine_reduce(self.h, C.c_int(root)), "engine_reduce")
 

@@ -115,9 +115,16 @@ def test_properties_at_config2():
     linearity in T (doubling every T doubles H, leaves S); atom additivity (the sum over
     atom shards that the multi-GPU NCCL reduce relies on); determinism run to run."""
     p = hb.generate_problem(64, 81, 3000, 1, 0)
-    r1 = hb.build_hs_refined(p)
+    r1 = hb.build_hs_refined(p)  # streamed: 8 atom chunks, H2D overlapped, beta=1 accumulation
     r2 = hb.build_hs_refined(p)
     assert np.array_equal(r1.H, r2.H) and np.array_equal(r1.S, r2.S)
+    e = hb.Engine(0, 64, 81, 3000)  # device-resident single-chunk build
+    e.upload(p)
+    e.build()
+    e.sync()
+    He, Se = e.download()
+    e.close()
+    assert rel(He, r1.H) <= 1e-13 and rel(Se, r1.S) <= 1e-13
     S = hb.mirror(r1.S.copy())
     S[np.diag_indices_from(S)] += 1e-8 * np.linalg.norm(S)
     np.linalg.cholesky(S)
