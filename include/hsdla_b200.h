@@ -168,6 +168,43 @@ int hsdla_b200_engine_kernel_times(hsdla_b200_engine* e, int reset, double* ms_s
  * measurement probe, not part of the H/S path. */
 int hsdla_b200_fp64_peak(int device, double seconds, double* tflops);
 
+/* ---- LAPW matching-coefficient setup (north_star subsystem 1) -------------
+ * Builds A, B and U on the GPU from the physical inputs instead of uploading
+ * them.  The reference has no implementation of this step (A, B
+ * are synthetic inputs there); the math is the standard LAPW matching of paper
+ * Eq. (basis), see paper_1712_07206_b200/csrc/lapw_setup.cuh:
+ *   A^{a,G}_lm = c [j_l(KR) udot'_l - K j_l'(KR) udot_l] / det,
+ *   B^{a,G}_lm = c [K j_l'(KR) u_l - j_l(KR) u'_l] / det,
+ *   c = 4 pi Omega^{-1/2} e^{iK.tau_a} i^l conj(Y_lm(K^)),  K = k + G,
+ *   det = u_l udot'_l - udot_l u'_l   (radial values at R = rmt of the atom's type),
+ * rows a*(lmax+1)^2 + l(l+1)+m, Y_lm with the Condon-Shortley phase; U row
+ * a*(lmax+1)^2 + lm = udot_norm[type(a)][l]. */
+typedef struct hsdla_b200_lapw {
+  uint64_t n_atoms, n_types, n_g;
+  int lmax;                  /* <= 20; N_L = (lmax+1)^2 */
+  double kpt[3];             /* k-point, Cartesian */
+  double omega;              /* unit-cell volume */
+  const double* gvec;        /* n_g x 3 Cartesian G vectors (G_j = gvec[3j..3j+2]) */
+  const double* tau;         /* n_atoms x 3 Cartesian atom positions */
+  const int32_t* atom_type;  /* n_atoms, in [0, n_types) */
+  const double* rmt;         /* n_types muffin-tin radii */
+  const double* u;           /* n_types x (lmax+1), row-major: u_l(R) */
+  const double* du;          /* u_l'(R) */
+  const double* udot;        /* udot_l(R) */
+  const double* dudot;       /* udot_l'(R) */
+  const double* udot_norm;   /* ||udot_l|| (the U diagonal) */
+} hsdla_b200_lapw;
+
+/* One-shot: A, B ((n_atoms (lmax+1)^2) x n_g complex, col-major) and U to host. */
+int hsdla_b200_lapw_coefficients(int device, const hsdla_b200_lapw* sys, double* A, double* B, double* U);
+/* Fill the engine's A, B, U for its shard [atom_begin, atom_begin + n_atoms_local) in HBM. */
+int hsdla_b200_engine_setup_lapw(hsdla_b200_engine* e, const hsdla_b200_lapw* sys, uint64_t atom_begin);
+/* H2D of the shard's T_AA, T_AB, T_BB blocks only (with setup_lapw: a build needs no A/B upload). */
+int hsdla_b200_engine_upload_operators(hsdla_b200_engine* e, const double* T_AA, const double* T_AB,
+                                       const double* T_BB, uint64_t atom_begin);
+/* Mean CUDA-event time (ms) of the last setup_lapw kernel and its bytes written. */
+int hsdla_b200_engine_setup_time(hsdla_b200_engine* e, double* ms, uint64_t* bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -9,6 +9,7 @@
  */
 #include "hsdla_oracle.h"
 
+#define _GNU_SOURCE
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
@@ -455,4 +456,121 @@ double orc_rel_frobenius_error_lower(uint64_t n, const double* x_, const double*
     }
   const double den = sqrt(ref);
   return sqrt(diff) / (den > 1e-300 ? den : 1e-300);
+}
+
+/* ------------------------------------------------------------------------ */
+/* LAPW matching coefficients (self-authored; see hsdla_oracle.h).          */
+/* ------------------------------------------------------------------------ */
+
+/* Y_lm(K^) with the Condon-Shortley phase, lm = l(l+1)+m: unnormalised
+ * P_l^m by the three-term recurrence in l, normalisation by lgamma. */
+void orc_ylm(int lmax, double kx, double ky, double kz, double* Yd) {
+  cx* Y = (cx*)Yd;
+  const double rho = sqrt(kx * kx + ky * ky), kn = sqrt(kx * kx + ky * ky + kz * kz);
+  const double x = kn > 0 ? kz / kn : 1.0, s = kn > 0 ? rho / kn : 0.0;
+  const double phi = (rho > 0) ? atan2(ky, kx) : 0.0;
+  for (int m = 0; m <= lmax; ++m) {
+    /* P_m^m = (-1)^m (2m-1)!! s^m */
+    double pmm = 1.0;
+    for (int k = 1; k <= m; ++k) pmm *= -(2.0 * k - 1.0) * s;
+    double pl2 = 0.0, pl1 = 0.0;
+    for (int l = m; l <= lmax; ++l) {
+      double p;
+      if (l == m) p = pmm;
+      else if (l == m + 1) p = x * (2.0 * m + 1.0) * pmm;
+      else p = ((2.0 * l - 1.0) * x * pl1 - (l + m - 1.0) * pl2) / (l - m);
+      pl2 = pl1;
+      pl1 = p;
+      const double norm = sqrt((2.0 * l + 1.0) / (4.0 * M_PI) * exp(lgamma(l - m + 1.0) - lgamma(l + m + 1.0)));
+      const double v = norm * p;
+      const int lm = l * (l + 1);
+      Y[lm + m] = cx_make(v * cos(m * phi), v * sin(m * phi));
+      if (m > 0) {
+        const double sg = (m & 1) ? -1.0 : 1.0;
+        Y[lm - m] = cx_make(sg * Y[lm + m].re, -sg * Y[lm + m].im);
+      }
+    }
+  }
+}
+
+/* j_l(x), l = 0..lmax: series below 1e-3, Miller downward recurrence otherwise. */
+void orc_sph_bessel(int lmax, double x, double* j) {
+  if (x < 1e-3) {
+    double xl = 1.0, df = 1.0;
+    for (int l = 0; l <= lmax; ++l) {
+      if (l) { xl *= x; df *= 2.0 * l + 1.0; }
+      j[l] = xl / df * (1.0 - x * x / (2.0 * (2 * l + 3)) + x * x * x * x / (8.0 * (2 * l + 3) * (2 * l + 5)));
+    }
+    return;
+  }
+  const int top = lmax + 40 + (int)(2.0 * x);
+  double jp1 = 0.0, jl = 1e-280;
+  double* tmp = calloc((size_t)lmax + 1, sizeof(double));
+  for (int l = top; l >= 1; --l) {
+    const double jm1 = (2.0 * l + 1.0) / x * jl - jp1;
+    jp1 = jl;
+    jl = jm1;
+    if (l - 1 <= lmax) tmp[l - 1] = jl;
+    if (fabs(jl) > 1e200) {
+      jl *= 1e-200;
+      jp1 *= 1e-200;
+      for (int m = l - 1; m <= lmax; ++m) tmp[m] *= 1e-200;
+    }
+  }
+  const double norm = (sin(x) / x) / jl;
+  for (int l = 0; l <= lmax; ++l) j[l] = tmp[l] * norm;
+  free(tmp);
+}
+
+int orc_lapw_coefficients(uint64_t n_atoms, uint64_t n_types, int lmax, uint64_t n_g, const double* kpt,
+                          const double* gvec, const double* tau, const int32_t* type, const double* rmt,
+                          const double* u, const double* du, const double* udot, const double* dudot,
+                          const double* udot_norm, double omega, double* Ad, double* Bd, double* U) {
+  const int nl = (lmax + 1) * (lmax + 1), nlv = lmax + 1;
+  const size_t K = n_atoms * (size_t)nl;
+  cx* A = (cx*)Ad;
+  cx* B = (cx*)Bd;
+  cx* Y = malloc(sizeof(cx) * nl);
+  double* jl = malloc(sizeof(double) * (nlv + 1));
+  const double pref = 4.0 * M_PI / sqrt(omega);
+  for (uint64_t a = 0; a < n_atoms; ++a) {
+    if (type[a] < 0 || (uint64_t)type[a] >= n_types) return 1;
+    for (int l = 0; l <= lmax; ++l)
+      for (int m = -l; m <= l; ++m) U[a * nl + l * (l + 1) + m] = udot_norm[type[a] * nlv + l];
+  }
+  for (uint64_t g = 0; g < n_g; ++g) {
+    const double kx = kpt[0] + gvec[3 * g], ky = kpt[1] + gvec[3 * g + 1], kz = kpt[2] + gvec[3 * g + 2];
+    const double kn = sqrt(kx * kx + ky * ky + kz * kz);
+    orc_ylm(lmax, kx, ky, kz, (double*)Y);
+    for (uint64_t a = 0; a < n_atoms; ++a) {
+      const int t = type[a];
+      const double R = rmt[t];
+      orc_sph_bessel(lmax + 1, kn * R, jl);
+      const double ph = kx * tau[3 * a] + ky * tau[3 * a + 1] + kz * tau[3 * a + 2];
+      const cx sf = cx_make(pref * cos(ph), pref * sin(ph));
+      for (int l = 0; l <= lmax; ++l) {
+        /* K j_l'(KR) from j_l' = j_{l-1} - (l+1)/x j_l (a different identity than the GPU's) */
+        double kjd;
+        const double xr = kn * R;
+        if (xr == 0.0) kjd = 0.0;
+        else if (l == 0) kjd = -kn * jl[1];
+        else kjd = kn * (jl[l - 1] - (l + 1.0) / xr * jl[l]);
+        const int ti = t * nlv + l;
+        const double det = u[ti] * dudot[ti] - udot[ti] * du[ti];
+        if (det == 0.0) return 2;
+        const double fa = (jl[l] * dudot[ti] - kjd * udot[ti]) / det;
+        const double fb = (kjd * u[ti] - jl[l] * du[ti]) / det;
+        const cx il = (l % 4 == 0) ? cx_make(1, 0) : (l % 4 == 1) ? cx_make(0, 1) : (l % 4 == 2) ? cx_make(-1, 0) : cx_make(0, -1);
+        for (int m = -l; m <= l; ++m) {
+          const int lm = l * (l + 1) + m;
+          const cx c = cx_mul(cx_mul(sf, il), cx_conj(Y[lm]));
+          A[a * nl + lm + g * K] = cx_scale(fa, c);
+          B[a * nl + lm + g * K] = cx_scale(fb, c);
+        }
+      }
+    }
+  }
+  free(Y);
+  free(jl);
+  return 0;
 }

@@ -52,6 +52,22 @@ int orc_build_hs_sampled(uint64_t na, uint64_t nl, uint64_t ng, const double* A,
                          const double* T_AA, const double* T_AB, const double* T_BB,
                          const double* U, const uint64_t* J, uint64_t nj, double* Hs, double* Ss);
 
+/* ---- LAPW matching-coefficient setup (north_star subsystem 1) -------------
+ * NO REFERENCE IMPLEMENTATION exists (SPEC.md:89-90 makes A, B synthetic inputs);
+ * this is a self-authored restatement of the standard LAPW matching (paper Eq.
+ * basis), "parity self-pinned": orc_ylm / orc_sph_bessel are
+ * checked against scipy.special.sph_harm_y / spherical_jn in tests/test_lapw.py.
+ * Algorithms deliberately differ from the GPU's (unnormalised Legendre recurrence
+ * + lgamma normalisation; Miller recurrence for every x >= 1e-3). */
+void orc_ylm(int lmax, double kx, double ky, double kz, double* Y /* 2*(lmax+1)^2 */);
+void orc_sph_bessel(int lmax, double x, double* j /* lmax+1 */);
+/* A, B: (n_atoms*(lmax+1)^2) x n_g complex, column-major; U: n_atoms*(lmax+1)^2.
+ * radial arrays are n_types x (lmax+1), row-major [t*(lmax+1)+l]. */
+int orc_lapw_coefficients(uint64_t n_atoms, uint64_t n_types, int lmax, uint64_t n_g, const double* kpt,
+                          const double* gvec, const double* tau, const int32_t* type, const double* rmt,
+                          const double* u, const double* du, const double* udot, const double* dudot,
+                          const double* udot_norm, double omega, double* A, double* B, double* U);
+
 /* proj/src/complex_matrix.cpp:106-118 */
 double orc_rel_frobenius_error_lower(uint64_t n, const double* x, const double* y);
 

@@ -137,6 +137,32 @@ class Restatement(_Base):
             raise ValueError(f"orc_build_hs_sampled rc={rc}")
         return Hs, Ss
 
+    def ylm(self, lmax, K):
+        Y = np.zeros((lmax + 1) ** 2, np.complex128)
+        self.lib.orc_ylm(C.c_int(lmax), *[C.c_double(float(v)) for v in K], _ptr(Y))
+        return Y
+
+    def sph_bessel(self, lmax, x):
+        j = np.zeros(lmax + 1)
+        self.lib.orc_sph_bessel(C.c_int(lmax), C.c_double(float(x)), _ptr(j))
+        return j
+
+    def lapw_coefficients(self, s):
+        """Self-authored LAPW matching coefficients (no reference implementation exists)."""
+        nl = (s.lmax + 1) ** 2
+        K = s.n_atoms * nl
+        A = np.zeros((K, s.n_g), np.complex128, order="F")
+        B = np.zeros((K, s.n_g), np.complex128, order="F")
+        U = np.zeros((nl, s.n_atoms), np.float64, order="F")
+        f = lambda a: np.ascontiguousarray(a, dtype=np.float64)
+        args = [f(s.kpt), f(s.gvec), f(s.tau), np.ascontiguousarray(s.atom_type, dtype=np.int32), f(s.rmt), f(s.u),
+                f(s.du), f(s.udot), f(s.dudot), f(s.udot_norm)]
+        rc = self.lib.orc_lapw_coefficients(_u64(s.n_atoms), _u64(s.n_types), C.c_int(s.lmax), _u64(s.n_g),
+                                            *[_ptr(a) for a in args], C.c_double(s.omega), _ptr(A), _ptr(B), _ptr(U))
+        if rc:
+            raise ValueError(f"orc_lapw_coefficients rc={rc}")
+        return A, B, U
+
     def rel_frobenius_error_lower(self, x, y):
         x = np.asfortranarray(x, dtype=np.complex128)
         y = np.asfortranarray(y, dtype=np.complex128)

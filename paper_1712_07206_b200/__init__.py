@@ -11,3 +11,4 @@ from .pipeline import (Engine, FlopLedger, HSResult, PhaseTime, PipelineConfig, 
                        nccl_unique_id, parse_strategy, shard_atoms, parse_variant, rel_frobenius_error_lower, release_cache)
 from .problem import (Preset, ProblemInstance, empty_problem, find_preset, generate_problem,  # noqa: F401
                       load_problem, presets, save_problem)
+from .lapw import LapwSystem, build_hs_lapw, lapw_coefficients, make_lapw_system  # noqa: F401,E402

@@ -37,6 +37,7 @@
 
 #include "../../include/hsdla_b200.h"
 #include "ctn_contract.cuh"
+#include "lapw_setup.cuh"
 
 namespace hsdla_b200 {
 
@@ -211,6 +212,8 @@ struct hsdla_b200_engine {
   std::vector<cudaEvent_t> ev_chunk_up;
   int last_algo = 0, launches = 0;
   bool built = false, reduced = false, uploaded_streamed = false;
+  cudaEvent_t ev_setup0 = nullptr, ev_setup1 = nullptr;  // last LAPW setup kernel
+  uint64_t setup_bytes = 0;
   // roofline: events around the whole-build S and H contraction launches, harvested lazily
   static constexpr int kRing = 64;
   struct KTimer {
@@ -251,7 +254,7 @@ static void engine_free(hsdla_b200_engine* e) {
   for (cudaEvent_t ev : e->ev_pool) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e->ev_chunk_up) cudaEventDestroy(ev);
   for (cudaEvent_t ev : {e->ev_begin, e->ev_end, e->ev_s_done, e->ev_s_red, e->ev_reduce_end, e->ev_up0, e->ev_up1,
-                         e->ev_s_d2h, e->ev_h_d2h})
+                         e->ev_s_d2h, e->ev_h_d2h, e->ev_setup0, e->ev_setup1})
     if (ev) cudaEventDestroy(ev);
   for (auto& t : e->ring)
     for (cudaEvent_t ev : {t.s0, t.s1, t.h0, t.h1})
@@ -383,7 +386,8 @@ static hsdla_b200_engine* engine_create(int device, uint64_t na, uint64_t nl, ui
     HS_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
     HS_CUDA(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
     HS_CUDA(cudaStreamCreateWithFlags(&e->comm_stream, cudaStreamNonBlocking));
-    for (cudaEvent_t* ev : {&e->ev_begin, &e->ev_end, &e->ev_reduce_end, &e->ev_up0, &e->ev_up1})
+    for (cudaEvent_t* ev : {&e->ev_begin, &e->ev_end, &e->ev_reduce_end, &e->ev_up0, &e->ev_up1, &e->ev_setup0,
+                            &e->ev_setup1})
       HS_CUDA(cudaEventCreate(ev));
     for (cudaEvent_t* ev : {&e->ev_s_done, &e->ev_s_red, &e->ev_s_d2h, &e->ev_h_d2h})
       HS_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
@@ -696,6 +700,112 @@ static void engine_download(hsdla_b200_engine* e, double* H, double* S) {
 }
 
 // ---------------------------------------------------------------------------
+// LAPW matching-coefficient setup
+// ---------------------------------------------------------------------------
+static void check_lapw(const hsdla_b200_lapw* sys) {
+  if (!sys || !sys->gvec || !sys->tau || !sys->atom_type || !sys->rmt || !sys->u || !sys->du || !sys->udot ||
+      !sys->dudot || !sys->udot_norm)
+    throw Fail{HSDLA_B200_DIMENSION_ERROR, "lapw: null pointer"};
+  if (sys->n_atoms < 1 || sys->n_types < 1 || sys->n_g < 1 || sys->lmax < 0 || sys->lmax > kLapwMaxL)
+    throw Fail{HSDLA_B200_DIMENSION_ERROR, "lapw: need n_atoms, n_types, n_g >= 1 and 0 <= lmax <= 20"};
+  if (!(sys->omega > 0.0)) throw Fail{HSDLA_B200_DIMENSION_ERROR, "lapw: omega must be > 0"};
+  for (uint64_t a = 0; a < sys->n_atoms; ++a)
+    if (sys->atom_type[a] < 0 || static_cast<uint64_t>(sys->atom_type[a]) >= sys->n_types)
+      throw Fail{HSDLA_B200_DIMENSION_ERROR, "lapw: atom_type out of range"};
+  const int nlv = sys->lmax + 1;
+  for (uint64_t t = 0; t < sys->n_types; ++t) {
+    if (!(sys->rmt[t] > 0.0)) throw Fail{HSDLA_B200_DIMENSION_ERROR, "lapw: rmt must be > 0"};
+    for (int l = 0; l < nlv; ++l) {
+      const size_t i = t * nlv + l;
+      if (sys->u[i] * sys->dudot[i] - sys->udot[i] * sys->du[i] == 0.0)
+        throw Fail{HSDLA_B200_DIMENSION_ERROR, "lapw: singular radial matching system (u udot' - udot u' == 0)"};
+    }
+  }
+}
+
+// Compute A, B (ld = ldo rows) and U for atoms [a0, a0+na) of sys on stream s.
+static void lapw_enqueue(const hsdla_b200_lapw* sys, uint64_t a0, uint64_t na, double2* A, double2* B, uint64_t ldo,
+                         double* U, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
+  const int nlv = sys->lmax + 1, nl = nlv * nlv;
+  const size_t shmem = (static_cast<size_t>(nl) + na + sys->n_types * nlv) * sizeof(double2) + nl + 16;
+  if (shmem > 200 * 1024) throw Fail{HSDLA_B200_SIZING_ERROR, "lapw: too many atoms per GPU shard for one column"};
+  std::vector<double> radial(sys->n_types * nlv * 4);
+  for (uint64_t t = 0; t < sys->n_types; ++t)
+    for (int l = 0; l < nlv; ++l) {
+      const size_t i = t * nlv + l;
+      radial[4 * i + 0] = sys->u[i];
+      radial[4 * i + 1] = sys->du[i];
+      radial[4 * i + 2] = sys->udot[i];
+      radial[4 * i + 3] = sys->dudot[i];
+    }
+  double *d_g = nullptr, *d_tau = nullptr, *d_rad = nullptr, *d_rmt = nullptr, *d_un = nullptr;
+  int32_t* d_type = nullptr;
+  HS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_g), sys->n_g * 3 * sizeof(double), s));
+  HS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_tau), na * 3 * sizeof(double), s));
+  HS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_type), na * sizeof(int32_t), s));
+  HS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_rad), radial.size() * sizeof(double), s));
+  HS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_rmt), sys->n_types * sizeof(double), s));
+  HS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_un), sys->n_types * nlv * sizeof(double), s));
+  HS_CUDA(cudaMemcpyAsync(d_g, sys->gvec, sys->n_g * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+  HS_CUDA(cudaMemcpyAsync(d_tau, sys->tau + 3 * a0, na * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+  HS_CUDA(cudaMemcpyAsync(d_type, sys->atom_type + a0, na * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  HS_CUDA(cudaMemcpyAsync(d_rad, radial.data(), radial.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  HS_CUDA(cudaMemcpyAsync(d_rmt, sys->rmt, sys->n_types * sizeof(double), cudaMemcpyHostToDevice, s));
+  HS_CUDA(cudaMemcpyAsync(d_un, sys->udot_norm, sys->n_types * nlv * sizeof(double), cudaMemcpyHostToDevice, s));
+  LapwDevParams P;
+  P.gvec = d_g;
+  P.tau = d_tau;
+  P.type = d_type;
+  P.radial = d_rad;
+  P.rmt = d_rmt;
+  P.kx = sys->kpt[0];
+  P.ky = sys->kpt[1];
+  P.kz = sys->kpt[2];
+  P.pref = 4.0 * M_PI / std::sqrt(sys->omega);
+  P.n_atoms = static_cast<int>(na);
+  P.n_types = static_cast<int>(sys->n_types);
+  P.lmax = sys->lmax;
+  P.n_g = static_cast<int>(sys->n_g);
+  P.A = A;
+  P.B = B;
+  P.ldo = ldo;
+  HS_CUDA(cudaFuncSetAttribute(lapw_setup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(shmem)));
+  if (ev0) HS_CUDA(cudaEventRecord(ev0, s));
+  lapw_setup_kernel<<<static_cast<unsigned>(sys->n_g), 256, shmem, s>>>(P);
+  HS_CUDA(cudaGetLastError());
+  if (ev1) HS_CUDA(cudaEventRecord(ev1, s));
+  const int rows = static_cast<int>(na * nl);
+  lapw_u_kernel<<<(rows + 255) / 256, 256, 0, s>>>(d_type, d_un, sys->lmax, static_cast<int>(na), U);
+  HS_CUDA(cudaGetLastError());
+  for (void* p : {(void*)d_g, (void*)d_tau, (void*)d_type, (void*)d_rad, (void*)d_rmt, (void*)d_un})
+    HS_CUDA(cudaFreeAsync(p, s));
+}
+
+static void engine_setup_lapw(hsdla_b200_engine* e, const hsdla_b200_lapw* sys, uint64_t a0) {
+  check_lapw(sys);
+  const uint64_t nlv = sys->lmax + 1;
+  if (nlv * nlv != e->nl || sys->n_g != e->ng || a0 + e->na > sys->n_atoms)
+    throw Fail{HSDLA_B200_DIMENSION_ERROR, "lapw system does not match the engine shard"};
+  HS_CUDA(cudaSetDevice(e->device));
+  lapw_enqueue(sys, a0, e->na, e->A, e->B, e->K, e->U, e->stream, e->ev_setup0, e->ev_setup1);
+  e->setup_bytes = 2 * e->K * e->ng * sizeof(double2);
+}
+
+static void engine_upload_operators(hsdla_b200_engine* e, const double* taa, const double* tab, const double* tbb,
+                                    uint64_t a0) {
+  if (!taa || !tab || !tbb) throw Fail{HSDLA_B200_DIMENSION_ERROR, "null operator pointer"};
+  HS_CUDA(cudaSetDevice(e->device));
+  const uint64_t blk = e->nl * e->nl;
+  const size_t bytes = e->na * blk * sizeof(double2);
+  HS_CUDA(cudaMemcpyAsync(e->Taa, reinterpret_cast<const double2*>(taa) + a0 * blk, bytes, cudaMemcpyHostToDevice,
+                          e->stream));
+  HS_CUDA(cudaMemcpyAsync(e->Tab, reinterpret_cast<const double2*>(tab) + a0 * blk, bytes, cudaMemcpyHostToDevice,
+                          e->stream));
+  HS_CUDA(cudaMemcpyAsync(e->Tbb, reinterpret_cast<const double2*>(tbb) + a0 * blk, bytes, cudaMemcpyHostToDevice,
+                          e->stream));
+}
+
+// ---------------------------------------------------------------------------
 // the one-shot drop-in: cached engines, atom sharding, NCCL reduce
 // ---------------------------------------------------------------------------
 struct EngineSet {
@@ -927,6 +1037,58 @@ int hsdla_b200_engine_kernel_times(hsdla_b200_engine* e, int reset, double* ms_s
       e->sum_s_ms = e->sum_h_ms = 0;
       e->sum_flops_h = e->timed_builds = 0;
     }
+  });
+}
+
+int hsdla_b200_lapw_coefficients(int device, const hsdla_b200_lapw* sys, double* A, double* B, double* U) {
+  return guarded([&] {
+    check_lapw(sys);
+    if (!A || !B || !U) throw Fail{HSDLA_B200_DIMENSION_ERROR, "null output"};
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+      (void)cudaGetLastError();
+      throw Fail{HSDLA_B200_CONFIG_ERROR, "no such CUDA device (the B200 path has no CPU fallback)"};
+    }
+    HS_CUDA(cudaSetDevice(device));
+    const uint64_t nlv = sys->lmax + 1, K = sys->n_atoms * nlv * nlv;
+    check_dims(sys->n_atoms, nlv * nlv, sys->n_g);
+    struct Buf {
+      void* p = nullptr;
+      ~Buf() {
+        if (p) cudaFree(p);
+      }
+    } dA, dB, dU;
+    HS_CUDA(cudaMalloc(&dA.p, K * sys->n_g * sizeof(double2)));
+    HS_CUDA(cudaMalloc(&dB.p, K * sys->n_g * sizeof(double2)));
+    HS_CUDA(cudaMalloc(&dU.p, K * sizeof(double)));
+    cudaStream_t s = 0;
+    lapw_enqueue(sys, 0, sys->n_atoms, static_cast<double2*>(dA.p), static_cast<double2*>(dB.p), K,
+                 static_cast<double*>(dU.p), s, nullptr, nullptr);
+    HS_CUDA(cudaMemcpy(A, dA.p, K * sys->n_g * sizeof(double2), cudaMemcpyDeviceToHost));
+    HS_CUDA(cudaMemcpy(B, dB.p, K * sys->n_g * sizeof(double2), cudaMemcpyDeviceToHost));
+    HS_CUDA(cudaMemcpy(U, dU.p, K * sizeof(double), cudaMemcpyDeviceToHost));
+  });
+}
+int hsdla_b200_engine_setup_lapw(hsdla_b200_engine* e, const hsdla_b200_lapw* sys, uint64_t atom_begin) {
+  return guarded([&] {
+    if (!e) throw Fail{HSDLA_B200_CONFIG_ERROR, "null engine"};
+    engine_setup_lapw(e, sys, atom_begin);
+  });
+}
+int hsdla_b200_engine_upload_operators(hsdla_b200_engine* e, const double* T_AA, const double* T_AB,
+                                       const double* T_BB, uint64_t atom_begin) {
+  return guarded([&] {
+    if (!e) throw Fail{HSDLA_B200_CONFIG_ERROR, "null engine"};
+    engine_upload_operators(e, T_AA, T_AB, T_BB, atom_begin);
+  });
+}
+int hsdla_b200_engine_setup_time(hsdla_b200_engine* e, double* ms, uint64_t* bytes) {
+  return guarded([&] {
+    if (!e) throw Fail{HSDLA_B200_CONFIG_ERROR, "null engine"};
+    if (!e->setup_bytes) throw Fail{HSDLA_B200_CONFIG_ERROR, "no setup_lapw has run"};
+    HS_CUDA(cudaEventSynchronize(e->ev_setup1));
+    if (ms) *ms = ev_ms(e->ev_setup0, e->ev_setup1);
+    if (bytes) *bytes = e->setup_bytes;
   });
 }
 
