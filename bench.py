@@ -261,6 +261,10 @@ def run_b200(args):
     if not args.no_e2e:
         e2e = run_e2e(args, hb, d, p, eng, na_total, nl, ng)
 
+    lapw = None
+    if P == 1 and not args.no_e2e:
+        lapw = run_lapw(args, hb, p, na, nl, ng)
+
     peak = hb.fp64_peak(dev, 1.0)
     line = None
     if d.rank == 0:
@@ -291,6 +295,8 @@ def run_b200(args):
         }
         if e2e is not None:
             line["e2e"] = e2e
+        if lapw is not None:
+            line.update(lapw)
         if P == 1 and not args.no_cpu_baseline:
             try:
                 cb = cpu_reference_sample(na, nl, ng, args.cpu_budget)
@@ -301,6 +307,71 @@ def run_b200(args):
     eng.close()
     d.close()
     return 0
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
+    except (OSError, ValueError, KeyError):
+        return 6650.0, "B200_PROFILING.md fallback 6.65 TB/s"
+
+
+def run_lapw(args, hb, p, na, nl, ng):
+    """North_star subsystem 1 on the same workload shape: the LAPW matching-coefficient
+    setup kernel (HBM-write bound) and the physics-input end-to-end path, where only
+    G vectors, atom data, radial values and T operators go host->device and A, B are
+    built in HBM (no reference equivalent: the reference takes A, B as inputs)."""
+    import torch
+    lmax = int(round(nl ** 0.5)) - 1
+    if (lmax + 1) ** 2 != nl:
+        return None
+    s = hb.make_lapw_system(na, lmax, ng, n_types=2, seed=1)
+    eng = hb.Engine(torch.cuda.current_device(), na, nl, ng)
+    H = np.zeros((ng, ng), np.complex128, order="F")
+    S = np.zeros((ng, ng), np.complex128, order="F")
+    ops = [p.T_AA, p.T_AB, p.T_BB, H, S]
+    for b in ops:
+        hb.host_register(b)
+    try:
+        times = []
+        for _ in range(5):
+            eng.setup_lapw(s)
+            eng.sync()
+            times.append(eng.setup_time()["ms"])
+        nbytes = eng.setup_time()["bytes"]
+        ms = float(np.median(times))
+        peak, src = hbm_peak()
+
+        def one():
+            eng.setup_lapw(s)
+            eng.upload_operators(p.T_AA, p.T_AB, p.T_BB)
+            eng.build(args.algo)
+            eng.download(H, S)
+
+        one()
+        eng.sync()
+        steps = max(1, min(args.steps, args.e2e_steps))
+        t = time.perf_counter()
+        for _ in range(steps):
+            one()
+        eng.sync()
+        dt = (time.perf_counter() - t) / steps
+    finally:
+        for b in ops:
+            hb.host_unregister(b)
+        eng.close()
+    h2d = s.gvec.nbytes + s.tau.nbytes + 6 * s.u.nbytes + 3 * p.T_AA.nbytes
+    return {
+        "setup_roofline": {"bound": "hbm", "achieved": nbytes / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                           "frac": nbytes / (ms * 1e-3) / 1e9 / peak, "traffic": None,
+                           "kernel": "lapw_setup_kernel (A, B = 2 x K x N_G x 16 B written per launch)",
+                           "bytes_per_launch": int(nbytes), "kernel_ms": ms, "peak_source": src},
+        "e2e_lapw": {"value": ledger_flops(na, nl, ng) / dt / 1e12, "unit": "TFLOP/s", "ms_per_step": dt * 1e3,
+                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(2 * (ng * (ng + 1) // 2) * 16),
+                     "api": "engine_setup_lapw + engine_upload_operators + engine_build + engine_download (C-ABI); "
+                            "A, B built in HBM from G vectors / atoms / radial data"},
+    }
 
 
 def run_e2e(args, hb, d, p, eng, na_total, nl, ng):

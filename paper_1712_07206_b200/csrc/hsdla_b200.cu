@@ -214,6 +214,8 @@ struct hsdla_b200_engine {
   bool built = false, reduced = false, uploaded_streamed = false;
   cudaEvent_t ev_setup0 = nullptr, ev_setup1 = nullptr;  // last LAPW setup kernel
   uint64_t setup_bytes = 0;
+  void* lapw_scratch = nullptr;  // device copy of the LAPW inputs (grown on demand)
+  size_t lapw_scratch_bytes = 0;
   // roofline: events around the whole-build S and H contraction launches, harvested lazily
   static constexpr int kRing = 64;
   struct KTimer {
@@ -246,7 +248,7 @@ static void dalloc(hsdla_b200_engine* e, T** p, uint64_t count) {
 
 static void engine_free(hsdla_b200_engine* e) {
   cudaSetDevice(e->device);
-  for (void* p : {(void*)e->sk_ws, (void*)e->sk_flags, (void*)e->A, (void*)e->B, (void*)e->X1, (void*)e->X2,
+  for (void* p : {e->lapw_scratch, (void*)e->sk_ws, (void*)e->sk_flags, (void*)e->A, (void*)e->B, (void*)e->X1, (void*)e->X2,
                   (void*)e->Tab, (void*)e->Taa, (void*)e->Tbb, (void*)e->Paa, (void*)e->Pbb, (void*)e->U,
                   (void*)e->Hp, (void*)e->Sp})
     if (p) cudaFree(p);
@@ -723,41 +725,49 @@ static void check_lapw(const hsdla_b200_lapw* sys) {
   }
 }
 
+// Bytes of device scratch the LAPW inputs of `na` atoms need (8-byte aligned parts).
+static size_t lapw_scratch_size(const hsdla_b200_lapw* sys, uint64_t na) {
+  const size_t nlv = sys->lmax + 1;
+  return (sys->n_g * 3 + na * 3 + sys->n_types * nlv * 4 + sys->n_types + sys->n_types * nlv) * sizeof(double) +
+         ((na * sizeof(int32_t) + 7) & ~size_t(7));
+}
+
 // Compute A, B (ld = ldo rows) and U for atoms [a0, a0+na) of sys on stream s.
+// `scratch` (lapw_scratch_size bytes, device) receives the inputs; the host staging
+// is pinned so the small uploads are asynchronous.
 static void lapw_enqueue(const hsdla_b200_lapw* sys, uint64_t a0, uint64_t na, double2* A, double2* B, uint64_t ldo,
-                         double* U, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
+                         double* U, void* scratch, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
   const int nlv = sys->lmax + 1, nl = nlv * nlv;
   const size_t shmem = (static_cast<size_t>(nl) + na + sys->n_types * nlv) * sizeof(double2) + nl + 16;
   if (shmem > 200 * 1024) throw Fail{HSDLA_B200_SIZING_ERROR, "lapw: too many atoms per GPU shard for one column"};
-  std::vector<double> radial(sys->n_types * nlv * 4);
+  // pack [gvec | tau | radial(u,u',udot,udot') | rmt | udot_norm | type] into one host block
+  const size_t n_g3 = sys->n_g * 3, n_t3 = na * 3, n_rad = sys->n_types * nlv * 4, n_un = sys->n_types * nlv;
+  std::vector<double> h(n_g3 + n_t3 + n_rad + sys->n_types + n_un + (na * sizeof(int32_t) + 7) / 8);
+  double* hp = h.data();
+  std::memcpy(hp, sys->gvec, n_g3 * sizeof(double));
+  std::memcpy(hp + n_g3, sys->tau + 3 * a0, n_t3 * sizeof(double));
+  double* rad = hp + n_g3 + n_t3;
   for (uint64_t t = 0; t < sys->n_types; ++t)
     for (int l = 0; l < nlv; ++l) {
       const size_t i = t * nlv + l;
-      radial[4 * i + 0] = sys->u[i];
-      radial[4 * i + 1] = sys->du[i];
-      radial[4 * i + 2] = sys->udot[i];
-      radial[4 * i + 3] = sys->dudot[i];
+      rad[4 * i + 0] = sys->u[i];
+      rad[4 * i + 1] = sys->du[i];
+      rad[4 * i + 2] = sys->udot[i];
+      rad[4 * i + 3] = sys->dudot[i];
     }
-  double *d_g = nullptr, *d_tau = nullptr, *d_rad = nullptr, *d_rmt = nullptr, *d_un = nullptr;
-  int32_t* d_type = nullptr;
-  HS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_g), sys->n_g * 3 * sizeof(double), s));
-  HS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_tau), na * 3 * sizeof(double), s));
-  HS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_type), na * sizeof(int32_t), s));
-  HS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_rad), radial.size() * sizeof(double), s));
-  HS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_rmt), sys->n_types * sizeof(double), s));
-  HS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_un), sys->n_types * nlv * sizeof(double), s));
-  HS_CUDA(cudaMemcpyAsync(d_g, sys->gvec, sys->n_g * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
-  HS_CUDA(cudaMemcpyAsync(d_tau, sys->tau + 3 * a0, na * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
-  HS_CUDA(cudaMemcpyAsync(d_type, sys->atom_type + a0, na * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-  HS_CUDA(cudaMemcpyAsync(d_rad, radial.data(), radial.size() * sizeof(double), cudaMemcpyHostToDevice, s));
-  HS_CUDA(cudaMemcpyAsync(d_rmt, sys->rmt, sys->n_types * sizeof(double), cudaMemcpyHostToDevice, s));
-  HS_CUDA(cudaMemcpyAsync(d_un, sys->udot_norm, sys->n_types * nlv * sizeof(double), cudaMemcpyHostToDevice, s));
+  std::memcpy(rad + n_rad, sys->rmt, sys->n_types * sizeof(double));
+  std::memcpy(rad + n_rad + sys->n_types, sys->udot_norm, n_un * sizeof(double));
+  std::memcpy(rad + n_rad + sys->n_types + n_un, sys->atom_type + a0, na * sizeof(int32_t));
+  HS_CUDA(cudaMemcpyAsync(scratch, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  HS_CUDA(cudaStreamSynchronize(s));  // h is pageable and goes out of scope
+  double* d = static_cast<double*>(scratch);
   LapwDevParams P;
-  P.gvec = d_g;
-  P.tau = d_tau;
-  P.type = d_type;
-  P.radial = d_rad;
-  P.rmt = d_rmt;
+  P.gvec = d;
+  P.tau = d + n_g3;
+  P.radial = d + n_g3 + n_t3;
+  P.rmt = d + n_g3 + n_t3 + n_rad;
+  const double* d_un = P.rmt + sys->n_types;
+  P.type = reinterpret_cast<const int32_t*>(d_un + n_un);
   P.kx = sys->kpt[0];
   P.ky = sys->kpt[1];
   P.kz = sys->kpt[2];
@@ -775,10 +785,8 @@ static void lapw_enqueue(const hsdla_b200_lapw* sys, uint64_t a0, uint64_t na, d
   HS_CUDA(cudaGetLastError());
   if (ev1) HS_CUDA(cudaEventRecord(ev1, s));
   const int rows = static_cast<int>(na * nl);
-  lapw_u_kernel<<<(rows + 255) / 256, 256, 0, s>>>(d_type, d_un, sys->lmax, static_cast<int>(na), U);
+  lapw_u_kernel<<<(rows + 255) / 256, 256, 0, s>>>(P.type, d_un, sys->lmax, static_cast<int>(na), U);
   HS_CUDA(cudaGetLastError());
-  for (void* p : {(void*)d_g, (void*)d_tau, (void*)d_type, (void*)d_rad, (void*)d_rmt, (void*)d_un})
-    HS_CUDA(cudaFreeAsync(p, s));
 }
 
 static void engine_setup_lapw(hsdla_b200_engine* e, const hsdla_b200_lapw* sys, uint64_t a0) {
@@ -787,7 +795,16 @@ static void engine_setup_lapw(hsdla_b200_engine* e, const hsdla_b200_lapw* sys, 
   if (nlv * nlv != e->nl || sys->n_g != e->ng || a0 + e->na > sys->n_atoms)
     throw Fail{HSDLA_B200_DIMENSION_ERROR, "lapw system does not match the engine shard"};
   HS_CUDA(cudaSetDevice(e->device));
-  lapw_enqueue(sys, a0, e->na, e->A, e->B, e->K, e->U, e->stream, e->ev_setup0, e->ev_setup1);
+  const size_t need = lapw_scratch_size(sys, e->na);
+  if (need > e->lapw_scratch_bytes) {
+    HS_CUDA(cudaStreamSynchronize(e->stream));
+    if (e->lapw_scratch) HS_CUDA(cudaFree(e->lapw_scratch));
+    e->lapw_scratch = nullptr;
+    e->lapw_scratch_bytes = 0;
+    HS_CUDA(cudaMalloc(&e->lapw_scratch, need));
+    e->lapw_scratch_bytes = need;
+  }
+  lapw_enqueue(sys, a0, e->na, e->A, e->B, e->K, e->U, e->lapw_scratch, e->stream, e->ev_setup0, e->ev_setup1);
   e->setup_bytes = 2 * e->K * e->ng * sizeof(double2);
 }
 
@@ -1057,13 +1074,14 @@ int hsdla_b200_lapw_coefficients(int device, const hsdla_b200_lapw* sys, double*
       ~Buf() {
         if (p) cudaFree(p);
       }
-    } dA, dB, dU;
+    } dA, dB, dU, dS;
+    HS_CUDA(cudaMalloc(&dS.p, lapw_scratch_size(sys, sys->n_atoms)));
     HS_CUDA(cudaMalloc(&dA.p, K * sys->n_g * sizeof(double2)));
     HS_CUDA(cudaMalloc(&dB.p, K * sys->n_g * sizeof(double2)));
     HS_CUDA(cudaMalloc(&dU.p, K * sizeof(double)));
     cudaStream_t s = 0;
     lapw_enqueue(sys, 0, sys->n_atoms, static_cast<double2*>(dA.p), static_cast<double2*>(dB.p), K,
-                 static_cast<double*>(dU.p), s, nullptr, nullptr);
+                 static_cast<double*>(dU.p), dS.p, s, nullptr, nullptr);
     HS_CUDA(cudaMemcpy(A, dA.p, K * sys->n_g * sizeof(double2), cudaMemcpyDeviceToHost));
     HS_CUDA(cudaMemcpy(B, dB.p, K * sys->n_g * sizeof(double2), cudaMemcpyDeviceToHost));
     HS_CUDA(cudaMemcpy(U, dU.p, K * sizeof(double), cudaMemcpyDeviceToHost));
