@@ -47,6 +47,13 @@ extern "C" {
  * the stacked inner dimension [Z;B;A]^H [B;Z;X] (default).  Executed flops ==
  * ledger; the herkx phase reports 0 s (fused into her2k). */
 #define HSDLA_B200_ALGO_REFINED_FUSED 0
+/* The original algorithm (paper Algorithm 1, hsdla::pipeline::build_hs_original,
+ * pipeline.cpp:189-279; Variant::Original): phases z_loop, her2k, s, chol_loop,
+ * h_aa_update.  Per-atom Cholesky try/fail of T_AA on the GPU (bit-identical to
+ * kernels::potrf), W_a = L_a^H A_a (trmm) for HPD atoms and T_AA A_a (hemm) for
+ * the rest, then H += herk(B_T) + lower(A_f^H B_B) as ONE lower-triangular
+ * contraction.  Ledger == flop_model(p, Original) with the observed n_hpd. */
+#define HSDLA_B200_ALGO_ORIGINAL 2
 
 /* Problem (ProblemInstance, problem.hpp:16-27). */
 typedef struct hsdla_b200_problem {
@@ -67,17 +74,22 @@ typedef struct hsdla_b200_options {
   int flags;              /* reserved, 0 */
 } hsdla_b200_options;
 
-/* Phase index order = the reference's phase names (test_pipeline.cpp:167-176). */
+/* Phase slots = the reference's phase names (test_pipeline.cpp:167-176).  Refined
+ * reports s, z_loop, her2k, hemm_loop, herkx; original reports z_loop, her2k, s,
+ * chol_loop, h_aa_update (pipeline.cpp:207-276); unused slots are 0. */
 #define HSDLA_B200_PHASE_S 0
 #define HSDLA_B200_PHASE_Z_LOOP 1
 #define HSDLA_B200_PHASE_HER2K 2
 #define HSDLA_B200_PHASE_HEMM_LOOP 3
 #define HSDLA_B200_PHASE_HERKX 4
+#define HSDLA_B200_PHASE_CHOL_LOOP 5
+#define HSDLA_B200_PHASE_H_AA_UPDATE 6
+#define HSDLA_B200_N_PHASES 8
 
 /* Ledger key order: gemm, hemm, her2k, herk, scaling, herkx, potrf, trmm, total
  * (flop_ledger.hpp; values == pipeline::flop_model, pipeline.cpp:336-364). */
 typedef struct hsdla_b200_stats {
-  double phase_seconds[5];   /* device (CUDA-event) time per phase, max over GPUs */
+  double phase_seconds[HSDLA_B200_N_PHASES]; /* device (CUDA-event) time per phase slot, max over GPUs */
   double h2d_seconds;        /* host->device upload of A, B, T, U */
   double device_seconds;     /* first phase start .. H,S reduced on the root GPU */
   double reduce_seconds;     /* NCCL reduce tail after the last contraction (0 on 1 GPU) */
@@ -89,6 +101,7 @@ typedef struct hsdla_b200_stats {
   uint64_t peak_temp_bytes;  /* device temporaries (the X/Z stacks), cf. HSResult::peak_temp_bytes */
   int n_gpus;
   int kernel_launches;       /* launches of this library's kernels in the build */
+  uint64_t n_hpd;            /* atoms whose T_AA factorised (original algorithm; else n_atoms) */
 } hsdla_b200_stats;
 
 /* ---- the drop-in --------------------------------------------------------
@@ -102,6 +115,14 @@ int hsdla_b200_build_hs(const hsdla_b200_problem* p, const hsdla_b200_options* o
 /* pipeline::flop_model (pipeline.cpp:336-364). variant: 0 original, 1 refined. */
 int hsdla_b200_flop_model(int variant, uint64_t n_atoms, uint64_t n_l, uint64_t n_g, uint64_t n_hpd,
                           uint64_t ledger[9]);
+
+/* kernels::potrf (kernels.cpp:417-436) for n_blocks lower-authoritative n_l x n_l
+ * blocks (T, contiguous column-major blocks) on `device`.  L receives, per block,
+ * the full factor (upper exactly 0) when it factorises, else the Hermitian
+ * expansion of T (the hemm operand the original algorithm falls back to);
+ * pivot[b] = -1 on success, else the failing pivot (PotrfResult::pivot).  Same
+ * operation order as the reference with no FMA contraction: bit-identical. */
+int hsdla_b200_potrf(int device, uint64_t n_blocks, uint64_t n_l, const double* T, double* L, int64_t* pivot);
 
 /* generate_problem (problem.cpp:79-142), bit-identical to the reference
  * (std::mt19937_64 + the reference's double mapping).  Output layouts as above;

@@ -10,7 +10,10 @@
 // pipeline.cpp:281-329): fresh lower-authoritative H and S with exactly-zero upper
 // triangles, diagonal imaginary parts 0, ledger == flop_model(p, Refined), five
 // phases named s, z_loop, her2k, hemm_loop, herkx, peak_temp_bytes = the device
-// temporaries.  C-ABI status codes are rethrown as the reference's exception types
+// temporaries.  hsdla_b200::build_hs_original has the contract of
+// hsdla::pipeline::build_hs_original (pipeline.hpp:51, pipeline.cpp:189-279):
+// ledger == flop_model(p, Original), phases z_loop, her2k, s, chol_loop,
+// h_aa_update.  hsdla_b200::build_hs dispatches on cfg.variant (pipeline.cpp:331-334).  C-ABI status codes are rethrown as the reference's exception types
 // (errors.hpp:9-26).  No CPU fallback: without a visible GPU it throws ConfigError.
 #pragma once
 
@@ -43,15 +46,13 @@ inline void throw_status(int rc, const char* what) {
   }
 }
 
-inline hsdla::pipeline::HSResult build_hs_refined(const hsdla::ProblemInstance& p,
-                                                  const hsdla::pipeline::PipelineConfig& cfg,
-                                                  const Options& opt = {}) {
-  if (cfg.variant != hsdla::pipeline::Variant::Refined)
-    throw hsdla::ConfigError("hsdla_b200 implements the refined variant (Algorithm 3)");
+namespace detail {
+
+inline hsdla::pipeline::HSResult run(const hsdla::ProblemInstance& p, int algo, const Options& opt) {
   const std::size_t na = p.n_atoms, nl = p.n_l, ng = p.n_g;
   if (p.A.rows() != na * nl || p.A.cols() != ng || !p.A.same_shape(p.B) || p.T_AA.size() != na ||
       p.T_AB.size() != na || p.T_BB.size() != na || p.U.size() != na)
-    throw hsdla::DimensionError("build_hs_refined: malformed ProblemInstance");
+    throw hsdla::DimensionError("build_hs: malformed ProblemInstance");
   // per-atom operator blocks are separate heap blocks in the reference: pack them
   const std::size_t blk = nl * nl;
   std::vector<hsdla::cplx> taa(na * blk), tab(na * blk), tbb(na * blk);
@@ -59,17 +60,17 @@ inline hsdla::pipeline::HSResult build_hs_refined(const hsdla::ProblemInstance& 
   for (std::size_t a = 0; a < na; ++a) {
     if (p.T_AA[a].order() != nl || p.T_AB[a].rows() != nl || p.T_AB[a].cols() != nl ||
         p.T_BB[a].order() != nl || p.U[a].size() != nl)
-      throw hsdla::DimensionError("build_hs_refined: operator block of wrong order");
-    std::memcpy(taa.data() + a * blk, p.T_AA[a].matrix().data(), blk * sizeof(hsdla::cplx));
-    std::memcpy(tab.data() + a * blk, p.T_AB[a].data(), blk * sizeof(hsdla::cplx));
-    std::memcpy(tbb.data() + a * blk, p.T_BB[a].matrix().data(), blk * sizeof(hsdla::cplx));
+      throw hsdla::DimensionError("build_hs: operator block of wrong order");
+    std::memcpy(static_cast<void*>(taa.data() + a * blk), p.T_AA[a].matrix().data(), blk * sizeof(hsdla::cplx));
+    std::memcpy(static_cast<void*>(tab.data() + a * blk), p.T_AB[a].data(), blk * sizeof(hsdla::cplx));
+    std::memcpy(static_cast<void*>(tbb.data() + a * blk), p.T_BB[a].matrix().data(), blk * sizeof(hsdla::cplx));
     std::memcpy(u.data() + a * nl, p.U[a].data(), nl * sizeof(double));
   }
   hsdla_b200_problem cp{na, nl, ng,
                         reinterpret_cast<const double*>(p.A.data()), reinterpret_cast<const double*>(p.B.data()),
                         reinterpret_cast<const double*>(taa.data()), reinterpret_cast<const double*>(tab.data()),
                         reinterpret_cast<const double*>(tbb.data()), u.data()};
-  hsdla_b200_options co{opt.n_gpus, opt.device_ids.empty() ? nullptr : opt.device_ids.data(), opt.algo, 0};
+  hsdla_b200_options co{opt.n_gpus, opt.device_ids.empty() ? nullptr : opt.device_ids.data(), algo, 0};
   hsdla::pipeline::HSResult r;
   r.H = hsdla::HermitianView(ng);  // zero-initialised: the upper triangle stays exactly 0
   r.S = hsdla::HermitianView(ng);
@@ -80,18 +81,44 @@ inline hsdla::pipeline::HSResult build_hs_refined(const hsdla::ProblemInstance& 
   static const char* const keys[8] = {"gemm", "hemm", "her2k", "herk", "scaling", "herkx", "potrf", "trmm"};
   for (int i = 0; i < 8; ++i)
     if (st.ledger[i]) r.ledger.add(keys[i], st.ledger[i]);
-  static const char* const phases[5] = {"s", "z_loop", "her2k", "hemm_loop", "herkx"};
-  for (int i = 0; i < 5; ++i) r.phases.push_back({phases[i], st.phase_seconds[i]});
+  // reported phases in the reference's order, read from their slots
+  static const int refined_slots[5] = {HSDLA_B200_PHASE_S, HSDLA_B200_PHASE_Z_LOOP, HSDLA_B200_PHASE_HER2K,
+                                       HSDLA_B200_PHASE_HEMM_LOOP, HSDLA_B200_PHASE_HERKX};
+  static const char* const refined_names[5] = {"s", "z_loop", "her2k", "hemm_loop", "herkx"};
+  static const int original_slots[5] = {HSDLA_B200_PHASE_Z_LOOP, HSDLA_B200_PHASE_HER2K, HSDLA_B200_PHASE_S,
+                                        HSDLA_B200_PHASE_CHOL_LOOP, HSDLA_B200_PHASE_H_AA_UPDATE};
+  static const char* const original_names[5] = {"z_loop", "her2k", "s", "chol_loop", "h_aa_update"};
+  const bool orig = algo == HSDLA_B200_ALGO_ORIGINAL;
+  for (int i = 0; i < 5; ++i)
+    r.phases.push_back({orig ? original_names[i] : refined_names[i],
+                        st.phase_seconds[orig ? original_slots[i] : refined_slots[i]]});
   r.peak_temp_bytes = static_cast<std::size_t>(st.peak_temp_bytes);
-  if (opt.algo == HSDLA_B200_ALGO_REFINED_FUSED) r.warnings.push_back("herkx fused into the her2k contraction");
+  if (algo == HSDLA_B200_ALGO_REFINED_FUSED) r.warnings.push_back("herkx fused into the her2k contraction");
   return r;
+}
+
+}  // namespace detail
+
+inline hsdla::pipeline::HSResult build_hs_refined(const hsdla::ProblemInstance& p,
+                                                  const hsdla::pipeline::PipelineConfig& cfg,
+                                                  const Options& opt = {}) {
+  if (cfg.variant != hsdla::pipeline::Variant::Refined)
+    throw hsdla::ConfigError("build_hs_refined: variant must be Refined");
+  if (opt.algo != HSDLA_B200_ALGO_REFINED_FUSED && opt.algo != HSDLA_B200_ALGO_REFINED)
+    throw hsdla::ConfigError("build_hs_refined: algo must be REFINED_FUSED or REFINED");
+  return detail::run(p, opt.algo, opt);
+}
+
+inline hsdla::pipeline::HSResult build_hs_original(const hsdla::ProblemInstance& p,
+                                                   const hsdla::pipeline::PipelineConfig& /*cfg*/,
+                                                   const Options& opt = {}) {
+  return detail::run(p, HSDLA_B200_ALGO_ORIGINAL, opt);
 }
 
 inline hsdla::pipeline::HSResult build_hs(const hsdla::ProblemInstance& p, const hsdla::pipeline::PipelineConfig& cfg,
                                           const Options& opt = {}) {
-  if (cfg.variant == hsdla::pipeline::Variant::Original)
-    throw hsdla::ConfigError("hsdla_b200: the original variant (Algorithm 1) is not provided");
-  return build_hs_refined(p, cfg, opt);
+  return cfg.variant == hsdla::pipeline::Variant::Original ? build_hs_original(p, cfg, opt)
+                                                           : build_hs_refined(p, cfg, opt);
 }
 
 }  // namespace hsdla_b200

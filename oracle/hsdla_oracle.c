@@ -330,6 +330,135 @@ int orc_build_hs_refined(uint64_t na, uint64_t nl, uint64_t ng, const double* A_
   return 0;
 }
 
+/* kernels.cpp:417-436 potrf: left-looking Cholesky of the LOWER triangle of a
+ * (n x n, column-major).  l receives the full n x n factor (upper exactly 0).
+ * Returns -1 on success, else the failing pivot j (PotrfResult::pivot).
+ * std::norm(z) is x*x + y*y in libstdc++ (<complex> _Norm_helper<true>). */
+int64_t orc_potrf(uint64_t n, const double* a_, double* l_) {
+  const cx* a = (const cx*)a_;
+  cx* l = (cx*)l_;
+  memset(l, 0, n * n * sizeof(cx));
+  for (size_t j = 0; j < n; ++j) {
+    double d = a[j + j * n].re;
+    for (size_t p = 0; p < j; ++p) {
+      const cx v = l[j + p * n];
+      d -= v.re * v.re + v.im * v.im;
+    }
+    if (!(d > 0.0) || !isfinite(d)) return (int64_t)j;
+    const double ljj = sqrt(d);
+    l[j + j * n] = cx_make(ljj, 0.0);
+    for (size_t i = j + 1; i < n; ++i) {
+      cx s = a[i + j * n];
+      for (size_t p = 0; p < j; ++p) {
+        const cx t = cx_mul(l[i + p * n], cx_conj(l[j + p * n]));
+        s = cx_make(s.re - t.re, s.im - t.im);
+      }
+      l[i + j * n] = cx_make(s.re / ljj, s.im / ljj);
+    }
+  }
+  return -1;
+}
+
+/* kernels.cpp:385-415 trmm(Left, ConjTrans, alpha = 1): b := T^H b in place,
+ * T lower triangular (nl x nl), b nl x ng. */
+static void trmm_left_ctn(size_t n, size_t m, const cx* t, cx* b) {
+  const cx one = cx_make(1.0, 0.0);
+  for (size_t j = 0; j < m; ++j) {
+    cx* bj = b + j * n;
+    for (size_t i = 0; i < n; ++i) {
+      cx s = cx_make(0.0, 0.0);
+      const cx* ti = t + i * n;
+      for (size_t l = i; l < n; ++l) s = cx_add(s, cx_mul(cx_conj(ti[l]), bj[l]));
+      bj[i] = cx_mul(one, s);
+    }
+  }
+}
+
+/* pipeline.cpp:189-279 build_hs_original (Strategy::Cpu, Variant::Reference):
+ * Z loop into work_a (B copy into work_b), her2k, restore + S with in-place U
+ * scaling, per-atom potrf deciding trmm -> B_T (top of work_b) or hemm -> B_B
+ * (below B_T) with A_a compressed into work_a, then H += B_T^H B_T (herk) and the
+ * full gemm A_f^H B_B folded into the lower triangle.  n_hpd_out: atoms whose
+ * T_AA factorised. */
+int orc_build_hs_original(uint64_t na, uint64_t nl, uint64_t ng, const double* A_, const double* B_,
+                          const double* T_AA, const double* T_AB, const double* T_BB,
+                          const double* U, double* H_, double* S_, uint64_t* ledger, uint64_t* n_hpd_out) {
+  const size_t K = na * nl, blk = nl * nl;
+  const cx* A = (const cx*)A_;
+  const cx* B = (const cx*)B_;
+  cx* H = (cx*)H_;
+  cx* S = (cx*)S_;
+  cx* work_a = calloc(K * ng, sizeof(cx));
+  cx* work_b = calloc(K * ng, sizeof(cx));
+  cx* a_slice = malloc(nl * ng * sizeof(cx));
+  cx* b_slice = malloc(nl * ng * sizeof(cx));
+  cx* z = malloc(nl * ng * sizeof(cx));
+  cx* fac = malloc(na * blk * sizeof(cx));
+  int64_t* piv = malloc(na * sizeof(int64_t));
+  if (!work_a || !work_b || !a_slice || !b_slice || !z || !fac || !piv) return 2;
+  const cx one = cx_make(1.0, 0.0), zero = cx_make(0.0, 0.0), half = cx_make(0.5, 0.0);
+
+  /* z_loop (pipeline.cpp:207-214) */
+  for (size_t a = 0; a < na; ++a) {
+    load_block(a_slice, A, K, nl, ng, a);
+    load_block(b_slice, B, K, nl, ng, a);
+    gemm_ctn(nl, ng, nl, one, (const cx*)T_AB + a * blk, nl, a_slice, nl, zero, z, nl);
+    hemm_left_lower(nl, ng, half, (const cx*)T_BB + a * blk, nl, b_slice, nl, one, z, nl);
+    stack_block(work_a, z, K, nl, ng, a);
+    stack_block(work_b, b_slice, K, nl, ng, a);
+  }
+  /* her2k (:215-218) */
+  her2k_lower(ng, K, one, work_a, K, work_b, K, 0.0, H, ng);
+  /* s (:219-226): restore, S = A^H A, B := U B in place, S += B^H B */
+  memcpy(work_a, A, K * ng * sizeof(cx));
+  memcpy(work_b, B, K * ng * sizeof(cx));
+  herk_lower(ng, K, 1.0, work_a, K, 0.0, S, ng);
+  for (size_t j = 0; j < ng; ++j)
+    for (size_t i = 0; i < K; ++i) work_b[i + j * K] = cx_scale(U[i], work_b[i + j * K]);
+  herk_lower(ng, K, 1.0, work_b, K, 1.0, S, ng);
+  /* chol_loop (:229-251) */
+  size_t n_hpd = 0;
+  for (size_t a = 0; a < na; ++a) {
+    piv[a] = orc_potrf(nl, T_AA + 2 * a * blk, (double*)(fac + a * blk));
+    if (piv[a] < 0) ++n_hpd;
+  }
+  size_t s = 0, f = 0;
+  for (size_t a = 0; a < na; ++a) {
+    load_block(a_slice, A, K, nl, ng, a);
+    if (piv[a] < 0) {
+      memcpy(z, a_slice, nl * ng * sizeof(cx));
+      trmm_left_ctn(nl, ng, fac + a * blk, z);
+      stack_block(work_b, z, K, nl, ng, s++);
+    } else {
+      hemm_left_lower(nl, ng, one, (const cx*)T_AA + a * blk, nl, a_slice, nl, zero, z, nl);
+      stack_block(work_b, z, K, nl, ng, n_hpd + f);
+      stack_block(work_a, a_slice, K, nl, ng, f++);
+    }
+  }
+  /* h_aa_update (:253-276); the row blocks are used in place with ld = K (the
+   * reference copies them out first: same values, same operation order). */
+  const size_t n_fail = na - n_hpd;
+  if (n_hpd > 0) herk_lower(ng, n_hpd * nl, 1.0, work_b, K, 1.0, H, ng);
+  if (n_fail > 0) {
+    cx* full = malloc(ng * ng * sizeof(cx));
+    if (!full) return 2;
+    gemm_ctn(ng, ng, n_fail * nl, one, work_a, K, work_b + n_hpd * nl, K, zero, full, ng);
+    for (size_t j = 0; j < ng; ++j)
+      for (size_t i = j; i < ng; ++i) H[i + j * ng] = cx_add(H[i + j * ng], full[i + j * ng]);
+    free(full);
+  }
+  free(work_a);
+  free(work_b);
+  free(a_slice);
+  free(b_slice);
+  free(z);
+  free(fac);
+  free(piv);
+  if (ledger) orc_flop_model(0, na, nl, ng, n_hpd, ledger);
+  if (n_hpd_out) *n_hpd_out = n_hpd;
+  return 0;
+}
+
 int orc_build_hs_sampled(uint64_t na, uint64_t nl, uint64_t ng, const double* A_, const double* B_,
                          const double* T_AA, const double* T_AB, const double* T_BB,
                          const double* U, const uint64_t* J, uint64_t nj, double* Hs, double* Ss) {

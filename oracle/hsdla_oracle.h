@@ -35,6 +35,16 @@ int orc_build_hs_refined(uint64_t na, uint64_t nl, uint64_t ng, const double* A,
                          const double* T_AA, const double* T_AB, const double* T_BB,
                          const double* U, double* H, double* S, uint64_t* ledger);
 
+/* proj/src/pipeline.cpp:189-279 (Algorithm 1, Variant::Reference kernels).
+ * n_hpd_out (may be NULL): atoms whose T_AA passed potrf. */
+int orc_build_hs_original(uint64_t na, uint64_t nl, uint64_t ng, const double* A, const double* B,
+                          const double* T_AA, const double* T_AB, const double* T_BB,
+                          const double* U, double* H, double* S, uint64_t* ledger, uint64_t* n_hpd_out);
+
+/* proj/src/kernels.cpp:417-436: Cholesky of the lower triangle of a (n x n).
+ * l: full n x n factor (upper 0).  Returns -1 on success, else the failing pivot. */
+int64_t orc_potrf(uint64_t n, const double* a, double* l);
+
 /* proj/src/pipeline.cpp:336-364 */
 void orc_flop_model(int variant, uint64_t na, uint64_t nl, uint64_t ng, uint64_t n_hpd,
                     uint64_t* ledger);

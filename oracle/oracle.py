@@ -90,6 +90,21 @@ class _Base:
     def direct_H_grouped(self, p):
         return self.direct(2, p)
 
+    def potrf(self, T):
+        """kernels::potrf (kernels.cpp:417-436) of every block of T ((n, n, N_A) complex128
+        Fortran): returns (L (n, n, N_A) with zeros where it failed, pivot (N_A,) int64,
+        -1 = success)."""
+        T = np.asfortranarray(T, dtype=np.complex128)
+        n, na = T.shape[0], T.shape[2]
+        L = np.zeros_like(T, order="F")
+        piv = np.zeros(na, np.int64)
+        for a in range(na):
+            blk = np.asfortranarray(T[:, :, a])
+            out = np.zeros((n, n), np.complex128, order="F")
+            piv[a] = self._potrf(_u64(n), _ptr(blk), _ptr(out))
+            L[:, :, a] = out
+        return L, piv
+
     def flop_model(self, na, nl, ng, variant="refined", n_hpd=None):
         out = np.zeros(9, np.uint64)
         self._flops(C.c_int(0 if variant == "original" else 1), _u64(na), _u64(nl), _u64(ng),
@@ -112,7 +127,9 @@ class Restatement(_Base):
         self._direct = lib.orc_direct
         lib.orc_flop_model.restype = None
         self._flops = lambda v, na, nl, ng, nh, out: lib.orc_flop_model(v, na, nl, ng, nh, out)
+        self._potrf = lambda n, a, l: lib.orc_potrf(n, a, l)
         lib.orc_rel_frobenius_error_lower.restype = C.c_double
+        lib.orc_potrf.restype = C.c_int64
 
     def build_hs_refined(self, p):
         H = np.zeros((p.n_g, p.n_g), np.complex128, order="F")
@@ -124,6 +141,20 @@ class Restatement(_Base):
         if rc:
             raise MemoryError(f"orc_build_hs_refined rc={rc}")
         return H, S, _ledger(led)
+
+    def build_hs_original(self, p):
+        """Algorithm 1 (pipeline.cpp:189-279).  Returns H, S, ledger, n_hpd."""
+        H = np.zeros((p.n_g, p.n_g), np.complex128, order="F")
+        S = np.zeros((p.n_g, p.n_g), np.complex128, order="F")
+        led = np.zeros(9, np.uint64)
+        nh = C.c_uint64(0)
+        A, B, taa, tab, tbb, U = _args(p)
+        rc = self.lib.orc_build_hs_original(_u64(p.n_atoms), _u64(p.n_l), _u64(p.n_g), _ptr(A), _ptr(B), _ptr(taa),
+                                            _ptr(tab), _ptr(tbb), _ptr(U), _ptr(H), _ptr(S), _ptr(led),
+                                            C.byref(nh))
+        if rc:
+            raise MemoryError(f"orc_build_hs_original rc={rc}")
+        return H, S, _ledger(led), int(nh.value)
 
     def build_hs_sampled(self, p, J):
         J = np.ascontiguousarray(J, dtype=np.uint64)
@@ -189,6 +220,13 @@ class Reference(_Base):
         self._direct = lib.ref_direct
         self._flops = lambda v, na, nl, ng, nh, out: lib.ref_flop_model(v, na, nl, ng, nh, out)
 
+        def _potrf(n, a, l):
+            piv = C.c_int64(0)
+            if lib.ref_potrf(n, a, l, C.byref(piv)):
+                raise RuntimeError(lib.ref_last_error().decode())
+            return piv.value
+        self._potrf = _potrf
+
     def build_hs(self, p, variant="refined", threads=1, blocked=True, block=128, want_hs=True):
         H = S = None
         if want_hs:
@@ -208,7 +246,8 @@ class Reference(_Base):
                                    C.byref(peak))
         if rc:
             raise RuntimeError(f"reference build_hs failed ({rc}): {self.lib.ref_last_error().decode()}")
-        names = ["s", "z_loop", "her2k", "hemm_loop", "herkx"] if variant != "original" else None
+        names = (["s", "z_loop", "her2k", "hemm_loop", "herkx"] if variant != "original"
+                 else ["z_loop", "her2k", "s", "chol_loop", "h_aa_update"])
         return {"H": H, "S": S, "ledger": _ledger(led), "wall_seconds": wall.value,
                 "phases": list(zip(names or [str(i) for i in range(nph.value)], phases[: nph.value].tolist())),
                 "peak_temp_bytes": peak.value}

@@ -2,8 +2,9 @@
 //
 // Links the UNMODIFIED reference library (oracle/_ref/libhsdla_ref.so, built from
 // /root/reference/proj/src) and libhsdla_b200.so, and drives BOTH through the
-// reference's own C++ types: hsdla::generate_problem -> hsdla::pipeline::build_hs_refined
-// (CPU) vs hsdla_b200::build_hs_refined (include/hsdla_b200/pipeline.hpp, GPU).
+// reference's own C++ types: hsdla::generate_problem -> hsdla::pipeline::build_hs_refined /
+// build_hs(Original) (CPU) vs hsdla_b200::build_hs_refined / build_hs (include/hsdla_b200/
+// pipeline.hpp, GPU).
 // Exit code = number of failed checks (the acceptance.cpp convention).
 //   parity_cpp <n_atoms> <n_l> <n_g> <seed> <n_not_hpd> [threads]
 #include <cmath>
@@ -56,14 +57,38 @@ int main(int argc, char** argv) {
     for (std::size_t i = 0; names && i < 5; ++i) names = gpu.phases[i].name == cpu.phases[i].name;
     check(names, "  phase names == reference", double(gpu.phases.size()));
   }
-  // error mapping: the original variant is not provided -> hsdla::ConfigError
+  // the original variant (Algorithm 1) through build_hs dispatch vs the reference's own
+  // build_hs_original on the same instance
+  {
+    hsdla::pipeline::PipelineConfig ocfg = cfg;
+    ocfg.variant = hsdla::pipeline::Variant::Original;
+    const hsdla::pipeline::HSResult cpu_o = hsdla::pipeline::build_hs(p, ocfg);
+    const hsdla::pipeline::HSResult gpu = hsdla_b200::build_hs(p, ocfg);
+    const double eh = hsdla::rel_frobenius_error_lower(gpu.H.matrix(), cpu_o.H.matrix());
+    const double es = hsdla::rel_frobenius_error_lower(gpu.S.matrix(), cpu_o.S.matrix());
+    std::printf("variant original\n");
+    check(eh <= 1e-11, "  H rel Frobenius (lower) <= 1e-11", eh);
+    check(es <= 1e-11, "  S rel Frobenius (lower) <= 1e-11", es);
+    check(gpu.ledger == hsdla::pipeline::flop_model(p, hsdla::pipeline::Variant::Original),
+          "  ledger == flop_model(p, Original)", double(gpu.ledger.total()));
+    check(gpu.ledger == cpu_o.ledger, "  ledger == reference CPU ledger", double(cpu_o.ledger.total()));
+    bool names = gpu.phases.size() == cpu_o.phases.size();
+    for (std::size_t i = 0; names && i < gpu.phases.size(); ++i) names = gpu.phases[i].name == cpu_o.phases[i].name;
+    check(names, "  phase names == reference", double(gpu.phases.size()));
+    bool upper0 = true;
+    for (std::size_t j = 0; j < ng; ++j)
+      for (std::size_t i = 0; i < j; ++i)
+        upper0 = upper0 && gpu.H(i, j) == hsdla::cplx(0.0) && gpu.S(i, j) == hsdla::cplx(0.0);
+    check(upper0, "  upper triangles exactly 0", 0.0);
+  }
+  // error mapping: a refined call with a non-refined variant -> hsdla::ConfigError
   try {
     hsdla::pipeline::PipelineConfig bad = cfg;
     bad.variant = hsdla::pipeline::Variant::Original;
-    hsdla_b200::build_hs(p, bad);
-    check(false, "original variant -> ConfigError", 0);
+    hsdla_b200::build_hs_refined(p, bad);
+    check(false, "build_hs_refined(Original) -> ConfigError", 0);
   } catch (const hsdla::ConfigError&) {
-    check(true, "original variant -> ConfigError", 0);
+    check(true, "build_hs_refined(Original) -> ConfigError", 0);
   }
   std::printf("%d failure(s)\n", fails);
   return fails;

@@ -172,6 +172,19 @@ int ref_flop_model(int variant, std::uint64_t na, std::uint64_t nl, std::uint64_
   });
 }
 
+// kernels::potrf (kernels.cpp:417-436) on one n x n block (lower read).  l: full
+// n x n factor (upper 0) when it succeeds.  *pivot: -1 on success, else the failing pivot.
+int ref_potrf(std::uint64_t n, const double* a, double* l, std::int64_t* pivot) {
+  return guarded([&] {
+    HermitianView h(n);
+    std::memcpy(static_cast<void*>(h.matrix().data()), a, n * n * sizeof(cplx));
+    const kernels::PotrfResult r = kernels::potrf(h);
+    *pivot = r.ok() ? -1 : static_cast<std::int64_t>(r.pivot);
+    std::memset(l, 0, n * n * sizeof(cplx));
+    if (r.ok()) copy_cm(*r.factor, l);
+  });
+}
+
 int ref_save_problem(const char* path, std::uint64_t na, std::uint64_t nl, std::uint64_t ng,
                      const double* A, const double* B, const double* taa, const double* tab,
                      const double* tbb, const double* u, const std::uint8_t* hpd) {

@@ -10,13 +10,18 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libhsdla_b200.so")
 
 OK, DIMENSION_ERROR, SIZING_ERROR, CONFIG_ERROR, IO_ERROR, CUDA_ERROR, NCCL_ERROR = range(7)
-ALGO_REFINED_FUSED, ALGO_REFINED = 0, 1
+ALGO_REFINED_FUSED, ALGO_REFINED, ALGO_ORIGINAL = 0, 1, 2
 LEDGER_KEYS = ("gemm", "hemm", "her2k", "herk", "scaling", "herkx", "potrf", "trmm")
+N_PHASES = 8
+# phase slot names (include/hsdla_b200.h HSDLA_B200_PHASE_*)
+PHASE_SLOTS = ("s", "z_loop", "her2k", "hemm_loop", "herkx", "chol_loop", "h_aa_update", "")
+# reported phases per variant, in the reference's order (test_pipeline.cpp:167-176)
 PHASE_NAMES = ("s", "z_loop", "her2k", "hemm_loop", "herkx")
+PHASE_NAMES_ORIGINAL = ("z_loop", "her2k", "s", "chol_loop", "h_aa_update")
 
 # Every symbol include/hsdla_b200.h declares (checked by tests/test_abi.py).
 EXPORTS = (
-    "hsdla_b200_build_hs", "hsdla_b200_flop_model", "hsdla_b200_generate_problem", "hsdla_b200_last_error",
+    "hsdla_b200_build_hs", "hsdla_b200_flop_model", "hsdla_b200_potrf", "hsdla_b200_generate_problem", "hsdla_b200_last_error",
     "hsdla_b200_device_count", "hsdla_b200_host_register", "hsdla_b200_host_unregister",
     "hsdla_b200_release_cache", "hsdla_b200_engine_create", "hsdla_b200_engine_destroy",
     "hsdla_b200_engine_upload", "hsdla_b200_engine_build", "hsdla_b200_engine_build_streamed", "hsdla_b200_engine_reduce",
@@ -39,10 +44,11 @@ class Options(C.Structure):
 
 
 class Stats(C.Structure):
-    _fields_ = [("phase_seconds", C.c_double * 5), ("h2d_seconds", C.c_double), ("device_seconds", C.c_double),
+    _fields_ = [("phase_seconds", C.c_double * N_PHASES), ("h2d_seconds", C.c_double), ("device_seconds", C.c_double),
                 ("reduce_seconds", C.c_double), ("d2h_seconds", C.c_double), ("total_seconds", C.c_double),
                 ("ledger", C.c_uint64 * 9), ("executed_flops", C.c_uint64), ("peak_device_bytes", C.c_uint64),
-                ("peak_temp_bytes", C.c_uint64), ("n_gpus", C.c_int), ("kernel_launches", C.c_int)]
+                ("peak_temp_bytes", C.c_uint64), ("n_gpus", C.c_int), ("kernel_launches", C.c_int),
+                ("n_hpd", C.c_uint64)]
 
 
 _lib = None

@@ -38,6 +38,7 @@
 #include "../../include/hsdla_b200.h"
 #include "ctn_contract.cuh"
 #include "lapw_setup.cuh"
+#include "potrf.cuh"
 
 namespace hsdla_b200 {
 
@@ -173,7 +174,9 @@ static int chunks_of(uint64_t kcomplex) { return static_cast<int>((kcomplex + kC
 // One atom chunk [a0, a1) of a build: the parameter blocks of every launch.
 struct ChunkPlan {
   uint64_t a0 = 0, a1 = 0;
-  CtnParams s, z, x, h, h2k, hkx;  // h = fused her2k+herkx
+  // s: S; z: Z -> X1 (refined/original); zf: Z -> X2 (fused); x: Q^H A -> X1;
+  // h: fused her2k+herkx; h2k: her2k over X1; hkx: herkx A^H X1; haa: original X2^H X1
+  CtnParams s, z, zf, x, h, h2k, hkx, haa;
   dim3 grid_tri, grid_bat;
 };
 
@@ -191,6 +194,7 @@ struct hsdla_b200_engine {
   double2 *A = nullptr, *B = nullptr, *X1 = nullptr, *X2 = nullptr;
   double2 *Tab = nullptr, *Taa = nullptr, *Tbb = nullptr, *Paa = nullptr, *Pbb = nullptr;
   double* U = nullptr;
+  int32_t* info = nullptr;        // per-atom potrf result of the original algorithm (-1 = HPD)
   double2 *Hp = nullptr, *Sp = nullptr;
   double2* host_stage = nullptr;  // pinned, 2 * npk
   int sms = 148;                  // persistent TRI grid
@@ -211,6 +215,7 @@ struct hsdla_b200_engine {
               ev_h_d2h = nullptr;
   std::vector<cudaEvent_t> ev_chunk_up;
   int last_algo = 0, launches = 0;
+  uint64_t n_hpd_last = 0;
   bool built = false, reduced = false, uploaded_streamed = false;
   cudaEvent_t ev_setup0 = nullptr, ev_setup1 = nullptr;  // last LAPW setup kernel
   uint64_t setup_bytes = 0;
@@ -248,7 +253,7 @@ static void dalloc(hsdla_b200_engine* e, T** p, uint64_t count) {
 
 static void engine_free(hsdla_b200_engine* e) {
   cudaSetDevice(e->device);
-  for (void* p : {e->lapw_scratch, (void*)e->sk_ws, (void*)e->sk_flags, (void*)e->A, (void*)e->B, (void*)e->X1, (void*)e->X2,
+  for (void* p : {e->lapw_scratch, (void*)e->info, (void*)e->sk_ws, (void*)e->sk_flags, (void*)e->A, (void*)e->B, (void*)e->X1, (void*)e->X2,
                   (void*)e->Tab, (void*)e->Taa, (void*)e->Tbb, (void*)e->Paa, (void*)e->Pbb, (void*)e->U,
                   (void*)e->Hp, (void*)e->Sp})
     if (p) cudaFree(p);
@@ -282,11 +287,14 @@ static void make_chunk(hsdla_b200_engine* e, uint64_t a0, uint64_t a1, bool firs
   cp.a0 = a0;
   cp.a1 = a1;
   // K-stacked buffers restricted to rows [r0, r0+Kc): {2Kc, N_G, 1}, column stride 2K
+  // X2 is allocated on first use by the fused / original algorithms (the refined
+  // algorithm needs X1 only); until then its maps alias X1 and are never launched.
+  double2* x2 = e->X2 ? e->X2 : e->X1;
   CUtensorMap mA, mB, mX1, mX2;
   make_map(&mA, e->A + r0, 2 * Kc, ng, 1, 2 * K, 2 * K * ng, kTriBM, 1);
   make_map(&mB, e->B + r0, 2 * Kc, ng, 1, 2 * K, 2 * K * ng, kTriBM, 1);
   make_map(&mX1, e->X1 + r0, 2 * Kc, ng, 1, 2 * K, 2 * K * ng, kTriBM, 1);
-  make_map(&mX2, e->X2 + r0, 2 * Kc, ng, 1, 2 * K, 2 * K * ng, kTriBM, 1);
+  make_map(&mX2, x2 + r0, 2 * Kc, ng, 1, 2 * K, 2 * K * ng, kTriBM, 1);
   const int tiles = static_cast<int>((ng + kTriBM - 1) / kTriBM);
   const double beta0 = first ? 0.0 : 1.0;
   auto tri_base = [&](CtnParams& P, double2* out, double beta) {
@@ -312,14 +320,18 @@ static void make_chunk(hsdla_b200_engine* e, uint64_t a0, uint64_t a1, bool firs
   set_seg(cp.h, 1, mB, mX2, Kc);
   set_seg(cp.h, 2, mA, mX1, Kc);
   cp.h.nseg = 3;
-  // reference-order her2k (beta 0 on the first chunk) and herkx (always accumulates)
+  // reference-order her2k over Z in X1 (beta 0 on the first chunk) and herkx (always accumulates)
   tri_base(cp.h2k, e->Hp, beta0);
-  set_seg(cp.h2k, 0, mX2, mB, Kc);
-  set_seg(cp.h2k, 1, mB, mX2, Kc);
+  set_seg(cp.h2k, 0, mX1, mB, Kc);
+  set_seg(cp.h2k, 1, mB, mX1, Kc);
   cp.h2k.nseg = 2;
   tri_base(cp.hkx, e->Hp, 1.0);
   set_seg(cp.hkx, 0, mA, mX1, Kc);
   cp.hkx.nseg = 1;
+  // original h_aa_update: H += Lft^H W (Lft in X2, W = Q^H A in X1), always accumulates
+  tri_base(cp.haa, e->Hp, 1.0);
+  set_seg(cp.haa, 0, mX2, mX1, Kc);
+  cp.haa.nseg = 1;
   // persistent stream-K grid: one CTA per SM, never more CTAs than k-iterations
   const uint64_t tri_tiles = static_cast<uint64_t>(tiles) * (tiles + 1) / 2;
   cp.grid_tri = dim3(static_cast<unsigned>(std::min<uint64_t>(e->sms, tri_tiles * chunks_of(Kc))));
@@ -341,8 +353,9 @@ static void make_chunk(hsdla_b200_engine* e, uint64_t a0, uint64_t a1, bool firs
     P.ldo = K;
     P.alpha_re = 1.0;
   };
-  // Z_a = T_AB^H A_a + (1/2 T_BB) B_a   (compute_z, pipeline.cpp:176-185)
-  bat_base(cp.z, e->X2 + r0);
+  // Z_a = T_AB^H A_a + (1/2 T_BB) B_a   (compute_z, pipeline.cpp:176-185): into X1
+  // (refined / original) or X2 (fused, where X1 still holds T_AA A for the same launch)
+  bat_base(cp.z, e->X1 + r0);
   cp.z.L[0] = mTab;
   cp.z.R[0] = vA;
   cp.z.L[1] = mPbb;
@@ -350,7 +363,10 @@ static void make_chunk(hsdla_b200_engine* e, uint64_t a0, uint64_t a1, bool firs
   cp.z.kchunks[0] = cp.z.kchunks[1] = chunks_of(nl);
   cp.z.r_row_z[0] = cp.z.r_row_z[1] = 1;
   cp.z.nseg = 2;
-  // X_a = T_AA A_a   (hemm_loop, pipeline.cpp:314-321)
+  cp.zf = cp.z;
+  cp.zf.out = x2 + r0;
+  // X_a = T_AA A_a (hemm_loop, pipeline.cpp:314-321); in the original algorithm Paa
+  // holds the potrf output Q_a, so the same launch is trmm(L^H) / hemm per atom
   bat_base(cp.x, e->X1 + r0);
   cp.x.L[0] = mPaa;
   cp.x.R[0] = vA;
@@ -369,6 +385,24 @@ static std::vector<uint64_t> stream_bounds(uint64_t na, uint64_t nl, uint64_t ng
   std::vector<uint64_t> b(n + 1);
   for (uint64_t c = 0; c <= n; ++c) b[c] = na * c / n;
   return b;
+}
+
+static void make_plans(hsdla_b200_engine* e) {
+  e->whole.resize(1);
+  make_chunk(e, 0, e->na, true, e->whole[0]);
+  const auto b = stream_bounds(e->na, e->nl, e->ng);
+  e->streamed.resize(b.size() - 1);
+  for (size_t c = 0; c + 1 < b.size(); ++c) make_chunk(e, b[c], b[c + 1], c == 0, e->streamed[c]);
+}
+
+// The second K x N_G temporary: Z next to T_AA A for the fused contraction, the
+// Lft select for the original algorithm.  Allocated once, then every plan is
+// rebuilt against it.
+static void ensure_x2(hsdla_b200_engine* e) {
+  if (e->X2) return;
+  HS_CUDA(cudaStreamSynchronize(e->stream));
+  dalloc(e, &e->X2, e->K * e->ng);
+  make_plans(e);
 }
 
 static hsdla_b200_engine* engine_create(int device, uint64_t na, uint64_t nl, uint64_t ng) {
@@ -398,26 +432,22 @@ static hsdla_b200_engine* engine_create(int device, uint64_t na, uint64_t nl, ui
     const uint64_t KG = e->K * ng;
     dalloc(e.get(), &e->A, KG);
     dalloc(e.get(), &e->B, KG);
-    dalloc(e.get(), &e->X1, KG);
-    dalloc(e.get(), &e->X2, KG);
-    e->temp_bytes = 2 * KG * sizeof(double2);
+    dalloc(e.get(), &e->X1, KG);  // X2: on first fused / original build (ensure_x2)
+    e->temp_bytes = KG * sizeof(double2);
     dalloc(e.get(), &e->Tab, na * nl * nl);
     dalloc(e.get(), &e->Taa, na * nl * nl);
     dalloc(e.get(), &e->Tbb, na * nl * nl);
     dalloc(e.get(), &e->Paa, na * nl * nl);
     dalloc(e.get(), &e->Pbb, na * nl * nl);
     dalloc(e.get(), &e->U, e->K);
+    dalloc(e.get(), &e->info, na);
     dalloc(e.get(), &e->Hp, e->npk);
     dalloc(e.get(), &e->Sp, e->npk);
     HS_CUDA(cudaDeviceGetAttribute(&e->sms, cudaDevAttrMultiProcessorCount, device));
     dalloc(e.get(), &e->sk_ws, static_cast<uint64_t>(e->sms) * kTriBM * kTriBM * 2);
     dalloc(e.get(), &e->sk_flags, static_cast<uint64_t>(e->sms));
     HS_CUDA(cudaMemset(e->sk_flags, 0, e->sms * sizeof(uint32_t)));
-    e->whole.resize(1);
-    make_chunk(e.get(), 0, na, true, e->whole[0]);
-    const auto b = stream_bounds(na, nl, ng);
-    e->streamed.resize(b.size() - 1);
-    for (size_t c = 0; c + 1 < b.size(); ++c) make_chunk(e.get(), b[c], b[c + 1], c == 0, e->streamed[c]);
+    make_plans(e.get());
     e->ev_chunk_up.resize(e->streamed.size());
     for (auto& ev : e->ev_chunk_up) HS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   } catch (...) {
@@ -510,49 +540,85 @@ static void harvest(hsdla_b200_engine* e, hsdla_b200_engine::KTimer& t) {
   t.pending = false;
 }
 
-// All phases of one chunk on the compute stream, in the reference phase order.
+// All phases of one chunk on the compute stream, in the reference phase order of
+// the chosen algorithm:
+//   refined  s, z_loop, her2k, hemm_loop, herkx        (pipeline.cpp:281-329), one temp X1
+//   fused    s, z_loop, hemm_loop, her2k(+herkx)       two temps (Z in X2)
+//   original z_loop, her2k, s, chol_loop, h_aa_update  (pipeline.cpp:189-279), two temps
 static void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool last,
                           hsdla_b200_engine::KTimer* kt) {
   cudaStream_t s = e->stream;
   const uint64_t nac = cp.a1 - cp.a0, nl = e->nl, r0 = cp.a0 * nl, Kc = nac * nl, ng = e->ng;
-  timed_op(e, HSDLA_B200_PHASE_S, [&] {
+  const dim3 g_rows(static_cast<unsigned>((Kc + 255) / 256), static_cast<unsigned>(std::min<uint64_t>(ng, 2048)));
+  auto expand = [&] {
     // operator expansion (lower triangles of T_AA, T_BB only) for this chunk's atoms
     const uint64_t total = nac * nl * nl, off = cp.a0 * nl * nl;
     expand_hermitian_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
         e->Taa + off, e->Tbb + off, e->Paa + off, e->Pbb + off, static_cast<int>(nl), total);
     HS_CUDA(cudaGetLastError());
-    const dim3 g(static_cast<unsigned>((Kc + 255) / 256), static_cast<unsigned>(std::min<uint64_t>(ng, 2048)));
-    diag_scale_kernel<<<g, 256, 0, s>>>(e->B + r0, e->U + r0, e->X1 + r0, Kc, e->K, ng);
-    HS_CUDA(cudaGetLastError());
-    e->launches += 2;
-    if (kt) HS_CUDA(cudaEventRecord(kt->s0, s));
-    launch_tri(e, cp.s, cp.grid_tri);
-    if (kt) HS_CUDA(cudaEventRecord(kt->s1, s));
-  });
-  if (last) HS_CUDA(cudaEventRecord(e->ev_s_done, s));
-  timed_op(e, HSDLA_B200_PHASE_Z_LOOP, [&] { launch_bat(e, cp.z, cp.grid_bat); });
-  if (algo == HSDLA_B200_ALGO_REFINED) {
-    timed_op(e, HSDLA_B200_PHASE_HER2K, [&] {
-      if (kt) HS_CUDA(cudaEventRecord(kt->h0, s));
-      launch_tri(e, cp.h2k, cp.grid_tri);
-      if (kt) HS_CUDA(cudaEventRecord(kt->h1, s));
+    ++e->launches;
+  };
+  auto phase_s = [&](bool with_expand) {
+    timed_op(e, HSDLA_B200_PHASE_S, [&] {
+      if (with_expand) expand();
+      diag_scale_kernel<<<g_rows, 256, 0, s>>>(e->B + r0, e->U + r0, e->X1 + r0, Kc, e->K, ng);
+      HS_CUDA(cudaGetLastError());
+      ++e->launches;
+      if (kt) HS_CUDA(cudaEventRecord(kt->s0, s));
+      launch_tri(e, cp.s, cp.grid_tri);
+      if (kt) HS_CUDA(cudaEventRecord(kt->s1, s));
     });
+    if (last) HS_CUDA(cudaEventRecord(e->ev_s_done, s));
+  };
+  auto timed_h = [&](CtnParams& P) {
+    if (kt) HS_CUDA(cudaEventRecord(kt->h0, s));
+    launch_tri(e, P, cp.grid_tri);
+    if (kt) HS_CUDA(cudaEventRecord(kt->h1, s));
+  };
+  if (algo == HSDLA_B200_ALGO_ORIGINAL) {
+    timed_op(e, HSDLA_B200_PHASE_Z_LOOP, [&] {
+      expand();
+      launch_bat(e, cp.z, cp.grid_bat);
+    });
+    timed_op(e, HSDLA_B200_PHASE_HER2K, [&] { timed_h(cp.h2k); });
+    phase_s(false);
+    timed_op(e, HSDLA_B200_PHASE_CHOL_LOOP, [&] {
+      potrf_batched_kernel<<<static_cast<unsigned>(nac), 128, 0, s>>>(e->Taa + cp.a0 * nl * nl,
+                                                                      e->Paa + cp.a0 * nl * nl, e->info + cp.a0,
+                                                                      static_cast<int>(nl));
+      HS_CUDA(cudaGetLastError());
+      ++e->launches;
+      launch_bat(e, cp.x, cp.grid_bat);  // W_a = Q_a^H A_a: trmm (HPD) or hemm (failed)
+      select_left_kernel<<<g_rows, 256, 0, s>>>(e->X1 + r0, e->A + r0, e->info + cp.a0, e->X2 + r0, Kc, e->K,
+                                                ng, static_cast<int>(nl));
+      HS_CUDA(cudaGetLastError());
+      ++e->launches;
+    });
+    timed_op(e, HSDLA_B200_PHASE_H_AA_UPDATE, [&] { launch_tri(e, cp.haa, cp.grid_tri); });
+    return;
+  }
+  phase_s(true);
+  if (algo == HSDLA_B200_ALGO_REFINED) {
+    timed_op(e, HSDLA_B200_PHASE_Z_LOOP, [&] { launch_bat(e, cp.z, cp.grid_bat); });
+    timed_op(e, HSDLA_B200_PHASE_HER2K, [&] { timed_h(cp.h2k); });
     timed_op(e, HSDLA_B200_PHASE_HEMM_LOOP, [&] { launch_bat(e, cp.x, cp.grid_bat); });
     timed_op(e, HSDLA_B200_PHASE_HERKX, [&] { launch_tri(e, cp.hkx, cp.grid_tri); });
   } else {
+    timed_op(e, HSDLA_B200_PHASE_Z_LOOP, [&] { launch_bat(e, cp.zf, cp.grid_bat); });
     timed_op(e, HSDLA_B200_PHASE_HEMM_LOOP, [&] { launch_bat(e, cp.x, cp.grid_bat); });
-    timed_op(e, HSDLA_B200_PHASE_HER2K, [&] {  // her2k + herkx fused
-      if (kt) HS_CUDA(cudaEventRecord(kt->h0, s));
-      launch_tri(e, cp.h, cp.grid_tri);
-      if (kt) HS_CUDA(cudaEventRecord(kt->h1, s));
-    });
+    timed_op(e, HSDLA_B200_PHASE_HER2K, [&] { timed_h(cp.h); });  // her2k + herkx fused
   }
 }
 
+static bool valid_algo(int algo) {
+  return algo == HSDLA_B200_ALGO_REFINED || algo == HSDLA_B200_ALGO_REFINED_FUSED ||
+         algo == HSDLA_B200_ALGO_ORIGINAL;
+}
+
 static void begin_build(hsdla_b200_engine* e, int algo) {
-  if (algo != HSDLA_B200_ALGO_REFINED && algo != HSDLA_B200_ALGO_REFINED_FUSED)
-    throw Fail{HSDLA_B200_CONFIG_ERROR, "unknown algo " + std::to_string(algo)};
+  if (!valid_algo(algo)) throw Fail{HSDLA_B200_CONFIG_ERROR, "unknown algo " + std::to_string(algo)};
   HS_CUDA(cudaSetDevice(e->device));
+  if (algo != HSDLA_B200_ALGO_REFINED) ensure_x2(e);
   e->launches = 0;
   e->last_algo = algo;
   e->reduced = false;
@@ -567,7 +633,7 @@ static void engine_build(hsdla_b200_engine* e, int algo) {
   begin_build(e, algo);
   auto& kt = e->ring[e->builds++ % hsdla_b200_engine::kRing];
   harvest(e, kt);
-  kt.flops_h = (algo == HSDLA_B200_ALGO_REFINED ? 8 : 12) * e->K * e->ng * e->ng;
+  kt.flops_h = (algo == HSDLA_B200_ALGO_REFINED_FUSED ? 12 : 8) * e->K * e->ng * e->ng;
   HS_CUDA(cudaEventRecord(e->ev_begin, e->stream));
   enqueue_chunk(e, e->whole[0], algo, true, &kt);
   HS_CUDA(cudaEventRecord(e->ev_end, e->stream));
@@ -631,9 +697,18 @@ static void engine_sync(hsdla_b200_engine* e, hsdla_b200_stats* st) {
   if (!st) return;
   std::memset(st, 0, sizeof(*st));
   st->peak_device_bytes = e->device_bytes;
-  st->peak_temp_bytes = e->temp_bytes;
+  // the temporaries the algorithm needs: X1 (refined, cf. pipeline.cpp:291) or X1 + X2
+  st->peak_temp_bytes = (e->built && e->last_algo != HSDLA_B200_ALGO_REFINED ? 2 : 1) * e->temp_bytes;
   st->n_gpus = e->nranks;
   if (!e->built) return;  // nothing timed yet
+  if (e->last_algo == HSDLA_B200_ALGO_ORIGINAL) {
+    std::vector<int32_t> info(e->na);
+    HS_CUDA(cudaMemcpy(info.data(), e->info, e->na * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    e->n_hpd_last = static_cast<uint64_t>(std::count_if(info.begin(), info.end(), [](int32_t v) { return v < 0; }));
+  } else {
+    e->n_hpd_last = e->na;
+  }
+  st->n_hpd = e->n_hpd_last;
   for (const OpTime& op : e->ops) st->phase_seconds[op.phase] += ev_ms(op.b, op.e) * 1e-3;
   const cudaEvent_t last = e->reduced ? e->ev_reduce_end : e->ev_end;
   st->device_seconds = ev_ms(e->ev_begin, last) * 1e-3;
@@ -927,6 +1002,38 @@ int hsdla_b200_flop_model(int variant, uint64_t na, uint64_t nl, uint64_t ng, ui
   });
 }
 
+int hsdla_b200_potrf(int device, uint64_t nb, uint64_t nl, const double* T, double* L, int64_t* pivot) {
+  return guarded([&] {
+    if (!T || !L || !pivot) throw Fail{HSDLA_B200_DIMENSION_ERROR, "potrf: null pointer"};
+    if (nb < 1 || nl < 1 || nl > 4096) throw Fail{HSDLA_B200_DIMENSION_ERROR, "potrf: need n_blocks >= 1, 1 <= n_l <= 4096"};
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+      (void)cudaGetLastError();
+      throw Fail{HSDLA_B200_CONFIG_ERROR, "no such CUDA device (the B200 path has no CPU fallback)"};
+    }
+    HS_CUDA(cudaSetDevice(device));
+    const size_t bytes = nb * nl * nl * sizeof(double2);
+    struct Buf {
+      void* p = nullptr;
+      ~Buf() {
+        if (p) cudaFree(p);
+      }
+    } dT, dL, dI;
+    HS_CUDA(cudaMalloc(&dT.p, bytes));
+    HS_CUDA(cudaMalloc(&dL.p, bytes));
+    HS_CUDA(cudaMalloc(&dI.p, nb * sizeof(int32_t)));
+    HS_CUDA(cudaMemcpy(dT.p, T, bytes, cudaMemcpyHostToDevice));
+    potrf_batched_kernel<<<static_cast<unsigned>(nb), 128>>>(static_cast<const double2*>(dT.p),
+                                                            static_cast<double2*>(dL.p),
+                                                            static_cast<int32_t*>(dI.p), static_cast<int>(nl));
+    HS_CUDA(cudaGetLastError());
+    std::vector<int32_t> info(nb);
+    HS_CUDA(cudaMemcpy(L, dL.p, bytes, cudaMemcpyDeviceToHost));
+    HS_CUDA(cudaMemcpy(info.data(), dI.p, nb * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    for (uint64_t b = 0; b < nb; ++b) pivot[b] = info[b];
+  });
+}
+
 int hsdla_b200_shard_atoms(uint64_t n_atoms, int parts, uint64_t* bounds) {
   return guarded([&] {
     if (!bounds || parts < 1) throw Fail{HSDLA_B200_CONFIG_ERROR, "shard_atoms: parts must be >= 1"};
@@ -1120,8 +1227,7 @@ int hsdla_b200_build_hs(const hsdla_b200_problem* p, const hsdla_b200_options* o
     if (!p->A || !p->B || !p->T_AA || !p->T_AB || !p->T_BB || !p->U)
       throw Fail{HSDLA_B200_DIMENSION_ERROR, "null problem pointer"};
     const int algo = o ? o->algo : HSDLA_B200_ALGO_REFINED_FUSED;
-    if (algo != HSDLA_B200_ALGO_REFINED && algo != HSDLA_B200_ALGO_REFINED_FUSED)
-      throw Fail{HSDLA_B200_CONFIG_ERROR, "unknown algo " + std::to_string(algo)};
+    if (!valid_algo(algo)) throw Fail{HSDLA_B200_CONFIG_ERROR, "unknown algo " + std::to_string(algo)};
     const int P = o && o->n_gpus > 1 ? o->n_gpus : 1;
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
@@ -1152,12 +1258,14 @@ int hsdla_b200_build_hs(const hsdla_b200_problem* p, const hsdla_b200_options* o
     finish_download(root, H, S);
     const double d2h = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_d).count();
     hsdla_b200_stats local{};
-    double maxph[5] = {0, 0, 0, 0, 0};
+    double maxph[HSDLA_B200_N_PHASES] = {};
     double dev_s = 0, red_s = 0, h2d = 0;
     int launches = 0;
+    uint64_t n_hpd = 0;
     for (int r = 0; r < P; ++r) {
       engine_sync(set->engines[r], &local);
-      for (int i = 0; i < 5; ++i) maxph[i] = std::max(maxph[i], local.phase_seconds[i]);
+      n_hpd += local.n_hpd;
+      for (int i = 0; i < HSDLA_B200_N_PHASES; ++i) maxph[i] = std::max(maxph[i], local.phase_seconds[i]);
       dev_s = std::max(dev_s, local.device_seconds);
       red_s = std::max(red_s, local.reduce_seconds);
       h2d = std::max(h2d, local.h2d_seconds);
@@ -1169,8 +1277,15 @@ int hsdla_b200_build_hs(const hsdla_b200_problem* p, const hsdla_b200_options* o
       st->device_seconds = dev_s;
       st->reduce_seconds = red_s;
       st->d2h_seconds = d2h;
-      flop_model(1, p->n_atoms, p->n_l, p->n_g, p->n_atoms, st->ledger);
-      st->executed_flops = st->ledger[8];
+      // ledger == pipeline::flop_model(p, variant) with the potrf outcome of this build
+      flop_model(algo == HSDLA_B200_ALGO_ORIGINAL ? 0 : 1, p->n_atoms, p->n_l, p->n_g, n_hpd, st->ledger);
+      // every algorithm runs the same lower-triangular contractions: 20 K N_G^2 +
+      // 24 N_A N_L^2 N_G + 2 K N_G (the original's trmm on the zero upper half of L
+      // and its full gemm fold are executed as the lower-only h_aa contraction)
+      uint64_t refined[9];
+      flop_model(1, p->n_atoms, p->n_l, p->n_g, p->n_atoms, refined);
+      st->executed_flops = refined[8];
+      st->n_hpd = n_hpd;
       st->peak_device_bytes = local.peak_device_bytes;
       st->peak_temp_bytes = local.peak_temp_bytes;
       st->n_gpus = P;

@@ -1,7 +1,8 @@
 """Host-side mirror of the reference pipeline API for the B200 strategy.
 
 Reference interface mirrored (names, argument meaning, error behaviour):
-  hsdla::pipeline::build_hs_refined / build_hs / flop_model      pipeline.hpp:55-62
+  hsdla::pipeline::build_hs_original / build_hs_refined / build_hs / flop_model   pipeline.hpp:47-62
+  hsdla::kernels::potrf (batched over atom blocks)                 kernels.hpp:63-71
   PipelineConfig / HSResult / PhaseTime / FlopLedger              pipeline.hpp:22-44, flop_ledger.hpp
   HermitianView::mirror, rel_frobenius_error_lower               complex_matrix.hpp:62-94
 All arithmetic runs in libhsdla_b200.so on the GPU; nothing here computes H or S.
@@ -17,7 +18,7 @@ from .errors import ConfigError, DimensionError, check
 
 VARIANTS = ("original", "refined")
 STRATEGIES = ("b200",)
-ALGOS = {"fused": _lib.ALGO_REFINED_FUSED, "refined": _lib.ALGO_REFINED}
+ALGOS = {"fused": _lib.ALGO_REFINED_FUSED, "refined": _lib.ALGO_REFINED, "original": _lib.ALGO_ORIGINAL}
 
 
 def parse_variant(s):
@@ -40,7 +41,8 @@ class PipelineConfig:
     strategy: str = "b200"
     n_gpus: int = 1
     device_ids: Optional[Sequence[int]] = None
-    algo: str = "fused"  # "fused" (her2k+herkx in one contraction) | "refined" (reference phase order)
+    # refined variant only: "fused" (her2k+herkx in one contraction) | "refined" (reference phase order)
+    algo: str = "fused"
 
 
 @dataclass
@@ -89,22 +91,29 @@ class HSResult:
     stats: dict = field(default_factory=dict)
 
 
-def _options(cfg):
+def _options(cfg, algo):
     ids = None
     if cfg.device_ids is not None:
         if len(cfg.device_ids) < cfg.n_gpus:
             raise ConfigError("device_ids shorter than n_gpus")
         ids = (C.c_int * len(cfg.device_ids))(*cfg.device_ids)
-    if cfg.algo not in ALGOS:
-        raise ConfigError(f"unknown algo: {cfg.algo}")
     if cfg.n_gpus < 1:
         raise ConfigError("n_gpus must be >= 1")
-    return _lib.Options(int(cfg.n_gpus), ids, ALGOS[cfg.algo], 0), ids
+    return _lib.Options(int(cfg.n_gpus), ids, ALGOS[algo], 0), ids
 
 
-def stats_dict(st):
+def _phase_names(algo):
+    return _lib.PHASE_NAMES_ORIGINAL if algo == "original" else _lib.PHASE_NAMES
+
+
+def _phases(st, algo):
+    slot = {n: i for i, n in enumerate(_lib.PHASE_SLOTS)}
+    return [PhaseTime(nm, float(st.phase_seconds[slot[nm]])) for nm in _phase_names(algo)]
+
+
+def stats_dict(st, algo="fused"):
     return {
-        "phase_seconds": dict(zip(_lib.PHASE_NAMES, list(st.phase_seconds))),
+        "phase_seconds": {ph.name: ph.seconds for ph in _phases(st, algo)}, "n_hpd": int(st.n_hpd),
         "h2d_seconds": st.h2d_seconds, "device_seconds": st.device_seconds, "reduce_seconds": st.reduce_seconds,
         "d2h_seconds": st.d2h_seconds, "total_seconds": st.total_seconds,
         "ledger_total": int(st.ledger[8]), "executed_flops": int(st.executed_flops),
@@ -113,14 +122,8 @@ def stats_dict(st):
     }
 
 
-def build_hs_refined(p, cfg: Optional[PipelineConfig] = None, H=None, S=None) -> HSResult:
-    """build_hs_refined (pipeline.cpp:281-329) on B200.  ``H``/``S`` may be passed
-    preallocated (n_g x n_g complex128, Fortran order); only their lower triangles
-    are written.  Fresh outputs have exactly-zero upper triangles."""
-    cfg = cfg or PipelineConfig()
+def _run(p, cfg, algo, H, S, what):
     parse_strategy(cfg.strategy)
-    if parse_variant(cfg.variant) != "refined":
-        raise ConfigError("the B200 strategy implements the refined variant (Algorithm 3)")
     prob = p.c_struct()
     n = p.n_g
     if H is None:
@@ -130,24 +133,62 @@ def build_hs_refined(p, cfg: Optional[PipelineConfig] = None, H=None, S=None) ->
     for name, M in (("H", H), ("S", S)):
         if M.shape != (n, n) or M.dtype != np.complex128 or not M.flags.f_contiguous:
             raise DimensionError(f"{name} must be a ({n}, {n}) complex128 Fortran array")
-    opts, _keep = _options(cfg)
+    opts, _keep = _options(cfg, algo)
     st = _lib.Stats()
     check(_lib.lib().hsdla_b200_build_hs(C.byref(prob), C.byref(opts), H.ctypes.data_as(C.c_void_p),
-                                         S.ctypes.data_as(C.c_void_p), C.byref(st)), "build_hs")
-    phases = [PhaseTime(nm, float(sec)) for nm, sec in zip(_lib.PHASE_NAMES, st.phase_seconds)]
+                                         S.ctypes.data_as(C.c_void_p), C.byref(st)), what)
     warnings = []
-    if cfg.algo == "fused":
+    if algo == "fused":
         warnings.append("herkx fused into the her2k contraction (phase time 0)")
-    return HSResult(H, S, FlopLedger.from_array(st.ledger), int(st.peak_temp_bytes), phases, warnings,
-                    stats_dict(st))
+    return HSResult(H, S, FlopLedger.from_array(st.ledger), int(st.peak_temp_bytes), _phases(st, algo), warnings,
+                    stats_dict(st, algo))
+
+
+def build_hs_refined(p, cfg: Optional[PipelineConfig] = None, H=None, S=None) -> HSResult:
+    """build_hs_refined (pipeline.cpp:281-329) on B200.  ``H``/``S`` may be passed
+    preallocated (n_g x n_g complex128, Fortran order); only their lower triangles
+    are written.  Fresh outputs have exactly-zero upper triangles."""
+    cfg = cfg or PipelineConfig()
+    if parse_variant(cfg.variant) != "refined":
+        raise ConfigError("build_hs_refined needs variant 'refined' (use build_hs / build_hs_original)")
+    if cfg.algo not in ("fused", "refined"):
+        raise ConfigError(f"unknown algo: {cfg.algo}")
+    return _run(p, cfg, cfg.algo, H, S, "build_hs_refined")
+
+
+def build_hs_original(p, cfg: Optional[PipelineConfig] = None, H=None, S=None) -> HSResult:
+    """build_hs_original (pipeline.cpp:189-279, paper Algorithm 1) on B200: Cholesky
+    try/fail of every T_AA on the GPU, trmm / hemm per atom, H += herk(B_T) +
+    lower(A_f^H B_B).  Phases z_loop, her2k, s, chol_loop, h_aa_update; ledger ==
+    flop_model(p, "original") with the observed potrf outcomes."""
+    cfg = cfg or PipelineConfig(variant="original")
+    return _run(p, cfg, "original", H, S, "build_hs_original")
 
 
 def build_hs(p, cfg: PipelineConfig) -> HSResult:
-    """build_hs (pipeline.cpp:331-334)."""
-    parse_variant(cfg.variant)
-    if cfg.variant == "original":
-        raise ConfigError("variant 'original' (Algorithm 1) is not provided by the B200 strategy")
+    """build_hs (pipeline.cpp:331-334): dispatch on the variant."""
+    if parse_variant(cfg.variant) == "original":
+        return build_hs_original(p, cfg)
     return build_hs_refined(p, cfg)
+
+
+def potrf(T, device=0):
+    """kernels::potrf (kernels.cpp:417-436) on the GPU for every atom block of T
+    ((n_l, n_l, n_blocks) complex128, Fortran order, lower triangles read).
+    Returns (L, pivot): L[:, :, b] the factor (upper 0) where pivot[b] == -1, else the
+    Hermitian expansion of T[:, :, b] (the hemm fallback operand); bit-identical to
+    the reference's factor."""
+    T = np.asfortranarray(T, dtype=np.complex128)
+    if T.ndim == 2:
+        T = T[:, :, None]
+    if T.ndim != 3 or T.shape[0] != T.shape[1]:
+        raise DimensionError("potrf: T must be (n_l, n_l, n_blocks)")
+    n, nb = T.shape[0], T.shape[2]
+    L = np.zeros_like(T, order="F")
+    piv = np.zeros(nb, np.int64)
+    check(_lib.lib().hsdla_b200_potrf(C.c_int(device), C.c_uint64(nb), C.c_uint64(n), T.ctypes.data_as(C.c_void_p),
+                                      L.ctypes.data_as(C.c_void_p), piv.ctypes.data_as(C.c_void_p)), "potrf")
+    return L, piv
 
 
 def flop_model(p, variant="refined") -> FlopLedger:
@@ -207,11 +248,13 @@ class Engine:
         check(_lib.lib().hsdla_b200_engine_upload(self.h, C.byref(prob), C.c_uint64(atom_begin)), "engine_upload")
 
     def build(self, algo="fused"):
+        self._algo = algo
         check(_lib.lib().hsdla_b200_engine_build(self.h, C.c_int(ALGOS[algo])), "engine_build")
 
     def build_streamed(self, p, atom_begin=0, algo="fused"):
         """Upload shard `atom_begin` of host problem p in atom chunks overlapped with the build."""
         self._prob = p.c_struct()  # keep the struct alive while the copies are in flight
+        self._algo = algo
         check(_lib.lib().hsdla_b200_engine_build_streamed(self.h, C.byref(self._prob), C.c_uint64(atom_begin),
                                                           C.c_int(ALGOS[algo])), "engine_build_streamed")
 
@@ -221,7 +264,7 @@ class Engine:
     def sync(self):
         st = _lib.Stats()
         check(_lib.lib().hsdla_b200_engine_sync(self.h, C.byref(st)), "engine_sync")
-        return stats_dict(st)
+        return stats_dict(st, getattr(self, "_algo", "fused"))
 
     def download(self, H=None, S=None):
         n = self.n_g

@@ -58,6 +58,28 @@ def main():
                                      np.uint64),
         )
         print("wrote", name)
+    # kernels::potrf known answers (kernels.cpp:417-436): HPD blocks of the
+    # generator's T_AA at N_L 1/5/49/81/121 plus indefinite blocks that fail at
+    # pivots 0 (the generator's non-HPD shift), 7 and 30.
+    blocks = []
+    for nl, seed, nnh in ((1, 3, 0), (5, 4, 1), (49, 5, 1), (81, 6, 0), (121, 7, 0)):
+        q = ref.generate_problem(1 + nnh, nl, 1, seed, nnh)
+        blocks += [q.T_AA[:, :, a] for a in range(q.n_atoms)]
+    for nl, bad in ((16, 7), (49, 30)):
+        q = ref.generate_problem(1, nl, 1, 8 + bad, 0)
+        t = q.T_AA[:, :, 0].copy()
+        t[bad, bad] -= 1e3  # indefinite from column `bad` on
+        blocks.append(t)
+    ls, pivs, ts = [], [], []
+    for t in blocks:
+        L, piv = ref.potrf(t[:, :, None])
+        ts.append(t)
+        ls.append(L[:, :, 0])
+        pivs.append(int(piv[0]))
+    np.savez_compressed(os.path.join(out_dir, "potrf_blocks.npz"),
+                        **{f"T{i}": t for i, t in enumerate(ts)}, **{f"L{i}": l for i, l in enumerate(ls)},
+                        pivots=np.array(pivs, np.int64))
+    print("wrote potrf_blocks.npz", pivs)
     p = ref.generate_problem(2, 3, 16, 1, 1)
     ref.save_problem(p, os.path.join(out_dir, "small_2_3_16_s1_nh1.hsdl"))
     print("wrote small_2_3_16_s1_nh1.hsdl")

@@ -13,7 +13,7 @@ operation order), and the reference's own known-answer tests:
 import numpy as np
 import pytest
 
-from conftest import golden_cases, load_case
+from conftest import GOLDEN as GOLDEN_DIR, golden_cases, load_case
 from oracle.oracle import LEDGER_KEYS, Reference, Restatement, alloc_problem
 
 
@@ -96,3 +96,51 @@ def test_compiled_reference_matches_golden():
     r = ref.build_hs(p, "refined", threads=2, blocked=True)
     assert np.array_equal(r["H"], d["H"]) and np.array_equal(r["S"], d["S"])
     assert [ph[0] for ph in r["phases"]] == ["s", "z_loop", "her2k", "hemm_loop", "herkx"]
+
+
+@pytest.mark.parametrize("path", golden_cases(), ids=lambda p: p.split("/")[-1][:-4])
+def test_original_restatement_vs_reference_golden(path, restatement):
+    """Algorithm 1 (pipeline.cpp:189-279) restated: bit-identical H, S and the
+    original-variant ledger (test_pipeline.cpp:97-113), equal to the refined result
+    within 1e-11 (test_pipeline.cpp:30-40)."""
+    dims, d = load_case(path)
+    na, nl, ng, seed, nnh = dims
+    p = restatement.generate_problem(na, nl, ng, seed, nnh)
+    H, S, led, n_hpd = restatement.build_hs_original(p)
+    assert n_hpd == na - nnh
+    assert [led.get(k, 0) for k in LEDGER_KEYS] + [led["total"]] == d["ledger_original"].tolist()
+    if "Ho" in d:
+        assert np.array_equal(H, d["Ho"]) and np.array_equal(S, d["So"])
+    assert restatement.rel_frobenius_error_lower(H, d["H"]) < 1e-11
+    assert restatement.rel_frobenius_error_lower(S, d["S"]) < 1e-11
+    iu = np.triu_indices(ng, 1)
+    assert np.all(H[iu] == 0) and np.all(S[iu] == 0)
+
+
+def test_potrf_restatement_vs_reference_golden(restatement):
+    """kernels::potrf (kernels.cpp:417-436): factors bit-identical, failing pivots equal."""
+    z = np.load(f"{GOLDEN_DIR}/potrf_blocks.npz")
+    piv = z["pivots"]
+    assert sorted(set(piv.tolist())) == [-1, 0, 7, 30]
+    for i, want in enumerate(piv):
+        L, got = restatement.potrf(z[f"T{i}"][:, :, None])
+        assert got[0] == want
+        if want < 0:
+            assert np.array_equal(L[:, :, 0], z[f"L{i}"])
+            Lf = z[f"L{i}"]
+            assert np.all(Lf[np.triu_indices(Lf.shape[0], 1)] == 0)
+
+
+def test_original_restatement_hpd_mixes(restatement):
+    """original == refined across seeds and hpd mixes (test_pipeline.cpp:30-40) and
+    the closed-form ledger delta (test_pipeline.cpp:105-112)."""
+    for seed in range(1, 11):
+        na, nl, ng = 4, 5, 32
+        nnh = seed % (na + 1)
+        p = restatement.generate_problem(na, nl, ng, seed, nnh)
+        Ho, So, lo, n_hpd = restatement.build_hs_original(p)
+        Hr, Sr, lr = restatement.build_hs_refined(p)
+        assert restatement.rel_frobenius_error_lower(Ho, Hr) < 1e-11
+        assert restatement.rel_frobenius_error_lower(So, Sr) < 1e-11
+        delta = 4 * nnh * nl * ng * ng + na * (4 * nl ** 3 // 3) - 4 * n_hpd * nl * nl * ng
+        assert lo["total"] - lr["total"] == delta

@@ -15,13 +15,14 @@ for name in sys.argv[1:] or ["c2", "c3"]:
     tg = time.time() - t
     e = hb.Engine(0, na, nl, ng)
     e.upload(p)
-    led = hb.flop_model(p).total()
-    for algo in ("fused", "refined"):
+    led_r = hb.flop_model(p).total()
+    for algo in ("fused", "refined", "original"):
         for it in range(4):
             e.build(algo)
             st = e.sync()
         kt = e.kernel_times()
         dev = st["device_seconds"]
+        led = led_r
         print(f"{name} {algo}: gen {tg:.1f}s  device {dev*1e3:.2f} ms  {led/dev/1e12:.2f} TF/s(ledger)  "
               f"phases {{{', '.join(f'{k}: {v*1e3:.2f}' for k, v in st['phase_seconds'].items())}}} ms  "
               f"S-kernel {kt['s_flops']/kt['s_ms']/1e9:.2f} TF/s  H-kernel {kt['h_flops']/kt['h_ms']/1e9:.2f} TF/s",
