@@ -112,6 +112,18 @@ typedef struct hsdla_b200_stats {
 int hsdla_b200_build_hs(const hsdla_b200_problem* p, const hsdla_b200_options* opts, double* H,
                         double* S, hsdla_b200_stats* stats);
 
+/* ---- HSDL v1 problem files (problem.cpp:144-243) ---------------------------
+ * Header of a file written by the reference's save_problem: dims and, when hpd
+ * is non-NULL, n_atoms hpd flags.  Bad magic / version / truncation / missing
+ * file -> HSDLA_B200_IO_ERROR (load_problem's IoError, test_io.cpp:47-63). */
+int hsdla_b200_problem_file_info(const char* path, uint64_t* n_atoms, uint64_t* n_l, uint64_t* n_g, uint8_t* hpd);
+/* build_hs(load_problem(path), cfg) without a host ProblemInstance: every GPU
+ * streams only its atom shard (A/B rows of each column, T blocks, U) from the file
+ * into HBM through a pinned double buffer, then builds device-resident.  Same
+ * outputs / stats contract as hsdla_b200_build_hs (h2d_seconds = file load). */
+int hsdla_b200_build_hs_file(const char* path, const hsdla_b200_options* opts, double* H, double* S,
+                             hsdla_b200_stats* stats);
+
 /* pipeline::flop_model (pipeline.cpp:336-364). variant: 0 original, 1 refined. */
 int hsdla_b200_flop_model(int variant, uint64_t n_atoms, uint64_t n_l, uint64_t n_g, uint64_t n_hpd,
                           uint64_t ledger[9]);
@@ -153,6 +165,12 @@ int hsdla_b200_engine_create(int device, uint64_t n_atoms_local, uint64_t n_l, u
 int hsdla_b200_engine_destroy(hsdla_b200_engine* e);
 /* H2D of atoms [atom_begin, atom_begin + n_atoms_local) of p (p->n_atoms total). */
 int hsdla_b200_engine_upload(hsdla_b200_engine* e, const hsdla_b200_problem* p, uint64_t atom_begin);
+/* Stream atoms [atom_begin, atom_begin + n_atoms_local) of an HSDL v1 file into
+ * the engine (pinned double-buffered pread -> H2D on the copy stream). */
+int hsdla_b200_engine_load(hsdla_b200_engine* e, const char* path, uint64_t atom_begin);
+/* Device-side synthetic inputs for timing sweeps (A, B, T ~ U(-1,1), U ~ U(0.5,1.5),
+ * counter-based hash of `seed`; NOT the reference generator). */
+int hsdla_b200_engine_fill_synthetic(hsdla_b200_engine* e, uint64_t seed);
 /* Enqueue the full build (all phases) on the engine stream; asynchronous. */
 int hsdla_b200_engine_build(hsdla_b200_engine* e, int algo);
 /* Streamed build from HOST memory: uploads shard `atom_begin` of p in atom chunks on

@@ -48,6 +48,25 @@ inline void throw_status(int rc, const char* what) {
 
 namespace detail {
 
+inline void fill_result(hsdla::pipeline::HSResult& r, const hsdla_b200_stats& st, int algo) {
+  static const char* const keys[8] = {"gemm", "hemm", "her2k", "herk", "scaling", "herkx", "potrf", "trmm"};
+  for (int i = 0; i < 8; ++i)
+    if (st.ledger[i]) r.ledger.add(keys[i], st.ledger[i]);
+  // reported phases in the reference's order, read from their slots
+  static const int refined_slots[5] = {HSDLA_B200_PHASE_S, HSDLA_B200_PHASE_Z_LOOP, HSDLA_B200_PHASE_HER2K,
+                                       HSDLA_B200_PHASE_HEMM_LOOP, HSDLA_B200_PHASE_HERKX};
+  static const char* const refined_names[5] = {"s", "z_loop", "her2k", "hemm_loop", "herkx"};
+  static const int original_slots[5] = {HSDLA_B200_PHASE_Z_LOOP, HSDLA_B200_PHASE_HER2K, HSDLA_B200_PHASE_S,
+                                        HSDLA_B200_PHASE_CHOL_LOOP, HSDLA_B200_PHASE_H_AA_UPDATE};
+  static const char* const original_names[5] = {"z_loop", "her2k", "s", "chol_loop", "h_aa_update"};
+  const bool orig = algo == HSDLA_B200_ALGO_ORIGINAL;
+  for (int i = 0; i < 5; ++i)
+    r.phases.push_back({orig ? original_names[i] : refined_names[i],
+                        st.phase_seconds[orig ? original_slots[i] : refined_slots[i]]});
+  r.peak_temp_bytes = static_cast<std::size_t>(st.peak_temp_bytes);
+  if (algo == HSDLA_B200_ALGO_REFINED_FUSED) r.warnings.push_back("herkx fused into the her2k contraction");
+}
+
 inline hsdla::pipeline::HSResult run(const hsdla::ProblemInstance& p, int algo, const Options& opt) {
   const std::size_t na = p.n_atoms, nl = p.n_l, ng = p.n_g;
   if (p.A.rows() != na * nl || p.A.cols() != ng || !p.A.same_shape(p.B) || p.T_AA.size() != na ||
@@ -78,22 +97,7 @@ inline hsdla::pipeline::HSResult run(const hsdla::ProblemInstance& p, int algo, 
   throw_status(hsdla_b200_build_hs(&cp, &co, reinterpret_cast<double*>(r.H.matrix().data()),
                                    reinterpret_cast<double*>(r.S.matrix().data()), &st),
                "hsdla_b200_build_hs");
-  static const char* const keys[8] = {"gemm", "hemm", "her2k", "herk", "scaling", "herkx", "potrf", "trmm"};
-  for (int i = 0; i < 8; ++i)
-    if (st.ledger[i]) r.ledger.add(keys[i], st.ledger[i]);
-  // reported phases in the reference's order, read from their slots
-  static const int refined_slots[5] = {HSDLA_B200_PHASE_S, HSDLA_B200_PHASE_Z_LOOP, HSDLA_B200_PHASE_HER2K,
-                                       HSDLA_B200_PHASE_HEMM_LOOP, HSDLA_B200_PHASE_HERKX};
-  static const char* const refined_names[5] = {"s", "z_loop", "her2k", "hemm_loop", "herkx"};
-  static const int original_slots[5] = {HSDLA_B200_PHASE_Z_LOOP, HSDLA_B200_PHASE_HER2K, HSDLA_B200_PHASE_S,
-                                        HSDLA_B200_PHASE_CHOL_LOOP, HSDLA_B200_PHASE_H_AA_UPDATE};
-  static const char* const original_names[5] = {"z_loop", "her2k", "s", "chol_loop", "h_aa_update"};
-  const bool orig = algo == HSDLA_B200_ALGO_ORIGINAL;
-  for (int i = 0; i < 5; ++i)
-    r.phases.push_back({orig ? original_names[i] : refined_names[i],
-                        st.phase_seconds[orig ? original_slots[i] : refined_slots[i]]});
-  r.peak_temp_bytes = static_cast<std::size_t>(st.peak_temp_bytes);
-  if (algo == HSDLA_B200_ALGO_REFINED_FUSED) r.warnings.push_back("herkx fused into the her2k contraction");
+  fill_result(r, st, algo);
   return r;
 }
 
@@ -113,6 +117,26 @@ inline hsdla::pipeline::HSResult build_hs_original(const hsdla::ProblemInstance&
                                                    const hsdla::pipeline::PipelineConfig& /*cfg*/,
                                                    const Options& opt = {}) {
   return detail::run(p, HSDLA_B200_ALGO_ORIGINAL, opt);
+}
+
+/// build_hs(load_problem(path), cfg) with the HSDL v1 file (problem.cpp:144-243) streamed
+/// shard by shard straight into HBM: no host ProblemInstance.  IoError on a missing,
+/// malformed or truncated file (test_io.cpp:47-63).
+inline hsdla::pipeline::HSResult build_hs_file(const std::string& path, const hsdla::pipeline::PipelineConfig& cfg,
+                                               const Options& opt = {}) {
+  const int algo = cfg.variant == hsdla::pipeline::Variant::Original ? HSDLA_B200_ALGO_ORIGINAL : opt.algo;
+  uint64_t na = 0, nl = 0, ng = 0;
+  throw_status(hsdla_b200_problem_file_info(path.c_str(), &na, &nl, &ng, nullptr), "hsdla_b200_problem_file_info");
+  hsdla_b200_options co{opt.n_gpus, opt.device_ids.empty() ? nullptr : opt.device_ids.data(), algo, 0};
+  hsdla::pipeline::HSResult r;
+  r.H = hsdla::HermitianView(ng);
+  r.S = hsdla::HermitianView(ng);
+  hsdla_b200_stats st{};
+  throw_status(hsdla_b200_build_hs_file(path.c_str(), &co, reinterpret_cast<double*>(r.H.matrix().data()),
+                                        reinterpret_cast<double*>(r.S.matrix().data()), &st),
+               "hsdla_b200_build_hs_file");
+  detail::fill_result(r, st, algo);
+  return r;
 }
 
 inline hsdla::pipeline::HSResult build_hs(const hsdla::ProblemInstance& p, const hsdla::pipeline::PipelineConfig& cfg,

@@ -7,7 +7,10 @@
 // pipeline.hpp, GPU).
 // Exit code = number of failed checks (the acceptance.cpp convention).
 //   parity_cpp <n_atoms> <n_l> <n_g> <seed> <n_not_hpd> [threads]
+#include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <string>
 #include <cstdio>
 #include <cstdlib>
 
@@ -80,6 +83,24 @@ int main(int argc, char** argv) {
       for (std::size_t i = 0; i < j; ++i)
         upper0 = upper0 && gpu.H(i, j) == hsdla::cplx(0.0) && gpu.S(i, j) == hsdla::cplx(0.0);
     check(upper0, "  upper triangles exactly 0", 0.0);
+  }
+  // HSDL v1 file written by the reference's save_problem, streamed into HBM by the drop-in
+  {
+    const std::string path = "/tmp/hsdla_b200_parity_cpp.hsdl";
+    hsdla::save_problem(p, path);
+    const hsdla::pipeline::HSResult gpu = hsdla_b200::build_hs_file(path, cfg);
+    const double eh = hsdla::rel_frobenius_error_lower(gpu.H.matrix(), cpu.H.matrix());
+    const double es = hsdla::rel_frobenius_error_lower(gpu.S.matrix(), cpu.S.matrix());
+    std::printf("build_hs_file\n");
+    check(eh <= 1e-11 && es <= 1e-11, "  H, S rel Frobenius (lower) <= 1e-11", std::max(eh, es));
+    check(gpu.ledger == cpu.ledger, "  ledger == reference CPU ledger", double(cpu.ledger.total()));
+    std::remove(path.c_str());
+    try {
+      hsdla_b200::build_hs_file("/nonexistent/nowhere.hsdl", cfg);
+      check(false, "  missing file -> IoError", 0);
+    } catch (const hsdla::IoError&) {
+      check(true, "  missing file -> IoError", 0);
+    }
   }
   // error mapping: a refined call with a non-refined variant -> hsdla::ConfigError
   try {

@@ -29,7 +29,8 @@ EXPORTS = (
     "hsdla_b200_engine_stream", "hsdla_b200_nccl_unique_id", "hsdla_b200_engine_set_comm",
     "hsdla_b200_engine_kernel_times", "hsdla_b200_fp64_peak", "hsdla_b200_shard_atoms",
     "hsdla_b200_lapw_coefficients", "hsdla_b200_engine_setup_lapw", "hsdla_b200_engine_upload_operators",
-    "hsdla_b200_engine_setup_time",
+    "hsdla_b200_engine_setup_time", "hsdla_b200_problem_file_info", "hsdla_b200_build_hs_file",
+    "hsdla_b200_engine_load", "hsdla_b200_engine_fill_synthetic",
 )
 
 

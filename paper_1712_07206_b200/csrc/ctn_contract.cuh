@@ -51,6 +51,7 @@ struct alignas(64) CtnParams {
   int m_valid;             // BATCH: valid output rows per atom (N_L)
   int tiles;               // TRI: tiles per dimension
   int tiles_total;         // TRI: lower tiles t(t+1)/2
+  int band;                // TRI: tile-row band of the grouped tile order (>= 1)
   double2* out;            // TRI: packed lower.  BATCH: column-major stacked buffer
   double* sk_ws;           // TRI stream-K: per-CTA partial-accumulator slots
   uint32_t* sk_flags;      // TRI stream-K: per-CTA publish flags (== epoch when the slot is ready)
@@ -109,13 +110,33 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
       : "d"(a), "d"(b));
 }
 
-// Lower-tile index t -> (ti, tj), ti >= tj, tiles ordered row by row.
-__device__ __forceinline__ void tri_tile(int t, int& ti, int& tj) {
-  int r = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+// Lower-tile index t -> (ti, tj), ti >= tj, in an L2-friendly grouped order:
+// tile rows are taken in bands of kBand rows (kBand = 1: plain row-by-row order) (band b holds the same tiles as rows
+// [b*kBand, (b+1)*kBand) of the row-by-row order, so the band start is the
+// row-major prefix), and inside a band the tiles go column by column.  One wave of
+// 148 persistent CTAs then covers ~kBand row blocks x ~148/kBand column blocks of
+// the operands instead of 1 x 148, so each k-slab of an operand block is fetched
+// from HBM once per wave and re-served from L2 to the other CTAs of its band.
+__device__ __forceinline__ void tri_tile(int t, int tiles, int kBand, int& ti, int& tj) {
+  int r = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);  // row in the row-by-row order
   while ((r + 1) * (r + 2) / 2 <= t) ++r;
   while (r * (r + 1) / 2 > t) --r;
-  ti = r;
-  tj = t - r * (r + 1) / 2;
+  const int r0 = (r / kBand) * kBand;
+  const int h = min(kBand, tiles - r0);  // rows in this band
+  int u = t - r0 * (r0 + 1) / 2;         // index inside the band
+  if (u < r0 * h) {                      // rectangular part: columns 0 .. r0-1, h tiles each
+    tj = u / h;
+    ti = r0 + (u - tj * h);
+    return;
+  }
+  u -= r0 * h;  // triangular part: column c (tj = r0 + c) holds rows r0+c .. r0+h-1
+  int c = 0;
+  while (u >= h - c) {
+    u -= h - c;
+    ++c;
+  }
+  tj = r0 + c;
+  ti = r0 + c + u;
 }
 
 __device__ __forceinline__ uint64_t packed_index(uint64_t n, uint64_t i, uint64_t j) {
@@ -234,7 +255,7 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>
   auto tile_origin = [&](int tile, int& row0, int& col0, int& atom) {
     if (MODE == kTri) {
       int ti, tj;
-      tri_tile(tile, ti, tj);
+      tri_tile(tile, P.tiles, P.band, ti, tj);
       row0 = ti * BM;
       col0 = tj * BN;
       atom = 0;

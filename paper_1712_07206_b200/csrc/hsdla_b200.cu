@@ -20,12 +20,16 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
+#include <fcntl.h>
 #include <nccl.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -103,6 +107,21 @@ __global__ void diag_scale_kernel(const double2* __restrict__ B, const double* _
   }
 }
 
+// Counter-based synthetic fill (splitmix64 of (seed, index)) -> U(lo, hi): device-side
+// inputs for the large-N scaling sweep, where host generation of 10-50 GB would
+// dominate.  Not the reference generator (generate_problem is bit-identical on the
+// host); contraction timing does not depend on the values.
+__global__ void fill_uniform_kernel(double* __restrict__ p, uint64_t n, uint64_t seed, double lo, double hi) {
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint64_t z = seed * 0x9E3779B97F4A7C15ULL + i + 0x632BE59BD9B4E019ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    z ^= z >> 31;
+    p[i] = lo + (hi - lo) * static_cast<double>(z >> 11) * 0x1.0p-53;
+  }
+}
+
 // Hermitian expansion from the LOWER triangle (kernels.cpp:152-167 reads only
 // h[l*ldh+i] for l <= i and conj(h[i*ldh+l]) above):
 //   Pbb[a](k,i) = 1/2 * T_BB[a](k,i),  Paa[a](k,i) = T_AA[a](k,i)  (full Hermitian)
@@ -170,6 +189,17 @@ static auto tri_kernel = ctn_contract_kernel<kTri, kTriBM, kTriBM, 2, 4, kTriSta
 static auto bat_kernel = ctn_contract_kernel<kBatch, kBatBM, kBatBN, 1, 8, kBatStages>;
 
 static int chunks_of(uint64_t kcomplex) { return static_cast<int>((kcomplex + kChunkC - 1) / kChunkC); }
+
+// Tile-row band of the TRI tile order (ctn_contract.cuh tri_tile); HSDLA_B200_TRI_BAND
+// overrides it for tuning experiments.
+static int tri_band() {
+  static int band = [] {
+    const char* v = std::getenv("HSDLA_B200_TRI_BAND");
+    const int b = v ? std::atoi(v) : 8;
+    return b >= 1 ? b : 1;
+  }();
+  return band;
+}
 
 // One atom chunk [a0, a1) of a build: the parameter blocks of every launch.
 struct ChunkPlan {
@@ -302,6 +332,7 @@ static void make_chunk(hsdla_b200_engine* e, uint64_t a0, uint64_t a1, bool firs
     P.n = static_cast<int>(ng);
     P.tiles = tiles;
     P.tiles_total = tiles * (tiles + 1) / 2;
+    P.band = tri_band();
     P.out = out;
     P.sk_ws = e->sk_ws;
     P.sk_flags = e->sk_flags;
@@ -484,6 +515,22 @@ static void upload_atoms(hsdla_b200_engine* e, const hsdla_b200_problem* p, uint
   HS_CUDA(cudaMemcpyAsync(e->Tbb + b0 * blk, reinterpret_cast<const double2*>(p->T_BB) + t0, tbytes,
                           cudaMemcpyHostToDevice, s));
   HS_CUDA(cudaMemcpyAsync(e->U + r0, p->U + g0, rows * sizeof(double), cudaMemcpyHostToDevice, s));
+}
+
+static void engine_fill_synthetic(hsdla_b200_engine* e, uint64_t seed) {
+  HS_CUDA(cudaSetDevice(e->device));
+  const unsigned grid = static_cast<unsigned>(e->sms * 8);
+  auto fill = [&](void* ptr, uint64_t n, uint64_t salt, double lo, double hi) {
+    fill_uniform_kernel<<<grid, 256, 0, e->stream>>>(static_cast<double*>(ptr), n, seed * 16 + salt, lo, hi);
+    HS_CUDA(cudaGetLastError());
+  };
+  const uint64_t KG2 = 2 * e->K * e->ng, T2 = 2 * e->na * e->nl * e->nl;
+  fill(e->A, KG2, 1, -1.0, 1.0);
+  fill(e->B, KG2, 2, -1.0, 1.0);
+  fill(e->Taa, T2, 3, -1.0, 1.0);
+  fill(e->Tab, T2, 4, -1.0, 1.0);
+  fill(e->Tbb, T2, 5, -1.0, 1.0);
+  fill(e->U, e->K, 6, 0.5, 1.5);
 }
 
 static void engine_upload(hsdla_b200_engine* e, const hsdla_b200_problem* p, uint64_t a0) {
@@ -800,21 +847,25 @@ static void check_lapw(const hsdla_b200_lapw* sys) {
   }
 }
 
-// Bytes of device scratch the LAPW inputs of `na` atoms need (8-byte aligned parts).
-static size_t lapw_scratch_size(const hsdla_b200_lapw* sys, uint64_t na) {
+// Bytes of device scratch the LAPW inputs and per-G tables of `na` atoms need.
+static size_t lapw_tables_bytes(const hsdla_b200_lapw* sys, uint64_t na) {
   const size_t nlv = sys->lmax + 1;
-  return (sys->n_g * 3 + na * 3 + sys->n_types * nlv * 4 + sys->n_types + sys->n_types * nlv) * sizeof(double) +
-         ((na * sizeof(int32_t) + 7) & ~size_t(7));
+  return sys->n_g * (nlv * nlv + sys->n_types * nlv + na) * sizeof(double2);
+}
+static size_t lapw_inputs_bytes(const hsdla_b200_lapw* sys, uint64_t na) {
+  const size_t nlv = sys->lmax + 1;
+  return ((sys->n_g * 3 + na * 3 + sys->n_types * nlv * 4 + sys->n_types + sys->n_types * nlv) * sizeof(double) +
+          ((na * sizeof(int32_t) + 7) & ~size_t(7)) + 255) & ~size_t(255);
+}
+static size_t lapw_scratch_size(const hsdla_b200_lapw* sys, uint64_t na) {
+  return lapw_inputs_bytes(sys, na) + lapw_tables_bytes(sys, na);
 }
 
 // Compute A, B (ld = ldo rows) and U for atoms [a0, a0+na) of sys on stream s.
-// `scratch` (lapw_scratch_size bytes, device) receives the inputs; the host staging
-// is pinned so the small uploads are asynchronous.
+// `scratch` (lapw_scratch_size bytes, device) receives the inputs and the per-G tables.
 static void lapw_enqueue(const hsdla_b200_lapw* sys, uint64_t a0, uint64_t na, double2* A, double2* B, uint64_t ldo,
                          double* U, void* scratch, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
   const int nlv = sys->lmax + 1, nl = nlv * nlv;
-  const size_t shmem = (static_cast<size_t>(nl) + na + sys->n_types * nlv) * sizeof(double2) + nl + 16;
-  if (shmem > 200 * 1024) throw Fail{HSDLA_B200_SIZING_ERROR, "lapw: too many atoms per GPU shard for one column"};
   // pack [gvec | tau | radial(u,u',udot,udot') | rmt | udot_norm | type] into one host block
   const size_t n_g3 = sys->n_g * 3, n_t3 = na * 3, n_rad = sys->n_types * nlv * 4, n_un = sys->n_types * nlv;
   std::vector<double> h(n_g3 + n_t3 + n_rad + sys->n_types + n_un + (na * sizeof(int32_t) + 7) / 8);
@@ -854,9 +905,23 @@ static void lapw_enqueue(const hsdla_b200_lapw* sys, uint64_t a0, uint64_t na, d
   P.A = A;
   P.B = B;
   P.ldo = ldo;
-  HS_CUDA(cudaFuncSetAttribute(lapw_setup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(shmem)));
+  double2* tabY = reinterpret_cast<double2*>(static_cast<char*>(scratch) + lapw_inputs_bytes(sys, na));
+  double2* tabF = tabY + sys->n_g * nl;
+  double2* tabS = tabF + sys->n_g * sys->n_types * nlv;
+  int dev = 0, sms = 148;
+  HS_CUDA(cudaGetDevice(&dev));
+  HS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const uint64_t items = sys->n_g * (nlv + sys->n_types + na);
+  const unsigned tgrid = static_cast<unsigned>(std::min<uint64_t>((items + 255) / 256, static_cast<uint64_t>(sms) * 16));
   if (ev0) HS_CUDA(cudaEventRecord(ev0, s));
-  lapw_setup_kernel<<<static_cast<unsigned>(sys->n_g), 256, shmem, s>>>(P);
+  lapw_tables_kernel<<<tgrid, 256, 0, s>>>(P, tabY, tabF, tabS);
+  HS_CUDA(cudaGetLastError());
+  constexpr int kRows = 4;
+  const uint64_t K = na * nl;
+  const uint64_t row_blocks = (K + 256 * kRows - 1) / (256 * kRows);
+  if (row_blocks > 65535) throw Fail{HSDLA_B200_SIZING_ERROR, "lapw: too many rows (atoms x N_L) per GPU shard"};
+  const dim3 sgrid(static_cast<unsigned>(sys->n_g), static_cast<unsigned>(row_blocks));
+  lapw_stream_kernel<kRows><<<sgrid, 256, 0, s>>>(P, tabY, tabF, tabS);
   HS_CUDA(cudaGetLastError());
   if (ev1) HS_CUDA(cudaEventRecord(ev1, s));
   const int rows = static_cast<int>(na * nl);
@@ -895,6 +960,209 @@ static void engine_upload_operators(hsdla_b200_engine* e, const double* taa, con
                           e->stream));
   HS_CUDA(cudaMemcpyAsync(e->Tbb, reinterpret_cast<const double2*>(tbb) + a0 * blk, bytes, cudaMemcpyHostToDevice,
                           e->stream));
+}
+
+// ---------------------------------------------------------------------------
+// HSDL v1 problem files (reference problem.cpp:144-243) streamed straight into
+// the engine's device buffers: header parse, then the shard's rows of every
+// A / B column, its T_AA / T_AB / T_BB blocks and U, read with pread() by a few
+// host threads into a double-buffered pinned staging ring and copied to HBM on the
+// copy stream while the next slab is read.  No host ProblemInstance is built.
+// ---------------------------------------------------------------------------
+struct HsdlHeader {
+  uint64_t na = 0, nl = 0, ng = 0;
+  uint64_t off_flags = 32, off_A = 0, off_B = 0, off_T = 0, off_U = 0, total = 0;
+  std::vector<uint8_t> hpd;
+};
+
+struct Fd {
+  int fd = -1;
+  ~Fd() {
+    if (fd >= 0) close(fd);
+  }
+};
+
+static void pread_all(int fd, void* dst, size_t bytes, uint64_t off) {
+  char* p = static_cast<char*>(dst);
+  while (bytes) {
+    const ssize_t r = pread(fd, p, bytes, static_cast<off_t>(off));
+    if (r <= 0) throw Fail{HSDLA_B200_IO_ERROR, "problem file truncated"};  // problem.cpp:157-160
+    p += r;
+    bytes -= static_cast<size_t>(r);
+    off += static_cast<uint64_t>(r);
+  }
+}
+
+// problem.cpp:197-225: magic "HSDL", version 1, dims, hpd bit flags; checked_total.
+static HsdlHeader read_hsdl_header(int fd, const char* path) {
+  HsdlHeader h;
+  char magic[4];
+  uint32_t version = 0;
+  uint64_t dims[3];
+  pread_all(fd, magic, 4, 0);
+  if (std::memcmp(magic, "HSDL", 4) != 0) throw Fail{HSDLA_B200_IO_ERROR, std::string("bad magic: ") + path};
+  pread_all(fd, &version, 4, 4);
+  if (version != 1) throw Fail{HSDLA_B200_IO_ERROR, "unsupported format version " + std::to_string(version)};
+  pread_all(fd, dims, sizeof(dims), 8);
+  h.na = dims[0];
+  h.nl = dims[1];
+  h.ng = dims[2];
+  const uint64_t max = UINT64_MAX / 16 / 4;  // checked_total (problem.cpp:69-75)
+  if (h.nl != 0 && h.na > max / h.nl) throw Fail{HSDLA_B200_SIZING_ERROR, "n_atoms * n_l overflows"};
+  if (h.ng != 0 && h.na * h.nl > max / h.ng) throw Fail{HSDLA_B200_SIZING_ERROR, "problem allocation overflows"};
+  const uint64_t nflag = (h.na + 7) / 8;
+  std::vector<uint8_t> flags(nflag);
+  if (nflag) pread_all(fd, flags.data(), nflag, 32);
+  h.hpd.resize(h.na);
+  for (uint64_t a = 0; a < h.na; ++a) h.hpd[a] = (flags[a / 8] >> (a % 8)) & 1u;
+  const uint64_t KG = h.na * h.nl * h.ng * 16;
+  h.off_A = 32 + nflag;
+  h.off_B = h.off_A + KG;
+  h.off_T = h.off_B + KG;
+  h.off_U = h.off_T + h.na * 3 * h.nl * h.nl * 16;
+  h.total = h.off_U + h.na * h.nl * 8;
+  struct stat sb;
+  if (fstat(fd, &sb) != 0 || static_cast<uint64_t>(sb.st_size) < h.total)
+    throw Fail{HSDLA_B200_IO_ERROR, "problem file truncated"};
+  return h;
+}
+
+static int open_hsdl(const char* path) {
+  if (!path) throw Fail{HSDLA_B200_IO_ERROR, "null path"};
+  const int fd = open(path, O_RDONLY);
+  if (fd < 0) throw Fail{HSDLA_B200_IO_ERROR, std::string("cannot open: ") + path};
+  return fd;
+}
+
+// Staging ring of two pinned slabs; slab s is free again once its event fired.
+struct Staging {
+  static constexpr size_t kSlab = size_t(64) << 20;
+  char* buf[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  bool busy[2] = {false, false};
+  int next = 0;
+  Staging() {
+    for (int i = 0; i < 2; ++i) {
+      HS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&buf[i]), kSlab));
+      HS_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    }
+  }
+  ~Staging() {
+    for (int i = 0; i < 2; ++i) {
+      if (ev[i]) {
+        cudaEventSynchronize(ev[i]);
+        cudaEventDestroy(ev[i]);
+      }
+      if (buf[i]) cudaFreeHost(buf[i]);
+    }
+  }
+  char* acquire(int& slot) {
+    slot = next;
+    next ^= 1;
+    if (busy[slot]) HS_CUDA(cudaEventSynchronize(ev[slot]));
+    busy[slot] = true;
+    return buf[slot];
+  }
+  void release(int slot, cudaStream_t s) { HS_CUDA(cudaEventRecord(ev[slot], s)); }
+};
+
+// Read `n` pieces of `piece` bytes at offsets off0 + i*stride into dst (packed),
+// split over up to 8 threads.
+static void pread_pieces(int fd, char* dst, uint64_t off0, uint64_t stride, size_t piece, uint64_t n) {
+  const uint64_t bytes = piece * n;
+  const unsigned nt = bytes < (size_t(8) << 20) ? 1u : std::min<unsigned>(8, static_cast<unsigned>(n));
+  std::vector<std::thread> th;
+  std::vector<Fail> errs(nt);
+  std::vector<char> bad(nt, 0);
+  for (unsigned t = 0; t < nt; ++t) {
+    const uint64_t i0 = n * t / nt, i1 = n * (t + 1) / nt;
+    auto work = [&, t, i0, i1] {
+      try {
+        if (stride == piece) {
+          pread_all(fd, dst + i0 * piece, (i1 - i0) * piece, off0 + i0 * stride);
+        } else {
+          for (uint64_t i = i0; i < i1; ++i) pread_all(fd, dst + i * piece, piece, off0 + i * stride);
+        }
+      } catch (const Fail& f) {
+        errs[t] = f;
+        bad[t] = 1;
+      }
+    };
+    if (nt == 1)
+      work();
+    else
+      th.emplace_back(work);
+  }
+  for (auto& x : th) x.join();
+  for (unsigned t = 0; t < nt; ++t)
+    if (bad[t]) throw errs[t];
+}
+
+static void engine_load_file(hsdla_b200_engine* e, const char* path, uint64_t a0) {
+  Fd f;
+  f.fd = open_hsdl(path);
+  const HsdlHeader h = read_hsdl_header(f.fd, path);
+  if (h.nl != e->nl || h.ng != e->ng || a0 + e->na > h.na)
+    throw Fail{HSDLA_B200_DIMENSION_ERROR, "problem file shape does not match the engine shard"};
+  HS_CUDA(cudaSetDevice(e->device));
+  cudaStream_t s = e->copy_stream;
+  // nothing may overwrite A/B/T/U while a previous build still reads them
+  HS_CUDA(cudaStreamWaitEvent(s, e->ev_end, 0));
+  Staging st;
+  const uint64_t K = e->K, Kf = h.na * h.nl, g0 = a0 * h.nl, ng = h.ng;
+  const size_t colb = K * sizeof(double2);
+  const uint64_t cols = std::max<uint64_t>(1, Staging::kSlab / colb);
+  for (int m = 0; m < 2; ++m) {  // A then B: the shard's K rows of every column
+    const uint64_t base = (m == 0 ? h.off_A : h.off_B) + g0 * 16;
+    double2* dst = m == 0 ? e->A : e->B;
+    for (uint64_t j0 = 0; j0 < ng; j0 += cols) {
+      const uint64_t nc = std::min(cols, ng - j0);
+      if (colb > Staging::kSlab) {  // a single column larger than a slab: split rows
+        for (uint64_t j = j0; j < j0 + nc; ++j)
+          for (uint64_t r0 = 0; r0 < K; r0 += Staging::kSlab / 16) {
+            const uint64_t nr = std::min<uint64_t>(Staging::kSlab / 16, K - r0);
+            int slot;
+            char* b = st.acquire(slot);
+            pread_pieces(f.fd, b, base + (j * Kf + r0) * 16, nr * 16, nr * 16, 1);
+            HS_CUDA(cudaMemcpyAsync(dst + j * K + r0, b, nr * 16, cudaMemcpyHostToDevice, s));
+            st.release(slot, s);
+          }
+        continue;
+      }
+      int slot;
+      char* b = st.acquire(slot);
+      pread_pieces(f.fd, b, base + j0 * Kf * 16, Kf * 16, colb, nc);
+      HS_CUDA(cudaMemcpyAsync(dst + j0 * K, b, nc * colb, cudaMemcpyHostToDevice, s));
+      st.release(slot, s);
+    }
+  }
+  // operator blocks of atoms [a0, a0 + na): T_AA, T_AB, T_BB interleaved per atom in the file
+  const uint64_t blk = h.nl * h.nl * 16;
+  const uint64_t atoms_per = std::max<uint64_t>(1, Staging::kSlab / (3 * blk));
+  for (uint64_t b0 = 0; b0 < e->na; b0 += atoms_per) {
+    const uint64_t nb = std::min(atoms_per, e->na - b0);
+    if (3 * blk > Staging::kSlab) throw Fail{HSDLA_B200_SIZING_ERROR, "operator block larger than the staging slab"};
+    int slot;
+    char* b = st.acquire(slot);
+    pread_pieces(f.fd, b, h.off_T + (a0 + b0) * 3 * blk, 3 * blk, 3 * blk, nb);
+    double2* dsts[3] = {e->Taa, e->Tab, e->Tbb};
+    for (int m = 0; m < 3; ++m)
+      HS_CUDA(cudaMemcpy2DAsync(reinterpret_cast<char*>(dsts[m]) + b0 * blk, blk, b + m * blk, 3 * blk, blk, nb,
+                                cudaMemcpyHostToDevice, s));
+    st.release(slot, s);
+  }
+  {
+    int slot;
+    char* b = st.acquire(slot);
+    const size_t ub = e->na * h.nl * sizeof(double);
+    if (ub > Staging::kSlab) throw Fail{HSDLA_B200_SIZING_ERROR, "U larger than the staging slab"};
+    pread_pieces(f.fd, b, h.off_U + a0 * h.nl * sizeof(double), ub, ub, 1);
+    HS_CUDA(cudaMemcpyAsync(e->U, b, ub, cudaMemcpyHostToDevice, s));
+    st.release(slot, s);
+  }
+  // the compute stream waits for the upload; Staging's destructor drains the ring
+  HS_CUDA(cudaEventRecord(e->ev_up1, s));
+  HS_CUDA(cudaStreamWaitEvent(e->stream, e->ev_up1, 0));
 }
 
 // ---------------------------------------------------------------------------
@@ -970,6 +1238,80 @@ static void flop_model(int variant, uint64_t na, uint64_t nl, uint64_t ng, uint6
     l[5] = 4 * na * nl * ng * ng;
   }
   for (int i = 0; i < 8; ++i) l[8] += l[i];
+}
+
+// The one-shot drop-in around a per-engine "start" (upload/load + enqueue build,
+// returning host seconds spent loading): device selection, engine cache, NCCL
+// reduce to the root, overlapped download, stats.
+template <class Start>
+static void one_shot(const hsdla_b200_options* o, uint64_t na, uint64_t nl, uint64_t ng, double* H, double* S,
+                     hsdla_b200_stats* st, std::chrono::steady_clock::time_point t0, Start&& start) {
+  const int algo = o ? o->algo : HSDLA_B200_ALGO_REFINED_FUSED;
+  if (!valid_algo(algo)) throw Fail{HSDLA_B200_CONFIG_ERROR, "unknown algo " + std::to_string(algo)};
+  const int P = o && o->n_gpus > 1 ? o->n_gpus : 1;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    (void)cudaGetLastError();
+    throw Fail{HSDLA_B200_CONFIG_ERROR, "no CUDA device visible (the B200 path has no CPU fallback)"};
+  }
+  std::vector<int> devs(P);
+  for (int r = 0; r < P; ++r) devs[r] = (o && o->device_ids) ? o->device_ids[r] : r;
+  for (int d : devs)
+    if (d < 0 || d >= ndev) throw Fail{HSDLA_B200_CONFIG_ERROR, "device id out of range"};
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  EngineSet* set = get_engines(devs, na, nl, ng);
+  double load_s = 0;
+  for (int r = 0; r < P; ++r) load_s = std::max(load_s, start(set->engines[r], set->atom0[r], algo));
+  if (P > 1) {
+    HS_NCCL(ncclGroupStart());
+    for (int r = 0; r < P; ++r) reduce_s(set->engines[r], 0);
+    HS_NCCL(ncclGroupEnd());
+    HS_NCCL(ncclGroupStart());
+    for (int r = 0; r < P; ++r) reduce_h(set->engines[r], 0);
+    HS_NCCL(ncclGroupEnd());
+    for (int r = 0; r < P; ++r) reduce_finish(set->engines[r]);
+  }
+  hsdla_b200_engine* root = set->engines[0];
+  HS_CUDA(cudaSetDevice(root->device));
+  enqueue_download(root);
+  const auto t_d = std::chrono::steady_clock::now();
+  finish_download(root, H, S);
+  const double d2h = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_d).count();
+  hsdla_b200_stats local{};
+  double maxph[HSDLA_B200_N_PHASES] = {};
+  double dev_s = 0, red_s = 0, h2d = 0;
+  int launches = 0;
+  uint64_t n_hpd = 0;
+  for (int r = 0; r < P; ++r) {
+    engine_sync(set->engines[r], &local);
+    n_hpd += local.n_hpd;
+    for (int i = 0; i < HSDLA_B200_N_PHASES; ++i) maxph[i] = std::max(maxph[i], local.phase_seconds[i]);
+    dev_s = std::max(dev_s, local.device_seconds);
+    red_s = std::max(red_s, local.reduce_seconds);
+    h2d = std::max(h2d, local.h2d_seconds);
+    launches += local.kernel_launches;
+  }
+  if (st) {
+    std::memcpy(st->phase_seconds, maxph, sizeof(maxph));
+    st->h2d_seconds = std::max(h2d, load_s);
+    st->device_seconds = dev_s;
+    st->reduce_seconds = red_s;
+    st->d2h_seconds = d2h;
+    // ledger == pipeline::flop_model(p, variant) with the potrf outcome of this build
+    flop_model(algo == HSDLA_B200_ALGO_ORIGINAL ? 0 : 1, na, nl, ng, n_hpd, st->ledger);
+    // every algorithm runs the same lower-triangular contractions: 20 K N_G^2 +
+    // 24 N_A N_L^2 N_G + 2 K N_G (the original's trmm on the zero upper half of L
+    // and its full gemm fold are executed as the lower-only h_aa contraction)
+    uint64_t refined[9];
+    flop_model(1, na, nl, ng, na, refined);
+    st->executed_flops = refined[8];
+    st->n_hpd = n_hpd;
+    st->peak_device_bytes = local.peak_device_bytes;
+    st->peak_temp_bytes = local.peak_temp_bytes;
+    st->n_gpus = P;
+    st->kernel_launches = launches;
+    st->total_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
 }
 
 }  // namespace hsdla_b200
@@ -1073,6 +1415,12 @@ int hsdla_b200_engine_upload(hsdla_b200_engine* e, const hsdla_b200_problem* p, 
   return guarded([&] {
     if (!e) throw Fail{HSDLA_B200_CONFIG_ERROR, "null engine"};
     engine_upload(e, p, a0);
+  });
+}
+int hsdla_b200_engine_fill_synthetic(hsdla_b200_engine* e, uint64_t seed) {
+  return guarded([&] {
+    if (!e) throw Fail{HSDLA_B200_CONFIG_ERROR, "null engine"};
+    engine_fill_synthetic(e, seed);
   });
 }
 int hsdla_b200_engine_build(hsdla_b200_engine* e, int algo) {
@@ -1226,72 +1574,53 @@ int hsdla_b200_build_hs(const hsdla_b200_problem* p, const hsdla_b200_options* o
     if (!H || !S) throw Fail{HSDLA_B200_DIMENSION_ERROR, "null H or S"};
     if (!p->A || !p->B || !p->T_AA || !p->T_AB || !p->T_BB || !p->U)
       throw Fail{HSDLA_B200_DIMENSION_ERROR, "null problem pointer"};
-    const int algo = o ? o->algo : HSDLA_B200_ALGO_REFINED_FUSED;
-    if (!valid_algo(algo)) throw Fail{HSDLA_B200_CONFIG_ERROR, "unknown algo " + std::to_string(algo)};
-    const int P = o && o->n_gpus > 1 ? o->n_gpus : 1;
-    int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
-      (void)cudaGetLastError();
-      throw Fail{HSDLA_B200_CONFIG_ERROR, "no CUDA device visible (the B200 path has no CPU fallback)"};
+    // streamed upload + build per GPU (chunk c+1's H2D overlaps chunk c's phases)
+    one_shot(o, p->n_atoms, p->n_l, p->n_g, H, S, st, t0, [&](hsdla_b200_engine* e, uint64_t a0, int algo) {
+      engine_build_streamed(e, p, a0, algo);
+      return 0.0;
+    });
+  });
+}
+
+int hsdla_b200_problem_file_info(const char* path, uint64_t* n_atoms, uint64_t* n_l, uint64_t* n_g, uint8_t* hpd) {
+  return guarded([&] {
+    Fd f;
+    f.fd = open_hsdl(path);
+    const HsdlHeader h = read_hsdl_header(f.fd, path);
+    if (n_atoms) *n_atoms = h.na;
+    if (n_l) *n_l = h.nl;
+    if (n_g) *n_g = h.ng;
+    if (hpd) std::copy(h.hpd.begin(), h.hpd.end(), hpd);
+  });
+}
+
+int hsdla_b200_engine_load(hsdla_b200_engine* e, const char* path, uint64_t atom_begin) {
+  return guarded([&] {
+    if (!e) throw Fail{HSDLA_B200_CONFIG_ERROR, "null engine"};
+    engine_load_file(e, path, atom_begin);
+  });
+}
+
+int hsdla_b200_build_hs_file(const char* path, const hsdla_b200_options* o, double* H, double* S,
+                             hsdla_b200_stats* st) {
+  return guarded([&] {
+    const auto t0 = std::chrono::steady_clock::now();
+    HsdlHeader h;
+    {
+      Fd f;
+      f.fd = open_hsdl(path);
+      h = read_hsdl_header(f.fd, path);
     }
-    std::vector<int> devs(P);
-    for (int r = 0; r < P; ++r) devs[r] = (o && o->device_ids) ? o->device_ids[r] : r;
-    for (int d : devs)
-      if (d < 0 || d >= ndev) throw Fail{HSDLA_B200_CONFIG_ERROR, "device id out of range"};
-    std::lock_guard<std::mutex> lk(g_cache_mu);
-    EngineSet* set = get_engines(devs, p->n_atoms, p->n_l, p->n_g);
-    // streamed upload + build per GPU
-    for (int r = 0; r < P; ++r) engine_build_streamed(set->engines[r], p, set->atom0[r], algo);
-    if (P > 1) {
-      HS_NCCL(ncclGroupStart());
-      for (int r = 0; r < P; ++r) reduce_s(set->engines[r], 0);
-      HS_NCCL(ncclGroupEnd());
-      HS_NCCL(ncclGroupStart());
-      for (int r = 0; r < P; ++r) reduce_h(set->engines[r], 0);
-      HS_NCCL(ncclGroupEnd());
-      for (int r = 0; r < P; ++r) reduce_finish(set->engines[r]);
-    }
-    hsdla_b200_engine* root = set->engines[0];
-    HS_CUDA(cudaSetDevice(root->device));
-    enqueue_download(root);
-    const auto t_d = std::chrono::steady_clock::now();
-    finish_download(root, H, S);
-    const double d2h = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_d).count();
-    hsdla_b200_stats local{};
-    double maxph[HSDLA_B200_N_PHASES] = {};
-    double dev_s = 0, red_s = 0, h2d = 0;
-    int launches = 0;
-    uint64_t n_hpd = 0;
-    for (int r = 0; r < P; ++r) {
-      engine_sync(set->engines[r], &local);
-      n_hpd += local.n_hpd;
-      for (int i = 0; i < HSDLA_B200_N_PHASES; ++i) maxph[i] = std::max(maxph[i], local.phase_seconds[i]);
-      dev_s = std::max(dev_s, local.device_seconds);
-      red_s = std::max(red_s, local.reduce_seconds);
-      h2d = std::max(h2d, local.h2d_seconds);
-      launches += local.kernel_launches;
-    }
-    if (st) {
-      std::memcpy(st->phase_seconds, maxph, sizeof(maxph));
-      st->h2d_seconds = h2d;
-      st->device_seconds = dev_s;
-      st->reduce_seconds = red_s;
-      st->d2h_seconds = d2h;
-      // ledger == pipeline::flop_model(p, variant) with the potrf outcome of this build
-      flop_model(algo == HSDLA_B200_ALGO_ORIGINAL ? 0 : 1, p->n_atoms, p->n_l, p->n_g, n_hpd, st->ledger);
-      // every algorithm runs the same lower-triangular contractions: 20 K N_G^2 +
-      // 24 N_A N_L^2 N_G + 2 K N_G (the original's trmm on the zero upper half of L
-      // and its full gemm fold are executed as the lower-only h_aa contraction)
-      uint64_t refined[9];
-      flop_model(1, p->n_atoms, p->n_l, p->n_g, p->n_atoms, refined);
-      st->executed_flops = refined[8];
-      st->n_hpd = n_hpd;
-      st->peak_device_bytes = local.peak_device_bytes;
-      st->peak_temp_bytes = local.peak_temp_bytes;
-      st->n_gpus = P;
-      st->kernel_launches = launches;
-      st->total_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    }
+    check_dims(h.na, h.nl, h.ng);
+    if (!H || !S) throw Fail{HSDLA_B200_DIMENSION_ERROR, "null H or S"};
+    // each GPU reads only its atom shard from the file, then builds device-resident
+    one_shot(o, h.na, h.nl, h.ng, H, S, st, t0, [&](hsdla_b200_engine* e, uint64_t a0, int algo) {
+      const auto tl = std::chrono::steady_clock::now();
+      engine_load_file(e, path, a0);
+      const double load_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - tl).count();
+      engine_build(e, algo);
+      return load_s;
+    });
   });
 }
 

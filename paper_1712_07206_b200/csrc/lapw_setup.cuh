@@ -19,12 +19,14 @@
 // Y_lm: orthonormal complex spherical harmonics with the Condon-Shortley phase
 // (scipy.special.sph_harm_y convention), Y_{l,-m} = (-1)^m conj(Y_lm).
 //
-// Kernel shape: one CTA per G column.  Per column the CTA computes Y_lm(K^)
-// (one lane per m, stable normalised-Legendre recursion), j_l / K j_l' per atom
-// type (series / upward / Miller downward recursion), e^{iK.tau_a} per atom and
-// the per-(type, l) matching factors into shared memory, then streams the
-// column's 2 * N_A * N_L complex outputs with coalesced 16-byte stores — an
-// HBM-write-bound kernel (roofline: 32 B per (atom, lm, G) written).
+// Two passes.  lapw_tables_kernel computes, fully parallel over independent
+// items, the per-G tables Y_lm(K^) (one thread per (G, m): stable normalised-
+// Legendre recursion), the matching factors (one thread per (G, type): j_l / K j_l'
+// by series / upward / Miller downward recursion) and the structure factors
+// e^{iK.tau_a} (one thread per (G, atom)).  lapw_stream_kernel then writes the
+// 2 * N_A * N_L complex outputs of every column with coalesced 16-byte streaming
+// stores, one thread per (row, column) — the HBM-write-bound pass (roofline: 32 B
+// per (atom, lm, G) written; table reads < 2 % of that, L2-resident).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -161,28 +163,40 @@ __host__ __device__ inline void k_direction(double kx, double ky, double kz, dou
   }
 }
 
-__global__ void __launch_bounds__(256) lapw_setup_kernel(const LapwDevParams P) {
-  extern __shared__ double2 sh[];
-  const int nl = (P.lmax + 1) * (P.lmax + 1);
-  const int nlv = P.lmax + 1;
-  double2* Y = sh;                           // nl
-  double2* sf = Y + nl;                      // n_atoms: pref * e^{iK.tau}
-  double2* fab = sf + P.n_atoms;             // n_types * nlv: (fa, fb)
-  int8_t* lof = reinterpret_cast<int8_t*>(fab + P.n_types * nlv);  // l of each lm
-
-  const int g = blockIdx.x;
-  const double kx = P.kx + P.gvec[3 * g], ky = P.ky + P.gvec[3 * g + 1], kz = P.kz + P.gvec[3 * g + 2];
-  double kn, x, sth, cph, sph;
-  k_direction(kx, ky, kz, kn, x, sth, cph, sph);
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (warp == 0) {
-    for (int m = lane; m <= P.lmax; m += 32) ylm_column(P.lmax, m, x, sth, cph, sph, Y);
-  } else if (warp == 1) {
-    for (int t = lane; t < P.n_types; t += 32) {
+// ---- pass 1: per-G tables (one thread per independent item) ----------------
+//   Y[g][lm]      = Y_lm(K_g^)                     (one item per (g, m >= 0))
+//   F[g][t][l]    = (fa, fb) matching factors         (one item per (g, type))
+//   SF[g][a]      = pref * e^{i K_g . tau_a}          (one item per (g, atom))
+// Item ranges are contiguous per kind so warps stay convergent.
+__global__ void __launch_bounds__(256) lapw_tables_kernel(const LapwDevParams P, double2* __restrict__ tabY,
+                                                          double2* __restrict__ tabF, double2* __restrict__ tabS) {
+  const int nlv = P.lmax + 1, nl = nlv * nlv;
+  const uint64_t ng = P.n_g;
+  const uint64_t nY = ng * nlv, nF = ng * P.n_types, nS = ng * P.n_atoms;
+  for (uint64_t it = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; it < nY + nF + nS;
+       it += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint64_t g;
+    int sub;
+    if (it < nY) {
+      g = it / nlv;
+      sub = static_cast<int>(it - g * nlv);
+    } else if (it < nY + nF) {
+      g = (it - nY) / P.n_types;
+      sub = static_cast<int>(it - nY - g * P.n_types);
+    } else {
+      g = (it - nY - nF) / P.n_atoms;
+      sub = static_cast<int>(it - nY - nF - g * P.n_atoms);
+    }
+    const double kx = P.kx + P.gvec[3 * g], ky = P.ky + P.gvec[3 * g + 1], kz = P.kz + P.gvec[3 * g + 2];
+    if (it < nY) {
+      double kn, x, sth, cph, sph;
+      k_direction(kx, ky, kz, kn, x, sth, cph, sph);
+      ylm_column(P.lmax, sub, x, sth, cph, sph, tabY + g * nl);
+    } else if (it < nY + nF) {
+      const int t = sub;
+      const double kn = sqrt(kx * kx + ky * ky + kz * kz);
       double jl[kLapwMaxL + 2];
-      const double R = P.rmt[t];
-      const double xr = kn * R;
+      const double xr = kn * P.rmt[t];
       sph_bessel(P.lmax + 1, xr, jl);
       for (int l = 0; l <= P.lmax; ++l) {
         // K j_l'(KR) = K [ l/x j_l - j_{l+1} ]  (recurrence valid for all l, x > 0); 0 at K = 0
@@ -190,48 +204,56 @@ __global__ void __launch_bounds__(256) lapw_setup_kernel(const LapwDevParams P) 
         const double* r = P.radial + (static_cast<size_t>(t) * nlv + l) * 4;
         const double u = r[0], du = r[1], ud = r[2], dud = r[3];
         const double det = u * dud - ud * du;
-        fab[t * nlv + l] = make_double2((jl[l] * dud - kjd * ud) / det, (kjd * u - jl[l] * du) / det);
+        tabF[(g * P.n_types + t) * nlv + l] = make_double2((jl[l] * dud - kjd * ud) / det, (kjd * u - jl[l] * du) / det);
       }
+    } else {
+      const int a = sub;
+      const double ph = kx * P.tau[3 * a] + ky * P.tau[3 * a + 1] + kz * P.tau[3 * a + 2];
+      double sn, cs;
+      sincos(ph, &sn, &cs);
+      tabS[g * P.n_atoms + a] = make_double2(P.pref * cs, P.pref * sn);
     }
   }
-  for (int lm = tid; lm < nl; lm += blockDim.x) {
-    int l = 0;
-    while ((l + 1) * (l + 1) <= lm) ++l;
-    lof[lm] = static_cast<int8_t>(l);
-  }
-  for (int a = tid; a < P.n_atoms; a += blockDim.x) {
-    const double ph = kx * P.tau[3 * a] + ky * P.tau[3 * a + 1] + kz * P.tau[3 * a + 2];
-    double s, c;
-    sincos(ph, &s, &c);
-    sf[a] = make_double2(P.pref * c, P.pref * s);
-  }
-  __syncthreads();
+}
 
-  // stream the column: one warp per atom block of N_L rows (contiguous in memory)
-  double2* colA = P.A + static_cast<uint64_t>(g) * P.ldo;
-  double2* colB = P.B + static_cast<uint64_t>(g) * P.ldo;
-  const int nwarps = blockDim.x >> 5;
-  for (int a = warp; a < P.n_atoms; a += nwarps) {
-    const double2 s = sf[a];
-    const int t = P.type[a];
-    const double2* f = fab + t * nlv;
-    for (int lm = lane; lm < nl; lm += 32) {
-      const int l = lof[lm];
-      const double2 y = Y[lm];
-      // c = s * i^l * conj(y)
-      double cr = s.x * y.x + s.y * y.y;   // s * conj(y)
-      double ci = s.y * y.x - s.x * y.y;
-      switch (l & 3) {  // multiply by i^l
-        case 1: { const double tr = -ci; ci = cr; cr = tr; } break;
-        case 2: cr = -cr; ci = -ci; break;
-        case 3: { const double tr = ci; ci = -cr; cr = tr; } break;
-        default: break;
-      }
-      const double2 fl = f[l];
-      const uint64_t row = static_cast<uint64_t>(a) * nl + lm;
-      __stcs(colA + row, make_double2(cr * fl.x, ci * fl.x));
-      __stcs(colB + row, make_double2(cr * fl.y, ci * fl.y));
+// ---- pass 2: the HBM-write-bound stream --------------------------------------
+// One thread per (row r = a*N_L + lm, column g) pair, rows fastest (coalesced
+// 16-byte streaming stores into both A and B); the tables are L2-resident reads
+// (< 2 % of the bytes written).  Each thread writes
+// ROWS rows 256 apart.  grid = (n_g, ceil(K / 256 / ROWS)).
+template <int ROWS>
+__global__ void __launch_bounds__(256) lapw_stream_kernel(const LapwDevParams P, const double2* __restrict__ tabY,
+                                                          const double2* __restrict__ tabF,
+                                                          const double2* __restrict__ tabS) {
+  const int nlv = P.lmax + 1, nl = nlv * nlv;
+  const uint64_t K = static_cast<uint64_t>(P.n_atoms) * nl;
+  const uint64_t g = blockIdx.x;
+  const double2* Y = tabY + g * nl;
+  const double2* F = tabF + g * P.n_types * nlv;
+  const double2* SF = tabS + g * P.n_atoms;
+  double2* colA = P.A + g * P.ldo;
+  double2* colB = P.B + g * P.ldo;
+#pragma unroll
+  for (int k = 0; k < ROWS; ++k) {
+    const uint64_t r = (static_cast<uint64_t>(blockIdx.y) * ROWS + k) * blockDim.x + threadIdx.x;
+    if (r >= K) return;
+    const int a = static_cast<int>(r / nl);
+    const int lm = static_cast<int>(r - static_cast<uint64_t>(a) * nl);
+    int l = static_cast<int>(sqrt(static_cast<double>(lm)));
+    l -= (l * l > lm);
+    l += ((l + 1) * (l + 1) <= lm);
+    const double2 y = __ldg(Y + lm), s = __ldg(SF + a), fl = __ldg(F + __ldg(P.type + a) * nlv + l);
+    // c = s * i^l * conj(y)
+    double cr = s.x * y.x + s.y * y.y;  // s * conj(y)
+    double ci = s.y * y.x - s.x * y.y;
+    switch (l & 3) {  // multiply by i^l
+      case 1: { const double tr = -ci; ci = cr; cr = tr; } break;
+      case 2: cr = -cr; ci = -ci; break;
+      case 3: { const double tr = ci; ci = -cr; cr = tr; } break;
+      default: break;
     }
+    __stcs(colA + r, make_double2(cr * fl.x, ci * fl.x));
+    __stcs(colB + r, make_double2(cr * fl.y, ci * fl.y));
   }
 }
 

@@ -8,6 +8,7 @@ Reference interface mirrored (names, argument meaning, error behaviour):
 All arithmetic runs in libhsdla_b200.so on the GPU; nothing here computes H or S.
 """
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
 
@@ -165,6 +166,44 @@ def build_hs_original(p, cfg: Optional[PipelineConfig] = None, H=None, S=None) -
     return _run(p, cfg, "original", H, S, "build_hs_original")
 
 
+def problem_file_info(path):
+    """Header of an HSDL v1 file (problem.cpp:197-225) read natively: (n_atoms, n_l,
+    n_g, hpd_flags).  IoError on a missing / malformed / truncated file."""
+    na, nl, ng = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    bpath = os.fsencode(path)
+    check(_lib.lib().hsdla_b200_problem_file_info(bpath, C.byref(na), C.byref(nl), C.byref(ng), None),
+          "problem_file_info")
+    hpd = np.zeros(na.value, np.uint8)
+    check(_lib.lib().hsdla_b200_problem_file_info(bpath, None, None, None, hpd.ctypes.data_as(C.c_void_p)),
+          "problem_file_info")
+    return na.value, nl.value, ng.value, hpd.astype(bool)
+
+
+def build_hs_file(path, cfg: Optional[PipelineConfig] = None, H=None, S=None) -> HSResult:
+    """build_hs(load_problem(path), cfg) with the file streamed shard by shard
+    straight into HBM (no host ProblemInstance)."""
+    cfg = cfg or PipelineConfig()
+    parse_strategy(cfg.strategy)
+    algo = "original" if parse_variant(cfg.variant) == "original" else cfg.algo
+    if algo not in ALGOS:
+        raise ConfigError(f"unknown algo: {algo}")
+    _na, _nl, n, _hpd = problem_file_info(path)
+    if H is None:
+        H = np.zeros((n, n), np.complex128, order="F")
+    if S is None:
+        S = np.zeros((n, n), np.complex128, order="F")
+    for name, M in (("H", H), ("S", S)):
+        if M.shape != (n, n) or M.dtype != np.complex128 or not M.flags.f_contiguous:
+            raise DimensionError(f"{name} must be a ({n}, {n}) complex128 Fortran array")
+    opts, _keep = _options(cfg, algo)
+    st = _lib.Stats()
+    check(_lib.lib().hsdla_b200_build_hs_file(os.fsencode(path), C.byref(opts), H.ctypes.data_as(C.c_void_p),
+                                              S.ctypes.data_as(C.c_void_p), C.byref(st)), "build_hs_file")
+    warnings = ["herkx fused into the her2k contraction (phase time 0)"] if algo == "fused" else []
+    return HSResult(H, S, FlopLedger.from_array(st.ledger), int(st.peak_temp_bytes), _phases(st, algo), warnings,
+                    stats_dict(st, algo))
+
+
 def build_hs(p, cfg: PipelineConfig) -> HSResult:
     """build_hs (pipeline.cpp:331-334): dispatch on the variant."""
     if parse_variant(cfg.variant) == "original":
@@ -246,6 +285,14 @@ class Engine:
     def upload(self, p, atom_begin=0):
         prob = p.c_struct()
         check(_lib.lib().hsdla_b200_engine_upload(self.h, C.byref(prob), C.c_uint64(atom_begin)), "engine_upload")
+
+    def fill_synthetic(self, seed=1):
+        """Device-side synthetic inputs (timing sweeps only; not the reference generator)."""
+        check(_lib.lib().hsdla_b200_engine_fill_synthetic(self.h, C.c_uint64(seed)), "engine_fill_synthetic")
+
+    def load(self, path, atom_begin=0):
+        """Stream this shard of an HSDL v1 file into the engine (hsdla_b200_engine_load)."""
+        check(_lib.lib().hsdla_b200_engine_load(self.h, os.fsencode(path), C.c_uint64(atom_begin)), "engine_load")
 
     def build(self, algo="fused"):
         self._algo = algo

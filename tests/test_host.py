@@ -100,3 +100,27 @@ def test_mirror_and_rel_error():
     X = hb.mirror(M.copy())
     assert np.allclose(X, X.conj().T) and np.all(np.diag(X).imag == 0)
     assert hb.rel_frobenius_error_lower(M, M) == 0.0
+
+
+def test_native_hsdl_header_reader(tmp_path):
+    """The library's own HSDL v1 header reader (the streaming loader's front end,
+    problem.cpp:197-225) on the reference-written file and on malformed files
+    (test_io.cpp:47-63): IoError for bad magic, bad version, truncation, no file."""
+    ref = os.path.join(GOLDEN, "small_2_3_16_s1_nh1.hsdl")
+    na, nl, ng, hpd = hb.problem_file_info(ref)
+    assert (na, nl, ng) == (2, 3, 16) and list(hpd) == [True, False]
+    src = open(ref, "rb").read()
+    cases = {"bad.hsdl": b"NOPE" + b"\0" * 64, "ver.hsdl": src[:4] + b"\x02\0\0\0" + src[8:],
+             "trunc.hsdl": src[: len(src) // 2], "hdr.hsdl": src[:20]}
+    for name, data in cases.items():
+        (tmp_path / name).write_bytes(data)
+        with pytest.raises(hb.IoError):
+            hb.problem_file_info(str(tmp_path / name))
+    with pytest.raises(hb.IoError):
+        hb.problem_file_info("/nonexistent/nowhere.hsdl")
+    with pytest.raises(hb.IoError):
+        hb.build_hs_file(str(tmp_path / "trunc.hsdl"))  # rejected before any device work
+    big = hb.generate_problem(37, 5, 9, 4, 11)
+    hb.save_problem(big, str(tmp_path / "big.hsdl"))
+    na, nl, ng, hpd = hb.problem_file_info(str(tmp_path / "big.hsdl"))
+    assert (na, nl, ng) == (37, 5, 9) and np.array_equal(hpd, big.hpd_flags)
