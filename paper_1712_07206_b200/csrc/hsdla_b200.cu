@@ -241,8 +241,9 @@ struct hsdla_b200_engine {
   size_t ev_used = 0;
   std::vector<hsdla_b200::OpTime> ops;
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr, ev_s_done = nullptr, ev_s_red = nullptr,
-              ev_reduce_end = nullptr, ev_up0 = nullptr, ev_up1 = nullptr, ev_s_d2h = nullptr,
-              ev_h_d2h = nullptr;
+              ev_reduce_end = nullptr, ev_up0 = nullptr, ev_up1 = nullptr, ev_s_d2h = nullptr;
+  static constexpr int kD2hPieces = 4;   // H downloads in column-range pieces, unpacked as each lands
+  cudaEvent_t ev_h_piece[kD2hPieces] = {};
   std::vector<cudaEvent_t> ev_chunk_up;
   int last_algo = 0, launches = 0;
   uint64_t n_hpd_last = 0;
@@ -290,8 +291,10 @@ static void engine_free(hsdla_b200_engine* e) {
   if (e->host_stage) cudaFreeHost(e->host_stage);
   for (cudaEvent_t ev : e->ev_pool) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e->ev_chunk_up) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : e->ev_h_piece)
+    if (ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : {e->ev_begin, e->ev_end, e->ev_s_done, e->ev_s_red, e->ev_reduce_end, e->ev_up0, e->ev_up1,
-                         e->ev_s_d2h, e->ev_h_d2h, e->ev_setup0, e->ev_setup1})
+                         e->ev_s_d2h, e->ev_setup0, e->ev_setup1})
     if (ev) cudaEventDestroy(ev);
   for (auto& t : e->ring)
     for (cudaEvent_t ev : {t.s0, t.s1, t.h0, t.h1})
@@ -408,13 +411,27 @@ static void make_chunk(hsdla_b200_engine* e, uint64_t a0, uint64_t a1, bool firs
                      static_cast<unsigned>((nl + kBatBM - 1) / kBatBM), static_cast<unsigned>(nac));
 }
 
-// Streamed chunking: ~8 chunks of whole atoms, each >= 2 atoms (small problems: 1 chunk).
+// Streamed chunking for the host-buffer drop-in: whole-atom chunks growing
+// geometrically, so the exposed upload of the first chunk is short and later
+// (larger) uploads still finish before the previous chunk's phases do.  The growth
+// factor follows the compute/upload time ratio of one atom, ~ N_G x 9e-4 on B200
+// (20 K N_G^2 flops at ~34 TF/s vs 32 K N_G bytes at ~50 GB/s pinned PCIe), kept
+// in [1.5, 4]; at most 8 chunks.  Small problems (< 64 MB of A+B): one chunk.
 static std::vector<uint64_t> stream_bounds(uint64_t na, uint64_t nl, uint64_t ng) {
-  uint64_t n = std::min<uint64_t>(8, na / 2);
-  if (na * nl * ng < (uint64_t(1) << 22)) n = 1;  // < 64 MB of A+B: nothing to overlap
-  n = std::max<uint64_t>(n, 1);
-  std::vector<uint64_t> b(n + 1);
-  for (uint64_t c = 0; c <= n; ++c) b[c] = na * c / n;
+  std::vector<uint64_t> b{0};
+  if (na * nl * ng < (uint64_t(1) << 22) || na < 2) {
+    b.push_back(na);
+    return b;
+  }
+  const double r = std::min(4.0, std::max(1.5, 0.8 * 9e-4 * static_cast<double>(ng)));
+  double size = std::max(1.0, static_cast<double>(na) / 16.0);
+  while (b.back() < na) {
+    const uint64_t left = na - b.back();
+    uint64_t take = std::min<uint64_t>(left, static_cast<uint64_t>(std::llround(size)));
+    if (b.size() == 8 || left - take < take / 2) take = left;  // cap the count, no tiny last chunk
+    b.push_back(b.back() + std::max<uint64_t>(take, 1));
+    size *= r;
+  }
   return b;
 }
 
@@ -456,8 +473,9 @@ static hsdla_b200_engine* engine_create(int device, uint64_t na, uint64_t nl, ui
     for (cudaEvent_t* ev : {&e->ev_begin, &e->ev_end, &e->ev_reduce_end, &e->ev_up0, &e->ev_up1, &e->ev_setup0,
                             &e->ev_setup1})
       HS_CUDA(cudaEventCreate(ev));
-    for (cudaEvent_t* ev : {&e->ev_s_done, &e->ev_s_red, &e->ev_s_d2h, &e->ev_h_d2h})
+    for (cudaEvent_t* ev : {&e->ev_s_done, &e->ev_s_red, &e->ev_s_d2h})
       HS_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
+    for (cudaEvent_t& ev : e->ev_h_piece) HS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     for (auto& t : e->ring)
       for (cudaEvent_t* ev : {&t.s0, &t.s1, &t.h0, &t.h1}) HS_CUDA(cudaEventCreate(ev));
     const uint64_t KG = e->K * ng;
@@ -764,30 +782,44 @@ static void engine_sync(hsdla_b200_engine* e, hsdla_b200_stats* st) {
   st->kernel_launches = e->launches;
 }
 
-// Unpack column-major packed lower into the lower triangle of an n x n matrix.
-static void unpack_lower(const double2* pk, double2* full, uint64_t n) {
+static inline uint64_t packed_col(uint64_t n, uint64_t j) { return j * (2 * n - j + 1) / 2; }
+
+// Unpack columns [c0, c1) of a column-major packed lower triangle (pk = the whole
+// packed array) into the lower triangle of an n x n matrix, over up to 16 threads
+// with equal element counts.
+static void unpack_lower(const double2* pk, double2* full, uint64_t n, uint64_t c0, uint64_t c1) {
   const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-  const uint64_t total = n * (n + 1) / 2;
+  const uint64_t base = packed_col(n, c0), total = packed_col(n, c1) - base;
   const unsigned nt = total < (1u << 18) ? 1u : hw;
   auto work = [&](uint64_t j0, uint64_t j1) {
-    for (uint64_t j = j0; j < j1; ++j)
-      std::memcpy(full + j * n + j, pk + j * (2 * n - j + 1) / 2, (n - j) * sizeof(double2));
+    for (uint64_t j = j0; j < j1; ++j) std::memcpy(full + j * n + j, pk + packed_col(n, j), (n - j) * sizeof(double2));
   };
   if (nt == 1) {
-    work(0, n);
+    work(c0, c1);
     return;
   }
-  std::vector<std::thread> th;  // nt column ranges of equal element count
-  uint64_t j = 0;
-  for (unsigned t = 0; t < nt && j < n; ++t) {
-    const uint64_t target = total * (t + 1) / nt;
+  std::vector<std::thread> th;
+  uint64_t j = c0;
+  for (unsigned t = 0; t < nt && j < c1; ++t) {
+    const uint64_t target = base + total * (t + 1) / nt;
     uint64_t j1 = j;
-    while (j1 < n && j1 * (2 * n - j1 + 1) / 2 < target) ++j1;
-    if (t == nt - 1) j1 = n;
+    while (j1 < c1 && packed_col(n, j1) < target) ++j1;
+    if (t == nt - 1) j1 = c1;
     th.emplace_back(work, j, j1);
     j = j1;
   }
   for (auto& t : th) t.join();
+}
+
+// Column boundaries of the kD2hPieces H download pieces (equal packed sizes).
+static uint64_t piece_col(uint64_t n, int q, int pieces) {
+  const uint64_t target = packed_col(n, n) * q / pieces;
+  uint64_t lo = 0, hi = n;  // first column whose packed start >= target
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) / 2;
+    if (packed_col(n, mid) < target) lo = mid + 1; else hi = mid;
+  }
+  return lo;
 }
 
 static void ensure_stage(hsdla_b200_engine* e) {
@@ -804,16 +836,28 @@ static void enqueue_download(hsdla_b200_engine* e) {
   HS_CUDA(cudaMemcpyAsync(e->host_stage + e->npk, e->Sp, bytes, cudaMemcpyDeviceToHost, e->copy_stream));
   HS_CUDA(cudaEventRecord(e->ev_s_d2h, e->copy_stream));
   HS_CUDA(cudaStreamWaitEvent(e->copy_stream, e->reduced ? e->ev_reduce_end : e->ev_end, 0));
-  HS_CUDA(cudaMemcpyAsync(e->host_stage, e->Hp, bytes, cudaMemcpyDeviceToHost, e->copy_stream));
-  HS_CUDA(cudaEventRecord(e->ev_h_d2h, e->copy_stream));
+  for (int q = 0; q < hsdla_b200_engine::kD2hPieces; ++q) {
+    const uint64_t b0 = packed_col(e->ng, piece_col(e->ng, q, hsdla_b200_engine::kD2hPieces));
+    const uint64_t b1 = packed_col(e->ng, piece_col(e->ng, q + 1, hsdla_b200_engine::kD2hPieces));
+    if (b1 > b0)
+      HS_CUDA(cudaMemcpyAsync(e->host_stage + b0, e->Hp + b0, (b1 - b0) * sizeof(double2), cudaMemcpyDeviceToHost,
+                              e->copy_stream));
+    HS_CUDA(cudaEventRecord(e->ev_h_piece[q], e->copy_stream));
+  }
 }
 
 // Unpack S as soon as its bytes land (H may still be computing), then H.
 static void finish_download(hsdla_b200_engine* e, double* H, double* S) {
   HS_CUDA(cudaEventSynchronize(e->ev_s_d2h));
-  if (S) unpack_lower(e->host_stage + e->npk, reinterpret_cast<double2*>(S), e->ng);
-  HS_CUDA(cudaEventSynchronize(e->ev_h_d2h));
-  if (H) unpack_lower(e->host_stage, reinterpret_cast<double2*>(H), e->ng);
+  if (S) unpack_lower(e->host_stage + e->npk, reinterpret_cast<double2*>(S), e->ng, 0, e->ng);
+  // H: unpack piece q while piece q+1 is still on the wire
+  for (int q = 0; q < hsdla_b200_engine::kD2hPieces; ++q) {
+    HS_CUDA(cudaEventSynchronize(e->ev_h_piece[q]));
+    if (H)
+      unpack_lower(e->host_stage, reinterpret_cast<double2*>(H), e->ng,
+                   piece_col(e->ng, q, hsdla_b200_engine::kD2hPieces),
+                   piece_col(e->ng, q + 1, hsdla_b200_engine::kD2hPieces));
+  }
 }
 
 static void engine_download(hsdla_b200_engine* e, double* H, double* S) {
@@ -854,7 +898,8 @@ static size_t lapw_tables_bytes(const hsdla_b200_lapw* sys, uint64_t na) {
 }
 static size_t lapw_inputs_bytes(const hsdla_b200_lapw* sys, uint64_t na) {
   const size_t nlv = sys->lmax + 1;
-  return ((sys->n_g * 3 + na * 3 + sys->n_types * nlv * 4 + sys->n_types + sys->n_types * nlv) * sizeof(double) +
+  return ((sys->n_g * 3 + na * 3 + sys->n_types * nlv * 4 + sys->n_types + sys->n_types * nlv + 4 * nlv * nlv) *
+              sizeof(double) +
           ((na * sizeof(int32_t) + 7) & ~size_t(7)) + 255) & ~size_t(255);
 }
 static size_t lapw_scratch_size(const hsdla_b200_lapw* sys, uint64_t na) {
@@ -866,9 +911,10 @@ static size_t lapw_scratch_size(const hsdla_b200_lapw* sys, uint64_t na) {
 static void lapw_enqueue(const hsdla_b200_lapw* sys, uint64_t a0, uint64_t na, double2* A, double2* B, uint64_t ldo,
                          double* U, void* scratch, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
   const int nlv = sys->lmax + 1, nl = nlv * nlv;
-  // pack [gvec | tau | radial(u,u',udot,udot') | rmt | udot_norm | type] into one host block
+  // pack [gvec | tau | radial(u,u',udot,udot') | rmt | udot_norm | ylm coefficients | type] into one host block
   const size_t n_g3 = sys->n_g * 3, n_t3 = na * 3, n_rad = sys->n_types * nlv * 4, n_un = sys->n_types * nlv;
-  std::vector<double> h(n_g3 + n_t3 + n_rad + sys->n_types + n_un + (na * sizeof(int32_t) + 7) / 8);
+  const size_t n_yc = 4 * static_cast<size_t>(nl);
+  std::vector<double> h(n_g3 + n_t3 + n_rad + sys->n_types + n_un + n_yc + (na * sizeof(int32_t) + 7) / 8);
   double* hp = h.data();
   std::memcpy(hp, sys->gvec, n_g3 * sizeof(double));
   std::memcpy(hp + n_g3, sys->tau + 3 * a0, n_t3 * sizeof(double));
@@ -883,7 +929,8 @@ static void lapw_enqueue(const hsdla_b200_lapw* sys, uint64_t a0, uint64_t na, d
     }
   std::memcpy(rad + n_rad, sys->rmt, sys->n_types * sizeof(double));
   std::memcpy(rad + n_rad + sys->n_types, sys->udot_norm, n_un * sizeof(double));
-  std::memcpy(rad + n_rad + sys->n_types + n_un, sys->atom_type + a0, na * sizeof(int32_t));
+  ylm_coefficients(sys->lmax, rad + n_rad + sys->n_types + n_un);
+  std::memcpy(rad + n_rad + sys->n_types + n_un + n_yc, sys->atom_type + a0, na * sizeof(int32_t));
   HS_CUDA(cudaMemcpyAsync(scratch, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, s));
   HS_CUDA(cudaStreamSynchronize(s));  // h is pageable and goes out of scope
   double* d = static_cast<double*>(scratch);
@@ -893,7 +940,8 @@ static void lapw_enqueue(const hsdla_b200_lapw* sys, uint64_t a0, uint64_t na, d
   P.radial = d + n_g3 + n_t3;
   P.rmt = d + n_g3 + n_t3 + n_rad;
   const double* d_un = P.rmt + sys->n_types;
-  P.type = reinterpret_cast<const int32_t*>(d_un + n_un);
+  P.ylm_coef = d_un + n_un;
+  P.type = reinterpret_cast<const int32_t*>(d_un + n_un + n_yc);
   P.kx = sys->kpt[0];
   P.ky = sys->kpt[1];
   P.kz = sys->kpt[2];

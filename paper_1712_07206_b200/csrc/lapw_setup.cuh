@@ -43,6 +43,7 @@ struct LapwDevParams {
   const int32_t* type;      // n_atoms
   const double* radial;     // n_types x (lmax+1) x 4: u, u', udot, udot'
   const double* rmt;        // n_types
+  const double* ylm_coef;   // 4 (lmax+1)^2: ylm_coefficients()
   double kx, ky, kz;
   double pref;              // 4 pi / sqrt(Omega)
   int n_atoms, n_types, lmax, n_g;
@@ -52,8 +53,10 @@ struct LapwDevParams {
 };
 
 // j_l(x) for l = 0..lmax (x >= 0), written to j[0..lmax].
+// Series only for x < 1e-3 (converges in 2-3 terms there); Miller / upward recurrence
+// otherwise, with 1/x hoisted out of the recurrences (no division on the chain).
 __host__ __device__ inline void sph_bessel(int lmax, double x, double* j) {
-  if (x < 1.0) {  // power series: j_l(x) = x^l/(2l+1)!! sum_k (-x^2/2)^k / (k! (2l+3)(2l+5)...(2l+2k+1))
+  if (x < 1e-3) {  // power series: j_l(x) = x^l/(2l+1)!! sum_k (-x^2/2)^k / (k! (2l+3)(2l+5)...(2l+2k+1))
     double xl = 1.0, df = 1.0;  // x^l, (2l+1)!!
     for (int l = 0; l <= lmax; ++l) {
       if (l > 0) {
@@ -73,18 +76,19 @@ __host__ __device__ inline void sph_bessel(int lmax, double x, double* j) {
   }
   double s, c;
   sincos(x, &s, &c);
-  const double j0 = s / x;
+  const double ix = 1.0 / x;
+  const double j0 = s * ix;
   if (x > lmax) {  // upward recurrence is stable for x > l
     j[0] = j0;
-    if (lmax >= 1) j[1] = s / (x * x) - c / x;
-    for (int l = 1; l < lmax; ++l) j[l + 1] = (2.0 * l + 1.0) / x * j[l] - j[l - 1];
+    if (lmax >= 1) j[1] = (j0 - c) * ix;
+    for (int l = 1; l < lmax; ++l) j[l + 1] = (2.0 * l + 1.0) * ix * j[l] - j[l - 1];
     return;
   }
   // Miller downward recurrence from well above lmax, normalised by j_0
   const int top = lmax + 30 + static_cast<int>(x);
   double jp1 = 0.0, jl = 1e-300, scale = 1.0;
   for (int l = top; l >= 1; --l) {
-    const double jm1 = (2.0 * l + 1.0) / x * jl - jp1;
+    const double jm1 = (2.0 * l + 1.0) * ix * jl - jp1;
     jp1 = jl;
     jl = jm1;  // now j_{l-1}
     if (l - 1 <= lmax) j[l - 1] = jl;
@@ -129,6 +133,59 @@ __host__ __device__ inline void ylm_column(int lmax, int m, double x, double sth
       const double b = sqrt((static_cast<double>(l - 1) * (l - 1) - static_cast<double>(m) * m) /
                             (4.0 * (l - 1) * (l - 1) - 1.0));
       p = a * (x * p_lm1 - b * p_lm2);
+    }
+    if (l > m) {
+      p_lm2 = p_lm1;
+      p_lm1 = p;
+    }
+    const int lm = l * (l + 1);
+    Y[lm + m] = make_double2(p * er, p * ei);
+    if (m > 0) Y[lm - m] = make_double2(sgn * p * er, -sgn * p * ei);
+  }
+}
+
+// The l-recurrence coefficients of ylm_column, tabulated once on the host (the same
+// correctly rounded sqrt / division results): index l*(lmax+1)+m.
+//   C[0][l*(lmax+1)+m] = a_lm = sqrt((4l^2-1)/(l^2-m^2))          (l >= m+2)
+//   C[1][l*(lmax+1)+m] = b_lm = sqrt(((l-1)^2-m^2)/(4(l-1)^2-1))   (l >= m+2)
+//   C[2][m]            = sqrt(2m+3)
+//   C[3][k]            = sqrt((2k+1)/(2k))                          (k >= 1)
+inline void ylm_coefficients(int lmax, double* C) {
+  const int n = (lmax + 1) * (lmax + 1);
+  for (int i = 0; i < 4 * n; ++i) C[i] = 0.0;
+  for (int m = 0; m <= lmax; ++m) {
+    C[2 * n + m] = sqrt(2.0 * m + 3.0);
+    if (m >= 1) C[3 * n + m] = sqrt((2.0 * m + 1.0) / (2.0 * m));
+    for (int l = m + 2; l <= lmax; ++l) {
+      C[l * (lmax + 1) + m] = sqrt((4.0 * l * l - 1.0) / (static_cast<double>(l) * l - static_cast<double>(m) * m));
+      C[n + l * (lmax + 1) + m] = sqrt((static_cast<double>(l - 1) * (l - 1) - static_cast<double>(m) * m) /
+                                       (4.0 * (l - 1) * (l - 1) - 1.0));
+    }
+  }
+}
+
+// ylm_column with the tabulated coefficients (no sqrt / division on the device).
+__device__ inline void ylm_column_tab(int lmax, int m, double x, double sth, double cph, double sph, double2* Y,
+                                      const double* __restrict__ C) {
+  const int n = (lmax + 1) * (lmax + 1);
+  double pmm = 0.28209479177387814;  // sqrt(1/(4 pi))
+  for (int k = 1; k <= m; ++k) pmm *= -C[3 * n + k] * sth;
+  double er = 1.0, ei = 0.0;
+  for (int k = 0; k < m; ++k) {
+    const double t = er * cph - ei * sph;
+    ei = er * sph + ei * cph;
+    er = t;
+  }
+  const double sgn = (m & 1) ? -1.0 : 1.0;
+  double p_lm2 = 0.0, p_lm1 = pmm;
+  for (int l = m; l <= lmax; ++l) {
+    double p;
+    if (l == m) {
+      p = pmm;
+    } else if (l == m + 1) {
+      p = C[2 * n + m] * x * pmm;
+    } else {
+      p = C[l * (lmax + 1) + m] * (x * p_lm1 - C[n + l * (lmax + 1) + m] * p_lm2);
     }
     if (l > m) {
       p_lm2 = p_lm1;
@@ -191,7 +248,7 @@ __global__ void __launch_bounds__(256) lapw_tables_kernel(const LapwDevParams P,
     if (it < nY) {
       double kn, x, sth, cph, sph;
       k_direction(kx, ky, kz, kn, x, sth, cph, sph);
-      ylm_column(P.lmax, sub, x, sth, cph, sph, tabY + g * nl);
+      ylm_column_tab(P.lmax, sub, x, sth, cph, sph, tabY + g * nl, P.ylm_coef);
     } else if (it < nY + nF) {
       const int t = sub;
       const double kn = sqrt(kx * kx + ky * ky + kz * kz);
