@@ -40,9 +40,14 @@ CONFIGS = {
 }
 
 
-def ledger_flops(na, nl, ng):
-    # pipeline.cpp:336-364, refined: 20 K N_G^2 + 24 N_A N_L^2 N_G + 2 K N_G
+def ledger_flops(na, nl, ng, variant="refined"):
+    # pipeline.cpp:336-364, refined: 20 K N_G^2 + 24 N_A N_L^2 N_G + 2 K N_G.  The original
+    # variant (generate_problem(..., n_not_hpd=0): every T_AA factorises) swaps the herkx
+    # and one hemm for potrf + trmm + herk(B_T).
     K = na * nl
+    if variant == "original":
+        return (20 * K * ng * ng + 16 * na * nl * nl * ng + 2 * K * ng + na * (4 * nl ** 3 // 3)
+                + 4 * na * nl * nl * ng)
     return 20 * K * ng * ng + 24 * na * nl * nl * ng + 2 * K * ng
 
 
@@ -253,7 +258,7 @@ def run_b200(args):
     ms = d.max(ms)
     kt = eng.kernel_times(reset=True)
     st = eng.sync()
-    F = ledger_flops(na_total, nl, ng)
+    F = ledger_flops(na_total, nl, ng, "original" if args.algo == "original" else "refined")
     value = F / (ms * 1e-3) / 1e12
 
     # ---- e2e through the public API with host buffers ----
