@@ -52,6 +52,8 @@ struct alignas(64) CtnParams {
   int tiles;               // TRI: tiles per dimension
   int tiles_total;         // TRI: lower tiles t(t+1)/2
   int band;                // TRI: tile-row band of the grouped tile order (>= 1)
+  int col_t0, col_t1;      // TRI, optional: only the lower tiles with col_t0 <= tj < col_t1
+                           // (col_t1 == 0: the whole lower triangle); tiles_total = their count
   double2* out;            // TRI: packed lower.  BATCH: column-major stacked buffer
   double* sk_ws;           // TRI stream-K: per-CTA partial-accumulator slots
   uint32_t* sk_flags;      // TRI stream-K: per-CTA publish flags (== epoch when the slot is ready)
@@ -137,6 +139,26 @@ __device__ __forceinline__ void tri_tile(int t, int tiles, int kBand, int& ti, i
   }
   tj = r0 + c;
   ti = r0 + c + u;
+}
+
+// Tile t of the lower tiles restricted to tile columns [c0, c1): the triangle of rows
+// c0 .. c1-1 first (row by row), then the full-width rows c1 .. (w = c1 - c0 tiles each).
+// A column band of tiles covers a contiguous range of packed-lower storage, so a
+// build's final H contraction can run band by band with each band's download
+// overlapping the next band's compute.
+__device__ __forceinline__ void tri_tile_cols(int t, int c0, int c1, int& ti, int& tj) {
+  const int w = c1 - c0, tri = w * (w + 1) / 2;
+  if (t < tri) {
+    int r = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while ((r + 1) * (r + 2) / 2 <= t) ++r;
+    while (r * (r + 1) / 2 > t) --r;
+    ti = c0 + r;
+    tj = c0 + t - r * (r + 1) / 2;
+  } else {
+    const int u = t - tri;
+    ti = c1 + u / w;
+    tj = c0 + u % w;
+  }
 }
 
 __device__ __forceinline__ uint64_t packed_index(uint64_t n, uint64_t i, uint64_t j) {
@@ -255,7 +277,10 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>
   auto tile_origin = [&](int tile, int& row0, int& col0, int& atom) {
     if (MODE == kTri) {
       int ti, tj;
-      tri_tile(tile, P.tiles, P.band, ti, tj);
+      if (P.col_t1 > 0)
+        tri_tile_cols(tile, P.col_t0, P.col_t1, ti, tj);
+      else
+        tri_tile(tile, P.tiles, P.band, ti, tj);
       row0 = ti * BM;
       col0 = tj * BN;
       atom = 0;

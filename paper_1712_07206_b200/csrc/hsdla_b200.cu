@@ -244,6 +244,10 @@ struct hsdla_b200_engine {
               ev_reduce_end = nullptr, ev_up0 = nullptr, ev_up1 = nullptr, ev_s_d2h = nullptr;
   static constexpr int kD2hPieces = 4;   // H downloads in column-range pieces, unpacked as each lands
   cudaEvent_t ev_h_piece[kD2hPieces] = {};
+  cudaEvent_t ev_h_band[kD2hPieces] = {};  // final H contraction finished tile-column band q
+  int piece_tiles[kD2hPieces + 1] = {};    // tile-column boundaries of the pieces / bands
+  bool band_final_h = false;               // this build runs its final H contraction band by band
+  bool banded = false;                     // ... and the last build did
   std::vector<cudaEvent_t> ev_chunk_up;
   int last_algo = 0, launches = 0;
   uint64_t n_hpd_last = 0;
@@ -292,6 +296,8 @@ static void engine_free(hsdla_b200_engine* e) {
   for (cudaEvent_t ev : e->ev_pool) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e->ev_chunk_up) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e->ev_h_piece)
+    if (ev) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : e->ev_h_band)
     if (ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : {e->ev_begin, e->ev_end, e->ev_s_done, e->ev_s_red, e->ev_reduce_end, e->ev_up0, e->ev_up1,
                          e->ev_s_d2h, e->ev_setup0, e->ev_setup1})
@@ -435,7 +441,24 @@ static std::vector<uint64_t> stream_bounds(uint64_t na, uint64_t nl, uint64_t ng
   return b;
 }
 
+// Tile-column boundaries splitting the lower tiles into kD2hPieces bands of about
+// equal tile count (column tj holds T - tj tiles); the packed H range of band q is
+// columns [64 c_q, 64 c_{q+1}).
+static void make_pieces(hsdla_b200_engine* e) {
+  const int T = static_cast<int>((e->ng + kTriBM - 1) / kTriBM), Q = hsdla_b200_engine::kD2hPieces;
+  const long long total = static_cast<long long>(T) * (T + 1) / 2;
+  e->piece_tiles[0] = 0;
+  int tj = 0;
+  long long acc = 0;
+  for (int q = 1; q < Q; ++q) {
+    while (tj < T && acc + (T - tj) <= total * q / Q) acc += T - tj++;
+    e->piece_tiles[q] = tj;
+  }
+  e->piece_tiles[Q] = T;
+}
+
 static void make_plans(hsdla_b200_engine* e) {
+  make_pieces(e);
   e->whole.resize(1);
   make_chunk(e, 0, e->na, true, e->whole[0]);
   const auto b = stream_bounds(e->na, e->nl, e->ng);
@@ -476,6 +499,7 @@ static hsdla_b200_engine* engine_create(int device, uint64_t na, uint64_t nl, ui
     for (cudaEvent_t* ev : {&e->ev_s_done, &e->ev_s_red, &e->ev_s_d2h})
       HS_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     for (cudaEvent_t& ev : e->ev_h_piece) HS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    for (cudaEvent_t& ev : e->ev_h_band) HS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     for (auto& t : e->ring)
       for (cudaEvent_t* ev : {&t.s0, &t.s1, &t.h0, &t.h1}) HS_CUDA(cudaEventCreate(ev));
     const uint64_t KG = e->K * ng;
@@ -613,6 +637,33 @@ static void harvest(hsdla_b200_engine* e, hsdla_b200_engine::KTimer& t) {
 static void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool last,
                           hsdla_b200_engine::KTimer* kt) {
   cudaStream_t s = e->stream;
+  // The build's final H contraction: whole, or band by band (tile-column bands of
+  // equal work, event after each) so the download of band q overlaps band q+1.
+  auto final_h = [&](const CtnParams& P) {
+    if (!(last && e->band_final_h)) {
+      CtnParams q = P;
+      launch_tri(e, q, cp.grid_tri);
+      return;
+    }
+    int iters = 0;
+    for (int sg = 0; sg < P.nseg; ++sg) iters += P.kchunks[sg];
+    const int T = P.tiles;
+    for (int q = 0; q < hsdla_b200_engine::kD2hPieces; ++q) {
+      const int c0 = e->piece_tiles[q], c1 = e->piece_tiles[q + 1];
+      long long cnt = 0;
+      for (int tj = c0; tj < c1; ++tj) cnt += T - tj;
+      if (cnt > 0) {
+        CtnParams b = P;
+        b.col_t0 = c0;
+        b.col_t1 = c1;
+        b.tiles_total = static_cast<int>(cnt);
+        const dim3 g(static_cast<unsigned>(std::min<long long>(e->sms, cnt * iters)));
+        launch_tri(e, b, g);
+      }
+      HS_CUDA(cudaEventRecord(e->ev_h_band[q], s));
+    }
+    e->banded = true;
+  };
   const uint64_t nac = cp.a1 - cp.a0, nl = e->nl, r0 = cp.a0 * nl, Kc = nac * nl, ng = e->ng;
   const dim3 g_rows(static_cast<unsigned>((Kc + 255) / 256), static_cast<unsigned>(std::min<uint64_t>(ng, 2048)));
   auto expand = [&] {
@@ -635,9 +686,12 @@ static void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool la
     });
     if (last) HS_CUDA(cudaEventRecord(e->ev_s_done, s));
   };
-  auto timed_h = [&](CtnParams& P) {
+  auto timed_h = [&](CtnParams& P, bool final) {
     if (kt) HS_CUDA(cudaEventRecord(kt->h0, s));
-    launch_tri(e, P, cp.grid_tri);
+    if (final)
+      final_h(P);
+    else
+      launch_tri(e, P, cp.grid_tri);
     if (kt) HS_CUDA(cudaEventRecord(kt->h1, s));
   };
   if (algo == HSDLA_B200_ALGO_ORIGINAL) {
@@ -645,7 +699,7 @@ static void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool la
       expand();
       launch_bat(e, cp.z, cp.grid_bat);
     });
-    timed_op(e, HSDLA_B200_PHASE_HER2K, [&] { timed_h(cp.h2k); });
+    timed_op(e, HSDLA_B200_PHASE_HER2K, [&] { timed_h(cp.h2k, false); });
     phase_s(false);
     timed_op(e, HSDLA_B200_PHASE_CHOL_LOOP, [&] {
       potrf_batched_kernel<<<static_cast<unsigned>(nac), 128, 0, s>>>(e->Taa + cp.a0 * nl * nl,
@@ -659,19 +713,19 @@ static void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool la
       HS_CUDA(cudaGetLastError());
       ++e->launches;
     });
-    timed_op(e, HSDLA_B200_PHASE_H_AA_UPDATE, [&] { launch_tri(e, cp.haa, cp.grid_tri); });
+    timed_op(e, HSDLA_B200_PHASE_H_AA_UPDATE, [&] { final_h(cp.haa); });
     return;
   }
   phase_s(true);
   if (algo == HSDLA_B200_ALGO_REFINED) {
     timed_op(e, HSDLA_B200_PHASE_Z_LOOP, [&] { launch_bat(e, cp.z, cp.grid_bat); });
-    timed_op(e, HSDLA_B200_PHASE_HER2K, [&] { timed_h(cp.h2k); });
+    timed_op(e, HSDLA_B200_PHASE_HER2K, [&] { timed_h(cp.h2k, false); });
     timed_op(e, HSDLA_B200_PHASE_HEMM_LOOP, [&] { launch_bat(e, cp.x, cp.grid_bat); });
-    timed_op(e, HSDLA_B200_PHASE_HERKX, [&] { launch_tri(e, cp.hkx, cp.grid_tri); });
+    timed_op(e, HSDLA_B200_PHASE_HERKX, [&] { final_h(cp.hkx); });
   } else {
     timed_op(e, HSDLA_B200_PHASE_Z_LOOP, [&] { launch_bat(e, cp.zf, cp.grid_bat); });
     timed_op(e, HSDLA_B200_PHASE_HEMM_LOOP, [&] { launch_bat(e, cp.x, cp.grid_bat); });
-    timed_op(e, HSDLA_B200_PHASE_HER2K, [&] { timed_h(cp.h); });  // her2k + herkx fused
+    timed_op(e, HSDLA_B200_PHASE_HER2K, [&] { timed_h(cp.h, true); });  // her2k + herkx fused
   }
 }
 
@@ -691,6 +745,7 @@ static void begin_build(hsdla_b200_engine* e, int algo) {
   e->ev_used = 0;
   e->ops.clear();
   e->built = true;
+  e->banded = false;
 }
 
 // Device-resident build: one chunk over all atoms (the bench's `value`).
@@ -811,15 +866,9 @@ static void unpack_lower(const double2* pk, double2* full, uint64_t n, uint64_t 
   for (auto& t : th) t.join();
 }
 
-// Column boundaries of the kD2hPieces H download pieces (equal packed sizes).
-static uint64_t piece_col(uint64_t n, int q, int pieces) {
-  const uint64_t target = packed_col(n, n) * q / pieces;
-  uint64_t lo = 0, hi = n;  // first column whose packed start >= target
-  while (lo < hi) {
-    const uint64_t mid = (lo + hi) / 2;
-    if (packed_col(n, mid) < target) lo = mid + 1; else hi = mid;
-  }
-  return lo;
+// First matrix column of download piece q (= tile-column band q of the final H launch).
+static uint64_t piece_col(const hsdla_b200_engine* e, int q) {
+  return std::min<uint64_t>(e->ng, static_cast<uint64_t>(e->piece_tiles[q]) * kTriBM);
 }
 
 static void ensure_stage(hsdla_b200_engine* e) {
@@ -835,10 +884,10 @@ static void enqueue_download(hsdla_b200_engine* e) {
   HS_CUDA(cudaStreamWaitEvent(e->copy_stream, e->reduced ? e->ev_s_red : e->ev_s_done, 0));
   HS_CUDA(cudaMemcpyAsync(e->host_stage + e->npk, e->Sp, bytes, cudaMemcpyDeviceToHost, e->copy_stream));
   HS_CUDA(cudaEventRecord(e->ev_s_d2h, e->copy_stream));
-  HS_CUDA(cudaStreamWaitEvent(e->copy_stream, e->reduced ? e->ev_reduce_end : e->ev_end, 0));
+  if (!e->banded) HS_CUDA(cudaStreamWaitEvent(e->copy_stream, e->reduced ? e->ev_reduce_end : e->ev_end, 0));
   for (int q = 0; q < hsdla_b200_engine::kD2hPieces; ++q) {
-    const uint64_t b0 = packed_col(e->ng, piece_col(e->ng, q, hsdla_b200_engine::kD2hPieces));
-    const uint64_t b1 = packed_col(e->ng, piece_col(e->ng, q + 1, hsdla_b200_engine::kD2hPieces));
+    if (e->banded) HS_CUDA(cudaStreamWaitEvent(e->copy_stream, e->ev_h_band[q], 0));
+    const uint64_t b0 = packed_col(e->ng, piece_col(e, q)), b1 = packed_col(e->ng, piece_col(e, q + 1));
     if (b1 > b0)
       HS_CUDA(cudaMemcpyAsync(e->host_stage + b0, e->Hp + b0, (b1 - b0) * sizeof(double2), cudaMemcpyDeviceToHost,
                               e->copy_stream));
@@ -854,9 +903,7 @@ static void finish_download(hsdla_b200_engine* e, double* H, double* S) {
   for (int q = 0; q < hsdla_b200_engine::kD2hPieces; ++q) {
     HS_CUDA(cudaEventSynchronize(e->ev_h_piece[q]));
     if (H)
-      unpack_lower(e->host_stage, reinterpret_cast<double2*>(H), e->ng,
-                   piece_col(e->ng, q, hsdla_b200_engine::kD2hPieces),
-                   piece_col(e->ng, q + 1, hsdla_b200_engine::kD2hPieces));
+      unpack_lower(e->host_stage, reinterpret_cast<double2*>(H), e->ng, piece_col(e, q), piece_col(e, q + 1));
   }
 }
 
@@ -1309,7 +1356,18 @@ static void one_shot(const hsdla_b200_options* o, uint64_t na, uint64_t nl, uint
   std::lock_guard<std::mutex> lk(g_cache_mu);
   EngineSet* set = get_engines(devs, na, nl, ng);
   double load_s = 0;
-  for (int r = 0; r < P; ++r) load_s = std::max(load_s, start(set->engines[r], set->atom0[r], algo));
+  for (int r = 0; r < P; ++r) {
+    hsdla_b200_engine* e = set->engines[r];
+    // one GPU: the final H contraction runs band by band so H's download overlaps it
+    e->band_final_h = P == 1;
+    try {
+      load_s = std::max(load_s, start(e, set->atom0[r], algo));
+    } catch (...) {
+      e->band_final_h = false;
+      throw;
+    }
+    e->band_final_h = false;
+  }
   if (P > 1) {
     HS_NCCL(ncclGroupStart());
     for (int r = 0; r < P; ++r) reduce_s(set->engines[r], 0);

@@ -177,3 +177,21 @@ def test_algos_agree():
     b = hb.build_hs_refined(p, hb.PipelineConfig(algo="refined"))
     assert rel(a.H, b.H) <= 1e-13 and rel(a.S, b.S) == 0.0
     assert a.stats["kernel_launches"] >= 5
+
+
+@pytest.mark.parametrize("algo", ["fused", "refined", "original"])
+def test_banded_final_h_matches_device_resident(algo):
+    """The one-shot drop-in runs its final H contraction in tile-column bands (each band's
+    download overlapping the next band); the device-resident engine runs it whole.
+    Both agree to rounding, and the bands cover every lower tile exactly once."""
+    for dims in ((24, 81, 2200, 9, 3), (3, 7, 70, 2, 1), (2, 5, 130, 4, 0)):
+        p = hb.generate_problem(*dims)
+        cfg = hb.PipelineConfig(variant="original") if algo == "original" else hb.PipelineConfig(algo=algo)
+        r = hb.build_hs(p, cfg)
+        e = hb.Engine(0, p.n_atoms, p.n_l, p.n_g)
+        e.upload(p)
+        e.build(algo)
+        e.sync()
+        H, S = e.download()
+        e.close()
+        assert rel(r.H, H) <= 1e-14 and rel(r.S, S) <= 1e-14, dims

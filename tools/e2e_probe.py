@@ -24,7 +24,20 @@ for name in sys.argv[1:] or ["c2"]:
         st = r.stats
         print(f"{name} call {it}: wall {dt*1e3:.2f} ms ({led/dt/1e12:.2f} TF/s)  total {st['total_seconds']*1e3:.2f}  "
               f"h2d {st['h2d_seconds']*1e3:.2f}  device {st['device_seconds']*1e3:.2f}  d2h+unpack {st['d2h_seconds']*1e3:.2f}"
-              f"  launches {st['kernel_launches']}", flush=True)
+              f"  launches {st['kernel_launches']}  phases " + " ".join(f"{k}:{v*1e3:.2f}" for k, v in st["phase_seconds"].items()), flush=True)
+    e = hb.Engine(0, na, nl, ng)
+    for it in range(3):
+        e.build_streamed(p, 0)
+        st = e.sync()
+    print(f"{name} engine streamed: device {st['device_seconds']*1e3:.2f} h2d {st['h2d_seconds']*1e3:.2f} phases " +
+          " ".join(f"{k}:{v*1e3:.2f}" for k, v in st["phase_seconds"].items()))
+    e.upload(p)
+    for it in range(3):
+        e.build()
+        st = e.sync()
+    print(f"{name} engine whole: device {st['device_seconds']*1e3:.2f} phases " +
+          " ".join(f"{k}:{v*1e3:.2f}" for k, v in st["phase_seconds"].items()))
+    e.close()
     for b in bufs:
         hb.host_unregister(b)
     hb.release_cache()
