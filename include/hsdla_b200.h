@@ -130,11 +130,41 @@ int hsdla_b200_flop_model(int variant, uint64_t n_atoms, uint64_t n_l, uint64_t 
 
 /* kernels::potrf (kernels.cpp:417-436) for n_blocks lower-authoritative n_l x n_l
  * blocks (T, contiguous column-major blocks) on `device`.  L receives, per block,
- * the full factor (upper exactly 0) when it factorises, else the Hermitian
- * expansion of T (the hemm operand the original algorithm falls back to);
+ * the full factor (upper exactly 0) when it factorises, else the operand Q with
+ * Q^H = T read from its lower triangle (full(T) with the diagonal conjugated: the
+ * hemm operand the original algorithm falls back to);
  * pivot[b] = -1 on success, else the failing pivot (PotrfResult::pivot).  Same
  * operation order as the reference with no FMA contraction: bit-identical. */
 int hsdla_b200_potrf(int device, uint64_t n_blocks, uint64_t n_l, const double* T, double* L, int64_t* pivot);
+
+/* ---- the reference kernel layer on the GPU (hsdla::kernels, kernels.hpp:24-75) ---
+ * Host matrices (interleaved complex, column-major, leading dimension in complex
+ * elements); each call uploads, runs the sm_100a contraction engine and downloads.
+ * alpha / beta marked `const double*` are complex (re, im).  Contracts of the
+ * reference kernels: herk / her2k / herkx read and write only the LOWER triangle of
+ * C (diagonal imaginary parts := 0, kernels.cpp:112,130,145); beta == 0 never
+ * reads C; alpha == 0 only scales C by beta; hemm reads only H's lower triangle;
+ * trmm uses only T's lower triangle.  ledger_flops (nullable) is INCREMENTED by the
+ * reference's closed-form charge (kernels.cpp:254,296,316,339,363,390,444),
+ * independent of alpha / beta.  Shapes as in kernels.hpp: herk A k x n; her2k /
+ * herkx A, B k x n; gemm op(A) m x k, op(B) k x n (trans 0 None, 1 ConjTrans);
+ * hemm H n x n, B, C n x m; trmm T n x n, B n x m in place; diag_scale X = diag(u) B
+ * (X may alias B). */
+int hsdla_b200_herk(int device, uint64_t n, uint64_t k, double alpha, const double* A, uint64_t lda, double beta,
+                    double* C, uint64_t ldc, uint64_t* ledger_flops);
+int hsdla_b200_her2k(int device, uint64_t n, uint64_t k, const double* alpha, const double* A, uint64_t lda,
+                     const double* B, uint64_t ldb, double beta, double* C, uint64_t ldc, uint64_t* ledger_flops);
+int hsdla_b200_herkx(int device, uint64_t n, uint64_t k, const double* alpha, const double* A, uint64_t lda,
+                     const double* B, uint64_t ldb, double beta, double* C, uint64_t ldc, uint64_t* ledger_flops);
+int hsdla_b200_gemm(int device, int trans_a, int trans_b, uint64_t m, uint64_t n, uint64_t k, const double* alpha,
+                    const double* A, uint64_t lda, const double* B, uint64_t ldb, const double* beta, double* C,
+                    uint64_t ldc, uint64_t* ledger_flops);
+int hsdla_b200_hemm(int device, uint64_t n, uint64_t m, const double* alpha, const double* H, uint64_t ldh,
+                    const double* B, uint64_t ldb, const double* beta, double* C, uint64_t ldc, uint64_t* ledger_flops);
+int hsdla_b200_trmm(int device, int trans, uint64_t n, uint64_t m, const double* alpha, const double* T, uint64_t ldt,
+                    double* B, uint64_t ldb, uint64_t* ledger_flops);
+int hsdla_b200_diag_scale(int device, uint64_t rows, uint64_t cols, const double* u, const double* B, uint64_t ldb,
+                          double* X, uint64_t ldx, uint64_t* ledger_flops);
 
 /* generate_problem (problem.cpp:79-142), bit-identical to the reference
  * (std::mt19937_64 + the reference's double mapping).  Output layouts as above;

@@ -15,3 +15,4 @@ from .pipeline import (Engine, FlopLedger, HSResult, PhaseTime, PipelineConfig, 
 from .problem import (Preset, ProblemInstance, empty_problem, find_preset, generate_problem,  # noqa: F401
                       load_problem, presets, save_problem)
 from .lapw import LapwSystem, build_hs_lapw, lapw_coefficients, make_lapw_system  # noqa: F401,E402
+from . import kernels  # noqa: F401,E402

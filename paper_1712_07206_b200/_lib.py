@@ -31,6 +31,8 @@ EXPORTS = (
     "hsdla_b200_lapw_coefficients", "hsdla_b200_engine_setup_lapw", "hsdla_b200_engine_upload_operators",
     "hsdla_b200_engine_setup_time", "hsdla_b200_problem_file_info", "hsdla_b200_build_hs_file",
     "hsdla_b200_engine_load", "hsdla_b200_engine_fill_synthetic",
+    "hsdla_b200_herk", "hsdla_b200_her2k", "hsdla_b200_herkx", "hsdla_b200_gemm", "hsdla_b200_hemm",
+    "hsdla_b200_trmm", "hsdla_b200_diag_scale",
 )
 
 

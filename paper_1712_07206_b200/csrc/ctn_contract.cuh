@@ -59,6 +59,9 @@ struct alignas(64) CtnParams {
   uint32_t* sk_flags;      // TRI stream-K: per-CTA publish flags (== epoch when the slot is ready)
   uint32_t epoch;          // TRI stream-K: unique per launch
   uint64_t ldo;            // BATCH: output leading dimension (complex elements)
+  const int* keep_diag_imag;  // TRI, optional: when non-null and *keep_diag_imag != 0 the diagonal's
+                              // imaginary part is kept (the original algorithm's full-gemm fold,
+                              // pipeline.cpp:266-271, does not zero it); else forced to 0
   double alpha_re, alpha_im;
   double beta;             // real; 0 => C is never read
 };
@@ -459,6 +462,7 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>
       int row0, col0, atom;
       tile_origin(pc.tile, row0, col0, atom);
       const double ar = P.alpha_re, ai = P.alpha_im, beta = P.beta;
+      const bool keep_di = MODE == kTri && P.keep_diag_imag != nullptr && *P.keep_diag_imag != 0;
 #pragma unroll
       for (int mb = 0; mb < MB; ++mb) {
         const int i = row0 + wm * Cfg::kWM + 8 * mb + pg;
@@ -472,7 +476,7 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>
             double vi = ar * xi + ai * xr;
             if (MODE == kTri) {
               if (i < P.n && j < P.n && i >= j) {
-                if (i == j) vi = 0.0;
+                if (i == j && !keep_di) vi = 0.0;
                 double2* dst = P.out + packed_index(P.n, i, j);
                 if (beta != 0.0) {
                   const double2 o = *dst;

@@ -122,9 +122,12 @@ __global__ void fill_uniform_kernel(double* __restrict__ p, uint64_t n, uint64_t
   }
 }
 
-// Hermitian expansion from the LOWER triangle (kernels.cpp:152-167 reads only
-// h[l*ldh+i] for l <= i and conj(h[i*ldh+l]) above):
-//   Pbb[a](k,i) = 1/2 * T_BB[a](k,i),  Paa[a](k,i) = T_AA[a](k,i)  (full Hermitian)
+// Left operands P with P^H = the reference's hemm operator, from the LOWER triangle
+// only (kernels.cpp:152-167 uses h(i,l) for l <= i — the diagonal as stored — and
+// conj(h(l,i)) for l > i).  The contraction computes P^H R, so
+//   P(k,i) = conj(T(i,k)) for k <= i,  T(k,i) for k > i
+// (= full(T) with the diagonal conjugated; identical for a real diagonal).
+//   Pbb[a] = 1/2 * P(T_BB[a]),  Paa[a] = P(T_AA[a])
 __global__ void expand_hermitian_kernel(const double2* __restrict__ taa, const double2* __restrict__ tbb,
                                         double2* __restrict__ paa, double2* __restrict__ pbb, int nl,
                                         uint64_t total) {
@@ -137,7 +140,7 @@ __global__ void expand_hermitian_kernel(const double2* __restrict__ taa, const d
   const uint64_t lo =
       a * blk + (k >= i ? (k + static_cast<uint64_t>(i) * nl) : (i + static_cast<uint64_t>(k) * nl));
   double2 vaa = taa[lo], vbb = tbb[lo];
-  if (k < i) {
+  if (k <= i) {
     vaa.y = -vaa.y;
     vbb.y = -vbb.y;
   }
@@ -225,6 +228,7 @@ struct hsdla_b200_engine {
   double2 *Tab = nullptr, *Taa = nullptr, *Tbb = nullptr, *Paa = nullptr, *Pbb = nullptr;
   double* U = nullptr;
   int32_t* info = nullptr;        // per-atom potrf result of the original algorithm (-1 = HPD)
+  int* n_fail = nullptr;          // original algorithm: failed atoms so far in this build
   double2 *Hp = nullptr, *Sp = nullptr;
   double2* host_stage = nullptr;  // pinned, 2 * npk
   int sms = 148;                  // persistent TRI grid
@@ -288,7 +292,7 @@ static void dalloc(hsdla_b200_engine* e, T** p, uint64_t count) {
 
 static void engine_free(hsdla_b200_engine* e) {
   cudaSetDevice(e->device);
-  for (void* p : {e->lapw_scratch, (void*)e->info, (void*)e->sk_ws, (void*)e->sk_flags, (void*)e->A, (void*)e->B, (void*)e->X1, (void*)e->X2,
+  for (void* p : {e->lapw_scratch, (void*)e->info, (void*)e->n_fail, (void*)e->sk_ws, (void*)e->sk_flags, (void*)e->A, (void*)e->B, (void*)e->X1, (void*)e->X2,
                   (void*)e->Tab, (void*)e->Taa, (void*)e->Tbb, (void*)e->Paa, (void*)e->Pbb, (void*)e->U,
                   (void*)e->Hp, (void*)e->Sp})
     if (p) cudaFree(p);
@@ -372,6 +376,7 @@ static void make_chunk(hsdla_b200_engine* e, uint64_t a0, uint64_t a1, bool firs
   tri_base(cp.haa, e->Hp, 1.0);
   set_seg(cp.haa, 0, mX2, mX1, Kc);
   cp.haa.nseg = 1;
+  cp.haa.keep_diag_imag = e->n_fail;  // keep the fold's diagonal imaginary part once an atom failed
   // persistent stream-K grid: one CTA per SM, never more CTAs than k-iterations
   const uint64_t tri_tiles = static_cast<uint64_t>(tiles) * (tiles + 1) / 2;
   cp.grid_tri = dim3(static_cast<unsigned>(std::min<uint64_t>(e->sms, tri_tiles * chunks_of(Kc))));
@@ -514,6 +519,7 @@ static hsdla_b200_engine* engine_create(int device, uint64_t na, uint64_t nl, ui
     dalloc(e.get(), &e->Pbb, na * nl * nl);
     dalloc(e.get(), &e->U, e->K);
     dalloc(e.get(), &e->info, na);
+    dalloc(e.get(), &e->n_fail, 1);
     dalloc(e.get(), &e->Hp, e->npk);
     dalloc(e.get(), &e->Sp, e->npk);
     HS_CUDA(cudaDeviceGetAttribute(&e->sms, cudaDevAttrMultiProcessorCount, device));
@@ -702,9 +708,10 @@ static void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool la
     timed_op(e, HSDLA_B200_PHASE_HER2K, [&] { timed_h(cp.h2k, false); });
     phase_s(false);
     timed_op(e, HSDLA_B200_PHASE_CHOL_LOOP, [&] {
+      if (cp.a0 == 0) HS_CUDA(cudaMemsetAsync(e->n_fail, 0, sizeof(int), s));  // first chunk of the build
       potrf_batched_kernel<<<static_cast<unsigned>(nac), 128, 0, s>>>(e->Taa + cp.a0 * nl * nl,
                                                                       e->Paa + cp.a0 * nl * nl, e->info + cp.a0,
-                                                                      static_cast<int>(nl));
+                                                                      static_cast<int>(nl), e->n_fail);
       HS_CUDA(cudaGetLastError());
       ++e->launches;
       launch_bat(e, cp.x, cp.grid_bat);  // W_a = Q_a^H A_a: trmm (HPD) or hemm (failed)
@@ -1420,6 +1427,232 @@ static void one_shot(const hsdla_b200_options* o, uint64_t na, uint64_t nl, uint
   }
 }
 
+// ---------------------------------------------------------------------------
+// The reference's kernel layer (hsdla::kernels, kernels.hpp:24-75) on the GPU.
+// Host matrices in and out (interleaved complex, column-major, explicit leading
+// dimensions), one call = upload, the contraction engine, download.  Same
+// semantics as the reference: triangular outputs lower only (upper never read or
+// written), beta == 0 never reads C, alpha == 0 only scales C (and still charges
+// the closed-form ledger), dimension errors -> DimensionError.
+// ---------------------------------------------------------------------------
+namespace kl {
+
+struct DevBuf {
+  void* p = nullptr;
+  DevBuf() = default;
+  explicit DevBuf(size_t bytes) { HS_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16))); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  double2* c() const { return static_cast<double2*>(p); }
+};
+
+__global__ void scale_kernel(double2* __restrict__ x, uint64_t rows, uint64_t cols, double br, double bi,
+                             int lower_only) {
+  for (uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < rows * cols;
+       idx += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t i = idx % rows, j = idx / rows;
+    if (lower_only && i < j) continue;
+    const double2 v = x[idx];
+    // beta == 0 writes an exact 0 without reading (scale_in_place, kernels.cpp:200-207)
+    x[idx] = (br == 0.0 && bi == 0.0) ? make_double2(0.0, 0.0) : make_double2(br * v.x - bi * v.y, br * v.y + bi * v.x);
+  }
+}
+
+// dst (c x r) = conj(src (r x c))^T, dense; with `lower` only src's lower triangle
+// (i >= j) is used (the rest is taken as 0) — the triangular operand of trmm.
+__global__ void conj_transpose_kernel(const double2* __restrict__ src, double2* __restrict__ dst, uint64_t r,
+                                      uint64_t c, int lower, int transpose) {
+  for (uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < r * c;
+       idx += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t i = idx % r, j = idx / r;  // source element (i, j)
+    double2 v = src[idx];
+    if (lower && i < j) v = make_double2(0.0, 0.0);
+    if (transpose)
+      dst[j + i * c] = make_double2(v.x, -v.y);
+    else
+      dst[idx] = v;
+  }
+}
+
+// The left operand L with L^H = the hemm operator of an n x n lower-authoritative H
+// (kernels.cpp:152-167: h(i,l) for l <= i, conj(h(l,i)) above):
+//   L(i,j) = h(i,j) for i > j,  conj(h(j,i)) for i <= j.
+__global__ void hermitian_full_kernel(const double2* __restrict__ h, double2* __restrict__ f, uint64_t n) {
+  for (uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < n * n;
+       idx += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t i = idx % n, j = idx / n;
+    double2 v = i > j ? h[i + j * n] : h[j + i * n];
+    if (i <= j) v.y = -v.y;
+    f[idx] = v;
+  }
+}
+
+__global__ void pack_lower_kernel(const double2* __restrict__ full, double2* __restrict__ pk, uint64_t n, int unpack) {
+  for (uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < n * n;
+       idx += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t i = idx % n, j = idx / n;
+    if (i < j) continue;
+    const uint64_t k = j * (2 * n - j + 1) / 2 + (i - j);
+    if (unpack)
+      const_cast<double2*>(full)[idx] = pk[k];
+    else
+      pk[k] = full[idx];
+  }
+}
+
+struct Ctx {
+  int sms = 148;
+  cudaStream_t s = nullptr;
+  explicit Ctx(int device) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+      (void)cudaGetLastError();
+      throw Fail{HSDLA_B200_CONFIG_ERROR, "no such CUDA device (the B200 path has no CPU fallback)"};
+    }
+    HS_CUDA(cudaSetDevice(device));
+    HS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    HS_CUDA(cudaFuncSetAttribute(tri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TriCfg::kSmemBytes));
+    HS_CUDA(cudaFuncSetAttribute(bat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BatCfg::kSmemBytes));
+    HS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  }
+  ~Ctx() {
+    if (s) cudaStreamDestroy(s);
+  }
+  unsigned grid(uint64_t n) const {
+    return static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(sms) * 16) + 0);
+  }
+  void up(double2* d, const double* h, uint64_t r, uint64_t c, uint64_t ld) {
+    if (r && c) HS_CUDA(cudaMemcpy2DAsync(d, r * 16, h, ld * 16, r * 16, c, cudaMemcpyHostToDevice, s));
+  }
+  void down(double* h, uint64_t ld, const double2* d, uint64_t r, uint64_t c) {
+    if (r && c) HS_CUDA(cudaMemcpy2DAsync(h, ld * 16, d, r * 16, r * 16, c, cudaMemcpyDeviceToHost, s));
+  }
+  void sync() { HS_CUDA(cudaStreamSynchronize(s)); }
+};
+
+static void need(bool ok, const char* what) {
+  if (!ok) throw Fail{HSDLA_B200_DIMENSION_ERROR, what};
+}
+
+// C(lower, n x n, device packed) = alpha * sum_s L_s^H R_s + beta * C over dense k x n operands.
+static void tri(Ctx& x, int nseg, const double2* const* L, const double2* const* R, uint64_t k, uint64_t n, double ar,
+                double ai, double beta, double2* Cp) {
+  const int tiles = static_cast<int>((n + kTriBM - 1) / kTriBM);
+  CtnParams P;
+  std::memset(&P, 0, sizeof(P));
+  for (int sg = 0; sg < nseg; ++sg) {
+    make_map(&P.L[sg], L[sg], 2 * k, n, 1, 2 * k, 2 * k * n, kTriBM, 1);
+    make_map(&P.R[sg], R[sg], 2 * k, n, 1, 2 * k, 2 * k * n, kTriBM, 1);
+    P.kchunks[sg] = chunks_of(k);
+  }
+  P.nseg = nseg;
+  P.n = static_cast<int>(n);
+  P.tiles = tiles;
+  P.tiles_total = tiles * (tiles + 1) / 2;
+  P.band = tri_band();
+  P.out = Cp;
+  DevBuf ws(static_cast<size_t>(x.sms) * kTriBM * kTriBM * 2 * sizeof(double)), flags(x.sms * sizeof(uint32_t));
+  HS_CUDA(cudaMemsetAsync(flags.p, 0, x.sms * sizeof(uint32_t), x.s));
+  P.sk_ws = static_cast<double*>(ws.p);
+  P.sk_flags = static_cast<uint32_t*>(flags.p);
+  P.epoch = 1;
+  P.alpha_re = ar;
+  P.alpha_im = ai;
+  P.beta = beta;
+  const uint64_t work = static_cast<uint64_t>(P.tiles_total) * chunks_of(k) * nseg;
+  const dim3 g(static_cast<unsigned>(std::min<uint64_t>(x.sms, work)));
+  tri_kernel<<<g, TriCfg::kThreads, TriCfg::kSmemBytes, x.s>>>(P);
+  HS_CUDA(cudaGetLastError());
+  x.sync();  // ws / flags go out of scope
+}
+
+// C (m x n, device dense, ld m) = alpha L^H R + beta C; L: k x m, R: k x n dense.
+static void rect(Ctx& x, const double2* L, const double2* R, uint64_t m, uint64_t n, uint64_t k, double ar, double ai,
+                 double beta, double2* C) {
+  CtnParams P;
+  std::memset(&P, 0, sizeof(P));
+  make_map(&P.L[0], L, 2 * k, m, 1, 2 * k, 2 * k * m, kBatBM, 1);
+  make_map(&P.R[0], R, 2 * k, 1, n, 2 * k, 2 * k, 1, kBatBN);
+  P.kchunks[0] = chunks_of(k);
+  P.r_row_z[0] = 1;
+  P.nseg = 1;
+  P.n = static_cast<int>(n);
+  P.m_valid = static_cast<int>(m);
+  P.out = C;
+  P.ldo = m;
+  P.alpha_re = ar;
+  P.alpha_im = ai;
+  P.beta = beta;
+  const dim3 g(static_cast<unsigned>((n + kBatBN - 1) / kBatBN), static_cast<unsigned>((m + kBatBM - 1) / kBatBM), 1);
+  if (g.y > 65535) throw Fail{HSDLA_B200_SIZING_ERROR, "rows exceed the batched-contraction grid"};
+  bat_kernel<<<g, BatCfg::kThreads, BatCfg::kSmemBytes, x.s>>>(P);
+  HS_CUDA(cudaGetLastError());
+}
+
+// Triangular family: herk (nseg 1, R = L), her2k (2), herkx (1).  C lower n x n host.
+static void tri_family(int device, int which, uint64_t n, uint64_t k, double ar, double ai, const double* A,
+                       uint64_t lda, const double* B, uint64_t ldb, double beta, double* C, uint64_t ldc) {
+  need(C != nullptr && ldc >= std::max<uint64_t>(n, 1), "C: null or ldc < n");
+  need(A != nullptr && lda >= std::max<uint64_t>(k, 1), "A: null or lda < k");
+  if (which != 0) need(B != nullptr && ldb >= std::max<uint64_t>(k, 1), "B: null or ldb < k");
+  if (n == 0) return;
+  Ctx x(device);
+  const uint64_t npk = n * (n + 1) / 2;
+  DevBuf dC(n * n * 16), dP(npk * 16);
+  const bool alpha0 = (ar == 0.0 && ai == 0.0) || k == 0;
+  if (beta != 0.0 || alpha0) x.up(dC.c(), C, n, n, ldc);
+  if (alpha0) {  // scale_lower_in_place (kernels.cpp:209-217): only C's lower triangle
+    scale_kernel<<<x.grid(n * n), 256, 0, x.s>>>(dC.c(), n, n, beta, 0.0, 1);
+  } else {
+    if (beta != 0.0) pack_lower_kernel<<<x.grid(n * n), 256, 0, x.s>>>(dC.c(), dP.c(), n, 0);
+    DevBuf dA(k * n * 16), dB(which != 0 ? k * n * 16 : 16);
+    x.up(dA.c(), A, k, n, lda);
+    if (which != 0) x.up(dB.c(), B, k, n, ldb);
+    if (which == 0) {
+      const double2* L[1] = {dA.c()};
+      tri(x, 1, L, L, k, n, ar, 0.0, beta, dP.c());
+    } else if (which == 1) {
+      // her2k: alpha A^H B + conj(alpha) B^H A = (conj(alpha) A)^H B + B^H (conj(alpha) A)
+      scale_kernel<<<x.grid(k * n), 256, 0, x.s>>>(dA.c(), k, n, ar, -ai, 0);
+      const double2* L[2] = {dA.c(), dB.c()};
+      const double2* R[2] = {dB.c(), dA.c()};
+      tri(x, 2, L, R, k, n, 1.0, 0.0, beta, dP.c());
+    } else {
+      const double2* L[1] = {dA.c()};
+      const double2* R[1] = {dB.c()};
+      tri(x, 1, L, R, k, n, ar, ai, beta, dP.c());
+    }
+    pack_lower_kernel<<<x.grid(n * n), 256, 0, x.s>>>(dC.c(), dP.c(), n, 1);
+  }
+  HS_CUDA(cudaGetLastError());
+  // lower triangle back into the caller's C, column by column (upper never written)
+  std::vector<double2> h(n * n);
+  HS_CUDA(cudaMemcpyAsync(h.data(), dC.p, n * n * 16, cudaMemcpyDeviceToHost, x.s));
+  x.sync();
+  for (uint64_t j = 0; j < n; ++j)
+    std::memcpy(reinterpret_cast<double2*>(C) + j * ldc + j, h.data() + j * n + j, (n - j) * 16);
+}
+
+// gemm core on device operands: C (m x n) = alpha opA^H-form ... + beta C, complex beta.
+static void gemm_dev(Ctx& x, const double2* Lk, const double2* Rk, uint64_t m, uint64_t n, uint64_t k, double ar,
+                     double ai, double br, double bi, double2* dC) {
+  double beta = 0.0;
+  if (br != 0.0 || bi != 0.0) {
+    if (!(br == 1.0 && bi == 0.0)) scale_kernel<<<x.grid(m * n), 256, 0, x.s>>>(dC, m, n, br, bi, 0);
+    beta = 1.0;
+  }
+  if ((ar == 0.0 && ai == 0.0) || k == 0) {
+    if (beta == 0.0) scale_kernel<<<x.grid(m * n), 256, 0, x.s>>>(dC, m, n, 0.0, 0.0, 0);
+    return;
+  }
+  rect(x, Lk, Rk, m, n, k, ar, ai, beta, dC);
+}
+
+}  // namespace kl
+
 }  // namespace hsdla_b200
 
 // ===========================================================================
@@ -1727,6 +1960,136 @@ int hsdla_b200_build_hs_file(const char* path, const hsdla_b200_options* o, doub
       engine_build(e, algo);
       return load_s;
     });
+  });
+}
+
+// ---- the reference kernel layer (kernels.hpp) --------------------------------
+int hsdla_b200_herk(int device, uint64_t n, uint64_t k, double alpha, const double* A, uint64_t lda, double beta,
+                    double* C, uint64_t ldc, uint64_t* ledger_flops) {
+  return guarded([&] {
+    kl::tri_family(device, 0, n, k, alpha, 0.0, A, lda, nullptr, 0, beta, C, ldc);
+    if (ledger_flops) *ledger_flops += 4 * k * n * n;  // kernels.cpp:316
+  });
+}
+int hsdla_b200_her2k(int device, uint64_t n, uint64_t k, const double* alpha, const double* A, uint64_t lda,
+                     const double* B, uint64_t ldb, double beta, double* C, uint64_t ldc, uint64_t* ledger_flops) {
+  return guarded([&] {
+    kl::need(alpha != nullptr, "null alpha");
+    kl::tri_family(device, 1, n, k, alpha[0], alpha[1], A, lda, B, ldb, beta, C, ldc);
+    if (ledger_flops) *ledger_flops += 8 * k * n * n;  // kernels.cpp:339
+  });
+}
+int hsdla_b200_herkx(int device, uint64_t n, uint64_t k, const double* alpha, const double* A, uint64_t lda,
+                     const double* B, uint64_t ldb, double beta, double* C, uint64_t ldc, uint64_t* ledger_flops) {
+  return guarded([&] {
+    kl::need(alpha != nullptr, "null alpha");
+    kl::tri_family(device, 2, n, k, alpha[0], alpha[1], A, lda, B, ldb, beta, C, ldc);
+    if (ledger_flops) *ledger_flops += 4 * k * n * n;  // kernels.cpp:363
+  });
+}
+
+int hsdla_b200_gemm(int device, int trans_a, int trans_b, uint64_t m, uint64_t n, uint64_t k, const double* alpha,
+                    const double* A, uint64_t lda, const double* B, uint64_t ldb, const double* beta, double* C,
+                    uint64_t ldc, uint64_t* ledger_flops) {
+  return guarded([&] {
+    kl::need(alpha && beta, "null alpha / beta");
+    kl::need((trans_a == 0 || trans_a == 1) && (trans_b == 0 || trans_b == 1), "trans must be 0 (None) or 1 (ConjTrans)");
+    // op(A) is m x k: A stored m x k (None) or k x m (ConjTrans); op(B) k x n: B k x n / n x k
+    const uint64_t ar = trans_a ? k : m, ac = trans_a ? m : k, br = trans_b ? n : k, bc = trans_b ? k : n;
+    kl::need(A && lda >= std::max<uint64_t>(ar, 1), "A: null or lda too small");
+    kl::need(B && ldb >= std::max<uint64_t>(br, 1), "B: null or ldb too small");
+    kl::need(C && ldc >= std::max<uint64_t>(m, 1), "C: null or ldc < m");
+    if (m && n) {
+      kl::Ctx x(device);
+      kl::DevBuf dA(ar * ac * 16), dB(br * bc * 16), dL(k * m * 16), dR(k * n * 16), dC(m * n * 16);
+      x.up(dA.c(), A, ar, ac, lda);
+      x.up(dB.c(), B, br, bc, ldb);
+      if (beta[0] != 0.0 || beta[1] != 0.0) x.up(dC.c(), C, m, n, ldc);
+      // the CTN core needs op(A)^H (k x m) and op(B) (k x n): conj-transpose where needed
+      // (the reference materialises the same conj transposes, kernels.cpp:262-271)
+      const double2* L = dA.c();
+      const double2* R = dB.c();
+      if (!trans_a && ar * ac) {
+        kl::conj_transpose_kernel<<<x.grid(ar * ac), 256, 0, x.s>>>(dA.c(), dL.c(), ar, ac, 0, 1);
+        L = dL.c();
+      }
+      if (trans_b && br * bc) {
+        kl::conj_transpose_kernel<<<x.grid(br * bc), 256, 0, x.s>>>(dB.c(), dR.c(), br, bc, 0, 1);
+        R = dR.c();
+      }
+      kl::gemm_dev(x, L, R, m, n, k, alpha[0], alpha[1], beta[0], beta[1], dC.c());
+      HS_CUDA(cudaGetLastError());
+      x.down(C, ldc, dC.c(), m, n);
+      x.sync();
+    }
+    if (ledger_flops) *ledger_flops += 8 * m * n * k;  // kernels.cpp:254
+  });
+}
+
+int hsdla_b200_hemm(int device, uint64_t n, uint64_t m, const double* alpha, const double* Hm, uint64_t ldh,
+                    const double* B, uint64_t ldb, const double* beta, double* C, uint64_t ldc, uint64_t* ledger_flops) {
+  return guarded([&] {
+    kl::need(alpha && beta, "null alpha / beta");
+    kl::need(Hm && ldh >= std::max<uint64_t>(n, 1), "H: null or ldh < n");
+    kl::need(B && ldb >= std::max<uint64_t>(n, 1), "B: null or ldb < n");
+    kl::need(C && ldc >= std::max<uint64_t>(n, 1), "C: null or ldc < n");
+    if (n && m) {
+      kl::Ctx x(device);
+      kl::DevBuf dH(n * n * 16), dF(n * n * 16), dB(n * m * 16), dC(n * m * 16);
+      x.up(dH.c(), Hm, n, n, ldh);
+      x.up(dB.c(), B, n, m, ldb);
+      if (beta[0] != 0.0 || beta[1] != 0.0) x.up(dC.c(), C, n, m, ldc);
+      // H B = L^H B with L^H = the reference's hemm operator (the CTN core)
+      kl::hermitian_full_kernel<<<x.grid(n * n), 256, 0, x.s>>>(dH.c(), dF.c(), n);
+      kl::gemm_dev(x, dF.c(), dB.c(), n, m, n, alpha[0], alpha[1], beta[0], beta[1], dC.c());
+      HS_CUDA(cudaGetLastError());
+      x.down(C, ldc, dC.c(), n, m);
+      x.sync();
+    }
+    if (ledger_flops) *ledger_flops += 8 * n * n * m;  // kernels.cpp:296
+  });
+}
+
+int hsdla_b200_trmm(int device, int trans, uint64_t n, uint64_t m, const double* alpha, const double* T, uint64_t ldt,
+                    double* B, uint64_t ldb, uint64_t* ledger_flops) {
+  return guarded([&] {
+    kl::need(alpha != nullptr, "null alpha");
+    kl::need(trans == 0 || trans == 1, "trans must be 0 (None) or 1 (ConjTrans)");
+    kl::need(T && ldt >= std::max<uint64_t>(n, 1), "T: null or ldt < n");
+    kl::need(B && ldb >= std::max<uint64_t>(n, 1), "B: null or ldb < n");
+    if (n && m) {
+      kl::Ctx x(device);
+      kl::DevBuf dT(n * n * 16), dL(n * n * 16), dB(n * m * 16), dC(n * m * 16);
+      x.up(dT.c(), T, n, n, ldt);
+      x.up(dB.c(), B, n, m, ldb);
+      // op(T) B = L^H B with L = lower(T) (ConjTrans) or L = lower(T)^H (None)
+      kl::conj_transpose_kernel<<<x.grid(n * n), 256, 0, x.s>>>(dT.c(), dL.c(), n, n, 1, trans ? 0 : 1);
+      kl::gemm_dev(x, dL.c(), dB.c(), n, m, n, alpha[0], alpha[1], 0.0, 0.0, dC.c());
+      HS_CUDA(cudaGetLastError());
+      x.down(B, ldb, dC.c(), n, m);
+      x.sync();
+    }
+    if (ledger_flops) *ledger_flops += 4 * n * n * m;  // kernels.cpp:390
+  });
+}
+
+int hsdla_b200_diag_scale(int device, uint64_t rows, uint64_t cols, const double* u, const double* B, uint64_t ldb,
+                          double* X, uint64_t ldx, uint64_t* ledger_flops) {
+  return guarded([&] {
+    kl::need(u && B && X && ldb >= std::max<uint64_t>(rows, 1) && ldx >= std::max<uint64_t>(rows, 1),
+             "diag_scale: null pointer or leading dimension < rows");
+    if (rows && cols) {
+      kl::Ctx x(device);
+      kl::DevBuf dB(rows * cols * 16), dX(rows * cols * 16), du(rows * 8);
+      x.up(dB.c(), B, rows, cols, ldb);
+      HS_CUDA(cudaMemcpyAsync(du.p, u, rows * 8, cudaMemcpyHostToDevice, x.s));
+      const dim3 g(static_cast<unsigned>((rows + 255) / 256), static_cast<unsigned>(std::min<uint64_t>(cols, 2048)));
+      diag_scale_kernel<<<g, 256, 0, x.s>>>(dB.c(), static_cast<const double*>(du.p), dX.c(), rows, rows, cols);
+      HS_CUDA(cudaGetLastError());
+      x.down(X, ldx, dX.c(), rows, cols);  // X may alias B (in place, kernels.cpp:438-450)
+      x.sync();
+    }
+    if (ledger_flops) *ledger_flops += 2 * rows * cols;  // kernels.cpp:444
   });
 }
 

@@ -13,7 +13,8 @@
 //     success: Q = L (lower factor, upper exactly 0), info = -1
 //              -> the batched contraction Q^H A_a is the reference's
 //                 trmm(Left, ConjTrans, L, A_a) (kernels.cpp:385-415);
-//     failure: Q = full(T_AA) expanded from the LOWER triangle, info = pivot
+//     failure: Q with Q^H = the hemm operator of T_AA's LOWER triangle (full(T_AA)
+//              with the diagonal conjugated), info = pivot
 //              -> Q^H A_a = T_AA A_a, the reference's hemm fallback.
 //   O(N_L^3 / 3) flops per atom (0.3 GFLOP at config 4): latency-bound, negligible
 //   next to the contractions; the block lives in L1/L2 (global scratch = Q itself).
@@ -30,8 +31,10 @@
 
 namespace hsdla_b200 {
 
+// n_fail (nullable) counts the atoms that did not factorise.
 __global__ void __launch_bounds__(128) potrf_batched_kernel(const double2* __restrict__ taa, double2* __restrict__ q,
-                                                            int32_t* __restrict__ info, int nl) {
+                                                            int32_t* __restrict__ info, int nl,
+                                                            int* __restrict__ n_fail = nullptr) {
   const uint64_t blk = static_cast<uint64_t>(nl) * nl;
   const double2* T = taa + blockIdx.x * blk;
   double2* L = q + blockIdx.x * blk;
@@ -77,15 +80,18 @@ __global__ void __launch_bounds__(128) potrf_batched_kernel(const double2* __res
     __syncthreads();
   }
   if (fail_at >= 0) {
-    // hemm operand: full Hermitian T_AA from its lower triangle (kernels.cpp:152-167)
+    // hemm operand Q, Q^H = T_AA read from its lower triangle (kernels.cpp:152-167)
     for (uint64_t idx = threadIdx.x; idx < blk; idx += blockDim.x) {
       const int k = static_cast<int>(idx % nl), i = static_cast<int>(idx / nl);  // element (k, i)
       double2 v = k >= i ? T[k + static_cast<uint64_t>(i) * nl] : T[i + static_cast<uint64_t>(k) * nl];
-      if (k < i) v.y = -v.y;
+      if (k <= i) v.y = -v.y;
       L[idx] = v;
     }
   }
-  if (threadIdx.x == 0) info[blockIdx.x] = fail_at;
+  if (threadIdx.x == 0) {
+    info[blockIdx.x] = fail_at;
+    if (fail_at >= 0 && n_fail) atomicAdd(n_fail, 1);
+  }
 }
 
 // X2[r, j] = info[atom(r)] < 0 ? X1[r, j] : A[r, j] for the rows [0, Kc) of a chunk

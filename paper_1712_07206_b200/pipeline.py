@@ -215,8 +215,8 @@ def potrf(T, device=0):
     """kernels::potrf (kernels.cpp:417-436) on the GPU for every atom block of T
     ((n_l, n_l, n_blocks) complex128, Fortran order, lower triangles read).
     Returns (L, pivot): L[:, :, b] the factor (upper 0) where pivot[b] == -1, else the
-    Hermitian expansion of T[:, :, b] (the hemm fallback operand); bit-identical to
-    the reference's factor."""
+    hemm fallback operand Q with Q^H = T[:, :, b] read from its lower triangle (full(T)
+    with the diagonal conjugated); factors bit-identical to the reference's."""
     T = np.asfortranarray(T, dtype=np.complex128)
     if T.ndim == 2:
         T = T[:, :, None]

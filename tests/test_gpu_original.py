@@ -33,8 +33,9 @@ def _need_gpu():
 
 
 def _hermitian_full(t):
-    lo = np.tril(t)
-    return lo + np.conj(np.tril(t, -1)).T
+    """Q with Q^H = the hemm operator of t's lower triangle: full(t), diagonal conjugated."""
+    q = np.tril(t, -1) + np.conj(np.tril(t, -1)).T
+    return q + np.diag(np.conj(np.diag(t)))
 
 
 def test_potrf_bitwise_vs_reference_golden():

@@ -195,3 +195,21 @@ def test_banded_final_h_matches_device_resident(algo):
         H, S = e.download()
         e.close()
         assert rel(r.H, H) <= 1e-14 and rel(r.S, S) <= 1e-14, dims
+
+
+@pytest.mark.parametrize("variant", ["refined", "original"])
+def test_operators_with_complex_diagonals_follow_reference_hemm(restatement, variant):
+    """The reference's hemm uses T's diagonal as stored (kernels.cpp:152-167), also a
+    non-real one; the device operand expansion reproduces that exactly."""
+    p = hb.generate_problem(5, 9, 60, 8, 2)
+    g = np.random.default_rng(3)
+    for T in (p.T_AA, p.T_BB):
+        for a in range(p.n_atoms):
+            T[np.arange(p.n_l), np.arange(p.n_l), a] += 1j * g.uniform(-0.5, 0.5, p.n_l)
+    if variant == "original":
+        H, S, _, _ = restatement.build_hs_original(p)
+        r = hb.build_hs_original(p)
+    else:
+        H, S, _ = restatement.build_hs_refined(p)
+        r = hb.build_hs_refined(p)
+    assert rel(r.H, H) <= TOL and rel(r.S, S) <= TOL
