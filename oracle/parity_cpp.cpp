@@ -16,6 +16,7 @@
 
 #include "hsdla/pipeline.hpp"
 #include "hsdla/problem.hpp"
+#include "hsdla_b200/kernels.hpp"
 #include "hsdla_b200/pipeline.hpp"
 
 int main(int argc, char** argv) {
@@ -101,6 +102,56 @@ int main(int argc, char** argv) {
     } catch (const hsdla::IoError&) {
       check(true, "  missing file -> IoError", 0);
     }
+  }
+  // the kernel layer (hsdla::kernels) against the reference's own CPU kernels on the same data
+  {
+    namespace rk = hsdla::kernels;
+    namespace gk = hsdla_b200::kernels;
+    const std::size_t kk = std::min<std::size_t>(na * nl, 300), n = std::min<std::size_t>(ng, 200);
+    hsdla::ComplexMatrix a(kk, n), b(kk, n);
+    for (std::size_t j = 0; j < n; ++j)
+      for (std::size_t i = 0; i < kk; ++i) {
+        a(i, j) = p.A(i, j);
+        b(i, j) = p.B(i, j);
+      }
+    auto rel_lower = [&](const hsdla::HermitianView& x, const hsdla::HermitianView& y) {
+      return hsdla::rel_frobenius_error_lower(x.matrix(), y.matrix());
+    };
+    const hsdla::cplx alpha(0.75, -0.5);
+    hsdla::FlopLedger lc, lg;
+    hsdla::HermitianView c1(n), c2(n);
+    rk::herk(1.5, a, 0.0, c1, &lc);
+    gk::herk(1.5, a, 0.0, c2, &lg);
+    check(rel_lower(c2, c1) <= 1e-13, "kernels::herk vs reference", rel_lower(c2, c1));
+    rk::her2k(alpha, a, b, 1.0, c1, &lc);
+    gk::her2k(alpha, a, b, 1.0, c2, &lg);
+    check(rel_lower(c2, c1) <= 1e-13, "kernels::her2k (beta 1) vs reference", rel_lower(c2, c1));
+    rk::herkx(alpha, a, b, 0.5, c1, &lc);
+    gk::herkx(alpha, a, b, 0.5, c2, &lg);
+    check(rel_lower(c2, c1) <= 1e-13, "kernels::herkx (beta 1/2) vs reference", rel_lower(c2, c1));
+    hsdla::ComplexMatrix g1(n, n), g2(n, n);
+    rk::gemm(alpha, a, rk::Trans::ConjTrans, b, rk::Trans::None, hsdla::cplx(0.0), g1, &lc);
+    gk::gemm(alpha, a, rk::Trans::ConjTrans, b, rk::Trans::None, hsdla::cplx(0.0), g2, &lg);
+    check(hsdla::rel_frobenius_error_lower(g2, g1) <= 1e-13, "kernels::gemm vs reference",
+          hsdla::rel_frobenius_error_lower(g2, g1));
+    const hsdla::HermitianView& t = p.T_AA[0];
+    hsdla::ComplexMatrix bs(nl, n), h1(nl, n), h2(nl, n);
+    for (std::size_t j = 0; j < n; ++j)
+      for (std::size_t i = 0; i < nl; ++i) bs(i, j) = p.B(i, j);
+    rk::hemm(rk::Side::Left, alpha, t, bs, hsdla::cplx(0.0), h1, &lc);
+    gk::hemm(rk::Side::Left, alpha, t, bs, hsdla::cplx(0.0), h2, &lg);
+    double eh = 0, nh = 0;
+    for (std::size_t i = 0; i < h1.size(); ++i) {
+      eh += std::norm(h2.data()[i] - h1.data()[i]);
+      nh += std::norm(h1.data()[i]);
+    }
+    check(std::sqrt(eh / nh) <= 1e-13, "kernels::hemm vs reference", std::sqrt(eh / nh));
+    const auto f1 = rk::potrf(t, &lc), f2 = gk::potrf(t, &lg);
+    bool same = f1.ok() == f2.ok();
+    if (same && f1.ok())
+      for (std::size_t i = 0; i < f1.factor->size(); ++i) same = same && f1.factor->data()[i] == f2.factor->data()[i];
+    check(same, "kernels::potrf bit-identical to reference", 0.0);
+    check(lg == lc, "kernel-layer ledger == reference ledger", double(lc.total()));
   }
   // error mapping: a refined call with a non-refined variant -> hsdla::ConfigError
   try {
