@@ -7,7 +7,8 @@ import sys
 sys.path.insert(0, ".")
 import paper_1712_07206_b200 as hb  # noqa: E402
 
-CFG = {"c1": (16, 49, 1000), "c2": (64, 81, 3000), "c3": (108, 121, 6000)}
+CFG = {"c1": (16, 49, 1000), "c2": (64, 81, 3000), "c3": (108, 121, 6000),
+       "g2k": (256, 81, 2000), "g10k": (16, 81, 10000), "g20k": (16, 81, 20000)}
 ap = argparse.ArgumentParser()
 ap.add_argument("config", nargs="?", default="c2")
 ap.add_argument("--builds", type=int, default=3)
