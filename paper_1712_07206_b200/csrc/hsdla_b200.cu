@@ -259,6 +259,11 @@ struct hsdla_b200_engine {
   cudaEvent_t ev_setup0 = nullptr, ev_setup1 = nullptr;  // last LAPW setup kernel
   uint64_t setup_bytes = 0;
   void* lapw_scratch = nullptr;  // device copy of the LAPW inputs (grown on demand)
+  // HSDL file reader: two pinned 64 MB staging slabs, allocated on first use
+  char* stage_buf[2] = {nullptr, nullptr};
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  bool stage_busy[2] = {false, false};
+  int stage_next = 0;
   size_t lapw_scratch_bytes = 0;
   // roofline: events around the whole-build S and H contraction launches, harvested lazily
   static constexpr int kRing = 64;
@@ -297,6 +302,13 @@ static void engine_free(hsdla_b200_engine* e) {
                   (void*)e->Hp, (void*)e->Sp})
     if (p) cudaFree(p);
   if (e->host_stage) cudaFreeHost(e->host_stage);
+  for (int i = 0; i < 2; ++i) {
+    if (e->stage_ev[i]) {
+      cudaEventSynchronize(e->stage_ev[i]);
+      cudaEventDestroy(e->stage_ev[i]);
+    }
+    if (e->stage_buf[i]) cudaFreeHost(e->stage_buf[i]);
+  }
   for (cudaEvent_t ev : e->ev_pool) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e->ev_chunk_up) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e->ev_h_piece)
@@ -1136,37 +1148,24 @@ static int open_hsdl(const char* path) {
   return fd;
 }
 
-// Staging ring of two pinned slabs; slab s is free again once its event fired.
-struct Staging {
-  static constexpr size_t kSlab = size_t(64) << 20;
-  char* buf[2] = {nullptr, nullptr};
-  cudaEvent_t ev[2] = {nullptr, nullptr};
-  bool busy[2] = {false, false};
-  int next = 0;
-  Staging() {
+// Staging ring of two pinned slabs owned by the engine; slab s is free again once
+// the copy that read it has completed.
+constexpr size_t kStageSlab = size_t(64) << 20;
+static char* stage_acquire(hsdla_b200_engine* e, int& slot) {
+  if (!e->stage_buf[0])
     for (int i = 0; i < 2; ++i) {
-      HS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&buf[i]), kSlab));
-      HS_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+      HS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&e->stage_buf[i]), kStageSlab));
+      HS_CUDA(cudaEventCreateWithFlags(&e->stage_ev[i], cudaEventDisableTiming));
     }
-  }
-  ~Staging() {
-    for (int i = 0; i < 2; ++i) {
-      if (ev[i]) {
-        cudaEventSynchronize(ev[i]);
-        cudaEventDestroy(ev[i]);
-      }
-      if (buf[i]) cudaFreeHost(buf[i]);
-    }
-  }
-  char* acquire(int& slot) {
-    slot = next;
-    next ^= 1;
-    if (busy[slot]) HS_CUDA(cudaEventSynchronize(ev[slot]));
-    busy[slot] = true;
-    return buf[slot];
-  }
-  void release(int slot, cudaStream_t s) { HS_CUDA(cudaEventRecord(ev[slot], s)); }
-};
+  slot = e->stage_next;
+  e->stage_next ^= 1;
+  if (e->stage_busy[slot]) HS_CUDA(cudaEventSynchronize(e->stage_ev[slot]));
+  e->stage_busy[slot] = true;
+  return e->stage_buf[slot];
+}
+static void stage_release(hsdla_b200_engine* e, int slot, cudaStream_t s) {
+  HS_CUDA(cudaEventRecord(e->stage_ev[slot], s));
+}
 
 // Read `n` pieces of `piece` bytes at offsets off0 + i*stride into dst (packed),
 // split over up to 8 threads.
@@ -1200,71 +1199,101 @@ static void pread_pieces(int fd, char* dst, uint64_t off0, uint64_t stride, size
     if (bad[t]) throw errs[t];
 }
 
-static void engine_load_file(hsdla_b200_engine* e, const char* path, uint64_t a0) {
-  Fd f;
+// Host-read + H2D (on stream s) of the engine-local atoms [b0, b1) of shard a0 of an
+// HSDL file: their rows of every A / B column (one pread per column when the rows
+// are a strict subset of the file's, else whole column slabs), their T blocks and U.
+static void load_atoms_from_file(hsdla_b200_engine* e, int fd, const HsdlHeader& h, uint64_t a0, uint64_t b0,
+                                 uint64_t b1, cudaStream_t s) {
+  const uint64_t K = e->K, Kf = h.na * h.nl, nl = h.nl, ng = h.ng;
+  const uint64_t r0 = b0 * nl, rows = (b1 - b0) * nl, g0 = (a0 + b0) * nl;
+  const size_t colb = rows * sizeof(double2);
+  for (int m = 0; m < 2; ++m) {  // A then B
+    const uint64_t base = (m == 0 ? h.off_A : h.off_B) + g0 * 16;
+    double2* dst = (m == 0 ? e->A : e->B) + r0;
+    if (colb > kStageSlab) {  // one column's rows exceed a slab: split the rows
+      for (uint64_t j = 0; j < ng; ++j)
+        for (uint64_t q0 = 0; q0 < rows; q0 += kStageSlab / 16) {
+          const uint64_t nr = std::min<uint64_t>(kStageSlab / 16, rows - q0);
+          int slot;
+          char* b = stage_acquire(e, slot);
+          pread_pieces(fd, b, base + (j * Kf + q0) * 16, nr * 16, nr * 16, 1);
+          HS_CUDA(cudaMemcpyAsync(dst + j * K + q0, b, nr * 16, cudaMemcpyHostToDevice, s));
+          stage_release(e, slot, s);
+        }
+      continue;
+    }
+    const uint64_t cols = std::max<uint64_t>(1, kStageSlab / colb);
+    for (uint64_t j0 = 0; j0 < ng; j0 += cols) {
+      const uint64_t nc = std::min(cols, ng - j0);
+      int slot;
+      char* b = stage_acquire(e, slot);
+      pread_pieces(fd, b, base + j0 * Kf * 16, Kf * 16, colb, nc);
+      HS_CUDA(cudaMemcpy2DAsync(dst + j0 * K, K * sizeof(double2), b, colb, colb, nc, cudaMemcpyHostToDevice, s));
+      stage_release(e, slot, s);
+    }
+  }
+  // operator blocks: T_AA, T_AB, T_BB interleaved per atom in the file
+  const uint64_t blk = nl * nl * 16;
+  if (3 * blk > kStageSlab) throw Fail{HSDLA_B200_SIZING_ERROR, "operator block larger than the staging slab"};
+  const uint64_t atoms_per = std::max<uint64_t>(1, kStageSlab / (3 * blk));
+  for (uint64_t c0 = b0; c0 < b1; c0 += atoms_per) {
+    const uint64_t nb = std::min(atoms_per, b1 - c0);
+    int slot;
+    char* b = stage_acquire(e, slot);
+    pread_pieces(fd, b, h.off_T + (a0 + c0) * 3 * blk, 3 * blk, 3 * blk, nb);
+    double2* dsts[3] = {e->Taa, e->Tab, e->Tbb};
+    for (int m = 0; m < 3; ++m)
+      HS_CUDA(cudaMemcpy2DAsync(reinterpret_cast<char*>(dsts[m]) + c0 * blk, blk, b + m * blk, 3 * blk, blk, nb,
+                                cudaMemcpyHostToDevice, s));
+    stage_release(e, slot, s);
+  }
+  const size_t ub = rows * sizeof(double);
+  if (ub > kStageSlab) throw Fail{HSDLA_B200_SIZING_ERROR, "U larger than the staging slab"};
+  int slot;
+  char* b = stage_acquire(e, slot);
+  pread_pieces(fd, b, h.off_U + g0 * sizeof(double), ub, ub, 1);
+  HS_CUDA(cudaMemcpyAsync(e->U + r0, b, ub, cudaMemcpyHostToDevice, s));
+  stage_release(e, slot, s);
+}
+
+static HsdlHeader open_shard(Fd& f, const char* path, const hsdla_b200_engine* e, uint64_t a0) {
   f.fd = open_hsdl(path);
-  const HsdlHeader h = read_hsdl_header(f.fd, path);
+  HsdlHeader h = read_hsdl_header(f.fd, path);
   if (h.nl != e->nl || h.ng != e->ng || a0 + e->na > h.na)
     throw Fail{HSDLA_B200_DIMENSION_ERROR, "problem file shape does not match the engine shard"};
+  return h;
+}
+
+static void engine_load_file(hsdla_b200_engine* e, const char* path, uint64_t a0) {
+  Fd f;
+  const HsdlHeader h = open_shard(f, path, e, a0);
   HS_CUDA(cudaSetDevice(e->device));
   cudaStream_t s = e->copy_stream;
   // nothing may overwrite A/B/T/U while a previous build still reads them
   HS_CUDA(cudaStreamWaitEvent(s, e->ev_end, 0));
-  Staging st;
-  const uint64_t K = e->K, Kf = h.na * h.nl, g0 = a0 * h.nl, ng = h.ng;
-  const size_t colb = K * sizeof(double2);
-  const uint64_t cols = std::max<uint64_t>(1, Staging::kSlab / colb);
-  for (int m = 0; m < 2; ++m) {  // A then B: the shard's K rows of every column
-    const uint64_t base = (m == 0 ? h.off_A : h.off_B) + g0 * 16;
-    double2* dst = m == 0 ? e->A : e->B;
-    for (uint64_t j0 = 0; j0 < ng; j0 += cols) {
-      const uint64_t nc = std::min(cols, ng - j0);
-      if (colb > Staging::kSlab) {  // a single column larger than a slab: split rows
-        for (uint64_t j = j0; j < j0 + nc; ++j)
-          for (uint64_t r0 = 0; r0 < K; r0 += Staging::kSlab / 16) {
-            const uint64_t nr = std::min<uint64_t>(Staging::kSlab / 16, K - r0);
-            int slot;
-            char* b = st.acquire(slot);
-            pread_pieces(f.fd, b, base + (j * Kf + r0) * 16, nr * 16, nr * 16, 1);
-            HS_CUDA(cudaMemcpyAsync(dst + j * K + r0, b, nr * 16, cudaMemcpyHostToDevice, s));
-            st.release(slot, s);
-          }
-        continue;
-      }
-      int slot;
-      char* b = st.acquire(slot);
-      pread_pieces(f.fd, b, base + j0 * Kf * 16, Kf * 16, colb, nc);
-      HS_CUDA(cudaMemcpyAsync(dst + j0 * K, b, nc * colb, cudaMemcpyHostToDevice, s));
-      st.release(slot, s);
-    }
-  }
-  // operator blocks of atoms [a0, a0 + na): T_AA, T_AB, T_BB interleaved per atom in the file
-  const uint64_t blk = h.nl * h.nl * 16;
-  const uint64_t atoms_per = std::max<uint64_t>(1, Staging::kSlab / (3 * blk));
-  for (uint64_t b0 = 0; b0 < e->na; b0 += atoms_per) {
-    const uint64_t nb = std::min(atoms_per, e->na - b0);
-    if (3 * blk > Staging::kSlab) throw Fail{HSDLA_B200_SIZING_ERROR, "operator block larger than the staging slab"};
-    int slot;
-    char* b = st.acquire(slot);
-    pread_pieces(f.fd, b, h.off_T + (a0 + b0) * 3 * blk, 3 * blk, 3 * blk, nb);
-    double2* dsts[3] = {e->Taa, e->Tab, e->Tbb};
-    for (int m = 0; m < 3; ++m)
-      HS_CUDA(cudaMemcpy2DAsync(reinterpret_cast<char*>(dsts[m]) + b0 * blk, blk, b + m * blk, 3 * blk, blk, nb,
-                                cudaMemcpyHostToDevice, s));
-    st.release(slot, s);
-  }
-  {
-    int slot;
-    char* b = st.acquire(slot);
-    const size_t ub = e->na * h.nl * sizeof(double);
-    if (ub > Staging::kSlab) throw Fail{HSDLA_B200_SIZING_ERROR, "U larger than the staging slab"};
-    pread_pieces(f.fd, b, h.off_U + a0 * h.nl * sizeof(double), ub, ub, 1);
-    HS_CUDA(cudaMemcpyAsync(e->U, b, ub, cudaMemcpyHostToDevice, s));
-    st.release(slot, s);
-  }
-  // the compute stream waits for the upload; Staging's destructor drains the ring
+  load_atoms_from_file(e, f.fd, h, a0, 0, e->na, s);
   HS_CUDA(cudaEventRecord(e->ev_up1, s));
   HS_CUDA(cudaStreamWaitEvent(e->stream, e->ev_up1, 0));
+}
+
+// Streamed build from an HSDL file: the host reads atom chunk c+1 from the file
+// while the GPU computes chunk c (the streamed chunk plans of the host-buffer path).
+static void engine_build_file(hsdla_b200_engine* e, const char* path, uint64_t a0, int algo) {
+  Fd f;
+  const HsdlHeader h = open_shard(f, path, e, a0);
+  begin_build(e, algo);
+  HS_CUDA(cudaStreamWaitEvent(e->copy_stream, e->ev_end, 0));
+  HS_CUDA(cudaEventRecord(e->ev_up0, e->copy_stream));
+  for (size_t c = 0; c < e->streamed.size(); ++c) {
+    load_atoms_from_file(e, f.fd, h, a0, e->streamed[c].a0, e->streamed[c].a1, e->copy_stream);
+    HS_CUDA(cudaEventRecord(e->ev_chunk_up[c], e->copy_stream));
+    HS_CUDA(cudaStreamWaitEvent(e->stream, e->ev_chunk_up[c], 0));
+    if (c == 0) HS_CUDA(cudaEventRecord(e->ev_begin, e->stream));
+    enqueue_chunk(e, e->streamed[c], algo, c + 1 == e->streamed.size(), nullptr);
+  }
+  HS_CUDA(cudaEventRecord(e->ev_up1, e->copy_stream));
+  HS_CUDA(cudaEventRecord(e->ev_end, e->stream));
+  e->uploaded_streamed = true;
 }
 
 // ---------------------------------------------------------------------------
@@ -1362,19 +1391,35 @@ static void one_shot(const hsdla_b200_options* o, uint64_t na, uint64_t nl, uint
     if (d < 0 || d >= ndev) throw Fail{HSDLA_B200_CONFIG_ERROR, "device id out of range"};
   std::lock_guard<std::mutex> lk(g_cache_mu);
   EngineSet* set = get_engines(devs, na, nl, ng);
-  double load_s = 0;
-  for (int r = 0; r < P; ++r) {
+  // One host thread per GPU (a file-backed start reads that GPU's shard on the host).
+  // One GPU: the final H contraction runs band by band so H's download overlaps it.
+  std::vector<double> load(P, 0.0);
+  std::vector<Fail> errs(P);
+  std::vector<char> bad(P, 0);
+  auto run = [&](int r) {
     hsdla_b200_engine* e = set->engines[r];
-    // one GPU: the final H contraction runs band by band so H's download overlaps it
     e->band_final_h = P == 1;
     try {
-      load_s = std::max(load_s, start(e, set->atom0[r], algo));
-    } catch (...) {
-      e->band_final_h = false;
-      throw;
+      load[r] = start(e, set->atom0[r], algo);
+    } catch (const Fail& f) {
+      errs[r] = f;
+      bad[r] = 1;
+    } catch (const std::exception& x) {
+      errs[r] = Fail{HSDLA_B200_CUDA_ERROR, x.what()};
+      bad[r] = 1;
     }
     e->band_final_h = false;
+  };
+  if (P == 1) {
+    run(0);
+  } else {
+    std::vector<std::thread> th;
+    for (int r = 0; r < P; ++r) th.emplace_back(run, r);
+    for (auto& t : th) t.join();
   }
+  for (int r = 0; r < P; ++r)
+    if (bad[r]) throw errs[r];
+  const double load_s = *std::max_element(load.begin(), load.end());
   if (P > 1) {
     HS_NCCL(ncclGroupStart());
     for (int r = 0; r < P; ++r) reduce_s(set->engines[r], 0);
@@ -1955,10 +2000,8 @@ int hsdla_b200_build_hs_file(const char* path, const hsdla_b200_options* o, doub
     // each GPU reads only its atom shard from the file, then builds device-resident
     one_shot(o, h.na, h.nl, h.ng, H, S, st, t0, [&](hsdla_b200_engine* e, uint64_t a0, int algo) {
       const auto tl = std::chrono::steady_clock::now();
-      engine_load_file(e, path, a0);
-      const double load_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - tl).count();
-      engine_build(e, algo);
-      return load_s;
+      engine_build_file(e, path, a0, algo);  // host file reads overlap the chunks' compute
+      return std::chrono::duration<double>(std::chrono::steady_clock::now() - tl).count();
     });
   });
 }
