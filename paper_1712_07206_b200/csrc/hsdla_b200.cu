@@ -29,6 +29,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -1548,9 +1549,46 @@ __global__ void pack_lower_kernel(const double2* __restrict__ full, double2* __r
   }
 }
 
+// Pinned staging ring per device for the kernel layer's host <-> device traffic
+// (page-locked double buffer, multi-threaded host packing): calls on one device are
+// serialised by its mutex.
+struct Ring {
+  std::mutex mu;
+  char* buf[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+};
+static constexpr size_t kRingSlab = size_t(32) << 20;
+static Ring& ring_for(int device) {
+  static std::mutex mu;
+  static std::map<int, std::unique_ptr<Ring>> rings;
+  std::lock_guard<std::mutex> lk(mu);
+  auto& r = rings[device];
+  if (!r) r = std::make_unique<Ring>();
+  return *r;
+}
+
+// fn(i) for i in [0, n) over up to 16 host threads when the work is large.
+template <class F>
+static void par_for(uint64_t n, uint64_t bytes, F&& fn) {
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const unsigned nt = bytes < (size_t(4) << 20) ? 1u : static_cast<unsigned>(std::min<uint64_t>(hw, n));
+  if (nt <= 1) {
+    for (uint64_t i = 0; i < n; ++i) fn(i);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < nt; ++t)
+    th.emplace_back([&, t] {
+      for (uint64_t i = n * t / nt; i < n * (t + 1) / nt; ++i) fn(i);
+    });
+  for (auto& x : th) x.join();
+}
+
 struct Ctx {
   int sms = 148;
   cudaStream_t s = nullptr;
+  Ring* ring = nullptr;
+  std::unique_lock<std::mutex> lock;
   explicit Ctx(int device) {
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
@@ -1562,18 +1600,102 @@ struct Ctx {
     HS_CUDA(cudaFuncSetAttribute(tri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TriCfg::kSmemBytes));
     HS_CUDA(cudaFuncSetAttribute(bat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BatCfg::kSmemBytes));
     HS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    ring = &ring_for(device);
+    lock = std::unique_lock<std::mutex>(ring->mu);
+    if (!ring->buf[0])
+      for (int i = 0; i < 2; ++i) {
+        HS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ring->buf[i]), kRingSlab));
+        HS_CUDA(cudaEventCreateWithFlags(&ring->ev[i], cudaEventDisableTiming));
+      }
   }
   ~Ctx() {
-    if (s) cudaStreamDestroy(s);
+    if (s) {
+      cudaStreamSynchronize(s);  // the ring's slabs may still be in flight
+      cudaStreamDestroy(s);
+    }
   }
   unsigned grid(uint64_t n) const {
     return static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(sms) * 16) + 0);
   }
+  // host r x c (leading dimension ld) -> dense device r x c, through the pinned ring
   void up(double2* d, const double* h, uint64_t r, uint64_t c, uint64_t ld) {
-    if (r && c) HS_CUDA(cudaMemcpy2DAsync(d, r * 16, h, ld * 16, r * 16, c, cudaMemcpyHostToDevice, s));
+    if (!r || !c) return;
+    const size_t colb = r * 16;
+    const double2* hc = reinterpret_cast<const double2*>(h);
+    if (colb > kRingSlab) {  // huge columns: pageable copy
+      HS_CUDA(cudaMemcpy2DAsync(d, colb, h, ld * 16, colb, c, cudaMemcpyHostToDevice, s));
+      return;
+    }
+    const uint64_t per = kRingSlab / colb;
+    int slot = 0;
+    for (uint64_t j0 = 0; j0 < c; j0 += per, slot ^= 1) {
+      const uint64_t nc = std::min(per, c - j0);
+      HS_CUDA(cudaEventSynchronize(ring->ev[slot]));
+      char* b = ring->buf[slot];
+      par_for(nc, nc * colb, [&](uint64_t j) { std::memcpy(b + j * colb, hc + (j0 + j) * ld, colb); });
+      HS_CUDA(cudaMemcpyAsync(d + j0 * r, b, nc * colb, cudaMemcpyHostToDevice, s));
+      HS_CUDA(cudaEventRecord(ring->ev[slot], s));
+    }
   }
+  // dense device r x c -> host r x c (leading dimension ld), through the pinned ring
   void down(double* h, uint64_t ld, const double2* d, uint64_t r, uint64_t c) {
-    if (r && c) HS_CUDA(cudaMemcpy2DAsync(h, ld * 16, d, r * 16, r * 16, c, cudaMemcpyDeviceToHost, s));
+    if (!r || !c) return;
+    const size_t colb = r * 16;
+    double2* hc = reinterpret_cast<double2*>(h);
+    if (colb > kRingSlab) {
+      HS_CUDA(cudaMemcpy2DAsync(h, ld * 16, d, colb, colb, c, cudaMemcpyDeviceToHost, s));
+      sync();
+      return;
+    }
+    const uint64_t per = kRingSlab / colb;
+    const uint64_t pieces = (c + per - 1) / per;
+    auto issue = [&](uint64_t q) {
+      const uint64_t j0 = q * per, nc = std::min(per, c - j0);
+      HS_CUDA(cudaMemcpyAsync(ring->buf[q & 1], d + j0 * r, nc * colb, cudaMemcpyDeviceToHost, s));
+      HS_CUDA(cudaEventRecord(ring->ev[q & 1], s));
+    };
+    issue(0);
+    for (uint64_t q = 0; q < pieces; ++q) {
+      if (q + 1 < pieces) issue(q + 1);  // the next slab lands while this one is unpacked
+      HS_CUDA(cudaEventSynchronize(ring->ev[q & 1]));
+      const uint64_t j0 = q * per, nc = std::min(per, c - j0);
+      const char* b = ring->buf[q & 1];
+      par_for(nc, nc * colb, [&](uint64_t j) { std::memcpy(hc + (j0 + j) * ld, b + j * colb, colb); });
+    }
+  }
+  // device packed-lower n x n -> the lower triangle of host C (ldc), upper untouched
+  void down_lower(double* C, uint64_t ldc, const double2* pk, uint64_t n) {
+    double2* hc = reinterpret_cast<double2*>(C);
+    auto pc = [&](uint64_t j) { return j * (2 * n - j + 1) / 2; };
+    std::vector<uint64_t> cuts{0};  // column ranges whose packed bytes fit a slab
+    while (cuts.back() < n) {
+      uint64_t j = cuts.back() + 1;
+      while (j < n && (pc(j + 1) - pc(cuts.back())) * 16 <= kRingSlab) ++j;
+      cuts.push_back(j);
+    }
+    const uint64_t pieces = cuts.size() - 1;
+    for (uint64_t q = 0; q < pieces; ++q)
+      if ((pc(cuts[q + 1]) - pc(cuts[q])) * 16 > kRingSlab) {  // a single column beyond a slab
+        std::vector<double2> tmp(pc(n));
+        HS_CUDA(cudaMemcpyAsync(tmp.data(), pk, pc(n) * 16, cudaMemcpyDeviceToHost, s));
+        sync();
+        for (uint64_t j = 0; j < n; ++j) std::memcpy(hc + j * ldc + j, tmp.data() + pc(j), (n - j) * 16);
+        return;
+      }
+    auto issue = [&](uint64_t q) {
+      const uint64_t b0 = pc(cuts[q]), b1 = pc(cuts[q + 1]);
+      HS_CUDA(cudaMemcpyAsync(ring->buf[q & 1], pk + b0, (b1 - b0) * 16, cudaMemcpyDeviceToHost, s));
+      HS_CUDA(cudaEventRecord(ring->ev[q & 1], s));
+    };
+    issue(0);
+    for (uint64_t q = 0; q < pieces; ++q) {
+      if (q + 1 < pieces) issue(q + 1);
+      HS_CUDA(cudaEventSynchronize(ring->ev[q & 1]));
+      const double2* b = reinterpret_cast<const double2*>(ring->buf[q & 1]);
+      const uint64_t j0 = cuts[q], base = pc(j0), ncol = cuts[q + 1] - j0;
+      par_for(ncol, (pc(cuts[q + 1]) - base) * 16,
+              [&](uint64_t t) { std::memcpy(hc + (j0 + t) * ldc + j0 + t, b + pc(j0 + t) - base, (n - j0 - t) * 16); });
+    }
   }
   void sync() { HS_CUDA(cudaStreamSynchronize(s)); }
 };
@@ -1651,6 +1773,7 @@ static void tri_family(int device, int which, uint64_t n, uint64_t k, double ar,
   if (beta != 0.0 || alpha0) x.up(dC.c(), C, n, n, ldc);
   if (alpha0) {  // scale_lower_in_place (kernels.cpp:209-217): only C's lower triangle
     scale_kernel<<<x.grid(n * n), 256, 0, x.s>>>(dC.c(), n, n, beta, 0.0, 1);
+    pack_lower_kernel<<<x.grid(n * n), 256, 0, x.s>>>(dC.c(), dP.c(), n, 0);
   } else {
     if (beta != 0.0) pack_lower_kernel<<<x.grid(n * n), 256, 0, x.s>>>(dC.c(), dP.c(), n, 0);
     DevBuf dA(k * n * 16), dB(which != 0 ? k * n * 16 : 16);
@@ -1670,15 +1793,11 @@ static void tri_family(int device, int which, uint64_t n, uint64_t k, double ar,
       const double2* R[1] = {dB.c()};
       tri(x, 1, L, R, k, n, ar, ai, beta, dP.c());
     }
-    pack_lower_kernel<<<x.grid(n * n), 256, 0, x.s>>>(dC.c(), dP.c(), n, 1);
   }
   HS_CUDA(cudaGetLastError());
-  // lower triangle back into the caller's C, column by column (upper never written)
-  std::vector<double2> h(n * n);
-  HS_CUDA(cudaMemcpyAsync(h.data(), dC.p, n * n * 16, cudaMemcpyDeviceToHost, x.s));
+  // lower triangle back into the caller's C (upper never written)
+  x.down_lower(C, ldc, dP.c(), n);
   x.sync();
-  for (uint64_t j = 0; j < n; ++j)
-    std::memcpy(reinterpret_cast<double2*>(C) + j * ldc + j, h.data() + j * n + j, (n - j) * 16);
 }
 
 // gemm core on device operands: C (m x n) = alpha opA^H-form ... + beta C, complex beta.
