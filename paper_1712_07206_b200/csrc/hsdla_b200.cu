@@ -184,7 +184,7 @@ static void make_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1,
 
 // kernel shapes (tools/tune_tri.cu sweep): TRI 64x64 tiles, 8 consumer warps of
 // 32x16; BATCH 32x128 tiles, 8 consumer warps of 32x16.
-constexpr int kTriBM = 64, kTriStages = 6;
+constexpr int kTriBM = 64, kTriStages = 8;  // power of two: slot / phase are bit ops in the loop
 using TriCfg = CtnCfg<kTri, kTriBM, kTriBM, 2, 4, kTriStages>;
 constexpr int kBatBM = 32, kBatBN = 128, kBatStages = 4;
 using BatCfg = CtnCfg<kBatch, kBatBM, kBatBN, 1, 8, kBatStages>;
