@@ -219,7 +219,9 @@ def run_b200(args):
     # this rank's 64-atom shard (independent synthetic atoms per rank)
     p = hb.generate_problem(na, nl, ng, 1 + d.rank, 0)
     eng = hb.Engine(dev, na, nl, ng)
-    if P > 1:
+    if P > 1 or args.force_comm:
+        # N > 1: NCCL reduce of the packed partials; --force-comm exercises the same
+        # path on one GPU with a 1-rank communicator (plumbing check)
         uid = d.bcast_bytes(hb.nccl_unique_id() if d.rank == 0 else None)
         eng.set_comm(uid, P, d.rank)
     eng.upload(p, 0)
@@ -487,6 +489,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--algo", default="fused", choices=["fused", "refined", "original"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--force-comm", action="store_true", help="NCCL communicator even at N=1 (plumbing check)")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU work for cpu_baseline")

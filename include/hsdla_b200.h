@@ -220,7 +220,9 @@ int hsdla_b200_engine_download(hsdla_b200_engine* e, double* H, double* S);
 int hsdla_b200_engine_device_results(hsdla_b200_engine* e, void** Hp, void** Sp);
 /* The cudaStream_t the engine launches on. */
 int hsdla_b200_engine_stream(hsdla_b200_engine* e, void** stream);
-/* NCCL: one communicator per engine (one rank per GPU; id from rank 0). */
+/* NCCL: one communicator per engine (one rank per GPU; id from rank 0).  id128 NULL
+ * with nranks 1 drops the communicator (reduce becomes a no-op); an id with nranks 1
+ * builds a single-rank communicator, so the reduce path runs through NCCL. */
 int hsdla_b200_nccl_unique_id(void* id128);
 int hsdla_b200_engine_set_comm(hsdla_b200_engine* e, const void* id128, int nranks, int rank);
 

@@ -1989,7 +1989,10 @@ int hsdla_b200_engine_set_comm(hsdla_b200_engine* e, const void* id128, int nran
     }
     e->nranks = nranks;
     e->rank = rank;
-    if (nranks == 1) return;
+    if (!id128) {
+      if (nranks > 1) throw Fail{HSDLA_B200_CONFIG_ERROR, "null NCCL id"};
+      return;  // single rank without a communicator: reduce is a no-op
+    }
     ncclUniqueId id;
     std::memcpy(&id, id128, sizeof(id));
     HS_NCCL(ncclCommInitRank(&e->comm, nranks, id, rank));

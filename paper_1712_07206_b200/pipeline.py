@@ -323,8 +323,8 @@ class Engine:
                                                     S.ctypes.data_as(C.c_void_p)), "engine_download")
         return H, S
 
-    def set_comm(self, uid: bytes, nranks, rank):
-        buf = C.create_string_buffer(uid, 128)
+    def set_comm(self, uid: Optional[bytes], nranks, rank):
+        buf = None if uid is None else C.create_string_buffer(uid, 128)
         check(_lib.lib().hsdla_b200_engine_set_comm(self.h, buf, C.c_int(nranks), C.c_int(rank)), "set_comm")
 
     def stream(self):

@@ -213,3 +213,27 @@ def test_operators_with_complex_diagonals_follow_reference_hemm(restatement, var
         H, S, _ = restatement.build_hs_refined(p)
         r = hb.build_hs_refined(p)
     assert rel(r.H, H) <= TOL and rel(r.S, S) <= TOL
+
+
+@pytest.mark.parametrize("algo", ["fused", "original"])
+def test_nccl_reduce_path_single_rank(restatement, algo):
+    """The multi-GPU reduce path (comm stream, S reduce overlapping H, ncclReduce of the
+    packed triangles, download ordered after the reduce) through a real 1-rank NCCL
+    communicator: same result as the communicator-free build."""
+    p = hb.generate_problem(6, 25, 300, 4, 1)
+    H0, S0 = (restatement.build_hs_original(p)[:2] if algo == "original" else restatement.build_hs_refined(p)[:2])
+    e = hb.Engine(0, p.n_atoms, p.n_l, p.n_g)
+    e.set_comm(hb.nccl_unique_id(), 1, 0)
+    for streamed in (False, True):
+        if streamed:
+            e.build_streamed(p, 0, algo)
+        else:
+            e.upload(p)
+            e.build(algo)
+        e.reduce(0)
+        st = e.sync()
+        H, S = e.download()
+        assert rel(H, H0) <= TOL and rel(S, S0) <= TOL
+        assert st["reduce_seconds"] >= 0.0
+    e.set_comm(None, 1, 0)
+    e.close()
