@@ -250,6 +250,7 @@ struct hsdla_b200_engine {
   static constexpr int kD2hPieces = 4;   // H downloads in column-range pieces, unpacked as each lands
   cudaEvent_t ev_h_piece[kD2hPieces] = {};
   cudaEvent_t ev_h_band[kD2hPieces] = {};  // final H contraction finished tile-column band q
+  cudaEvent_t ev_h_red[kD2hPieces] = {};   // ... and band q's packed range is reduced (NCCL)
   int piece_tiles[kD2hPieces + 1] = {};    // tile-column boundaries of the pieces / bands
   bool band_final_h = false;               // this build runs its final H contraction band by band
   bool banded = false;                     // ... and the last build did
@@ -315,6 +316,8 @@ static void engine_free(hsdla_b200_engine* e) {
   for (cudaEvent_t ev : e->ev_h_piece)
     if (ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e->ev_h_band)
+    if (ev) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : e->ev_h_red)
     if (ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : {e->ev_begin, e->ev_end, e->ev_s_done, e->ev_s_red, e->ev_reduce_end, e->ev_up0, e->ev_up1,
                          e->ev_s_d2h, e->ev_setup0, e->ev_setup1})
@@ -475,6 +478,13 @@ static void make_pieces(hsdla_b200_engine* e) {
   e->piece_tiles[Q] = T;
 }
 
+static inline uint64_t packed_col(uint64_t n, uint64_t j) { return j * (2 * n - j + 1) / 2; }
+
+// First matrix column of download piece q (= tile-column band q of the final H launch).
+static uint64_t piece_col(const hsdla_b200_engine* e, int q) {
+  return std::min<uint64_t>(e->ng, static_cast<uint64_t>(e->piece_tiles[q]) * kTriBM);
+}
+
 static void make_plans(hsdla_b200_engine* e) {
   make_pieces(e);
   e->whole.resize(1);
@@ -518,6 +528,7 @@ static hsdla_b200_engine* engine_create(int device, uint64_t na, uint64_t nl, ui
       HS_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     for (cudaEvent_t& ev : e->ev_h_piece) HS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     for (cudaEvent_t& ev : e->ev_h_band) HS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    for (cudaEvent_t& ev : e->ev_h_red) HS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     for (auto& t : e->ring)
       for (cudaEvent_t* ev : {&t.s0, &t.s1, &t.h0, &t.h1}) HS_CUDA(cudaEventCreate(ev));
     const uint64_t KG = e->K * ng;
@@ -659,7 +670,9 @@ static void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool la
   // The build's final H contraction: whole, or band by band (tile-column bands of
   // equal work, event after each) so the download of band q overlaps band q+1.
   auto final_h = [&](const CtnParams& P) {
-    if (!(last && e->band_final_h)) {
+    // bands: the one-shot drop-in (download overlaps) and every multi-rank build (the
+    // NCCL reduce of band q overlaps the compute of band q+1)
+    if (!(last && (e->band_final_h || e->comm))) {
       CtnParams q = P;
       launch_tri(e, q, cp.grid_tri);
       return;
@@ -809,11 +822,32 @@ static void reduce_s(hsdla_b200_engine* e, int root) {
   HS_CUDA(cudaStreamWaitEvent(e->comm_stream, e->ev_s_done, 0));
   HS_NCCL(ncclReduce(e->Sp, e->Sp, 2 * e->npk, ncclFloat64, ncclSum, root, e->comm, e->comm_stream));
 }
-static void reduce_h(hsdla_b200_engine* e, int root) {
+static void reduce_h_mark(hsdla_b200_engine* e) {
   HS_CUDA(cudaSetDevice(e->device));
   HS_CUDA(cudaEventRecord(e->ev_s_red, e->comm_stream));
-  HS_CUDA(cudaStreamWaitEvent(e->comm_stream, e->ev_end, 0));
-  HS_NCCL(ncclReduce(e->Hp, e->Hp, 2 * e->npk, ncclFloat64, ncclSum, root, e->comm, e->comm_stream));
+}
+// H reduce of band q (banded build) or of the whole packed H (q = -1).
+static void reduce_h_band(hsdla_b200_engine* e, int root, int q) {
+  HS_CUDA(cudaSetDevice(e->device));
+  uint64_t b0 = 0, b1 = e->npk;
+  if (q >= 0) {
+    HS_CUDA(cudaStreamWaitEvent(e->comm_stream, e->ev_h_band[q], 0));
+    b0 = packed_col(e->ng, piece_col(e, q));
+    b1 = packed_col(e->ng, piece_col(e, q + 1));
+  } else {
+    HS_CUDA(cudaStreamWaitEvent(e->comm_stream, e->ev_end, 0));
+  }
+  if (b1 > b0)
+    HS_NCCL(ncclReduce(e->Hp + b0, e->Hp + b0, 2 * (b1 - b0), ncclFloat64, ncclSum, root, e->comm, e->comm_stream));
+  if (q >= 0) HS_CUDA(cudaEventRecord(e->ev_h_red[q], e->comm_stream));
+}
+static void reduce_h(hsdla_b200_engine* e, int root) {
+  reduce_h_mark(e);
+  if (e->banded) {
+    for (int q = 0; q < hsdla_b200_engine::kD2hPieces; ++q) reduce_h_band(e, root, q);
+  } else {
+    reduce_h_band(e, root, -1);
+  }
 }
 static void reduce_finish(hsdla_b200_engine* e) {
   HS_CUDA(cudaSetDevice(e->device));
@@ -857,7 +891,6 @@ static void engine_sync(hsdla_b200_engine* e, hsdla_b200_stats* st) {
   st->kernel_launches = e->launches;
 }
 
-static inline uint64_t packed_col(uint64_t n, uint64_t j) { return j * (2 * n - j + 1) / 2; }
 
 // Unpack columns [c0, c1) of a column-major packed lower triangle (pk = the whole
 // packed array) into the lower triangle of an n x n matrix, over up to 16 threads
@@ -886,11 +919,6 @@ static void unpack_lower(const double2* pk, double2* full, uint64_t n, uint64_t 
   for (auto& t : th) t.join();
 }
 
-// First matrix column of download piece q (= tile-column band q of the final H launch).
-static uint64_t piece_col(const hsdla_b200_engine* e, int q) {
-  return std::min<uint64_t>(e->ng, static_cast<uint64_t>(e->piece_tiles[q]) * kTriBM);
-}
-
 static void ensure_stage(hsdla_b200_engine* e) {
   if (!e->host_stage)
     HS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&e->host_stage), 2 * e->npk * sizeof(double2)));
@@ -906,7 +934,8 @@ static void enqueue_download(hsdla_b200_engine* e) {
   HS_CUDA(cudaEventRecord(e->ev_s_d2h, e->copy_stream));
   if (!e->banded) HS_CUDA(cudaStreamWaitEvent(e->copy_stream, e->reduced ? e->ev_reduce_end : e->ev_end, 0));
   for (int q = 0; q < hsdla_b200_engine::kD2hPieces; ++q) {
-    if (e->banded) HS_CUDA(cudaStreamWaitEvent(e->copy_stream, e->ev_h_band[q], 0));
+    // banded: piece q is final once band q is computed (one GPU) or reduced (NCCL)
+    if (e->banded) HS_CUDA(cudaStreamWaitEvent(e->copy_stream, e->reduced ? e->ev_h_red[q] : e->ev_h_band[q], 0));
     const uint64_t b0 = packed_col(e->ng, piece_col(e, q)), b1 = packed_col(e->ng, piece_col(e, q + 1));
     if (b1 > b0)
       HS_CUDA(cudaMemcpyAsync(e->host_stage + b0, e->Hp + b0, (b1 - b0) * sizeof(double2), cudaMemcpyDeviceToHost,
@@ -1399,7 +1428,7 @@ static void one_shot(const hsdla_b200_options* o, uint64_t na, uint64_t nl, uint
   std::vector<char> bad(P, 0);
   auto run = [&](int r) {
     hsdla_b200_engine* e = set->engines[r];
-    e->band_final_h = P == 1;
+    e->band_final_h = true;
     try {
       load[r] = start(e, set->atom0[r], algo);
     } catch (const Fail& f) {
@@ -1425,9 +1454,14 @@ static void one_shot(const hsdla_b200_options* o, uint64_t na, uint64_t nl, uint
     HS_NCCL(ncclGroupStart());
     for (int r = 0; r < P; ++r) reduce_s(set->engines[r], 0);
     HS_NCCL(ncclGroupEnd());
-    HS_NCCL(ncclGroupStart());
-    for (int r = 0; r < P; ++r) reduce_h(set->engines[r], 0);
-    HS_NCCL(ncclGroupEnd());
+    // H: one NCCL group per tile-column band, so band q's reduce overlaps band q+1
+    for (int r = 0; r < P; ++r) reduce_h_mark(set->engines[r]);
+    const bool banded = set->engines[0]->banded;
+    for (int q = banded ? 0 : -1; q < (banded ? hsdla_b200_engine::kD2hPieces : 0); ++q) {
+      HS_NCCL(ncclGroupStart());
+      for (int r = 0; r < P; ++r) reduce_h_band(set->engines[r], 0, q);
+      HS_NCCL(ncclGroupEnd());
+    }
     for (int r = 0; r < P; ++r) reduce_finish(set->engines[r]);
   }
   hsdla_b200_engine* root = set->engines[0];
