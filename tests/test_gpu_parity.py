@@ -237,3 +237,24 @@ def test_nccl_reduce_path_single_rank(restatement, algo):
         assert st["reduce_seconds"] >= 0.0
     e.set_comm(None, 1, 0)
     e.close()
+
+
+EDGE_DIMS = [(1, 1, 1, 1, 0), (1, 2, 2, 2, 0), (3, 3, 63, 3, 1), (2, 5, 65, 4, 1), (1, 7, 129, 5, 0),
+             (7, 1, 200, 6, 3), (9, 4, 1, 7, 2), (2, 9, 64, 8, 0), (5, 2, 257, 9, 5), (3, 17, 3, 10, 1)]
+
+
+@pytest.mark.parametrize("dims", EDGE_DIMS, ids=lambda d: "x".join(map(str, d[:3])))
+def test_edge_shapes_all_algorithms(restatement, dims):
+    """Ragged / degenerate shapes: N_G and K = N_A N_L not multiples of the 8-complex k-slab or
+    the 64-wide tiles, N_L = 1, N_G = 1..3, one atom, all-failed potrf mixes."""
+    p = hb.generate_problem(*dims)
+    H, S, _ = restatement.build_hs_refined(p)
+    Ho, So, _, n_hpd = restatement.build_hs_original(p)
+    n = p.n_g
+    iu = np.triu_indices(n, 1)
+    for cfg in (hb.PipelineConfig(), hb.PipelineConfig(algo="refined"), hb.PipelineConfig(variant="original")):
+        r = hb.build_hs(p, cfg)
+        Hw, Sw = (Ho, So) if cfg.variant == "original" else (H, S)
+        assert rel(r.H, Hw) <= TOL and rel(r.S, Sw) <= TOL, (dims, cfg)
+        assert np.all(r.H[iu] == 0) and np.all(r.S[iu] == 0)
+        assert r.ledger == hb.flop_model(p, cfg.variant)
