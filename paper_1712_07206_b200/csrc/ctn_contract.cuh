@@ -463,40 +463,46 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>
       tile_origin(pc.tile, row0, col0, atom);
       const double ar = P.alpha_re, ai = P.alpha_im, beta = P.beta;
       const bool keep_di = MODE == kTri && P.keep_diag_imag != nullptr && *P.keep_diag_imag != 0;
+      // destination of accumulator element (mb, nb, e); nullptr outside the output
+      auto dst_of = [&](int mb, int nb, int e) -> double2* {
+        const int i = row0 + wm * Cfg::kWM + 8 * mb + pg;
+        const int j = col0 + wn * Cfg::kWN + 8 * nb + (e ? 4 + q : q);
+        if (MODE == kTri) return (i < P.n && j < P.n && i >= j) ? P.out + packed_index(P.n, i, j) : nullptr;
+        return (i < P.m_valid && j < P.n)
+                   ? P.out + (static_cast<uint64_t>(atom) * P.m_valid + i) + static_cast<uint64_t>(j) * P.ldo
+                   : nullptr;
+      };
+      // Per row block mb: with beta != 0 gather its old values first (NB x 2 independent
+      // loads in flight together), then combine and store.
 #pragma unroll
       for (int mb = 0; mb < MB; ++mb) {
         const int i = row0 + wm * Cfg::kWM + 8 * mb + pg;
+        double2 old[NB][2];
+        if (beta != 0.0) {
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const double2* d = dst_of(mb, nb, e);
+              old[nb][e] = d ? __ldcg(d) : make_double2(0.0, 0.0);
+            }
+        }
 #pragma unroll
         for (int nb = 0; nb < NB; ++nb) {
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
+            double2* d = dst_of(mb, nb, e);
+            if (!d) continue;
             const int j = col0 + wn * Cfg::kWN + 8 * nb + (e ? 4 + q : q);
             const double xr = acc[mb][nb][e][0], xi = acc[mb][nb][e][1];
             double vr = ar * xr - ai * xi;
             double vi = ar * xi + ai * xr;
-            if (MODE == kTri) {
-              if (i < P.n && j < P.n && i >= j) {
-                if (i == j && !keep_di) vi = 0.0;
-                double2* dst = P.out + packed_index(P.n, i, j);
-                if (beta != 0.0) {
-                  const double2 o = *dst;
-                  vr += beta * o.x;
-                  vi += beta * o.y;
-                }
-                *dst = make_double2(vr, vi);
-              }
-            } else {
-              if (i < P.m_valid && j < P.n) {
-                double2* dst =
-                    P.out + (static_cast<uint64_t>(atom) * P.m_valid + i) + static_cast<uint64_t>(j) * P.ldo;
-                if (beta != 0.0) {
-                  const double2 o = *dst;
-                  vr += beta * o.x;
-                  vi += beta * o.y;
-                }
-                *dst = make_double2(vr, vi);
-              }
+            if (MODE == kTri && i == j && !keep_di) vi = 0.0;
+            if (beta != 0.0) {
+              vr += beta * old[nb][e].x;
+              vi += beta * old[nb][e].y;
             }
+            *d = make_double2(vr, vi);
           }
         }
       }
