@@ -347,13 +347,16 @@ def run_lapw(args, hb, p, na, nl, ng):
     for b in ops:
         hb.host_register(b)
     try:
-        times = []
+        times, stimes = [], []
         for _ in range(5):
             eng.setup_lapw(s)
             eng.sync()
-            times.append(eng.setup_time()["ms"])
+            t_ = eng.setup_time()
+            times.append(t_["ms"])
+            stimes.append(t_["stream_ms"])
         nbytes = eng.setup_time()["bytes"]
         ms = float(np.median(times))
+        sms = float(np.median(stimes))
         peak, src = hbm_peak()
 
         def one():
@@ -376,12 +379,13 @@ def run_lapw(args, hb, p, na, nl, ng):
         eng.close()
     h2d = s.gvec.nbytes + s.tau.nbytes + 6 * s.u.nbytes + 3 * p.T_AA.nbytes
     return {
-        "setup_roofline": {"bound": "hbm", "achieved": nbytes / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
-                           "frac": nbytes / (ms * 1e-3) / 1e9 / peak,
-                           "traffic": load_traffic(args.config, "setup_dram_bytes_per_launch"),
-                           "kernel": "lapw_tables_kernel + lapw_stream_kernel (A, B = 2 x K x N_G x 16 B written "
-                                     "per launch; time = both kernels)",
-                           "bytes_per_launch": int(nbytes), "kernel_ms": ms, "peak_source": src},
+        "setup_roofline": {"bound": "hbm", "achieved": nbytes / (sms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                           "frac": nbytes / (sms * 1e-3) / 1e9 / peak,
+                           "traffic": load_traffic(args.config, "setup_stream_dram_bytes_per_launch"),
+                           "kernel": "lapw_stream_kernel (the HBM-write pass: A, B = 2 x K x N_G x 16 B per launch)",
+                           "bytes_per_launch": int(nbytes), "kernel_ms": sms, "peak_source": src,
+                           "setup_ms_total": ms, "setup_gbs_total": nbytes / (ms * 1e-3) / 1e9,
+                           "note": "setup = lapw_tables_kernel (latency-bound per-G tables) + lapw_stream_kernel"},
         "e2e_lapw": {"value": ledger_flops(na, nl, ng) / dt / 1e12, "unit": "TFLOP/s", "ms_per_step": dt * 1e3,
                      "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(2 * (ng * (ng + 1) // 2) * 16),
                      "api": "engine_setup_lapw + engine_upload_operators + engine_build + engine_download (C-ABI); "

@@ -273,8 +273,9 @@ int hsdla_b200_engine_setup_lapw(hsdla_b200_engine* e, const hsdla_b200_lapw* sy
 /* H2D of the shard's T_AA, T_AB, T_BB blocks only (with setup_lapw: a build needs no A/B upload). */
 int hsdla_b200_engine_upload_operators(hsdla_b200_engine* e, const double* T_AA, const double* T_AB,
                                        const double* T_BB, uint64_t atom_begin);
-/* Mean CUDA-event time (ms) of the last setup_lapw kernel and its bytes written. */
-int hsdla_b200_engine_setup_time(hsdla_b200_engine* e, double* ms, uint64_t* bytes);
+/* CUDA-event times (ms) of the last setup_lapw: both kernels (ms) and the HBM-write
+ * stream kernel alone (ms_stream, nullable), and the bytes written. */
+int hsdla_b200_engine_setup_time(hsdla_b200_engine* e, double* ms, uint64_t* bytes, double* ms_stream);
 
 #ifdef __cplusplus
 }

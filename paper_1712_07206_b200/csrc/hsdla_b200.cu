@@ -258,7 +258,8 @@ struct hsdla_b200_engine {
   int last_algo = 0, launches = 0;
   uint64_t n_hpd_last = 0;
   bool built = false, reduced = false, uploaded_streamed = false;
-  cudaEvent_t ev_setup0 = nullptr, ev_setup1 = nullptr;  // last LAPW setup kernel
+  cudaEvent_t ev_setup0 = nullptr, ev_setup1 = nullptr;  // last LAPW setup (tables + stream kernels)
+  cudaEvent_t ev_setup_mid = nullptr;                      // between the two kernels
   uint64_t setup_bytes = 0;
   void* lapw_scratch = nullptr;  // device copy of the LAPW inputs (grown on demand)
   // HSDL file reader: two pinned 64 MB staging slabs, allocated on first use
@@ -320,7 +321,7 @@ static void engine_free(hsdla_b200_engine* e) {
   for (cudaEvent_t ev : e->ev_h_red)
     if (ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : {e->ev_begin, e->ev_end, e->ev_s_done, e->ev_s_red, e->ev_reduce_end, e->ev_up0, e->ev_up1,
-                         e->ev_s_d2h, e->ev_setup0, e->ev_setup1})
+                         e->ev_s_d2h, e->ev_setup0, e->ev_setup1, e->ev_setup_mid})
     if (ev) cudaEventDestroy(ev);
   for (auto& t : e->ring)
     for (cudaEvent_t ev : {t.s0, t.s1, t.h0, t.h1})
@@ -522,7 +523,7 @@ static hsdla_b200_engine* engine_create(int device, uint64_t na, uint64_t nl, ui
     HS_CUDA(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
     HS_CUDA(cudaStreamCreateWithFlags(&e->comm_stream, cudaStreamNonBlocking));
     for (cudaEvent_t* ev : {&e->ev_begin, &e->ev_end, &e->ev_reduce_end, &e->ev_up0, &e->ev_up1, &e->ev_setup0,
-                            &e->ev_setup1})
+                            &e->ev_setup1, &e->ev_setup_mid})
       HS_CUDA(cudaEventCreate(ev));
     for (cudaEvent_t* ev : {&e->ev_s_done, &e->ev_s_red, &e->ev_s_d2h})
       HS_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
@@ -1005,7 +1006,8 @@ static size_t lapw_scratch_size(const hsdla_b200_lapw* sys, uint64_t na) {
 // Compute A, B (ld = ldo rows) and U for atoms [a0, a0+na) of sys on stream s.
 // `scratch` (lapw_scratch_size bytes, device) receives the inputs and the per-G tables.
 static void lapw_enqueue(const hsdla_b200_lapw* sys, uint64_t a0, uint64_t na, double2* A, double2* B, uint64_t ldo,
-                         double* U, void* scratch, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
+                         double* U, void* scratch, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1,
+                         cudaEvent_t ev_mid = nullptr) {
   const int nlv = sys->lmax + 1, nl = nlv * nlv;
   // pack [gvec | tau | radial(u,u',udot,udot') | rmt | udot_norm | ylm coefficients | type] into one host block
   const size_t n_g3 = sys->n_g * 3, n_t3 = na * 3, n_rad = sys->n_types * nlv * 4, n_un = sys->n_types * nlv;
@@ -1060,6 +1062,7 @@ static void lapw_enqueue(const hsdla_b200_lapw* sys, uint64_t a0, uint64_t na, d
   if (ev0) HS_CUDA(cudaEventRecord(ev0, s));
   lapw_tables_kernel<<<tgrid, 256, 0, s>>>(P, tabY, tabF, tabS);
   HS_CUDA(cudaGetLastError());
+  if (ev_mid) HS_CUDA(cudaEventRecord(ev_mid, s));
   constexpr int kRows = 4;
   const uint64_t K = na * nl;
   const uint64_t row_blocks = (K + 256 * kRows - 1) / (256 * kRows);
@@ -1088,7 +1091,8 @@ static void engine_setup_lapw(hsdla_b200_engine* e, const hsdla_b200_lapw* sys, 
     HS_CUDA(cudaMalloc(&e->lapw_scratch, need));
     e->lapw_scratch_bytes = need;
   }
-  lapw_enqueue(sys, a0, e->na, e->A, e->B, e->K, e->U, e->lapw_scratch, e->stream, e->ev_setup0, e->ev_setup1);
+  lapw_enqueue(sys, a0, e->na, e->A, e->B, e->K, e->U, e->lapw_scratch, e->stream, e->ev_setup0, e->ev_setup1,
+               e->ev_setup_mid);
   e->setup_bytes = 2 * e->K * e->ng * sizeof(double2);
 }
 
@@ -2095,12 +2099,13 @@ int hsdla_b200_engine_upload_operators(hsdla_b200_engine* e, const double* T_AA,
     engine_upload_operators(e, T_AA, T_AB, T_BB, atom_begin);
   });
 }
-int hsdla_b200_engine_setup_time(hsdla_b200_engine* e, double* ms, uint64_t* bytes) {
+int hsdla_b200_engine_setup_time(hsdla_b200_engine* e, double* ms, uint64_t* bytes, double* ms_stream) {
   return guarded([&] {
     if (!e) throw Fail{HSDLA_B200_CONFIG_ERROR, "null engine"};
     if (!e->setup_bytes) throw Fail{HSDLA_B200_CONFIG_ERROR, "no setup_lapw has run"};
     HS_CUDA(cudaEventSynchronize(e->ev_setup1));
     if (ms) *ms = ev_ms(e->ev_setup0, e->ev_setup1);
+    if (ms_stream) *ms_stream = ev_ms(e->ev_setup_mid, e->ev_setup1);
     if (bytes) *bytes = e->setup_bytes;
   });
 }

@@ -140,9 +140,12 @@ def _engine_upload_operators(eng, T_AA, T_AB, T_BB, atom_begin=0):
 
 
 def _engine_setup_time(eng):
-    ms, nb = C.c_double(), C.c_uint64()
-    check(_lib.lib().hsdla_b200_engine_setup_time(eng.h, C.byref(ms), C.byref(nb)), "engine_setup_time")
-    return {"ms": ms.value, "bytes": nb.value}
+    """CUDA-event times of the last setup: ms (tables + stream kernels), stream_ms (the
+    HBM-write stream kernel alone) and the bytes written."""
+    ms, nb, ms_s = C.c_double(), C.c_uint64(), C.c_double()
+    check(_lib.lib().hsdla_b200_engine_setup_time(eng.h, C.byref(ms), C.byref(nb), C.byref(ms_s)),
+          "engine_setup_time")
+    return {"ms": ms.value, "bytes": nb.value, "stream_ms": ms_s.value}
 
 
 Engine.setup_lapw = _engine_setup_lapw
