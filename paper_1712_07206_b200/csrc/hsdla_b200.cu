@@ -606,6 +606,101 @@ static void engine_fill_synthetic(hsdla_b200_engine* e, uint64_t seed) {
   fill(e->U, e->K, 6, 0.5, 1.5);
 }
 
+// fn(i) for i in [0, n) over up to 16 host threads when the work is large.
+template <class F>
+static void par_for(uint64_t n, uint64_t bytes, F&& fn) {
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const unsigned nt = bytes < (size_t(4) << 20) ? 1u : static_cast<unsigned>(std::min<uint64_t>(hw, n));
+  if (nt <= 1) {
+    for (uint64_t i = 0; i < n; ++i) fn(i);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < nt; ++t)
+    th.emplace_back([&, t] {
+      for (uint64_t i = n * t / nt; i < n * (t + 1) / nt; ++i) fn(i);
+    });
+  for (auto& x : th) x.join();
+}
+
+// Staging ring of two pinned slabs owned by the engine; slab s is free again once
+// the copy that read it has completed.
+constexpr size_t kStageSlab = size_t(64) << 20;
+static char* stage_acquire(hsdla_b200_engine* e, int& slot) {
+  if (!e->stage_buf[0])
+    for (int i = 0; i < 2; ++i) {
+      HS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&e->stage_buf[i]), kStageSlab));
+      HS_CUDA(cudaEventCreateWithFlags(&e->stage_ev[i], cudaEventDisableTiming));
+    }
+  slot = e->stage_next;
+  e->stage_next ^= 1;
+  if (e->stage_busy[slot]) HS_CUDA(cudaEventSynchronize(e->stage_ev[slot]));
+  e->stage_busy[slot] = true;
+  return e->stage_buf[slot];
+}
+static void stage_release(hsdla_b200_engine* e, int slot, cudaStream_t s) {
+  HS_CUDA(cudaEventRecord(e->stage_ev[slot], s));
+}
+
+// True if [p, p + bytes) is page-locked host memory (registered or cudaMallocHost).
+static bool is_pinned(const void* p, size_t bytes) {
+  if (!p || !bytes) return true;
+  cudaPointerAttributes a0{}, a1{};
+  const void* last = static_cast<const char*>(p) + bytes - 1;
+  if (cudaPointerGetAttributes(&a0, p) != cudaSuccess || cudaPointerGetAttributes(&a1, last) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return false;
+  }
+  return a0.type == cudaMemoryTypeHost && a1.type == cudaMemoryTypeHost;
+}
+
+// upload_atoms for PAGEABLE caller buffers: the rows of atoms [b0, b1) are packed by up
+// to 16 host threads into the engine's pinned staging slabs and copied from there
+// (a pageable cudaMemcpy is host-synchronous and single-threaded, ~10 GB/s).
+static void upload_atoms_staged(hsdla_b200_engine* e, const hsdla_b200_problem* p, uint64_t a0, uint64_t b0,
+                                uint64_t b1, cudaStream_t s) {
+  const uint64_t Kg = p->n_atoms * p->n_l, nl = e->nl, ng = e->ng;
+  const uint64_t r0 = b0 * nl, rows = (b1 - b0) * nl, g0 = (a0 + b0) * nl;
+  const size_t colb = rows * sizeof(double2);
+  for (int m = 0; m < 2; ++m) {
+    const double2* src = reinterpret_cast<const double2*>(m == 0 ? p->A : p->B) + g0;
+    double2* dst = (m == 0 ? e->A : e->B) + r0;
+    if (colb > kStageSlab) {  // one column's rows exceed a slab: direct (pageable) copy
+      HS_CUDA(cudaMemcpy2DAsync(dst, e->K * sizeof(double2), src, Kg * sizeof(double2), colb, ng,
+                                cudaMemcpyHostToDevice, s));
+      continue;
+    }
+    const uint64_t cols = std::max<uint64_t>(1, kStageSlab / colb);
+    for (uint64_t j0 = 0; j0 < ng; j0 += cols) {
+      const uint64_t nc = std::min(cols, ng - j0);
+      int slot;
+      char* b = stage_acquire(e, slot);
+      par_for(nc, nc * colb, [&](uint64_t j) { std::memcpy(b + j * colb, src + (j0 + j) * Kg, colb); });
+      HS_CUDA(cudaMemcpy2DAsync(dst + j0 * e->K, e->K * sizeof(double2), b, colb, colb, nc, cudaMemcpyHostToDevice,
+                                s));
+      stage_release(e, slot, s);
+    }
+  }
+  // operator blocks and U: small, packed into one slab
+  const uint64_t blk = nl * nl, nb = b1 - b0;
+  const size_t tb = nb * blk * sizeof(double2), ub = rows * sizeof(double);
+  if (3 * tb + ub > kStageSlab) {
+    upload_atoms(e, p, a0, b0, b1, s);  // (re-copies A, B: only for > 64 MB of operators per chunk)
+    return;
+  }
+  int slot;
+  char* b = stage_acquire(e, slot);
+  const double* srcs[3] = {p->T_AA, p->T_AB, p->T_BB};
+  double2* dsts[3] = {e->Taa, e->Tab, e->Tbb};
+  for (int m = 0; m < 3; ++m) {
+    std::memcpy(b + m * tb, reinterpret_cast<const double2*>(srcs[m]) + (a0 + b0) * blk, tb);
+    HS_CUDA(cudaMemcpyAsync(dsts[m] + b0 * blk, b + m * tb, tb, cudaMemcpyHostToDevice, s));
+  }
+  std::memcpy(b + 3 * tb, p->U + g0, ub);
+  HS_CUDA(cudaMemcpyAsync(e->U + r0, b + 3 * tb, ub, cudaMemcpyHostToDevice, s));
+  stage_release(e, slot, s);
+}
+
 static void engine_upload(hsdla_b200_engine* e, const hsdla_b200_problem* p, uint64_t a0) {
   check_problem(e, p, a0);
   HS_CUDA(cudaSetDevice(e->device));
@@ -801,16 +896,27 @@ static void engine_build_streamed(hsdla_b200_engine* e, const hsdla_b200_problem
   // the copy stream may only overwrite A/B/T/U once the previous build has consumed them
   HS_CUDA(cudaStreamWaitEvent(e->copy_stream, e->ev_end, 0));
   HS_CUDA(cudaEventRecord(e->ev_up0, e->copy_stream));
-  for (size_t c = 0; c < e->streamed.size(); ++c) {
-    upload_atoms(e, p, a0, e->streamed[c].a0, e->streamed[c].a1, e->copy_stream);
-    HS_CUDA(cudaEventRecord(e->ev_chunk_up[c], e->copy_stream));
+  const uint64_t ab_bytes = p->n_atoms * p->n_l * p->n_g * sizeof(double2);
+  const bool pinned = is_pinned(p->A, ab_bytes) && is_pinned(p->B, ab_bytes);
+  if (pinned) {
+    // page-locked inputs: every chunk's copies are asynchronous, enqueue them all first
+    for (size_t c = 0; c < e->streamed.size(); ++c) {
+      upload_atoms(e, p, a0, e->streamed[c].a0, e->streamed[c].a1, e->copy_stream);
+      HS_CUDA(cudaEventRecord(e->ev_chunk_up[c], e->copy_stream));
+    }
   }
-  HS_CUDA(cudaEventRecord(e->ev_up1, e->copy_stream));
   for (size_t c = 0; c < e->streamed.size(); ++c) {
+    if (!pinned) {
+      // pageable inputs: the host packs chunk c into the pinned slabs while the GPU
+      // already computes chunk c-1 (its phases were enqueued in the previous iteration)
+      upload_atoms_staged(e, p, a0, e->streamed[c].a0, e->streamed[c].a1, e->copy_stream);
+      HS_CUDA(cudaEventRecord(e->ev_chunk_up[c], e->copy_stream));
+    }
     HS_CUDA(cudaStreamWaitEvent(e->stream, e->ev_chunk_up[c], 0));
     if (c == 0) HS_CUDA(cudaEventRecord(e->ev_begin, e->stream));
     enqueue_chunk(e, e->streamed[c], algo, c + 1 == e->streamed.size(), nullptr);
   }
+  HS_CUDA(cudaEventRecord(e->ev_up1, e->copy_stream));
   HS_CUDA(cudaEventRecord(e->ev_end, e->stream));
   e->uploaded_streamed = true;
 }
@@ -1180,25 +1286,6 @@ static int open_hsdl(const char* path) {
   const int fd = open(path, O_RDONLY);
   if (fd < 0) throw Fail{HSDLA_B200_IO_ERROR, std::string("cannot open: ") + path};
   return fd;
-}
-
-// Staging ring of two pinned slabs owned by the engine; slab s is free again once
-// the copy that read it has completed.
-constexpr size_t kStageSlab = size_t(64) << 20;
-static char* stage_acquire(hsdla_b200_engine* e, int& slot) {
-  if (!e->stage_buf[0])
-    for (int i = 0; i < 2; ++i) {
-      HS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&e->stage_buf[i]), kStageSlab));
-      HS_CUDA(cudaEventCreateWithFlags(&e->stage_ev[i], cudaEventDisableTiming));
-    }
-  slot = e->stage_next;
-  e->stage_next ^= 1;
-  if (e->stage_busy[slot]) HS_CUDA(cudaEventSynchronize(e->stage_ev[slot]));
-  e->stage_busy[slot] = true;
-  return e->stage_buf[slot];
-}
-static void stage_release(hsdla_b200_engine* e, int slot, cudaStream_t s) {
-  HS_CUDA(cudaEventRecord(e->stage_ev[slot], s));
 }
 
 // Read `n` pieces of `piece` bytes at offsets off0 + i*stride into dst (packed),
@@ -1603,23 +1690,6 @@ static Ring& ring_for(int device) {
   auto& r = rings[device];
   if (!r) r = std::make_unique<Ring>();
   return *r;
-}
-
-// fn(i) for i in [0, n) over up to 16 host threads when the work is large.
-template <class F>
-static void par_for(uint64_t n, uint64_t bytes, F&& fn) {
-  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-  const unsigned nt = bytes < (size_t(4) << 20) ? 1u : static_cast<unsigned>(std::min<uint64_t>(hw, n));
-  if (nt <= 1) {
-    for (uint64_t i = 0; i < n; ++i) fn(i);
-    return;
-  }
-  std::vector<std::thread> th;
-  for (unsigned t = 0; t < nt; ++t)
-    th.emplace_back([&, t] {
-      for (uint64_t i = n * t / nt; i < n * (t + 1) / nt; ++i) fn(i);
-    });
-  for (auto& x : th) x.join();
 }
 
 struct Ctx {
