@@ -54,14 +54,14 @@ void run(const char* name, double2* A, double2* B, double2* out, uint64_t K, uin
   static double* ws = nullptr;
   static uint32_t* flags = nullptr;
   if (!ws) {
-    cudaMalloc(&ws, 148ull * 128 * 128 * 2 * 8);
-    cudaMalloc(&flags, 148 * 4);
-    cudaMemset(flags, 0, 148 * 4);
+    cudaMalloc(&ws, 4 * 148ull * 128 * 128 * 2 * 8);
+    cudaMalloc(&flags, 4 * 148 * 4);
+    cudaMemset(flags, 0, 4 * 148 * 4);
   }
   P.sk_ws = ws;
   P.sk_flags = flags;
   static uint32_t epoch = 0;
-  int grid = 148;
+  int grid = 148 * MINB;
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::kThreads, Cfg::kSmemBytes);
   cudaEvent_t e0, e1;
@@ -95,14 +95,11 @@ int main(int argc, char** argv) {
   fill<<<1024, 256>>>((double*)A, 2 * K * ng, 1);
   fill<<<1024, 256>>>((double*)B, 2 * K * ng, 2);
   printf("K %lu N_G %lu nseg %d\n", K, ng, nseg);
-  run<64, 2, 4, 6, 1>("64 2x4 (32x16) st6 minb1 [current]", A, B, out, K, ng, nseg);
-  run<64, 4, 4, 6, 1>("64 4x4 (16x16) st6 minb1", A, B, out, K, ng, nseg);
-  run<64, 4, 4, 4, 1>("64 4x4 (16x16) st4 minb1", A, B, out, K, ng, nseg);
-  run<64, 2, 4, 8, 1>("64 2x4 (32x16) st8 minb1", A, B, out, K, ng, nseg);
+  run<64, 2, 4, 8, 1>("64 2x4 (32x16) st8 minb1 [current]", A, B, out, K, ng, nseg);
+  run<32, 1, 2, 8, 2>("32 1x2 (32x16) st8 minb2", A, B, out, K, ng, nseg);
+  run<32, 1, 2, 8, 3>("32 1x2 (32x16) st8 minb3", A, B, out, K, ng, nseg);
+  run<32, 2, 2, 8, 2>("32 2x2 (16x16) st8 minb2", A, B, out, K, ng, nseg);
+  run<32, 1, 4, 8, 2>("32 1x4 (32x8) st8 minb2", A, B, out, K, ng, nseg);
   run<64, 2, 4, 4, 1>("64 2x4 (32x16) st4 minb1", A, B, out, K, ng, nseg);
-  run<64, 2, 8, 4, 1>("64 2x8 (32x8) st4 minb1", A, B, out, K, ng, nseg);
-  run<64, 4, 2, 6, 1>("64 4x2 (16x32) st6 minb1", A, B, out, K, ng, nseg);
-  run<128, 4, 4, 4, 1>("128 4x4 (32x32) st4 minb1", A, B, out, K, ng, nseg);
-  run<64, 2, 4, 6, 1>("64 2x4 (32x16) st6 minb1 [current]", A, B, out, K, ng, nseg);
   return 0;
 }
