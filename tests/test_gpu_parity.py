@@ -95,9 +95,11 @@ def test_config1_full_vs_oracle():
     assert r.ledger == hb.flop_model(p)
 
 
-@pytest.mark.parametrize("dims", [(64, 81, 3000), (108, 121, 6000)], ids=["config2", "config3"])
+@pytest.mark.parametrize("dims", [(64, 81, 3000), (108, 121, 6000), (512, 121, 13000)],
+                         ids=["config2", "config3", "config4"])
 def test_sampled_parity_at_config_sizes(dims, restatement):
-    """Configs 2/3 at full size: principal-submatrix sampling (SURVEY §7 hard part 3):
+    """Configs 2/3/4 at full size (config 4: 26 GB of A, B through the pageable host-buffer
+    path): principal-submatrix sampling (SURVEY §7 hard part 3):
     H[J,J], S[J,J] depend only on columns J of A, B; the oracle runs the J-sliced problem."""
     na, nl, ng = dims
     p = hb.generate_problem(na, nl, ng, 1, 0)
