@@ -768,7 +768,8 @@ static void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool la
   auto final_h = [&](const CtnParams& P) {
     // bands: the one-shot drop-in (download overlaps) and every multi-rank build (the
     // NCCL reduce of band q overlaps the compute of band q+1)
-    if (!(last && (e->band_final_h || e->comm))) {
+    // (only with >= 4 tile waves: smaller final launches would mostly be stream-K tails)
+    if (!(last && (e->band_final_h || e->comm) && P.tiles_total >= 4 * e->sms)) {
       CtnParams q = P;
       launch_tri(e, q, cp.grid_tri);
       return;
