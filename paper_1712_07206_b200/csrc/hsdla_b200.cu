@@ -26,12 +26,15 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -89,6 +92,113 @@ int guarded(F&& f) {
     g_last_error = e.what();
     return HSDLA_B200_CUDA_ERROR;
   }
+}
+
+// ---------------------------------------------------------------------------
+// Host worker pool for the host-side data movement (packing pageable inputs into
+// pinned slabs, unpacking packed triangles, page-cache reads): persistent threads,
+// so a 64 MB slab does not pay ~16 thread creations.  run(n, f) executes f(0..n-1)
+// on the workers and the calling thread and returns when all are done; calls from
+// different host threads are serialised.
+// ---------------------------------------------------------------------------
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool pool;
+    return pool;
+  }
+  unsigned width() const { return static_cast<unsigned>(workers_.size()) + 1; }
+  void run(uint64_t n, const std::function<void(uint64_t)>& f) {
+    if (n == 0) return;
+    if (n == 1 || workers_.empty()) {
+      for (uint64_t i = 0; i < n; ++i) f(i);
+      return;
+    }
+    std::lock_guard<std::mutex> call(call_mu_);
+    Job job;
+    job.f = &f;
+    job.n = n;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      cur_ = &job;
+      job.users = 1;  // the caller
+      ++gen_;
+    }
+    cv_.notify_all();
+    process(job);
+    std::unique_lock<std::mutex> lk(mu_);
+    // the job lives on this stack frame: return only once no worker can touch it
+    done_cv_.wait(lk, [&] { return job.done == job.n && job.users == 0; });
+    cur_ = nullptr;
+  }
+
+ private:
+  struct Job {
+    const std::function<void(uint64_t)>* f = nullptr;
+    uint64_t n = 0, done = 0;
+    std::atomic<uint64_t> next{0};
+    int users = 0;
+  };
+  HostPool() {
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    for (unsigned t = 1; t < hw; ++t) workers_.emplace_back([this] { loop(); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+  // Claim and run items of `job`; the caller of process() is one of job.users.
+  void process(Job& job) {
+    uint64_t d = 0;
+    for (uint64_t i = job.next.fetch_add(1); i < job.n; i = job.next.fetch_add(1)) {
+      (*job.f)(i);
+      ++d;
+    }
+    std::lock_guard<std::mutex> lk(mu_);
+    job.done += d;
+    --job.users;
+    if (job.done == job.n && job.users == 0) done_cv_.notify_all();
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      Job* job;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || (gen_ != seen && cur_ != nullptr); });
+        if (stop_) return;
+        seen = gen_;
+        job = cur_;
+        ++job->users;
+      }
+      process(*job);
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_, call_mu_;
+  std::condition_variable cv_, done_cv_;
+  Job* cur_ = nullptr;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+// fn(i) for i in [0, n), in `parts` contiguous ranges on the host pool when the work
+// is large (>= 4 MB), else inline.
+template <class F>
+static void par_for(uint64_t n, uint64_t bytes, F&& fn) {
+  HostPool& pool = HostPool::get();
+  const uint64_t parts = bytes < (size_t(4) << 20) ? 1 : std::min<uint64_t>(pool.width(), n);
+  if (parts <= 1) {
+    for (uint64_t i = 0; i < n; ++i) fn(i);
+    return;
+  }
+  pool.run(parts, [&](uint64_t t) {
+    for (uint64_t i = n * t / parts; i < n * (t + 1) / parts; ++i) fn(i);
+  });
 }
 
 // ---------------------------------------------------------------------------
@@ -240,7 +350,7 @@ struct hsdla_b200_engine {
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
 
-  std::vector<hsdla_b200::ChunkPlan> whole, streamed;
+  std::vector<hsdla_b200::ChunkPlan> whole, streamed, streamed_pg;  // streamed: pinned / pageable feed
   // per-build timing
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
@@ -442,17 +552,22 @@ static void make_chunk(hsdla_b200_engine* e, uint64_t a0, uint64_t a1, bool firs
 // Streamed chunking for the host-buffer drop-in: whole-atom chunks growing
 // geometrically, so the exposed upload of the first chunk is short and later
 // (larger) uploads still finish before the previous chunk's phases do.  The growth
-// factor follows the compute/upload time ratio of one atom, ~ N_G x 9e-4 on B200
-// (20 K N_G^2 flops at ~34 TF/s vs 32 K N_G bytes at ~50 GB/s pinned PCIe), kept
-// in [1.5, 4]; at most 8 chunks.  Small problems (< 64 MB of A+B): one chunk.
-static std::vector<uint64_t> stream_bounds(uint64_t na, uint64_t nl, uint64_t ng) {
+// factor follows rho, the compute/upload time ratio of one atom:
+//   rho = (20 K N_G^2 / 34 TF/s) / (32 K N_G B / rate) = N_G * rate * 1.84e-14,
+// r = clamp(0.8 rho, 1, 4); the first chunk is the larger of N_A/16 and the head of an
+// 8-term geometric series summing to N_A; at most 8 chunks.  `rate` is the host->device
+// feed: ~50 GB/s for page-locked inputs (PCIe), ~20 GB/s for pageable inputs packed by
+// host threads or for page-cached HSDL files.  Small problems (< 64 MB of A+B): one chunk.
+static std::vector<uint64_t> stream_bounds(uint64_t na, uint64_t nl, uint64_t ng, double rate) {
   std::vector<uint64_t> b{0};
   if (na * nl * ng < (uint64_t(1) << 22) || na < 2) {
     b.push_back(na);
     return b;
   }
-  const double r = std::min(4.0, std::max(1.5, 0.8 * 9e-4 * static_cast<double>(ng)));
-  double size = std::max(1.0, static_cast<double>(na) / 16.0);
+  const double rho = static_cast<double>(ng) * rate * 1.84e-14;
+  const double r = std::min(4.0, std::max(1.0, 0.8 * rho));
+  const double head = r > 1.0001 ? (r - 1.0) / (std::pow(r, 8.0) - 1.0) : 1.0 / 8.0;
+  double size = std::max(1.0, static_cast<double>(na) * std::max(1.0 / 16.0, head));
   while (b.back() < na) {
     const uint64_t left = na - b.back();
     uint64_t take = std::min<uint64_t>(left, static_cast<uint64_t>(std::llround(size)));
@@ -490,9 +605,12 @@ static void make_plans(hsdla_b200_engine* e) {
   make_pieces(e);
   e->whole.resize(1);
   make_chunk(e, 0, e->na, true, e->whole[0]);
-  const auto b = stream_bounds(e->na, e->nl, e->ng);
+  const auto b = stream_bounds(e->na, e->nl, e->ng, 50e9);
   e->streamed.resize(b.size() - 1);
   for (size_t c = 0; c + 1 < b.size(); ++c) make_chunk(e, b[c], b[c + 1], c == 0, e->streamed[c]);
+  const auto bp = stream_bounds(e->na, e->nl, e->ng, 20e9);
+  e->streamed_pg.resize(bp.size() - 1);
+  for (size_t c = 0; c + 1 < bp.size(); ++c) make_chunk(e, bp[c], bp[c + 1], c == 0, e->streamed_pg[c]);
 }
 
 // The second K x N_G temporary: Z next to T_AA A for the fused contraction, the
@@ -552,7 +670,7 @@ static hsdla_b200_engine* engine_create(int device, uint64_t na, uint64_t nl, ui
     dalloc(e.get(), &e->sk_flags, static_cast<uint64_t>(e->sms));
     HS_CUDA(cudaMemset(e->sk_flags, 0, e->sms * sizeof(uint32_t)));
     make_plans(e.get());
-    e->ev_chunk_up.resize(e->streamed.size());
+    e->ev_chunk_up.resize(std::max(e->streamed.size(), e->streamed_pg.size()));
     for (auto& ev : e->ev_chunk_up) HS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   } catch (...) {
     engine_free(e.get());
@@ -604,23 +722,6 @@ static void engine_fill_synthetic(hsdla_b200_engine* e, uint64_t seed) {
   fill(e->Tab, T2, 4, -1.0, 1.0);
   fill(e->Tbb, T2, 5, -1.0, 1.0);
   fill(e->U, e->K, 6, 0.5, 1.5);
-}
-
-// fn(i) for i in [0, n) over up to 16 host threads when the work is large.
-template <class F>
-static void par_for(uint64_t n, uint64_t bytes, F&& fn) {
-  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-  const unsigned nt = bytes < (size_t(4) << 20) ? 1u : static_cast<unsigned>(std::min<uint64_t>(hw, n));
-  if (nt <= 1) {
-    for (uint64_t i = 0; i < n; ++i) fn(i);
-    return;
-  }
-  std::vector<std::thread> th;
-  for (unsigned t = 0; t < nt; ++t)
-    th.emplace_back([&, t] {
-      for (uint64_t i = n * t / nt; i < n * (t + 1) / nt; ++i) fn(i);
-    });
-  for (auto& x : th) x.join();
 }
 
 // Staging ring of two pinned slabs owned by the engine; slab s is free again once
@@ -899,23 +1000,24 @@ static void engine_build_streamed(hsdla_b200_engine* e, const hsdla_b200_problem
   HS_CUDA(cudaEventRecord(e->ev_up0, e->copy_stream));
   const uint64_t ab_bytes = p->n_atoms * p->n_l * p->n_g * sizeof(double2);
   const bool pinned = is_pinned(p->A, ab_bytes) && is_pinned(p->B, ab_bytes);
+  auto& plan = pinned ? e->streamed : e->streamed_pg;
   if (pinned) {
     // page-locked inputs: every chunk's copies are asynchronous, enqueue them all first
-    for (size_t c = 0; c < e->streamed.size(); ++c) {
-      upload_atoms(e, p, a0, e->streamed[c].a0, e->streamed[c].a1, e->copy_stream);
+    for (size_t c = 0; c < plan.size(); ++c) {
+      upload_atoms(e, p, a0, plan[c].a0, plan[c].a1, e->copy_stream);
       HS_CUDA(cudaEventRecord(e->ev_chunk_up[c], e->copy_stream));
     }
   }
-  for (size_t c = 0; c < e->streamed.size(); ++c) {
+  for (size_t c = 0; c < plan.size(); ++c) {
     if (!pinned) {
       // pageable inputs: the host packs chunk c into the pinned slabs while the GPU
       // already computes chunk c-1 (its phases were enqueued in the previous iteration)
-      upload_atoms_staged(e, p, a0, e->streamed[c].a0, e->streamed[c].a1, e->copy_stream);
+      upload_atoms_staged(e, p, a0, plan[c].a0, plan[c].a1, e->copy_stream);
       HS_CUDA(cudaEventRecord(e->ev_chunk_up[c], e->copy_stream));
     }
     HS_CUDA(cudaStreamWaitEvent(e->stream, e->ev_chunk_up[c], 0));
     if (c == 0) HS_CUDA(cudaEventRecord(e->ev_begin, e->stream));
-    enqueue_chunk(e, e->streamed[c], algo, c + 1 == e->streamed.size(), nullptr);
+    enqueue_chunk(e, plan[c], algo, c + 1 == plan.size(), nullptr);
   }
   HS_CUDA(cudaEventRecord(e->ev_up1, e->copy_stream));
   HS_CUDA(cudaEventRecord(e->ev_end, e->stream));
@@ -1004,27 +1106,22 @@ static void engine_sync(hsdla_b200_engine* e, hsdla_b200_stats* st) {
 // packed array) into the lower triangle of an n x n matrix, over up to 16 threads
 // with equal element counts.
 static void unpack_lower(const double2* pk, double2* full, uint64_t n, uint64_t c0, uint64_t c1) {
-  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  HostPool& pool = HostPool::get();
   const uint64_t base = packed_col(n, c0), total = packed_col(n, c1) - base;
-  const unsigned nt = total < (1u << 18) ? 1u : hw;
-  auto work = [&](uint64_t j0, uint64_t j1) {
-    for (uint64_t j = j0; j < j1; ++j) std::memcpy(full + j * n + j, pk + packed_col(n, j), (n - j) * sizeof(double2));
-  };
-  if (nt == 1) {
-    work(c0, c1);
-    return;
-  }
-  std::vector<std::thread> th;
-  uint64_t j = c0;
-  for (unsigned t = 0; t < nt && j < c1; ++t) {
-    const uint64_t target = base + total * (t + 1) / nt;
-    uint64_t j1 = j;
+  const unsigned nt = total < (1u << 18) ? 1u : pool.width();
+  // nt column ranges of equal element count
+  std::vector<uint64_t> cut{c0};
+  for (unsigned t = 1; t < nt; ++t) {
+    const uint64_t target = base + total * t / nt;
+    uint64_t j1 = cut.back();
     while (j1 < c1 && packed_col(n, j1) < target) ++j1;
-    if (t == nt - 1) j1 = c1;
-    th.emplace_back(work, j, j1);
-    j = j1;
+    cut.push_back(j1);
   }
-  for (auto& t : th) t.join();
+  cut.push_back(c1);
+  pool.run(nt, [&](uint64_t t) {
+    for (uint64_t j = cut[t]; j < cut[t + 1]; ++j)
+      std::memcpy(full + j * n + j, pk + packed_col(n, j), (n - j) * sizeof(double2));
+  });
 }
 
 static void ensure_stage(hsdla_b200_engine* e) {
@@ -1293,30 +1390,22 @@ static int open_hsdl(const char* path) {
 // split over up to 8 threads.
 static void pread_pieces(int fd, char* dst, uint64_t off0, uint64_t stride, size_t piece, uint64_t n) {
   const uint64_t bytes = piece * n;
-  const unsigned nt = bytes < (size_t(8) << 20) ? 1u : std::min<unsigned>(8, static_cast<unsigned>(n));
-  std::vector<std::thread> th;
+  const unsigned nt = bytes < (size_t(8) << 20) ? 1u : std::min<unsigned>(HostPool::get().width(), static_cast<unsigned>(n));
   std::vector<Fail> errs(nt);
   std::vector<char> bad(nt, 0);
-  for (unsigned t = 0; t < nt; ++t) {
+  HostPool::get().run(nt, [&](uint64_t t) {
     const uint64_t i0 = n * t / nt, i1 = n * (t + 1) / nt;
-    auto work = [&, t, i0, i1] {
-      try {
-        if (stride == piece) {
-          pread_all(fd, dst + i0 * piece, (i1 - i0) * piece, off0 + i0 * stride);
-        } else {
-          for (uint64_t i = i0; i < i1; ++i) pread_all(fd, dst + i * piece, piece, off0 + i * stride);
-        }
-      } catch (const Fail& f) {
-        errs[t] = f;
-        bad[t] = 1;
+    try {
+      if (stride == piece) {
+        pread_all(fd, dst + i0 * piece, (i1 - i0) * piece, off0 + i0 * stride);
+      } else {
+        for (uint64_t i = i0; i < i1; ++i) pread_all(fd, dst + i * piece, piece, off0 + i * stride);
       }
-    };
-    if (nt == 1)
-      work();
-    else
-      th.emplace_back(work);
-  }
-  for (auto& x : th) x.join();
+    } catch (const Fail& f) {
+      errs[t] = f;
+      bad[t] = 1;
+    }
+  });
   for (unsigned t = 0; t < nt; ++t)
     if (bad[t]) throw errs[t];
 }
@@ -1406,12 +1495,13 @@ static void engine_build_file(hsdla_b200_engine* e, const char* path, uint64_t a
   begin_build(e, algo);
   HS_CUDA(cudaStreamWaitEvent(e->copy_stream, e->ev_end, 0));
   HS_CUDA(cudaEventRecord(e->ev_up0, e->copy_stream));
-  for (size_t c = 0; c < e->streamed.size(); ++c) {
-    load_atoms_from_file(e, f.fd, h, a0, e->streamed[c].a0, e->streamed[c].a1, e->copy_stream);
+  auto& plan = e->streamed_pg;  // page-cache reads feed ~20 GB/s
+  for (size_t c = 0; c < plan.size(); ++c) {
+    load_atoms_from_file(e, f.fd, h, a0, plan[c].a0, plan[c].a1, e->copy_stream);
     HS_CUDA(cudaEventRecord(e->ev_chunk_up[c], e->copy_stream));
     HS_CUDA(cudaStreamWaitEvent(e->stream, e->ev_chunk_up[c], 0));
     if (c == 0) HS_CUDA(cudaEventRecord(e->ev_begin, e->stream));
-    enqueue_chunk(e, e->streamed[c], algo, c + 1 == e->streamed.size(), nullptr);
+    enqueue_chunk(e, plan[c], algo, c + 1 == plan.size(), nullptr);
   }
   HS_CUDA(cudaEventRecord(e->ev_up1, e->copy_stream));
   HS_CUDA(cudaEventRecord(e->ev_end, e->stream));
