@@ -265,8 +265,10 @@ def run_b200(args):
 
     # the kernel layer first: host-buffer (un)registration by the e2e legs below leaves the
     # host's page state noisy for a while, which this pageable-input path is sensitive to
+    # side legs (kernel layer, HSDL file) only where their host copies stay small
+    small = 2 * na * nl * ng * 16 <= (4 << 30)
     klayer = None
-    if P == 1 and not args.no_e2e:
+    if P == 1 and not args.no_e2e and small:
         klayer = run_kernel_layer(hb, p, nl, ng)
 
     # ---- e2e through the public API with host buffers ----
@@ -277,7 +279,7 @@ def run_b200(args):
     lapw = file_leg = None
     if P == 1 and not args.no_e2e:
         lapw = run_lapw(args, hb, p, na, nl, ng)
-        file_leg = run_file(args, hb, p, na, nl, ng)
+        file_leg = run_file(args, hb, p, na, nl, ng) if small else None
 
     peak = hb.fp64_peak(dev, 1.0)
     line = None
