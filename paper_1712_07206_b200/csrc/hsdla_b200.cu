@@ -22,6 +22,7 @@
 #include <cudaTypedefs.h>
 #include <fcntl.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 #include <sys/stat.h>
 #include <unistd.h>
 
@@ -818,9 +819,19 @@ static cudaEvent_t next_event(hsdla_b200_engine* e) {
   return e->ev_pool[e->ev_used++];
 }
 
-// CUDA-event bracket of one phase op on the compute stream.
+// NVTX range names of the phase slots (include/hsdla_b200.h HSDLA_B200_PHASE_*).
+static const char* const kPhaseNames[HSDLA_B200_N_PHASES] = {"s",         "z_loop",    "her2k",       "hemm_loop",
+                                                             "herkx",     "chol_loop", "h_aa_update", "-"};
+
+// CUDA-event bracket of one phase op on the compute stream (plus an NVTX range
+// around its enqueue, for nsys / ncu --nvtx timelines).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 template <class F>
 static void timed_op(hsdla_b200_engine* e, int phase, F&& body) {
+  NvtxRange range(kPhaseNames[phase]);
   cudaEvent_t b = next_event(e), end = next_event(e);
   HS_CUDA(cudaEventRecord(b, e->stream));
   body();

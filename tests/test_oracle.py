@@ -144,3 +144,20 @@ def test_original_restatement_hpd_mixes(restatement):
         assert restatement.rel_frobenius_error_lower(So, Sr) < 1e-11
         delta = 4 * nnh * nl * ng * ng + na * (4 * nl ** 3 // 3) - 4 * n_hpd * nl * nl * ng
         assert lo["total"] - lr["total"] == delta
+
+
+def test_parity_checker_negative_control(restatement):
+    """The reference CLI's --corrupt-h negative control (hsdla_cli.cpp:120,346-347): a single
+    perturbed lower-triangle element must push the relative Frobenius error past the 1e-11
+    bar, and an upper-triangle change must not count (lower triangle authoritative)."""
+    import paper_1712_07206_b200 as hb
+    dims, d = load_case(golden_cases()[-1])
+    H = d["H"].copy()
+    assert hb.rel_frobenius_error_lower(H, d["H"]) == 0.0
+    i, j = H.shape[0] - 1, 0
+    H[i, j] += 1e-9 * np.linalg.norm(np.tril(d["H"]))
+    assert hb.rel_frobenius_error_lower(H, d["H"]) > 1e-11
+    assert restatement.rel_frobenius_error_lower(H, d["H"]) > 1e-11
+    U = d["H"].copy()
+    U[0, U.shape[0] - 1] += 1.0
+    assert hb.rel_frobenius_error_lower(U, d["H"]) == 0.0
