@@ -327,6 +327,12 @@ class Engine:
         buf = None if uid is None else C.create_string_buffer(uid, 128)
         check(_lib.lib().hsdla_b200_engine_set_comm(self.h, buf, C.c_int(nranks), C.c_int(rank)), "set_comm")
 
+    def device_results(self):
+        """Device pointers (ints) of the packed-lower H and S (LAPACK 'L' packed, column-major)."""
+        h, s_ = C.c_void_p(), C.c_void_p()
+        check(_lib.lib().hsdla_b200_engine_device_results(self.h, C.byref(h), C.byref(s_)), "engine_device_results")
+        return h.value, s_.value
+
     def stream(self):
         s = C.c_void_p()
         check(_lib.lib().hsdla_b200_engine_stream(self.h, C.byref(s)), "engine_stream")

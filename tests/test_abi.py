@@ -41,3 +41,14 @@ def test_status_codes_and_last_error():
     assert L.hsdla_b200_engine_create(C.c_int(0), C.c_uint64(0), C.c_uint64(1), C.c_uint64(1), C.byref(h)) == \
         _lib.DIMENSION_ERROR
     assert hb.flop_model(hb.empty_problem(2, 3, 4)).total() > 0
+
+
+def test_library_then_torch_share_one_nccl():
+    """Loading libhsdla_b200.so before torch must not break torch: both resolve the same
+    libnccl.so.2 (the library links torch's bundled NCCL and records it as its RUNPATH)."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, %r); import paper_1712_07206_b200 as hb; hb._lib.lib(); "
+            "import torch, torch.distributed; print('ok', torch.__version__)" % ROOT)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
