@@ -289,3 +289,35 @@ def test_bitwise_determinism_stress():
             e.sync()
             assert torch.equal(th, h0) and torch.equal(ts, s0), algo
     e.close()
+
+
+def test_concurrent_host_threads(restatement):
+    """The drop-in and the kernel layer called from several host threads at once (ctypes
+    releases the GIL): engine-cache, staging-ring and host-pool locking keep every result
+    exact."""
+    import threading
+    from paper_1712_07206_b200 import kernels as K
+    p = hb.generate_problem(6, 25, 400, 3, 1)
+    H0, S0, _ = restatement.build_hs_refined(p)
+    A = p.A
+    C0 = np.zeros((p.n_g, p.n_g), np.complex128, order="F")
+    K.herk(1.0, A, 0.0, C0)
+    errs = []
+
+    def worker(i):
+        try:
+            for _ in range(3):
+                r = hb.build_hs_refined(p)
+                assert rel(r.H, H0) <= TOL and rel(r.S, S0) <= TOL
+                C = np.zeros_like(C0, order="F")
+                K.herk(1.0, A, 0.0, C)
+                assert np.array_equal(C, C0)
+        except Exception as ex:  # noqa: BLE001 - reported below
+            errs.append(f"{i}: {ex!r}")
+
+    th = [threading.Thread(target=worker, args=(i,)) for i in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
