@@ -40,6 +40,14 @@ CONFIGS = {
 }
 
 
+def executed_flops(na, nl, ng, arith):
+    """Real flops the GPU executes for one build (any algorithm): the complex-MAC work
+    20 K N_G^2 + 24 N_A N_L^2 N_G at 8 flops per MAC (4M) or 6 (3M), plus 2 K N_G."""
+    K = na * nl
+    cmac8 = 20 * K * ng * ng + 24 * na * nl * nl * ng
+    return (cmac8 // 8 * 6 if arith == "3m" else cmac8) + 2 * K * ng
+
+
 def ledger_flops(na, nl, ng, variant="refined"):
     # pipeline.cpp:336-364, refined: 20 K N_G^2 + 24 N_A N_L^2 N_G + 2 K N_G.  The original
     # variant (generate_problem(..., n_not_hpd=0): every T_AA factorises) swaps the herkx
@@ -218,7 +226,9 @@ def run_b200(args):
     na_total = na * P
     # this rank's 64-atom shard (independent synthetic atoms per rank)
     p = hb.generate_problem(na, nl, ng, 1 + d.rank, 0)
+    hb.set_default_arith(args.arith)  # kernel layer + any engine created below
     eng = hb.Engine(dev, na, nl, ng)
+    eng.set_arith(args.arith)
     if P > 1 or args.force_comm:
         # N > 1: NCCL reduce of the packed partials; --force-comm exercises the same
         # path on one GPU with a 1-rank communicator (plumbing check)
@@ -262,6 +272,25 @@ def run_b200(args):
     st = eng.sync()
     F = ledger_flops(na_total, nl, ng, "original" if args.algo == "original" else "refined")
     value = F / (ms * 1e-3) / 1e12
+    exec_tf = executed_flops(na_total, nl, ng, args.arith) / (ms * 1e-3) / 1e12
+
+    # the same device-resident build with the plain 4-multiplication arithmetic, for reference
+    ms4 = None
+    if args.arith == "3m":
+        eng.set_arith("4m")
+        for _ in range(2):
+            step()
+        eng.sync()
+        d.barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        ev1.synchronize()
+        eng.sync()
+        d.barrier()
+        ms4 = d.max(ev0.elapsed_time(ev1) / args.steps)
+        eng.set_arith("3m")
 
     # the kernel layer first: host-buffer (un)registration by the e2e legs below leaves the
     # host's page state noisy for a while, which this pageable-input path is sensitive to
@@ -284,13 +313,19 @@ def run_b200(args):
     peak = hb.fp64_peak(dev, 1.0)
     line = None
     if d.rank == 0:
-        h_tf = kt["h_flops"] / (kt["h_ms"] * 1e-3) / 1e12
+        xf = 0.75 if args.arith == "3m" else 1.0  # executed / ledger flops of a contraction
+        h_led = kt["h_flops"] / (kt["h_ms"] * 1e-3) / 1e12
+        h_tf = h_led * xf
         traffic = load_traffic(args.config)
         roofline = {"bound": "tensor", "achieved": h_tf, "peak": peak, "unit": "TFLOP/s", "frac": h_tf / peak,
                     "traffic": traffic,
-                    "kernel": "ctn_contract_kernel<TRI> fused H = [Z;B;A]^H [B;Z;X] (12 K N_G^2 flops/launch)",
-                    "kernel_ms": kt["h_ms"], "flops_per_launch": kt["h_flops"],
-                    "s_kernel_tflops": kt["s_flops"] / (kt["s_ms"] * 1e-3) / 1e12,
+                    "kernel": "ctn_contract_kernel<TRI> fused H = [Z;B;A]^H [B;Z;X]: 12 K N_G^2 ledger flops per "
+                              f"launch, {'9 (3M: 6 real flops per complex MAC)' if xf < 1 else '12'} K N_G^2 "
+                              "executed; achieved = executed flops / mean launch time",
+                    "achieved_ledger": h_led, "arith": args.arith,
+                    "kernel_ms": kt["h_ms"], "flops_per_launch": int(kt["h_flops"] * xf),
+                    "ledger_flops_per_launch": kt["h_flops"],
+                    "s_kernel_tflops": kt["s_flops"] * xf / (kt["s_ms"] * 1e-3) / 1e12,
                     "peak_source": "FP64 DMMA m8n8k4 loop measured in-process after the timed region "
                                    "(MEASURED_PEAKS.json has no FP64 entry)"}
         line = {
@@ -300,15 +335,24 @@ def run_b200(args):
             "data": "synthetic (generate_problem, bit-identical to the reference generator; seed 1+rank)",
             "config": {"workload": f"{args.config}: {desc}" + (f" x {P} GPUs (atoms per GPU fixed)" if P > 1 else ""),
                        "n_atoms": na_total, "n_atoms_per_gpu": na, "n_l": nl, "n_g": ng, "algo": args.algo,
+                       "arith": args.arith + (" (Gauss 3-multiplication complex products: 6 executed real "
+                                              "flops per complex MAC, all FP64; value counts the reference "
+                                              "ledger's 8)" if args.arith == "3m" else " (4 real DMMAs per "
+                                              "complex MAC)"),
                        "parallelism": f"atom-sharded x{P}" + (" + NCCL reduce of packed H,S" if P > 1 else ""),
                        "l2": f"inputs A,B {2 * na * nl * ng * 16 / 1e6:.0f} MB per GPU > 126 MB L2 (no flush)"},
             "build_ms": ms,
-            "fp64_frac_of_peak": value / (P * peak),
+            "fp64_frac_of_peak": exec_tf / (P * peak),
+            "executed_tflops": exec_tf,
+            "ledger_frac_of_peak": value / (P * peak),
             "phase_ms": {k: v * 1e3 for k, v in st["phase_seconds"].items()},
             "roofline": roofline,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
         }
+        if ms4 is not None:
+            line["value_4m"] = F / (ms4 * 1e-3) / 1e12
+            line["ms_per_step_4m"] = ms4
         if e2e is not None:
             line["e2e"] = e2e
         if lapw is not None:
@@ -412,7 +456,7 @@ def run_file(args, hb, p, na, nl, ng):
         path = os.path.join(td, "problem.hsdl")
         hb.save_problem(p, path)
         fbytes = os.path.getsize(path)
-        cfg = hb.PipelineConfig(algo=args.algo if args.algo != "original" else "fused")
+        cfg = hb.PipelineConfig(algo=args.algo if args.algo != "original" else "fused", arith=args.arith)
         hb.build_hs_file(path, cfg, H=H, S=S)  # warm: engine cache + page cache
         steps = max(1, min(args.steps, 5))
         t = time.perf_counter()
@@ -460,12 +504,17 @@ def run_e2e(args, hb, d, p, eng, na_total, nl, ng):
     d2h = 2 * (ng * (ng + 1) // 2) * 16
     try:
         if P == 1:
-            cfg = hb.PipelineConfig(algo=args.algo)
-            hb.build_hs_refined(p, cfg, H=H, S=S)  # warm the engine cache
+            if args.algo == "original":
+                cfg = hb.PipelineConfig(variant="original", arith=args.arith)
+                call = lambda: hb.build_hs_original(p, cfg, H=H, S=S)  # noqa: E731
+            else:
+                cfg = hb.PipelineConfig(algo=args.algo, arith=args.arith)
+                call = lambda: hb.build_hs_refined(p, cfg, H=H, S=S)  # noqa: E731
+            call()  # warm the engine cache
             torch.cuda.synchronize()
             t = time.perf_counter()
             for _ in range(steps):
-                hb.build_hs_refined(p, cfg, H=H, S=S)
+                call()
             dt = (time.perf_counter() - t) / steps
             hb.release_cache()
         else:
@@ -499,6 +548,7 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--algo", default="fused", choices=["fused", "refined", "original"])
+    ap.add_argument("--arith", default="3m", choices=["3m", "4m"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--force-comm", action="store_true", help="NCCL communicator even at N=1 (plumbing check)")
     ap.add_argument("--e2e-steps", type=int, default=10)

@@ -55,6 +55,18 @@ extern "C" {
  * contraction.  Ledger == flop_model(p, Original) with the observed n_hpd. */
 #define HSDLA_B200_ALGO_ORIGINAL 2
 
+/* ---- complex arithmetic of the contractions --------------------------------
+ * 3M (default): Gauss's three-real-multiplication complex product, the ZGEMM3M
+ *   scheme: per k, t1 += a_r b_r, t2 += a_i b_i, t3 += (a_r - a_i)(b_r + b_i), then
+ *   Re = t1 + t2, Im = t3 - t1 + t2.  All FP64; 6 executed real flops per complex MAC
+ *   (the ledger still counts 8), so a build is ~1/4 fewer tensor-core operations.
+ *   Relative error stays at the 1e-15 level (the bar is 1e-11).
+ * 4M: four real DMMAs per complex MAC, plain FP64 rounding per product. */
+#define HSDLA_B200_ARITH_3M 0
+#define HSDLA_B200_ARITH_4M 1
+/* hsdla_b200_options.flags: force the 4M arithmetic for this call. */
+#define HSDLA_B200_FLAG_ARITH_4M 1u
+
 /* Problem (ProblemInstance, problem.hpp:16-27). */
 typedef struct hsdla_b200_problem {
   uint64_t n_atoms, n_l, n_g;
@@ -71,7 +83,7 @@ typedef struct hsdla_b200_options {
   int n_gpus;             /* 0 or 1: one GPU; >1: atoms sharded, NCCL reduce to device_ids[0] */
   const int* device_ids;  /* NULL: devices 0..n_gpus-1 */
   int algo;               /* HSDLA_B200_ALGO_* */
-  int flags;              /* reserved, 0 */
+  int flags;              /* 0 or HSDLA_B200_FLAG_ARITH_4M */
 } hsdla_b200_options;
 
 /* Phase slots = the reference's phase names (test_pipeline.cpp:167-176).  Refined
@@ -96,7 +108,7 @@ typedef struct hsdla_b200_stats {
   double d2h_seconds;        /* packed-triangle download + unpack into H, S */
   double total_seconds;      /* wall time of the call */
   uint64_t ledger[9];
-  uint64_t executed_flops;   /* algorithmic flops of the kernels actually run */
+  uint64_t executed_flops;   /* real flops the GPU executes (3M: 6 per complex MAC; ledger: 8) */
   uint64_t peak_device_bytes;/* device bytes held by the largest shard */
   uint64_t peak_temp_bytes;  /* device temporaries (the X/Z stacks), cf. HSResult::peak_temp_bytes */
   int n_gpus;
@@ -201,6 +213,10 @@ int hsdla_b200_engine_load(hsdla_b200_engine* e, const char* path, uint64_t atom
 /* Device-side synthetic inputs for timing sweeps (A, B, T ~ U(-1,1), U ~ U(0.5,1.5),
  * counter-based hash of `seed`; NOT the reference generator). */
 int hsdla_b200_engine_fill_synthetic(hsdla_b200_engine* e, uint64_t seed);
+/* Complex arithmetic of this engine's contractions (HSDLA_B200_ARITH_*); new engines
+ * and the kernel layer take the process default, set by hsdla_b200_set_default_arith. */
+int hsdla_b200_engine_set_arith(hsdla_b200_engine* e, int arith);
+int hsdla_b200_set_default_arith(int arith);
 /* Enqueue the full build (all phases) on the engine stream; asynchronous. */
 int hsdla_b200_engine_build(hsdla_b200_engine* e, int algo);
 /* Streamed build from HOST memory: uploads shard `atom_begin` of p in atom chunks on

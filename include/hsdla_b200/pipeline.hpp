@@ -32,6 +32,7 @@ struct Options {
   int n_gpus = 1;                             // atoms sharded over n_gpus, NCCL reduce to device_ids[0]
   std::vector<int> device_ids;                // empty: 0..n_gpus-1
   int algo = HSDLA_B200_ALGO_REFINED_FUSED;   // or HSDLA_B200_ALGO_REFINED (reference phase order)
+  int arith = HSDLA_B200_ARITH_3M;            // or HSDLA_B200_ARITH_4M (plain 4-multiplication complex)
 };
 
 inline void throw_status(int rc, const char* what) {
@@ -89,7 +90,8 @@ inline hsdla::pipeline::HSResult run(const hsdla::ProblemInstance& p, int algo, 
                         reinterpret_cast<const double*>(p.A.data()), reinterpret_cast<const double*>(p.B.data()),
                         reinterpret_cast<const double*>(taa.data()), reinterpret_cast<const double*>(tab.data()),
                         reinterpret_cast<const double*>(tbb.data()), u.data()};
-  hsdla_b200_options co{opt.n_gpus, opt.device_ids.empty() ? nullptr : opt.device_ids.data(), algo, 0};
+  hsdla_b200_options co{opt.n_gpus, opt.device_ids.empty() ? nullptr : opt.device_ids.data(), algo,
+                        opt.arith == HSDLA_B200_ARITH_4M ? static_cast<int>(HSDLA_B200_FLAG_ARITH_4M) : 0};
   hsdla::pipeline::HSResult r;
   r.H = hsdla::HermitianView(ng);  // zero-initialised: the upper triangle stays exactly 0
   r.S = hsdla::HermitianView(ng);
@@ -127,7 +129,8 @@ inline hsdla::pipeline::HSResult build_hs_file(const std::string& path, const hs
   const int algo = cfg.variant == hsdla::pipeline::Variant::Original ? HSDLA_B200_ALGO_ORIGINAL : opt.algo;
   uint64_t na = 0, nl = 0, ng = 0;
   throw_status(hsdla_b200_problem_file_info(path.c_str(), &na, &nl, &ng, nullptr), "hsdla_b200_problem_file_info");
-  hsdla_b200_options co{opt.n_gpus, opt.device_ids.empty() ? nullptr : opt.device_ids.data(), algo, 0};
+  hsdla_b200_options co{opt.n_gpus, opt.device_ids.empty() ? nullptr : opt.device_ids.data(), algo,
+                        opt.arith == HSDLA_B200_ARITH_4M ? static_cast<int>(HSDLA_B200_FLAG_ARITH_4M) : 0};
   hsdla::pipeline::HSResult r;
   r.H = hsdla::HermitianView(ng);
   r.S = hsdla::HermitianView(ng);

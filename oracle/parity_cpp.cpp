@@ -37,13 +37,15 @@ int main(int argc, char** argv) {
     std::printf("%-44s %s (%.3e)\n", what, ok ? "PASS" : "FAIL", v);
     if (!ok) ++fails;
   };
-  for (int algo : {HSDLA_B200_ALGO_REFINED_FUSED, HSDLA_B200_ALGO_REFINED}) {
+  for (int algo : {HSDLA_B200_ALGO_REFINED_FUSED, HSDLA_B200_ALGO_REFINED, HSDLA_B200_ALGO_REFINED_FUSED + 100}) {
     hsdla_b200::Options opt;
+    opt.arith = algo >= 100 ? HSDLA_B200_ARITH_4M : HSDLA_B200_ARITH_3M;  // +100: the fused algorithm in 4M
+    algo %= 100;
     opt.algo = algo;
     const hsdla::pipeline::HSResult gpu = hsdla_b200::build_hs_refined(p, cfg, opt);
     const double eh = hsdla::rel_frobenius_error_lower(gpu.H.matrix(), cpu.H.matrix());
     const double es = hsdla::rel_frobenius_error_lower(gpu.S.matrix(), cpu.S.matrix());
-    std::printf("algo %d\n", algo);
+    std::printf("algo %d arith %s\n", algo, opt.arith == HSDLA_B200_ARITH_4M ? "4M" : "3M");
     check(eh <= 1e-11, "  H rel Frobenius (lower) <= 1e-11", eh);
     check(es <= 1e-11, "  S rel Frobenius (lower) <= 1e-11", es);
     check(gpu.ledger == hsdla::pipeline::flop_model(p, hsdla::pipeline::Variant::Refined),

@@ -11,6 +11,8 @@ LIB_PATH = os.path.join(HERE, "libhsdla_b200.so")
 
 OK, DIMENSION_ERROR, SIZING_ERROR, CONFIG_ERROR, IO_ERROR, CUDA_ERROR, NCCL_ERROR = range(7)
 ALGO_REFINED_FUSED, ALGO_REFINED, ALGO_ORIGINAL = 0, 1, 2
+ARITH = {"3m": 0, "4m": 1}  # HSDLA_B200_ARITH_*: Gauss 3-multiplication / plain 4-multiplication complex
+FLAG_ARITH_4M = 1
 LEDGER_KEYS = ("gemm", "hemm", "her2k", "herk", "scaling", "herkx", "potrf", "trmm")
 N_PHASES = 8
 # phase slot names (include/hsdla_b200.h HSDLA_B200_PHASE_*)
@@ -32,7 +34,7 @@ EXPORTS = (
     "hsdla_b200_engine_setup_time", "hsdla_b200_problem_file_info", "hsdla_b200_build_hs_file",
     "hsdla_b200_engine_load", "hsdla_b200_engine_fill_synthetic",
     "hsdla_b200_herk", "hsdla_b200_her2k", "hsdla_b200_herkx", "hsdla_b200_gemm", "hsdla_b200_hemm",
-    "hsdla_b200_trmm", "hsdla_b200_diag_scale",
+    "hsdla_b200_trmm", "hsdla_b200_diag_scale", "hsdla_b200_engine_set_arith", "hsdla_b200_set_default_arith",
 )
 
 

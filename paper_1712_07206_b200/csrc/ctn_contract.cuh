@@ -17,14 +17,14 @@
 //   * one elected producer lane streams 128-byte k-slabs of both operands with
 //     TMA (cp.async.bulk.tensor, SWIZZLE_128B) into a STAGES-deep smem ring,
 //     completion tracked by mbarrier transaction counts;
-//   * 4 consumer warps each own a 32x32 complex output tile and run
-//     mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).  Interleaved complex storage maps
-//     straight onto real DMMA: for the 4 complex k of one quad, lane q loads the
-//     whole complex number (re, im) with one LDS.128, and the k permutation
-//     "step 0 = real parts, step 1 = imaginary parts" gives
-//        Re += a_re b_re + a_im b_im,   Im += a_re b_im + a_im (-b_re)
-//     i.e. exactly 8 real flops per complex MAC (the ledger convention,
-//     flop_ledger.hpp) and no 3M trick (rounding stays plain).
+//   * 8 consumer warps (two warpgroups) each own a 32x16 complex output tile and
+//     run mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4); the producer has a warpgroup of its
+//     own so setmaxnreg can hand its registers to the consumers (232 each).
+//     Interleaved complex storage maps straight onto real DMMA: for the 4 complex k
+//     of one quad, lane q loads the whole complex number (re, im) with one LDS.128.
+//     4M (G3M = 0): Re += a_re b_re + a_im b_im, Im += a_re b_im + a_im (-b_re):
+//     8 real flops per complex MAC, the ledger convention (flop_ledger.hpp).
+//     3M (G3M = 1, default): Gauss's product, 3 real DMMAs (6 flops) per complex MAC.
 //   * smem rows for mma row g are permuted (perm(g) = (g&1)<<2 | g>>1) so the
 //     LDS.128 quarter-warps of the swizzled tile are bank-conflict free.
 #pragma once
@@ -172,7 +172,14 @@ __device__ __forceinline__ uint64_t packed_index(uint64_t n, uint64_t i, uint64_
 template <int MODE, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES>
 struct CtnCfg {
   static constexpr int kConsumerWarps = WARPS_M * WARPS_N;
-  static constexpr int kThreads = (kConsumerWarps + 1) * 32;
+  // warp specialisation with register rebalancing: the consumer warps form whole
+  // warpgroups and the producer gets a warpgroup of its own (one TMA lane, three idle
+  // warps), so setmaxnreg can move registers from the producer to the consumers
+  static constexpr int kProducerWarps = 4;
+  static constexpr int kThreads = (kConsumerWarps + kProducerWarps) * 32;
+  static constexpr int kProducerRegs = 40;
+  static constexpr int kConsumerRegs =
+      ((65536 / kThreads / 8 * 8) * kThreads - kProducerRegs * kProducerWarps * 32) / (kConsumerWarps * 32) / 8 * 8;
   static constexpr int kWM = BM / WARPS_M;
   static constexpr int kWN = BN / WARPS_N;
   static constexpr int kMB = kWM / 8;
@@ -245,13 +252,19 @@ __device__ __forceinline__ void consumer_bar(int nthreads) {
   asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
 
-template <int MODE, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, int MINB = 1>
+// G3M = 0: four real DMMAs per complex MAC (8 flops, plain FP64 rounding).
+// G3M = 1: Gauss's three-multiplication complex product (the ZGEMM3M scheme, 6 executed
+//   flops per complex MAC): per k, t1 += a_r b_r, t2 += a_i b_i, t3 += (a_r - a_i)(b_r + b_i),
+//   then Re(conj(a) b) = t1 + t2 and Im = t3 - t1 + t2.  Still all-FP64; the imaginary
+//   part's rounding error bound grows by a small constant factor.
+template <int MODE, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, int MINB = 1, int G3M = 0>
 __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>::kThreads, MINB)
     ctn_contract_kernel(const __grid_constant__ CtnParams P) {
   using Cfg = CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>;
   constexpr int MB = Cfg::kMB, NB = Cfg::kNB;
   constexpr int NCT = Cfg::kConsumerWarps * 32;  // consumer threads
-  constexpr int NACC = MB * NB * 4;              // accumulator doubles per consumer thread
+  constexpr int NS = G3M ? 3 : 2;                // accumulator sets per output element
+  constexpr int NACC = MB * NB * 2 * NS;         // accumulator doubles per consumer thread
   static_assert(BM % (8 * WARPS_M) == 0 && BN % (8 * WARPS_N) == 0, "tile shape");
 
   extern __shared__ uint8_t smem_raw[];
@@ -294,9 +307,11 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>
     }
   };
 
-  if (warp == Cfg::kConsumerWarps) {
+  static_assert(Cfg::kConsumerWarps % 4 == 0, "consumer warps must form whole warpgroups");
+  if (warp >= Cfg::kConsumerWarps) {
     // ===================== TMA producer (one lane) =========================
-    if (lane == 0) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(Cfg::kProducerRegs) : "memory");
+    if (warp == Cfg::kConsumerWarps && lane == 0) {
       for (int s = 0; s < P.nseg; ++s) {
         prefetch_map(&P.L[s]);
         prefetch_map(&P.R[s]);
@@ -339,6 +354,7 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>
   }
 
   // ======================= DMMA consumers =================================
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(Cfg::kConsumerRegs) : "memory");
   const int ctid = threadIdx.x;  // 0 .. NCT-1
   const int wm = warp % WARPS_M;
   const int wn = warp / WARPS_M;
@@ -360,19 +376,22 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>
   if (MODE != kTri) pc = Piece{0, 0, iters, 0};
   int it = 0;
   while (have) {
-    double acc[MB][NB][2][2];  // [mb][nb][e][re/im]
+    double acc[MB][NB][2][NS];  // [mb][nb][e][re, im] or [t1, t2, t3]
 #pragma unroll
     for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
       for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) acc[mb][nb][e][0] = acc[mb][nb][e][1] = 0.0;
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+          for (int r = 0; r < NS; ++r) acc[mb][nb][e][r] = 0.0;
 
     // Software-pipelined main loop: the fragments of step s+1 (next kk, or the next
     // stage's first kk) are loaded before the 32 DMMAs of step s issue, so LDS latency
     // and the stage-full wait hide behind the tensor pipe.
     struct Frag {
       double2 a[MB], b[NB];
+      double sa[G3M ? MB : 1], sb[G3M ? NB : 1];  // 3M: a_r - a_i, b_r + b_i
     };
     auto load_frag = [&](Frag& f, const uint8_t* st, int kk) {
       const uint32_t base = smem_u32(st) + offK[kk];
@@ -381,7 +400,34 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>
 #pragma unroll
       for (int nb = 0; nb < NB; ++nb) f.b[nb] = lds128(base + offR[nb]);
     };
+    // 3M operand sums, formed one step ahead of their use (off the DMMA issue path)
+    auto sum_frag = [&](Frag& f) {
+      if (G3M) {
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) f.sa[mb] = f.a[mb].x - f.a[mb].y;
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) f.sb[nb] = f.b[nb].x + f.b[nb].y;
+      }
+    };
     auto mma_frag = [&](const Frag& f) {
+      if (G3M) {
+        // three independent sweeps (t3, t1, t2) so consecutive DMMAs never share an
+        // accumulator; the operand sums were formed one step ahead (sum_frag)
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb)
+            dmma(acc[mb][nb][0][NS - 1], acc[mb][nb][1][NS - 1], f.sa[mb], f.sb[nb]);
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb) dmma(acc[mb][nb][0][0], acc[mb][nb][1][0], f.a[mb].x, f.b[nb].x);
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb) dmma(acc[mb][nb][0][1], acc[mb][nb][1][1], f.a[mb].y, f.b[nb].y);
+        return;
+      }
       // Four independent sweeps so consecutive DMMAs never share an accumulator.
 #pragma unroll
       for (int mb = 0; mb < MB; ++mb)
@@ -406,18 +452,21 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>
         const int slot = it % STAGES;
         mbar_wait(&full[slot], (it / STAGES) & 1);
         load_frag(f0, smem + slot * Cfg::kStageBytes, 0);
+        sum_frag(f0);
       }
       for (int c = pc.k0; c < pc.k1; ++c, ++it) {
         const int slot = it % STAGES;
         const uint8_t* st = smem + slot * Cfg::kStageBytes;
         load_frag(f1, st, 1);
         mma_frag(f0);
+        sum_frag(f1);
         if (c + 1 < pc.k1) {
           const int nslot = (it + 1) % STAGES;
           mbar_wait(&full[nslot], ((it + 1) / STAGES) & 1);
           load_frag(f0, smem + nslot * Cfg::kStageBytes, 0);
         }
         mma_frag(f1);
+        if (c + 1 < pc.k1) sum_frag(f0);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
       }
@@ -433,7 +482,8 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>
 #pragma unroll
           for (int e = 0; e < 2; ++e)
 #pragma unroll
-            for (int r = 0; r < 2; ++r) __stcg(ws + ((((mb * NB + nb) * 2 + e) * 2 + r) * NCT + ctid), acc[mb][nb][e][r]);
+            for (int r = 0; r < NS; ++r)
+              __stcg(ws + ((((mb * NB + nb) * 2 + e) * NS + r) * NCT + ctid), acc[mb][nb][e][r]);
       __threadfence();
       consumer_bar(NCT);
       if (ctid == 0) st_release_u32(P.sk_flags + blockIdx.x, P.epoch);
@@ -454,8 +504,8 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>
 #pragma unroll
               for (int e = 0; e < 2; ++e)
 #pragma unroll
-                for (int r = 0; r < 2; ++r)
-                  acc[mb][nb][e][r] += __ldcg(ws + ((((mb * NB + nb) * 2 + e) * 2 + r) * NCT + ctid));
+                for (int r = 0; r < NS; ++r)
+                  acc[mb][nb][e][r] += __ldcg(ws + ((((mb * NB + nb) * 2 + e) * NS + r) * NCT + ctid));
         }
       }
       // ---- epilogue ---------------------------------------------------------
@@ -494,7 +544,8 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>
             double2* d = dst_of(mb, nb, e);
             if (!d) continue;
             const int j = col0 + wn * Cfg::kWN + 8 * nb + (e ? 4 + q : q);
-            const double xr = acc[mb][nb][e][0], xi = acc[mb][nb][e][1];
+            const double xr = G3M ? acc[mb][nb][e][0] + acc[mb][nb][e][1] : acc[mb][nb][e][0];
+            const double xi = G3M ? acc[mb][nb][e][NS - 1] - acc[mb][nb][e][0] + acc[mb][nb][e][1] : acc[mb][nb][e][1];
             double vr = ar * xr - ai * xi;
             double vi = ar * xi + ai * xr;
             if (MODE == kTri && i == j && !keep_di) vi = 0.0;

@@ -300,8 +300,23 @@ using TriCfg = CtnCfg<kTri, kTriBM, kTriBM, 2, 4, kTriStages>;
 constexpr int kBatBM = 32, kBatBN = 128, kBatStages = 4;
 using BatCfg = CtnCfg<kBatch, kBatBM, kBatBN, 1, 8, kBatStages>;
 
-static auto tri_kernel = ctn_contract_kernel<kTri, kTriBM, kTriBM, 2, 4, kTriStages>;
-static auto bat_kernel = ctn_contract_kernel<kBatch, kBatBM, kBatBN, 1, 8, kBatStages>;
+// [arith]: HSDLA_B200_ARITH_3M (Gauss, 3 real DMMAs per complex MAC) / _4M (4 DMMAs)
+static decltype(&ctn_contract_kernel<kTri, kTriBM, kTriBM, 2, 4, kTriStages>) const tri_kernels[2] = {
+    ctn_contract_kernel<kTri, kTriBM, kTriBM, 2, 4, kTriStages, 1, 1>,
+    ctn_contract_kernel<kTri, kTriBM, kTriBM, 2, 4, kTriStages, 1, 0>};
+static decltype(&ctn_contract_kernel<kBatch, kBatBM, kBatBN, 1, 8, kBatStages>) const bat_kernels[2] = {
+    ctn_contract_kernel<kBatch, kBatBM, kBatBN, 1, 8, kBatStages, 1, 1>,
+    ctn_contract_kernel<kBatch, kBatBM, kBatBN, 1, 8, kBatStages, 1, 0>};
+// stream-K partial-accumulator slot per CTA: 64 x 64 outputs x 3 sets (3M) doubles
+constexpr uint64_t kSkSlot = uint64_t(kTriBM) * kTriBM * 3;
+static std::atomic<int> g_default_arith{HSDLA_B200_ARITH_3M};  // hsdla_b200_set_default_arith
+
+static void set_kernel_attributes() {
+  for (int a = 0; a < 2; ++a) {
+    HS_CUDA(cudaFuncSetAttribute(tri_kernels[a], cudaFuncAttributeMaxDynamicSharedMemorySize, TriCfg::kSmemBytes));
+    HS_CUDA(cudaFuncSetAttribute(bat_kernels[a], cudaFuncAttributeMaxDynamicSharedMemorySize, BatCfg::kSmemBytes));
+  }
+}
 
 static int chunks_of(uint64_t kcomplex) { return static_cast<int>((kcomplex + kChunkC - 1) / kChunkC); }
 
@@ -367,6 +382,7 @@ struct hsdla_b200_engine {
   bool banded = false;                     // ... and the last build did
   std::vector<cudaEvent_t> ev_chunk_up;
   int last_algo = 0, launches = 0;
+  int arith = HSDLA_B200_ARITH_3M;  // complex product scheme of the contractions
   uint64_t n_hpd_last = 0;
   bool built = false, reduced = false, uploaded_streamed = false;
   cudaEvent_t ev_setup0 = nullptr, ev_setup1 = nullptr;  // last LAPW setup (tables + stream kernels)
@@ -636,8 +652,8 @@ static hsdla_b200_engine* engine_create(int device, uint64_t na, uint64_t nl, ui
   try {
     HS_CUDA(cudaSetDevice(device));
     // Attributes are per-device for the current context: set them on every device.
-    HS_CUDA(cudaFuncSetAttribute(tri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TriCfg::kSmemBytes));
-    HS_CUDA(cudaFuncSetAttribute(bat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BatCfg::kSmemBytes));
+    set_kernel_attributes();
+    e->arith = g_default_arith.load();
     HS_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
     HS_CUDA(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
     HS_CUDA(cudaStreamCreateWithFlags(&e->comm_stream, cudaStreamNonBlocking));
@@ -667,7 +683,7 @@ static hsdla_b200_engine* engine_create(int device, uint64_t na, uint64_t nl, ui
     dalloc(e.get(), &e->Hp, e->npk);
     dalloc(e.get(), &e->Sp, e->npk);
     HS_CUDA(cudaDeviceGetAttribute(&e->sms, cudaDevAttrMultiProcessorCount, device));
-    dalloc(e.get(), &e->sk_ws, static_cast<uint64_t>(e->sms) * kTriBM * kTriBM * 2);
+    dalloc(e.get(), &e->sk_ws, static_cast<uint64_t>(e->sms) * kSkSlot);
     dalloc(e.get(), &e->sk_flags, static_cast<uint64_t>(e->sms));
     HS_CUDA(cudaMemset(e->sk_flags, 0, e->sms * sizeof(uint32_t)));
     make_plans(e.get());
@@ -841,12 +857,12 @@ static void timed_op(hsdla_b200_engine* e, int phase, F&& body) {
 
 static void launch_tri(hsdla_b200_engine* e, CtnParams& P, const dim3& grid) {
   P.epoch = ++e->epoch;  // fresh stream-K flag generation per launch
-  tri_kernel<<<grid, TriCfg::kThreads, TriCfg::kSmemBytes, e->stream>>>(P);
+  tri_kernels[e->arith]<<<grid, TriCfg::kThreads, TriCfg::kSmemBytes, e->stream>>>(P);
   HS_CUDA(cudaGetLastError());
   ++e->launches;
 }
 static void launch_bat(hsdla_b200_engine* e, const CtnParams& P, const dim3& grid) {
-  bat_kernel<<<grid, BatCfg::kThreads, BatCfg::kSmemBytes, e->stream>>>(P);
+  bat_kernels[e->arith]<<<grid, BatCfg::kThreads, BatCfg::kSmemBytes, e->stream>>>(P);
   HS_CUDA(cudaGetLastError());
   ++e->launches;
 }
@@ -1083,6 +1099,8 @@ static void engine_reduce(hsdla_b200_engine* e, int root) {
   reduce_finish(e);
 }
 
+static uint64_t executed_flops(uint64_t na, uint64_t nl, uint64_t ng, int arith);
+
 static void engine_sync(hsdla_b200_engine* e, hsdla_b200_stats* st) {
   HS_CUDA(cudaSetDevice(e->device));
   HS_CUDA(cudaStreamSynchronize(e->stream));
@@ -1104,6 +1122,7 @@ static void engine_sync(hsdla_b200_engine* e, hsdla_b200_stats* st) {
     e->n_hpd_last = e->na;
   }
   st->n_hpd = e->n_hpd_last;
+  st->executed_flops = executed_flops(e->na, e->nl, e->ng, e->arith);
   for (const OpTime& op : e->ops) st->phase_seconds[op.phase] += ev_ms(op.b, op.e) * 1e-3;
   const cudaEvent_t last = e->reduced ? e->ev_reduce_end : e->ev_end;
   st->device_seconds = ev_ms(e->ev_begin, last) * 1e-3;
@@ -1594,6 +1613,16 @@ static void flop_model(int variant, uint64_t na, uint64_t nl, uint64_t ng, uint6
   for (int i = 0; i < 8; ++i) l[8] += l[i];
 }
 
+// Real flops the GPU executes for a build.  Every algorithm runs the same
+// lower-triangular contractions, 20 K N_G^2 + 24 N_A N_L^2 N_G complex-MAC flops at 8
+// per MAC (the original's trmm on the zero upper half of L and its full gemm fold are
+// executed as the lower-only h_aa contraction), plus 2 K N_G for diag_scale; the 3M
+// arithmetic executes 6 real flops per complex MAC.
+static uint64_t executed_flops(uint64_t na, uint64_t nl, uint64_t ng, int arith) {
+  const uint64_t K = na * nl, cmac8 = 20 * K * ng * ng + 24 * na * nl * nl * ng;
+  return (arith == HSDLA_B200_ARITH_3M ? cmac8 / 8 * 6 : cmac8) + 2 * K * ng;
+}
+
 // The one-shot drop-in around a per-engine "start" (upload/load + enqueue build,
 // returning host seconds spent loading): device selection, engine cache, NCCL
 // reduce to the root, overlapped download, stats.
@@ -1602,6 +1631,8 @@ static void one_shot(const hsdla_b200_options* o, uint64_t na, uint64_t nl, uint
                      hsdla_b200_stats* st, std::chrono::steady_clock::time_point t0, Start&& start) {
   const int algo = o ? o->algo : HSDLA_B200_ALGO_REFINED_FUSED;
   if (!valid_algo(algo)) throw Fail{HSDLA_B200_CONFIG_ERROR, "unknown algo " + std::to_string(algo)};
+  if (o && (o->flags & ~HSDLA_B200_FLAG_ARITH_4M)) throw Fail{HSDLA_B200_CONFIG_ERROR, "unknown option flags"};
+  const int arith = o && (o->flags & HSDLA_B200_FLAG_ARITH_4M) ? HSDLA_B200_ARITH_4M : HSDLA_B200_ARITH_3M;
   const int P = o && o->n_gpus > 1 ? o->n_gpus : 1;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
@@ -1622,6 +1653,7 @@ static void one_shot(const hsdla_b200_options* o, uint64_t na, uint64_t nl, uint
   auto run = [&](int r) {
     hsdla_b200_engine* e = set->engines[r];
     e->band_final_h = true;
+    e->arith = arith;
     try {
       load[r] = start(e, set->atom0[r], algo);
     } catch (const Fail& f) {
@@ -1685,12 +1717,7 @@ static void one_shot(const hsdla_b200_options* o, uint64_t na, uint64_t nl, uint
     st->d2h_seconds = d2h;
     // ledger == pipeline::flop_model(p, variant) with the potrf outcome of this build
     flop_model(algo == HSDLA_B200_ALGO_ORIGINAL ? 0 : 1, na, nl, ng, n_hpd, st->ledger);
-    // every algorithm runs the same lower-triangular contractions: 20 K N_G^2 +
-    // 24 N_A N_L^2 N_G + 2 K N_G (the original's trmm on the zero upper half of L
-    // and its full gemm fold are executed as the lower-only h_aa contraction)
-    uint64_t refined[9];
-    flop_model(1, na, nl, ng, na, refined);
-    st->executed_flops = refined[8];
+    st->executed_flops = executed_flops(na, nl, ng, arith);
     st->n_hpd = n_hpd;
     st->peak_device_bytes = local.peak_device_bytes;
     st->peak_temp_bytes = local.peak_temp_bytes;
@@ -1796,6 +1823,7 @@ static Ring& ring_for(int device) {
 
 struct Ctx {
   int sms = 148;
+  int arith = HSDLA_B200_ARITH_3M;
   cudaStream_t s = nullptr;
   Ring* ring = nullptr;
   std::unique_lock<std::mutex> lock;
@@ -1807,8 +1835,8 @@ struct Ctx {
     }
     HS_CUDA(cudaSetDevice(device));
     HS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-    HS_CUDA(cudaFuncSetAttribute(tri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TriCfg::kSmemBytes));
-    HS_CUDA(cudaFuncSetAttribute(bat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BatCfg::kSmemBytes));
+    set_kernel_attributes();
+    arith = g_default_arith.load();
     HS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     ring = &ring_for(device);
     lock = std::unique_lock<std::mutex>(ring->mu);
@@ -1931,7 +1959,7 @@ static void tri(Ctx& x, int nseg, const double2* const* L, const double2* const*
   P.tiles_total = tiles * (tiles + 1) / 2;
   P.band = tri_band();
   P.out = Cp;
-  DevBuf ws(static_cast<size_t>(x.sms) * kTriBM * kTriBM * 2 * sizeof(double)), flags(x.sms * sizeof(uint32_t));
+  DevBuf ws(static_cast<size_t>(x.sms) * kSkSlot * sizeof(double)), flags(x.sms * sizeof(uint32_t));
   HS_CUDA(cudaMemsetAsync(flags.p, 0, x.sms * sizeof(uint32_t), x.s));
   P.sk_ws = static_cast<double*>(ws.p);
   P.sk_flags = static_cast<uint32_t*>(flags.p);
@@ -1941,7 +1969,7 @@ static void tri(Ctx& x, int nseg, const double2* const* L, const double2* const*
   P.beta = beta;
   const uint64_t work = static_cast<uint64_t>(P.tiles_total) * chunks_of(k) * nseg;
   const dim3 g(static_cast<unsigned>(std::min<uint64_t>(x.sms, work)));
-  tri_kernel<<<g, TriCfg::kThreads, TriCfg::kSmemBytes, x.s>>>(P);
+  tri_kernels[x.arith]<<<g, TriCfg::kThreads, TriCfg::kSmemBytes, x.s>>>(P);
   HS_CUDA(cudaGetLastError());
   x.sync();  // ws / flags go out of scope
 }
@@ -1965,7 +1993,7 @@ static void rect(Ctx& x, const double2* L, const double2* R, uint64_t m, uint64_
   P.beta = beta;
   const dim3 g(static_cast<unsigned>((n + kBatBN - 1) / kBatBN), static_cast<unsigned>((m + kBatBM - 1) / kBatBM), 1);
   if (g.y > 65535) throw Fail{HSDLA_B200_SIZING_ERROR, "rows exceed the batched-contraction grid"};
-  bat_kernel<<<g, BatCfg::kThreads, BatCfg::kSmemBytes, x.s>>>(P);
+  bat_kernels[x.arith]<<<g, BatCfg::kThreads, BatCfg::kSmemBytes, x.s>>>(P);
   HS_CUDA(cudaGetLastError());
 }
 
@@ -2134,6 +2162,21 @@ int hsdla_b200_engine_fill_synthetic(hsdla_b200_engine* e, uint64_t seed) {
   return guarded([&] {
     if (!e) throw Fail{HSDLA_B200_CONFIG_ERROR, "null engine"};
     engine_fill_synthetic(e, seed);
+  });
+}
+int hsdla_b200_engine_set_arith(hsdla_b200_engine* e, int arith) {
+  return guarded([&] {
+    if (!e) throw Fail{HSDLA_B200_CONFIG_ERROR, "null engine"};
+    if (arith != HSDLA_B200_ARITH_3M && arith != HSDLA_B200_ARITH_4M)
+      throw Fail{HSDLA_B200_CONFIG_ERROR, "arith must be HSDLA_B200_ARITH_3M or _4M"};
+    e->arith = arith;
+  });
+}
+int hsdla_b200_set_default_arith(int arith) {
+  return guarded([&] {
+    if (arith != HSDLA_B200_ARITH_3M && arith != HSDLA_B200_ARITH_4M)
+      throw Fail{HSDLA_B200_CONFIG_ERROR, "arith must be HSDLA_B200_ARITH_3M or _4M"};
+    g_default_arith.store(arith);
   });
 }
 int hsdla_b200_engine_build(hsdla_b200_engine* e, int algo) {

@@ -44,6 +44,9 @@ class PipelineConfig:
     device_ids: Optional[Sequence[int]] = None
     # refined variant only: "fused" (her2k+herkx in one contraction) | "refined" (reference phase order)
     algo: str = "fused"
+    # complex arithmetic of the contractions: "3m" (Gauss, 6 executed flops per complex MAC,
+    # the default) | "4m" (four real multiplications, plain FP64 rounding per product)
+    arith: str = "3m"
 
 
 @dataclass
@@ -100,7 +103,10 @@ def _options(cfg, algo):
         ids = (C.c_int * len(cfg.device_ids))(*cfg.device_ids)
     if cfg.n_gpus < 1:
         raise ConfigError("n_gpus must be >= 1")
-    return _lib.Options(int(cfg.n_gpus), ids, ALGOS[algo], 0), ids
+    if cfg.arith not in _lib.ARITH:
+        raise ConfigError(f"unknown arith: {cfg.arith} (3m | 4m)")
+    flags = _lib.FLAG_ARITH_4M if cfg.arith == "4m" else 0
+    return _lib.Options(int(cfg.n_gpus), ids, ALGOS[algo], flags), ids
 
 
 def _phase_names(algo):
@@ -290,6 +296,12 @@ class Engine:
         """Device-side synthetic inputs (timing sweeps only; not the reference generator)."""
         check(_lib.lib().hsdla_b200_engine_fill_synthetic(self.h, C.c_uint64(seed)), "engine_fill_synthetic")
 
+    def set_arith(self, arith):
+        """Complex arithmetic of this engine's contractions: "3m" (default) or "4m"."""
+        if arith not in _lib.ARITH:
+            raise ConfigError(f"unknown arith: {arith} (3m | 4m)")
+        check(_lib.lib().hsdla_b200_engine_set_arith(self.h, C.c_int(_lib.ARITH[arith])), "engine_set_arith")
+
     def load(self, path, atom_begin=0):
         """Stream this shard of an HSDL v1 file into the engine (hsdla_b200_engine_load)."""
         check(_lib.lib().hsdla_b200_engine_load(self.h, os.fsencode(path), C.c_uint64(atom_begin)), "engine_load")
@@ -348,6 +360,13 @@ class Engine:
               "kernel_times")
         return {"s_ms": ms_s.value, "h_ms": ms_h.value, "s_flops": fs.value, "h_flops": fh.value,
                 "builds": nb.value}
+
+
+def set_default_arith(arith):
+    """Process default complex arithmetic for new engines and the kernel layer ("3m" | "4m")."""
+    if arith not in _lib.ARITH:
+        raise ConfigError(f"unknown arith: {arith} (3m | 4m)")
+    check(_lib.lib().hsdla_b200_set_default_arith(C.c_int(_lib.ARITH[arith])), "set_default_arith")
 
 
 def fp64_peak(device=0, seconds=0.5):

@@ -26,12 +26,12 @@ def _need_gpu():
     hb.release_cache()
 
 
-@pytest.mark.parametrize("algo", ["fused", "refined"])
+@pytest.mark.parametrize("algo,arith", [("fused", "3m"), ("refined", "3m"), ("fused", "4m"), ("refined", "4m")])
 @pytest.mark.parametrize("path", golden_cases(), ids=lambda p: p.split("/")[-1][:-4])
-def test_golden_parity(path, algo):
+def test_golden_parity(path, algo, arith):
     dims, d = load_case(path)
     p = as_problem(d, dims)
-    r = hb.build_hs_refined(p, hb.PipelineConfig(algo=algo))
+    r = hb.build_hs_refined(p, hb.PipelineConfig(algo=algo, arith=arith))
     assert rel(r.H, d["H"]) <= TOL, rel(r.H, d["H"])
     assert rel(r.S, d["S"]) <= TOL, rel(r.S, d["S"])
     ng = dims[2]
@@ -321,3 +321,25 @@ def test_concurrent_host_threads(restatement):
     for t in th:
         t.join()
     assert not errs, errs
+
+
+def test_arith_modes_agree_and_account(restatement):
+    """3M and 4M complex arithmetic: both within the bar of the reference-pinned oracle,
+    each bitwise deterministic, 3M executes 3/4 of the contraction flops; the ledger is
+    identical (the reference's flop model counts 8 real flops per complex MAC)."""
+    p = hb.generate_problem(16, 49, 600, 2, 3)
+    H, S, _ = restatement.build_hs_refined(p)
+    res = {}
+    for arith in ("3m", "4m"):
+        a = hb.build_hs_refined(p, hb.PipelineConfig(arith=arith))
+        b = hb.build_hs_refined(p, hb.PipelineConfig(arith=arith))
+        assert np.array_equal(a.H, b.H) and np.array_equal(a.S, b.S)
+        assert rel(a.H, H) <= 1e-13 and rel(a.S, S) <= 1e-13, (arith, rel(a.H, H), rel(a.S, S))
+        res[arith] = a
+    assert res["3m"].ledger == res["4m"].ledger == hb.flop_model(p)
+    K, ng = p.n_atoms * p.n_l, p.n_g
+    cmac = 20 * K * ng * ng + 24 * p.n_atoms * p.n_l ** 2 * ng
+    assert res["4m"].stats["executed_flops"] == cmac + 2 * K * ng
+    assert res["3m"].stats["executed_flops"] == cmac // 8 * 6 + 2 * K * ng
+    with pytest.raises(hb.ConfigError):
+        hb.build_hs_refined(p, hb.PipelineConfig(arith="2m"))

@@ -28,10 +28,10 @@ __global__ void fill(double* p, size_t n, unsigned seed) {
   }
 }
 
-template <int BM, int WM, int WN, int ST, int MINB>
+template <int BM, int WM, int WN, int ST, int MINB, int G3M = 0>
 void run(const char* name, double2* A, double2* B, double2* out, uint64_t K, uint64_t ng, int nseg) {
   using Cfg = CtnCfg<kTri, BM, BM, WM, WN, ST>;
-  auto kern = ctn_contract_kernel<kTri, BM, BM, WM, WN, ST, MINB>;
+  auto kern = ctn_contract_kernel<kTri, BM, BM, WM, WN, ST, MINB, G3M>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
   CtnParams P;
   memset(&P, 0, sizeof(P));
@@ -81,7 +81,7 @@ void run(const char* name, double2* A, double2* B, double2* out, uint64_t K, uin
   }
   cudaError_t err = cudaGetLastError();
   double flops = 4.0 * nseg * K * (double)ng * ng;
-  printf("%-34s occ %d grid %6d  %8.3f ms  %6.2f TF/s  %s\n", name, occ, grid, best, flops / best / 1e9,
+  printf("%-34s occ %d grid %6d  %8.3f ms  %6.2f TF/s(ledger)  %s\n", name, occ, grid, best, flops / best / 1e9,
          err ? cudaGetErrorString(err) : "");
 }
 
@@ -95,11 +95,11 @@ int main(int argc, char** argv) {
   fill<<<1024, 256>>>((double*)A, 2 * K * ng, 1);
   fill<<<1024, 256>>>((double*)B, 2 * K * ng, 2);
   printf("K %lu N_G %lu nseg %d\n", K, ng, nseg);
-  run<64, 2, 4, 8, 1>("64 2x4 (32x16) st8 minb1 [current]", A, B, out, K, ng, nseg);
-  run<32, 1, 2, 8, 2>("32 1x2 (32x16) st8 minb2", A, B, out, K, ng, nseg);
-  run<32, 1, 2, 8, 3>("32 1x2 (32x16) st8 minb3", A, B, out, K, ng, nseg);
-  run<32, 2, 2, 8, 2>("32 2x2 (16x16) st8 minb2", A, B, out, K, ng, nseg);
-  run<32, 1, 4, 8, 2>("32 1x4 (32x8) st8 minb2", A, B, out, K, ng, nseg);
-  run<64, 2, 4, 4, 1>("64 2x4 (32x16) st4 minb1", A, B, out, K, ng, nseg);
+  run<64, 2, 4, 8, 1>("64 2x4 (32x16) st8 [current, 4M]", A, B, out, K, ng, nseg);
+  run<64, 2, 4, 8, 1, 2>("64 2x4 st8 3M sweeps t1 t2 t3", A, B, out, K, ng, nseg);
+  run<64, 2, 4, 8, 1, 3>("64 2x4 st8 3M mb-outer", A, B, out, K, ng, nseg);
+  run<64, 2, 4, 8, 1, 4>("64 2x4 st8 3M sweeps t3 t1 t2", A, B, out, K, ng, nseg);
+  run<64, 2, 4, 4, 1, 2>("64 2x4 st4 3M sweeps t1 t2 t3", A, B, out, K, ng, nseg);
+  run<64, 2, 4, 8, 1, 2>("64 2x4 st8 3M sweeps t1 t2 t3", A, B, out, K, ng, nseg);
   return 0;
 }
