@@ -169,7 +169,9 @@ __device__ __forceinline__ uint64_t packed_index(uint64_t n, uint64_t i, uint64_
   return j * (2 * n - j + 1) / 2 + (i - j);
 }
 
-template <int MODE, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES>
+// KSUB: 128-byte k-slabs (8 complex) per pipeline stage; one full/empty mbarrier
+// handshake per stage, so KSUB > 1 amortises the synchronisation over more DMMAs.
+template <int MODE, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, int KSUB = 1>
 struct CtnCfg {
   static constexpr int kConsumerWarps = WARPS_M * WARPS_N;
   // warp specialisation with register rebalancing: the consumer warps form whole
@@ -184,8 +186,10 @@ struct CtnCfg {
   static constexpr int kWN = BN / WARPS_N;
   static constexpr int kMB = kWM / 8;
   static constexpr int kNB = kWN / 8;
-  static constexpr int kStageL = BM * 128;
-  static constexpr int kStageR = BN * 128;
+  static constexpr int kSubL = BM * 128;  // one k-slab of the left operand tile
+  static constexpr int kSubR = BN * 128;
+  static constexpr int kStageL = KSUB * kSubL;
+  static constexpr int kStageR = KSUB * kSubR;
   static constexpr int kStageBytes = kStageL + kStageR;
   static constexpr int kSmemBytes = STAGES * kStageBytes + 1024 /*align*/ + 2 * STAGES * 8 + 64;
 };
@@ -257,10 +261,10 @@ __device__ __forceinline__ void consumer_bar(int nthreads) {
 //   flops per complex MAC): per k, t1 += a_r b_r, t2 += a_i b_i, t3 += (a_r - a_i)(b_r + b_i),
 //   then Re(conj(a) b) = t1 + t2 and Im = t3 - t1 + t2.  Still all-FP64; the imaginary
 //   part's rounding error bound grows by a small constant factor.
-template <int MODE, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, int MINB = 1, int G3M = 0>
-__global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>::kThreads, MINB)
+template <int MODE, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, int MINB = 1, int G3M = 0, int KSUB = 1>
+__global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES, KSUB>::kThreads, MINB)
     ctn_contract_kernel(const __grid_constant__ CtnParams P) {
-  using Cfg = CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>;
+  using Cfg = CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES, KSUB>;
   constexpr int MB = Cfg::kMB, NB = Cfg::kNB;
   constexpr int NCT = Cfg::kConsumerWarps * 32;  // consumer threads
   constexpr int NS = G3M ? 3 : 2;                // accumulator sets per output element
@@ -326,26 +330,29 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>
         tile_origin(pc.tile, row0, col0, atom);
         int seg = 0, kc = pc.k0;
         while (seg < P.nseg - 1 && kc >= P.kchunks[seg]) kc -= P.kchunks[seg++];
-        for (int c = pc.k0; c < pc.k1; ++c, ++it) {
-          while (kc >= P.kchunks[seg]) {
-            kc = 0;
-            ++seg;
-          }
+        for (int c = pc.k0; c < pc.k1; c += KSUB, ++it) {
+          const int n = min(KSUB, pc.k1 - c);  // k-slabs in this stage
           const int slot = it % STAGES;
           mbar_wait(&empty[slot], ((it / STAGES) & 1) ^ 1);
-          uint8_t* sL = smem + slot * Cfg::kStageBytes;
-          uint8_t* sR = sL + Cfg::kStageL;
-          mbar_arrive_expect_tx(&full[slot], Cfg::kStageBytes);
-          const int x = kc * 2 * kChunkC;
-          if (P.l_row_z[seg])
-            tma_load_3d(sL, &P.L[seg], x, atom, row0, &full[slot]);
-          else
-            tma_load_3d(sL, &P.L[seg], x, row0, atom, &full[slot]);
-          if (P.r_row_z[seg])
-            tma_load_3d(sR, &P.R[seg], x, atom, col0, &full[slot]);
-          else
-            tma_load_3d(sR, &P.R[seg], x, col0, atom, &full[slot]);
-          ++kc;
+          mbar_arrive_expect_tx(&full[slot], n * (Cfg::kSubL + Cfg::kSubR));
+          for (int u = 0; u < n; ++u) {
+            while (kc >= P.kchunks[seg]) {
+              kc = 0;
+              ++seg;
+            }
+            uint8_t* sL = smem + slot * Cfg::kStageBytes + u * Cfg::kSubL;
+            uint8_t* sR = smem + slot * Cfg::kStageBytes + Cfg::kStageL + u * Cfg::kSubR;
+            const int x = kc * 2 * kChunkC;
+            if (P.l_row_z[seg])
+              tma_load_3d(sL, &P.L[seg], x, atom, row0, &full[slot]);
+            else
+              tma_load_3d(sL, &P.L[seg], x, row0, atom, &full[slot]);
+            if (P.r_row_z[seg])
+              tma_load_3d(sR, &P.R[seg], x, atom, col0, &full[slot]);
+            else
+              tma_load_3d(sR, &P.R[seg], x, col0, atom, &full[slot]);
+            ++kc;
+          }
         }
         have = MODE == kTri ? sched.next(pc) : false;
       }
@@ -366,7 +373,7 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>
 #pragma unroll
   for (int mb = 0; mb < MB; ++mb) offL[mb] = (wm * Cfg::kWM + 8 * mb + pg) * 128;
 #pragma unroll
-  for (int nb = 0; nb < NB; ++nb) offR[nb] = Cfg::kStageL + (wn * Cfg::kWN + 8 * nb + pg) * 128;
+  for (int nb = 0; nb < NB; ++nb) offR[nb] = Cfg::kStageL + (wn * Cfg::kWN + 8 * nb + pg) * 128;  // sub-slab 0
 #pragma unroll
   for (int kk = 0; kk < 2; ++kk) offK[kk] = ((4 * kk + q) ^ pg) << 4;
 
@@ -393,12 +400,12 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>
       double2 a[MB], b[NB];
       double sa[G3M ? MB : 1], sb[G3M ? NB : 1];  // 3M: a_r - a_i, b_r + b_i
     };
-    auto load_frag = [&](Frag& f, const uint8_t* st, int kk) {
+    auto load_frag = [&](Frag& f, const uint8_t* st, int u, int kk) {
       const uint32_t base = smem_u32(st) + offK[kk];
 #pragma unroll
-      for (int mb = 0; mb < MB; ++mb) f.a[mb] = lds128(base + offL[mb]);
+      for (int mb = 0; mb < MB; ++mb) f.a[mb] = lds128(base + u * Cfg::kSubL + offL[mb]);
 #pragma unroll
-      for (int nb = 0; nb < NB; ++nb) f.b[nb] = lds128(base + offR[nb]);
+      for (int nb = 0; nb < NB; ++nb) f.b[nb] = lds128(base + u * Cfg::kSubR + offR[nb]);
     };
     // 3M operand sums, formed one step ahead of their use (off the DMMA issue path)
     auto sum_frag = [&](Frag& f) {
@@ -451,22 +458,32 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES>
       {
         const int slot = it % STAGES;
         mbar_wait(&full[slot], (it / STAGES) & 1);
-        load_frag(f0, smem + slot * Cfg::kStageBytes, 0);
+        load_frag(f0, smem + slot * Cfg::kStageBytes, 0, 0);
         sum_frag(f0);
       }
-      for (int c = pc.k0; c < pc.k1; ++c, ++it) {
+      for (int c = pc.k0; c < pc.k1; c += KSUB, ++it) {
+        const int n = min(KSUB, pc.k1 - c);
         const int slot = it % STAGES;
         const uint8_t* st = smem + slot * Cfg::kStageBytes;
-        load_frag(f1, st, 1);
-        mma_frag(f0);
-        sum_frag(f1);
-        if (c + 1 < pc.k1) {
-          const int nslot = (it + 1) % STAGES;
-          mbar_wait(&full[nslot], ((it + 1) / STAGES) & 1);
-          load_frag(f0, smem + nslot * Cfg::kStageBytes, 0);
+#pragma unroll
+        for (int u = 0; u < KSUB; ++u) {
+          if (u < n) {
+            load_frag(f1, st, u, 1);
+            mma_frag(f0);
+            sum_frag(f1);
+            // the next step's fragments: sub-slab u+1 of this stage, or the next stage
+            const bool more = u + 1 < n || c + KSUB < pc.k1;
+            if (u + 1 < n) {
+              load_frag(f0, st, u + 1, 0);
+            } else if (c + KSUB < pc.k1) {
+              const int nslot = (it + 1) % STAGES;
+              mbar_wait(&full[nslot], ((it + 1) / STAGES) & 1);
+              load_frag(f0, smem + nslot * Cfg::kStageBytes, 0, 0);
+            }
+            mma_frag(f1);
+            if (more) sum_frag(f0);
+          }
         }
-        mma_frag(f1);
-        if (c + 1 < pc.k1) sum_frag(f0);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
       }

@@ -16,6 +16,7 @@ import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
 import paper_1712_07206_b200 as hb  # noqa: E402
 
 NAMED = {"c1": (16, 49, 1000), "c2": (64, 81, 3000), "c3": (108, 121, 6000), "c4": (512, 121, 13000)}
@@ -34,6 +35,7 @@ def points(only):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--algo", default="fused", choices=["fused", "refined", "original"])
+    ap.add_argument("--arith", default="3m", choices=["3m", "4m"])
     ap.add_argument("--out", default="gpurun_out/sweep.jsonl")
     ap.add_argument("--only", default="")
     ap.add_argument("--budget", type=float, default=4.0, help="seconds of timed builds per point (>= 2 builds)")
@@ -44,6 +46,7 @@ def main():
         for name, na, nl, ng in points(args.only):
             t0 = time.time()
             e = hb.Engine(0, na, nl, ng)
+            e.set_arith(args.arith)
             e.fill_synthetic(1)
             e.build(args.algo)  # warm-up (also allocates X2 for fused / original)
             st = e.sync()
@@ -58,7 +61,9 @@ def main():
             t = sum(dev) / len(dev)
             rec = {"point": name, "n_atoms": na, "n_l": nl, "n_g": ng, "algo": args.algo, "builds": n,
                    "build_ms": t * 1e3, "min_ms": min(dev) * 1e3, "ledger_flops": led,
-                   "tflops": led / t / 1e12, "frac_of_dmma_peak": led / t / 1e12 / peak, "dmma_peak_tflops": peak,
+                   "tflops": led / t / 1e12, "ledger_frac_of_dmma_peak": led / t / 1e12 / peak, "dmma_peak_tflops": peak,
+                   "arith": args.arith, "executed_tflops": bench.executed_flops(na, nl, ng, args.arith) / t / 1e12,
+                   "executed_frac_of_dmma_peak": bench.executed_flops(na, nl, ng, args.arith) / t / 1e12 / peak,
                    "s_kernel_tflops": kt["s_flops"] / kt["s_ms"] / 1e9 if kt["s_ms"] else None,
                    "h_kernel_tflops": kt["h_flops"] / kt["h_ms"] / 1e9 if kt["h_ms"] else None,
                    "phase_ms": {k: v * 1e3 for k, v in st["phase_seconds"].items()},

@@ -28,10 +28,10 @@ __global__ void fill(double* p, size_t n, unsigned seed) {
   }
 }
 
-template <int BM, int WM, int WN, int ST, int MINB, int G3M = 0>
+template <int BM, int WM, int WN, int ST, int MINB, int G3M = 0, int KSUB = 1>
 void run(const char* name, double2* A, double2* B, double2* out, uint64_t K, uint64_t ng, int nseg) {
-  using Cfg = CtnCfg<kTri, BM, BM, WM, WN, ST>;
-  auto kern = ctn_contract_kernel<kTri, BM, BM, WM, WN, ST, MINB, G3M>;
+  using Cfg = CtnCfg<kTri, BM, BM, WM, WN, ST, KSUB>;
+  auto kern = ctn_contract_kernel<kTri, BM, BM, WM, WN, ST, MINB, G3M, KSUB>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
   CtnParams P;
   memset(&P, 0, sizeof(P));
@@ -95,11 +95,12 @@ int main(int argc, char** argv) {
   fill<<<1024, 256>>>((double*)A, 2 * K * ng, 1);
   fill<<<1024, 256>>>((double*)B, 2 * K * ng, 2);
   printf("K %lu N_G %lu nseg %d\n", K, ng, nseg);
-  run<64, 2, 4, 8, 1>("64 2x4 (32x16) st8 [current, 4M]", A, B, out, K, ng, nseg);
-  run<64, 2, 4, 8, 1, 2>("64 2x4 st8 3M sweeps t1 t2 t3", A, B, out, K, ng, nseg);
-  run<64, 2, 4, 8, 1, 3>("64 2x4 st8 3M mb-outer", A, B, out, K, ng, nseg);
-  run<64, 2, 4, 8, 1, 4>("64 2x4 st8 3M sweeps t3 t1 t2", A, B, out, K, ng, nseg);
-  run<64, 2, 4, 4, 1, 2>("64 2x4 st4 3M sweeps t1 t2 t3", A, B, out, K, ng, nseg);
-  run<64, 2, 4, 8, 1, 2>("64 2x4 st8 3M sweeps t1 t2 t3", A, B, out, K, ng, nseg);
+  run<64, 2, 4, 8, 1, 0, 1>("4M st8 ksub1", A, B, out, K, ng, nseg);
+  run<64, 2, 4, 4, 1, 0, 2>("4M st4 ksub2", A, B, out, K, ng, nseg);
+  run<64, 2, 4, 8, 1, 1, 1>("3M st8 ksub1 [current]", A, B, out, K, ng, nseg);
+  run<64, 2, 4, 4, 1, 1, 2>("3M st4 ksub2", A, B, out, K, ng, nseg);
+  run<64, 2, 4, 2, 1, 1, 4>("3M st2 ksub4", A, B, out, K, ng, nseg);
+  run<64, 2, 4, 4, 1, 1, 3>("3M st4 ksub3", A, B, out, K, ng, nseg);
+  run<64, 2, 4, 8, 1, 1, 1>("3M st8 ksub1 [current]", A, B, out, K, ng, nseg);
   return 0;
 }
