@@ -8,6 +8,7 @@
 using namespace hsdla_b200;
 
 static PFN_cuTensorMapEncodeTiled_v12000 enc;
+static std::vector<double> ref3m;  // first 3M variant's output (all 3M variants must match it bitwise)
 static void make_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
                      uint64_t s2, uint32_t b1, uint32_t b2) {
   cuuint64_t dims[3] = {d0, d1, d2};
@@ -81,8 +82,16 @@ void run(const char* name, double2* A, double2* B, double2* out, uint64_t K, uin
   }
   cudaError_t err = cudaGetLastError();
   double flops = 4.0 * nseg * K * (double)ng * ng;
-  printf("%-34s occ %d grid %6d  %8.3f ms  %6.2f TF/s(ledger)  %s\n", name, occ, grid, best, flops / best / 1e9,
-         err ? cudaGetErrorString(err) : "");
+  // bitwise comparison against the first 3M variant's output (same sums, same DMMA order)
+  std::vector<double> h(ng * (ng + 1));
+  cudaMemcpy(h.data(), out, h.size() * 8, cudaMemcpyDeviceToHost);
+  size_t ndiff = 0;
+  if (G3M) {
+    if (ref3m.empty()) ref3m = h;
+    for (size_t i = 0; i < h.size(); ++i) ndiff += h[i] != ref3m[i];
+  }
+  printf("%-34s occ %d grid %6d  %8.3f ms  %6.2f TF/s(ledger)  diff-vs-3M %zu  %s\n", name, occ, grid, best,
+         flops / best / 1e9, ndiff, err ? cudaGetErrorString(err) : "");
 }
 
 int main(int argc, char** argv) {
@@ -99,8 +108,6 @@ int main(int argc, char** argv) {
   run<64, 2, 4, 4, 1, 0, 2>("4M st4 ksub2", A, B, out, K, ng, nseg);
   run<64, 2, 4, 8, 1, 1, 1>("3M st8 ksub1 [current]", A, B, out, K, ng, nseg);
   run<64, 2, 4, 4, 1, 1, 2>("3M st4 ksub2", A, B, out, K, ng, nseg);
-  run<64, 2, 4, 2, 1, 1, 4>("3M st2 ksub4", A, B, out, K, ng, nseg);
-  run<64, 2, 4, 4, 1, 1, 3>("3M st4 ksub3", A, B, out, K, ng, nseg);
   run<64, 2, 4, 8, 1, 1, 1>("3M st8 ksub1 [current]", A, B, out, K, ng, nseg);
   return 0;
 }
