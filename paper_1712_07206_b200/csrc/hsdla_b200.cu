@@ -373,7 +373,7 @@ struct hsdla_b200_engine {
   std::vector<hsdla_b200::OpTime> ops;
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr, ev_s_done = nullptr, ev_s_red = nullptr,
               ev_reduce_end = nullptr, ev_up0 = nullptr, ev_up1 = nullptr, ev_s_d2h = nullptr;
-  static constexpr int kD2hPieces = 4;   // H downloads in column-range pieces, unpacked as each lands
+  static constexpr int kD2hPieces = 8;   // H downloads in column-range pieces, unpacked as each lands
   cudaEvent_t ev_h_piece[kD2hPieces] = {};
   cudaEvent_t ev_h_band[kD2hPieces] = {};  // final H contraction finished tile-column band q
   cudaEvent_t ev_h_red[kD2hPieces] = {};   // ... and band q's packed range is reduced (NCCL)
@@ -571,20 +571,29 @@ static void make_chunk(hsdla_b200_engine* e, uint64_t a0, uint64_t a1, bool firs
 // (larger) uploads still finish before the previous chunk's phases do.  The growth
 // factor follows rho, the compute/upload time ratio of one atom:
 //   rho = (20 K N_G^2 / 34 TF/s) / (32 K N_G B / rate) = N_G * rate * 1.84e-14,
-// r = clamp(0.8 rho, 1, 4); the first chunk is the larger of N_A/16 and the head of an
-// 8-term geometric series summing to N_A; at most 8 chunks.  `rate` is the host->device
+// r = clamp(0.8 rho, 1, 4); the first chunk is the larger of N_A/32 and the head of an
+// 8-term geometric series summing to N_A; at most 8 chunks.  (The 34 TF/s is the 4M
+// rate; calibrating it to 3M's faster compute gives more, smaller chunks, and every
+// extra chunk costs ~0.2 ms at C2 in per-launch epilogues and ramps: tools/stream_tune.py
+// measured N_A/32 with the 4M constant best, 24.5 ms per call against 24.6-25.1.)  `rate` is the host->device
 // feed: ~50 GB/s for page-locked inputs (PCIe), ~20 GB/s for pageable inputs packed by
 // host threads or for page-cached HSDL files.  Small problems (< 64 MB of A+B): one chunk.
+// Development knobs for the streaming / banding heuristics (tools/stream_tune.py).
+static double env_double(const char* name, double dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atof(v) : dflt;
+}
+
 static std::vector<uint64_t> stream_bounds(uint64_t na, uint64_t nl, uint64_t ng, double rate) {
   std::vector<uint64_t> b{0};
   if (na * nl * ng < (uint64_t(1) << 22) || na < 2) {
     b.push_back(na);
     return b;
   }
-  const double rho = static_cast<double>(ng) * rate * 1.84e-14;
+  const double rho = static_cast<double>(ng) * rate * env_double("HSDLA_B200_STREAM_C", 1.84e-14);
   const double r = std::min(4.0, std::max(1.0, 0.8 * rho));
   const double head = r > 1.0001 ? (r - 1.0) / (std::pow(r, 8.0) - 1.0) : 1.0 / 8.0;
-  double size = std::max(1.0, static_cast<double>(na) * std::max(1.0 / 16.0, head));
+  double size = std::max(1.0, static_cast<double>(na) * std::max(env_double("HSDLA_B200_STREAM_FLOOR", 1.0 / 32.0), head));
   while (b.back() < na) {
     const uint64_t left = na - b.back();
     uint64_t take = std::min<uint64_t>(left, static_cast<uint64_t>(std::llround(size)));
@@ -595,17 +604,28 @@ static std::vector<uint64_t> stream_bounds(uint64_t na, uint64_t nl, uint64_t ng
   return b;
 }
 
-// Tile-column boundaries splitting the lower tiles into kD2hPieces bands of about
-// equal tile count (column tj holds T - tj tiles); the packed H range of band q is
-// columns [64 c_q, 64 c_{q+1}).
+// Tile-column boundaries splitting the lower tiles into kD2hPieces bands (column tj
+// holds T - tj tiles); the packed H range of band q is columns [64 c_q, 64 c_{q+1}).
+// Band q's download and host unpack run while band q+1 computes, so only the last
+// band's copy is exposed after the kernels end.  Band q+1 holds kBandRatio x band q's
+// tiles: 8 equal bands (ratio 1) measured best at C2 (tools/stream_tune.py: 24.5 ms
+// per call against 24.75 with 4 equal bands; shrinking bands, ratio 0.8 / 0.7, lost
+// 0.1-0.6 ms because the small last launches run below full efficiency).
 static void make_pieces(hsdla_b200_engine* e) {
+  const double kBandRatio = env_double("HSDLA_B200_BAND_RATIO", 1.0);
   const int T = static_cast<int>((e->ng + kTriBM - 1) / kTriBM), Q = hsdla_b200_engine::kD2hPieces;
   const long long total = static_cast<long long>(T) * (T + 1) / 2;
+  double wsum = 0, w = 1;
+  for (int q = 0; q < Q; ++q, w *= kBandRatio) wsum += w;
   e->piece_tiles[0] = 0;
   int tj = 0;
   long long acc = 0;
-  for (int q = 1; q < Q; ++q) {
-    while (tj < T && acc + (T - tj) <= total * q / Q) acc += T - tj++;
+  double cum = 0;
+  w = 1;
+  for (int q = 1; q < Q; ++q, w *= kBandRatio) {
+    cum += w;
+    const long long target = static_cast<long long>(static_cast<double>(total) * cum / wsum);
+    while (tj < T && acc + (T - tj) <= target) acc += T - tj++;
     e->piece_tiles[q] = tj;
   }
   e->piece_tiles[Q] = T;
@@ -892,7 +912,7 @@ static void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool la
                           hsdla_b200_engine::KTimer* kt) {
   cudaStream_t s = e->stream;
   // The build's final H contraction: whole, or band by band (tile-column bands of
-  // equal work, event after each) so the download of band q overlaps band q+1.
+  // equal work, event after each; make_pieces) so the download of band q overlaps band q+1.
   auto final_h = [&](const CtnParams& P) {
     // bands: the one-shot drop-in (download overlaps) and every multi-rank build (the
     // NCCL reduce of band q overlaps the compute of band q+1)
