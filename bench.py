@@ -147,12 +147,16 @@ class Dist:
 
 
 # ---------------------------------------------------------------------------
-def cpu_reference_sample(na, nl, ng, budget_s, steps=1, warmup=0):
+def cpu_reference_sample(na, nl, ng, budget_s, steps=1, warmup=0, mode="atoms"):
     """Time the reference CPU build_hs_refined (Strategy::Cpu, BlockedParallel,
-    block 128, all host threads) on an ATOM-subsampled instance of the workload:
-    same N_L and N_G (so the reference's column-panel parallelism is the full-size
-    one), N_A' atoms chosen so one step takes ~budget_s.  H and S are sums over
-    atoms, so ledger-flops/s on N_A' atoms is the full-size rate."""
+    block 128, all host threads) on a subsampled instance of the workload.
+
+    mode "atoms": same N_L and N_G (so the reference's column-panel parallelism is the
+    full-size one), N_A' atoms chosen so one step takes ~budget_s.  H and S are sums
+    over atoms, so ledger-flops/s on N_A' atoms is the full-size rate (an upper bound
+    when the short K' = N_A' N_L dot products stay in cache).
+    mode "columns" (SURVEY section 8d for C4/C5): all atoms, N_G' < N_G columns chosen so
+    one step takes ~budget_s; the full-length K dot products of the full-size run."""
     from oracle.oracle import Reference, Restatement
     threads = os.cpu_count() or 1
     if Reference.available():
@@ -161,23 +165,58 @@ def cpu_reference_sample(na, nl, ng, budget_s, steps=1, warmup=0):
     else:  # the C restatement (single-threaded port)
         ref, kind, threads = Restatement(), "port", 1
         run = lambda p: ref.build_hs_refined(p)
+    na_s, ng_s = na, ng
+    if mode == "columns" and kind == "reference":
+        # full-size time extrapolated phase by phase: s, her2k, herkx ~ K N_G^2;
+        # z_loop, hemm_loop ~ N_A N_L^2 N_G (the sample's N_G' is chosen by the same model)
+        quad = ("s", "her2k", "herkx")
+
+        def split(res):
+            ph = dict(res["phases"])
+            big = sum(v for k, v in ph.items() if k in quad)
+            return big, sum(ph.values()) - big
+
+        ng_p = min(ng, 256)
+        big, small = split(ref.build_hs(ref.generate_problem(na, nl, ng_p, 1, 0), "refined", threads=threads,
+                                        blocked=True, block=128, want_hs=False))
+        a_, b_ = big / ng_p ** 2, small / ng_p
+        ng_s = int(min(ng, max(ng_p, (-b_ + (b_ * b_ + 4 * a_ * budget_s) ** 0.5) / (2 * a_ + 1e-30))))
+        p = ref.generate_problem(na, nl, ng_s, 1, 0)
+        for _ in range(warmup):
+            run(p)
+        ts = []
+        for _ in range(steps):
+            t = time.perf_counter()
+            res = ref.build_hs(p, "refined", threads=threads, blocked=True, block=128, want_hs=False)
+            ts.append(time.perf_counter() - t)
+            big, small = split(res)
+        dt = sum(ts) / len(ts)
+        t_full = big * (ng / ng_s) ** 2 + small * (ng / ng_s) + max(0.0, dt - big - small) * (ng / ng_s) ** 2
+        return {"value": ledger_flops(na, nl, ng) / t_full / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": kind,
+                "sample": f"refined H+S of ({na} atoms, N_L {nl}, {ng_s} of {ng} G-vectors), full-size time "
+                          f"extrapolated per phase (K N_G^2 phases x (N_G/N_G')^2, per-atom phases x N_G/N_G'): "
+                          f"{t_full:.1f} s per k-point; reference Strategy::Cpu BlockedParallel block 128, "
+                          f"{threads} threads, {dt:.2f} s per sample",
+                "seconds_per_sample": dt, "seconds_full_extrapolated": t_full, "n_atoms_sample": na,
+                "n_g_sample": ng_s, "sampling": "columns (extrapolated)"}
     p = ref.generate_problem(1, nl, ng, 1, 0)
     t = time.perf_counter()
     run(p)
     rate = ledger_flops(1, nl, ng) / max(time.perf_counter() - t, 1e-6)
     na_s = int(max(1, min(na, budget_s * rate / ledger_flops(1, nl, ng))))
-    p = ref.generate_problem(na_s, nl, ng, 1, 0)
+    p = ref.generate_problem(na_s, nl, ng_s, 1, 0)
     for _ in range(warmup):
         run(p)
     t = time.perf_counter()
     for _ in range(steps):
         run(p)
     dt = (time.perf_counter() - t) / steps
-    return {"value": ledger_flops(na_s, nl, ng) / dt / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": kind,
-            "sample": f"refined H+S of ({na_s} of {na} atoms, N_L {nl}, N_G {ng}); "
+    what = f"{na_s} of {na} atoms, N_L {nl}, N_G {ng}"
+    return {"value": ledger_flops(na_s, nl, ng_s) / dt / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": kind,
+            "sample": f"refined H+S of ({what}); "
                       f"{'reference Strategy::Cpu BlockedParallel block 128' if kind == 'reference' else 'C port'}"
                       f", {threads} threads, {dt:.2f} s per k-point sample",
-            "seconds_per_sample": dt, "n_atoms_sample": na_s}
+            "seconds_per_sample": dt, "n_atoms_sample": na_s, "n_g_sample": ng_s, "sampling": mode}
 
 
 def run_reference_arm(args):
