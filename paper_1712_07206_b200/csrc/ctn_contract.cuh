@@ -539,38 +539,56 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES,
                    ? P.out + (static_cast<uint64_t>(atom) * P.m_valid + i) + static_cast<uint64_t>(j) * P.ldo
                    : nullptr;
       };
-      // Per row block mb: with beta != 0 gather its old values first (NB x 2 independent
-      // loads in flight together), then combine and store.
+      // Fold the accumulator sets into (Re, Im) first (3M: frees a third of them).  With
+      // beta != 0 the old values are gathered MG row blocks at a time (MG x NB x 2 loads in
+      // flight together; all MB at once would exceed the 168 registers ptxas allocates
+      // under the 384-thread launch bound), then combined and stored.
+      double2 x[MB][NB][2];
 #pragma unroll
-      for (int mb = 0; mb < MB; ++mb) {
-        const int i = row0 + wm * Cfg::kWM + 8 * mb + pg;
-        double2 old[NB][2];
+      for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            x[mb][nb][e] = G3M ? make_double2(acc[mb][nb][e][0] + acc[mb][nb][e][1],
+                                              acc[mb][nb][e][NS - 1] - acc[mb][nb][e][0] + acc[mb][nb][e][1])
+                               : make_double2(acc[mb][nb][e][0], acc[mb][nb][e][1]);
+      constexpr int MG = MB % 2 == 0 ? 2 : 1;
+#pragma unroll
+      for (int m0 = 0; m0 < MB; m0 += MG) {
+        double2 old[MG][NB][2];
         if (beta != 0.0) {
 #pragma unroll
-          for (int nb = 0; nb < NB; ++nb)
+          for (int u = 0; u < MG; ++u)
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const double2* d = dst_of(mb, nb, e);
-              old[nb][e] = d ? __ldcg(d) : make_double2(0.0, 0.0);
-            }
+            for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const double2* d = dst_of(m0 + u, nb, e);
+                old[u][nb][e] = d ? __ldcg(d) : make_double2(0.0, 0.0);
+              }
         }
 #pragma unroll
-        for (int nb = 0; nb < NB; ++nb) {
+        for (int u = 0; u < MG; ++u) {
+          const int mb = m0 + u;
+          const int i = row0 + wm * Cfg::kWM + 8 * mb + pg;
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            double2* d = dst_of(mb, nb, e);
-            if (!d) continue;
-            const int j = col0 + wn * Cfg::kWN + 8 * nb + (e ? 4 + q : q);
-            const double xr = G3M ? acc[mb][nb][e][0] + acc[mb][nb][e][1] : acc[mb][nb][e][0];
-            const double xi = G3M ? acc[mb][nb][e][NS - 1] - acc[mb][nb][e][0] + acc[mb][nb][e][1] : acc[mb][nb][e][1];
-            double vr = ar * xr - ai * xi;
-            double vi = ar * xi + ai * xr;
-            if (MODE == kTri && i == j && !keep_di) vi = 0.0;
-            if (beta != 0.0) {
-              vr += beta * old[nb][e].x;
-              vi += beta * old[nb][e].y;
+          for (int nb = 0; nb < NB; ++nb) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              double2* d = dst_of(mb, nb, e);
+              if (!d) continue;
+              const int j = col0 + wn * Cfg::kWN + 8 * nb + (e ? 4 + q : q);
+              const double xr = x[mb][nb][e].x, xi = x[mb][nb][e].y;
+              double vr = ar * xr - ai * xi;
+              double vi = ar * xi + ai * xr;
+              if (MODE == kTri && i == j && !keep_di) vi = 0.0;
+              if (beta != 0.0) {
+                vr += beta * old[u][nb][e].x;
+                vi += beta * old[u][nb][e].y;
+              }
+              *d = make_double2(vr, vi);
             }
-            *d = make_double2(vr, vi);
           }
         }
       }
