@@ -40,12 +40,20 @@ CONFIGS = {
 }
 
 
-def executed_flops(na, nl, ng, arith):
-    """Real flops the GPU executes for one build (any algorithm): the complex-MAC work
-    20 K N_G^2 + 24 N_A N_L^2 N_G at 8 flops per MAC (4M) or 6 (3M), plus 2 K N_G."""
+def executed_flops(na, nl, ng, arith, algo="merged"):
+    """Real flops the GPU executes for one build: the complex-MAC work at 8 flops per MAC
+    (4M) or 6 (3M) -- 16 K N_G^2 + 32 N_A N_L^2 N_G for the merged algorithm, 20 K N_G^2 +
+    24 N_A N_L^2 N_G for the others -- plus 2 K N_G."""
     K = na * nl
-    cmac8 = 20 * K * ng * ng + 24 * na * nl * nl * ng
+    if algo == "merged":
+        cmac8 = 16 * K * ng * ng + 32 * na * nl * nl * ng
+    else:
+        cmac8 = 20 * K * ng * ng + 24 * na * nl * nl * ng
     return (cmac8 // 8 * 6 if arith == "3m" else cmac8) + 2 * K * ng
+
+
+H_KERNEL = {"merged": "merged H = [A;B]^H [W_A;W_B]", "fused": "fused H = [Z;B;A]^H [B;Z;X]",
+            "refined": "her2k [Z;B]^H [B;Z]", "original": "h_aa_update Lft^H W"}
 
 
 def ledger_flops(na, nl, ng, variant="refined"):
@@ -311,7 +319,7 @@ def run_b200(args):
     st = eng.sync()
     F = ledger_flops(na_total, nl, ng, "original" if args.algo == "original" else "refined")
     value = F / (ms * 1e-3) / 1e12
-    exec_tf = executed_flops(na_total, nl, ng, args.arith) / (ms * 1e-3) / 1e12
+    exec_tf = executed_flops(na_total, nl, ng, args.arith, args.algo) / (ms * 1e-3) / 1e12
 
     # the same device-resident build with the plain 4-multiplication arithmetic, for reference
     ms4 = None
@@ -358,9 +366,10 @@ def run_b200(args):
         traffic = load_traffic(args.config)
         roofline = {"bound": "tensor", "achieved": h_tf, "peak": peak, "unit": "TFLOP/s", "frac": h_tf / peak,
                     "traffic": traffic,
-                    "kernel": "ctn_contract_kernel<TRI> fused H = [Z;B;A]^H [B;Z;X]: 12 K N_G^2 ledger flops per "
-                              f"launch, {'9 (3M: 6 real flops per complex MAC)' if xf < 1 else '12'} K N_G^2 "
-                              "executed; achieved = executed flops / mean launch time",
+                    "kernel": f"ctn_contract_kernel<TRI> {H_KERNEL.get(args.algo, 'H contraction')}: "
+                              f"{kt['h_flops'] // (na * nl * ng * ng)} K N_G^2 "
+                              f"flops per launch at 8 per complex MAC, {'6 per MAC executed (3M)' if xf < 1 else 'all executed (4M)'}; "
+                              "achieved = executed flops / mean launch time",
                     "achieved_ledger": h_led, "arith": args.arith,
                     "kernel_ms": kt["h_ms"], "flops_per_launch": int(kt["h_flops"] * xf),
                     "ledger_flops_per_launch": kt["h_flops"],
@@ -495,7 +504,7 @@ def run_file(args, hb, p, na, nl, ng):
         path = os.path.join(td, "problem.hsdl")
         hb.save_problem(p, path)
         fbytes = os.path.getsize(path)
-        cfg = hb.PipelineConfig(algo=args.algo if args.algo != "original" else "fused", arith=args.arith)
+        cfg = hb.PipelineConfig(algo=args.algo if args.algo != "original" else "merged", arith=args.arith)
         hb.build_hs_file(path, cfg, H=H, S=S)  # warm: engine cache + page cache
         steps = max(1, min(args.steps, 5))
         t = time.perf_counter()
@@ -586,7 +595,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--algo", default="fused", choices=["fused", "refined", "original"])
+    ap.add_argument("--algo", default="merged", choices=["merged", "fused", "refined", "original"])
     ap.add_argument("--arith", default="3m", choices=["3m", "4m"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--force-comm", action="store_true", help="NCCL communicator even at N=1 (plumbing check)")

@@ -40,13 +40,21 @@ extern "C" {
 #define HSDLA_B200_NCCL_ERROR 6      /* NCCL failure */
 
 /* ---- algorithms ------------------------------------------------------- */
+/* Merged (default): Algorithm 3's sums restated per atom as H_a = Y_a^H M_a Y_a with
+ * Y_a = [A_a; B_a] and the Hermitian block operator M_a = [[T_AA, T_AB], [T_AB^H, T_BB]]
+ * (pipeline.cpp:302-324 evaluates the same sum as Z^H B + B^H Z + A^H (T_AA A)).  Phase
+ * z_loop builds W_A = T_AA A + T_AB B and W_B = T_AB^H A + T_BB B (four per-atom
+ * products); phase her2k is ONE lower-triangular contraction [A;B]^H [W_A;W_B] over 2K.
+ * Executed 16 K N_G^2 + 32 N_A N_L^2 N_G complex-MAC flops against the ledger's
+ * 20 K N_G^2 + 24 N_A N_L^2 N_G; hemm_loop and herkx report 0 s. */
+#define HSDLA_B200_ALGO_REFINED_MERGED 0
 /* Reference phase order s, z_loop, her2k, hemm_loop, herkx; five launches of the
  * contraction engine, executed flops == the reference ledger. */
 #define HSDLA_B200_ALGO_REFINED 1
-/* Same products; her2k and herkx run as ONE lower-triangular contraction over
- * the stacked inner dimension [Z;B;A]^H [B;Z;X] (default).  Executed flops ==
- * ledger; the herkx phase reports 0 s (fused into her2k). */
-#define HSDLA_B200_ALGO_REFINED_FUSED 0
+/* Same products as REFINED; her2k and herkx run as ONE lower-triangular contraction
+ * over the stacked inner dimension [Z;B;A]^H [B;Z;X] (3K).  Executed flops == ledger;
+ * the herkx phase reports 0 s (fused into her2k). */
+#define HSDLA_B200_ALGO_REFINED_FUSED 3
 /* The original algorithm (paper Algorithm 1, hsdla::pipeline::build_hs_original,
  * pipeline.cpp:189-279; Variant::Original): phases z_loop, her2k, s, chol_loop,
  * h_aa_update.  Per-atom Cholesky try/fail of T_AA on the GPU (bit-identical to
@@ -244,7 +252,7 @@ int hsdla_b200_engine_set_comm(hsdla_b200_engine* e, const void* id128, int nran
 
 /* Contraction-kernel timing for the roofline: mean CUDA-event duration (ms) of
  * the S contraction (herk+herk, 8 K N_G^2 flops) and the H contraction launch
- * (fused: 12 K N_G^2; refined algo: the her2k launch, 8 K N_G^2) over every
+ * (fused: 12 K N_G^2; merged: 8 K N_G^2; refined algo: the her2k launch, 8 K N_G^2) over every
  * build since the last reset, recorded on the engine stream without per-build
  * host syncs.  reset != 0 clears the accumulators after reading. */
 int hsdla_b200_engine_kernel_times(hsdla_b200_engine* e, int reset, double* ms_s, double* ms_h,

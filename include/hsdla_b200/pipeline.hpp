@@ -31,7 +31,7 @@ namespace hsdla_b200 {
 struct Options {
   int n_gpus = 1;                             // atoms sharded over n_gpus, NCCL reduce to device_ids[0]
   std::vector<int> device_ids;                // empty: 0..n_gpus-1
-  int algo = HSDLA_B200_ALGO_REFINED_FUSED;   // or HSDLA_B200_ALGO_REFINED (reference phase order)
+  int algo = HSDLA_B200_ALGO_REFINED_MERGED;  // or REFINED_FUSED, or REFINED (reference phase order)
   int arith = HSDLA_B200_ARITH_3M;            // or HSDLA_B200_ARITH_4M (plain 4-multiplication complex)
 };
 
@@ -66,6 +66,8 @@ inline void fill_result(hsdla::pipeline::HSResult& r, const hsdla_b200_stats& st
                         st.phase_seconds[orig ? original_slots[i] : refined_slots[i]]});
   r.peak_temp_bytes = static_cast<std::size_t>(st.peak_temp_bytes);
   if (algo == HSDLA_B200_ALGO_REFINED_FUSED) r.warnings.push_back("herkx fused into the her2k contraction");
+  if (algo == HSDLA_B200_ALGO_REFINED_MERGED)
+    r.warnings.push_back("her2k, hemm_loop and herkx merged into one H contraction [A;B]^H [W_A;W_B]");
 }
 
 inline hsdla::pipeline::HSResult run(const hsdla::ProblemInstance& p, int algo, const Options& opt) {
@@ -110,8 +112,9 @@ inline hsdla::pipeline::HSResult build_hs_refined(const hsdla::ProblemInstance& 
                                                   const Options& opt = {}) {
   if (cfg.variant != hsdla::pipeline::Variant::Refined)
     throw hsdla::ConfigError("build_hs_refined: variant must be Refined");
-  if (opt.algo != HSDLA_B200_ALGO_REFINED_FUSED && opt.algo != HSDLA_B200_ALGO_REFINED)
-    throw hsdla::ConfigError("build_hs_refined: algo must be REFINED_FUSED or REFINED");
+  if (opt.algo != HSDLA_B200_ALGO_REFINED_MERGED && opt.algo != HSDLA_B200_ALGO_REFINED_FUSED &&
+      opt.algo != HSDLA_B200_ALGO_REFINED)
+    throw hsdla::ConfigError("build_hs_refined: algo must be REFINED_MERGED, REFINED_FUSED or REFINED");
   return detail::run(p, opt.algo, opt);
 }
 

@@ -37,9 +37,10 @@ int main(int argc, char** argv) {
     std::printf("%-44s %s (%.3e)\n", what, ok ? "PASS" : "FAIL", v);
     if (!ok) ++fails;
   };
-  for (int algo : {HSDLA_B200_ALGO_REFINED_FUSED, HSDLA_B200_ALGO_REFINED, HSDLA_B200_ALGO_REFINED_FUSED + 100}) {
+  for (int algo : {HSDLA_B200_ALGO_REFINED_MERGED, HSDLA_B200_ALGO_REFINED_FUSED, HSDLA_B200_ALGO_REFINED,
+                   HSDLA_B200_ALGO_REFINED_MERGED + 100, HSDLA_B200_ALGO_REFINED_FUSED + 100}) {
     hsdla_b200::Options opt;
-    opt.arith = algo >= 100 ? HSDLA_B200_ARITH_4M : HSDLA_B200_ARITH_3M;  // +100: the fused algorithm in 4M
+    opt.arith = algo >= 100 ? HSDLA_B200_ARITH_4M : HSDLA_B200_ARITH_3M;  // +100: the same algorithm in 4M
     algo %= 100;
     opt.algo = algo;
     const hsdla::pipeline::HSResult gpu = hsdla_b200::build_hs_refined(p, cfg, opt);

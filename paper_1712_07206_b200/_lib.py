@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libhsdla_b200.so")
 
 OK, DIMENSION_ERROR, SIZING_ERROR, CONFIG_ERROR, IO_ERROR, CUDA_ERROR, NCCL_ERROR = range(7)
-ALGO_REFINED_FUSED, ALGO_REFINED, ALGO_ORIGINAL = 0, 1, 2
+ALGO_REFINED_MERGED, ALGO_REFINED, ALGO_ORIGINAL, ALGO_REFINED_FUSED = 0, 1, 2, 3
 ARITH = {"3m": 0, "4m": 1}  # HSDLA_B200_ARITH_*: Gauss 3-multiplication / plain 4-multiplication complex
 FLAG_ARITH_4M = 1
 LEDGER_KEYS = ("gemm", "hemm", "her2k", "herk", "scaling", "herkx", "potrf", "trmm")

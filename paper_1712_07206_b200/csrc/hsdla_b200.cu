@@ -8,7 +8,15 @@
 //           T_AA A (hemm_loop, pipeline.cpp:314-321)
 //   X2      K x N_G: Z = T_AB^H A + 1/2 T_BB B (z_loop, pipeline.cpp:302-307)
 //   Tab     raw per-atom T_AB blocks (used as-is: Z = T_AB^H A is a CTN product)
-//   Pbb,Paa 1/2 full(T_BB), full(T_AA) expanded from the LOWER triangles only
+//   Pbb,Paa 1/2 full(T_BB) (full(T_BB) for the merged algorithm), full(T_AA) expanded
+//           from the LOWER triangles only
+//   Pab     T_AB^H per atom (merged algorithm: W_A = T_AA A + T_AB B)
+//
+// The merged algorithm (default) restates Algorithm 3 as one contraction per matrix:
+// per atom, H_a = Y_a^H M_a Y_a with Y_a = [A_a; B_a] and the Hermitian block operator
+// M_a = [[T_AA, T_AB], [T_AB^H, T_BB]] (the same sum pipeline.cpp:302-324 evaluates as
+// Z^H B + B^H Z + A^H (T_AA A)), so H = [A; B]^H [W_A; W_B] with W_A = T_AA A + T_AB B in
+// X1 and W_B = T_AB^H A + T_BB B in X2: 16 K N_G^2 contraction flops instead of 20.
 //   Hp, Sp  packed-lower N_G(N_G+1)/2 complex (halves D2H and NCCL bytes)
 //
 // A build is a list of atom CHUNKS.  The device-resident build is one chunk over
@@ -239,10 +247,11 @@ __global__ void fill_uniform_kernel(double* __restrict__ p, uint64_t n, uint64_t
 // conj(h(l,i)) for l > i).  The contraction computes P^H R, so
 //   P(k,i) = conj(T(i,k)) for k <= i,  T(k,i) for k > i
 // (= full(T) with the diagonal conjugated; identical for a real diagonal).
-//   Pbb[a] = 1/2 * P(T_BB[a]),  Paa[a] = P(T_AA[a])
+//   Pbb[a] = bscale * P(T_BB[a]),  Paa[a] = P(T_AA[a])  (bscale 1/2; 1 for the merged algorithm)
 __global__ void expand_hermitian_kernel(const double2* __restrict__ taa, const double2* __restrict__ tbb,
                                         double2* __restrict__ paa, double2* __restrict__ pbb, int nl,
-                                        uint64_t total) {
+                                        uint64_t total, double bscale, const double2* __restrict__ tab,
+                                        double2* __restrict__ pab) {
   const uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= total) return;
   const uint64_t blk = static_cast<uint64_t>(nl) * nl;
@@ -257,7 +266,15 @@ __global__ void expand_hermitian_kernel(const double2* __restrict__ taa, const d
     vbb.y = -vbb.y;
   }
   paa[idx] = vaa;
-  pbb[idx] = make_double2(0.5 * vbb.x, 0.5 * vbb.y);
+  // merged (pab != nullptr): B^H T_BB B stands for the reference's Z^H B + B^H Z share
+  // 1/2 B^H (T_BB + T_BB^H) B (hemm reads T_BB's diagonal as stored, kernels.cpp:152-167),
+  // i.e. T_BB with its diagonal's imaginary part dropped
+  if (pab && k == i) vbb.y = 0.0;
+  pbb[idx] = make_double2(bscale * vbb.x, bscale * vbb.y);
+  if (pab) {  // Pab[a](k, i) = conj(T_AB[a](i, k)): Pab^H B = T_AB B
+    const double2 v = tab[a * blk + i + static_cast<uint64_t>(k) * nl];
+    pab[idx] = make_double2(v.x, -v.y);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -336,7 +353,8 @@ struct ChunkPlan {
   uint64_t a0 = 0, a1 = 0;
   // s: S; z: Z -> X1 (refined/original); zf: Z -> X2 (fused); x: Q^H A -> X1;
   // h: fused her2k+herkx; h2k: her2k over X1; hkx: herkx A^H X1; haa: original X2^H X1
-  CtnParams s, z, zf, x, h, h2k, hkx, haa;
+  // merged: wa: W_A = T_AA A + T_AB B -> X1; wb: W_B = T_AB^H A + T_BB B -> X2; hm: [A;B]^H [X1;X2]
+  CtnParams s, z, zf, x, h, h2k, hkx, haa, wa, wb, hm;
   dim3 grid_tri, grid_bat;
 };
 
@@ -352,7 +370,7 @@ struct hsdla_b200_engine {
   uint64_t na = 0, nl = 0, ng = 0, K = 0, npk = 0;
   cudaStream_t stream = nullptr, copy_stream = nullptr, comm_stream = nullptr;
   double2 *A = nullptr, *B = nullptr, *X1 = nullptr, *X2 = nullptr;
-  double2 *Tab = nullptr, *Taa = nullptr, *Tbb = nullptr, *Paa = nullptr, *Pbb = nullptr;
+  double2 *Tab = nullptr, *Taa = nullptr, *Tbb = nullptr, *Paa = nullptr, *Pbb = nullptr, *Pab = nullptr;
   double* U = nullptr;
   int32_t* info = nullptr;        // per-atom potrf result of the original algorithm (-1 = HPD)
   int* n_fail = nullptr;          // original algorithm: failed atoms so far in this build
@@ -428,7 +446,7 @@ static void dalloc(hsdla_b200_engine* e, T** p, uint64_t count) {
 static void engine_free(hsdla_b200_engine* e) {
   cudaSetDevice(e->device);
   for (void* p : {e->lapw_scratch, (void*)e->info, (void*)e->n_fail, (void*)e->sk_ws, (void*)e->sk_flags, (void*)e->A, (void*)e->B, (void*)e->X1, (void*)e->X2,
-                  (void*)e->Tab, (void*)e->Taa, (void*)e->Tbb, (void*)e->Paa, (void*)e->Pbb, (void*)e->U,
+                  (void*)e->Tab, (void*)e->Taa, (void*)e->Tbb, (void*)e->Paa, (void*)e->Pbb, (void*)e->Pab, (void*)e->U,
                   (void*)e->Hp, (void*)e->Sp})
     if (p) cudaFree(p);
   if (e->host_stage) cudaFreeHost(e->host_stage);
@@ -516,6 +534,11 @@ static void make_chunk(hsdla_b200_engine* e, uint64_t a0, uint64_t a1, bool firs
   tri_base(cp.hkx, e->Hp, 1.0);
   set_seg(cp.hkx, 0, mA, mX1, Kc);
   cp.hkx.nseg = 1;
+  // merged H = A^H W_A + B^H W_B (W_A in X1, W_B in X2)
+  tri_base(cp.hm, e->Hp, beta0);
+  set_seg(cp.hm, 0, mA, mX1, Kc);
+  set_seg(cp.hm, 1, mB, mX2, Kc);
+  cp.hm.nseg = 2;
   // original h_aa_update: H += Lft^H W (Lft in X2, W = Q^H A in X1), always accumulates
   tri_base(cp.haa, e->Hp, 1.0);
   set_seg(cp.haa, 0, mX2, mX1, Kc);
@@ -528,10 +551,11 @@ static void make_chunk(hsdla_b200_engine* e, uint64_t a0, uint64_t a1, bool firs
   // batched per-atom products: operators {2nl, nl, nac} (row i in dim 1, atom in dim 2),
   // coefficient views {2nl, nac, ng} (atom in dim 1, G row in dim 2).
   const uint64_t blk = nl * nl;
-  CUtensorMap mTab, mPbb, mPaa, vA, vB;
+  CUtensorMap mTab, mPbb, mPaa, mPab, vA, vB;
   make_map(&mTab, e->Tab + a0 * blk, 2 * nl, nl, nac, 2 * nl, 2 * blk, kBatBM, 1);
   make_map(&mPbb, e->Pbb + a0 * blk, 2 * nl, nl, nac, 2 * nl, 2 * blk, kBatBM, 1);
   make_map(&mPaa, e->Paa + a0 * blk, 2 * nl, nl, nac, 2 * nl, 2 * blk, kBatBM, 1);
+  make_map(&mPab, e->Pab + a0 * blk, 2 * nl, nl, nac, 2 * nl, 2 * blk, kBatBM, 1);
   make_map(&vA, e->A + r0, 2 * nl, nac, ng, 2 * nl, 2 * K, 1, kBatBN);
   make_map(&vB, e->B + r0, 2 * nl, nac, ng, 2 * nl, 2 * K, 1, kBatBN);
   auto bat_base = [&](CtnParams& P, double2* out) {
@@ -562,6 +586,17 @@ static void make_chunk(hsdla_b200_engine* e, uint64_t a0, uint64_t a1, bool firs
   cp.x.kchunks[0] = chunks_of(nl);
   cp.x.r_row_z[0] = 1;
   cp.x.nseg = 1;
+  // merged: W_A = T_AA A_a + T_AB B_a -> X1, W_B = T_AB^H A_a + T_BB B_a -> X2
+  bat_base(cp.wa, e->X1 + r0);
+  cp.wa.L[0] = mPaa;
+  cp.wa.R[0] = vA;
+  cp.wa.L[1] = mPab;
+  cp.wa.R[1] = vB;
+  cp.wa.kchunks[0] = cp.wa.kchunks[1] = chunks_of(nl);
+  cp.wa.r_row_z[0] = cp.wa.r_row_z[1] = 1;
+  cp.wa.nseg = 2;
+  cp.wb = cp.z;  // T_AB^H A_a + Pbb^H B_a with Pbb = full(T_BB) in a merged build
+  cp.wb.out = x2 + r0;
   cp.grid_bat = dim3(static_cast<unsigned>((ng + kBatBN - 1) / kBatBN),
                      static_cast<unsigned>((nl + kBatBM - 1) / kBatBM), static_cast<unsigned>(nac));
 }
@@ -697,6 +732,7 @@ static hsdla_b200_engine* engine_create(int device, uint64_t na, uint64_t nl, ui
     dalloc(e.get(), &e->Tbb, na * nl * nl);
     dalloc(e.get(), &e->Paa, na * nl * nl);
     dalloc(e.get(), &e->Pbb, na * nl * nl);
+    dalloc(e.get(), &e->Pab, na * nl * nl);
     dalloc(e.get(), &e->U, e->K);
     dalloc(e.get(), &e->info, na);
     dalloc(e.get(), &e->n_fail, 1);
@@ -946,8 +982,10 @@ static void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool la
   auto expand = [&] {
     // operator expansion (lower triangles of T_AA, T_BB only) for this chunk's atoms
     const uint64_t total = nac * nl * nl, off = cp.a0 * nl * nl;
+    const bool merged = algo == HSDLA_B200_ALGO_REFINED_MERGED;
     expand_hermitian_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
-        e->Taa + off, e->Tbb + off, e->Paa + off, e->Pbb + off, static_cast<int>(nl), total);
+        e->Taa + off, e->Tbb + off, e->Paa + off, e->Pbb + off, static_cast<int>(nl), total, merged ? 1.0 : 0.5,
+        e->Tab + off, merged ? e->Pab + off : nullptr);
     HS_CUDA(cudaGetLastError());
     ++e->launches;
   };
@@ -1000,6 +1038,12 @@ static void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool la
     timed_op(e, HSDLA_B200_PHASE_HER2K, [&] { timed_h(cp.h2k, false); });
     timed_op(e, HSDLA_B200_PHASE_HEMM_LOOP, [&] { launch_bat(e, cp.x, cp.grid_bat); });
     timed_op(e, HSDLA_B200_PHASE_HERKX, [&] { final_h(cp.hkx); });
+  } else if (algo == HSDLA_B200_ALGO_REFINED_MERGED) {
+    timed_op(e, HSDLA_B200_PHASE_Z_LOOP, [&] {
+      launch_bat(e, cp.wa, cp.grid_bat);
+      launch_bat(e, cp.wb, cp.grid_bat);
+    });
+    timed_op(e, HSDLA_B200_PHASE_HER2K, [&] { timed_h(cp.hm, true); });  // her2k + herkx merged
   } else {
     timed_op(e, HSDLA_B200_PHASE_Z_LOOP, [&] { launch_bat(e, cp.zf, cp.grid_bat); });
     timed_op(e, HSDLA_B200_PHASE_HEMM_LOOP, [&] { launch_bat(e, cp.x, cp.grid_bat); });
@@ -1009,7 +1053,7 @@ static void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool la
 
 static bool valid_algo(int algo) {
   return algo == HSDLA_B200_ALGO_REFINED || algo == HSDLA_B200_ALGO_REFINED_FUSED ||
-         algo == HSDLA_B200_ALGO_ORIGINAL;
+         algo == HSDLA_B200_ALGO_REFINED_MERGED || algo == HSDLA_B200_ALGO_ORIGINAL;
 }
 
 static void begin_build(hsdla_b200_engine* e, int algo) {
@@ -1119,7 +1163,7 @@ static void engine_reduce(hsdla_b200_engine* e, int root) {
   reduce_finish(e);
 }
 
-static uint64_t executed_flops(uint64_t na, uint64_t nl, uint64_t ng, int arith);
+static uint64_t executed_flops(uint64_t na, uint64_t nl, uint64_t ng, int arith, int algo);
 
 static void engine_sync(hsdla_b200_engine* e, hsdla_b200_stats* st) {
   HS_CUDA(cudaSetDevice(e->device));
@@ -1142,7 +1186,7 @@ static void engine_sync(hsdla_b200_engine* e, hsdla_b200_stats* st) {
     e->n_hpd_last = e->na;
   }
   st->n_hpd = e->n_hpd_last;
-  st->executed_flops = executed_flops(e->na, e->nl, e->ng, e->arith);
+  st->executed_flops = executed_flops(e->na, e->nl, e->ng, e->arith, e->last_algo);
   for (const OpTime& op : e->ops) st->phase_seconds[op.phase] += ev_ms(op.b, op.e) * 1e-3;
   const cudaEvent_t last = e->reduced ? e->ev_reduce_end : e->ev_end;
   st->device_seconds = ev_ms(e->ev_begin, last) * 1e-3;
@@ -1633,13 +1677,16 @@ static void flop_model(int variant, uint64_t na, uint64_t nl, uint64_t ng, uint6
   for (int i = 0; i < 8; ++i) l[8] += l[i];
 }
 
-// Real flops the GPU executes for a build.  Every algorithm runs the same
-// lower-triangular contractions, 20 K N_G^2 + 24 N_A N_L^2 N_G complex-MAC flops at 8
-// per MAC (the original's trmm on the zero upper half of L and its full gemm fold are
-// executed as the lower-only h_aa contraction), plus 2 K N_G for diag_scale; the 3M
+// Real flops the GPU executes for a build.  The refined, fused and original algorithms
+// run lower-triangular contractions of 20 K N_G^2 + 24 N_A N_L^2 N_G complex-MAC flops at
+// 8 per MAC (the original's trmm on the zero upper half of L and its full gemm fold are
+// executed as the lower-only h_aa contraction); the merged one 16 K N_G^2 + 32 N_A N_L^2
+// N_G (two H segments, four per-atom products).  Plus 2 K N_G for diag_scale; the 3M
 // arithmetic executes 6 real flops per complex MAC.
-static uint64_t executed_flops(uint64_t na, uint64_t nl, uint64_t ng, int arith) {
-  const uint64_t K = na * nl, cmac8 = 20 * K * ng * ng + 24 * na * nl * nl * ng;
+static uint64_t executed_flops(uint64_t na, uint64_t nl, uint64_t ng, int arith, int algo) {
+  const uint64_t K = na * nl;
+  const uint64_t cmac8 = algo == HSDLA_B200_ALGO_REFINED_MERGED ? 16 * K * ng * ng + 32 * na * nl * nl * ng
+                                                                : 20 * K * ng * ng + 24 * na * nl * nl * ng;
   return (arith == HSDLA_B200_ARITH_3M ? cmac8 / 8 * 6 : cmac8) + 2 * K * ng;
 }
 
@@ -1649,7 +1696,7 @@ static uint64_t executed_flops(uint64_t na, uint64_t nl, uint64_t ng, int arith)
 template <class Start>
 static void one_shot(const hsdla_b200_options* o, uint64_t na, uint64_t nl, uint64_t ng, double* H, double* S,
                      hsdla_b200_stats* st, std::chrono::steady_clock::time_point t0, Start&& start) {
-  const int algo = o ? o->algo : HSDLA_B200_ALGO_REFINED_FUSED;
+  const int algo = o ? o->algo : HSDLA_B200_ALGO_REFINED_MERGED;
   if (!valid_algo(algo)) throw Fail{HSDLA_B200_CONFIG_ERROR, "unknown algo " + std::to_string(algo)};
   if (o && (o->flags & ~HSDLA_B200_FLAG_ARITH_4M)) throw Fail{HSDLA_B200_CONFIG_ERROR, "unknown option flags"};
   const int arith = o && (o->flags & HSDLA_B200_FLAG_ARITH_4M) ? HSDLA_B200_ARITH_4M : HSDLA_B200_ARITH_3M;
@@ -1737,7 +1784,7 @@ static void one_shot(const hsdla_b200_options* o, uint64_t na, uint64_t nl, uint
     st->d2h_seconds = d2h;
     // ledger == pipeline::flop_model(p, variant) with the potrf outcome of this build
     flop_model(algo == HSDLA_B200_ALGO_ORIGINAL ? 0 : 1, na, nl, ng, n_hpd, st->ledger);
-    st->executed_flops = executed_flops(na, nl, ng, arith);
+    st->executed_flops = executed_flops(na, nl, ng, arith, algo);
     st->n_hpd = n_hpd;
     st->peak_device_bytes = local.peak_device_bytes;
     st->peak_temp_bytes = local.peak_temp_bytes;

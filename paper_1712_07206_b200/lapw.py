@@ -153,7 +153,7 @@ Engine.upload_operators = _engine_upload_operators
 Engine.setup_time = _engine_setup_time
 
 
-def build_hs_lapw(sys_: LapwSystem, T_AA, T_AB, T_BB, algo="fused", device=0) -> HSResult:
+def build_hs_lapw(sys_: LapwSystem, T_AA, T_AB, T_BB, algo="merged", device=0) -> HSResult:
     """H and S of one k-point straight from the LAPW description: A, B, U are built in
     HBM by the setup kernel (never cross PCIe), T operators are uploaded, then the
     refined H/S build runs.  T_*: complex128 (N_L, N_L, n_atoms) Fortran order."""

@@ -19,7 +19,18 @@ from .errors import ConfigError, DimensionError, check
 
 VARIANTS = ("original", "refined")
 STRATEGIES = ("b200",)
-ALGOS = {"fused": _lib.ALGO_REFINED_FUSED, "refined": _lib.ALGO_REFINED, "original": _lib.ALGO_ORIGINAL}
+ALGOS = {"merged": _lib.ALGO_REFINED_MERGED, "fused": _lib.ALGO_REFINED_FUSED, "refined": _lib.ALGO_REFINED,
+         "original": _lib.ALGO_ORIGINAL}
+REFINED_ALGOS = ("merged", "fused", "refined")
+
+
+def _algo_warnings(algo):
+    if algo == "fused":
+        return ["herkx fused into the her2k contraction (phase time 0)"]
+    if algo == "merged":
+        return ["her2k, hemm_loop and herkx merged: z_loop builds W = M Y per atom, her2k is the one H "
+                "contraction [A;B]^H W (hemm_loop, herkx 0 s)"]
+    return []
 
 
 def parse_variant(s):
@@ -42,8 +53,9 @@ class PipelineConfig:
     strategy: str = "b200"
     n_gpus: int = 1
     device_ids: Optional[Sequence[int]] = None
-    # refined variant only: "fused" (her2k+herkx in one contraction) | "refined" (reference phase order)
-    algo: str = "fused"
+    # refined variant only: "merged" (default: H = [A;B]^H [W_A;W_B], 16 K N_G^2 contraction flops) |
+    # "fused" (her2k+herkx in one contraction over [Z;B;A], 20 K N_G^2) | "refined" (reference phase order)
+    algo: str = "merged"
     # complex arithmetic of the contractions: "3m" (Gauss, 6 executed flops per complex MAC,
     # the default) | "4m" (four real multiplications, plain FP64 rounding per product)
     arith: str = "3m"
@@ -118,7 +130,7 @@ def _phases(st, algo):
     return [PhaseTime(nm, float(st.phase_seconds[slot[nm]])) for nm in _phase_names(algo)]
 
 
-def stats_dict(st, algo="fused"):
+def stats_dict(st, algo="merged"):
     return {
         "phase_seconds": {ph.name: ph.seconds for ph in _phases(st, algo)}, "n_hpd": int(st.n_hpd),
         "h2d_seconds": st.h2d_seconds, "device_seconds": st.device_seconds, "reduce_seconds": st.reduce_seconds,
@@ -144,9 +156,7 @@ def _run(p, cfg, algo, H, S, what):
     st = _lib.Stats()
     check(_lib.lib().hsdla_b200_build_hs(C.byref(prob), C.byref(opts), H.ctypes.data_as(C.c_void_p),
                                          S.ctypes.data_as(C.c_void_p), C.byref(st)), what)
-    warnings = []
-    if algo == "fused":
-        warnings.append("herkx fused into the her2k contraction (phase time 0)")
+    warnings = _algo_warnings(algo)
     return HSResult(H, S, FlopLedger.from_array(st.ledger), int(st.peak_temp_bytes), _phases(st, algo), warnings,
                     stats_dict(st, algo))
 
@@ -158,7 +168,7 @@ def build_hs_refined(p, cfg: Optional[PipelineConfig] = None, H=None, S=None) ->
     cfg = cfg or PipelineConfig()
     if parse_variant(cfg.variant) != "refined":
         raise ConfigError("build_hs_refined needs variant 'refined' (use build_hs / build_hs_original)")
-    if cfg.algo not in ("fused", "refined"):
+    if cfg.algo not in REFINED_ALGOS:
         raise ConfigError(f"unknown algo: {cfg.algo}")
     return _run(p, cfg, cfg.algo, H, S, "build_hs_refined")
 
@@ -205,7 +215,7 @@ def build_hs_file(path, cfg: Optional[PipelineConfig] = None, H=None, S=None) ->
     st = _lib.Stats()
     check(_lib.lib().hsdla_b200_build_hs_file(os.fsencode(path), C.byref(opts), H.ctypes.data_as(C.c_void_p),
                                               S.ctypes.data_as(C.c_void_p), C.byref(st)), "build_hs_file")
-    warnings = ["herkx fused into the her2k contraction (phase time 0)"] if algo == "fused" else []
+    warnings = _algo_warnings(algo)
     return HSResult(H, S, FlopLedger.from_array(st.ledger), int(st.peak_temp_bytes), _phases(st, algo), warnings,
                     stats_dict(st, algo))
 
@@ -306,11 +316,11 @@ class Engine:
         """Stream this shard of an HSDL v1 file into the engine (hsdla_b200_engine_load)."""
         check(_lib.lib().hsdla_b200_engine_load(self.h, os.fsencode(path), C.c_uint64(atom_begin)), "engine_load")
 
-    def build(self, algo="fused"):
+    def build(self, algo="merged"):
         self._algo = algo
         check(_lib.lib().hsdla_b200_engine_build(self.h, C.c_int(ALGOS[algo])), "engine_build")
 
-    def build_streamed(self, p, atom_begin=0, algo="fused"):
+    def build_streamed(self, p, atom_begin=0, algo="merged"):
         """Upload shard `atom_begin` of host problem p in atom chunks overlapped with the build."""
         self._prob = p.c_struct()  # keep the struct alive while the copies are in flight
         self._algo = algo
@@ -323,7 +333,7 @@ class Engine:
     def sync(self):
         st = _lib.Stats()
         check(_lib.lib().hsdla_b200_engine_sync(self.h, C.byref(st)), "engine_sync")
-        return stats_dict(st, getattr(self, "_algo", "fused"))
+        return stats_dict(st, getattr(self, "_algo", "merged"))
 
     def download(self, H=None, S=None):
         n = self.n_g

@@ -26,7 +26,8 @@ def _need_gpu():
     hb.release_cache()
 
 
-@pytest.mark.parametrize("algo,arith", [("fused", "3m"), ("refined", "3m"), ("fused", "4m"), ("refined", "4m")])
+@pytest.mark.parametrize("algo,arith", [("merged", "3m"), ("fused", "3m"), ("refined", "3m"), ("merged", "4m"),
+                                       ("fused", "4m"), ("refined", "4m")])
 @pytest.mark.parametrize("path", golden_cases(), ids=lambda p: p.split("/")[-1][:-4])
 def test_golden_parity(path, algo, arith):
     dims, d = load_case(path)
@@ -177,11 +178,18 @@ def test_algos_agree():
     p = hb.generate_problem(7, 49, 515, 2, 0)
     a = hb.build_hs_refined(p, hb.PipelineConfig(algo="fused"))
     b = hb.build_hs_refined(p, hb.PipelineConfig(algo="refined"))
+    m = hb.build_hs_refined(p, hb.PipelineConfig(algo="merged"))
     assert rel(a.H, b.H) <= 1e-13 and rel(a.S, b.S) == 0.0
+    assert rel(m.H, b.H) <= 1e-13 and rel(m.S, b.S) == 0.0
     assert a.stats["kernel_launches"] >= 5
+    # merged: 16 K N_G^2 + 32 N_A N_L^2 N_G complex-MAC flops (3M: 6 per MAC) + 2 K N_G
+    K = p.n_atoms * p.n_l
+    assert m.stats["executed_flops"] == (16 * K * p.n_g ** 2 + 32 * p.n_atoms * p.n_l ** 2 * p.n_g) // 8 * 6 + \
+        2 * K * p.n_g
+    assert m.ledger.total() == a.ledger.total()
 
 
-@pytest.mark.parametrize("algo", ["fused", "refined", "original"])
+@pytest.mark.parametrize("algo", ["merged", "fused", "refined", "original"])
 def test_banded_final_h_matches_device_resident(algo):
     """The one-shot drop-in runs its final H contraction in tile-column bands (each band's
     download overlapping the next band); the device-resident engine runs it whole.
@@ -199,8 +207,8 @@ def test_banded_final_h_matches_device_resident(algo):
         assert rel(r.H, H) <= 1e-14 and rel(r.S, S) <= 1e-14, dims
 
 
-@pytest.mark.parametrize("variant", ["refined", "original"])
-def test_operators_with_complex_diagonals_follow_reference_hemm(restatement, variant):
+@pytest.mark.parametrize("algo", ["merged", "fused", "refined", "original"])
+def test_operators_with_complex_diagonals_follow_reference_hemm(restatement, algo):
     """The reference's hemm uses T's diagonal as stored (kernels.cpp:152-167), also a
     non-real one; the device operand expansion reproduces that exactly."""
     p = hb.generate_problem(5, 9, 60, 8, 2)
@@ -208,16 +216,16 @@ def test_operators_with_complex_diagonals_follow_reference_hemm(restatement, var
     for T in (p.T_AA, p.T_BB):
         for a in range(p.n_atoms):
             T[np.arange(p.n_l), np.arange(p.n_l), a] += 1j * g.uniform(-0.5, 0.5, p.n_l)
-    if variant == "original":
+    if algo == "original":
         H, S, _, _ = restatement.build_hs_original(p)
         r = hb.build_hs_original(p)
     else:
         H, S, _ = restatement.build_hs_refined(p)
-        r = hb.build_hs_refined(p)
+        r = hb.build_hs_refined(p, hb.PipelineConfig(algo=algo))
     assert rel(r.H, H) <= TOL and rel(r.S, S) <= TOL
 
 
-@pytest.mark.parametrize("algo", ["fused", "original"])
+@pytest.mark.parametrize("algo", ["merged", "fused", "original"])
 def test_nccl_reduce_path_single_rank(restatement, algo):
     """The multi-GPU reduce path (comm stream, S reduce overlapping H, ncclReduce of the
     packed triangles, download ordered after the reduce) through a real 1-rank NCCL
@@ -280,7 +288,7 @@ def test_bitwise_determinism_stress():
         return torch.as_tensor(_A(), device="cuda")
 
     th, ts = as_tensor(Hp), as_tensor(Sp)
-    for algo in ("fused", "refined", "original"):
+    for algo in ("merged", "fused", "refined", "original"):
         e.build(algo)
         e.sync()
         h0, s0 = th.clone(), ts.clone()
@@ -329,17 +337,21 @@ def test_arith_modes_agree_and_account(restatement):
     identical (the reference's flop model counts 8 real flops per complex MAC)."""
     p = hb.generate_problem(16, 49, 600, 2, 3)
     H, S, _ = restatement.build_hs_refined(p)
-    res = {}
-    for arith in ("3m", "4m"):
-        a = hb.build_hs_refined(p, hb.PipelineConfig(arith=arith))
-        b = hb.build_hs_refined(p, hb.PipelineConfig(arith=arith))
-        assert np.array_equal(a.H, b.H) and np.array_equal(a.S, b.S)
-        assert rel(a.H, H) <= 1e-13 and rel(a.S, S) <= 1e-13, (arith, rel(a.H, H), rel(a.S, S))
-        res[arith] = a
-    assert res["3m"].ledger == res["4m"].ledger == hb.flop_model(p)
     K, ng = p.n_atoms * p.n_l, p.n_g
-    cmac = 20 * K * ng * ng + 24 * p.n_atoms * p.n_l ** 2 * ng
-    assert res["4m"].stats["executed_flops"] == cmac + 2 * K * ng
-    assert res["3m"].stats["executed_flops"] == cmac // 8 * 6 + 2 * K * ng
+    for algo in ("merged", "fused"):
+        res = {}
+        for arith in ("3m", "4m"):
+            a = hb.build_hs_refined(p, hb.PipelineConfig(algo=algo, arith=arith))
+            b = hb.build_hs_refined(p, hb.PipelineConfig(algo=algo, arith=arith))
+            assert np.array_equal(a.H, b.H) and np.array_equal(a.S, b.S)
+            assert rel(a.H, H) <= 1e-13 and rel(a.S, S) <= 1e-13, (algo, arith, rel(a.H, H), rel(a.S, S))
+            res[arith] = a
+        assert res["3m"].ledger == res["4m"].ledger == hb.flop_model(p)
+        if algo == "merged":
+            cmac = 16 * K * ng * ng + 32 * p.n_atoms * p.n_l ** 2 * ng
+        else:
+            cmac = 20 * K * ng * ng + 24 * p.n_atoms * p.n_l ** 2 * ng
+        assert res["4m"].stats["executed_flops"] == cmac + 2 * K * ng
+        assert res["3m"].stats["executed_flops"] == cmac // 8 * 6 + 2 * K * ng
     with pytest.raises(hb.ConfigError):
         hb.build_hs_refined(p, hb.PipelineConfig(arith="2m"))

@@ -12,7 +12,7 @@ CFG = {"c1": (16, 49, 1000), "c2": (64, 81, 3000), "c3": (108, 121, 6000),
 ap = argparse.ArgumentParser()
 ap.add_argument("config", nargs="?", default="c2")
 ap.add_argument("--builds", type=int, default=3)
-ap.add_argument("--algo", default="fused")
+ap.add_argument("--algo", default="merged")
 ap.add_argument("--lapw", action="store_true")
 a = ap.parse_args()
 na, nl, ng = CFG[a.config]

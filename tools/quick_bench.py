@@ -16,7 +16,7 @@ for name in sys.argv[1:] or ["c2", "c3"]:
     e = hb.Engine(0, na, nl, ng)
     e.upload(p)
     led_r = hb.flop_model(p).total()
-    for algo in ("fused", "refined", "original"):
+    for algo in ("merged", "fused", "refined", "original"):
         for it in range(4):
             e.build(algo)
             st = e.sync()

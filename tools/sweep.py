@@ -34,7 +34,7 @@ def points(only):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--algo", default="fused", choices=["fused", "refined", "original"])
+    ap.add_argument("--algo", default="merged", choices=["merged", "fused", "refined", "original"])
     ap.add_argument("--arith", default="3m", choices=["3m", "4m"])
     ap.add_argument("--out", default="gpurun_out/sweep.jsonl")
     ap.add_argument("--only", default="")
@@ -62,8 +62,8 @@ def main():
             rec = {"point": name, "n_atoms": na, "n_l": nl, "n_g": ng, "algo": args.algo, "builds": n,
                    "build_ms": t * 1e3, "min_ms": min(dev) * 1e3, "ledger_flops": led,
                    "tflops": led / t / 1e12, "ledger_frac_of_dmma_peak": led / t / 1e12 / peak, "dmma_peak_tflops": peak,
-                   "arith": args.arith, "executed_tflops": bench.executed_flops(na, nl, ng, args.arith) / t / 1e12,
-                   "executed_frac_of_dmma_peak": bench.executed_flops(na, nl, ng, args.arith) / t / 1e12 / peak,
+                   "arith": args.arith, "executed_tflops": bench.executed_flops(na, nl, ng, args.arith, args.algo) / t / 1e12,
+                   "executed_frac_of_dmma_peak": bench.executed_flops(na, nl, ng, args.arith, args.algo) / t / 1e12 / peak,
                    "s_kernel_tflops": kt["s_flops"] / kt["s_ms"] / 1e9 if kt["s_ms"] else None,
                    "h_kernel_tflops": kt["h_flops"] / kt["h_ms"] / 1e9 if kt["h_ms"] else None,
                    "phase_ms": {k: v * 1e3 for k, v in st["phase_seconds"].items()},
