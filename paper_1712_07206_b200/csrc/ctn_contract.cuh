@@ -9,7 +9,8 @@
 //     herkx_cols :137-150).  Tiles enumerate the t(t+1)/2 lower tiles
 //     (the idea of hybrid_dynamic.cpp:54-112), the strict upper triangle is never
 //     touched and diagonal imaginary parts are forced to 0 (kernels.cpp:112).
-//   * BATCH mode: per-atom rectangular products Z_a = T_AB^H A_a + 1/2 T_BB B_a and
+//   * BATCH mode (persistent: CTAs loop over column x row x atom tiles, so the next
+//     tile's TMA loads overlap the current tile's epilogue): per-atom rectangular products Z_a = T_AB^H A_a + 1/2 T_BB B_a and
 //     X_a = T_AA A_a (compute_z pipeline.cpp:176-185 and the hemm_loop
 //     :314-321) written straight into the stacked K x N_G buffers.
 //
@@ -59,6 +60,8 @@ struct alignas(64) CtnParams {
   uint32_t* sk_flags;      // TRI stream-K: per-CTA publish flags (== epoch when the slot is ready)
   uint32_t epoch;          // TRI stream-K: unique per launch
   uint64_t ldo;            // BATCH: output leading dimension (complex elements)
+  int bat_tx, bat_ty;      // BATCH: column tiles, row tiles per atom
+  int bat_tiles;           // BATCH: bat_tx * bat_ty * atoms (persistent CTAs loop over them)
   const int* keep_diag_imag;  // TRI, optional: when non-null and *keep_diag_imag != 0 the diagonal's
                               // imaginary part is kept (the original algorithm's full-gemm fold,
                               // pipeline.cpp:266-271, does not zero it); else forced to 0
@@ -195,7 +198,7 @@ struct CtnCfg {
 };
 
 // ---------------------------------------------------------------------------
-// Work decomposition.  BATCH: one whole tile per CTA (grid = tiles x atoms).
+// Work decomposition.  BATCH: persistent CTAs, whole tiles blockIdx.x, +gridDim.x, ...
 // TRI: persistent CTAs (grid = #SMs) with a data-parallel + stream-K split:
 // all full waves but the last are whole tiles (tile b, b+G, ...); the remaining
 // tiles' k-iterations are divided evenly over the G CTAs, so the last wave has no
@@ -305,9 +308,11 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES,
       col0 = tj * BN;
       atom = 0;
     } else {
-      col0 = blockIdx.x * BN;
-      row0 = blockIdx.y * BM;
-      atom = blockIdx.z;
+      // persistent BATCH: tile = (column tile fastest, then row tile, then atom)
+      const int tx = tile % P.bat_tx, rest = tile / P.bat_tx;
+      col0 = tx * BN;
+      row0 = (rest % P.bat_ty) * BM;
+      atom = rest / P.bat_ty;
     }
   };
 
@@ -322,8 +327,9 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES,
       }
       TriSched sched(P.tiles_total, iters, gridDim.x, blockIdx.x);
       Piece pc;
-      bool have = MODE == kTri ? sched.next(pc) : true;
-      if (MODE != kTri) pc = Piece{0, 0, iters, 0};
+      int bt = blockIdx.x;  // BATCH: tiles blockIdx.x, + gridDim.x, ...
+      bool have = MODE == kTri ? sched.next(pc) : bt < P.bat_tiles;
+      if (MODE != kTri) pc = Piece{bt, 0, iters, 0};
       int it = 0;
       while (have) {
         int row0, col0, atom;
@@ -354,7 +360,13 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES,
             ++kc;
           }
         }
-        have = MODE == kTri ? sched.next(pc) : false;
+        if (MODE == kTri) {
+          have = sched.next(pc);
+        } else {
+          bt += gridDim.x;
+          have = bt < P.bat_tiles;
+          pc = Piece{bt, 0, iters, 0};
+        }
       }
     }
     return;
@@ -379,8 +391,9 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES,
 
   TriSched sched(P.tiles_total, iters, gridDim.x, blockIdx.x);
   Piece pc;
-  bool have = MODE == kTri ? sched.next(pc) : true;
-  if (MODE != kTri) pc = Piece{0, 0, iters, 0};
+  int bt = blockIdx.x;
+  bool have = MODE == kTri ? sched.next(pc) : bt < P.bat_tiles;
+  if (MODE != kTri) pc = Piece{bt, 0, iters, 0};
   int it = 0;
   while (have) {
     double acc[MB][NB][2][NS];  // [mb][nb][e][re, im] or [t1, t2, t3]
@@ -593,7 +606,13 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES,
         }
       }
     }
-    have = MODE == kTri ? sched.next(pc) : false;
+    if (MODE == kTri) {
+      have = sched.next(pc);
+    } else {
+      bt += gridDim.x;
+      have = bt < P.bat_tiles;
+      pc = Piece{bt, 0, iters, 0};
+    }
   }
 }
 

@@ -558,6 +558,9 @@ static void make_chunk(hsdla_b200_engine* e, uint64_t a0, uint64_t a1, bool firs
   make_map(&mPab, e->Pab + a0 * blk, 2 * nl, nl, nac, 2 * nl, 2 * blk, kBatBM, 1);
   make_map(&vA, e->A + r0, 2 * nl, nac, ng, 2 * nl, 2 * K, 1, kBatBN);
   make_map(&vB, e->B + r0, 2 * nl, nac, ng, 2 * nl, 2 * K, 1, kBatBN);
+  const int bat_tx = static_cast<int>((ng + kBatBN - 1) / kBatBN), bat_ty = static_cast<int>((nl + kBatBM - 1) / kBatBM);
+  const uint64_t bat_tiles = static_cast<uint64_t>(bat_tx) * bat_ty * nac;
+  if (bat_tiles > static_cast<uint64_t>(INT32_MAX)) throw Fail{HSDLA_B200_SIZING_ERROR, "too many batched tiles"};
   auto bat_base = [&](CtnParams& P, double2* out) {
     std::memset(&P, 0, sizeof(P));
     P.n = static_cast<int>(ng);
@@ -565,6 +568,9 @@ static void make_chunk(hsdla_b200_engine* e, uint64_t a0, uint64_t a1, bool firs
     P.out = out;
     P.ldo = K;
     P.alpha_re = 1.0;
+    P.bat_tx = bat_tx;
+    P.bat_ty = bat_ty;
+    P.bat_tiles = static_cast<int>(bat_tiles);
   };
   // Z_a = T_AB^H A_a + (1/2 T_BB) B_a   (compute_z, pipeline.cpp:176-185): into X1
   // (refined / original) or X2 (fused, where X1 still holds T_AA A for the same launch)
@@ -597,8 +603,8 @@ static void make_chunk(hsdla_b200_engine* e, uint64_t a0, uint64_t a1, bool firs
   cp.wa.nseg = 2;
   cp.wb = cp.z;  // T_AB^H A_a + Pbb^H B_a with Pbb = full(T_BB) in a merged build
   cp.wb.out = x2 + r0;
-  cp.grid_bat = dim3(static_cast<unsigned>((ng + kBatBN - 1) / kBatBN),
-                     static_cast<unsigned>((nl + kBatBM - 1) / kBatBM), static_cast<unsigned>(nac));
+  // persistent: one CTA per SM (the 384-thread CTA holds the whole register file)
+  cp.grid_bat = dim3(static_cast<unsigned>(std::min<uint64_t>(bat_tiles, e->sms)));
 }
 
 // Streamed chunking for the host-buffer drop-in: whole-atom chunks growing
@@ -2058,8 +2064,12 @@ static void rect(Ctx& x, const double2* L, const double2* R, uint64_t m, uint64_
   P.alpha_re = ar;
   P.alpha_im = ai;
   P.beta = beta;
-  const dim3 g(static_cast<unsigned>((n + kBatBN - 1) / kBatBN), static_cast<unsigned>((m + kBatBM - 1) / kBatBM), 1);
-  if (g.y > 65535) throw Fail{HSDLA_B200_SIZING_ERROR, "rows exceed the batched-contraction grid"};
+  const uint64_t tx = (n + kBatBN - 1) / kBatBN, ty = (m + kBatBM - 1) / kBatBM;
+  if (tx * ty > static_cast<uint64_t>(INT32_MAX)) throw Fail{HSDLA_B200_SIZING_ERROR, "too many batched tiles"};
+  P.bat_tx = static_cast<int>(tx);
+  P.bat_ty = static_cast<int>(ty);
+  P.bat_tiles = static_cast<int>(tx * ty);
+  const dim3 g(static_cast<unsigned>(std::min<uint64_t>(tx * ty, x.sms)));
   bat_kernels[x.arith]<<<g, BatCfg::kThreads, BatCfg::kSmemBytes, x.s>>>(P);
   HS_CUDA(cudaGetLastError());
 }
