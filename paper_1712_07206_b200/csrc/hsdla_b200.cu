@@ -612,11 +612,12 @@ static void make_chunk(hsdla_b200_engine* e, uint64_t a0, uint64_t a1, bool firs
 // (larger) uploads still finish before the previous chunk's phases do.  The growth
 // factor follows rho, the compute/upload time ratio of one atom:
 //   rho = (20 K N_G^2 / 34 TF/s) / (32 K N_G B / rate) = N_G * rate * 1.84e-14,
-// r = clamp(0.8 rho, 1, 4); the first chunk is the larger of N_A/32 and the head of an
+// r = clamp(0.8 rho, 1, 4); the first chunk is the larger of N_A/16 and the head of an
 // 8-term geometric series summing to N_A; at most 8 chunks.  (The 34 TF/s is the 4M
-// rate; calibrating it to 3M's faster compute gives more, smaller chunks, and every
-// extra chunk costs ~0.2 ms at C2 in per-launch epilogues and ramps: tools/stream_tune.py
-// measured N_A/32 with the 4M constant best, 24.5 ms per call against 24.6-25.1.)  `rate` is the host->device
+// fused rate; calibrating it to the merged 3M build's faster compute gives more,
+// smaller chunks, and every extra chunk costs ~0.2 ms at C2 in per-launch epilogues and
+// ramps: tools/stream_tune.py measured N_A/16 with this constant best for the merged
+// build, 20.5 ms per call at C2 against 20.8-23.8 for the other settings; C3 is flat.)  `rate` is the host->device
 // feed: ~50 GB/s for page-locked inputs (PCIe), ~20 GB/s for pageable inputs packed by
 // host threads or for page-cached HSDL files.  Small problems (< 64 MB of A+B): one chunk.
 // Development knobs for the streaming / banding heuristics (tools/stream_tune.py).
@@ -634,7 +635,7 @@ static std::vector<uint64_t> stream_bounds(uint64_t na, uint64_t nl, uint64_t ng
   const double rho = static_cast<double>(ng) * rate * env_double("HSDLA_B200_STREAM_C", 1.84e-14);
   const double r = std::min(4.0, std::max(1.0, 0.8 * rho));
   const double head = r > 1.0001 ? (r - 1.0) / (std::pow(r, 8.0) - 1.0) : 1.0 / 8.0;
-  double size = std::max(1.0, static_cast<double>(na) * std::max(env_double("HSDLA_B200_STREAM_FLOOR", 1.0 / 32.0), head));
+  double size = std::max(1.0, static_cast<double>(na) * std::max(env_double("HSDLA_B200_STREAM_FLOOR", 1.0 / 16.0), head));
   while (b.back() < na) {
     const uint64_t left = na - b.back();
     uint64_t take = std::min<uint64_t>(left, static_cast<uint64_t>(std::llround(size)));
