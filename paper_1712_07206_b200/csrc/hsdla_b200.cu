@@ -1811,14 +1811,30 @@ static void one_shot(const hsdla_b200_options* o, uint64_t na, uint64_t nl, uint
 // ---------------------------------------------------------------------------
 namespace kl {
 
+// Per-call device temporaries of the kernel layer, stream-ordered from the device's
+// default memory pool with an unbounded release threshold: repeated calls reuse the
+// cached blocks instead of paying cudaMalloc / cudaFree (a device-wide sync) every call.
+// hsdla_b200_release_cache() trims the pool.
+static void keep_pool_cached(int device) {
+  static std::once_flag once[64];
+  std::call_once(once[device & 63], [device] {
+    cudaMemPool_t pool;
+    HS_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = UINT64_MAX;
+    HS_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  });
+}
 struct DevBuf {
   void* p = nullptr;
+  cudaStream_t s = nullptr;
   DevBuf() = default;
-  explicit DevBuf(size_t bytes) { HS_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16))); }
+  DevBuf(size_t bytes, cudaStream_t stream) : s(stream) {
+    HS_CUDA(cudaMallocAsync(&p, std::max<size_t>(bytes, 16), s));
+  }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, s);
   }
   double2* c() const { return static_cast<double2*>(p); }
 };
@@ -1910,6 +1926,7 @@ struct Ctx {
     HS_CUDA(cudaSetDevice(device));
     HS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     set_kernel_attributes();
+    keep_pool_cached(device);
     arith = g_default_arith.load();
     HS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     ring = &ring_for(device);
@@ -2033,7 +2050,7 @@ static void tri(Ctx& x, int nseg, const double2* const* L, const double2* const*
   P.tiles_total = tiles * (tiles + 1) / 2;
   P.band = tri_band();
   P.out = Cp;
-  DevBuf ws(static_cast<size_t>(x.sms) * kSkSlot * sizeof(double)), flags(x.sms * sizeof(uint32_t));
+  DevBuf ws(static_cast<size_t>(x.sms) * kSkSlot * sizeof(double), x.s), flags(x.sms * sizeof(uint32_t), x.s);
   HS_CUDA(cudaMemsetAsync(flags.p, 0, x.sms * sizeof(uint32_t), x.s));
   P.sk_ws = static_cast<double*>(ws.p);
   P.sk_flags = static_cast<uint32_t*>(flags.p);
@@ -2084,7 +2101,7 @@ static void tri_family(int device, int which, uint64_t n, uint64_t k, double ar,
   if (n == 0) return;
   Ctx x(device);
   const uint64_t npk = n * (n + 1) / 2;
-  DevBuf dC(n * n * 16), dP(npk * 16);
+  DevBuf dC(n * n * 16, x.s), dP(npk * 16, x.s);
   const bool alpha0 = (ar == 0.0 && ai == 0.0) || k == 0;
   if (beta != 0.0 || alpha0) x.up(dC.c(), C, n, n, ldc);
   if (alpha0) {  // scale_lower_in_place (kernels.cpp:209-217): only C's lower triangle
@@ -2092,7 +2109,7 @@ static void tri_family(int device, int which, uint64_t n, uint64_t k, double ar,
     pack_lower_kernel<<<x.grid(n * n), 256, 0, x.s>>>(dC.c(), dP.c(), n, 0);
   } else {
     if (beta != 0.0) pack_lower_kernel<<<x.grid(n * n), 256, 0, x.s>>>(dC.c(), dP.c(), n, 0);
-    DevBuf dA(k * n * 16), dB(which != 0 ? k * n * 16 : 16);
+    DevBuf dA(k * n * 16, x.s), dB(which != 0 ? k * n * 16 : 16, x.s);
     x.up(dA.c(), A, k, n, lda);
     if (which != 0) x.up(dB.c(), B, k, n, ldb);
     if (which == 0) {
@@ -2214,6 +2231,24 @@ int hsdla_b200_release_cache(void) {
   return guarded([&] {
     std::lock_guard<std::mutex> lk(g_cache_mu);
     g_cache.clear();
+    // the kernel layer's cached temporaries (keep_pool_cached)
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess) {
+      (void)cudaGetLastError();
+      return;
+    }
+    for (int d = 0; d < ndev; ++d) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) {
+        int cur = 0;
+        (void)cudaGetDevice(&cur);
+        (void)cudaSetDevice(d);
+        (void)cudaDeviceSynchronize();
+        (void)cudaMemPoolTrimTo(pool, 0);
+        (void)cudaSetDevice(cur);
+      }
+    }
+    (void)cudaGetLastError();
   });
 }
 
@@ -2498,7 +2533,8 @@ int hsdla_b200_gemm(int device, int trans_a, int trans_b, uint64_t m, uint64_t n
     kl::need(C && ldc >= std::max<uint64_t>(m, 1), "C: null or ldc < m");
     if (m && n) {
       kl::Ctx x(device);
-      kl::DevBuf dA(ar * ac * 16), dB(br * bc * 16), dL(k * m * 16), dR(k * n * 16), dC(m * n * 16);
+      kl::DevBuf dA(ar * ac * 16, x.s), dB(br * bc * 16, x.s), dL(k * m * 16, x.s), dR(k * n * 16, x.s),
+          dC(m * n * 16, x.s);
       x.up(dA.c(), A, ar, ac, lda);
       x.up(dB.c(), B, br, bc, ldb);
       if (beta[0] != 0.0 || beta[1] != 0.0) x.up(dC.c(), C, m, n, ldc);
@@ -2532,7 +2568,7 @@ int hsdla_b200_hemm(int device, uint64_t n, uint64_t m, const double* alpha, con
     kl::need(C && ldc >= std::max<uint64_t>(n, 1), "C: null or ldc < n");
     if (n && m) {
       kl::Ctx x(device);
-      kl::DevBuf dH(n * n * 16), dF(n * n * 16), dB(n * m * 16), dC(n * m * 16);
+      kl::DevBuf dH(n * n * 16, x.s), dF(n * n * 16, x.s), dB(n * m * 16, x.s), dC(n * m * 16, x.s);
       x.up(dH.c(), Hm, n, n, ldh);
       x.up(dB.c(), B, n, m, ldb);
       if (beta[0] != 0.0 || beta[1] != 0.0) x.up(dC.c(), C, n, m, ldc);
@@ -2556,7 +2592,7 @@ int hsdla_b200_trmm(int device, int trans, uint64_t n, uint64_t m, const double*
     kl::need(B && ldb >= std::max<uint64_t>(n, 1), "B: null or ldb < n");
     if (n && m) {
       kl::Ctx x(device);
-      kl::DevBuf dT(n * n * 16), dL(n * n * 16), dB(n * m * 16), dC(n * m * 16);
+      kl::DevBuf dT(n * n * 16, x.s), dL(n * n * 16, x.s), dB(n * m * 16, x.s), dC(n * m * 16, x.s);
       x.up(dT.c(), T, n, n, ldt);
       x.up(dB.c(), B, n, m, ldb);
       // op(T) B = L^H B with L = lower(T) (ConjTrans) or L = lower(T)^H (None)
@@ -2577,7 +2613,7 @@ int hsdla_b200_diag_scale(int device, uint64_t rows, uint64_t cols, const double
              "diag_scale: null pointer or leading dimension < rows");
     if (rows && cols) {
       kl::Ctx x(device);
-      kl::DevBuf dB(rows * cols * 16), dX(rows * cols * 16), du(rows * 8);
+      kl::DevBuf dB(rows * cols * 16, x.s), dX(rows * cols * 16, x.s), du(rows * 8, x.s);
       x.up(dB.c(), B, rows, cols, ldb);
       HS_CUDA(cudaMemcpyAsync(du.p, u, rows * 8, cudaMemcpyHostToDevice, x.s));
       const dim3 g(static_cast<unsigned>((rows + 255) / 256), static_cast<unsigned>(std::min<uint64_t>(cols, 2048)));

@@ -1,6 +1,6 @@
 """Small, fixed workload for ncu captures (development helper): `builds` device-resident
-fused builds of a config, or `--lapw` setup passes.  Launch order per build: S (TRI),
-Z (BATCH), X (BATCH), H (TRI) contraction kernels (plus expand / diag_scale)."""
+builds of a config (default algo merged), or `--lapw` setup passes.  Launch order per
+merged build: expand, diag_scale, S (TRI), W_A (BATCH), W_B (BATCH), H (TRI)."""
 import argparse
 import sys
 
