@@ -628,6 +628,16 @@ static double env_double(const char* name, double dflt) {
 
 static std::vector<uint64_t> stream_bounds(uint64_t na, uint64_t nl, uint64_t ng, double rate) {
   std::vector<uint64_t> b{0};
+  if (const char* plan = std::getenv("HSDLA_B200_STREAM_PLAN")) {  // explicit chunk sizes "4,9,19" (tuning)
+    for (const char* c = plan; *c && b.back() < na;) {
+      const uint64_t take = std::strtoull(c, const_cast<char**>(&c), 10);
+      if (take == 0) break;
+      b.push_back(std::min(na, b.back() + take));
+      while (*c == ',') ++c;
+    }
+    if (b.back() < na) b.push_back(na);
+    return b;
+  }
   if (na * nl * ng < (uint64_t(1) << 22) || na < 2) {
     b.push_back(na);
     return b;
@@ -1250,16 +1260,36 @@ static void enqueue_download(hsdla_b200_engine* e) {
   }
 }
 
+// HSDLA_B200_TRACE=1: host timestamps of the drop-in's download phase on stderr (tuning).
+static bool trace_on() {
+  static const bool on = [] {
+    const char* v = std::getenv("HSDLA_B200_TRACE");
+    return v && *v == '1';
+  }();
+  return on;
+}
+
 // Unpack S as soon as its bytes land (H may still be computing), then H.
-static void finish_download(hsdla_b200_engine* e, double* H, double* S) {
+static void finish_download(hsdla_b200_engine* e, double* H, double* S,
+                            std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now()) {
+  auto ms = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); };
+  std::string tr;
+  auto mark = [&](const char* what) {
+    if (trace_on()) tr += std::string(" ") + what + "=" + std::to_string(ms()).substr(0, 6);
+  };
   HS_CUDA(cudaEventSynchronize(e->ev_s_d2h));
+  mark("s_landed");
   if (S) unpack_lower(e->host_stage + e->npk, reinterpret_cast<double2*>(S), e->ng, 0, e->ng);
+  mark("s_unpacked");
   // H: unpack piece q while piece q+1 is still on the wire
   for (int q = 0; q < hsdla_b200_engine::kD2hPieces; ++q) {
     HS_CUDA(cudaEventSynchronize(e->ev_h_piece[q]));
+    mark("h_landed");
     if (H)
       unpack_lower(e->host_stage, reinterpret_cast<double2*>(H), e->ng, piece_col(e, q), piece_col(e, q + 1));
+    mark("h_unpacked");
   }
+  if (trace_on()) std::fprintf(stderr, "[hsdla_b200 trace] download (ms since call start):%s\n", tr.c_str());
 }
 
 static void engine_download(hsdla_b200_engine* e, double* H, double* S) {
@@ -1767,7 +1797,10 @@ static void one_shot(const hsdla_b200_options* o, uint64_t na, uint64_t nl, uint
   HS_CUDA(cudaSetDevice(root->device));
   enqueue_download(root);
   const auto t_d = std::chrono::steady_clock::now();
-  finish_download(root, H, S);
+  if (trace_on())
+    std::fprintf(stderr, "[hsdla_b200 trace] enqueued at %.3f ms since call start\n",
+                 std::chrono::duration<double, std::milli>(t_d - t0).count());
+  finish_download(root, H, S, t0);
   const double d2h = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_d).count();
   hsdla_b200_stats local{};
   double maxph[HSDLA_B200_N_PHASES] = {};

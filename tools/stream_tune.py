@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--cs", default="1.84e-14,1.45e-14")
     ap.add_argument("--ratios", default="1.0,0.8,0.7")
     ap.add_argument("--calls", type=int, default=6)
+    ap.add_argument("--plans", default="", help="explicit chunk plans 'a,b,c;d,e' (HSDLA_B200_STREAM_PLAN)")
     ap.add_argument("--out", default="gpurun_out/stream_tune.jsonl")
     a = ap.parse_args()
     na, nl, ng = CFG[a.config]
@@ -38,7 +39,12 @@ def main():
     led = hb.flop_model(p).total()
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
     with open(a.out, "a") as f:
-        for fl, c, r in itertools.product(a.floors.split(","), a.cs.split(","), a.ratios.split(",")):
+        grid = ([(a.floors.split(",")[0], a.cs.split(",")[0], a.ratios.split(",")[0], pl) for pl in a.plans.split(";")]
+                if a.plans else [(*t, "") for t in itertools.product(a.floors.split(","), a.cs.split(","),
+                                                                     a.ratios.split(","))])
+        for fl, c, r, plan in grid:
+            if plan:
+                os.environ["HSDLA_B200_STREAM_PLAN"] = plan
             os.environ["HSDLA_B200_STREAM_FLOOR"] = fl
             os.environ["HSDLA_B200_STREAM_C"] = c
             os.environ["HSDLA_B200_BAND_RATIO"] = r
@@ -50,7 +56,7 @@ def main():
                 res = hb.build_hs_refined(p, H=H, S=S)
                 ts.append(time.perf_counter() - t)
                 dev.append(res.stats["device_seconds"])
-            rec = {"config": a.config, "floor": float(fl), "c": float(c), "band_ratio": float(r),
+            rec = {"config": a.config, "plan": plan, "floor": float(fl), "c": float(c), "band_ratio": float(r),
                    "wall_ms": float(np.median(ts)) * 1e3, "device_ms": float(np.median(dev)) * 1e3,
                    "tflops": led / float(np.median(ts)) / 1e12, "launches": res.stats["kernel_launches"]}
             print(json.dumps(rec), flush=True)
