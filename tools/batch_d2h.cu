@@ -26,6 +26,20 @@ __global__ void gather_lower(const double2* __restrict__ pk, double2* full, size
   for (size_t i = threadIdx.x; i < len; i += blockDim.x) full[j * n + j + i] = pk[base + i];
 }
 
+// a DMMA-bound kernel (~1 ms) to time alone and next to a concurrent D2H
+__global__ void busy(double* out, int iters) {
+  double a = threadIdx.x * 1e-6, b = 1.0 - threadIdx.x * 1e-7, c[8][2] = {};
+  for (int it = 0; it < iters; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  if (s == 12345.678) out[threadIdx.x] = s;
+}
+
 int main(int argc, char** argv) {
   const size_t n = argc > 1 ? atoll(argv[1]) : 3000, npk = n * (n + 1) / 2;
   char *dpk, *hpk, *hfull;
@@ -41,6 +55,54 @@ int main(int argc, char** argv) {
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
+  {
+    cudaStream_t s2;
+    CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+    double* junk;
+    CK(cudaMalloc(&junk, 4096 * 8));
+    for (int mode = 0; mode < 4; ++mode) {
+      CK(cudaDeviceSynchronize());
+      CK(cudaEventRecord(e0, s));
+      busy<<<148, 256, 0, s>>>(junk, 4000);
+      CK(cudaEventRecord(e1, s));
+      if (mode == 1) CK(cudaMemcpyAsync(hpk, dpk, 8 << 20, cudaMemcpyDeviceToHost, s2));        // 8 MB D2H, pinned
+      if (mode == 2) CK(cudaMemcpyAsync(hpk, dpk, npk * 16, cudaMemcpyDeviceToHost, s2));       // whole packed D2H
+      if (mode == 3) CK(cudaMemcpyAsync(dpk, hpk, npk * 16, cudaMemcpyHostToDevice, s2));       // H2D
+      CK(cudaEventSynchronize(e1));
+      CK(cudaDeviceSynchronize());
+      float ms;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      printf("busy kernel %s: %.3f ms\n", mode == 0 ? "alone" : mode == 1 ? "+ 8 MB D2H" : mode == 2 ? "+ packed D2H" : "+ packed H2D", ms);
+    }
+    // the drop-in's pattern: kernel 1; D2H (copy stream, after kernel 1) overlapping kernel 2;
+    // the host waits for the D2H and unpacks it on 16 threads while kernel 2 runs
+    cudaEvent_t k1, dd, e2a, e2b;
+    CK(cudaEventCreate(&k1)); CK(cudaEventCreate(&dd)); CK(cudaEventCreate(&e2a)); CK(cudaEventCreate(&e2b));
+    for (int mode = 0; mode < 6; ++mode) {
+      CK(cudaDeviceSynchronize());
+      busy<<<148, 256, 0, s>>>(junk, 1000);
+      CK(cudaEventRecord(k1, s));
+      CK(cudaEventRecord(e2a, s));
+      busy<<<148, 256, 0, s>>>(junk, 4000);
+      CK(cudaEventRecord(e2b, s));
+      if (mode % 3 >= 1) {
+        CK(cudaStreamWaitEvent(s2, k1, 0));
+        CK(cudaMemcpyAsync(hpk, dpk, 8 << 20, cudaMemcpyDeviceToHost, s2));
+        CK(cudaEventRecord(dd, s2));
+      }
+      if (mode % 3 == 2) {
+        CK(cudaEventSynchronize(dd));
+        std::vector<std::thread> th;
+        for (int t = 0; t < 16; ++t)
+          th.emplace_back([&, t] { memcpy(hfull + t * (1 << 20), hpk + t * (512 << 10), 512 << 10); });
+        for (auto& x : th) x.join();
+      }
+      CK(cudaEventSynchronize(e2b));
+      float ms;
+      CK(cudaEventElapsedTime(&ms, e2a, e2b));
+      printf("kernel 2 %s: %.3f ms\n", mode % 3 == 0 ? "alone" : mode % 3 == 1 ? "+ dependent D2H" : "+ D2H + host unpack", ms);
+    }
+  }
   for (int rep = 0; rep < 3; ++rep) {
     CK(cudaEventRecord(e0, s));
     CK(cudaMemcpyAsync(hpk, dpk, npk * 16, cudaMemcpyDeviceToHost, s));
