@@ -484,6 +484,8 @@ def run_lapw(args, hb, p, na, nl, ng):
                            "kernel": "lapw_stream_kernel (the HBM-write pass: A, B = 2 x K x N_G x 16 B per launch)",
                            "bytes_per_launch": int(nbytes), "kernel_ms": sms, "peak_source": src,
                            "setup_ms_total": ms, "setup_gbs_total": nbytes / (ms * 1e-3) / 1e9,
+                           # north_star quotes the setup against the 8 TB/s HBM3e spec
+                           "frac_of_spec_8000": nbytes / (sms * 1e-3) / 1e9 / 8000.0,
                            "note": "setup = lapw_tables_kernel (latency-bound per-G tables) + lapw_stream_kernel"},
         "e2e_lapw": {"value": ledger_flops(na, nl, ng) / dt / 1e12, "unit": "TFLOP/s", "ms_per_step": dt * 1e3,
                      "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(2 * (ng * (ng + 1) // 2) * 16),

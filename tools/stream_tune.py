@@ -16,7 +16,7 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1712_07206_b200 as hb  # noqa: E402
 
-CFG = {"c2": (64, 81, 3000), "c3": (108, 121, 6000)}
+CFG = {"c1": (16, 49, 1000), "c2": (64, 81, 3000), "c3": (108, 121, 6000)}
 
 
 def main():
