@@ -34,6 +34,8 @@
 #include <sys/stat.h>
 #include <unistd.h>
 
+#include <immintrin.h>
+
 #include <algorithm>
 #include <atomic>
 #include <chrono>
@@ -195,6 +197,34 @@ class HostPool {
   bool stop_ = false;
 };
 
+// Host copy with non-temporal (streaming) stores: the destination lines are written without
+// being read first (no read-for-ownership), so a pack into a pinned slab costs read +
+// write of the bytes instead of read + read + write -- the host memory bandwidth the
+// concurrent DMA also needs.  Callers fence (sfence) before publishing the data.
+static void copy_nt(void* dst, const void* src, size_t bytes) {
+  char* d = static_cast<char*>(dst);
+  const char* s = static_cast<const char*>(src);
+  // head: up to the next 16-byte boundary of the destination
+  const size_t head = std::min(bytes, (16 - (reinterpret_cast<uintptr_t>(d) & 15)) & 15);
+  std::memcpy(d, s, head);
+  d += head;
+  s += head;
+  bytes -= head;
+  size_t n = bytes / 16;
+  __m128i* dv = reinterpret_cast<__m128i*>(d);
+  const __m128i* sv = reinterpret_cast<const __m128i*>(s);
+  for (; n >= 4; n -= 4, dv += 4, sv += 4) {
+    const __m128i a = _mm_loadu_si128(sv), b = _mm_loadu_si128(sv + 1), c = _mm_loadu_si128(sv + 2),
+                  e = _mm_loadu_si128(sv + 3);
+    _mm_stream_si128(dv, a);
+    _mm_stream_si128(dv + 1, b);
+    _mm_stream_si128(dv + 2, c);
+    _mm_stream_si128(dv + 3, e);
+  }
+  for (; n; --n, ++dv, ++sv) _mm_stream_si128(dv, _mm_loadu_si128(sv));
+  std::memcpy(dv, sv, bytes & 15);
+}
+
 // fn(i) for i in [0, n), in `parts` contiguous ranges on the host pool when the work
 // is large (>= 4 MB), else inline.
 template <class F>
@@ -207,6 +237,7 @@ static void par_for(uint64_t n, uint64_t bytes, F&& fn) {
   }
   pool.run(parts, [&](uint64_t t) {
     for (uint64_t i = n * t / parts; i < n * (t + 1) / parts; ++i) fn(i);
+    _mm_sfence();  // streaming stores (copy_nt) visible before the job completes
   });
 }
 
@@ -866,7 +897,8 @@ static void upload_atoms_staged(hsdla_b200_engine* e, const hsdla_b200_problem* 
       const uint64_t nc = std::min(cols, ng - j0);
       int slot;
       char* b = stage_acquire(e, slot);
-      par_for(nc, nc * colb, [&](uint64_t j) { std::memcpy(b + j * colb, src + (j0 + j) * Kg, colb); });
+      par_for(nc, nc * colb, [&](uint64_t j) { copy_nt(b + j * colb, src + (j0 + j) * Kg, colb); });
+      _mm_sfence();  // the single-threaded case of par_for
       HS_CUDA(cudaMemcpy2DAsync(dst + j0 * e->K, e->K * sizeof(double2), b, colb, colb, nc, cudaMemcpyHostToDevice,
                                 s));
       stage_release(e, slot, s);
@@ -1231,7 +1263,8 @@ static void unpack_lower(const double2* pk, double2* full, uint64_t n, uint64_t 
   cut.push_back(c1);
   pool.run(nt, [&](uint64_t t) {
     for (uint64_t j = cut[t]; j < cut[t + 1]; ++j)
-      std::memcpy(full + j * n + j, pk + packed_col(n, j), (n - j) * sizeof(double2));
+      copy_nt(full + j * n + j, pk + packed_col(n, j), (n - j) * sizeof(double2));
+    _mm_sfence();
   });
 }
 
