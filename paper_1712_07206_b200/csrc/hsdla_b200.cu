@@ -440,6 +440,8 @@ struct hsdla_b200_engine {
   void* lapw_scratch = nullptr;  // device copy of the LAPW inputs (grown on demand)
   // HSDL file reader: two pinned 64 MB staging slabs, allocated on first use
   char* stage_buf[2] = {nullptr, nullptr};
+  double tr_pack_ms = 0, tr_wait_ms = 0;  // HSDLA_B200_TRACE: pageable staging accounting
+  uint64_t tr_pack_bytes = 0;
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   bool stage_busy[2] = {false, false};
   int stage_next = 0;
@@ -848,6 +850,18 @@ static void engine_fill_synthetic(hsdla_b200_engine* e, uint64_t seed) {
 // Staging ring of two pinned slabs owned by the engine; slab s is free again once
 // the copy that read it has completed.
 constexpr size_t kStageSlab = size_t(64) << 20;
+// HSDLA_B200_TRACE=1: host-side timelines of the drop-in (staging, download) on stderr (tuning).
+static bool trace_on() {
+  static const bool on = [] {
+    const char* v = std::getenv("HSDLA_B200_TRACE");
+    return v && *v == '1';
+  }();
+  return on;
+}
+static double host_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 static char* stage_acquire(hsdla_b200_engine* e, int& slot) {
   if (!e->stage_buf[0])
     for (int i = 0; i < 2; ++i) {
@@ -856,7 +870,11 @@ static char* stage_acquire(hsdla_b200_engine* e, int& slot) {
     }
   slot = e->stage_next;
   e->stage_next ^= 1;
-  if (e->stage_busy[slot]) HS_CUDA(cudaEventSynchronize(e->stage_ev[slot]));
+  if (e->stage_busy[slot]) {
+    const double t0 = trace_on() ? host_ms() : 0.0;
+    HS_CUDA(cudaEventSynchronize(e->stage_ev[slot]));
+    if (trace_on()) e->tr_wait_ms += host_ms() - t0;
+  }
   e->stage_busy[slot] = true;
   return e->stage_buf[slot];
 }
@@ -897,30 +915,44 @@ static void upload_atoms_staged(hsdla_b200_engine* e, const hsdla_b200_problem* 
       const uint64_t nc = std::min(cols, ng - j0);
       int slot;
       char* b = stage_acquire(e, slot);
+      const double t0 = trace_on() ? host_ms() : 0.0;
       par_for(nc, nc * colb, [&](uint64_t j) { copy_nt(b + j * colb, src + (j0 + j) * Kg, colb); });
       _mm_sfence();  // the single-threaded case of par_for
+      if (trace_on()) {
+        e->tr_pack_ms += host_ms() - t0;
+        e->tr_pack_bytes += nc * colb;
+      }
       HS_CUDA(cudaMemcpy2DAsync(dst + j0 * e->K, e->K * sizeof(double2), b, colb, colb, nc, cudaMemcpyHostToDevice,
                                 s));
       stage_release(e, slot, s);
     }
   }
-  // operator blocks and U: small, packed into one slab
-  const uint64_t blk = nl * nl, nb = b1 - b0;
-  const size_t tb = nb * blk * sizeof(double2), ub = rows * sizeof(double);
-  if (3 * tb + ub > kStageSlab) {
-    upload_atoms(e, p, a0, b0, b1, s);  // (re-copies A, B: only for > 64 MB of operators per chunk)
-    return;
-  }
-  int slot;
-  char* b = stage_acquire(e, slot);
+  // operator blocks (T_AA, T_AB, T_BB per atom), then U, through the slabs: groups of
+  // atoms whose three blocks fit one slab (large chunks of large-N_L atoms need several)
+  const uint64_t blk = nl * nl, bb = blk * sizeof(double2);
+  if (3 * bb > kStageSlab) throw Fail{HSDLA_B200_SIZING_ERROR, "operator blocks larger than the staging slab"};
+  const uint64_t per = std::max<uint64_t>(1, kStageSlab / (3 * bb));
   const double* srcs[3] = {p->T_AA, p->T_AB, p->T_BB};
   double2* dsts[3] = {e->Taa, e->Tab, e->Tbb};
-  for (int m = 0; m < 3; ++m) {
-    std::memcpy(b + m * tb, reinterpret_cast<const double2*>(srcs[m]) + (a0 + b0) * blk, tb);
-    HS_CUDA(cudaMemcpyAsync(dsts[m] + b0 * blk, b + m * tb, tb, cudaMemcpyHostToDevice, s));
+  for (uint64_t c0 = b0; c0 < b1; c0 += per) {
+    const uint64_t nb = std::min(per, b1 - c0);
+    const size_t tb = nb * bb;
+    int slot;
+    char* b = stage_acquire(e, slot);
+    par_for(3, 3 * tb, [&](uint64_t m) {
+      copy_nt(b + m * tb, reinterpret_cast<const double2*>(srcs[m]) + (a0 + c0) * blk, tb);
+    });
+    _mm_sfence();
+    for (int m = 0; m < 3; ++m)
+      HS_CUDA(cudaMemcpyAsync(dsts[m] + c0 * blk, b + m * tb, tb, cudaMemcpyHostToDevice, s));
+    stage_release(e, slot, s);
   }
-  std::memcpy(b + 3 * tb, p->U + g0, ub);
-  HS_CUDA(cudaMemcpyAsync(e->U + r0, b + 3 * tb, ub, cudaMemcpyHostToDevice, s));
+  const size_t ub = rows * sizeof(double);
+  if (ub > kStageSlab) throw Fail{HSDLA_B200_SIZING_ERROR, "U larger than the staging slab"};
+  int slot;
+  char* b = stage_acquire(e, slot);
+  std::memcpy(b, p->U + g0, ub);
+  HS_CUDA(cudaMemcpyAsync(e->U + r0, b, ub, cudaMemcpyHostToDevice, s));
   stage_release(e, slot, s);
 }
 
@@ -1140,7 +1172,11 @@ static void engine_build_streamed(hsdla_b200_engine* e, const hsdla_b200_problem
   HS_CUDA(cudaEventRecord(e->ev_up0, e->copy_stream));
   const uint64_t ab_bytes = p->n_atoms * p->n_l * p->n_g * sizeof(double2);
   const bool pinned = is_pinned(p->A, ab_bytes) && is_pinned(p->B, ab_bytes);
-  auto& plan = pinned ? e->streamed : e->streamed_pg;
+  // pageable rows are packed into pinned slabs at ~60 GB/s (copy_nt) and DMA'd from there,
+  // a feed close to page-locked inputs, so both use the same plan (HSDLA_B200_PAGEABLE_PLAN=pg:
+  // the slower-feed plan the HSDL file path uses)
+  const char* pgp = std::getenv("HSDLA_B200_PAGEABLE_PLAN");
+  auto& plan = pinned || !(pgp && std::strcmp(pgp, "pg") == 0) ? e->streamed : e->streamed_pg;
   if (pinned) {
     // page-locked inputs: every chunk's copies are asynchronous, enqueue them all first
     for (size_t c = 0; c < plan.size(); ++c) {
@@ -1162,6 +1198,13 @@ static void engine_build_streamed(hsdla_b200_engine* e, const hsdla_b200_problem
   HS_CUDA(cudaEventRecord(e->ev_up1, e->copy_stream));
   HS_CUDA(cudaEventRecord(e->ev_end, e->stream));
   e->uploaded_streamed = true;
+  if (trace_on() && !pinned) {
+    std::fprintf(stderr, "[hsdla_b200 trace] pageable staging: packed %.0f MB in %.1f ms (%.1f GB/s), waited %.1f ms "
+                 "for slabs, %zu chunks\n", e->tr_pack_bytes / 1e6, e->tr_pack_ms,
+                 e->tr_pack_bytes / std::max(e->tr_pack_ms, 1e-9) / 1e6, e->tr_wait_ms, plan.size());
+    e->tr_pack_ms = e->tr_wait_ms = 0;
+    e->tr_pack_bytes = 0;
+  }
 }
 
 // NCCL sum-reduce of the packed partials to `root`, split so S's reduce overlaps the
@@ -1293,14 +1336,6 @@ static void enqueue_download(hsdla_b200_engine* e) {
   }
 }
 
-// HSDLA_B200_TRACE=1: host timestamps of the drop-in's download phase on stderr (tuning).
-static bool trace_on() {
-  static const bool on = [] {
-    const char* v = std::getenv("HSDLA_B200_TRACE");
-    return v && *v == '1';
-  }();
-  return on;
-}
 
 // Unpack S as soon as its bytes land (H may still be computing), then H.
 static void finish_download(hsdla_b200_engine* e, double* H, double* S,
