@@ -31,6 +31,7 @@
 #include <fcntl.h>
 #include <nccl.h>
 #include <nvtx3/nvToolsExt.h>
+#include <sys/mman.h>
 #include <sys/stat.h>
 #include <unistd.h>
 
@@ -440,6 +441,12 @@ struct hsdla_b200_engine {
   void* lapw_scratch = nullptr;  // device copy of the LAPW inputs (grown on demand)
   // HSDL file reader: two pinned 64 MB staging slabs, allocated on first use
   char* stage_buf[2] = {nullptr, nullptr};
+  // HSDL file view: a read-only mapping of the last file this engine loaded, kept while the
+  // file's (device, inode, size, mtime) stay the same, so repeated k-point calls on one file
+  // copy rows straight out of the page cache without a pread per column piece
+  const char* fmap = nullptr;
+  size_t fmap_len = 0;
+  struct stat fmap_st {};
   double tr_pack_ms = 0, tr_wait_ms = 0;  // HSDLA_B200_TRACE: pageable staging accounting
   uint64_t tr_pack_bytes = 0;
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
@@ -483,6 +490,7 @@ static void engine_free(hsdla_b200_engine* e) {
                   (void*)e->Hp, (void*)e->Sp})
     if (p) cudaFree(p);
   if (e->host_stage) cudaFreeHost(e->host_stage);
+  if (e->fmap) munmap(const_cast<char*>(e->fmap), e->fmap_len);
   for (int i = 0; i < 2; ++i) {
     if (e->stage_ev[i]) {
       cudaEventSynchronize(e->stage_ev[i]);
@@ -1609,6 +1617,40 @@ static void pread_pieces(int fd, char* dst, uint64_t off0, uint64_t stride, size
     if (bad[t]) throw errs[t];
 }
 
+// The engine's cached read-only view of the open file `fd` (nullptr: mapping unavailable,
+// the caller preads).  A different or changed file (device, inode, size, mtime) is
+// remapped; MAP_POPULATE faults the page-cache pages in once per mapping.  The file
+// must not be truncated while a call reads it (as for any mapped reader).
+static const char* file_view(hsdla_b200_engine* e, int fd) {
+  struct stat st {};
+  if (fstat(fd, &st) != 0 || st.st_size <= 0) return nullptr;
+  if (e->fmap && st.st_dev == e->fmap_st.st_dev && st.st_ino == e->fmap_st.st_ino &&
+      st.st_size == e->fmap_st.st_size && st.st_mtim.tv_sec == e->fmap_st.st_mtim.tv_sec &&
+      st.st_mtim.tv_nsec == e->fmap_st.st_mtim.tv_nsec)
+    return e->fmap;
+  if (e->fmap) munmap(const_cast<char*>(e->fmap), e->fmap_len);
+  e->fmap = nullptr;
+  void* m = mmap(nullptr, static_cast<size_t>(st.st_size), PROT_READ, MAP_SHARED | MAP_POPULATE, fd, 0);
+  if (m == MAP_FAILED) return nullptr;
+  e->fmap = static_cast<const char*>(m);
+  e->fmap_len = static_cast<size_t>(st.st_size);
+  e->fmap_st = st;
+  return e->fmap;
+}
+
+// pread_pieces through the file view when there is one: copy_nt from the mapped page cache
+// on the host pool (no syscall per piece)
+static void read_pieces(hsdla_b200_engine* e, const char* view, int fd, char* dst, uint64_t off0, uint64_t stride,
+                        size_t piece, uint64_t n) {
+  if (!view) {
+    pread_pieces(fd, dst, off0, stride, piece, n);
+    return;
+  }
+  if (n && off0 + (n - 1) * stride + piece > e->fmap_len) throw Fail{HSDLA_B200_IO_ERROR, "truncated problem file"};
+  par_for(n, n * piece, [&](uint64_t i) { copy_nt(dst + i * piece, view + off0 + i * stride, piece); });
+  _mm_sfence();
+}
+
 // Host-read + H2D (on stream s) of the engine-local atoms [b0, b1) of shard a0 of an
 // HSDL file: their rows of every A / B column (one pread per column when the rows
 // are a strict subset of the file's, else whole column slabs), their T blocks and U.
@@ -1617,6 +1659,7 @@ static void load_atoms_from_file(hsdla_b200_engine* e, int fd, const HsdlHeader&
   const uint64_t K = e->K, Kf = h.na * h.nl, nl = h.nl, ng = h.ng;
   const uint64_t r0 = b0 * nl, rows = (b1 - b0) * nl, g0 = (a0 + b0) * nl;
   const size_t colb = rows * sizeof(double2);
+  const char* view = file_view(e, fd);
   for (int m = 0; m < 2; ++m) {  // A then B
     const uint64_t base = (m == 0 ? h.off_A : h.off_B) + g0 * 16;
     double2* dst = (m == 0 ? e->A : e->B) + r0;
@@ -1626,7 +1669,7 @@ static void load_atoms_from_file(hsdla_b200_engine* e, int fd, const HsdlHeader&
           const uint64_t nr = std::min<uint64_t>(kStageSlab / 16, rows - q0);
           int slot;
           char* b = stage_acquire(e, slot);
-          pread_pieces(fd, b, base + (j * Kf + q0) * 16, nr * 16, nr * 16, 1);
+          read_pieces(e, view, fd, b, base + (j * Kf + q0) * 16, nr * 16, nr * 16, 1);
           HS_CUDA(cudaMemcpyAsync(dst + j * K + q0, b, nr * 16, cudaMemcpyHostToDevice, s));
           stage_release(e, slot, s);
         }
@@ -1637,7 +1680,7 @@ static void load_atoms_from_file(hsdla_b200_engine* e, int fd, const HsdlHeader&
       const uint64_t nc = std::min(cols, ng - j0);
       int slot;
       char* b = stage_acquire(e, slot);
-      pread_pieces(fd, b, base + j0 * Kf * 16, Kf * 16, colb, nc);
+      read_pieces(e, view, fd, b, base + j0 * Kf * 16, Kf * 16, colb, nc);
       HS_CUDA(cudaMemcpy2DAsync(dst + j0 * K, K * sizeof(double2), b, colb, colb, nc, cudaMemcpyHostToDevice, s));
       stage_release(e, slot, s);
     }
@@ -1650,7 +1693,7 @@ static void load_atoms_from_file(hsdla_b200_engine* e, int fd, const HsdlHeader&
     const uint64_t nb = std::min(atoms_per, b1 - c0);
     int slot;
     char* b = stage_acquire(e, slot);
-    pread_pieces(fd, b, h.off_T + (a0 + c0) * 3 * blk, 3 * blk, 3 * blk, nb);
+    read_pieces(e, view, fd, b, h.off_T + (a0 + c0) * 3 * blk, 3 * blk, 3 * blk, nb);
     double2* dsts[3] = {e->Taa, e->Tab, e->Tbb};
     for (int m = 0; m < 3; ++m)
       HS_CUDA(cudaMemcpy2DAsync(reinterpret_cast<char*>(dsts[m]) + c0 * blk, blk, b + m * blk, 3 * blk, blk, nb,
@@ -1661,7 +1704,7 @@ static void load_atoms_from_file(hsdla_b200_engine* e, int fd, const HsdlHeader&
   if (ub > kStageSlab) throw Fail{HSDLA_B200_SIZING_ERROR, "U larger than the staging slab"};
   int slot;
   char* b = stage_acquire(e, slot);
-  pread_pieces(fd, b, h.off_U + g0 * sizeof(double), ub, ub, 1);
+  read_pieces(e, view, fd, b, h.off_U + g0 * sizeof(double), ub, ub, 1);
   HS_CUDA(cudaMemcpyAsync(e->U + r0, b, ub, cudaMemcpyHostToDevice, s));
   stage_release(e, slot, s);
 }
@@ -1694,7 +1737,10 @@ static void engine_build_file(hsdla_b200_engine* e, const char* path, uint64_t a
   begin_build(e, algo);
   HS_CUDA(cudaStreamWaitEvent(e->copy_stream, e->ev_end, 0));
   HS_CUDA(cudaEventRecord(e->ev_up0, e->copy_stream));
-  auto& plan = e->streamed_pg;  // page-cache reads feed ~20 GB/s
+  // the mapped file view feeds ~36-42 GB/s (copy_nt from the page cache), close to the
+  // page-locked feed; HSDLA_B200_FILE_PLAN=pg selects the slower-feed plan (pread fallback)
+  const char* fpl = std::getenv("HSDLA_B200_FILE_PLAN");
+  auto& plan = fpl && std::strcmp(fpl, "pg") == 0 ? e->streamed_pg : e->streamed;
   for (size_t c = 0; c < plan.size(); ++c) {
     load_atoms_from_file(e, f.fd, h, a0, plan[c].a0, plan[c].a1, e->copy_stream);
     HS_CUDA(cudaEventRecord(e->ev_chunk_up[c], e->copy_stream));
