@@ -75,3 +75,35 @@ def test_engine_load_shape_mismatch(tmp_path):
     with pytest.raises(hb.DimensionError):
         e.load(path, 2)  # atoms 2..4 exceed the file's 4 atoms
     e.close()
+
+
+def test_file_view_follows_a_rewritten_file(tmp_path):
+    """The engine keeps a read-only mapping of the last file it loaded; rewriting the file
+    (same shape, other values) between calls must remap it, so the second build sees the
+    new contents, and the same file again reproduces the first result bit for bit."""
+    path = str(tmp_path / "p.hsdl")
+    p1 = hb.generate_problem(6, 25, 400, 1, 0)
+    p2 = hb.generate_problem(6, 25, 400, 2, 0)
+    hb.save_problem(p1, path)
+    r1 = hb.build_hs_file(path)
+    hb.save_problem(p2, path)
+    os.utime(path, ns=(0, os.stat(path).st_mtime_ns + 1_000_000))  # a distinct mtime even on coarse clocks
+    r2 = hb.build_hs_file(path)
+    w2 = hb.build_hs_refined(p2)
+    assert rel(r2.H, w2.H) <= TOL and rel(r2.S, w2.S) <= TOL
+    assert rel(r2.H, r1.H) > 1e-3
+    hb.save_problem(p1, path)
+    r3 = hb.build_hs_file(path)
+    assert np.array_equal(r3.H, r1.H) and np.array_equal(r3.S, r1.S)
+
+
+def test_truncated_file_is_an_io_error(tmp_path):
+    """A file cut short after its header: IoError from the loader, never a crash."""
+    p = hb.generate_problem(4, 9, 300, 3, 0)
+    path = str(tmp_path / "t.hsdl")
+    hb.save_problem(p, path)
+    size = os.path.getsize(path)
+    with open(path, "r+b") as f:
+        f.truncate(size // 2)
+    with pytest.raises(hb.IoError):
+        hb.build_hs_file(path)

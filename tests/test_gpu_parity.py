@@ -355,3 +355,30 @@ def test_arith_modes_agree_and_account(restatement):
         assert res["3m"].stats["executed_flops"] == cmac // 8 * 6 + 2 * K * ng
     with pytest.raises(hb.ConfigError):
         hb.build_hs_refined(p, hb.PipelineConfig(arith="2m"))
+
+
+def test_pageable_and_pinned_inputs_agree_bitwise_with_multi_slab_operator_chunks(restatement, monkeypatch):
+    """The host-buffer drop-in with pageable inputs (rows and operator blocks packed into
+    pinned slabs with streaming stores) and with registered inputs runs the same chunk plan,
+    so H and S are bitwise identical.  A forced 100-atom chunk at N_L 121 carries
+    3 x 100 x 121^2 x 16 B = 70 MB of operator blocks, more than one 64 MB staging slab."""
+    monkeypatch.setenv("HSDLA_B200_STREAM_PLAN", "100,20")
+    hb.release_cache()
+    try:
+        p = hb.generate_problem(120, 121, 300, 5, 0)
+        a = hb.build_hs_refined(p)
+        bufs = [p.A, p.B, p.T_AA, p.T_AB, p.T_BB, p.U]
+        for b in bufs:
+            hb.host_register(b)
+        try:
+            b_ = hb.build_hs_refined(p)
+        finally:
+            for b in bufs:
+                hb.host_unregister(b)
+    finally:
+        hb.release_cache()
+    assert np.array_equal(a.H, b_.H) and np.array_equal(a.S, b_.S)
+    J = np.sort(np.random.default_rng(4).choice(p.n_g, size=32, replace=False))
+    Hs, Ss = restatement.build_hs_sampled(p, J)
+    assert rel(np.asfortranarray(a.H[np.ix_(J, J)]), Hs) <= TOL
+    assert rel(np.asfortranarray(a.S[np.ix_(J, J)]), Ss) <= TOL
