@@ -2108,7 +2108,8 @@ struct Ctx {
       const uint64_t nc = std::min(per, c - j0);
       HS_CUDA(cudaEventSynchronize(ring->ev[slot]));
       char* b = ring->buf[slot];
-      par_for(nc, nc * colb, [&](uint64_t j) { std::memcpy(b + j * colb, hc + (j0 + j) * ld, colb); });
+      par_for(nc, nc * colb, [&](uint64_t j) { copy_nt(b + j * colb, hc + (j0 + j) * ld, colb); });
+      _mm_sfence();
       HS_CUDA(cudaMemcpyAsync(d + j0 * r, b, nc * colb, cudaMemcpyHostToDevice, s));
       HS_CUDA(cudaEventRecord(ring->ev[slot], s));
     }
@@ -2136,7 +2137,8 @@ struct Ctx {
       HS_CUDA(cudaEventSynchronize(ring->ev[q & 1]));
       const uint64_t j0 = q * per, nc = std::min(per, c - j0);
       const char* b = ring->buf[q & 1];
-      par_for(nc, nc * colb, [&](uint64_t j) { std::memcpy(hc + (j0 + j) * ld, b + j * colb, colb); });
+      par_for(nc, nc * colb, [&](uint64_t j) { copy_nt(hc + (j0 + j) * ld, b + j * colb, colb); });
+      _mm_sfence();
     }
   }
   // device packed-lower n x n -> the lower triangle of host C (ldc), upper untouched
@@ -2170,7 +2172,8 @@ struct Ctx {
       const double2* b = reinterpret_cast<const double2*>(ring->buf[q & 1]);
       const uint64_t j0 = cuts[q], base = pc(j0), ncol = cuts[q + 1] - j0;
       par_for(ncol, (pc(cuts[q + 1]) - base) * 16,
-              [&](uint64_t t) { std::memcpy(hc + (j0 + t) * ldc + j0 + t, b + pc(j0 + t) - base, (n - j0 - t) * 16); });
+              [&](uint64_t t) { copy_nt(hc + (j0 + t) * ldc + j0 + t, b + pc(j0 + t) - base, (n - j0 - t) * 16); });
+      _mm_sfence();
     }
   }
   void sync() { HS_CUDA(cudaStreamSynchronize(s)); }
