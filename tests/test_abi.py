@@ -52,3 +52,14 @@ def test_library_then_torch_share_one_nccl():
             "import torch, torch.distributed; print('ok', torch.__version__)" % ROOT)
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_python_constants_match_the_header():
+    """The ctypes mirror's algorithm / arithmetic numbering equals include/hsdla_b200.h."""
+    from paper_1712_07206_b200.pipeline import ALGOS
+    src = open(os.path.join(ROOT, "include", "hsdla_b200.h")).read()
+    defs = {m.group(1): int(m.group(2)) for m in re.finditer(r"#define (HSDLA_B200_\w+)\s+(\d+)u?\b", src)}
+    assert ALGOS == {"merged": defs["HSDLA_B200_ALGO_REFINED_MERGED"], "refined": defs["HSDLA_B200_ALGO_REFINED"],
+                     "original": defs["HSDLA_B200_ALGO_ORIGINAL"], "fused": defs["HSDLA_B200_ALGO_REFINED_FUSED"]}
+    assert _lib.ARITH == {"3m": defs["HSDLA_B200_ARITH_3M"], "4m": defs["HSDLA_B200_ARITH_4M"]}
+    assert _lib.FLAG_ARITH_4M == defs["HSDLA_B200_FLAG_ARITH_4M"]

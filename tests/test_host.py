@@ -79,6 +79,12 @@ def test_config_errors():
         hb.build_hs(p, hb.PipelineConfig(variant="original"))
     with pytest.raises(hb.ConfigError):
         hb.parse_variant("x")
+    with pytest.raises(hb.ConfigError):
+        hb.build_hs_refined(p, hb.PipelineConfig(algo="bogus"))
+    # the C-ABI algorithm numbering the Python mirror relies on (include/hsdla_b200.h)
+    from paper_1712_07206_b200.pipeline import ALGOS
+    assert ALGOS == {"merged": 0, "refined": 1, "original": 2, "fused": 3}
+    assert hb.PipelineConfig().algo == "merged"
     with pytest.raises(hb.DimensionError):
         bad = hb.generate_problem(1, 2, 4, 81, 0)
         bad.A = np.ascontiguousarray(bad.A)  # C order is not the reference layout
