@@ -18,7 +18,8 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1712_07206_b200 as hb  # noqa: E402
 
-CFG = {"c1": (16, 49, 1000), "c2": (64, 81, 3000), "c3": (108, 121, 6000), "c4": (512, 121, 13000)}
+CFG = {"c1": (16, 49, 1000), "c2": (64, 81, 3000), "c3": (108, 121, 6000), "c4": (512, 121, 13000),
+       "c5_na64_ng20000": (64, 81, 20000), "c5_na256_ng10000": (256, 81, 10000), "c5_na1024_ng5000": (1024, 81, 5000)}
 
 
 def timed(p, H, S, n):
