@@ -225,6 +225,12 @@ int hsdla_b200_engine_fill_synthetic(hsdla_b200_engine* e, uint64_t seed);
  * and the kernel layer take the process default, set by hsdla_b200_set_default_arith. */
 int hsdla_b200_engine_set_arith(hsdla_b200_engine* e, int arith);
 int hsdla_b200_set_default_arith(int arith);
+/* on != 0: this engine's builds run their final H contraction in tile-column bands, so an
+ * hsdla_b200_engine_download enqueued right after the build overlaps H's D2H and host
+ * unpack with the remaining bands (as the one-shot drop-in does); S's download already
+ * overlaps the H phases.  Costs ~1 % of device time (smaller final launches); off by
+ * default (device-resident builds that are not downloaded). */
+int hsdla_b200_engine_set_download_overlap(hsdla_b200_engine* e, int on);
 /* Enqueue the full build (all phases) on the engine stream; asynchronous. */
 int hsdla_b200_engine_build(hsdla_b200_engine* e, int algo);
 /* Streamed build from HOST memory: uploads shard `atom_begin` of p in atom chunks on

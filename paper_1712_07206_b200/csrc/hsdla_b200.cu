@@ -429,6 +429,7 @@ struct hsdla_b200_engine {
   cudaEvent_t ev_h_red[kD2hPieces] = {};   // ... and band q's packed range is reduced (NCCL)
   int piece_tiles[kD2hPieces + 1] = {};    // tile-column boundaries of the pieces / bands
   bool band_final_h = false;               // this build runs its final H contraction band by band
+  bool overlap_dl = false;                 // engine builds band their final H (a download follows)
   bool banded = false;                     // ... and the last build did
   std::vector<cudaEvent_t> ev_chunk_up;
   int last_algo = 0, launches = 0;
@@ -1157,6 +1158,7 @@ static void begin_build(hsdla_b200_engine* e, int algo) {
   e->ops.clear();
   e->built = true;
   e->banded = false;
+  if (e->overlap_dl) e->band_final_h = true;  // (the one-shot drop-in sets and clears it itself)
 }
 
 // Device-resident build: one chunk over all atoms (the bench's `value`).
@@ -2433,6 +2435,13 @@ int hsdla_b200_engine_set_arith(hsdla_b200_engine* e, int arith) {
     if (arith != HSDLA_B200_ARITH_3M && arith != HSDLA_B200_ARITH_4M)
       throw Fail{HSDLA_B200_CONFIG_ERROR, "arith must be HSDLA_B200_ARITH_3M or _4M"};
     e->arith = arith;
+  });
+}
+int hsdla_b200_engine_set_download_overlap(hsdla_b200_engine* e, int on) {
+  return guarded([&] {
+    if (!e) throw Fail{HSDLA_B200_CONFIG_ERROR, "null engine"};
+    e->overlap_dl = on != 0;
+    if (!on) e->band_final_h = false;
   });
 }
 int hsdla_b200_set_default_arith(int arith) {

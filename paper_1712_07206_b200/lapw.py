@@ -165,6 +165,7 @@ def build_hs_lapw(sys_: LapwSystem, T_AA, T_AB, T_BB, algo="merged", device=0) -
             raise DimensionError(f"T operators must be ({nl}, {nl}, {sys_.n_atoms})")
     eng = Engine(device, sys_.n_atoms, nl, sys_.n_g)
     try:
+        eng.set_download_overlap(True)
         eng.setup_lapw(sys_)
         eng.upload_operators(T_AA, T_AB, T_BB)
         eng.build(algo)

@@ -312,6 +312,12 @@ class Engine:
             raise ConfigError(f"unknown arith: {arith} (3m | 4m)")
         check(_lib.lib().hsdla_b200_engine_set_arith(self.h, C.c_int(_lib.ARITH[arith])), "engine_set_arith")
 
+    def set_download_overlap(self, on=True):
+        """Band the final H contraction of this engine's builds so that a download issued right
+        after build() overlaps it (hsdla_b200_engine_set_download_overlap)."""
+        check(_lib.lib().hsdla_b200_engine_set_download_overlap(self.h, C.c_int(1 if on else 0)),
+              "engine_set_download_overlap")
+
     def load(self, path, atom_begin=0):
         """Stream this shard of an HSDL v1 file into the engine (hsdla_b200_engine_load)."""
         check(_lib.lib().hsdla_b200_engine_load(self.h, os.fsencode(path), C.c_uint64(atom_begin)), "engine_load")

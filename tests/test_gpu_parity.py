@@ -382,3 +382,19 @@ def test_pageable_and_pinned_inputs_agree_bitwise_with_multi_slab_operator_chunk
     Hs, Ss = restatement.build_hs_sampled(p, J)
     assert rel(np.asfortranarray(a.H[np.ix_(J, J)]), Hs) <= TOL
     assert rel(np.asfortranarray(a.S[np.ix_(J, J)]), Ss) <= TOL
+
+
+def test_engine_download_overlap_matches_whole_build():
+    """hsdla_b200_engine_set_download_overlap: the device-resident build bands its final H
+    contraction (band downloads overlap the remaining bands); same H, S to rounding."""
+    p = hb.generate_problem(24, 81, 2200, 9, 3)
+    out = []
+    for on in (False, True):
+        e = hb.Engine(0, p.n_atoms, p.n_l, p.n_g)
+        e.set_download_overlap(on)
+        e.upload(p)
+        e.build()
+        out.append(e.download())
+        e.sync()
+        e.close()
+    assert rel(out[1][0], out[0][0]) <= 1e-14 and rel(out[1][1], out[0][1]) <= 1e-14
