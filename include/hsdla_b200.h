@@ -127,8 +127,10 @@ typedef struct hsdla_b200_stats {
 /* ---- the drop-in --------------------------------------------------------
  * build_hs_refined (pipeline.cpp:281-329) on the GPU(s).  Writes the lower
  * triangles of the caller-allocated H and S (n_g*n_g complex each, col-major).
- * Engines (device buffers) are cached per (device, shape) across calls; host
- * buffers registered with hsdla_b200_host_register() upload at full PCIe rate. */
+ * Engines (device buffers) are cached per (device, shape) across calls.  Host
+ * buffers registered with hsdla_b200_host_register() are DMA'd directly; ordinary
+ * pageable buffers are packed through pinned slabs by the host pool (streaming
+ * stores, ~60 GB/s), both in atom chunks overlapped with the build. */
 int hsdla_b200_build_hs(const hsdla_b200_problem* p, const hsdla_b200_options* opts, double* H,
                         double* S, hsdla_b200_stats* stats);
 
@@ -139,8 +141,11 @@ int hsdla_b200_build_hs(const hsdla_b200_problem* p, const hsdla_b200_options* o
 int hsdla_b200_problem_file_info(const char* path, uint64_t* n_atoms, uint64_t* n_l, uint64_t* n_g, uint8_t* hpd);
 /* build_hs(load_problem(path), cfg) without a host ProblemInstance: every GPU
  * streams only its atom shard (A/B rows of each column, T blocks, U) from the file
- * into HBM through a pinned double buffer, then builds device-resident.  Same
- * outputs / stats contract as hsdla_b200_build_hs (h2d_seconds = file load). */
+ * into HBM through a pinned double buffer, in atom chunks overlapped with the build.
+ * Rows are copied out of a read-only mapping of the file that the engine keeps while
+ * the file's (device, inode, size, mtime) are unchanged; the file must not be
+ * truncated during a call.  Same outputs / stats contract as hsdla_b200_build_hs
+ * (h2d_seconds = file load). */
 int hsdla_b200_build_hs_file(const char* path, const hsdla_b200_options* opts, double* H, double* S,
                              hsdla_b200_stats* stats);
 
