@@ -68,3 +68,25 @@ def test_reference_arm_under_torchrun_world_2():
     assert len(lines) == 1, r.stdout
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+
+
+@pytest.mark.gpu
+def test_b200_arm_under_torchrun_with_nccl_plumbing():
+    """bench.py as the driver launches it for N > 1 (torchrun, env rendezvous), here with one
+    rank and --force-comm: the NCCL reduce path (comm stream, banded H reduce) in the timed
+    region and the multi-rank e2e leg (build_streamed + reduce + rank-0 download)."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                        "--gpus", "1", "--config", "c1", "--steps", "2", "--warmup", "3", "--no-cpu-baseline",
+                        "--force-comm", "--e2e-steps", "2"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 1 and d["value"] > 1.0 and d["e2e"]["value"] > 0
