@@ -387,6 +387,9 @@ struct ChunkPlan {
   // h: fused her2k+herkx; h2k: her2k over X1; hkx: herkx A^H X1; haa: original X2^H X1
   // merged: wa: W_A = T_AA A + T_AB B -> X1; wb: W_B = T_AB^H A + T_BB B -> X2; hm: [A;B]^H [X1;X2]
   CtnParams s, z, zf, x, h, h2k, hkx, haa, wa, wb, hm;
+  // the S contraction split by segment (first streamed chunk: A^H A starts on A's rows
+  // while B, T, U are still on the wire; (UB)^H (UB) accumulates once they landed)
+  CtnParams sA, sB;
   dim3 grid_tri, grid_bat;
 };
 
@@ -422,7 +425,8 @@ struct hsdla_b200_engine {
   size_t ev_used = 0;
   std::vector<hsdla_b200::OpTime> ops;
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr, ev_s_done = nullptr, ev_s_red = nullptr,
-              ev_reduce_end = nullptr, ev_up0 = nullptr, ev_up1 = nullptr, ev_s_d2h = nullptr;
+              ev_reduce_end = nullptr, ev_up0 = nullptr, ev_up1 = nullptr, ev_s_d2h = nullptr,
+              ev_a0 = nullptr;  // the first streamed chunk's A rows landed
   static constexpr int kD2hPieces = 8;   // H downloads in column-range pieces, unpacked as each lands
   cudaEvent_t ev_h_piece[kD2hPieces] = {};
   cudaEvent_t ev_h_band[kD2hPieces] = {};  // final H contraction finished tile-column band q
@@ -507,7 +511,7 @@ static void engine_free(hsdla_b200_engine* e) {
     if (ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e->ev_h_red)
     if (ev) cudaEventDestroy(ev);
-  for (cudaEvent_t ev : {e->ev_begin, e->ev_end, e->ev_s_done, e->ev_s_red, e->ev_reduce_end, e->ev_up0, e->ev_up1,
+  for (cudaEvent_t ev : {e->ev_a0, e->ev_begin, e->ev_end, e->ev_s_done, e->ev_s_red, e->ev_reduce_end, e->ev_up0, e->ev_up1,
                          e->ev_s_d2h, e->ev_setup0, e->ev_setup1, e->ev_setup_mid})
     if (ev) cudaEventDestroy(ev);
   for (auto& t : e->ring)
@@ -562,6 +566,12 @@ static void make_chunk(hsdla_b200_engine* e, uint64_t a0, uint64_t a1, bool firs
   set_seg(cp.s, 0, mA, mA, Kc);
   set_seg(cp.s, 1, mX1, mX1, Kc);
   cp.s.nseg = 2;
+  tri_base(cp.sA, e->Sp, beta0);
+  set_seg(cp.sA, 0, mA, mA, Kc);
+  cp.sA.nseg = 1;
+  tri_base(cp.sB, e->Sp, 1.0);
+  set_seg(cp.sB, 0, mX1, mX1, Kc);
+  cp.sB.nseg = 1;
   // fused H = Z^H B + B^H Z + A^H X   (pipeline.cpp:311 + :324)
   tri_base(cp.h, e->Hp, beta0);
   set_seg(cp.h, 0, mX2, mB, Kc);
@@ -774,7 +784,7 @@ static hsdla_b200_engine* engine_create(int device, uint64_t na, uint64_t nl, ui
     for (cudaEvent_t* ev : {&e->ev_begin, &e->ev_end, &e->ev_reduce_end, &e->ev_up0, &e->ev_up1, &e->ev_setup0,
                             &e->ev_setup1, &e->ev_setup_mid})
       HS_CUDA(cudaEventCreate(ev));
-    for (cudaEvent_t* ev : {&e->ev_s_done, &e->ev_s_red, &e->ev_s_d2h})
+    for (cudaEvent_t* ev : {&e->ev_s_done, &e->ev_s_red, &e->ev_s_d2h, &e->ev_a0})
       HS_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     for (cudaEvent_t& ev : e->ev_h_piece) HS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     for (cudaEvent_t& ev : e->ev_h_band) HS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -820,12 +830,13 @@ static void check_problem(const hsdla_b200_engine* e, const hsdla_b200_problem* 
 
 // H2D of local atoms [b0, b1) (engine-local indices) of shard a0 of p, on stream s.
 static void upload_atoms(hsdla_b200_engine* e, const hsdla_b200_problem* p, uint64_t a0, uint64_t b0, uint64_t b1,
-                         cudaStream_t s) {
+                         cudaStream_t s, cudaEvent_t ev_a = nullptr) {
   const uint64_t Kg = p->n_atoms * p->n_l;  // caller's leading dimension
   const uint64_t nl = e->nl, r0 = b0 * nl, rows = (b1 - b0) * nl, g0 = (a0 + b0) * nl;
   const size_t width = rows * sizeof(double2);
   HS_CUDA(cudaMemcpy2DAsync(e->A + r0, e->K * sizeof(double2), reinterpret_cast<const double2*>(p->A) + g0,
                             Kg * sizeof(double2), width, e->ng, cudaMemcpyHostToDevice, s));
+  if (ev_a) HS_CUDA(cudaEventRecord(ev_a, s));
   HS_CUDA(cudaMemcpy2DAsync(e->B + r0, e->K * sizeof(double2), reinterpret_cast<const double2*>(p->B) + g0,
                             Kg * sizeof(double2), width, e->ng, cudaMemcpyHostToDevice, s));
   const uint64_t blk = nl * nl;
@@ -906,12 +917,14 @@ static bool is_pinned(const void* p, size_t bytes) {
 // upload_atoms for PAGEABLE caller buffers: the rows of atoms [b0, b1) are packed by up
 // to 16 host threads into the engine's pinned staging slabs and copied from there
 // (a pageable cudaMemcpy is host-synchronous and single-threaded, ~10 GB/s).
+// parts: 1 = A rows, 2 = B rows + operator blocks + U, 3 = all
 static void upload_atoms_staged(hsdla_b200_engine* e, const hsdla_b200_problem* p, uint64_t a0, uint64_t b0,
-                                uint64_t b1, cudaStream_t s) {
+                                uint64_t b1, cudaStream_t s, int parts = 3) {
   const uint64_t Kg = p->n_atoms * p->n_l, nl = e->nl, ng = e->ng;
   const uint64_t r0 = b0 * nl, rows = (b1 - b0) * nl, g0 = (a0 + b0) * nl;
   const size_t colb = rows * sizeof(double2);
   for (int m = 0; m < 2; ++m) {
+    if (!(parts & (m == 0 ? 1 : 2))) continue;
     const double2* src = reinterpret_cast<const double2*>(m == 0 ? p->A : p->B) + g0;
     double2* dst = (m == 0 ? e->A : e->B) + r0;
     if (colb > kStageSlab) {  // one column's rows exceed a slab: direct (pageable) copy
@@ -936,6 +949,7 @@ static void upload_atoms_staged(hsdla_b200_engine* e, const hsdla_b200_problem* 
       stage_release(e, slot, s);
     }
   }
+  if (!(parts & 2)) return;
   // operator blocks (T_AA, T_AB, T_BB per atom), then U, through the slabs: groups of
   // atoms whose three blocks fit one slab (large chunks of large-N_L atoms need several)
   const uint64_t blk = nl * nl, bb = blk * sizeof(double2);
@@ -1034,8 +1048,9 @@ static void harvest(hsdla_b200_engine* e, hsdla_b200_engine::KTimer& t) {
 //   refined  s, z_loop, her2k, hemm_loop, herkx        (pipeline.cpp:281-329), one temp X1
 //   fused    s, z_loop, hemm_loop, her2k(+herkx)       two temps (Z in X2)
 //   original z_loop, her2k, s, chol_loop, h_aa_update  (pipeline.cpp:189-279), two temps
+// s_rest: the chunk's A^H A half of S already ran (enqueue_s_first); phase s adds (UB)^H (UB).
 static void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool last,
-                          hsdla_b200_engine::KTimer* kt) {
+                          hsdla_b200_engine::KTimer* kt, bool s_rest = false) {
   cudaStream_t s = e->stream;
   // The build's final H contraction: whole, or band by band (tile-column bands of
   // equal work, event after each; make_pieces) so the download of band q overlaps band q+1.
@@ -1086,7 +1101,7 @@ static void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool la
       HS_CUDA(cudaGetLastError());
       ++e->launches;
       if (kt) HS_CUDA(cudaEventRecord(kt->s0, s));
-      launch_tri(e, cp.s, cp.grid_tri);
+      launch_tri(e, s_rest ? cp.sB : cp.s, cp.grid_tri);
       if (kt) HS_CUDA(cudaEventRecord(kt->s1, s));
     });
     if (last) HS_CUDA(cudaEventRecord(e->ev_s_done, s));
@@ -1141,6 +1156,12 @@ static void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool la
   }
 }
 
+// The first streamed chunk's A^H A half of S, enqueued as soon as its A rows landed (the
+// stream already waits for them): it overlaps the upload of B, T and U.
+static void enqueue_s_first(hsdla_b200_engine* e, ChunkPlan& cp) {
+  timed_op(e, HSDLA_B200_PHASE_S, [&] { launch_tri(e, cp.sA, cp.grid_tri); });
+}
+
 static bool valid_algo(int algo) {
   return algo == HSDLA_B200_ALGO_REFINED || algo == HSDLA_B200_ALGO_REFINED_FUSED ||
          algo == HSDLA_B200_ALGO_REFINED_MERGED || algo == HSDLA_B200_ALGO_ORIGINAL;
@@ -1187,23 +1208,38 @@ static void engine_build_streamed(hsdla_b200_engine* e, const hsdla_b200_problem
   // the slower-feed plan the HSDL file path uses)
   const char* pgp = std::getenv("HSDLA_B200_PAGEABLE_PLAN");
   auto& plan = pinned || !(pgp && std::strcmp(pgp, "pg") == 0) ? e->streamed : e->streamed_pg;
+  // The first chunk's S starts with its A^H A half as soon as A's rows landed, hiding part
+  // of the one upload nothing can overlap (not for the original algorithm, whose first
+  // phase needs B and T; HSDLA_B200_SPLIT_S=0 disables it for comparisons)
+  const char* sp = std::getenv("HSDLA_B200_SPLIT_S");
+  const bool split = algo != HSDLA_B200_ALGO_ORIGINAL && !(sp && *sp == '0');
   if (pinned) {
     // page-locked inputs: every chunk's copies are asynchronous, enqueue them all first
     for (size_t c = 0; c < plan.size(); ++c) {
-      upload_atoms(e, p, a0, plan[c].a0, plan[c].a1, e->copy_stream);
+      upload_atoms(e, p, a0, plan[c].a0, plan[c].a1, e->copy_stream, c == 0 && split ? e->ev_a0 : nullptr);
       HS_CUDA(cudaEventRecord(e->ev_chunk_up[c], e->copy_stream));
     }
   }
   for (size_t c = 0; c < plan.size(); ++c) {
+    const bool first_split = c == 0 && split;
+    if (first_split) {
+      if (!pinned) {
+        upload_atoms_staged(e, p, a0, plan[c].a0, plan[c].a1, e->copy_stream, 1);
+        HS_CUDA(cudaEventRecord(e->ev_a0, e->copy_stream));
+      }
+      HS_CUDA(cudaStreamWaitEvent(e->stream, e->ev_a0, 0));
+      HS_CUDA(cudaEventRecord(e->ev_begin, e->stream));
+      enqueue_s_first(e, plan[c]);
+    }
     if (!pinned) {
       // pageable inputs: the host packs chunk c into the pinned slabs while the GPU
       // already computes chunk c-1 (its phases were enqueued in the previous iteration)
-      upload_atoms_staged(e, p, a0, plan[c].a0, plan[c].a1, e->copy_stream);
+      upload_atoms_staged(e, p, a0, plan[c].a0, plan[c].a1, e->copy_stream, first_split ? 2 : 3);
       HS_CUDA(cudaEventRecord(e->ev_chunk_up[c], e->copy_stream));
     }
     HS_CUDA(cudaStreamWaitEvent(e->stream, e->ev_chunk_up[c], 0));
-    if (c == 0) HS_CUDA(cudaEventRecord(e->ev_begin, e->stream));
-    enqueue_chunk(e, plan[c], algo, c + 1 == plan.size(), nullptr);
+    if (c == 0 && !first_split) HS_CUDA(cudaEventRecord(e->ev_begin, e->stream));
+    enqueue_chunk(e, plan[c], algo, c + 1 == plan.size(), nullptr, first_split);
   }
   HS_CUDA(cudaEventRecord(e->ev_up1, e->copy_stream));
   HS_CUDA(cudaEventRecord(e->ev_end, e->stream));
