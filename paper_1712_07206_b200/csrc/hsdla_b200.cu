@@ -4,20 +4,20 @@
 // Device data layout (one engine per GPU / atom shard, all HBM-resident):
 //   A, B    K x N_G complex, column-major, ld = K (= the reference stacking,
 //           problem.hpp:20-21; uploaded with strided 2-D copies from the caller)
-//   X1      K x N_G: first U*B (phase s, diag_scale kernels.cpp:438-450), then
-//           T_AA A (hemm_loop, pipeline.cpp:314-321)
-//   X2      K x N_G: Z = T_AB^H A + 1/2 T_BB B (z_loop, pipeline.cpp:302-307)
+//   X1      K x N_G: first U*B (phase s, diag_scale kernels.cpp:438-450), then W_A
+//           (merged) or T_AA A (hemm_loop, pipeline.cpp:314-321)
+//   X2      K x N_G: W_B (merged) or Z = T_AB^H A + 1/2 T_BB B (z_loop, pipeline.cpp:302-307)
 //   Tab     raw per-atom T_AB blocks (used as-is: Z = T_AB^H A is a CTN product)
 //   Pbb,Paa 1/2 full(T_BB) (full(T_BB) for the merged algorithm), full(T_AA) expanded
 //           from the LOWER triangles only
 //   Pab     T_AB^H per atom (merged algorithm: W_A = T_AA A + T_AB B)
+//   Hp, Sp  packed-lower N_G(N_G+1)/2 complex (halves D2H and NCCL bytes)
 //
 // The merged algorithm (default) restates Algorithm 3 as one contraction per matrix:
 // per atom, H_a = Y_a^H M_a Y_a with Y_a = [A_a; B_a] and the Hermitian block operator
 // M_a = [[T_AA, T_AB], [T_AB^H, T_BB]] (the same sum pipeline.cpp:302-324 evaluates as
 // Z^H B + B^H Z + A^H (T_AA A)), so H = [A; B]^H [W_A; W_B] with W_A = T_AA A + T_AB B in
 // X1 and W_B = T_AB^H A + T_BB B in X2: 16 K N_G^2 contraction flops instead of 20.
-//   Hp, Sp  packed-lower N_G(N_G+1)/2 complex (halves D2H and NCCL bytes)
 //
 // A build is a list of atom CHUNKS.  The device-resident build is one chunk over
 // all atoms.  The streamed build (the one-shot drop-in with host buffers) splits
