@@ -398,3 +398,41 @@ def test_engine_download_overlap_matches_whole_build():
         e.sync()
         e.close()
     assert rel(out[1][0], out[0][0]) <= 1e-14 and rel(out[1][1], out[0][1]) <= 1e-14
+
+
+def test_no_device_or_host_leaks_across_many_calls(tmp_path):
+    """Many drop-in calls over varying shapes, algorithms, pinned / pageable inputs and a file,
+    then release_cache(): device memory returns to its starting level (engines, staging slabs,
+    the kernel layer's pooled temporaries and the file view are all released)."""
+    import torch
+    from paper_1712_07206_b200 import kernels as K
+    hb.release_cache()
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    rng = np.random.default_rng(5)
+    path = str(tmp_path / "p.hsdl")
+    for it in range(12):
+        na, nl, ng = int(rng.integers(1, 9)), int(rng.choice([5, 9, 25, 49])), int(rng.integers(40, 400))
+        p = hb.generate_problem(na, nl, ng, it + 1, int(rng.integers(0, na + 1)))
+        algo = ("merged", "fused", "refined")[it % 3]
+        if it % 4 == 3:
+            bufs = [p.A, p.B, p.T_AA, p.T_AB, p.T_BB, p.U]
+            for b in bufs:
+                hb.host_register(b)
+            try:
+                hb.build_hs_refined(p, hb.PipelineConfig(algo=algo))
+            finally:
+                for b in bufs:
+                    hb.host_unregister(b)
+        else:
+            hb.build_hs_refined(p, hb.PipelineConfig(algo=algo))
+        if it % 5 == 0:
+            hb.build_hs_original(p)
+            hb.save_problem(p, path)
+            hb.build_hs_file(path)
+            C = np.zeros((ng, ng), np.complex128, order="F")
+            K.herk(1.0, p.A, 0.0, C)
+    hb.release_cache()
+    torch.cuda.synchronize()
+    free1 = torch.cuda.mem_get_info()[0]
+    assert free1 >= free0 - (64 << 20), (free0, free1)
