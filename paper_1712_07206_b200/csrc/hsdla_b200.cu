@@ -445,7 +445,8 @@ struct hsdla_b200_engine {
   uint64_t setup_bytes = 0;
   void* lapw_scratch = nullptr;  // device copy of the LAPW inputs (grown on demand)
   // HSDL file reader: two pinned 64 MB staging slabs, allocated on first use
-  char* stage_buf[2] = {nullptr, nullptr};
+  static constexpr int kStageSlabs = 4;  // pinned staging slabs, used round robin (8 measured no better)
+  char* stage_buf[kStageSlabs] = {};
   // HSDL file view: a read-only mapping of the last file this engine loaded, kept while the
   // file's (device, inode, size, mtime) stay the same, so repeated k-point calls on one file
   // copy rows straight out of the page cache without a pread per column piece
@@ -454,8 +455,8 @@ struct hsdla_b200_engine {
   struct stat fmap_st {};
   double tr_pack_ms = 0, tr_wait_ms = 0;  // HSDLA_B200_TRACE: pageable staging accounting
   uint64_t tr_pack_bytes = 0;
-  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
-  bool stage_busy[2] = {false, false};
+  cudaEvent_t stage_ev[kStageSlabs] = {};
+  bool stage_busy[kStageSlabs] = {};
   int stage_next = 0;
   size_t lapw_scratch_bytes = 0;
   // roofline: events around the whole-build S and H contraction launches, harvested lazily
@@ -496,7 +497,7 @@ static void engine_free(hsdla_b200_engine* e) {
     if (p) cudaFree(p);
   if (e->host_stage) cudaFreeHost(e->host_stage);
   if (e->fmap) munmap(const_cast<char*>(e->fmap), e->fmap_len);
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < hsdla_b200_engine::kStageSlabs; ++i) {
     if (e->stage_ev[i]) {
       cudaEventSynchronize(e->stage_ev[i]);
       cudaEventDestroy(e->stage_ev[i]);
@@ -884,12 +885,12 @@ static double host_ms() {
 
 static char* stage_acquire(hsdla_b200_engine* e, int& slot) {
   if (!e->stage_buf[0])
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < hsdla_b200_engine::kStageSlabs; ++i) {
       HS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&e->stage_buf[i]), kStageSlab));
       HS_CUDA(cudaEventCreateWithFlags(&e->stage_ev[i], cudaEventDisableTiming));
     }
   slot = e->stage_next;
-  e->stage_next ^= 1;
+  e->stage_next = (e->stage_next + 1) % hsdla_b200_engine::kStageSlabs;
   if (e->stage_busy[slot]) {
     const double t0 = trace_on() ? host_ms() : 0.0;
     HS_CUDA(cudaEventSynchronize(e->stage_ev[slot]));
