@@ -141,7 +141,7 @@ int hsdla_b200_build_hs(const hsdla_b200_problem* p, const hsdla_b200_options* o
 int hsdla_b200_problem_file_info(const char* path, uint64_t* n_atoms, uint64_t* n_l, uint64_t* n_g, uint8_t* hpd);
 /* build_hs(load_problem(path), cfg) without a host ProblemInstance: every GPU
  * streams only its atom shard (A/B rows of each column, T blocks, U) from the file
- * into HBM through a pinned double buffer, in atom chunks overlapped with the build.
+ * into HBM through pinned staging slabs, in atom chunks overlapped with the build.
  * Rows are copied out of a read-only mapping of the file that the engine keeps while
  * the file's (device, inode, size, mtime) are unchanged; the file must not be
  * truncated during a call.  Same outputs / stats contract as hsdla_b200_build_hs
