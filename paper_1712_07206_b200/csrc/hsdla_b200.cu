@@ -2080,12 +2080,13 @@ __global__ void pack_lower_kernel(const double2* __restrict__ full, double2* __r
 }
 
 // Pinned staging ring per device for the kernel layer's host <-> device traffic
-// (page-locked double buffer, multi-threaded host packing): calls on one device are
-// serialised by its mutex.
+// (kRingSlabs page-locked slabs used round robin, multi-threaded host packing): calls on
+// one device are serialised by its mutex.
+static constexpr int kRingSlabs = 4;
 struct Ring {
   std::mutex mu;
-  char* buf[2] = {nullptr, nullptr};
-  cudaEvent_t ev[2] = {nullptr, nullptr};
+  char* buf[kRingSlabs] = {};
+  cudaEvent_t ev[kRingSlabs] = {};
 };
 static constexpr size_t kRingSlab = size_t(32) << 20;
 static Ring& ring_for(int device) {
@@ -2118,7 +2119,7 @@ struct Ctx {
     ring = &ring_for(device);
     lock = std::unique_lock<std::mutex>(ring->mu);
     if (!ring->buf[0])
-      for (int i = 0; i < 2; ++i) {
+      for (int i = 0; i < kRingSlabs; ++i) {
         HS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ring->buf[i]), kRingSlab));
         HS_CUDA(cudaEventCreateWithFlags(&ring->ev[i], cudaEventDisableTiming));
       }
@@ -2143,7 +2144,7 @@ struct Ctx {
     }
     const uint64_t per = kRingSlab / colb;
     int slot = 0;
-    for (uint64_t j0 = 0; j0 < c; j0 += per, slot ^= 1) {
+    for (uint64_t j0 = 0; j0 < c; j0 += per, slot = (slot + 1) % kRingSlabs) {
       const uint64_t nc = std::min(per, c - j0);
       HS_CUDA(cudaEventSynchronize(ring->ev[slot]));
       char* b = ring->buf[slot];
@@ -2167,15 +2168,16 @@ struct Ctx {
     const uint64_t pieces = (c + per - 1) / per;
     auto issue = [&](uint64_t q) {
       const uint64_t j0 = q * per, nc = std::min(per, c - j0);
-      HS_CUDA(cudaMemcpyAsync(ring->buf[q & 1], d + j0 * r, nc * colb, cudaMemcpyDeviceToHost, s));
-      HS_CUDA(cudaEventRecord(ring->ev[q & 1], s));
+      HS_CUDA(cudaMemcpyAsync(ring->buf[q % kRingSlabs], d + j0 * r, nc * colb, cudaMemcpyDeviceToHost, s));
+      HS_CUDA(cudaEventRecord(ring->ev[q % kRingSlabs], s));
     };
-    issue(0);
+    for (uint64_t q = 0; q + 1 < kRingSlabs && q < pieces; ++q) issue(q);
     for (uint64_t q = 0; q < pieces; ++q) {
-      if (q + 1 < pieces) issue(q + 1);  // the next slab lands while this one is unpacked
-      HS_CUDA(cudaEventSynchronize(ring->ev[q & 1]));
+      // the next slabs land while this one is unpacked (slab of q + kRingSlabs - 1 = q - 1's)
+      if (q + kRingSlabs - 1 < pieces) issue(q + kRingSlabs - 1);
+      HS_CUDA(cudaEventSynchronize(ring->ev[q % kRingSlabs]));
       const uint64_t j0 = q * per, nc = std::min(per, c - j0);
-      const char* b = ring->buf[q & 1];
+      const char* b = ring->buf[q % kRingSlabs];
       par_for(nc, nc * colb, [&](uint64_t j) { copy_nt(hc + (j0 + j) * ld, b + j * colb, colb); });
       _mm_sfence();
     }
@@ -2201,14 +2203,14 @@ struct Ctx {
       }
     auto issue = [&](uint64_t q) {
       const uint64_t b0 = pc(cuts[q]), b1 = pc(cuts[q + 1]);
-      HS_CUDA(cudaMemcpyAsync(ring->buf[q & 1], pk + b0, (b1 - b0) * 16, cudaMemcpyDeviceToHost, s));
-      HS_CUDA(cudaEventRecord(ring->ev[q & 1], s));
+      HS_CUDA(cudaMemcpyAsync(ring->buf[q % kRingSlabs], pk + b0, (b1 - b0) * 16, cudaMemcpyDeviceToHost, s));
+      HS_CUDA(cudaEventRecord(ring->ev[q % kRingSlabs], s));
     };
-    issue(0);
+    for (uint64_t q = 0; q + 1 < kRingSlabs && q < pieces; ++q) issue(q);
     for (uint64_t q = 0; q < pieces; ++q) {
-      if (q + 1 < pieces) issue(q + 1);
-      HS_CUDA(cudaEventSynchronize(ring->ev[q & 1]));
-      const double2* b = reinterpret_cast<const double2*>(ring->buf[q & 1]);
+      if (q + kRingSlabs - 1 < pieces) issue(q + kRingSlabs - 1);
+      HS_CUDA(cudaEventSynchronize(ring->ev[q % kRingSlabs]));
+      const double2* b = reinterpret_cast<const double2*>(ring->buf[q % kRingSlabs]);
       const uint64_t j0 = cuts[q], base = pc(j0), ncol = cuts[q + 1] - j0;
       par_for(ncol, (pc(cuts[q + 1]) - base) * 16,
               [&](uint64_t t) { copy_nt(hc + (j0 + t) * ldc + j0 + t, b + pc(j0 + t) - base, (n - j0 - t) * 16); });
