@@ -436,3 +436,18 @@ def test_no_device_or_host_leaks_across_many_calls(tmp_path):
     torch.cuda.synchronize()
     free1 = torch.cuda.mem_get_info()[0]
     assert free1 >= free0 - (64 << 20), (free0, free1)
+
+
+def test_first_chunk_split_s_matches_unsplit(monkeypatch):
+    """The streamed drop-in starts the first chunk's S with its A^H A half on A's rows alone
+    (HSDLA_B200_SPLIT_S=0 turns it off): both orders agree to FP64 rounding."""
+    p = hb.generate_problem(24, 81, 1200, 6, 0)
+    out = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("HSDLA_B200_SPLIT_S", flag)
+        monkeypatch.setenv("HSDLA_B200_STREAM_PLAN", "3,7,14")
+        hb.release_cache()
+        out.append(hb.build_hs_refined(p))
+    hb.release_cache()
+    assert rel(out[0].S, out[1].S) <= 1e-14 and rel(out[0].H, out[1].H) <= 1e-14
+    assert out[0].stats["kernel_launches"] == out[1].stats["kernel_launches"] + 1
