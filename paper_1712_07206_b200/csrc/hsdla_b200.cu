@@ -35,7 +35,13 @@
 #include <sys/stat.h>
 #include <unistd.h>
 
+#if defined(__x86_64__) || defined(__i386__)
 #include <immintrin.h>
+#define HSDLA_B200_NT_STORES 1
+#else  // other hosts (e.g. Grace): plain copies, no fence needed
+#define HSDLA_B200_NT_STORES 0
+static inline void _mm_sfence() {}
+#endif
 
 #include <algorithm>
 #include <atomic>
@@ -203,6 +209,9 @@ class HostPool {
 // write of the bytes instead of read + read + write -- the host memory bandwidth the
 // concurrent DMA also needs.  Callers fence (sfence) before publishing the data.
 static void copy_nt(void* dst, const void* src, size_t bytes) {
+#if !HSDLA_B200_NT_STORES
+  std::memcpy(dst, src, bytes);
+#else
   char* d = static_cast<char*>(dst);
   const char* s = static_cast<const char*>(src);
   // head: up to the next 16-byte boundary of the destination
@@ -224,6 +233,7 @@ static void copy_nt(void* dst, const void* src, size_t bytes) {
   }
   for (; n; --n, ++dv, ++sv) _mm_stream_si128(dv, _mm_loadu_si128(sv));
   std::memcpy(dv, sv, bytes & 15);
+#endif
 }
 
 // fn(i) for i in [0, n), in `parts` contiguous ranges on the host pool when the work
