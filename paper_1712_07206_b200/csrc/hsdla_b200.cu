@@ -436,7 +436,9 @@ struct hsdla_b200_engine {
   std::vector<hsdla_b200::OpTime> ops;
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr, ev_s_done = nullptr, ev_s_red = nullptr,
               ev_reduce_end = nullptr, ev_up0 = nullptr, ev_up1 = nullptr, ev_s_d2h = nullptr,
-              ev_a0 = nullptr;  // the first streamed chunk's A rows landed
+              ev_a0 = nullptr,   // the first streamed chunk's A rows landed
+              ev_ops = nullptr;  // operators uploaded on the copy stream (engine_upload_operators)
+  bool ops_pending = false;      // the next build must wait for ev_ops before expanding T
   static constexpr int kD2hPieces = 8;   // H downloads in column-range pieces, unpacked as each lands
   cudaEvent_t ev_h_piece[kD2hPieces] = {};
   cudaEvent_t ev_h_band[kD2hPieces] = {};  // final H contraction finished tile-column band q
@@ -522,7 +524,7 @@ static void engine_free(hsdla_b200_engine* e) {
     if (ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e->ev_h_red)
     if (ev) cudaEventDestroy(ev);
-  for (cudaEvent_t ev : {e->ev_a0, e->ev_begin, e->ev_end, e->ev_s_done, e->ev_s_red, e->ev_reduce_end, e->ev_up0, e->ev_up1,
+  for (cudaEvent_t ev : {e->ev_a0, e->ev_ops, e->ev_begin, e->ev_end, e->ev_s_done, e->ev_s_red, e->ev_reduce_end, e->ev_up0, e->ev_up1,
                          e->ev_s_d2h, e->ev_setup0, e->ev_setup1, e->ev_setup_mid})
     if (ev) cudaEventDestroy(ev);
   for (auto& t : e->ring)
@@ -795,7 +797,7 @@ static hsdla_b200_engine* engine_create(int device, uint64_t na, uint64_t nl, ui
     for (cudaEvent_t* ev : {&e->ev_begin, &e->ev_end, &e->ev_reduce_end, &e->ev_up0, &e->ev_up1, &e->ev_setup0,
                             &e->ev_setup1, &e->ev_setup_mid})
       HS_CUDA(cudaEventCreate(ev));
-    for (cudaEvent_t* ev : {&e->ev_s_done, &e->ev_s_red, &e->ev_s_d2h, &e->ev_a0})
+    for (cudaEvent_t* ev : {&e->ev_s_done, &e->ev_s_red, &e->ev_s_d2h, &e->ev_a0, &e->ev_ops})
       HS_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     for (cudaEvent_t& ev : e->ev_h_piece) HS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     for (cudaEvent_t& ev : e->ev_h_band) HS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -1105,9 +1107,13 @@ static void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool la
     HS_CUDA(cudaGetLastError());
     ++e->launches;
   };
-  auto phase_s = [&](bool with_expand) {
+  // operators uploaded on the copy stream (engine_upload_operators): wait before expanding
+  auto expand_ops = [&] {
+    if (e->ops_pending) HS_CUDA(cudaStreamWaitEvent(s, e->ev_ops, 0));
+    expand();
+  };
+  auto phase_s = [&] {
     timed_op(e, HSDLA_B200_PHASE_S, [&] {
-      if (with_expand) expand();
       diag_scale_kernel<<<g_rows, 256, 0, s>>>(e->B + r0, e->U + r0, e->X1 + r0, Kc, e->K, ng);
       HS_CUDA(cudaGetLastError());
       ++e->launches;
@@ -1127,11 +1133,11 @@ static void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool la
   };
   if (algo == HSDLA_B200_ALGO_ORIGINAL) {
     timed_op(e, HSDLA_B200_PHASE_Z_LOOP, [&] {
-      expand();
+      expand_ops();
       launch_bat(e, cp.z, cp.grid_bat);
     });
     timed_op(e, HSDLA_B200_PHASE_HER2K, [&] { timed_h(cp.h2k, false); });
-    phase_s(false);
+    phase_s();
     timed_op(e, HSDLA_B200_PHASE_CHOL_LOOP, [&] {
       if (cp.a0 == 0) HS_CUDA(cudaMemsetAsync(e->n_fail, 0, sizeof(int), s));  // first chunk of the build
       potrf_batched_kernel<<<static_cast<unsigned>(nac), 128, 0, s>>>(e->Taa + cp.a0 * nl * nl,
@@ -1148,20 +1154,29 @@ static void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool la
     timed_op(e, HSDLA_B200_PHASE_H_AA_UPDATE, [&] { final_h(cp.haa); });
     return;
   }
-  phase_s(true);
+  // S needs no operator: it runs before the expansion (and, after an operator upload on the
+  // copy stream, while the operators travel)
+  phase_s();
   if (algo == HSDLA_B200_ALGO_REFINED) {
-    timed_op(e, HSDLA_B200_PHASE_Z_LOOP, [&] { launch_bat(e, cp.z, cp.grid_bat); });
+    timed_op(e, HSDLA_B200_PHASE_Z_LOOP, [&] {
+      expand_ops();
+      launch_bat(e, cp.z, cp.grid_bat);
+    });
     timed_op(e, HSDLA_B200_PHASE_HER2K, [&] { timed_h(cp.h2k, false); });
     timed_op(e, HSDLA_B200_PHASE_HEMM_LOOP, [&] { launch_bat(e, cp.x, cp.grid_bat); });
     timed_op(e, HSDLA_B200_PHASE_HERKX, [&] { final_h(cp.hkx); });
   } else if (algo == HSDLA_B200_ALGO_REFINED_MERGED) {
     timed_op(e, HSDLA_B200_PHASE_Z_LOOP, [&] {
+      expand_ops();
       launch_bat(e, cp.wa, cp.grid_bat);
       launch_bat(e, cp.wb, cp.grid_bat);
     });
     timed_op(e, HSDLA_B200_PHASE_HER2K, [&] { timed_h(cp.hm, true); });  // her2k + herkx merged
   } else {
-    timed_op(e, HSDLA_B200_PHASE_Z_LOOP, [&] { launch_bat(e, cp.zf, cp.grid_bat); });
+    timed_op(e, HSDLA_B200_PHASE_Z_LOOP, [&] {
+      expand_ops();
+      launch_bat(e, cp.zf, cp.grid_bat);
+    });
     timed_op(e, HSDLA_B200_PHASE_HEMM_LOOP, [&] { launch_bat(e, cp.x, cp.grid_bat); });
     timed_op(e, HSDLA_B200_PHASE_HER2K, [&] { timed_h(cp.h, true); });  // her2k + herkx fused
   }
@@ -1201,6 +1216,7 @@ static void engine_build(hsdla_b200_engine* e, int algo) {
   kt.flops_h = (algo == HSDLA_B200_ALGO_REFINED_FUSED ? 12 : 8) * e->K * e->ng * e->ng;
   HS_CUDA(cudaEventRecord(e->ev_begin, e->stream));
   enqueue_chunk(e, e->whole[0], algo, true, &kt);
+  e->ops_pending = false;
   HS_CUDA(cudaEventRecord(e->ev_end, e->stream));
   kt.pending = true;
 }
@@ -1562,12 +1578,15 @@ static void engine_upload_operators(hsdla_b200_engine* e, const double* taa, con
   HS_CUDA(cudaSetDevice(e->device));
   const uint64_t blk = e->nl * e->nl;
   const size_t bytes = e->na * blk * sizeof(double2);
-  HS_CUDA(cudaMemcpyAsync(e->Taa, reinterpret_cast<const double2*>(taa) + a0 * blk, bytes, cudaMemcpyHostToDevice,
-                          e->stream));
-  HS_CUDA(cudaMemcpyAsync(e->Tab, reinterpret_cast<const double2*>(tab) + a0 * blk, bytes, cudaMemcpyHostToDevice,
-                          e->stream));
-  HS_CUDA(cudaMemcpyAsync(e->Tbb, reinterpret_cast<const double2*>(tbb) + a0 * blk, bytes, cudaMemcpyHostToDevice,
-                          e->stream));
+  // on the copy stream, so the next build's S contraction (which needs no operator) runs
+  // while they travel; the build waits for ev_ops before its operator expansion
+  cudaStream_t cs = e->copy_stream;
+  HS_CUDA(cudaStreamWaitEvent(cs, e->ev_end, 0));  // the previous build is done with T
+  HS_CUDA(cudaMemcpyAsync(e->Taa, reinterpret_cast<const double2*>(taa) + a0 * blk, bytes, cudaMemcpyHostToDevice, cs));
+  HS_CUDA(cudaMemcpyAsync(e->Tab, reinterpret_cast<const double2*>(tab) + a0 * blk, bytes, cudaMemcpyHostToDevice, cs));
+  HS_CUDA(cudaMemcpyAsync(e->Tbb, reinterpret_cast<const double2*>(tbb) + a0 * blk, bytes, cudaMemcpyHostToDevice, cs));
+  HS_CUDA(cudaEventRecord(e->ev_ops, cs));
+  e->ops_pending = true;
 }
 
 // ---------------------------------------------------------------------------
