@@ -305,7 +305,10 @@ typedef struct hsdla_b200_lapw {
 int hsdla_b200_lapw_coefficients(int device, const hsdla_b200_lapw* sys, double* A, double* B, double* U);
 /* Fill the engine's A, B, U for its shard [atom_begin, atom_begin + n_atoms_local) in HBM. */
 int hsdla_b200_engine_setup_lapw(hsdla_b200_engine* e, const hsdla_b200_lapw* sys, uint64_t atom_begin);
-/* H2D of the shard's T_AA, T_AB, T_BB blocks only (with setup_lapw: a build needs no A/B upload). */
+/* H2D of the shard's T_AA, T_AB, T_BB blocks only (with setup_lapw: a build needs no A/B upload).
+ * Asynchronous, on the engine's copy stream (after the previous build is done with T); the next
+ * build's S contraction runs meanwhile and its operator expansion waits for the copies.  Page-
+ * locked sources must stay valid until that build has been synchronised. */
 int hsdla_b200_engine_upload_operators(hsdla_b200_engine* e, const double* T_AA, const double* T_AB,
                                        const double* T_BB, uint64_t atom_begin);
 /* CUDA-event times (ms) of the last setup_lapw: both kernels (ms) and the HBM-write

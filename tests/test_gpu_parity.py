@@ -451,3 +451,28 @@ def test_first_chunk_split_s_matches_unsplit(monkeypatch):
     hb.release_cache()
     assert rel(out[0].S, out[1].S) <= 1e-14 and rel(out[0].H, out[1].H) <= 1e-14
     assert out[0].stats["kernel_launches"] == out[1].stats["kernel_launches"] + 1
+
+
+@pytest.mark.parametrize("algo", ["merged", "fused", "refined", "original"])
+def test_operators_uploaded_on_the_copy_stream(algo):
+    """engine_upload_operators copies T on the copy stream (the build's S runs meanwhile and
+    waits for them only before the operator expansion): re-uploading new operators between
+    two builds of one engine gives each build its own operators' result."""
+    p = hb.generate_problem(6, 25, 300, 4, 2)
+    q = hb.generate_problem(6, 25, 300, 5, 2)  # other operators, same shape
+    want_p = hb.build_hs(p, hb.PipelineConfig(variant="original") if algo == "original" else
+                         hb.PipelineConfig(algo=algo))
+    q.A, q.B, q.U = p.A, p.B, p.U              # same coefficients, q's operators
+    want_q = hb.build_hs(q, hb.PipelineConfig(variant="original") if algo == "original" else
+                         hb.PipelineConfig(algo=algo))
+    e = hb.Engine(0, p.n_atoms, p.n_l, p.n_g)
+    e.upload(p)
+    got = []
+    for prob in (q, p, q):
+        e.upload_operators(prob.T_AA, prob.T_AB, prob.T_BB)
+        e.build(algo)
+        got.append(e.download())
+    e.sync()
+    e.close()
+    for (H, S), want in zip(got, (want_q, want_p, want_q)):
+        assert rel(H, want.H) <= 1e-13 and rel(S, want.S) <= 1e-13
