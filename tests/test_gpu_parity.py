@@ -5,6 +5,8 @@ Bar (north_star): relative Frobenius error of the lower triangle <= 1e-11 on H a
 behavioural contract: upper triangle never written, diagonal imag 0,
 T_AA/T_BB read from the lower triangle only, ledger == flop_model, five phases.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -94,6 +96,21 @@ def test_config1_full_vs_oracle():
         Hr, Sr, _ = Restatement().build_hs_refined(p)
     assert rel(r.H, Hr) <= TOL and rel(r.S, Sr) <= TOL
     assert r.ledger == hb.flop_model(p)
+
+
+def test_config2_full_vs_unmodified_reference():
+    """Config 2 (64 atoms, lmax 8, N_G 3000), the bench workload, in full against the
+    unmodified reference's own CPU run (oracle/_ref, BlockedParallel on every host core,
+    ~20 s on the GPU box), for the default (merged) and the reference-order algorithms."""
+    from oracle.oracle import Reference
+    if not Reference.available():
+        pytest.skip("oracle/_ref not built")
+    p = hb.generate_problem(64, 81, 3000, 1, 0)
+    ref = Reference().build_hs(p, "refined", threads=os.cpu_count() or 1, blocked=True)
+    for algo in ("merged", "refined"):
+        r = hb.build_hs_refined(p, hb.PipelineConfig(algo=algo))
+        assert rel(r.H, ref["H"]) <= TOL and rel(r.S, ref["S"]) <= TOL, algo
+        assert r.ledger == hb.flop_model(p)
 
 
 @pytest.mark.parametrize("dims", [(64, 81, 3000), (108, 121, 6000), (512, 121, 13000)],
