@@ -134,6 +134,17 @@ typedef struct hsdla_b200_stats {
 int hsdla_b200_build_hs(const hsdla_b200_problem* p, const hsdla_b200_options* opts, double* H,
                         double* S, hsdla_b200_stats* stats);
 
+/* n_k k-points of one cell in one call (an extension beside the per-k-point drop-in): the
+ * operators and U of `common` are k-independent and uploaded once; A[k], B[k] (same layout as
+ * hsdla_b200_problem.A/B, common->A/B unused) give each k-point's coefficients and H[k], S[k]
+ * receive its lower triangles.  On one GPU (opts->n_gpus <= 1): while k-point k builds, k+1's
+ * A, B are uploaded and k-1's H, S downloaded and unpacked, so the per-k-point cost approaches
+ * the device-resident build.  Results equal n_k hsdla_b200_build_hs calls to FP64 rounding
+ * (the per-call path chunks its uploads).  stats: the last k-point's, total_seconds = batch. */
+int hsdla_b200_build_hs_kpoints(const hsdla_b200_problem* common, uint64_t n_k, const double* const* A,
+                                const double* const* B, const hsdla_b200_options* opts, double* const* H,
+                                double* const* S, hsdla_b200_stats* stats);
+
 /* ---- HSDL v1 problem files (problem.cpp:144-243) ---------------------------
  * Header of a file written by the reference's save_problem: dims and, when hpd
  * is non-NULL, n_atoms hpd flags.  Bad magic / version / truncation / missing

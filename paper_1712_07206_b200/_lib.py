@@ -35,7 +35,7 @@ EXPORTS = (
     "hsdla_b200_engine_load", "hsdla_b200_engine_fill_synthetic",
     "hsdla_b200_herk", "hsdla_b200_her2k", "hsdla_b200_herkx", "hsdla_b200_gemm", "hsdla_b200_hemm",
     "hsdla_b200_trmm", "hsdla_b200_diag_scale", "hsdla_b200_engine_set_arith", "hsdla_b200_set_default_arith",
-    "hsdla_b200_engine_set_download_overlap",
+    "hsdla_b200_engine_set_download_overlap", "hsdla_b200_build_hs_kpoints",
 )
 
 

@@ -430,6 +430,13 @@ struct hsdla_b200_engine {
   int nranks = 1, rank = 0;
 
   std::vector<hsdla_b200::ChunkPlan> whole, streamed, streamed_pg;  // streamed: pinned / pageable feed
+  // k-point batches (hsdla_b200_build_hs_kpoints): a second A/B set and its plan, an upload
+  // stream, per-set events; wait_before_* make the next enqueue_chunk wait (S / H storage reuse)
+  double2 *A2 = nullptr, *B2 = nullptr;
+  std::vector<hsdla_b200::ChunkPlan> whole2;
+  cudaStream_t h2d_stream = nullptr;
+  cudaEvent_t ev_kup[2] = {}, ev_kbuilt[2] = {};
+  cudaEvent_t wait_before_s = nullptr, wait_before_h = nullptr;
   // per-build timing
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
@@ -505,10 +512,13 @@ static void engine_free(hsdla_b200_engine* e) {
   cudaSetDevice(e->device);
   for (void* p : {e->lapw_scratch, (void*)e->info, (void*)e->n_fail, (void*)e->sk_ws, (void*)e->sk_flags, (void*)e->A, (void*)e->B, (void*)e->X1, (void*)e->X2,
                   (void*)e->Tab, (void*)e->Taa, (void*)e->Tbb, (void*)e->Paa, (void*)e->Pbb, (void*)e->Pab, (void*)e->U,
-                  (void*)e->Hp, (void*)e->Sp})
+                  (void*)e->Hp, (void*)e->Sp, (void*)e->A2, (void*)e->B2})
     if (p) cudaFree(p);
   if (e->host_stage) cudaFreeHost(e->host_stage);
   if (e->fmap) munmap(const_cast<char*>(e->fmap), e->fmap_len);
+  for (cudaEvent_t ev : {e->ev_kup[0], e->ev_kup[1], e->ev_kbuilt[0], e->ev_kbuilt[1]})
+    if (ev) cudaEventDestroy(ev);
+  if (e->h2d_stream) cudaStreamDestroy(e->h2d_stream);
   for (int i = 0; i < hsdla_b200_engine::kStageSlabs; ++i) {
     if (e->stage_ev[i]) {
       cudaEventSynchronize(e->stage_ev[i]);
@@ -842,16 +852,20 @@ static void check_problem(const hsdla_b200_engine* e, const hsdla_b200_problem* 
 }
 
 // H2D of local atoms [b0, b1) (engine-local indices) of shard a0 of p, on stream s.
+// parts: 1 = A rows, 2 = B rows, 4 = operator blocks + U (7: everything)
 static void upload_atoms(hsdla_b200_engine* e, const hsdla_b200_problem* p, uint64_t a0, uint64_t b0, uint64_t b1,
-                         cudaStream_t s, cudaEvent_t ev_a = nullptr) {
+                         cudaStream_t s, cudaEvent_t ev_a = nullptr, int parts = 7) {
   const uint64_t Kg = p->n_atoms * p->n_l;  // caller's leading dimension
   const uint64_t nl = e->nl, r0 = b0 * nl, rows = (b1 - b0) * nl, g0 = (a0 + b0) * nl;
   const size_t width = rows * sizeof(double2);
-  HS_CUDA(cudaMemcpy2DAsync(e->A + r0, e->K * sizeof(double2), reinterpret_cast<const double2*>(p->A) + g0,
-                            Kg * sizeof(double2), width, e->ng, cudaMemcpyHostToDevice, s));
+  if (parts & 1)
+    HS_CUDA(cudaMemcpy2DAsync(e->A + r0, e->K * sizeof(double2), reinterpret_cast<const double2*>(p->A) + g0,
+                              Kg * sizeof(double2), width, e->ng, cudaMemcpyHostToDevice, s));
   if (ev_a) HS_CUDA(cudaEventRecord(ev_a, s));
-  HS_CUDA(cudaMemcpy2DAsync(e->B + r0, e->K * sizeof(double2), reinterpret_cast<const double2*>(p->B) + g0,
-                            Kg * sizeof(double2), width, e->ng, cudaMemcpyHostToDevice, s));
+  if (parts & 2)
+    HS_CUDA(cudaMemcpy2DAsync(e->B + r0, e->K * sizeof(double2), reinterpret_cast<const double2*>(p->B) + g0,
+                              Kg * sizeof(double2), width, e->ng, cudaMemcpyHostToDevice, s));
+  if (!(parts & 4)) return;
   const uint64_t blk = nl * nl;
   const size_t tbytes = (b1 - b0) * blk * sizeof(double2);
   const uint64_t t0 = (a0 + b0) * blk;
@@ -930,9 +944,9 @@ static bool is_pinned(const void* p, size_t bytes) {
 // upload_atoms for PAGEABLE caller buffers: the rows of atoms [b0, b1) are packed by up
 // to 16 host threads into the engine's pinned staging slabs and copied from there
 // (a pageable cudaMemcpy is host-synchronous and single-threaded, ~10 GB/s).
-// parts: 1 = A rows, 2 = B rows + operator blocks + U, 3 = all
+// parts: 1 = A rows, 2 = B rows, 4 = operator blocks + U (7: everything)
 static void upload_atoms_staged(hsdla_b200_engine* e, const hsdla_b200_problem* p, uint64_t a0, uint64_t b0,
-                                uint64_t b1, cudaStream_t s, int parts = 3) {
+                                uint64_t b1, cudaStream_t s, int parts = 7) {
   const uint64_t Kg = p->n_atoms * p->n_l, nl = e->nl, ng = e->ng;
   const uint64_t r0 = b0 * nl, rows = (b1 - b0) * nl, g0 = (a0 + b0) * nl;
   const size_t colb = rows * sizeof(double2);
@@ -962,7 +976,7 @@ static void upload_atoms_staged(hsdla_b200_engine* e, const hsdla_b200_problem* 
       stage_release(e, slot, s);
     }
   }
-  if (!(parts & 2)) return;
+  if (!(parts & 4)) return;
   // operator blocks (T_AA, T_AB, T_BB per atom), then U, through the slabs: groups of
   // atoms whose three blocks fit one slab (large chunks of large-N_L atoms need several)
   const uint64_t blk = nl * nl, bb = blk * sizeof(double2);
@@ -1068,6 +1082,7 @@ static void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool la
   // The build's final H contraction: whole, or band by band (tile-column bands of
   // equal work, event after each; make_pieces) so the download of band q overlaps band q+1.
   auto final_h = [&](const CtnParams& P) {
+    if (e->wait_before_h) HS_CUDA(cudaStreamWaitEvent(s, e->wait_before_h, 0));  // H storage reuse
     // bands: the one-shot drop-in (download overlaps) and every multi-rank build (the
     // NCCL reduce of band q overlaps the compute of band q+1)
     // (only with >= 4 tile waves: smaller final launches would mostly be stream-K tails)
@@ -1114,6 +1129,7 @@ static void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool la
   };
   auto phase_s = [&] {
     timed_op(e, HSDLA_B200_PHASE_S, [&] {
+      if (e->wait_before_s) HS_CUDA(cudaStreamWaitEvent(s, e->wait_before_s, 0));
       diag_scale_kernel<<<g_rows, 256, 0, s>>>(e->B + r0, e->U + r0, e->X1 + r0, Kc, e->K, ng);
       HS_CUDA(cudaGetLastError());
       ++e->launches;
@@ -1124,6 +1140,7 @@ static void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool la
     if (last) HS_CUDA(cudaEventRecord(e->ev_s_done, s));
   };
   auto timed_h = [&](CtnParams& P, bool final) {
+    if (e->wait_before_h) HS_CUDA(cudaStreamWaitEvent(s, e->wait_before_h, 0));  // H storage reuse
     if (kt) HS_CUDA(cudaEventRecord(kt->h0, s));
     if (final)
       final_h(P);
@@ -1261,7 +1278,7 @@ static void engine_build_streamed(hsdla_b200_engine* e, const hsdla_b200_problem
     if (!pinned) {
       // pageable inputs: the host packs chunk c into the pinned slabs while the GPU
       // already computes chunk c-1 (its phases were enqueued in the previous iteration)
-      upload_atoms_staged(e, p, a0, plan[c].a0, plan[c].a1, e->copy_stream, first_split ? 2 : 3);
+      upload_atoms_staged(e, p, a0, plan[c].a0, plan[c].a1, e->copy_stream, first_split ? 6 : 7);
       HS_CUDA(cudaEventRecord(e->ev_chunk_up[c], e->copy_stream));
     }
     HS_CUDA(cudaStreamWaitEvent(e->stream, e->ev_chunk_up[c], 0));
@@ -1278,6 +1295,97 @@ static void engine_build_streamed(hsdla_b200_engine* e, const hsdla_b200_problem
     e->tr_pack_ms = e->tr_wait_ms = 0;
     e->tr_pack_bytes = 0;
   }
+}
+
+static void enqueue_download(hsdla_b200_engine* e);
+static void finish_download(hsdla_b200_engine* e, double* H, double* S, std::chrono::steady_clock::time_point t0);
+
+// ---- k-point batches -----------------------------------------------------------------
+// The second A/B set, the upload stream and the plan over the second set (rebuilt every
+// batch: X2 may have appeared since).
+static void ensure_kpoints(hsdla_b200_engine* e, int algo) {
+  if (algo != HSDLA_B200_ALGO_REFINED) ensure_x2(e);
+  if (!e->A2) {
+    HS_CUDA(cudaStreamSynchronize(e->stream));
+    dalloc(e, &e->A2, e->K * e->ng);
+    dalloc(e, &e->B2, e->K * e->ng);
+    HS_CUDA(cudaStreamCreateWithFlags(&e->h2d_stream, cudaStreamNonBlocking));
+    for (cudaEvent_t* ev : {&e->ev_kup[0], &e->ev_kup[1], &e->ev_kbuilt[0], &e->ev_kbuilt[1]})
+      HS_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
+  }
+  std::swap(e->A, e->A2);
+  std::swap(e->B, e->B2);
+  e->whole2.resize(1);
+  make_chunk(e, 0, e->na, true, e->whole2[0]);
+  std::swap(e->A, e->A2);
+  std::swap(e->B, e->B2);
+}
+
+// n_k k-points of one cell: the operators and U are k-independent (uploaded once), A_k and B_k
+// alternate between two device sets.  While k-point k builds, the next one's A, B go up on
+// the upload stream (or are packed into the staging slabs by the host) and k-1's H, S come
+// down and are unpacked; the per-k-point cost approaches the device-resident build.
+static void engine_kpoints(hsdla_b200_engine* e, const hsdla_b200_problem* common, uint64_t nk,
+                           const double* const* A, const double* const* B, int algo, double* const* H,
+                           double* const* S) {
+  ensure_kpoints(e, algo);
+  upload_atoms(e, common, 0, 0, e->na, e->stream, nullptr, 4);  // T and U, once
+  const size_t ab_bytes = e->K * e->ng * sizeof(double2);
+  auto upload = [&](uint64_t k) {
+    hsdla_b200_problem pk = *common;
+    pk.A = A[k];
+    pk.B = B[k];
+    const int set = static_cast<int>(k & 1);
+    HS_CUDA(cudaStreamWaitEvent(e->h2d_stream, e->ev_kbuilt[set], 0));  // k-2 is done with this set
+    if (set) {
+      std::swap(e->A, e->A2);
+      std::swap(e->B, e->B2);
+    }
+    if (is_pinned(A[k], ab_bytes) && is_pinned(B[k], ab_bytes))
+      upload_atoms(e, &pk, 0, 0, e->na, e->h2d_stream, nullptr, 3);
+    else
+      upload_atoms_staged(e, &pk, 0, 0, e->na, e->h2d_stream, 3);
+    if (set) {
+      std::swap(e->A, e->A2);
+      std::swap(e->B, e->B2);
+    }
+    HS_CUDA(cudaEventRecord(e->ev_kup[set], e->h2d_stream));
+  };
+  upload(0);
+  for (uint64_t k = 0; k < nk; ++k) {
+    const int set = static_cast<int>(k & 1);
+    begin_build(e, algo);
+    e->band_final_h = true;
+    HS_CUDA(cudaStreamWaitEvent(e->stream, e->ev_kup[set], 0));
+    HS_CUDA(cudaEventRecord(e->ev_begin, e->stream));
+    // S and H storage: k-1's downloads (enqueued in the previous iteration) first
+    e->wait_before_s = k ? e->ev_s_d2h : nullptr;
+    e->wait_before_h = k ? e->ev_h_piece[hsdla_b200_engine::kD2hPieces - 1] : nullptr;
+    // the set's buffers also for the launches that take raw pointers (diag_scale, select_left)
+    if (set) {
+      std::swap(e->A, e->A2);
+      std::swap(e->B, e->B2);
+    }
+    enqueue_chunk(e, set ? e->whole2[0] : e->whole[0], algo, true, nullptr);
+    if (set) {
+      std::swap(e->A, e->A2);
+      std::swap(e->B, e->B2);
+    }
+    e->wait_before_s = e->wait_before_h = nullptr;
+    e->band_final_h = false;
+    HS_CUDA(cudaEventRecord(e->ev_kbuilt[set], e->stream));
+    HS_CUDA(cudaEventRecord(e->ev_end, e->stream));
+    const double t_enq = trace_on() ? host_ms() : 0.0;
+    if (k + 1 < nk) upload(k + 1);                  // overlaps build k
+    const double t_up = trace_on() ? host_ms() : 0.0;
+    if (k) finish_download(e, H[k - 1], S[k - 1], std::chrono::steady_clock::now());  // overlaps build k
+    enqueue_download(e);
+    if (trace_on())
+      std::fprintf(stderr, "[hsdla_b200 trace] k-point %llu: build enqueued %.2f, upload enqueued +%.2f, "
+                   "previous download finished +%.2f ms\n", static_cast<unsigned long long>(k), t_enq,
+                   t_up - t_enq, host_ms() - t_up);
+  }
+  finish_download(e, H[nk - 1], S[nk - 1], std::chrono::steady_clock::now());
 }
 
 // NCCL sum-reduce of the packed partials to `root`, split so S's reduce overlaps the
@@ -2679,6 +2787,46 @@ int hsdla_b200_build_hs(const hsdla_b200_problem* p, const hsdla_b200_options* o
       engine_build_streamed(e, p, a0, algo);
       return 0.0;
     });
+  });
+}
+
+int hsdla_b200_build_hs_kpoints(const hsdla_b200_problem* common, uint64_t n_k, const double* const* A,
+                                const double* const* B, const hsdla_b200_options* o, double* const* H,
+                                double* const* S, hsdla_b200_stats* st) {
+  return guarded([&] {
+    const auto t0 = std::chrono::steady_clock::now();
+    if (!common) throw Fail{HSDLA_B200_DIMENSION_ERROR, "null problem"};
+    check_dims(common->n_atoms, common->n_l, common->n_g);
+    if (!common->T_AA || !common->T_AB || !common->T_BB || !common->U)
+      throw Fail{HSDLA_B200_DIMENSION_ERROR, "null operator / U pointer"};
+    if (n_k == 0) return;
+    if (!A || !B || !H || !S) throw Fail{HSDLA_B200_DIMENSION_ERROR, "null k-point array"};
+    for (uint64_t k = 0; k < n_k; ++k)
+      if (!A[k] || !B[k] || !H[k] || !S[k]) throw Fail{HSDLA_B200_DIMENSION_ERROR, "null k-point buffer"};
+    if (o && o->n_gpus > 1) throw Fail{HSDLA_B200_CONFIG_ERROR, "k-point batches run on one GPU"};
+    const int algo = o ? o->algo : HSDLA_B200_ALGO_REFINED_MERGED;
+    if (!valid_algo(algo)) throw Fail{HSDLA_B200_CONFIG_ERROR, "unknown algo " + std::to_string(algo)};
+    if (o && (o->flags & ~HSDLA_B200_FLAG_ARITH_4M)) throw Fail{HSDLA_B200_CONFIG_ERROR, "unknown option flags"};
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+      (void)cudaGetLastError();
+      throw Fail{HSDLA_B200_CONFIG_ERROR, "no CUDA device visible (the B200 path has no CPU fallback)"};
+    }
+    const int dev = o && o->device_ids ? o->device_ids[0] : 0;
+    if (dev < 0 || dev >= ndev) throw Fail{HSDLA_B200_CONFIG_ERROR, "device id out of range"};
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    hsdla_b200_engine* e = get_engines({dev}, common->n_atoms, common->n_l, common->n_g)->engines[0];
+    HS_CUDA(cudaSetDevice(e->device));
+    e->arith = o && (o->flags & HSDLA_B200_FLAG_ARITH_4M) ? HSDLA_B200_ARITH_4M : HSDLA_B200_ARITH_3M;
+    engine_kpoints(e, common, n_k, A, B, algo, H, S);
+    if (st) {
+      engine_sync(e, st);  // the last k-point's device stats
+      st->total_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      flop_model(algo == HSDLA_B200_ALGO_ORIGINAL ? 0 : 1, common->n_atoms, common->n_l, common->n_g, st->n_hpd,
+                 st->ledger);
+    } else {
+      HS_CUDA(cudaStreamSynchronize(e->stream));
+    }
   });
 }
 

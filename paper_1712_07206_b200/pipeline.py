@@ -173,6 +173,38 @@ def build_hs_refined(p, cfg: Optional[PipelineConfig] = None, H=None, S=None) ->
     return _run(p, cfg, cfg.algo, H, S, "build_hs_refined")
 
 
+def build_hs_kpoints(p, As, Bs, cfg: Optional[PipelineConfig] = None, Hs=None, Ss=None):
+    """n k-points of one cell in one call (hsdla_b200_build_hs_kpoints): p's operators and U are
+    shared, As[k] / Bs[k] are each k-point's coefficients (p.A / p.B layout).  Uploads of k+1 and
+    downloads of k-1 overlap the build of k.  Returns (list of HSResult-like (H, S) pairs,
+    stats of the last k-point with total_seconds for the batch)."""
+    cfg = cfg or PipelineConfig()
+    parse_strategy(cfg.strategy)
+    algo = "original" if parse_variant(cfg.variant) == "original" else cfg.algo
+    if algo not in ALGOS:
+        raise ConfigError(f"unknown algo: {algo}")
+    nk = len(As)
+    if len(Bs) != nk:
+        raise DimensionError("As and Bs differ in length")
+    n = p.n_g
+    shape = (p.n_atoms * p.n_l, n)
+    for M in list(As) + list(Bs):
+        if M.shape != shape or M.dtype != np.complex128 or not M.flags.f_contiguous:
+            raise DimensionError(f"A/B must be {shape} complex128 Fortran arrays")
+    Hs = Hs or [np.zeros((n, n), np.complex128, order="F") for _ in range(nk)]
+    Ss = Ss or [np.zeros((n, n), np.complex128, order="F") for _ in range(nk)]
+    for M in list(Hs) + list(Ss):
+        if M.shape != (n, n) or M.dtype != np.complex128 or not M.flags.f_contiguous:
+            raise DimensionError(f"H/S must be ({n}, {n}) complex128 Fortran arrays")
+    prob = p.c_struct()
+    opts, _keep = _options(cfg, algo)
+    ptrs = lambda L: (C.c_void_p * nk)(*[M.ctypes.data for M in L])  # noqa: E731
+    st = _lib.Stats()
+    check(_lib.lib().hsdla_b200_build_hs_kpoints(C.byref(prob), C.c_uint64(nk), ptrs(As), ptrs(Bs), C.byref(opts),
+                                                 ptrs(Hs), ptrs(Ss), C.byref(st)), "build_hs_kpoints")
+    return list(zip(Hs, Ss)), stats_dict(st, algo)
+
+
 def build_hs_original(p, cfg: Optional[PipelineConfig] = None, H=None, S=None) -> HSResult:
     """build_hs_original (pipeline.cpp:189-279, paper Algorithm 1) on B200: Cholesky
     try/fail of every T_AA on the GPU, trmm / hemm per atom, H += herk(B_T) +

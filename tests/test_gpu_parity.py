@@ -493,3 +493,34 @@ def test_operators_uploaded_on_the_copy_stream(algo):
     e.close()
     for (H, S), want in zip(got, (want_q, want_p, want_q)):
         assert rel(H, want.H) <= 1e-13 and rel(S, want.S) <= 1e-13
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_kpoint_batch_matches_per_call_builds(pinned):
+    """hsdla_b200_build_hs_kpoints: n k-points sharing the operators and U, their A, B
+    alternating between two device sets with uploads / downloads overlapping the builds:
+    every k-point equals its own per-call build (to FP64 rounding), for pinned and pageable
+    coefficients, in the default and the original algorithm."""
+    base = hb.generate_problem(12, 49, 700, 3, 2)
+    kps = [hb.generate_problem(12, 49, 700, 10 + k, 2) for k in range(5)]
+    As = [q.A for q in kps]
+    Bs = [q.B for q in kps]
+    if pinned:
+        for M in As + Bs:
+            hb.host_register(M)
+    try:
+        for cfg in (hb.PipelineConfig(), hb.PipelineConfig(variant="original")):
+            got, st = hb.build_hs_kpoints(base, As, Bs, cfg)
+            assert len(got) == 5 and st["total_seconds"] > 0
+            for k, (H, S) in enumerate(got):
+                pk = hb.generate_problem(12, 49, 700, 3, 2)
+                pk.A, pk.B = As[k], Bs[k]
+                want = hb.build_hs(pk, cfg)
+                assert rel(H, want.H) <= 1e-13 and rel(S, want.S) <= 1e-13, k
+                iu = np.triu_indices(700, 1)
+                assert np.all(H[iu] == 0) and np.all(S[iu] == 0)
+    finally:
+        if pinned:
+            for M in As + Bs:
+                hb.host_unregister(M)
+        hb.release_cache()
