@@ -1258,9 +1258,17 @@ static void engine_build_streamed(hsdla_b200_engine* e, const hsdla_b200_problem
   const char* sp = std::getenv("HSDLA_B200_SPLIT_S");
   const bool split = algo != HSDLA_B200_ALGO_ORIGINAL && !(sp && *sp == '0');
   if (pinned) {
-    // page-locked inputs: every chunk's copies are asynchronous, enqueue them all first
+    // page-locked inputs: every chunk's copies are asynchronous, enqueue them all first.  The
+    // small operator blocks and U of a caller who registered only A and B go through the
+    // staging slabs: a pageable cudaMemcpyAsync would block the host until the copy stream
+    // drained, serialising every upload before the first launch.
+    const uint64_t blk_bytes = p->n_atoms * p->n_l * p->n_l * sizeof(double2);
+    const bool ops_pinned = is_pinned(p->T_AA, blk_bytes) && is_pinned(p->T_AB, blk_bytes) &&
+                            is_pinned(p->T_BB, blk_bytes) && is_pinned(p->U, p->n_atoms * p->n_l * sizeof(double));
     for (size_t c = 0; c < plan.size(); ++c) {
-      upload_atoms(e, p, a0, plan[c].a0, plan[c].a1, e->copy_stream, c == 0 && split ? e->ev_a0 : nullptr);
+      upload_atoms(e, p, a0, plan[c].a0, plan[c].a1, e->copy_stream, c == 0 && split ? e->ev_a0 : nullptr,
+                   ops_pinned ? 7 : 3);
+      if (!ops_pinned) upload_atoms_staged(e, p, a0, plan[c].a0, plan[c].a1, e->copy_stream, 4);
       HS_CUDA(cudaEventRecord(e->ev_chunk_up[c], e->copy_stream));
     }
   }
@@ -1329,7 +1337,6 @@ static void engine_kpoints(hsdla_b200_engine* e, const hsdla_b200_problem* commo
                            const double* const* A, const double* const* B, int algo, double* const* H,
                            double* const* S) {
   ensure_kpoints(e, algo);
-  upload_atoms(e, common, 0, 0, e->na, e->stream, nullptr, 4);  // T and U, once
   const size_t ab_bytes = e->K * e->ng * sizeof(double2);
   auto upload = [&](uint64_t k) {
     hsdla_b200_problem pk = *common;
@@ -1351,9 +1358,22 @@ static void engine_kpoints(hsdla_b200_engine* e, const hsdla_b200_problem* commo
     }
     HS_CUDA(cudaEventRecord(e->ev_kup[set], e->h2d_stream));
   };
-  upload(0);
   for (uint64_t k = 0; k < nk; ++k) {
     const int set = static_cast<int>(k & 1);
+    if (k == 0) {
+      // the first k-point streams in atom chunks like the per-call drop-in (its upload
+      // overlaps its own build); it also brings T and U, which every later k-point reuses
+      hsdla_b200_problem p0 = *common;
+      p0.A = A[0];
+      p0.B = B[0];
+      e->band_final_h = true;
+      engine_build_streamed(e, &p0, 0, algo);
+      e->band_final_h = false;
+      HS_CUDA(cudaEventRecord(e->ev_kbuilt[0], e->stream));
+      if (nk > 1) upload(1);
+      enqueue_download(e);
+      continue;
+    }
     begin_build(e, algo);
     e->band_final_h = true;
     HS_CUDA(cudaStreamWaitEvent(e->stream, e->ev_kup[set], 0));
