@@ -352,10 +352,11 @@ def run_b200(args):
     if not args.no_e2e:
         e2e = run_e2e(args, hb, d, p, eng, na_total, nl, ng)
 
-    lapw = file_leg = None
+    lapw = file_leg = kpoints = None
     if P == 1 and not args.no_e2e:
         lapw = run_lapw(args, hb, p, na, nl, ng)
         file_leg = run_file(args, hb, p, na, nl, ng) if small else None
+        kpoints = run_kpoints(args, hb, p, na, nl, ng) if small and args.algo != "original" else None
 
     peak = hb.fp64_peak(dev, 1.0)
     line = None
@@ -407,6 +408,8 @@ def run_b200(args):
             line.update(lapw)
         if file_leg is not None:
             line["e2e_file"] = file_leg
+        if kpoints is not None:
+            line["e2e_kpoints"] = kpoints
         if klayer is not None:
             line["kernel_layer"] = klayer
         if P == 1 and not args.no_cpu_baseline:
@@ -522,6 +525,27 @@ def run_file(args, hb, p, na, nl, ng):
     return {"value": ledger_flops(na, nl, ng) / dt / 1e12, "unit": "TFLOP/s", "ms_per_step": dt * 1e3,
             "file_bytes": int(fbytes), "load_ms": load * 1e3, "load_gbs": fbytes / load / 1e9,
             "api": "paper_1712_07206_b200.build_hs_file -> hsdla_b200_build_hs_file (C-ABI)"}
+
+
+def run_kpoints(args, hb, p, na, nl, ng, nk=8):
+    """The k-point batch extension (hsdla_b200_build_hs_kpoints): nk k-points of the cell
+    sharing T and U, plain (pageable) numpy coefficients, every k-point's H, S downloaded.
+    Informational beside `e2e` (the per-call drop-in, the contract's number)."""
+    As = [p.A] + [hb.generate_problem(na, nl, ng, 100 + k, 0).A for k in range(nk - 1)]
+    Bs = [p.B] + [hb.generate_problem(na, nl, ng, 100 + k, 0).B for k in range(nk - 1)]
+    Hs = [np.zeros((ng, ng), np.complex128, order="F") for _ in range(nk)]
+    Ss = [np.zeros((ng, ng), np.complex128, order="F") for _ in range(nk)]
+    cfg = hb.PipelineConfig(algo=args.algo, arith=args.arith)
+    hb.build_hs_kpoints(p, As, Bs, cfg, Hs=Hs, Ss=Ss)  # warm
+    t = time.perf_counter()
+    hb.build_hs_kpoints(p, As, Bs, cfg, Hs=Hs, Ss=Ss)
+    dt = (time.perf_counter() - t) / nk
+    hb.release_cache()
+    return {"value": ledger_flops(na, nl, ng) / dt / 1e12, "unit": "TFLOP/s", "ms_per_kpoint": dt * 1e3,
+            "k_points": nk, "inputs": "pageable", "h2d_bytes_per_kpoint": int(p.A.nbytes + p.B.nbytes),
+            "d2h_bytes_per_kpoint": int(2 * (ng * (ng + 1) // 2) * 16),
+            "api": "paper_1712_07206_b200.build_hs_kpoints -> hsdla_b200_build_hs_kpoints (C-ABI; extension: "
+                   "k-independent T, U uploaded once, uploads / downloads overlap the builds)"}
 
 
 def run_kernel_layer(hb, p, nl, ng):
