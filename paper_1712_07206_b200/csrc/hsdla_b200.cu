@@ -25,6 +25,8 @@
 // chunk c's phases run, and every contraction accumulates into H, S (beta = 1 after
 // the first chunk) — H and S are sums over atoms, so any chunking is exact up to
 // FP64 rounding order.  S is downloaded and unpacked on the host while H computes.
+// A k-point batch (hsdla_b200_build_hs_kpoints) alternates two A/B sets so the next
+// k-point's upload and the previous one's download overlap the current build.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
