@@ -70,15 +70,22 @@ inline void fill_result(hsdla::pipeline::HSResult& r, const hsdla_b200_stats& st
     r.warnings.push_back("her2k, hemm_loop and herkx merged into one H contraction [A;B]^H [W_A;W_B]");
 }
 
-inline hsdla::pipeline::HSResult run(const hsdla::ProblemInstance& p, int algo, const Options& opt) {
+// The reference keeps each atom's operator blocks and U in separate heap blocks: pack them
+// into the contiguous layout of the C-ABI.
+struct PackedOps {
+  std::vector<hsdla::cplx> taa, tab, tbb;
+  std::vector<double> u;
+};
+inline PackedOps pack_ops(const hsdla::ProblemInstance& p) {
   const std::size_t na = p.n_atoms, nl = p.n_l, ng = p.n_g;
   if (p.A.rows() != na * nl || p.A.cols() != ng || !p.A.same_shape(p.B) || p.T_AA.size() != na ||
       p.T_AB.size() != na || p.T_BB.size() != na || p.U.size() != na)
     throw hsdla::DimensionError("build_hs: malformed ProblemInstance");
-  // per-atom operator blocks are separate heap blocks in the reference: pack them
   const std::size_t blk = nl * nl;
-  std::vector<hsdla::cplx> taa(na * blk), tab(na * blk), tbb(na * blk);
-  std::vector<double> u(na * nl);
+  PackedOps o{std::vector<hsdla::cplx>(na * blk), std::vector<hsdla::cplx>(na * blk),
+              std::vector<hsdla::cplx>(na * blk), std::vector<double>(na * nl)};
+  std::vector<hsdla::cplx>&taa = o.taa, &tab = o.tab, &tbb = o.tbb;
+  std::vector<double>& u = o.u;
   for (std::size_t a = 0; a < na; ++a) {
     if (p.T_AA[a].order() != nl || p.T_AB[a].rows() != nl || p.T_AB[a].cols() != nl ||
         p.T_BB[a].order() != nl || p.U[a].size() != nl)
@@ -88,6 +95,14 @@ inline hsdla::pipeline::HSResult run(const hsdla::ProblemInstance& p, int algo, 
     std::memcpy(static_cast<void*>(tbb.data() + a * blk), p.T_BB[a].matrix().data(), blk * sizeof(hsdla::cplx));
     std::memcpy(u.data() + a * nl, p.U[a].data(), nl * sizeof(double));
   }
+  return o;
+}
+
+inline hsdla::pipeline::HSResult run(const hsdla::ProblemInstance& p, int algo, const Options& opt) {
+  const std::size_t na = p.n_atoms, nl = p.n_l, ng = p.n_g;
+  const PackedOps ops = pack_ops(p);
+  const std::vector<hsdla::cplx>&taa = ops.taa, &tab = ops.tab, &tbb = ops.tbb;
+  const std::vector<double>& u = ops.u;
   hsdla_b200_problem cp{na, nl, ng,
                         reinterpret_cast<const double*>(p.A.data()), reinterpret_cast<const double*>(p.B.data()),
                         reinterpret_cast<const double*>(taa.data()), reinterpret_cast<const double*>(tab.data()),
@@ -143,6 +158,47 @@ inline hsdla::pipeline::HSResult build_hs_file(const std::string& path, const hs
                "hsdla_b200_build_hs_file");
   detail::fill_result(r, st, algo);
   return r;
+}
+
+/// k-point batch (an extension beside the per-k-point drop-in; hsdla_b200_build_hs_kpoints):
+/// `cell` supplies the k-independent operators and U (its A, B are not used), As[k] / Bs[k] each
+/// k-point's coefficients ((n_atoms n_l) x n_g, as ProblemInstance::A / B).  On one GPU the
+/// upload of k+1 and the download of k-1 overlap the build of k.  Same results as one
+/// build_hs per k-point, to FP64 rounding.
+inline std::vector<hsdla::pipeline::HSResult> build_hs_kpoints(const hsdla::ProblemInstance& cell,
+                                                               const std::vector<hsdla::ComplexMatrix>& As,
+                                                               const std::vector<hsdla::ComplexMatrix>& Bs,
+                                                               const hsdla::pipeline::PipelineConfig& cfg,
+                                                               const Options& opt = {}) {
+  const std::size_t na = cell.n_atoms, nl = cell.n_l, ng = cell.n_g, nk = As.size();
+  if (Bs.size() != nk) throw hsdla::DimensionError("build_hs_kpoints: As and Bs differ in length");
+  for (std::size_t k = 0; k < nk; ++k)
+    if (As[k].rows() != na * nl || As[k].cols() != ng || !As[k].same_shape(Bs[k]))
+      throw hsdla::DimensionError("build_hs_kpoints: k-point coefficients of wrong shape");
+  const int algo = cfg.variant == hsdla::pipeline::Variant::Original ? HSDLA_B200_ALGO_ORIGINAL : opt.algo;
+  const detail::PackedOps ops = detail::pack_ops(cell);
+  hsdla_b200_problem cp{na, nl, ng, nullptr, nullptr,
+                        reinterpret_cast<const double*>(ops.taa.data()), reinterpret_cast<const double*>(ops.tab.data()),
+                        reinterpret_cast<const double*>(ops.tbb.data()), ops.u.data()};
+  hsdla_b200_options co{opt.n_gpus, opt.device_ids.empty() ? nullptr : opt.device_ids.data(), algo,
+                        opt.arith == HSDLA_B200_ARITH_4M ? static_cast<int>(HSDLA_B200_FLAG_ARITH_4M) : 0};
+  std::vector<hsdla::pipeline::HSResult> out(nk);
+  std::vector<const double*> a(nk), b(nk);
+  std::vector<double*> h(nk), s(nk);
+  for (std::size_t k = 0; k < nk; ++k) {
+    out[k].H = hsdla::HermitianView(ng);
+    out[k].S = hsdla::HermitianView(ng);
+    a[k] = reinterpret_cast<const double*>(As[k].data());
+    b[k] = reinterpret_cast<const double*>(Bs[k].data());
+    h[k] = reinterpret_cast<double*>(out[k].H.matrix().data());
+    s[k] = reinterpret_cast<double*>(out[k].S.matrix().data());
+  }
+  if (nk == 0) return out;
+  hsdla_b200_stats st{};
+  throw_status(hsdla_b200_build_hs_kpoints(&cp, nk, a.data(), b.data(), &co, h.data(), s.data(), &st),
+               "hsdla_b200_build_hs_kpoints");
+  for (auto& r : out) detail::fill_result(r, st, algo);
+  return out;
 }
 
 inline hsdla::pipeline::HSResult build_hs(const hsdla::ProblemInstance& p, const hsdla::pipeline::PipelineConfig& cfg,

@@ -88,6 +88,29 @@ int main(int argc, char** argv) {
         upper0 = upper0 && gpu.H(i, j) == hsdla::cplx(0.0) && gpu.S(i, j) == hsdla::cplx(0.0);
     check(upper0, "  upper triangles exactly 0", 0.0);
   }
+  // k-point batch (extension): three k-points of the cell, the first being p's own coefficients;
+  // each equals the reference CPU run on that k-point's problem
+  {
+    std::vector<hsdla::ComplexMatrix> As{p.A}, Bs{p.B};
+    std::vector<hsdla::ProblemInstance> kp;
+    for (uint64_t k = 1; k < 3; ++k) {
+      kp.push_back(hsdla::generate_problem(na, nl, ng, seed + 100 + k, nnh));
+      As.push_back(kp.back().A);
+      Bs.push_back(kp.back().B);
+    }
+    const auto got = hsdla_b200::build_hs_kpoints(p, As, Bs, cfg);
+    std::printf("build_hs_kpoints (3 k-points)\n");
+    double worst = 0.0;
+    for (std::size_t k = 0; k < 3; ++k) {
+      hsdla::ProblemInstance pk = p;
+      pk.A = As[k];
+      pk.B = Bs[k];
+      const hsdla::pipeline::HSResult ref = k == 0 ? cpu : hsdla::pipeline::build_hs_refined(pk, cfg);
+      worst = std::max({worst, hsdla::rel_frobenius_error_lower(got[k].H.matrix(), ref.H.matrix()),
+                        hsdla::rel_frobenius_error_lower(got[k].S.matrix(), ref.S.matrix())});
+    }
+    check(got.size() == 3 && worst <= 1e-11, "  every k-point: H, S rel Frobenius (lower) <= 1e-11", worst);
+  }
   // HSDL v1 file written by the reference's save_problem, streamed into HBM by the drop-in
   {
     const std::string path = "/tmp/hsdla_b200_parity_cpp.hsdl";
