@@ -1,22 +1,33 @@
 #!/usr/bin/env python
 """Benchmark: HSDLA H+S construction per k-point on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl b200|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--scaling weak|strong]
+                    [--reduce scatter|root] [--impl b200|reference]
 
 One "step" = one k-point: the full refined H/S build (pipeline.cpp:281-329) of one
-synthetic problem.  Default workload = BASELINE.json configs[1] ("NaCl-like cell:
-64 atoms, lmax=8, N_G~3000, single k-point on 1 B200") = (64, 81, 3000).
-Under torchrun (N>1) every rank holds 64 atoms of a 64N-atom cell (weak scaling:
-fixed per-GPU work); the partial packed H and S are summed to rank 0 with NCCL
-(the path's one real exchange step) inside the timed region.
+synthetic problem (generate_problem, seed 1: the reference generator, bit-identical).
+Default workload = BASELINE.json configs[1] ("NaCl-like cell: 64 atoms, lmax=8, N_G~3000,
+single k-point on 1 B200") = (64, 81, 3000).
 
-`value` = reference-ledger FLOP/s (flop_model, pipeline.cpp:336-364; complex MAC =
-8 flops) of the whole job with inputs already in HBM, device-timed with CUDA events
-on the engine stream, max over ranks.  `e2e` = the same metric through the public
-drop-in API with host buffers (pinned) — H2D of the inputs and D2H of H, S inside
-the timed region.  `roofline` = the dominant kernel (the fused H contraction) against
-the FP64 DMMA peak measured in-process.  `cpu_baseline` = the reference CPU path
-(oracle/_ref, compiled from the reference sources) on this host.
+Multi-GPU (torchrun, one process per GPU): ONE problem is atom-sharded over the N ranks
+(each rank generates only its shard, generate_problem_shard) and the partial packed H, S are
+summed with NCCL inside the timed region (the path's one exchange step):
+  --scaling weak   (default) the problem has 64 N atoms of config c2 -- fixed work per GPU;
+  --scaling strong the config's own atom count split N ways (BASELINE configs[2..3]: c3 at
+                   N = 1/2/4/8, c4 at N = 8) -- fixed total work.
+At N = 1 both are the single-GPU line of the config.  --reduce scatter (default: every GPU
+receives its slices of H, S) or root (ncclReduce onto rank 0).
+
+`value` = reference-ledger FLOP/s (flop_model, pipeline.cpp:336-364; complex MAC = 8 flops)
+of the whole job with inputs already in HBM, device-timed with CUDA events on the engine
+stream, max over ranks.  `fp64_frac_of_peak` = EXECUTED flops per second / (N x the measured
+FP64 DMMA peak) -- the efficiency figure (the ledger rate can exceed the peak: the merged
+algorithm and the 3M products execute fewer flops than the reference's ledger counts).
+`e2e` = the same metric through the public drop-in API with PAGEABLE host buffers (a plain
+numpy / std::vector caller) -- H2D of the inputs and D2H of H, S inside the timed region;
+`e2e_pinned` is the same with page-locked buffers.  `roofline` = the dominant kernel (the H
+contraction) against the FP64 DMMA peak measured in-process.  `cpu_baseline` = the reference
+CPU path (oracle/_ref, compiled from the reference sources) on this host.
 """
 import argparse
 import json
@@ -142,6 +153,14 @@ class Dist:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
+    def sum(self, x):
+        if self.world == 1:
+            return x
+        import torch
+        t = torch.tensor([float(x)], dtype=torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        return float(t.item())
+
     def bcast_bytes(self, b):
         if self.world == 1:
             return b
@@ -227,23 +246,66 @@ def cpu_reference_sample(na, nl, ng, budget_s, steps=1, warmup=0, mode="atoms"):
             "seconds_per_sample": dt, "n_atoms_sample": na_s, "n_g_sample": ng_s, "sampling": mode}
 
 
+def workload(args, world):
+    """(n_atoms_total, n_l, n_g, description) of this run: weak scaling multiplies the config's
+    atoms by the rank count, strong scaling keeps them."""
+    na, nl, ng, desc = CONFIGS[args.config]
+    if world > 1 and args.scaling == "weak":
+        return na * world, nl, ng, f"{desc} x {world} (one {na * world}-atom cell, {na} atoms per GPU)"
+    return na, nl, ng, desc
+
+
 def run_reference_arm(args):
+    """The reference's own CPU build_hs_refined (oracle/_ref: the unmodified sources compiled
+    here; Strategy::Cpu, BlockedParallel, block 128, every host thread) on the B200 arm's
+    workload.  Timed steps run the FULL problem when K of them fit ~15 minutes (C2: ~22 s
+    each on 16 threads); otherwise an atom-subsampled instance of the same N_L and N_G
+    (same_config false).  Warm-up steps run a small atom sample (the code path, not the size)."""
     d = Dist()
     if d.rank != 0:
         d.close()
         return 0
-    na, nl, ng, desc = CONFIGS[args.config]
-    per_step = max(1.0, min(30.0, 150.0 / max(1, args.steps + args.warmup)))
-    cb = cpu_reference_sample(na, nl, ng, per_step, steps=args.steps, warmup=args.warmup)
+    from oracle.oracle import Reference, Restatement
+    na, nl, ng, desc = workload(args, args.gpus)
+    threads = os.cpu_count() or 1
+    if Reference.available():
+        ref, kind = Reference(), "reference"
+        run = lambda p: ref.build_hs(p, "refined", threads=threads, blocked=True, block=128, want_hs=False)  # noqa
+    else:
+        ref, kind, threads = Restatement(), "port", 1
+        run = lambda p: ref.build_hs_refined(p)  # noqa: E731
+    # rate probe on one atom (same N_L, N_G): predicts the full step
+    p1 = ref.generate_problem(1, nl, ng, 1, 0)
+    t = time.perf_counter()
+    run(p1)
+    rate1 = ledger_flops(1, nl, ng) / max(time.perf_counter() - t, 1e-6)
+    t_full = ledger_flops(na, nl, ng) / rate1
+    full = t_full * args.steps <= args.ref_budget
+    na_s = na if full else int(max(1, min(na, 30.0 * rate1 / ledger_flops(1, nl, ng))))
+    pw = ref.generate_problem(max(1, min(na_s, 4)), nl, ng, 1, 0)
+    for _ in range(args.warmup):
+        run(pw)
+    p = ref.generate_problem(na_s, nl, ng, 1, 0)
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        run(p)
+    dt = (time.perf_counter() - t) / args.steps
+    value = ledger_flops(na_s, nl, ng) / dt / 1e12
+    sample = (f"refined H+S of the full ({na} atoms, N_L {nl}, N_G {ng}) problem" if full else
+              f"refined H+S of ({na_s} of {na} atoms, N_L {nl}, N_G {ng}); H, S are sums over atoms, so the "
+              f"ledger rate is the full-size one") + \
+        f"; {'reference Strategy::Cpu BlockedParallel block 128' if kind == 'reference' else 'C port'}, " \
+        f"{threads} threads, {dt:.2f} s per step"
     line = {
-        "metric": METRIC, "value": cb["value"], "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": cb["seconds_per_sample"] * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generate_problem)",
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": args.scaling,
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generate_problem, seed 1)",
         "impl": "reference",
         "config": {"workload": f"{args.config}: {desc}", "n_atoms": na, "n_l": nl, "n_g": ng,
-                   "sampled_n_atoms": cb["n_atoms_sample"]},
-        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
-        "e2e": {"value": cb["value"], "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                   "timed_n_atoms": na_s, "same_config": full,
+                   "warmup": f"{pw.n_atoms}-atom sample per warm-up step"},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     d.close()
@@ -269,18 +331,23 @@ def run_b200(args):
     P = d.world
     dev = d.local
     torch.cuda.set_device(dev)
-    na, nl, ng, desc = CONFIGS[args.config]
-    na_total = na * P
-    # this rank's 64-atom shard (independent synthetic atoms per rank)
-    p = hb.generate_problem(na, nl, ng, 1 + d.rank, 0)
+    na_total, nl, ng, desc = workload(args, P)
+    bounds = hb.shard_atoms(na_total, P)
+    a0, a1 = bounds[d.rank], bounds[d.rank + 1]
+    # this rank's atom shard of ONE problem (bit-identical rows of generate_problem(na_total, ...))
+    p = (hb.generate_problem(na_total, nl, ng, 1, 0) if P == 1 else
+         hb.generate_problem_shard(na_total, nl, ng, a0, a1, 1, 0))
+    na = p.n_atoms
     hb.set_default_arith(args.arith)  # kernel layer + any engine created below
     eng = hb.Engine(dev, na, nl, ng)
     eng.set_arith(args.arith)
-    if P > 1 or args.force_comm:
-        # N > 1: NCCL reduce of the packed partials; --force-comm exercises the same
-        # path on one GPU with a 1-rank communicator (plumbing check)
+    multi = P > 1 or args.force_comm
+    if multi:
+        # N > 1: NCCL sum of the packed partials; --force-comm exercises the same path on one
+        # GPU with a 1-rank communicator (plumbing check)
         uid = d.bcast_bytes(hb.nccl_unique_id() if d.rank == 0 else None)
         eng.set_comm(uid, P, d.rank)
+        eng.set_reduce_mode(args.reduce)
     eng.upload(p, 0)
     eng.sync()
     stream = torch.cuda.ExternalStream(eng.stream(), device=dev)
@@ -323,7 +390,7 @@ def run_b200(args):
 
     # the same device-resident build with the plain 4-multiplication arithmetic, for reference
     ms4 = None
-    if args.arith == "3m":
+    if args.arith == "3m" and not args.no_4m:
         eng.set_arith("4m")
         for _ in range(2):
             step()
@@ -348,9 +415,11 @@ def run_b200(args):
         klayer = run_kernel_layer(hb, p, nl, ng)
 
     # ---- e2e through the public API with host buffers ----
-    e2e = None
+    e2e = e2e_pinned = None
     if not args.no_e2e:
-        e2e = run_e2e(args, hb, d, p, eng, na_total, nl, ng)
+        e2e = run_e2e(args, hb, d, p, eng, na_total, nl, ng, pinned=False)
+        if P == 1:
+            e2e_pinned = run_e2e(args, hb, d, p, eng, na_total, nl, ng, pinned=True)
 
     lapw = file_leg = kpoints = None
     if P == 1 and not args.no_e2e:
@@ -364,13 +433,13 @@ def run_b200(args):
         xf = 0.75 if args.arith == "3m" else 1.0  # executed / ledger flops of a contraction
         h_led = kt["h_flops"] / (kt["h_ms"] * 1e-3) / 1e12
         h_tf = h_led * xf
-        traffic = load_traffic(args.config)
+        traffic = load_traffic(args.config) if P == 1 else None
         roofline = {"bound": "tensor", "achieved": h_tf, "peak": peak, "unit": "TFLOP/s", "frac": h_tf / peak,
                     "traffic": traffic,
                     "kernel": f"ctn_contract_kernel<TRI> {H_KERNEL.get(args.algo, 'H contraction')}: "
-                              f"{kt['h_flops'] // (na * nl * ng * ng)} K N_G^2 "
+                              f"{round(kt['h_flops'] / (na * nl * ng * ng))} K N_G^2 "
                               f"flops per launch at 8 per complex MAC, {'6 per MAC executed (3M)' if xf < 1 else 'all executed (4M)'}; "
-                              "achieved = executed flops / mean launch time",
+                              "achieved = executed flops / mean launch time (rank 0)",
                     "achieved_ledger": h_led, "arith": args.arith,
                     "kernel_ms": kt["h_ms"], "flops_per_launch": int(kt["h_flops"] * xf),
                     "ledger_flops_per_launch": kt["h_flops"],
@@ -379,22 +448,25 @@ def run_b200(args):
                                    "(MEASURED_PEAKS.json has no FP64 entry)"}
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": P, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": args.scaling if P > 1 else "weak",
             "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (generate_problem, bit-identical to the reference generator; seed 1+rank)",
-            "config": {"workload": f"{args.config}: {desc}" + (f" x {P} GPUs (atoms per GPU fixed)" if P > 1 else ""),
-                       "n_atoms": na_total, "n_atoms_per_gpu": na, "n_l": nl, "n_g": ng, "algo": args.algo,
+            "data": "synthetic (generate_problem seed 1, bit-identical to the reference generator; each rank "
+                    "generates its own atom shard)",
+            "config": {"workload": f"{args.config}: {desc}", "n_atoms": na_total, "n_atoms_per_gpu": na_total / P,
+                       "n_l": nl, "n_g": ng, "algo": args.algo,
                        "arith": args.arith + (" (Gauss 3-multiplication complex products: 6 executed real "
                                               "flops per complex MAC, all FP64; value counts the reference "
                                               "ledger's 8)" if args.arith == "3m" else " (4 real DMMAs per "
                                               "complex MAC)"),
-                       "parallelism": f"atom-sharded x{P}" + (" + NCCL reduce of packed H,S" if P > 1 else ""),
+                       "parallelism": f"atom-sharded x{P}" + (f" + NCCL {'reduce-scatter' if args.reduce == 'scatter' else 'reduce'}"
+                                                              f" of packed H,S (timed)" if multi else ""),
                        "l2": f"inputs A,B {2 * na * nl * ng * 16 / 1e6:.0f} MB per GPU > 126 MB L2 (no flush)"},
             "build_ms": ms,
             "fp64_frac_of_peak": exec_tf / (P * peak),
             "executed_tflops": exec_tf,
-            "ledger_frac_of_peak": value / (P * peak),
             "phase_ms": {k: v * 1e3 for k, v in st["phase_seconds"].items()},
+            "reduce_ms": st["reduce_seconds"] * 1e3,
             "roofline": roofline,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
@@ -404,6 +476,8 @@ def run_b200(args):
             line["ms_per_step_4m"] = ms4
         if e2e is not None:
             line["e2e"] = e2e
+        if e2e_pinned is not None:
+            line["e2e_pinned"] = e2e_pinned
         if lapw is not None:
             line.update(lapw)
         if file_leg is not None:
@@ -565,18 +639,23 @@ def run_kernel_layer(hb, p, nl, ng):
                      "shape": f"A {k} x {ng}", "api": "paper_1712_07206_b200.kernels.herk -> hsdla_b200_herk"}}
 
 
-def run_e2e(args, hb, d, p, eng, na_total, nl, ng):
-    """Same metric through the public API with host buffers: every step copies the
-    inputs host->device (pinned) and reads H, S back (packed-lower D2H + unpack)."""
+def run_e2e(args, hb, d, p, eng, na_total, nl, ng, pinned=False):
+    """Same metric through the public API with host buffers: every step copies the inputs
+    host->device and reads H, S back (packed-lower D2H + unpack).  N = 1: the drop-in
+    build_hs_refined -> hsdla_b200_build_hs; N > 1: per rank the engine API (streamed upload of
+    its shard, NCCL reduce, download of the ranges it owns into its host H, S).  pinned=False:
+    plain pageable numpy buffers (the reference caller's std::vector reality); True: the
+    same buffers page-locked (hsdla_b200_host_register) outside the timed region."""
     import torch
     P = d.world
     steps = max(1, min(args.steps, args.e2e_steps))
     H = np.zeros((ng, ng), np.complex128, order="F")
     S = np.zeros((ng, ng), np.complex128, order="F")
-    bufs = [p.A, p.B, p.T_AA, p.T_AB, p.T_BB, p.U, H, S]
+    bufs = [p.A, p.B, p.T_AA, p.T_AB, p.T_BB, p.U, H, S] if pinned else []
     for b in bufs:
         hb.host_register(b)
-    h2d = sum(b.nbytes for b in (p.A, p.B, p.T_AA, p.T_AB, p.T_BB, p.U)) * P
+    h2d = sum(b.nbytes for b in (p.A, p.B, p.T_AA, p.T_AB, p.T_BB, p.U))
+    h2d = int(d.sum(h2d)) if P > 1 else h2d
     d2h = 2 * (ng * (ng + 1) // 2) * 16
     try:
         if P == 1:
@@ -594,11 +673,12 @@ def run_e2e(args, hb, d, p, eng, na_total, nl, ng):
             dt = (time.perf_counter() - t) / steps
             hb.release_cache()
         else:
+            eng.set_download_overlap(True)  # band the final H: each band's reduce + D2H overlaps the next
+
             def one():
                 eng.build_streamed(p, 0, args.algo)
                 eng.reduce(0)
-                if d.rank == 0:
-                    eng.download(H, S)
+                eng.download(H, S)
                 eng.sync()
             one()
             d.barrier()
@@ -607,29 +687,37 @@ def run_e2e(args, hb, d, p, eng, na_total, nl, ng):
                 one()
             d.barrier()
             dt = d.max((time.perf_counter() - t) / steps)
+            eng.set_download_overlap(False)
     finally:
         for b in bufs:
             hb.host_unregister(b)
     return {"value": ledger_flops(na_total, nl, ng) / dt / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": dt * 1e3, "steps": steps,
+            "host_buffers": "page-locked" if pinned else "pageable",
             "api": "paper_1712_07206_b200.build_hs_refined -> hsdla_b200_build_hs (C-ABI)" if P == 1
-            else "hsdla_b200_engine_upload/build/reduce/download (C-ABI)"}
+            else f"hsdla_b200_engine_build_streamed / reduce ({args.reduce}) / download (C-ABI), one process per GPU"}
 
 
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--algo", default="merged", choices=["merged", "fused", "refined", "original"])
     ap.add_argument("--arith", default="3m", choices=["3m", "4m"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak = 64 N atoms of c2 (fixed work per GPU); strong = the config's atoms split N ways")
+    ap.add_argument("--reduce", default="scatter", choices=["scatter", "root"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-4m", action="store_true", help="skip the 4M re-timing of the device-resident build")
     ap.add_argument("--force-comm", action="store_true", help="NCCL communicator even at N=1 (plumbing check)")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU work for cpu_baseline")
+    ap.add_argument("--ref-budget", type=float, default=900.0,
+                    help="--impl reference: run the full problem when K steps are predicted to fit this many seconds")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -74,6 +74,22 @@ extern "C" {
 #define HSDLA_B200_ARITH_4M 1
 /* hsdla_b200_options.flags: force the 4M arithmetic for this call. */
 #define HSDLA_B200_FLAG_ARITH_4M 1u
+/* hsdla_b200_options.flags: multi-GPU calls sum H, S onto the first GPU (ncclReduce) and
+ * download from it alone, instead of the default reduce-scatter where every GPU receives
+ * and downloads its own slices of H and S. */
+#define HSDLA_B200_FLAG_REDUCE_ROOT 2u
+
+/* ---- the multi-GPU collective ------------------------------------------------
+ * H and S are sums over atoms (pipeline.cpp:296-324): the GPUs of a column window hold
+ * partial packed triangles of disjoint atom shards and sum them.  The result is reduced in
+ * segments (the tile-column bands of the final H contraction when it runs banded, which
+ * overlaps each band's reduce with the next band's compute; else the whole window).
+ *   ROOT:    every segment summed onto rank `root` (ncclReduce).
+ *   SCATTER: rank r of P owns the r-th of P equal slices of every segment (the last rank also
+ *            the remainder): ncclReduceScatter in place, so each GPU receives 1/P of H and S
+ *            and downloads its own slices over its own PCIe link (hsdla_b200_engine_owned). */
+#define HSDLA_B200_REDUCE_ROOT 0
+#define HSDLA_B200_REDUCE_SCATTER 1
 
 /* Problem (ProblemInstance, problem.hpp:16-27). */
 typedef struct hsdla_b200_problem {
@@ -88,10 +104,19 @@ typedef struct hsdla_b200_problem {
 
 /* Options (PipelineConfig, pipeline.hpp:22-30, with the B200 strategy fields). */
 typedef struct hsdla_b200_options {
-  int n_gpus;             /* 0 or 1: one GPU; >1: atoms sharded, NCCL reduce to device_ids[0] */
-  const int* device_ids;  /* NULL: devices 0..n_gpus-1 */
+  int n_gpus;             /* 0 or 1: one GPU; >1: a grid of col_groups column windows x
+                             n_gpus / col_groups atom shards (see hsdla_b200_shard) */
+  const int* device_ids;  /* NULL: devices 0..n_gpus-1.  A device may repeat: the engines that
+                             share it are summed by a kernel instead of NCCL (single-GPU
+                             emulation of the multi-GPU grid; every atom shard of a window must
+                             then be on that one device) */
   int algo;               /* HSDLA_B200_ALGO_* */
-  int flags;              /* 0 or HSDLA_B200_FLAG_ARITH_4M */
+  int flags;              /* HSDLA_B200_FLAG_ARITH_4M | HSDLA_B200_FLAG_REDUCE_ROOT */
+  int col_groups;         /* 2-D tiling of H and S: number of column windows (must divide n_gpus).
+                             0: automatic -- 1 (atom sharding only, H and S replicated per GPU)
+                             unless the per-GPU memory estimate exceeds mem_budget_gb, then the
+                             smallest divisor of n_gpus that fits */
+  double mem_budget_gb;   /* per-GPU device memory for the automatic choice; 0: 90 % of free */
 } hsdla_b200_options;
 
 /* Phase slots = the reference's phase names (test_pipeline.cpp:167-176).  Refined
@@ -122,6 +147,8 @@ typedef struct hsdla_b200_stats {
   int n_gpus;
   int kernel_launches;       /* launches of this library's kernels in the build */
   uint64_t n_hpd;            /* atoms whose T_AA factorised (original algorithm; else n_atoms) */
+  int col_groups;            /* column windows of the grid that ran (1: H, S replicated per GPU) */
+  int reduce_mode;           /* HSDLA_B200_REDUCE_* of a multi-GPU call */
 } hsdla_b200_stats;
 
 /* ---- the drop-in --------------------------------------------------------
@@ -136,14 +163,17 @@ int hsdla_b200_build_hs(const hsdla_b200_problem* p, const hsdla_b200_options* o
 
 /* n_k k-points of one cell in one call (an extension beside the per-k-point drop-in): the
  * operators and U of `common` are k-independent and uploaded once; A[k], B[k] (same layout as
- * hsdla_b200_problem.A/B, common->A/B unused) give each k-point's coefficients and H[k], S[k]
- * receive its lower triangles.  On one GPU (opts->n_gpus <= 1): while k-point k builds, k+1's
+ * hsdla_b200_problem.A/B with n_g[k] columns; common->A/B unused) give each k-point's
+ * coefficients and H[k], S[k] (n_g[k] x n_g[k]) receive its lower triangles.  n_g NULL: every
+ * k-point has common->n_g G vectors; else the basis size may differ per k-point (N_G(k) of a
+ * real FLAPW k-point set): the engine is allocated for the largest and re-targeted per k-point
+ * without reallocation.  On one GPU (opts->n_gpus <= 1): while k-point k builds, k+1's
  * A, B are uploaded and k-1's H, S downloaded and unpacked, so the per-k-point cost approaches
  * the device-resident build.  Results equal n_k hsdla_b200_build_hs calls to FP64 rounding
  * (the per-call path chunks its uploads).  stats: the last k-point's, total_seconds = batch. */
-int hsdla_b200_build_hs_kpoints(const hsdla_b200_problem* common, uint64_t n_k, const double* const* A,
-                                const double* const* B, const hsdla_b200_options* opts, double* const* H,
-                                double* const* S, hsdla_b200_stats* stats);
+int hsdla_b200_build_hs_kpoints(const hsdla_b200_problem* common, uint64_t n_k, const uint64_t* n_g,
+                                const double* const* A, const double* const* B, const hsdla_b200_options* opts,
+                                double* const* H, double* const* S, hsdla_b200_stats* stats);
 
 /* ---- HSDL v1 problem files (problem.cpp:144-243) ---------------------------
  * Header of a file written by the reference's save_problem: dims and, when hpd
@@ -209,6 +239,15 @@ int hsdla_b200_generate_problem(uint64_t n_atoms, uint64_t n_l, uint64_t n_g, ui
                                 uint64_t n_not_hpd, double* A, double* B, double* T_AA, double* T_AB,
                                 double* T_BB, double* U, uint8_t* hpd);
 
+/* generate_problem restricted to the atoms [atom_begin, atom_end) of the n_atoms-atom instance:
+ * bit-identical to rows [atom_begin*n_l, atom_end*n_l) of A and B and blocks atom_begin..
+ * atom_end-1 of T_AA, T_AB, T_BB, U, hpd of the full instance (the generator stream is skipped,
+ * not stored), so each rank of a multi-GPU run generates only its own shard.  Output layouts
+ * as above with n_atoms := atom_end - atom_begin (A, B leading dimension (atom_end-atom_begin)*n_l). */
+int hsdla_b200_generate_problem_shard(uint64_t n_atoms, uint64_t n_l, uint64_t n_g, uint64_t seed,
+                                      uint64_t n_not_hpd, uint64_t atom_begin, uint64_t atom_end, double* A,
+                                      double* B, double* T_AA, double* T_AB, double* T_BB, double* U, uint8_t* hpd);
+
 /* Contiguous, count-balanced atom ranges for `parts` GPUs:
  * bounds[r] .. bounds[r+1] is shard r; bounds has parts+1 entries. */
 int hsdla_b200_shard_atoms(uint64_t n_atoms, int parts, uint64_t* bounds);
@@ -228,6 +267,23 @@ typedef struct hsdla_b200_engine hsdla_b200_engine;
 
 int hsdla_b200_engine_create(int device, uint64_t n_atoms_local, uint64_t n_l, uint64_t n_g,
                              hsdla_b200_engine** out);
+/* An engine for one shard of a multi-GPU grid: n_atoms_local atoms (an atom shard; the reduce
+ * sums the shards' partials) and the COLUMN WINDOW [col_begin, col_end) of H and S (2-D
+ * owner-computes tiling for N_G too large to replicate H and S on every GPU: engines of
+ * different windows compute disjoint tile-column bands of the lower triangle, no exchange).
+ * A window holds the operand columns [col_begin, n_g) (its tiles' rows) and the packed range
+ * of its columns.  col_end 0 means n_g; col_begin and col_end (unless n_g) are multiples of 64.
+ * n_g_capacity >= n_g (0: n_g) sizes a whole-window engine for later hsdla_b200_engine_reshape
+ * to other N_G without reallocation. */
+typedef struct hsdla_b200_shard {
+  uint64_t n_atoms_local, n_l, n_g;
+  uint64_t col_begin, col_end;
+  uint64_t n_g_capacity;
+} hsdla_b200_shard;
+int hsdla_b200_engine_create_shard(int device, const hsdla_b200_shard* shard, hsdla_b200_engine** out);
+/* Re-target the engine at N_G = n_g (whole window) within its capacity; HSDLA_B200_SIZING_ERROR
+ * if it does not fit.  Inputs must be uploaded again. */
+int hsdla_b200_engine_reshape(hsdla_b200_engine* e, uint64_t n_g);
 int hsdla_b200_engine_destroy(hsdla_b200_engine* e);
 /* H2D of atoms [atom_begin, atom_begin + n_atoms_local) of p (p->n_atoms total). */
 int hsdla_b200_engine_upload(hsdla_b200_engine* e, const hsdla_b200_problem* p, uint64_t atom_begin);
@@ -255,12 +311,26 @@ int hsdla_b200_engine_build(hsdla_b200_engine* e, int algo);
  * reduce / sync / download as for engine_build. */
 int hsdla_b200_engine_build_streamed(hsdla_b200_engine* e, const hsdla_b200_problem* p, uint64_t atom_begin,
                                      int algo);
-/* NCCL sum-reduce of the packed partial H and S to rank `root` (no-op without comm). */
+/* NCCL sum of the packed partial H and S over the engine's communicator (no-op without one),
+ * in the engine's reduce mode (HSDLA_B200_REDUCE_ROOT onto rank `root`, the default, or
+ * HSDLA_B200_REDUCE_SCATTER).  Every rank of the communicator calls it. */
 int hsdla_b200_engine_reduce(hsdla_b200_engine* e, int root);
+int hsdla_b200_engine_set_reduce_mode(hsdla_b200_engine* e, int mode);
+/* The reduce of a group of engines of THIS process that share a column window (disjoint atom
+ * shards): with communicators (one per engine, one rank each, e.g. from ncclCommInitAll) the
+ * NCCL calls of all engines are grouped; engines without one must share a device and are
+ * summed by a deterministic kernel (rank order).  engines[r] is rank r. */
+int hsdla_b200_group_reduce(hsdla_b200_engine* const* engines, int n, int mode, int root);
+/* The packed-lower index ranges (global, [begin, end) pairs) of H and S this engine holds final
+ * values for after the last build / reduce -- what hsdla_b200_engine_download writes.  ranges
+ * holds 2 * max entries; *n receives the count (which may exceed max). */
+int hsdla_b200_engine_owned(hsdla_b200_engine* e, uint64_t* ranges, uint64_t max, uint64_t* n);
 /* Wait for the engine's streams; fills phase/device timings of the last build. */
 int hsdla_b200_engine_sync(hsdla_b200_engine* e, hsdla_b200_stats* stats);
-/* D2H of the packed triangles, unpacked into the lower triangles of H, S
- * (either may be NULL). Synchronous. */
+/* D2H of the packed ranges this engine owns (all of its window before a reduce; its slices
+ * after a SCATTER reduce; everything on the root / nothing elsewhere after a ROOT reduce),
+ * unpacked into the lower triangles of the n_g x n_g matrices H, S (either may be NULL).
+ * Synchronous. */
 int hsdla_b200_engine_download(hsdla_b200_engine* e, double* H, double* S);
 /* Packed lower (LAPACK 'L' packed, column-major) device pointers of H and S. */
 int hsdla_b200_engine_device_results(hsdla_b200_engine* e, void** Hp, void** Sp);

@@ -29,10 +29,14 @@
 namespace hsdla_b200 {
 
 struct Options {
-  int n_gpus = 1;                             // atoms sharded over n_gpus, NCCL reduce to device_ids[0]
+  int n_gpus = 1;                             // GPUs: col_groups column windows x atom shards
   std::vector<int> device_ids;                // empty: 0..n_gpus-1
   int algo = HSDLA_B200_ALGO_REFINED_MERGED;  // or REFINED_FUSED, or REFINED (reference phase order)
   int arith = HSDLA_B200_ARITH_3M;            // or HSDLA_B200_ARITH_4M (plain 4-multiplication complex)
+  bool reduce_to_root = false;                // true: ncclReduce onto device_ids[0]; false: reduce-scatter,
+                                              // every GPU downloads its own slices
+  int col_groups = 0;                         // 2-D tiling of H, S (0: automatic by memory budget)
+  double mem_budget_gb = 0.0;                 // per-GPU budget of the automatic choice (0: 90 % of free)
 };
 
 inline void throw_status(int rc, const char* what) {
@@ -48,6 +52,30 @@ inline void throw_status(int rc, const char* what) {
 }
 
 namespace detail {
+
+inline hsdla_b200_options c_options(const Options& opt, int algo) {
+  hsdla_b200_options co{};
+  co.n_gpus = opt.n_gpus;
+  co.device_ids = opt.device_ids.empty() ? nullptr : opt.device_ids.data();
+  co.algo = algo;
+  co.flags = (opt.arith == HSDLA_B200_ARITH_4M ? static_cast<int>(HSDLA_B200_FLAG_ARITH_4M) : 0) |
+             (opt.reduce_to_root ? static_cast<int>(HSDLA_B200_FLAG_REDUCE_ROOT) : 0);
+  co.col_groups = opt.col_groups;
+  co.mem_budget_gb = opt.mem_budget_gb;
+  return co;
+}
+
+// The algorithm a call runs: Original for Variant::Original, else opt.algo, which must then
+// be one of the refined algorithms (build_hs_refined's check, pipeline.hpp:55).
+inline int refined_algo(const Options& opt, const char* what) {
+  if (opt.algo != HSDLA_B200_ALGO_REFINED_MERGED && opt.algo != HSDLA_B200_ALGO_REFINED_FUSED &&
+      opt.algo != HSDLA_B200_ALGO_REFINED)
+    throw hsdla::ConfigError(std::string(what) + ": algo must be REFINED_MERGED, REFINED_FUSED or REFINED");
+  return opt.algo;
+}
+inline int algo_of(const hsdla::pipeline::PipelineConfig& cfg, const Options& opt, const char* what) {
+  return cfg.variant == hsdla::pipeline::Variant::Original ? HSDLA_B200_ALGO_ORIGINAL : refined_algo(opt, what);
+}
 
 inline void fill_result(hsdla::pipeline::HSResult& r, const hsdla_b200_stats& st, int algo) {
   static const char* const keys[8] = {"gemm", "hemm", "her2k", "herk", "scaling", "herkx", "potrf", "trmm"};
@@ -71,15 +99,19 @@ inline void fill_result(hsdla::pipeline::HSResult& r, const hsdla_b200_stats& st
 }
 
 // The reference keeps each atom's operator blocks and U in separate heap blocks: pack them
-// into the contiguous layout of the C-ABI.
+// into the contiguous layout of the C-ABI.  pack_ops validates the operators and U only
+// (the k-point batch does not use the cell's A, B); check_coefficients validates A, B.
 struct PackedOps {
   std::vector<hsdla::cplx> taa, tab, tbb;
   std::vector<double> u;
 };
+inline void check_coefficients(const hsdla::ProblemInstance& p) {
+  if (p.A.rows() != p.n_atoms * p.n_l || p.A.cols() != p.n_g || !p.A.same_shape(p.B))
+    throw hsdla::DimensionError("build_hs: malformed ProblemInstance");
+}
 inline PackedOps pack_ops(const hsdla::ProblemInstance& p) {
-  const std::size_t na = p.n_atoms, nl = p.n_l, ng = p.n_g;
-  if (p.A.rows() != na * nl || p.A.cols() != ng || !p.A.same_shape(p.B) || p.T_AA.size() != na ||
-      p.T_AB.size() != na || p.T_BB.size() != na || p.U.size() != na)
+  const std::size_t na = p.n_atoms, nl = p.n_l;
+  if (p.T_AA.size() != na || p.T_AB.size() != na || p.T_BB.size() != na || p.U.size() != na)
     throw hsdla::DimensionError("build_hs: malformed ProblemInstance");
   const std::size_t blk = nl * nl;
   PackedOps o{std::vector<hsdla::cplx>(na * blk), std::vector<hsdla::cplx>(na * blk),
@@ -100,6 +132,7 @@ inline PackedOps pack_ops(const hsdla::ProblemInstance& p) {
 
 inline hsdla::pipeline::HSResult run(const hsdla::ProblemInstance& p, int algo, const Options& opt) {
   const std::size_t na = p.n_atoms, nl = p.n_l, ng = p.n_g;
+  check_coefficients(p);
   const PackedOps ops = pack_ops(p);
   const std::vector<hsdla::cplx>&taa = ops.taa, &tab = ops.tab, &tbb = ops.tbb;
   const std::vector<double>& u = ops.u;
@@ -107,8 +140,7 @@ inline hsdla::pipeline::HSResult run(const hsdla::ProblemInstance& p, int algo, 
                         reinterpret_cast<const double*>(p.A.data()), reinterpret_cast<const double*>(p.B.data()),
                         reinterpret_cast<const double*>(taa.data()), reinterpret_cast<const double*>(tab.data()),
                         reinterpret_cast<const double*>(tbb.data()), u.data()};
-  hsdla_b200_options co{opt.n_gpus, opt.device_ids.empty() ? nullptr : opt.device_ids.data(), algo,
-                        opt.arith == HSDLA_B200_ARITH_4M ? static_cast<int>(HSDLA_B200_FLAG_ARITH_4M) : 0};
+  const hsdla_b200_options co = c_options(opt, algo);
   hsdla::pipeline::HSResult r;
   r.H = hsdla::HermitianView(ng);  // zero-initialised: the upper triangle stays exactly 0
   r.S = hsdla::HermitianView(ng);
@@ -127,10 +159,7 @@ inline hsdla::pipeline::HSResult build_hs_refined(const hsdla::ProblemInstance& 
                                                   const Options& opt = {}) {
   if (cfg.variant != hsdla::pipeline::Variant::Refined)
     throw hsdla::ConfigError("build_hs_refined: variant must be Refined");
-  if (opt.algo != HSDLA_B200_ALGO_REFINED_MERGED && opt.algo != HSDLA_B200_ALGO_REFINED_FUSED &&
-      opt.algo != HSDLA_B200_ALGO_REFINED)
-    throw hsdla::ConfigError("build_hs_refined: algo must be REFINED_MERGED, REFINED_FUSED or REFINED");
-  return detail::run(p, opt.algo, opt);
+  return detail::run(p, detail::refined_algo(opt, "build_hs_refined"), opt);
 }
 
 inline hsdla::pipeline::HSResult build_hs_original(const hsdla::ProblemInstance& p,
@@ -144,11 +173,10 @@ inline hsdla::pipeline::HSResult build_hs_original(const hsdla::ProblemInstance&
 /// malformed or truncated file (test_io.cpp:47-63).
 inline hsdla::pipeline::HSResult build_hs_file(const std::string& path, const hsdla::pipeline::PipelineConfig& cfg,
                                                const Options& opt = {}) {
-  const int algo = cfg.variant == hsdla::pipeline::Variant::Original ? HSDLA_B200_ALGO_ORIGINAL : opt.algo;
+  const int algo = detail::algo_of(cfg, opt, "build_hs_file");
   uint64_t na = 0, nl = 0, ng = 0;
   throw_status(hsdla_b200_problem_file_info(path.c_str(), &na, &nl, &ng, nullptr), "hsdla_b200_problem_file_info");
-  hsdla_b200_options co{opt.n_gpus, opt.device_ids.empty() ? nullptr : opt.device_ids.data(), algo,
-                        opt.arith == HSDLA_B200_ARITH_4M ? static_cast<int>(HSDLA_B200_FLAG_ARITH_4M) : 0};
+  const hsdla_b200_options co = detail::c_options(opt, algo);
   hsdla::pipeline::HSResult r;
   r.H = hsdla::HermitianView(ng);
   r.S = hsdla::HermitianView(ng);
@@ -161,33 +189,37 @@ inline hsdla::pipeline::HSResult build_hs_file(const std::string& path, const hs
 }
 
 /// k-point batch (an extension beside the per-k-point drop-in; hsdla_b200_build_hs_kpoints):
-/// `cell` supplies the k-independent operators and U (its A, B are not used), As[k] / Bs[k] each
-/// k-point's coefficients ((n_atoms n_l) x n_g, as ProblemInstance::A / B).  On one GPU the
-/// upload of k+1 and the download of k-1 overlap the build of k.  Same results as one
-/// build_hs per k-point, to FP64 rounding.
+/// `cell` supplies the k-independent operators and U (its A, B are not used and not checked),
+/// As[k] / Bs[k] each k-point's coefficients ((n_atoms n_l) x N_G(k), as ProblemInstance::A / B;
+/// N_G(k) may differ per k-point).  On one GPU the upload of k+1 and the download of k-1
+/// overlap the build of k.  Same results as one build_hs per k-point, to FP64 rounding.
+/// Ledgers are per k-point (flop_model at N_G(k)); phase times are the LAST k-point's device
+/// times (the batch pipelines the k-points, so earlier ones have no separate phase record).
 inline std::vector<hsdla::pipeline::HSResult> build_hs_kpoints(const hsdla::ProblemInstance& cell,
                                                                const std::vector<hsdla::ComplexMatrix>& As,
                                                                const std::vector<hsdla::ComplexMatrix>& Bs,
                                                                const hsdla::pipeline::PipelineConfig& cfg,
                                                                const Options& opt = {}) {
-  const std::size_t na = cell.n_atoms, nl = cell.n_l, ng = cell.n_g, nk = As.size();
+  const std::size_t na = cell.n_atoms, nl = cell.n_l, nk = As.size();
   if (Bs.size() != nk) throw hsdla::DimensionError("build_hs_kpoints: As and Bs differ in length");
-  for (std::size_t k = 0; k < nk; ++k)
-    if (As[k].rows() != na * nl || As[k].cols() != ng || !As[k].same_shape(Bs[k]))
+  std::vector<uint64_t> ngk(nk);
+  for (std::size_t k = 0; k < nk; ++k) {
+    if (As[k].rows() != na * nl || As[k].cols() < 1 || !As[k].same_shape(Bs[k]))
       throw hsdla::DimensionError("build_hs_kpoints: k-point coefficients of wrong shape");
-  const int algo = cfg.variant == hsdla::pipeline::Variant::Original ? HSDLA_B200_ALGO_ORIGINAL : opt.algo;
+    ngk[k] = As[k].cols();
+  }
+  const int algo = detail::algo_of(cfg, opt, "build_hs_kpoints");
   const detail::PackedOps ops = detail::pack_ops(cell);
-  hsdla_b200_problem cp{na, nl, ng, nullptr, nullptr,
+  hsdla_b200_problem cp{na, nl, nk ? ngk[0] : cell.n_g, nullptr, nullptr,
                         reinterpret_cast<const double*>(ops.taa.data()), reinterpret_cast<const double*>(ops.tab.data()),
                         reinterpret_cast<const double*>(ops.tbb.data()), ops.u.data()};
-  hsdla_b200_options co{opt.n_gpus, opt.device_ids.empty() ? nullptr : opt.device_ids.data(), algo,
-                        opt.arith == HSDLA_B200_ARITH_4M ? static_cast<int>(HSDLA_B200_FLAG_ARITH_4M) : 0};
+  const hsdla_b200_options co = detail::c_options(opt, algo);
   std::vector<hsdla::pipeline::HSResult> out(nk);
   std::vector<const double*> a(nk), b(nk);
   std::vector<double*> h(nk), s(nk);
   for (std::size_t k = 0; k < nk; ++k) {
-    out[k].H = hsdla::HermitianView(ng);
-    out[k].S = hsdla::HermitianView(ng);
+    out[k].H = hsdla::HermitianView(ngk[k]);
+    out[k].S = hsdla::HermitianView(ngk[k]);
     a[k] = reinterpret_cast<const double*>(As[k].data());
     b[k] = reinterpret_cast<const double*>(Bs[k].data());
     h[k] = reinterpret_cast<double*>(out[k].H.matrix().data());
@@ -195,9 +227,15 @@ inline std::vector<hsdla::pipeline::HSResult> build_hs_kpoints(const hsdla::Prob
   }
   if (nk == 0) return out;
   hsdla_b200_stats st{};
-  throw_status(hsdla_b200_build_hs_kpoints(&cp, nk, a.data(), b.data(), &co, h.data(), s.data(), &st),
+  throw_status(hsdla_b200_build_hs_kpoints(&cp, nk, ngk.data(), a.data(), b.data(), &co, h.data(), s.data(), &st),
                "hsdla_b200_build_hs_kpoints");
-  for (auto& r : out) detail::fill_result(r, st, algo);
+  for (std::size_t k = 0; k < nk; ++k) {
+    hsdla_b200_stats sk = st;  // the ledger of k-point k (flop_model at N_G(k))
+    throw_status(hsdla_b200_flop_model(algo == HSDLA_B200_ALGO_ORIGINAL ? 0 : 1, na, nl, ngk[k], st.n_hpd,
+                                       sk.ledger),
+                 "hsdla_b200_flop_model");
+    detail::fill_result(out[k], sk, algo);
+  }
   return out;
 }
 

@@ -633,20 +633,25 @@ void orc_sph_bessel(int lmax, double x, double* j) {
     return;
   }
   const int top = lmax + 40 + (int)(2.0 * x);
-  double jp1 = 0.0, jl = 1e-280;
+  double jp1 = 0.0, jl = 1e-280, m1 = 0.0; /* m1: the unnormalised j_1 */
   double* tmp = calloc((size_t)lmax + 1, sizeof(double));
   for (int l = top; l >= 1; --l) {
     const double jm1 = (2.0 * l + 1.0) / x * jl - jp1;
     jp1 = jl;
     jl = jm1;
     if (l - 1 <= lmax) tmp[l - 1] = jl;
+    if (l - 1 == 1) m1 = jl;
     if (fabs(jl) > 1e200) {
       jl *= 1e-200;
       jp1 *= 1e-200;
+      m1 *= 1e-200;
       for (int m = l - 1; m <= lmax; ++m) tmp[m] *= 1e-200;
     }
   }
-  const double norm = (sin(x) / x) / jl;
+  /* normalise by the larger of j_0 and j_1 (they never vanish together: exact next to
+     the zeros x = n pi of j_0) */
+  const double j0 = sin(x) / x, j1 = (sin(x) / x - cos(x)) / x;
+  const double norm = fabs(j1) > fabs(j0) ? j1 / m1 : j0 / jl;
   for (int l = 0; l <= lmax; ++l) j[l] = tmp[l] * norm;
   free(tmp);
 }

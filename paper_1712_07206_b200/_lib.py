@@ -13,6 +13,8 @@ OK, DIMENSION_ERROR, SIZING_ERROR, CONFIG_ERROR, IO_ERROR, CUDA_ERROR, NCCL_ERRO
 ALGO_REFINED_MERGED, ALGO_REFINED, ALGO_ORIGINAL, ALGO_REFINED_FUSED = 0, 1, 2, 3
 ARITH = {"3m": 0, "4m": 1}  # HSDLA_B200_ARITH_*: Gauss 3-multiplication / plain 4-multiplication complex
 FLAG_ARITH_4M = 1
+FLAG_REDUCE_ROOT = 2
+REDUCE = {"root": 0, "scatter": 1}  # HSDLA_B200_REDUCE_*
 LEDGER_KEYS = ("gemm", "hemm", "her2k", "herk", "scaling", "herkx", "potrf", "trmm")
 N_PHASES = 8
 # phase slot names (include/hsdla_b200.h HSDLA_B200_PHASE_*)
@@ -36,6 +38,8 @@ EXPORTS = (
     "hsdla_b200_herk", "hsdla_b200_her2k", "hsdla_b200_herkx", "hsdla_b200_gemm", "hsdla_b200_hemm",
     "hsdla_b200_trmm", "hsdla_b200_diag_scale", "hsdla_b200_engine_set_arith", "hsdla_b200_set_default_arith",
     "hsdla_b200_engine_set_download_overlap", "hsdla_b200_build_hs_kpoints",
+    "hsdla_b200_engine_create_shard", "hsdla_b200_engine_reshape", "hsdla_b200_engine_set_reduce_mode",
+    "hsdla_b200_group_reduce", "hsdla_b200_engine_owned", "hsdla_b200_generate_problem_shard",
 )
 
 
@@ -46,7 +50,13 @@ class Problem(C.Structure):
 
 
 class Options(C.Structure):
-    _fields_ = [("n_gpus", C.c_int), ("device_ids", C.POINTER(C.c_int)), ("algo", C.c_int), ("flags", C.c_int)]
+    _fields_ = [("n_gpus", C.c_int), ("device_ids", C.POINTER(C.c_int)), ("algo", C.c_int), ("flags", C.c_int),
+                ("col_groups", C.c_int), ("mem_budget_gb", C.c_double)]
+
+
+class Shard(C.Structure):
+    _fields_ = [("n_atoms_local", C.c_uint64), ("n_l", C.c_uint64), ("n_g", C.c_uint64),
+                ("col_begin", C.c_uint64), ("col_end", C.c_uint64), ("n_g_capacity", C.c_uint64)]
 
 
 class Stats(C.Structure):
@@ -54,7 +64,7 @@ class Stats(C.Structure):
                 ("reduce_seconds", C.c_double), ("d2h_seconds", C.c_double), ("total_seconds", C.c_double),
                 ("ledger", C.c_uint64 * 9), ("executed_flops", C.c_uint64), ("peak_device_bytes", C.c_uint64),
                 ("peak_temp_bytes", C.c_uint64), ("n_gpus", C.c_int), ("kernel_launches", C.c_int),
-                ("n_hpd", C.c_uint64)]
+                ("n_hpd", C.c_uint64), ("col_groups", C.c_int), ("reduce_mode", C.c_int)]
 
 
 _lib = None

@@ -34,40 +34,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "ctn_params.hpp"
+
 namespace hsdla_b200 {
-
-constexpr int kMaxSeg = 3;
-constexpr int kChunkC = 8;  // complex k per TMA slab (128 B rows)
-
-enum CtnMode { kTri = 0, kBatch = 1 };
-
-struct alignas(64) CtnParams {
-  CUtensorMap L[kMaxSeg];  // left operands (conjugated), 3-D maps
-  CUtensorMap R[kMaxSeg];  // right operands
-  int kchunks[kMaxSeg];    // 8-complex slabs per segment
-  int l_row_z[kMaxSeg];    // 1: tile row coordinate in dim 2, atom in dim 1; 0: row in dim 1, atom in dim 2
-  int r_row_z[kMaxSeg];
-  int nseg;
-  int n;                   // TRI: order N_G.  BATCH: number of output columns (N_G)
-  int m_valid;             // BATCH: valid output rows per atom (N_L)
-  int tiles;               // TRI: tiles per dimension
-  int tiles_total;         // TRI: lower tiles t(t+1)/2
-  int band;                // TRI: tile-row band of the grouped tile order (>= 1)
-  int col_t0, col_t1;      // TRI, optional: only the lower tiles with col_t0 <= tj < col_t1
-                           // (col_t1 == 0: the whole lower triangle); tiles_total = their count
-  double2* out;            // TRI: packed lower.  BATCH: column-major stacked buffer
-  double* sk_ws;           // TRI stream-K: per-CTA partial-accumulator slots
-  uint32_t* sk_flags;      // TRI stream-K: per-CTA publish flags (== epoch when the slot is ready)
-  uint32_t epoch;          // TRI stream-K: unique per launch
-  uint64_t ldo;            // BATCH: output leading dimension (complex elements)
-  int bat_tx, bat_ty;      // BATCH: column tiles, row tiles per atom
-  int bat_tiles;           // BATCH: bat_tx * bat_ty * atoms (persistent CTAs loop over them)
-  const int* keep_diag_imag;  // TRI, optional: when non-null and *keep_diag_imag != 0 the diagonal's
-                              // imaginary part is kept (the original algorithm's full-gemm fold,
-                              // pipeline.cpp:266-271, does not zero it); else forced to 0
-  double alpha_re, alpha_im;
-  double beta;             // real; 0 => C is never read
-};
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -349,14 +318,16 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES,
             uint8_t* sL = smem + slot * Cfg::kStageBytes + u * Cfg::kSubL;
             uint8_t* sR = smem + slot * Cfg::kStageBytes + Cfg::kStageL + u * Cfg::kSubR;
             const int x = kc * 2 * kChunkC;
+            // TRI: operand columns are held from global column g0 on (column windows)
+            const int lr = MODE == kTri ? row0 - P.g0 : row0, lc = MODE == kTri ? col0 - P.g0 : col0;
             if (P.l_row_z[seg])
-              tma_load_3d(sL, &P.L[seg], x, atom, row0, &full[slot]);
+              tma_load_3d(sL, &P.L[seg], x, atom, lr, &full[slot]);
             else
-              tma_load_3d(sL, &P.L[seg], x, row0, atom, &full[slot]);
+              tma_load_3d(sL, &P.L[seg], x, lr, atom, &full[slot]);
             if (P.r_row_z[seg])
-              tma_load_3d(sR, &P.R[seg], x, atom, col0, &full[slot]);
+              tma_load_3d(sR, &P.R[seg], x, atom, lc, &full[slot]);
             else
-              tma_load_3d(sR, &P.R[seg], x, col0, atom, &full[slot]);
+              tma_load_3d(sR, &P.R[seg], x, lc, atom, &full[slot]);
             ++kc;
           }
         }
@@ -547,7 +518,7 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES,
       auto dst_of = [&](int mb, int nb, int e) -> double2* {
         const int i = row0 + wm * Cfg::kWM + 8 * mb + pg;
         const int j = col0 + wn * Cfg::kWN + 8 * nb + (e ? 4 + q : q);
-        if (MODE == kTri) return (i < P.n && j < P.n && i >= j) ? P.out + packed_index(P.n, i, j) : nullptr;
+        if (MODE == kTri) return (i < P.n && j < P.n && i >= j) ? P.out + (packed_index(P.n, i, j) - P.pk0) : nullptr;
         return (i < P.m_valid && j < P.n)
                    ? P.out + (static_cast<uint64_t>(atom) * P.m_valid + i) + static_cast<uint64_t>(j) * P.ldo
                    : nullptr;

@@ -1,0 +1,252 @@
+// The per-GPU device engine of the HSDLA refined H/S construction (drop-in for
+// hsdla::pipeline::build_hs_refined, reference pipeline.cpp:281-329).
+//
+// Device data layout (one engine per GPU / shard, all HBM-resident):
+//   A, B    K x ncol complex, column-major, ld = K (the reference stacking,
+//           problem.hpp:20-21), columns [c0, N_G) of the problem; two sets when a
+//           k-point batch alternates them (set 1 allocated on first use)
+//   X1      K x ncol: first U*B (phase s, diag_scale kernels.cpp:438-450), then W_A
+//           (merged) or T_AA A (hemm_loop, pipeline.cpp:314-321)
+//   X2      K x ncol: W_B (merged) or Z = T_AB^H A + 1/2 T_BB B (z_loop, pipeline.cpp:302-307)
+//   Tab     raw per-atom T_AB blocks (used as-is: Z = T_AB^H A is a CTN product)
+//   Pbb,Paa 1/2 full(T_BB) (full(T_BB) for the merged algorithm), full(T_AA) expanded
+//           from the LOWER triangles only
+//   Pab     T_AB^H per atom (merged algorithm: W_A = T_AA A + T_AB B)
+//   Hp, Sp  the engine's column window [c0, c1) of packed-lower N_G x N_G storage:
+//           global packed indices [pk0, pk0 + npk) (LAPACK 'L' packing; halves D2H and
+//           NCCL bytes).  The whole triangle when the window is [0, N_G).
+//
+// Shards.  An engine holds n_atoms_local atoms of a problem (the atom shard: its
+// partial H, S are summed over shards by the reduce) and one COLUMN WINDOW of H and S
+// (2-D owner-computes tiling for N_G too large to replicate H and S: engines of
+// different windows compute disjoint tile-column bands of the lower triangle and
+// never exchange data).  A window [c0, c1) needs the operand columns [c0, N_G) (the
+// rows i >= j of its tiles), so its A, B, X hold ncol = N_G - c0 columns.
+//
+// The merged algorithm (default) restates Algorithm 3 as one contraction per matrix:
+// per atom, H_a = Y_a^H M_a Y_a with Y_a = [A_a; B_a] and the Hermitian block operator
+// M_a = [[T_AA, T_AB], [T_AB^H, T_BB]] (the same sum pipeline.cpp:302-324 evaluates as
+// Z^H B + B^H Z + A^H (T_AA A)), so H = [A; B]^H [W_A; W_B] with W_A = T_AA A + T_AB B in
+// X1 and W_B = T_AB^H A + T_BB B in X2: 16 K N_G^2 contraction flops instead of 20.
+//
+// A build is a list of atom CHUNKS.  The device-resident build is one chunk over
+// all atoms.  The streamed build (the one-shot drop-in with host buffers) splits
+// the atoms into chunks: chunk c+1 is copied host->device on the copy stream while
+// chunk c's phases run, and every contraction accumulates into H, S (beta = 1 after
+// the first chunk) — H and S are sums over atoms, so any chunking is exact up to
+// FP64 rounding order.  S is downloaded and unpacked on the host while H computes.
+// A k-point batch (hsdla_b200_build_hs_kpoints) alternates the two A/B sets so the next
+// k-point's upload and the previous one's download overlap the current build.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <sys/stat.h>
+
+#include <chrono>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+#include "ctn_params.hpp"
+
+namespace hsdla_b200 {
+
+// One atom chunk [a0, a1) of a build over one A/B set: the parameter blocks of every launch.
+struct ChunkPlan {
+  uint64_t a0 = 0, a1 = 0;
+  const double2* A = nullptr;  // the set's A / B (raw-pointer launches: diag_scale, select_left)
+  const double2* B = nullptr;
+  // s: S; z: Z -> X1 (refined/original); zf: Z -> X2 (fused); x: Q^H A -> X1;
+  // h: fused her2k+herkx; h2k: her2k over X1; hkx: herkx A^H X1; haa: original X2^H X1
+  // merged: wa: W_A = T_AA A + T_AB B -> X1; wb: W_B = T_AB^H A + T_BB B -> X2; hm: [A;B]^H [X1;X2]
+  CtnParams s, z, zf, x, h, h2k, hkx, haa, wa, wb, hm;
+  // the S contraction split by segment (first streamed chunk: A^H A starts on A's rows
+  // while B, T, U are still on the wire; (UB)^H (UB) accumulates once they landed)
+  CtnParams sA, sB;
+  dim3 grid_tri, grid_bat;
+};
+
+struct OpTime {
+  int phase;
+  cudaEvent_t b, e;
+};
+
+// A packed-lower index range [b0, b1) (global indices) copied to the host stage at
+// local offset b0 - pk0 and final once `ready` (on the copy stream) has completed.
+struct DlPiece {
+  uint64_t b0, b1;
+  cudaEvent_t ready;
+};
+// The download of one build, snapshotted at enqueue time (the engine may be reshaped
+// for the next k-point before the host unpacks this one).
+struct Download {
+  uint64_t ng = 0, pk0 = 0;
+  std::vector<DlPiece> s, h;
+  bool pending = false;
+};
+
+// Collective mode of hsdla_b200_engine_reduce (include/hsdla_b200.h HSDLA_B200_REDUCE_*).
+enum ReduceMode { kReduceRoot = 0, kReduceScatter = 1 };
+
+}  // namespace hsdla_b200
+
+struct hsdla_b200_engine {
+  int device = 0;
+  // ---- geometry ----
+  uint64_t na = 0, nl = 0, K = 0;  // local atoms, K = na * nl
+  uint64_t ng = 0;                 // N_G of the problem (global)
+  uint64_t c0 = 0, c1 = 0;         // H/S column window [c0, c1)
+  uint64_t ncol = 0;               // operand columns held: [c0, ng)
+  uint64_t pk0 = 0, npk = 0;       // window's global packed range [pk0, pk0 + npk)
+  uint64_t cap_cols = 0, cap_pk = 0;  // allocated capacity (columns of A/B/X, packed elements)
+  // ---- streams / buffers ----
+  cudaStream_t stream = nullptr, copy_stream = nullptr, comm_stream = nullptr;
+  double2* Aset[2] = {};  // A/B sets (set 1: k-point batches)
+  double2* Bset[2] = {};
+  double2 *X1 = nullptr, *X2 = nullptr;
+  double2 *Tab = nullptr, *Taa = nullptr, *Tbb = nullptr, *Paa = nullptr, *Pbb = nullptr, *Pab = nullptr;
+  double* U = nullptr;
+  int32_t* info = nullptr;        // per-atom potrf result of the original algorithm (-1 = HPD)
+  int* n_fail = nullptr;          // original algorithm: failed atoms so far in this build
+  double2 *Hp = nullptr, *Sp = nullptr;
+  double2* host_stage = nullptr;  // pinned, 2 * cap_pk (H at [0, npk), S at [cap_pk, cap_pk + npk))
+  int sms = 148;                  // persistent TRI grid
+  double* sk_ws = nullptr;        // stream-K workspace (sms slots x 64x64 complex)
+  uint32_t* sk_flags = nullptr;
+  uint32_t epoch = 0;
+  uint64_t device_bytes = 0, temp_bytes = 0;
+  // ---- collective group (ranks that share this window; their partials are summed) ----
+  ncclComm_t comm = nullptr;
+  bool comm_owned = true;         // false: the communicator belongs to the drop-in's cache
+  std::vector<hsdla_b200_engine*> local_group;  // same-device group reduced by a sum kernel (no NCCL)
+  int nranks = 1, rank = 0;
+  int red_mode = hsdla_b200::kReduceRoot;
+  int red_root = 0;
+
+  std::vector<hsdla_b200::ChunkPlan> whole, streamed, streamed_pg;  // streamed: pinned / pageable feed
+  bool streamed_dirty = true;                                       // streamed plans need a rebuild
+  std::vector<hsdla_b200::ChunkPlan> whole2;                        // set 1 (k-point batches)
+  cudaStream_t h2d_stream = nullptr;
+  cudaEvent_t ev_kup[2] = {}, ev_kbuilt[2] = {};
+  cudaEvent_t wait_before_s = nullptr, wait_before_h = nullptr;  // next enqueue_chunk waits (storage reuse)
+  // per-build timing
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<hsdla_b200::OpTime> ops;
+  cudaEvent_t ev_begin = nullptr, ev_end = nullptr, ev_s_done = nullptr, ev_s_red = nullptr,
+              ev_reduce_end = nullptr, ev_up0 = nullptr, ev_up1 = nullptr,
+              ev_a0 = nullptr,   // the first streamed chunk's A rows landed
+              ev_ops = nullptr;  // operators uploaded on the copy stream (engine_upload_operators)
+  bool ops_pending = false;      // the next build must wait for ev_ops before expanding T
+  static constexpr int kD2hPieces = 8;   // H downloads in column-range pieces, unpacked as each lands
+  cudaEvent_t ev_h_band[kD2hPieces] = {};  // final H contraction finished tile-column band q
+  cudaEvent_t ev_h_red[kD2hPieces] = {};   // ... and band q's packed range is reduced
+  int piece_tiles[kD2hPieces + 1] = {};    // tile-column boundaries of the pieces / bands
+  bool band_final_h = false;               // this build runs its final H contraction band by band
+  bool overlap_dl = false;                 // engine builds band their final H (a download follows)
+  bool banded = false;                     // ... and the last build did
+  // download pieces: events recorded on the copy stream (S: up to 1, H: up to kD2hPieces)
+  cudaEvent_t ev_dl_s = nullptr;
+  cudaEvent_t ev_dl_h[kD2hPieces] = {};
+  hsdla_b200::Download dl;                 // the enqueued, not yet unpacked download
+  std::vector<cudaEvent_t> ev_chunk_up;
+  int last_algo = 0, launches = 0;
+  int arith = HSDLA_B200_ARITH_3M;  // complex product scheme of the contractions
+  uint64_t n_hpd_last = 0;
+  bool built = false, reduced = false, uploaded_streamed = false;
+  cudaEvent_t ev_setup0 = nullptr, ev_setup1 = nullptr;  // last LAPW setup (tables + stream kernels)
+  cudaEvent_t ev_setup_mid = nullptr;                      // between the two kernels
+  uint64_t setup_bytes = 0;
+  void* lapw_scratch = nullptr;  // device copy of the LAPW inputs (grown on demand)
+  size_t lapw_scratch_bytes = 0;
+  // pinned staging slabs for pageable inputs and HSDL files, allocated on first use
+  static constexpr int kStageSlabs = 4;  // used round robin (8 measured no better)
+  char* stage_buf[kStageSlabs] = {};
+  cudaEvent_t stage_ev[kStageSlabs] = {};
+  bool stage_busy[kStageSlabs] = {};
+  int stage_next = 0;
+  // HSDL file view: a read-only mapping of the last file this engine loaded, kept while the
+  // file's (device, inode, size, mtime) stay the same, so repeated k-point calls on one file
+  // copy rows straight out of the page cache without a pread per column piece
+  const char* fmap = nullptr;
+  size_t fmap_len = 0;
+  struct stat fmap_st {};
+  double tr_pack_ms = 0, tr_wait_ms = 0;  // HSDLA_B200_TRACE: pageable staging accounting
+  uint64_t tr_pack_bytes = 0;
+  // roofline: events around the whole-build S and H contraction launches, harvested lazily
+  static constexpr int kRing = 64;
+  struct KTimer {
+    cudaEvent_t s0 = nullptr, s1 = nullptr, h0 = nullptr, h1 = nullptr;
+    bool pending = false;
+    uint64_t flops_h = 0, flops_s = 0;
+  } ring[kRing];
+  uint64_t builds = 0;
+  double sum_s_ms = 0, sum_h_ms = 0;
+  uint64_t sum_flops_h = 0, sum_flops_s = 0, timed_builds = 0;
+
+  double2* A(int set = 0) const { return Aset[set]; }
+  double2* B(int set = 0) const { return Bset[set]; }
+};
+
+namespace hsdla_b200 {
+
+// Engine shard description (hsdla_b200_shard in the C-ABI, with defaults resolved).
+struct ShardSpec {
+  uint64_t na = 0, nl = 0, ng = 0;
+  uint64_t c0 = 0, c1 = 0;       // column window; c1 == 0: [0, ng)
+  uint64_t ng_capacity = 0;      // allocate for up to this N_G (0: ng)
+};
+
+constexpr size_t kStageSlab = size_t(64) << 20;
+
+void check_dims(uint64_t na, uint64_t nl, uint64_t ng);
+bool valid_algo(int algo);
+hsdla_b200_engine* engine_create(int device, const ShardSpec& spec);
+void engine_free(hsdla_b200_engine* e);
+// Re-target an engine at N_G = ng (column window [c0, c1), c1 == 0: whole) within its
+// allocated capacity; false (engine unchanged) if it does not fit.  Waits for the engine.
+bool engine_reshape(hsdla_b200_engine* e, uint64_t ng, uint64_t c0 = 0, uint64_t c1 = 0);
+void engine_upload(hsdla_b200_engine* e, const hsdla_b200_problem* p, uint64_t a0);
+void engine_fill_synthetic(hsdla_b200_engine* e, uint64_t seed);
+void engine_build(hsdla_b200_engine* e, int algo);
+void engine_build_streamed(hsdla_b200_engine* e, const hsdla_b200_problem* p, uint64_t a0, int algo);
+void engine_kpoints(hsdla_b200_engine* e, const hsdla_b200_problem* common, uint64_t nk, const uint64_t* ngk,
+                    const double* const* A, const double* const* B, int algo, double* const* H, double* const* S);
+void engine_reduce(hsdla_b200_engine* e, int root);
+// The sum of the partials of a group of engines (same window, disjoint atom shards): NCCL
+// (every engine has a communicator; grouped calls across the engines of this process) or,
+// for engines that share one device, a deterministic sum kernel.  mode kReduceRoot: the
+// whole result on rank `root`; kReduceScatter: every rank owns a contiguous slice of each
+// band (hsdla_b200_engine_owned).  Overlaps the H phases band by band.
+void group_reduce(const std::vector<hsdla_b200_engine*>& g, int mode, int root);
+void engine_sync(hsdla_b200_engine* e, hsdla_b200_stats* st);
+// Enqueue the D2H of the packed ranges this engine owns (all of them before a reduce),
+// then unpack them into the lower triangles of H, S (either may be null).
+void enqueue_download(hsdla_b200_engine* e);
+void finish_download(hsdla_b200_engine* e, double* H, double* S,
+                     std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now());
+void engine_download(hsdla_b200_engine* e, double* H, double* S);
+// Packed ranges of the current result this engine holds final values for.
+std::vector<std::pair<uint64_t, uint64_t>> engine_owned(const hsdla_b200_engine* e);
+uint64_t executed_flops(uint64_t na, uint64_t nl, uint64_t ng, int arith, int algo);
+void flop_model(int variant, uint64_t na, uint64_t nl, uint64_t ng, uint64_t n_hpd, uint64_t* l);
+float ev_ms(cudaEvent_t a, cudaEvent_t b);
+void harvest(hsdla_b200_engine* e, hsdla_b200_engine::KTimer& t);
+
+// building blocks shared with the HSDL-file and LAPW front ends
+void begin_build(hsdla_b200_engine* e, int algo);
+void ensure_streamed_plans(hsdla_b200_engine* e);
+void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool last, hsdla_b200_engine::KTimer* kt,
+                   bool s_rest = false);
+char* stage_acquire(hsdla_b200_engine* e, int& slot);
+void stage_release(hsdla_b200_engine* e, int slot, cudaStream_t s);
+
+// HSDL v1 files (hsdl_file.cpp)
+void engine_load_file(hsdla_b200_engine* e, const char* path, uint64_t a0);
+void engine_build_file(hsdla_b200_engine* e, const char* path, uint64_t a0, int algo);
+void release_file_view(hsdla_b200_engine* e);
+
+}  // namespace hsdla_b200

@@ -1,0 +1,503 @@
+// The reference's kernel layer (hsdla::kernels, kernels.hpp:24-75) on the GPU: host
+// matrices in and out, one call = upload, the contraction engine, download.
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "common.hpp"
+#include "device.hpp"
+#include "host_pool.hpp"
+
+namespace hsdla_b200 {
+
+// ---------------------------------------------------------------------------
+// The reference's kernel layer (hsdla::kernels, kernels.hpp:24-75) on the GPU.
+// Host matrices in and out (interleaved complex, column-major, explicit leading
+// dimensions), one call = upload, the contraction engine, download.  Same
+// semantics as the reference: triangular outputs lower only (upper never read or
+// written), beta == 0 never reads C, alpha == 0 only scales C (and still charges
+// the closed-form ledger), dimension errors -> DimensionError.
+// ---------------------------------------------------------------------------
+namespace kl {
+
+// Per-call device temporaries of the kernel layer, stream-ordered from the device's
+// default memory pool with an unbounded release threshold: repeated calls reuse the
+// cached blocks instead of paying cudaMalloc / cudaFree (a device-wide sync) every call.
+// hsdla_b200_release_cache() trims the pool.
+static void keep_pool_cached(int device) {
+  static std::once_flag once[64];
+  std::call_once(once[device & 63], [device] {
+    cudaMemPool_t pool;
+    HS_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = UINT64_MAX;
+    HS_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  });
+}
+struct DevBuf {
+  void* p = nullptr;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(size_t bytes, cudaStream_t stream) : s(stream) {
+    HS_CUDA(cudaMallocAsync(&p, std::max<size_t>(bytes, 16), s));
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+  double2* c() const { return static_cast<double2*>(p); }
+};
+
+__global__ void scale_kernel(double2* __restrict__ x, uint64_t rows, uint64_t cols, double br, double bi,
+                             int lower_only) {
+  for (uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < rows * cols;
+       idx += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t i = idx % rows, j = idx / rows;
+    if (lower_only && i < j) continue;
+    const double2 v = x[idx];
+    // beta == 0 writes an exact 0 without reading (scale_in_place, kernels.cpp:200-207)
+    x[idx] = (br == 0.0 && bi == 0.0) ? make_double2(0.0, 0.0) : make_double2(br * v.x - bi * v.y, br * v.y + bi * v.x);
+  }
+}
+
+// dst (c x r) = conj(src (r x c))^T, dense; with `lower` only src's lower triangle
+// (i >= j) is used (the rest is taken as 0) — the triangular operand of trmm.
+__global__ void conj_transpose_kernel(const double2* __restrict__ src, double2* __restrict__ dst, uint64_t r,
+                                      uint64_t c, int lower, int transpose) {
+  for (uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < r * c;
+       idx += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t i = idx % r, j = idx / r;  // source element (i, j)
+    double2 v = src[idx];
+    if (lower && i < j) v = make_double2(0.0, 0.0);
+    if (transpose)
+      dst[j + i * c] = make_double2(v.x, -v.y);
+    else
+      dst[idx] = v;
+  }
+}
+
+// The left operand L with L^H = the hemm operator of an n x n lower-authoritative H
+// (kernels.cpp:152-167: h(i,l) for l <= i, conj(h(l,i)) above):
+//   L(i,j) = h(i,j) for i > j,  conj(h(j,i)) for i <= j.
+__global__ void hermitian_full_kernel(const double2* __restrict__ h, double2* __restrict__ f, uint64_t n) {
+  for (uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < n * n;
+       idx += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t i = idx % n, j = idx / n;
+    double2 v = i > j ? h[i + j * n] : h[j + i * n];
+    if (i <= j) v.y = -v.y;
+    f[idx] = v;
+  }
+}
+
+__global__ void pack_lower_kernel(const double2* __restrict__ full, double2* __restrict__ pk, uint64_t n, int unpack) {
+  for (uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < n * n;
+       idx += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t i = idx % n, j = idx / n;
+    if (i < j) continue;
+    const uint64_t k = j * (2 * n - j + 1) / 2 + (i - j);
+    if (unpack)
+      const_cast<double2*>(full)[idx] = pk[k];
+    else
+      pk[k] = full[idx];
+  }
+}
+
+// Pinned staging ring per device for the kernel layer's host <-> device traffic
+// (kRingSlabs page-locked slabs used round robin, multi-threaded host packing): calls on
+// one device are serialised by its mutex.
+static constexpr int kRingSlabs = 4;
+struct Ring {
+  std::mutex mu;
+  char* buf[kRingSlabs] = {};
+  cudaEvent_t ev[kRingSlabs] = {};
+};
+static constexpr size_t kRingSlab = size_t(32) << 20;
+static Ring& ring_for(int device) {
+  static std::mutex mu;
+  static std::map<int, std::unique_ptr<Ring>> rings;
+  std::lock_guard<std::mutex> lk(mu);
+  auto& r = rings[device];
+  if (!r) r = std::make_unique<Ring>();
+  return *r;
+}
+
+struct Ctx {
+  int sms = 148;
+  int arith = HSDLA_B200_ARITH_3M;
+  cudaStream_t s = nullptr;
+  Ring* ring = nullptr;
+  std::unique_lock<std::mutex> lock;
+  explicit Ctx(int device) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+      (void)cudaGetLastError();
+      throw Fail{HSDLA_B200_CONFIG_ERROR, "no such CUDA device (the B200 path has no CPU fallback)"};
+    }
+    HS_CUDA(cudaSetDevice(device));
+    HS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    set_kernel_attributes();
+    keep_pool_cached(device);
+    arith = g_default_arith.load();
+    HS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    ring = &ring_for(device);
+    lock = std::unique_lock<std::mutex>(ring->mu);
+    if (!ring->buf[0])
+      for (int i = 0; i < kRingSlabs; ++i) {
+        HS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ring->buf[i]), kRingSlab));
+        HS_CUDA(cudaEventCreateWithFlags(&ring->ev[i], cudaEventDisableTiming));
+      }
+  }
+  ~Ctx() {
+    if (s) {
+      cudaStreamSynchronize(s);  // the ring's slabs may still be in flight
+      cudaStreamDestroy(s);
+    }
+  }
+  unsigned grid(uint64_t n) const {
+    return static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(sms) * 16) + 0);
+  }
+  // host r x c (leading dimension ld) -> dense device r x c, through the pinned ring
+  void up(double2* d, const double* h, uint64_t r, uint64_t c, uint64_t ld) {
+    if (!r || !c) return;
+    const size_t colb = r * 16;
+    const double2* hc = reinterpret_cast<const double2*>(h);
+    if (colb > kRingSlab) {  // huge columns: pageable copy
+      HS_CUDA(cudaMemcpy2DAsync(d, colb, h, ld * 16, colb, c, cudaMemcpyHostToDevice, s));
+      return;
+    }
+    const uint64_t per = kRingSlab / colb;
+    int slot = 0;
+    for (uint64_t j0 = 0; j0 < c; j0 += per, slot = (slot + 1) % kRingSlabs) {
+      const uint64_t nc = std::min(per, c - j0);
+      HS_CUDA(cudaEventSynchronize(ring->ev[slot]));
+      char* b = ring->buf[slot];
+      par_for(nc, nc * colb, [&](uint64_t j) { copy_nt(b + j * colb, hc + (j0 + j) * ld, colb); });
+      _mm_sfence();
+      HS_CUDA(cudaMemcpyAsync(d + j0 * r, b, nc * colb, cudaMemcpyHostToDevice, s));
+      HS_CUDA(cudaEventRecord(ring->ev[slot], s));
+    }
+  }
+  // dense device r x c -> host r x c (leading dimension ld), through the pinned ring
+  void down(double* h, uint64_t ld, const double2* d, uint64_t r, uint64_t c) {
+    if (!r || !c) return;
+    const size_t colb = r * 16;
+    double2* hc = reinterpret_cast<double2*>(h);
+    if (colb > kRingSlab) {
+      HS_CUDA(cudaMemcpy2DAsync(h, ld * 16, d, colb, colb, c, cudaMemcpyDeviceToHost, s));
+      sync();
+      return;
+    }
+    const uint64_t per = kRingSlab / colb;
+    const uint64_t pieces = (c + per - 1) / per;
+    auto issue = [&](uint64_t q) {
+      const uint64_t j0 = q * per, nc = std::min(per, c - j0);
+      HS_CUDA(cudaMemcpyAsync(ring->buf[q % kRingSlabs], d + j0 * r, nc * colb, cudaMemcpyDeviceToHost, s));
+      HS_CUDA(cudaEventRecord(ring->ev[q % kRingSlabs], s));
+    };
+    for (uint64_t q = 0; q + 1 < kRingSlabs && q < pieces; ++q) issue(q);
+    for (uint64_t q = 0; q < pieces; ++q) {
+      // the next slabs land while this one is unpacked (slab of q + kRingSlabs - 1 = q - 1's)
+      if (q + kRingSlabs - 1 < pieces) issue(q + kRingSlabs - 1);
+      HS_CUDA(cudaEventSynchronize(ring->ev[q % kRingSlabs]));
+      const uint64_t j0 = q * per, nc = std::min(per, c - j0);
+      const char* b = ring->buf[q % kRingSlabs];
+      par_for(nc, nc * colb, [&](uint64_t j) { copy_nt(hc + (j0 + j) * ld, b + j * colb, colb); });
+      _mm_sfence();
+    }
+  }
+  // device packed-lower n x n -> the lower triangle of host C (ldc), upper untouched
+  void down_lower(double* C, uint64_t ldc, const double2* pk, uint64_t n) {
+    double2* hc = reinterpret_cast<double2*>(C);
+    auto pc = [&](uint64_t j) { return j * (2 * n - j + 1) / 2; };
+    std::vector<uint64_t> cuts{0};  // column ranges whose packed bytes fit a slab
+    while (cuts.back() < n) {
+      uint64_t j = cuts.back() + 1;
+      while (j < n && (pc(j + 1) - pc(cuts.back())) * 16 <= kRingSlab) ++j;
+      cuts.push_back(j);
+    }
+    const uint64_t pieces = cuts.size() - 1;
+    for (uint64_t q = 0; q < pieces; ++q)
+      if ((pc(cuts[q + 1]) - pc(cuts[q])) * 16 > kRingSlab) {  // a single column beyond a slab
+        std::vector<double2> tmp(pc(n));
+        HS_CUDA(cudaMemcpyAsync(tmp.data(), pk, pc(n) * 16, cudaMemcpyDeviceToHost, s));
+        sync();
+        for (uint64_t j = 0; j < n; ++j) std::memcpy(hc + j * ldc + j, tmp.data() + pc(j), (n - j) * 16);
+        return;
+      }
+    auto issue = [&](uint64_t q) {
+      const uint64_t b0 = pc(cuts[q]), b1 = pc(cuts[q + 1]);
+      HS_CUDA(cudaMemcpyAsync(ring->buf[q % kRingSlabs], pk + b0, (b1 - b0) * 16, cudaMemcpyDeviceToHost, s));
+      HS_CUDA(cudaEventRecord(ring->ev[q % kRingSlabs], s));
+    };
+    for (uint64_t q = 0; q + 1 < kRingSlabs && q < pieces; ++q) issue(q);
+    for (uint64_t q = 0; q < pieces; ++q) {
+      if (q + kRingSlabs - 1 < pieces) issue(q + kRingSlabs - 1);
+      HS_CUDA(cudaEventSynchronize(ring->ev[q % kRingSlabs]));
+      const double2* b = reinterpret_cast<const double2*>(ring->buf[q % kRingSlabs]);
+      const uint64_t j0 = cuts[q], base = pc(j0), ncol = cuts[q + 1] - j0;
+      par_for(ncol, (pc(cuts[q + 1]) - base) * 16,
+              [&](uint64_t t) { copy_nt(hc + (j0 + t) * ldc + j0 + t, b + pc(j0 + t) - base, (n - j0 - t) * 16); });
+      _mm_sfence();
+    }
+  }
+  void sync() { HS_CUDA(cudaStreamSynchronize(s)); }
+};
+
+static void need(bool ok, const char* what) {
+  if (!ok) throw Fail{HSDLA_B200_DIMENSION_ERROR, what};
+}
+
+// C(lower, n x n, device packed) = alpha * sum_s L_s^H R_s + beta * C over dense k x n operands.
+static void tri(Ctx& x, int nseg, const double2* const* L, const double2* const* R, uint64_t k, uint64_t n, double ar,
+                double ai, double beta, double2* Cp) {
+  const int tiles = static_cast<int>((n + kTriBM - 1) / kTriBM);
+  CtnParams P;
+  std::memset(&P, 0, sizeof(P));
+  for (int sg = 0; sg < nseg; ++sg) {
+    make_map(&P.L[sg], L[sg], 2 * k, n, 1, 2 * k, 2 * k * n, kTriBM, 1);
+    make_map(&P.R[sg], R[sg], 2 * k, n, 1, 2 * k, 2 * k * n, kTriBM, 1);
+    P.kchunks[sg] = chunks_of(k);
+  }
+  P.nseg = nseg;
+  P.n = static_cast<int>(n);
+  P.tiles = tiles;
+  P.tiles_total = tiles * (tiles + 1) / 2;
+  P.band = tri_band();
+  P.out = Cp;
+  DevBuf ws(static_cast<size_t>(x.sms) * kSkSlot * sizeof(double), x.s), flags(x.sms * sizeof(uint32_t), x.s);
+  HS_CUDA(cudaMemsetAsync(flags.p, 0, x.sms * sizeof(uint32_t), x.s));
+  P.sk_ws = static_cast<double*>(ws.p);
+  P.sk_flags = static_cast<uint32_t*>(flags.p);
+  P.epoch = 1;
+  P.alpha_re = ar;
+  P.alpha_im = ai;
+  P.beta = beta;
+  const uint64_t work = static_cast<uint64_t>(P.tiles_total) * chunks_of(k) * nseg;
+  const dim3 g(static_cast<unsigned>(std::min<uint64_t>(x.sms, work)));
+  launch_tri_kernel(x.arith, g, P, x.s);
+  x.sync();  // ws / flags go out of scope
+}
+
+// C (m x n, device dense, ld m) = alpha L^H R + beta C; L: k x m, R: k x n dense.
+static void rect(Ctx& x, const double2* L, const double2* R, uint64_t m, uint64_t n, uint64_t k, double ar, double ai,
+                 double beta, double2* C) {
+  CtnParams P;
+  std::memset(&P, 0, sizeof(P));
+  make_map(&P.L[0], L, 2 * k, m, 1, 2 * k, 2 * k * m, kBatBM, 1);
+  make_map(&P.R[0], R, 2 * k, 1, n, 2 * k, 2 * k, 1, kBatBN);
+  P.kchunks[0] = chunks_of(k);
+  P.r_row_z[0] = 1;
+  P.nseg = 1;
+  P.n = static_cast<int>(n);
+  P.m_valid = static_cast<int>(m);
+  P.out = C;
+  P.ldo = m;
+  P.alpha_re = ar;
+  P.alpha_im = ai;
+  P.beta = beta;
+  const uint64_t tx = (n + kBatBN - 1) / kBatBN, ty = (m + kBatBM - 1) / kBatBM;
+  if (tx * ty > static_cast<uint64_t>(INT32_MAX)) throw Fail{HSDLA_B200_SIZING_ERROR, "too many batched tiles"};
+  P.bat_tx = static_cast<int>(tx);
+  P.bat_ty = static_cast<int>(ty);
+  P.bat_tiles = static_cast<int>(tx * ty);
+  const dim3 g(static_cast<unsigned>(std::min<uint64_t>(tx * ty, x.sms)));
+  launch_bat_kernel(x.arith, g, P, x.s);
+}
+
+// Triangular family: herk (nseg 1, R = L), her2k (2), herkx (1).  C lower n x n host.
+static void tri_family(int device, int which, uint64_t n, uint64_t k, double ar, double ai, const double* A,
+                       uint64_t lda, const double* B, uint64_t ldb, double beta, double* C, uint64_t ldc) {
+  need(C != nullptr && ldc >= std::max<uint64_t>(n, 1), "C: null or ldc < n");
+  need(A != nullptr && lda >= std::max<uint64_t>(k, 1), "A: null or lda < k");
+  if (which != 0) need(B != nullptr && ldb >= std::max<uint64_t>(k, 1), "B: null or ldb < k");
+  if (n == 0) return;
+  Ctx x(device);
+  const uint64_t npk = n * (n + 1) / 2;
+  DevBuf dC(n * n * 16, x.s), dP(npk * 16, x.s);
+  const bool alpha0 = (ar == 0.0 && ai == 0.0) || k == 0;
+  if (beta != 0.0 || alpha0) x.up(dC.c(), C, n, n, ldc);
+  if (alpha0) {  // scale_lower_in_place (kernels.cpp:209-217): only C's lower triangle
+    scale_kernel<<<x.grid(n * n), 256, 0, x.s>>>(dC.c(), n, n, beta, 0.0, 1);
+    pack_lower_kernel<<<x.grid(n * n), 256, 0, x.s>>>(dC.c(), dP.c(), n, 0);
+  } else {
+    if (beta != 0.0) pack_lower_kernel<<<x.grid(n * n), 256, 0, x.s>>>(dC.c(), dP.c(), n, 0);
+    DevBuf dA(k * n * 16, x.s), dB(which != 0 ? k * n * 16 : 16, x.s);
+    x.up(dA.c(), A, k, n, lda);
+    if (which != 0) x.up(dB.c(), B, k, n, ldb);
+    if (which == 0) {
+      const double2* L[1] = {dA.c()};
+      tri(x, 1, L, L, k, n, ar, 0.0, beta, dP.c());
+    } else if (which == 1) {
+      // her2k: alpha A^H B + conj(alpha) B^H A = (conj(alpha) A)^H B + B^H (conj(alpha) A)
+      scale_kernel<<<x.grid(k * n), 256, 0, x.s>>>(dA.c(), k, n, ar, -ai, 0);
+      const double2* L[2] = {dA.c(), dB.c()};
+      const double2* R[2] = {dB.c(), dA.c()};
+      tri(x, 2, L, R, k, n, 1.0, 0.0, beta, dP.c());
+    } else {
+      const double2* L[1] = {dA.c()};
+      const double2* R[1] = {dB.c()};
+      tri(x, 1, L, R, k, n, ar, ai, beta, dP.c());
+    }
+  }
+  HS_CUDA(cudaGetLastError());
+  // lower triangle back into the caller's C (upper never written)
+  x.down_lower(C, ldc, dP.c(), n);
+  x.sync();
+}
+
+// gemm core on device operands: C (m x n) = alpha opA^H-form ... + beta C, complex beta.
+static void gemm_dev(Ctx& x, const double2* Lk, const double2* Rk, uint64_t m, uint64_t n, uint64_t k, double ar,
+                     double ai, double br, double bi, double2* dC) {
+  double beta = 0.0;
+  if (br != 0.0 || bi != 0.0) {
+    if (!(br == 1.0 && bi == 0.0)) scale_kernel<<<x.grid(m * n), 256, 0, x.s>>>(dC, m, n, br, bi, 0);
+    beta = 1.0;
+  }
+  if ((ar == 0.0 && ai == 0.0) || k == 0) {
+    if (beta == 0.0) scale_kernel<<<x.grid(m * n), 256, 0, x.s>>>(dC, m, n, 0.0, 0.0, 0);
+    return;
+  }
+  rect(x, Lk, Rk, m, n, k, ar, ai, beta, dC);
+}
+
+}  // namespace kl
+
+}  // namespace hsdla_b200
+
+using namespace hsdla_b200;
+
+extern "C" {
+
+// ---- the reference kernel layer (kernels.hpp) --------------------------------
+int hsdla_b200_herk(int device, uint64_t n, uint64_t k, double alpha, const double* A, uint64_t lda, double beta,
+                    double* C, uint64_t ldc, uint64_t* ledger_flops) {
+  return guarded([&] {
+    kl::tri_family(device, 0, n, k, alpha, 0.0, A, lda, nullptr, 0, beta, C, ldc);
+    if (ledger_flops) *ledger_flops += 4 * k * n * n;  // kernels.cpp:316
+  });
+}
+int hsdla_b200_her2k(int device, uint64_t n, uint64_t k, const double* alpha, const double* A, uint64_t lda,
+                     const double* B, uint64_t ldb, double beta, double* C, uint64_t ldc, uint64_t* ledger_flops) {
+  return guarded([&] {
+    kl::need(alpha != nullptr, "null alpha");
+    kl::tri_family(device, 1, n, k, alpha[0], alpha[1], A, lda, B, ldb, beta, C, ldc);
+    if (ledger_flops) *ledger_flops += 8 * k * n * n;  // kernels.cpp:339
+  });
+}
+int hsdla_b200_herkx(int device, uint64_t n, uint64_t k, const double* alpha, const double* A, uint64_t lda,
+                     const double* B, uint64_t ldb, double beta, double* C, uint64_t ldc, uint64_t* ledger_flops) {
+  return guarded([&] {
+    kl::need(alpha != nullptr, "null alpha");
+    kl::tri_family(device, 2, n, k, alpha[0], alpha[1], A, lda, B, ldb, beta, C, ldc);
+    if (ledger_flops) *ledger_flops += 4 * k * n * n;  // kernels.cpp:363
+  });
+}
+
+int hsdla_b200_gemm(int device, int trans_a, int trans_b, uint64_t m, uint64_t n, uint64_t k, const double* alpha,
+                    const double* A, uint64_t lda, const double* B, uint64_t ldb, const double* beta, double* C,
+                    uint64_t ldc, uint64_t* ledger_flops) {
+  return guarded([&] {
+    kl::need(alpha && beta, "null alpha / beta");
+    kl::need((trans_a == 0 || trans_a == 1) && (trans_b == 0 || trans_b == 1), "trans must be 0 (None) or 1 (ConjTrans)");
+    // op(A) is m x k: A stored m x k (None) or k x m (ConjTrans); op(B) k x n: B k x n / n x k
+    const uint64_t ar = trans_a ? k : m, ac = trans_a ? m : k, br = trans_b ? n : k, bc = trans_b ? k : n;
+    kl::need(A && lda >= std::max<uint64_t>(ar, 1), "A: null or lda too small");
+    kl::need(B && ldb >= std::max<uint64_t>(br, 1), "B: null or ldb too small");
+    kl::need(C && ldc >= std::max<uint64_t>(m, 1), "C: null or ldc < m");
+    if (m && n) {
+      kl::Ctx x(device);
+      kl::DevBuf dA(ar * ac * 16, x.s), dB(br * bc * 16, x.s), dL(k * m * 16, x.s), dR(k * n * 16, x.s),
+          dC(m * n * 16, x.s);
+      x.up(dA.c(), A, ar, ac, lda);
+      x.up(dB.c(), B, br, bc, ldb);
+      if (beta[0] != 0.0 || beta[1] != 0.0) x.up(dC.c(), C, m, n, ldc);
+      // the CTN core needs op(A)^H (k x m) and op(B) (k x n): conj-transpose where needed
+      // (the reference materialises the same conj transposes, kernels.cpp:262-271)
+      const double2* L = dA.c();
+      const double2* R = dB.c();
+      if (!trans_a && ar * ac != 0) {
+        kl::conj_transpose_kernel<<<x.grid(ar * ac), 256, 0, x.s>>>(dA.c(), dL.c(), ar, ac, 0, 1);
+        L = dL.c();
+      }
+      if (trans_b && br * bc != 0) {
+        kl::conj_transpose_kernel<<<x.grid(br * bc), 256, 0, x.s>>>(dB.c(), dR.c(), br, bc, 0, 1);
+        R = dR.c();
+      }
+      kl::gemm_dev(x, L, R, m, n, k, alpha[0], alpha[1], beta[0], beta[1], dC.c());
+      HS_CUDA(cudaGetLastError());
+      x.down(C, ldc, dC.c(), m, n);
+      x.sync();
+    }
+    if (ledger_flops) *ledger_flops += 8 * m * n * k;  // kernels.cpp:254
+  });
+}
+
+int hsdla_b200_hemm(int device, uint64_t n, uint64_t m, const double* alpha, const double* Hm, uint64_t ldh,
+                    const double* B, uint64_t ldb, const double* beta, double* C, uint64_t ldc, uint64_t* ledger_flops) {
+  return guarded([&] {
+    kl::need(alpha && beta, "null alpha / beta");
+    kl::need(Hm && ldh >= std::max<uint64_t>(n, 1), "H: null or ldh < n");
+    kl::need(B && ldb >= std::max<uint64_t>(n, 1), "B: null or ldb < n");
+    kl::need(C && ldc >= std::max<uint64_t>(n, 1), "C: null or ldc < n");
+    if (n && m) {
+      kl::Ctx x(device);
+      kl::DevBuf dH(n * n * 16, x.s), dF(n * n * 16, x.s), dB(n * m * 16, x.s), dC(n * m * 16, x.s);
+      x.up(dH.c(), Hm, n, n, ldh);
+      x.up(dB.c(), B, n, m, ldb);
+      if (beta[0] != 0.0 || beta[1] != 0.0) x.up(dC.c(), C, n, m, ldc);
+      // H B = L^H B with L^H = the reference's hemm operator (the CTN core)
+      kl::hermitian_full_kernel<<<x.grid(n * n), 256, 0, x.s>>>(dH.c(), dF.c(), n);
+      kl::gemm_dev(x, dF.c(), dB.c(), n, m, n, alpha[0], alpha[1], beta[0], beta[1], dC.c());
+      HS_CUDA(cudaGetLastError());
+      x.down(C, ldc, dC.c(), n, m);
+      x.sync();
+    }
+    if (ledger_flops) *ledger_flops += 8 * n * n * m;  // kernels.cpp:296
+  });
+}
+
+int hsdla_b200_trmm(int device, int trans, uint64_t n, uint64_t m, const double* alpha, const double* T, uint64_t ldt,
+                    double* B, uint64_t ldb, uint64_t* ledger_flops) {
+  return guarded([&] {
+    kl::need(alpha != nullptr, "null alpha");
+    kl::need(trans == 0 || trans == 1, "trans must be 0 (None) or 1 (ConjTrans)");
+    kl::need(T && ldt >= std::max<uint64_t>(n, 1), "T: null or ldt < n");
+    kl::need(B && ldb >= std::max<uint64_t>(n, 1), "B: null or ldb < n");
+    if (n && m) {
+      kl::Ctx x(device);
+      kl::DevBuf dT(n * n * 16, x.s), dL(n * n * 16, x.s), dB(n * m * 16, x.s), dC(n * m * 16, x.s);
+      x.up(dT.c(), T, n, n, ldt);
+      x.up(dB.c(), B, n, m, ldb);
+      // op(T) B = L^H B with L = lower(T) (ConjTrans) or L = lower(T)^H (None)
+      kl::conj_transpose_kernel<<<x.grid(n * n), 256, 0, x.s>>>(dT.c(), dL.c(), n, n, 1, trans ? 0 : 1);
+      kl::gemm_dev(x, dL.c(), dB.c(), n, m, n, alpha[0], alpha[1], 0.0, 0.0, dC.c());
+      HS_CUDA(cudaGetLastError());
+      x.down(B, ldb, dC.c(), n, m);
+      x.sync();
+    }
+    if (ledger_flops) *ledger_flops += 4 * n * n * m;  // kernels.cpp:390
+  });
+}
+
+int hsdla_b200_diag_scale(int device, uint64_t rows, uint64_t cols, const double* u, const double* B, uint64_t ldb,
+                          double* X, uint64_t ldx, uint64_t* ledger_flops) {
+  return guarded([&] {
+    kl::need(u && B && X && ldb >= std::max<uint64_t>(rows, 1) && ldx >= std::max<uint64_t>(rows, 1),
+             "diag_scale: null pointer or leading dimension < rows");
+    if (rows && cols) {
+      kl::Ctx x(device);
+      kl::DevBuf dB(rows * cols * 16, x.s), dX(rows * cols * 16, x.s), du(rows * 8, x.s);
+      x.up(dB.c(), B, rows, cols, ldb);
+      HS_CUDA(cudaMemcpyAsync(du.p, u, rows * 8, cudaMemcpyHostToDevice, x.s));
+      launch_diag_scale(dB.c(), static_cast<const double*>(du.p), dX.c(), rows, rows, cols, x.s);
+      x.down(X, ldx, dX.c(), rows, cols);  // X may alias B (in place, kernels.cpp:438-450)
+      x.sync();
+    }
+    if (ledger_flops) *ledger_flops += 2 * rows * cols;  // kernels.cpp:444
+  });
+}
+
+}  // extern "C"

@@ -84,25 +84,31 @@ __host__ __device__ inline void sph_bessel(int lmax, double x, double* j) {
     for (int l = 1; l < lmax; ++l) j[l + 1] = (2.0 * l + 1.0) * ix * j[l] - j[l - 1];
     return;
   }
-  // Miller downward recurrence from well above lmax, normalised by j_0
+  // Miller downward recurrence from well above lmax.  Normalised by whichever of
+  // j_0 = sin x / x and j_1 = (sin x / x - cos x) / x is larger in magnitude: they never
+  // vanish together, so the normalisation keeps full precision next to the zeros of j_0
+  // (x = n pi, where normalising by j_0 alone loses every digit).  In the Miller range
+  // (1e-3 <= x <= lmax) j_1 is chosen only for |j_1| > |j_0|, i.e. x > 2, where its
+  // formula has no cancellation.
   const int top = lmax + 30 + static_cast<int>(x);
-  double jp1 = 0.0, jl = 1e-300, scale = 1.0;
+  double jp1 = 0.0, jl = 1e-300, m1 = 0.0;  // m1: the unnormalised j_1
   for (int l = top; l >= 1; --l) {
     const double jm1 = (2.0 * l + 1.0) * ix * jl - jp1;
     jp1 = jl;
     jl = jm1;  // now j_{l-1}
     if (l - 1 <= lmax) j[l - 1] = jl;
+    if (l - 1 == 1) m1 = jl;
     if (fabs(jl) > 1e250) {  // rescale everything computed so far
       const double f = 1e-250;
       jl *= f;
       jp1 *= f;
+      m1 *= f;
       for (int m = l - 1; m <= lmax; ++m) j[m] *= f;
-      scale *= f;
     }
   }
-  const double norm = j0 / jl;
+  const double j1 = (j0 - c) * ix;
+  const double norm = fabs(j1) > fabs(j0) ? j1 / m1 : j0 / jl;
   for (int l = 0; l <= lmax; ++l) j[l] *= norm;
-  (void)scale;
 }
 
 // Y_lm(theta, phi) for one m >= 0 and all l in [m, lmax], as the complex values

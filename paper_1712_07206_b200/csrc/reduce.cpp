@@ -1,0 +1,339 @@
+// The path's one exchange step and the way out of the device: the sum of the partial
+// H, S of the engines that share a column window (H and S are sums over
+// atoms, pipeline.cpp:296-324), ownership of the reduced ranges, downloads into the
+// caller's lower triangles, and per-build statistics.
+//
+// Reduce segments.  A build's result is reduced segment by segment: the tile-column bands
+// of a banded final H contraction (band q's reduce overlaps band q+1's compute; S, computed
+// first, uses the same segments and overlaps the H phases), or the whole window.  In
+// SCATTER mode rank r of P owns the r-th of P equal slices of every segment (the last rank
+// also the remainder): ncclReduceScatter in place (+ an ncclReduce of the remainder), so no
+// GPU receives more than 1/P of H and S and every GPU downloads its own slices over its own
+// PCIe link.  ROOT mode sums everything onto one rank (ncclReduce).  Engines that share one
+// device (single-GPU emulation of a multi-GPU grid, tests) are summed by a deterministic
+// kernel on the owner's stream instead of NCCL; ownership is identical.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+
+#include "device.hpp"
+#include "engine.hpp"
+#include "host_pool.hpp"
+
+namespace hsdla_b200 {
+
+using Range = std::pair<uint64_t, uint64_t>;
+
+static uint64_t piece_col(const hsdla_b200_engine* e, int q) {
+  return std::min<uint64_t>(e->ng, static_cast<uint64_t>(e->piece_tiles[q]) * kTriBM);
+}
+
+// Global packed ranges of the reduce segments of the last build (see the file comment).
+static std::vector<Range> segments(const hsdla_b200_engine* e) {
+  std::vector<Range> s;
+  if (e->banded) {
+    for (int q = 0; q < hsdla_b200_engine::kD2hPieces; ++q)
+      s.emplace_back(packed_col(e->ng, piece_col(e, q)), packed_col(e->ng, piece_col(e, q + 1)));
+  } else {
+    s.emplace_back(e->pk0, e->pk0 + e->npk);
+  }
+  return s;
+}
+
+// The slice of segment [s0, s1) that rank r of P owns after a SCATTER reduce.
+static Range scatter_slice(uint64_t s0, uint64_t s1, int r, int P) {
+  const uint64_t rc = (s1 - s0) / static_cast<uint64_t>(P);
+  const uint64_t o0 = s0 + static_cast<uint64_t>(r) * rc;
+  return {o0, r == P - 1 ? s1 : o0 + rc};
+}
+
+// The part of segment [s0, s1) this engine holds final values for.
+static Range owned_part(const hsdla_b200_engine* e, uint64_t s0, uint64_t s1) {
+  if (!e->reduced || e->nranks <= 1) return {s0, s1};
+  if (e->red_mode == kReduceRoot) return e->rank == e->red_root ? Range{s0, s1} : Range{s1, s1};
+  return scatter_slice(s0, s1, e->rank, e->nranks);
+}
+
+std::vector<Range> engine_owned(const hsdla_b200_engine* e) {
+  std::vector<Range> out;
+  if (!e->built) return out;
+  for (const Range& sg : segments(e)) {
+    const Range o = owned_part(e, sg.first, sg.second);
+    if (o.second > o.first) out.push_back(o);
+  }
+  return out;
+}
+
+// NCCL reduce of one segment of `buf` (the engine's packed window) on its comm stream.
+static void nccl_segment(hsdla_b200_engine* e, double2* buf, Range sg, int mode, int root) {
+  const uint64_t len = sg.second - sg.first;
+  if (!len) return;
+  double2* base = buf + (sg.first - e->pk0);
+  if (mode == kReduceRoot) {
+    HS_NCCL(ncclReduce(base, base, 2 * len, ncclFloat64, ncclSum, root, e->comm, e->comm_stream));
+    return;
+  }
+  const uint64_t P = static_cast<uint64_t>(e->nranks), rc = len / P, rem = len - P * rc;
+  if (rc)  // in place: rank r's slice is base + r rc
+    HS_NCCL(ncclReduceScatter(base, base + static_cast<uint64_t>(e->rank) * rc, 2 * rc, ncclFloat64, ncclSum,
+                              e->comm, e->comm_stream));
+  if (rem)
+    HS_NCCL(ncclReduce(base + P * rc, base + P * rc, 2 * rem, ncclFloat64, ncclSum, e->nranks - 1, e->comm,
+                       e->comm_stream));
+}
+
+// Same-device group: every owner sums its slice (or the root the whole segment) from all
+// members' buffers, in rank order, after all members finished the segment (`ready`).
+static void local_segment(const std::vector<hsdla_b200_engine*>& g, bool s_matrix, Range sg, int mode, int root,
+                          cudaEvent_t (*ready)(hsdla_b200_engine*, int), int q) {
+  const int P = static_cast<int>(g.size());
+  for (int r = 0; r < P; ++r) {
+    hsdla_b200_engine* o = g[r];
+    Range part;
+    if (mode == kReduceRoot) {
+      if (r != root) continue;
+      part = sg;
+    } else {
+      part = scatter_slice(sg.first, sg.second, r, P);
+    }
+    for (hsdla_b200_engine* m : g) HS_CUDA(cudaStreamWaitEvent(o->comm_stream, ready(m, q), 0));
+    const uint64_t n = part.second - part.first;
+    if (!n) continue;
+    std::vector<const double2*> in(P);
+    for (int i = 0; i < P; ++i) in[i] = (s_matrix ? g[i]->Sp : g[i]->Hp) + (part.first - g[i]->pk0);
+    launch_sum_partials((s_matrix ? o->Sp : o->Hp) + (part.first - o->pk0), in.data(), P, n, o->comm_stream);
+  }
+}
+
+static cudaEvent_t ev_s_ready(hsdla_b200_engine* e, int) { return e->ev_s_done; }
+static cudaEvent_t ev_h_ready(hsdla_b200_engine* e, int q) { return q < 0 ? e->ev_end : e->ev_h_band[q]; }
+
+void group_reduce(const std::vector<hsdla_b200_engine*>& g, int mode, int root) {
+  if (g.empty()) return;
+  const int P = static_cast<int>(g.size());
+  if (mode != kReduceRoot && mode != kReduceScatter) throw Fail{HSDLA_B200_CONFIG_ERROR, "unknown reduce mode"};
+  const bool nccl = g[0]->comm != nullptr;
+  const int nr = nccl ? g[0]->nranks : P;
+  if (root < 0 || root >= nr) throw Fail{HSDLA_B200_CONFIG_ERROR, "reduce root out of range"};
+  for (hsdla_b200_engine* e : g) {
+    if ((e->comm != nullptr) != nccl) throw Fail{HSDLA_B200_CONFIG_ERROR, "mixed NCCL / local reduce group"};
+    if (!e->built) throw Fail{HSDLA_B200_CONFIG_ERROR, "reduce before build"};
+    if (e->ng != g[0]->ng || e->c0 != g[0]->c0 || e->c1 != g[0]->c1 || e->banded != g[0]->banded)
+      throw Fail{HSDLA_B200_CONFIG_ERROR, "reduce group members differ in shape / window / banding"};
+    if (!nccl && e->device != g[0]->device)
+      throw Fail{HSDLA_B200_CONFIG_ERROR, "engines without a communicator must share one device"};
+  }
+  if (!nccl) {
+    if (P <= 1) return;  // a single engine holds the sum already
+    for (int r = 0; r < P; ++r) {
+      g[r]->nranks = P;
+      g[r]->rank = r;
+    }
+  }
+  const std::vector<Range> segs = segments(g[0]);
+  const bool banded = g[0]->banded;
+  auto run = [&](bool s_matrix) {
+    for (size_t q = 0; q < segs.size(); ++q) {
+      const int qi = banded ? static_cast<int>(q) : -1;
+      if (nccl) {
+        HS_NCCL(ncclGroupStart());
+        for (hsdla_b200_engine* e : g) {
+          HS_CUDA(cudaSetDevice(e->device));
+          HS_CUDA(cudaStreamWaitEvent(e->comm_stream, s_matrix ? e->ev_s_done : ev_h_ready(e, qi), 0));
+          nccl_segment(e, s_matrix ? e->Sp : e->Hp, segs[q], mode, root);
+        }
+        HS_NCCL(ncclGroupEnd());
+      } else {
+        HS_CUDA(cudaSetDevice(g[0]->device));
+        local_segment(g, s_matrix, segs[q], mode, root, s_matrix ? ev_s_ready : ev_h_ready, qi);
+      }
+      if (!s_matrix && banded)
+        for (hsdla_b200_engine* e : g) {
+          HS_CUDA(cudaSetDevice(e->device));
+          HS_CUDA(cudaEventRecord(e->ev_h_red[q], e->comm_stream));
+        }
+    }
+    if (s_matrix)
+      for (hsdla_b200_engine* e : g) {
+        HS_CUDA(cudaSetDevice(e->device));
+        HS_CUDA(cudaEventRecord(e->ev_s_red, e->comm_stream));
+      }
+  };
+  // S first (its partials are final after phase s: this overlaps the H phases), then H
+  run(true);
+  run(false);
+  for (hsdla_b200_engine* e : g) {
+    HS_CUDA(cudaSetDevice(e->device));
+    HS_CUDA(cudaEventRecord(e->ev_reduce_end, e->comm_stream));
+    HS_CUDA(cudaStreamWaitEvent(e->stream, e->ev_reduce_end, 0));
+    e->red_mode = mode;
+    e->red_root = root;
+    e->reduced = true;
+  }
+  // a local group's owners read the other members' buffers on their own comm streams: no
+  // member may start its next build (overwrite H, S) before every owner is done
+  if (!nccl)
+    for (hsdla_b200_engine* m : g)
+      for (hsdla_b200_engine* o : g)
+        if (m != o) HS_CUDA(cudaStreamWaitEvent(m->stream, o->ev_reduce_end, 0));
+}
+
+// Multi-process use: this process's engine is one rank of its window's communicator.
+void engine_reduce(hsdla_b200_engine* e, int root) {
+  if (!e->comm) return;
+  group_reduce({e}, e->red_mode, root);
+}
+
+uint64_t executed_flops(uint64_t na, uint64_t nl, uint64_t ng, int arith, int algo) {
+  // Real flops the GPU executes for a build.  The refined, fused and original algorithms
+  // run lower-triangular contractions of 20 K N_G^2 + 24 N_A N_L^2 N_G complex-MAC flops at
+  // 8 per MAC (the original's trmm on the zero upper half of L and its full gemm fold are
+  // executed as the lower-only h_aa contraction); the merged one 16 K N_G^2 + 32 N_A N_L^2
+  // N_G (two H segments, four per-atom products).  Plus 2 K N_G for diag_scale; the 3M
+  // arithmetic executes 6 real flops per complex MAC.
+  const uint64_t K = na * nl;
+  const uint64_t cmac8 = algo == HSDLA_B200_ALGO_REFINED_MERGED ? 16 * K * ng * ng + 32 * na * nl * nl * ng
+                                                                : 20 * K * ng * ng + 24 * na * nl * nl * ng;
+  return (arith == HSDLA_B200_ARITH_3M ? cmac8 / 8 * 6 : cmac8) + 2 * K * ng;
+}
+
+void flop_model(int variant, uint64_t na, uint64_t nl, uint64_t ng, uint64_t n_hpd, uint64_t* l) {
+  // pipeline.cpp:336-364
+  const uint64_t n_fail = na - std::min(n_hpd, na);
+  std::memset(l, 0, 9 * sizeof(uint64_t));
+  l[0] = 8 * na * nl * nl * ng;
+  l[1] = 8 * na * nl * nl * ng;
+  l[2] = 8 * na * nl * ng * ng;
+  l[3] = 8 * na * nl * ng * ng;
+  l[4] = 2 * na * nl * ng;
+  if (variant == 0) {
+    l[6] = na * (4 * nl * nl * nl / 3);
+    if (n_hpd > 0) {
+      l[7] = 4 * n_hpd * nl * nl * ng;
+      l[3] += 4 * n_hpd * nl * ng * ng;
+    }
+    if (n_fail > 0) {
+      l[1] += 8 * n_fail * nl * nl * ng;
+      l[0] += 8 * n_fail * nl * ng * ng;
+    }
+  } else {
+    l[1] += 8 * na * nl * nl * ng;
+    l[5] = 4 * na * nl * ng * ng;
+  }
+  for (int i = 0; i < 8; ++i) l[8] += l[i];
+}
+
+void engine_sync(hsdla_b200_engine* e, hsdla_b200_stats* st) {
+  HS_CUDA(cudaSetDevice(e->device));
+  HS_CUDA(cudaStreamSynchronize(e->stream));
+  HS_CUDA(cudaStreamSynchronize(e->copy_stream));
+  HS_CUDA(cudaStreamSynchronize(e->comm_stream));
+  for (auto& t : e->ring) harvest(e, t);
+  if (!st) return;
+  std::memset(st, 0, sizeof(*st));
+  st->peak_device_bytes = e->device_bytes;
+  // the temporaries the algorithm needs: X1 (refined, cf. pipeline.cpp:291) or X1 + X2
+  st->peak_temp_bytes = (e->built && e->last_algo != HSDLA_B200_ALGO_REFINED ? 2 : 1) * e->temp_bytes;
+  st->n_gpus = e->nranks;
+  st->col_groups = 1;
+  st->reduce_mode = e->red_mode;
+  if (!e->built) return;  // nothing timed yet
+  if (e->last_algo == HSDLA_B200_ALGO_ORIGINAL) {
+    std::vector<int32_t> info(e->na);
+    HS_CUDA(cudaMemcpy(info.data(), e->info, e->na * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    e->n_hpd_last = static_cast<uint64_t>(std::count_if(info.begin(), info.end(), [](int32_t v) { return v < 0; }));
+  } else {
+    e->n_hpd_last = e->na;
+  }
+  st->n_hpd = e->n_hpd_last;
+  st->executed_flops = executed_flops(e->na, e->nl, e->ng, e->arith, e->last_algo);
+  for (const OpTime& op : e->ops) st->phase_seconds[op.phase] += ev_ms(op.b, op.e) * 1e-3;
+  const cudaEvent_t last = e->reduced ? e->ev_reduce_end : e->ev_end;
+  st->device_seconds = ev_ms(e->ev_begin, last) * 1e-3;
+  st->reduce_seconds = e->reduced ? ev_ms(e->ev_end, e->ev_reduce_end) * 1e-3 : 0.0;
+  if (e->uploaded_streamed) st->h2d_seconds = ev_ms(e->ev_up0, e->ev_up1) * 1e-3;
+  st->kernel_launches = e->launches;
+}
+
+static void ensure_stage(hsdla_b200_engine* e) {
+  if (!e->host_stage)
+    HS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&e->host_stage), 2 * e->cap_pk * sizeof(double2)));
+}
+
+// Enqueue the packed-triangle D2H of the ranges this engine owns on the copy stream: S
+// (after phase s / its reduce), then H in kD2hPieces column pieces (after band q / its
+// reduce when banded, else after the build / its reduce), each piece's event recorded so
+// the host unpacks piece q while q+1 is on the wire.  Every event is recorded every time
+// (the next k-point's build waits on the last one).
+void enqueue_download(hsdla_b200_engine* e) {
+  HS_CUDA(cudaSetDevice(e->device));
+  ensure_stage(e);
+  Download& d = e->dl;
+  d.ng = e->ng;
+  d.pk0 = e->pk0;
+  d.s.clear();
+  d.h.clear();
+  const std::vector<Range> own = engine_owned(e);
+  cudaStream_t cs = e->copy_stream;
+  HS_CUDA(cudaStreamWaitEvent(cs, e->reduced ? e->ev_s_red : e->ev_s_done, 0));
+  for (const Range& o : own) {
+    HS_CUDA(cudaMemcpyAsync(e->host_stage + e->cap_pk + (o.first - e->pk0), e->Sp + (o.first - e->pk0),
+                            (o.second - o.first) * sizeof(double2), cudaMemcpyDeviceToHost, cs));
+    d.s.push_back({o.first, o.second, e->ev_dl_s});
+  }
+  HS_CUDA(cudaEventRecord(e->ev_dl_s, cs));
+  if (!e->banded) HS_CUDA(cudaStreamWaitEvent(cs, e->reduced ? e->ev_reduce_end : e->ev_end, 0));
+  for (int q = 0; q < hsdla_b200_engine::kD2hPieces; ++q) {
+    // banded: piece q is final once band q is computed (one engine) or reduced (group)
+    if (e->banded) HS_CUDA(cudaStreamWaitEvent(cs, e->reduced ? e->ev_h_red[q] : e->ev_h_band[q], 0));
+    const uint64_t p0 = packed_col(e->ng, piece_col(e, q)), p1 = packed_col(e->ng, piece_col(e, q + 1));
+    for (const Range& o : own) {
+      const uint64_t b0 = std::max(p0, o.first), b1 = std::min(p1, o.second);
+      if (b1 <= b0) continue;
+      HS_CUDA(cudaMemcpyAsync(e->host_stage + (b0 - e->pk0), e->Hp + (b0 - e->pk0), (b1 - b0) * sizeof(double2),
+                              cudaMemcpyDeviceToHost, cs));
+      d.h.push_back({b0, b1, e->ev_dl_h[q]});
+    }
+    HS_CUDA(cudaEventRecord(e->ev_dl_h[q], cs));
+  }
+  d.pending = true;
+}
+
+// Unpack S as soon as its bytes land (H may still be computing), then H piece by piece.
+void finish_download(hsdla_b200_engine* e, double* H, double* S, std::chrono::steady_clock::time_point t0) {
+  Download& d = e->dl;
+  if (!d.pending) return;
+  auto ms = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); };
+  std::string tr;
+  auto mark = [&](const char* what) {
+    if (trace_on()) tr += std::string(" ") + what + "=" + std::to_string(ms()).substr(0, 6);
+  };
+  d.pending = false;
+  HS_CUDA(cudaEventSynchronize(e->ev_dl_s));
+  mark("s_landed");
+  if (S)
+    for (const DlPiece& p : d.s)
+      unpack_range(e->host_stage + e->cap_pk + (p.b0 - d.pk0), reinterpret_cast<double2*>(S), d.ng, p.b0, p.b1);
+  mark("s_unpacked");
+  cudaEvent_t waited = nullptr;
+  for (const DlPiece& p : d.h) {
+    if (p.ready != waited) {
+      HS_CUDA(cudaEventSynchronize(p.ready));
+      waited = p.ready;
+      mark("h_landed");
+    }
+    if (H) unpack_range(e->host_stage + (p.b0 - d.pk0), reinterpret_cast<double2*>(H), d.ng, p.b0, p.b1);
+  }
+  HS_CUDA(cudaEventSynchronize(e->ev_dl_h[hsdla_b200_engine::kD2hPieces - 1]));
+  mark("h_unpacked");
+  if (trace_on()) std::fprintf(stderr, "[hsdla_b200 trace] download (ms since call start):%s\n", tr.c_str());
+}
+
+void engine_download(hsdla_b200_engine* e, double* H, double* S) {
+  HS_CUDA(cudaSetDevice(e->device));
+  if (!e->built) throw Fail{HSDLA_B200_CONFIG_ERROR, "download before build"};
+  enqueue_download(e);
+  finish_download(e, H, S);
+}
+
+}  // namespace hsdla_b200

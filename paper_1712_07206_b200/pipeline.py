@@ -59,6 +59,12 @@ class PipelineConfig:
     # complex arithmetic of the contractions: "3m" (Gauss, 6 executed flops per complex MAC,
     # the default) | "4m" (four real multiplications, plain FP64 rounding per product)
     arith: str = "3m"
+    # multi-GPU: "scatter" (default: every GPU receives and downloads its own slices of H, S) |
+    # "root" (ncclReduce onto the first GPU, which downloads everything)
+    reduce: str = "scatter"
+    # 2-D tiling of H, S into column windows (0: automatic, by the per-GPU memory budget)
+    col_groups: int = 0
+    mem_budget_gb: float = 0.0
 
 
 @dataclass
@@ -117,8 +123,10 @@ def _options(cfg, algo):
         raise ConfigError("n_gpus must be >= 1")
     if cfg.arith not in _lib.ARITH:
         raise ConfigError(f"unknown arith: {cfg.arith} (3m | 4m)")
-    flags = _lib.FLAG_ARITH_4M if cfg.arith == "4m" else 0
-    return _lib.Options(int(cfg.n_gpus), ids, ALGOS[algo], flags), ids
+    if cfg.reduce not in _lib.REDUCE:
+        raise ConfigError(f"unknown reduce: {cfg.reduce} (scatter | root)")
+    flags = (_lib.FLAG_ARITH_4M if cfg.arith == "4m" else 0) | (_lib.FLAG_REDUCE_ROOT if cfg.reduce == "root" else 0)
+    return _lib.Options(int(cfg.n_gpus), ids, ALGOS[algo], flags, int(cfg.col_groups), float(cfg.mem_budget_gb)), ids
 
 
 def _phase_names(algo):
@@ -137,7 +145,8 @@ def stats_dict(st, algo="merged"):
         "d2h_seconds": st.d2h_seconds, "total_seconds": st.total_seconds,
         "ledger_total": int(st.ledger[8]), "executed_flops": int(st.executed_flops),
         "peak_device_bytes": int(st.peak_device_bytes), "peak_temp_bytes": int(st.peak_temp_bytes),
-        "n_gpus": st.n_gpus, "kernel_launches": st.kernel_launches,
+        "n_gpus": st.n_gpus, "kernel_launches": st.kernel_launches, "col_groups": st.col_groups,
+        "reduce": {v: k for k, v in _lib.REDUCE.items()}.get(st.reduce_mode, "root"),
     }
 
 
@@ -175,9 +184,9 @@ def build_hs_refined(p, cfg: Optional[PipelineConfig] = None, H=None, S=None) ->
 
 def build_hs_kpoints(p, As, Bs, cfg: Optional[PipelineConfig] = None, Hs=None, Ss=None):
     """n k-points of one cell in one call (hsdla_b200_build_hs_kpoints): p's operators and U are
-    shared, As[k] / Bs[k] are each k-point's coefficients (p.A / p.B layout).  Uploads of k+1 and
-    downloads of k-1 overlap the build of k.  Returns (list of HSResult-like (H, S) pairs,
-    stats of the last k-point with total_seconds for the batch)."""
+    shared, As[k] / Bs[k] are each k-point's coefficients ((n_atoms n_l) x N_G(k), p.A's layout;
+    N_G(k) may differ per k-point).  Uploads of k+1 and downloads of k-1 overlap the build of k.
+    Returns (list of (H, S) pairs, stats of the last k-point with total_seconds for the batch)."""
     cfg = cfg or PipelineConfig()
     parse_strategy(cfg.strategy)
     algo = "original" if parse_variant(cfg.variant) == "original" else cfg.algo
@@ -186,22 +195,28 @@ def build_hs_kpoints(p, As, Bs, cfg: Optional[PipelineConfig] = None, Hs=None, S
     nk = len(As)
     if len(Bs) != nk:
         raise DimensionError("As and Bs differ in length")
-    n = p.n_g
-    shape = (p.n_atoms * p.n_l, n)
-    for M in list(As) + list(Bs):
-        if M.shape != shape or M.dtype != np.complex128 or not M.flags.f_contiguous:
-            raise DimensionError(f"A/B must be {shape} complex128 Fortran arrays")
-    Hs = Hs or [np.zeros((n, n), np.complex128, order="F") for _ in range(nk)]
-    Ss = Ss or [np.zeros((n, n), np.complex128, order="F") for _ in range(nk)]
-    for M in list(Hs) + list(Ss):
-        if M.shape != (n, n) or M.dtype != np.complex128 or not M.flags.f_contiguous:
-            raise DimensionError(f"H/S must be ({n}, {n}) complex128 Fortran arrays")
+    K = p.n_atoms * p.n_l
+    ngk = []
+    for A_, B_ in zip(As, Bs):
+        for M in (A_, B_):
+            if M.ndim != 2 or M.shape[0] != K or M.dtype != np.complex128 or not M.flags.f_contiguous:
+                raise DimensionError(f"A/B must be ({K}, N_G(k)) complex128 Fortran arrays")
+        if A_.shape != B_.shape:
+            raise DimensionError("A[k] and B[k] differ in shape")
+        ngk.append(A_.shape[1])
+    Hs = Hs or [np.zeros((n, n), np.complex128, order="F") for n in ngk]
+    Ss = Ss or [np.zeros((n, n), np.complex128, order="F") for n in ngk]
+    for n, H_, S_ in zip(ngk, Hs, Ss):
+        for M in (H_, S_):
+            if M.shape != (n, n) or M.dtype != np.complex128 or not M.flags.f_contiguous:
+                raise DimensionError(f"H/S must be ({n}, {n}) complex128 Fortran arrays")
     prob = p.c_struct()
     opts, _keep = _options(cfg, algo)
     ptrs = lambda L: (C.c_void_p * nk)(*[M.ctypes.data for M in L])  # noqa: E731
+    ng_arr = (C.c_uint64 * max(nk, 1))(*ngk)
     st = _lib.Stats()
-    check(_lib.lib().hsdla_b200_build_hs_kpoints(C.byref(prob), C.c_uint64(nk), ptrs(As), ptrs(Bs), C.byref(opts),
-                                                 ptrs(Hs), ptrs(Ss), C.byref(st)), "build_hs_kpoints")
+    check(_lib.lib().hsdla_b200_build_hs_kpoints(C.byref(prob), C.c_uint64(nk), ng_arr, ptrs(As), ptrs(Bs),
+                                                 C.byref(opts), ptrs(Hs), ptrs(Ss), C.byref(st)), "build_hs_kpoints")
     return list(zip(Hs, Ss)), stats_dict(st, algo)
 
 
@@ -309,15 +324,37 @@ def rel_frobenius_error_lower(x, y):
 
 
 class Engine:
-    """Device-resident engine for one atom shard on one GPU (C-ABI hsdla_b200_engine_*)."""
+    """Device-resident engine for one shard on one GPU (C-ABI hsdla_b200_engine_*): n_atoms_local
+    atoms (an atom shard) and the column window [col_begin, col_end) of H and S (col_end 0: n_g;
+    2-D tiling: engines of different windows compute disjoint tile-column bands).  n_g_capacity
+    sizes a whole-window engine for reshape() to larger N_G without reallocation."""
 
-    def __init__(self, device, n_atoms_local, n_l, n_g):
+    def __init__(self, device, n_atoms_local, n_l, n_g, col_begin=0, col_end=0, n_g_capacity=0):
         h = C.c_void_p()
-        check(_lib.lib().hsdla_b200_engine_create(C.c_int(device), C.c_uint64(n_atoms_local), C.c_uint64(n_l),
-                                                  C.c_uint64(n_g), C.byref(h)), "engine_create")
+        sh = _lib.Shard(n_atoms_local, n_l, n_g, col_begin, col_end, n_g_capacity)
+        check(_lib.lib().hsdla_b200_engine_create_shard(C.c_int(device), C.byref(sh), C.byref(h)), "engine_create")
         self.h = h
         self.n_g = n_g
         self.device = device
+
+    def reshape(self, n_g):
+        """Re-target a whole-window engine at N_G = n_g within its capacity (inputs must be re-uploaded)."""
+        check(_lib.lib().hsdla_b200_engine_reshape(self.h, C.c_uint64(n_g)), "engine_reshape")
+        self.n_g = n_g
+
+    def set_reduce_mode(self, mode):
+        """"root" (ncclReduce onto the reduce root; the default) or "scatter" (every rank owns slices)."""
+        if mode not in _lib.REDUCE:
+            raise ConfigError(f"unknown reduce mode: {mode} (root | scatter)")
+        check(_lib.lib().hsdla_b200_engine_set_reduce_mode(self.h, C.c_int(_lib.REDUCE[mode])), "set_reduce_mode")
+
+    def owned(self):
+        """Global packed-lower index ranges [(begin, end), ...] this engine holds final values for."""
+        n = C.c_uint64()
+        check(_lib.lib().hsdla_b200_engine_owned(self.h, None, C.c_uint64(0), C.byref(n)), "engine_owned")
+        buf = (C.c_uint64 * max(1, 2 * n.value))()
+        check(_lib.lib().hsdla_b200_engine_owned(self.h, buf, n, C.byref(n)), "engine_owned")
+        return [(int(buf[2 * i]), int(buf[2 * i + 1])) for i in range(n.value)]
 
     def close(self):
         if self.h:
@@ -408,6 +445,17 @@ class Engine:
               "kernel_times")
         return {"s_ms": ms_s.value, "h_ms": ms_h.value, "s_flops": fs.value, "h_flops": fh.value,
                 "builds": nb.value}
+
+
+def group_reduce(engines, mode="scatter", root=0):
+    """hsdla_b200_group_reduce: sum the partial H, S of engines of this process that share a
+    column window (disjoint atom shards; engines[r] is rank r): grouped NCCL calls when each has
+    a communicator, else (one shared device) a deterministic sum kernel."""
+    if mode not in _lib.REDUCE:
+        raise ConfigError(f"unknown reduce mode: {mode} (root | scatter)")
+    arr = (C.c_void_p * len(engines))(*[e.h.value for e in engines])
+    check(_lib.lib().hsdla_b200_group_reduce(arr, C.c_int(len(engines)), C.c_int(_lib.REDUCE[mode]), C.c_int(root)),
+          "group_reduce")
 
 
 def set_default_arith(arith):

@@ -89,6 +89,28 @@ def generate_problem(n_atoms, n_l, n_g, seed=1, n_not_hpd=0):
     return p
 
 
+def generate_problem_shard(n_atoms, n_l, n_g, atom_begin, atom_end, seed=1, n_not_hpd=0):
+    """Atoms [atom_begin, atom_end) of generate_problem(n_atoms, n_l, n_g, seed, n_not_hpd), bit-identical
+    to the same rows / blocks of the full instance, generated without the other atoms' storage (each
+    rank of a multi-GPU run builds only its own shard).  Returns a ProblemInstance of atom_end -
+    atom_begin atoms; its `atom_begin` / `n_atoms_total` attributes record where it sits."""
+    if n_atoms < 1 or n_l < 1 or n_g < 1:
+        raise DimensionError("generate_problem_shard: all dims must be >= 1")
+    if n_not_hpd > n_atoms or not 0 <= atom_begin < atom_end <= n_atoms:
+        raise DimensionError("generate_problem_shard: need n_not_hpd <= n_atoms, 0 <= atom_begin < atom_end <= n_atoms")
+    na = atom_end - atom_begin
+    p = empty_problem(na, n_l, n_g)
+    hpd = np.zeros(na, np.uint8)
+    ptr = lambda a: a.ctypes.data_as(C.c_void_p)
+    check(_lib.lib().hsdla_b200_generate_problem_shard(
+        C.c_uint64(n_atoms), C.c_uint64(n_l), C.c_uint64(n_g), C.c_uint64(seed), C.c_uint64(n_not_hpd),
+        C.c_uint64(atom_begin), C.c_uint64(atom_end), ptr(p.A), ptr(p.B), ptr(p.T_AA), ptr(p.T_AB), ptr(p.T_BB),
+        ptr(p.U), ptr(hpd)), "generate_problem_shard")
+    p.hpd_flags = hpd.astype(np.bool_)
+    p.atom_begin, p.n_atoms_total = atom_begin, n_atoms
+    return p
+
+
 # ---- presets (problem.cpp:247-270) -----------------------------------------
 @dataclass
 class Preset:

@@ -63,3 +63,18 @@ def test_python_constants_match_the_header():
                      "original": defs["HSDLA_B200_ALGO_ORIGINAL"], "fused": defs["HSDLA_B200_ALGO_REFINED_FUSED"]}
     assert _lib.ARITH == {"3m": defs["HSDLA_B200_ARITH_3M"], "4m": defs["HSDLA_B200_ARITH_4M"]}
     assert _lib.FLAG_ARITH_4M == defs["HSDLA_B200_FLAG_ARITH_4M"]
+    assert _lib.FLAG_REDUCE_ROOT == defs["HSDLA_B200_FLAG_REDUCE_ROOT"]
+    assert _lib.REDUCE == {"root": defs["HSDLA_B200_REDUCE_ROOT"], "scatter": defs["HSDLA_B200_REDUCE_SCATTER"]}
+
+
+def test_ctypes_structs_match_the_header_layout():
+    """Options / Shard field order and sizes as declared in include/hsdla_b200.h (the ctypes
+    mirror must not drift from the C structs the library reads)."""
+    import ctypes as C
+    assert [f for f, _ in _lib.Options._fields_] == ["n_gpus", "device_ids", "algo", "flags", "col_groups",
+                                                      "mem_budget_gb"]
+    assert C.sizeof(_lib.Options) == 40  # int, pad, ptr, 3 x int, pad, double
+    assert [f for f, _ in _lib.Shard._fields_] == ["n_atoms_local", "n_l", "n_g", "col_begin", "col_end",
+                                                    "n_g_capacity"]
+    assert C.sizeof(_lib.Shard) == 48
+

@@ -45,6 +45,9 @@ def test_b200_arm_line():
     rf = d["roofline"]
     assert rf["bound"] == "tensor" and 0 < rf["frac"] <= 1.05 and rf["unit"] == "TFLOP/s"
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["value"] > 0
+    assert d["e2e"]["host_buffers"] == "pageable" and d["e2e_pinned"]["host_buffers"] == "page-locked"
+    # every "fraction of peak" is an executed-flop efficiency (<= 1); the ledger rate is `value`
+    assert 0 < d["fp64_frac_of_peak"] <= 1.0 and "ledger_frac_of_peak" not in d
     assert d["gpu_launches"] > 0 and "sm_mhz" in d["clocks"]
     assert d["setup_roofline"]["bound"] == "hbm" and d["e2e_file"]["value"] > 0
 
@@ -90,3 +93,4 @@ def test_b200_arm_under_torchrun_with_nccl_plumbing():
     assert len(lines) == 1, r.stdout
     d = json.loads(lines[0])
     assert d["n_gpus"] == 1 and d["value"] > 1.0 and d["e2e"]["value"] > 0
+    assert "reduce-scatter" in d["config"]["parallelism"]

@@ -19,6 +19,23 @@ def test_generate_problem_bitwise_vs_reference(path):
     assert p.A.flags.f_contiguous
 
 
+@pytest.mark.parametrize("dims,lo,hi", [((7, 6, 48, 3, 2), 0, 7), ((7, 6, 48, 3, 2), 2, 5), ((7, 6, 48, 3, 2), 6, 7),
+                                         ((5, 9, 97, 11, 5), 1, 3), ((16, 49, 200, 1, 0), 8, 16)])
+def test_generate_problem_shard_is_the_full_instance_rows(dims, lo, hi):
+    """Each rank of a multi-GPU run generates only its atoms: bit-identical to the same rows /
+    blocks of the full generate_problem (the generator stream of other atoms is skipped)."""
+    na, nl, ng, seed, nnh = dims
+    full = hb.generate_problem(*dims)
+    sh = hb.generate_problem_shard(na, nl, ng, lo, hi, seed, nnh)
+    assert sh.n_atoms == hi - lo and sh.atom_begin == lo and sh.n_atoms_total == na
+    assert np.array_equal(sh.A, full.A[lo * nl:hi * nl]) and np.array_equal(sh.B, full.B[lo * nl:hi * nl])
+    for k in ("T_AA", "T_AB", "T_BB", "U"):
+        assert np.array_equal(getattr(sh, k), getattr(full, k)[..., lo:hi]), k
+    assert np.array_equal(sh.hpd_flags, full.hpd_flags[lo:hi])
+    with pytest.raises(hb.DimensionError):
+        hb.generate_problem_shard(na, nl, ng, hi, lo, seed, nnh)
+
+
 def test_generate_problem_dimension_errors():
     with pytest.raises(hb.DimensionError):
         hb.generate_problem(0, 1, 1)
