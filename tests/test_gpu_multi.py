@@ -243,8 +243,9 @@ def test_kpoints_with_varying_basis_size(algo):
     cfg = hb.PipelineConfig(variant="original") if algo == "original" else hb.PipelineConfig()
     got, st = hb.build_hs_kpoints(base, [q.A for q in kps], [q.B for q in kps], cfg)
     for k, (H, S) in enumerate(got):
-        pk = hb.generate_problem(12, 49, ngk[k], 3, 2)
-        pk.A, pk.B = kps[k].A, kps[k].B
+        # the cell's operators and U with k-point k's coefficients
+        pk = hb.ProblemInstance(12, 49, ngk[k], kps[k].A, kps[k].B, base.T_AA, base.T_AB, base.T_BB, base.U,
+                                base.hpd_flags)
         want = hb.build_hs(pk, cfg)
         assert H.shape == (ngk[k], ngk[k])
         assert rel(H, want.H) <= 1e-13 and rel(S, want.S) <= 1e-13, k
