@@ -113,11 +113,10 @@ def test_config2_full_vs_unmodified_reference():
         assert r.ledger == hb.flop_model(p)
 
 
-@pytest.mark.parametrize("dims", [(64, 81, 3000), (108, 121, 6000), (512, 121, 13000)],
-                         ids=["config2", "config3", "config4"])
+@pytest.mark.parametrize("dims", [(64, 81, 3000)], ids=["config2"])
 def test_sampled_parity_at_config_sizes(dims, restatement):
-    """Configs 2/3/4 at full size (config 4: 26 GB of A, B through the pageable host-buffer
-    path): principal-submatrix sampling (SURVEY §7 hard part 3):
+    """Config 2 (configs 3-5: tests/test_gpu_large.py against the unmodified reference):
+    principal-submatrix sampling (SURVEY §7 hard part 3):
     H[J,J], S[J,J] depend only on columns J of A, B; the oracle runs the J-sliced problem."""
     na, nl, ng = dims
     p = hb.generate_problem(na, nl, ng, 1, 0)
