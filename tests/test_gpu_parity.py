@@ -523,3 +523,24 @@ def test_kpoint_batch_matches_per_call_builds(pinned):
             for M in As + Bs:
                 hb.host_unregister(M)
         hb.release_cache()
+
+
+def test_kpoint_batch_banded_final_h_storage_reuse():
+    """N_G = 2240 (35 tile columns, 630 lower tiles >= 4 x 148): every k-point's final H runs
+    band by band, and build k reuses the H, S storage while the banded D2H of k-1 is still in
+    flight (build k waits on k-1's last band download and on its S download).  Every k-point
+    equals its own per-call build."""
+    ng = 2240
+    base = hb.generate_problem(6, 16, ng, 3, 1)
+    kps = [hb.generate_problem(6, 16, ng, 20 + k, 1) for k in range(4)]
+    As = [q.A for q in kps]
+    Bs = [q.B for q in kps]
+    try:
+        got, _ = hb.build_hs_kpoints(base, As, Bs, hb.PipelineConfig())
+        for k, (H, S) in enumerate(got):
+            pk = hb.generate_problem(6, 16, ng, 3, 1)
+            pk.A, pk.B = As[k], Bs[k]
+            want = hb.build_hs_refined(pk)
+            assert rel(H, want.H) <= 1e-13 and rel(S, want.S) <= 1e-13, k
+    finally:
+        hb.release_cache()
