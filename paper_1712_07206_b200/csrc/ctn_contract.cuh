@@ -143,13 +143,15 @@ __device__ __forceinline__ uint64_t packed_index(uint64_t n, uint64_t i, uint64_
 
 // KSUB: 128-byte k-slabs (8 complex) per pipeline stage; one full/empty mbarrier
 // handshake per stage, so KSUB > 1 amortises the synchronisation over more DMMAs.
-template <int MODE, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, int KSUB = 1>
+// PW: producer warps.  4: the producer is a warpgroup of its own (one TMA lane, three idle
+// warps) and setmaxnreg moves registers from it to the consumers at run time; ptxas still
+// compiles the consumers against the 384-thread launch bound (168 registers).  1: a single
+// producer warp, no setmaxnreg; the 288-thread launch bound lets ptxas give every thread
+// up to 224 registers, room for larger warp tiles.
+template <int MODE, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, int KSUB = 1, int PW = 4>
 struct CtnCfg {
   static constexpr int kConsumerWarps = WARPS_M * WARPS_N;
-  // warp specialisation with register rebalancing: the consumer warps form whole
-  // warpgroups and the producer gets a warpgroup of its own (one TMA lane, three idle
-  // warps), so setmaxnreg can move registers from the producer to the consumers
-  static constexpr int kProducerWarps = 4;
+  static constexpr int kProducerWarps = PW;
   static constexpr int kThreads = (kConsumerWarps + kProducerWarps) * 32;
   static constexpr int kProducerRegs = 40;
   static constexpr int kConsumerRegs =
@@ -233,10 +235,11 @@ __device__ __forceinline__ void consumer_bar(int nthreads) {
 //   flops per complex MAC): per k, t1 += a_r b_r, t2 += a_i b_i, t3 += (a_r - a_i)(b_r + b_i),
 //   then Re(conj(a) b) = t1 + t2 and Im = t3 - t1 + t2.  Still all-FP64; the imaginary
 //   part's rounding error bound grows by a small constant factor.
-template <int MODE, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, int MINB = 1, int G3M = 0, int KSUB = 1>
-__global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES, KSUB>::kThreads, MINB)
+template <int MODE, int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, int MINB = 1, int G3M = 0, int KSUB = 1,
+          int PW = 4>
+__global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES, KSUB, PW>::kThreads, MINB)
     ctn_contract_kernel(const __grid_constant__ CtnParams P) {
-  using Cfg = CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES, KSUB>;
+  using Cfg = CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES, KSUB, PW>;
   constexpr int MB = Cfg::kMB, NB = Cfg::kNB;
   constexpr int NCT = Cfg::kConsumerWarps * 32;  // consumer threads
   constexpr int NS = G3M ? 3 : 2;                // accumulator sets per output element
@@ -285,10 +288,10 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES,
     }
   };
 
-  static_assert(Cfg::kConsumerWarps % 4 == 0, "consumer warps must form whole warpgroups");
+  static_assert(PW == 1 || Cfg::kConsumerWarps % 4 == 0, "consumer warps must form whole warpgroups");
   if (warp >= Cfg::kConsumerWarps) {
     // ===================== TMA producer (one lane) =========================
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(Cfg::kProducerRegs) : "memory");
+    if (PW == 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(Cfg::kProducerRegs) : "memory");
     if (warp == Cfg::kConsumerWarps && lane == 0) {
       for (int s = 0; s < P.nseg; ++s) {
         prefetch_map(&P.L[s]);
@@ -344,7 +347,7 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES,
   }
 
   // ======================= DMMA consumers =================================
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(Cfg::kConsumerRegs) : "memory");
+  if (PW == 4) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(Cfg::kConsumerRegs) : "memory");
   const int ctid = threadIdx.x;  // 0 .. NCT-1
   const int wm = warp % WARPS_M;
   const int wn = warp / WARPS_M;
@@ -437,6 +440,18 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES,
 #pragma unroll
         for (int nb = 0; nb < NB; ++nb) dmma(acc[mb][nb][0][1], acc[mb][nb][1][1], f.a[mb].y, -f.b[nb].x);
     };
+    // BATCH: k-slab c is the last of a segment whose length leaves <= 4 valid k in it
+    auto half_pad = [&](int c) {
+      bool h = false;
+      int end = 0;
+#pragma unroll
+      for (int s = 0; s < kMaxSeg; ++s)
+        if (s < P.nseg) {
+          end += P.kchunks[s];
+          h |= c == end - 1 && P.half_last[s];
+        }
+      return h;
+    };
     if (pc.k1 > pc.k0) {
       Frag f0, f1;
       {
@@ -449,6 +464,20 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES,
         const int n = min(KSUB, pc.k1 - c);
         const int slot = it % STAGES;
         const uint8_t* st = smem + slot * Cfg::kStageBytes;
+        if (MODE == kBatch && KSUB == 1 && half_pad(c)) {
+          // the segment's last slab holds <= 4 valid k: its second half (kk = 1) is TMA
+          // zero-fill, so only the first half's DMMAs issue (N_L = 81: 84 of 88 k per segment)
+          mma_frag(f0);
+          if (c + 1 < pc.k1) {
+            const int nslot = (it + 1) % STAGES;
+            mbar_wait(&full[nslot], ((it + 1) / STAGES) & 1);
+            load_frag(f0, smem + nslot * Cfg::kStageBytes, 0, 0);
+            sum_frag(f0);
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[slot]);
+          continue;
+        }
 #pragma unroll
         for (int u = 0; u < KSUB; ++u) {
           if (u < n) {
@@ -519,9 +548,11 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES,
         const int i = row0 + wm * Cfg::kWM + 8 * mb + pg;
         const int j = col0 + wn * Cfg::kWN + 8 * nb + (e ? 4 + q : q);
         if (MODE == kTri) return (i < P.n && j < P.n && i >= j) ? P.out + (packed_index(P.n, i, j) - P.pk0) : nullptr;
-        return (i < P.m_valid && j < P.n)
-                   ? P.out + (static_cast<uint64_t>(atom) * P.m_valid + i) + static_cast<uint64_t>(j) * P.ldo
-                   : nullptr;
+        if (i >= P.m_valid || j >= P.n) return nullptr;
+        const int mr = P.m_row ? P.m_row : P.m_valid;
+        const bool hi = i >= mr;  // stacked W: rows [m_row, m_valid) are W_B's, in out2
+        return (hi ? P.out2 : P.out) + (static_cast<uint64_t>(atom) * mr + (hi ? i - mr : i)) +
+               static_cast<uint64_t>(j) * P.ldo;
       };
       // Fold the accumulator sets into (Re, Im) first (3M: frees a third of them).  With
       // beta != 0 the old values are gathered MG row blocks at a time (MG x NB x 2 loads in

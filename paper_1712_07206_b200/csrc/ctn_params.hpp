@@ -19,9 +19,13 @@ struct alignas(64) CtnParams {
   int kchunks[kMaxSeg];    // 8-complex slabs per segment
   int l_row_z[kMaxSeg];    // 1: tile row coordinate in dim 2, atom in dim 1; 0: row in dim 1, atom in dim 2
   int r_row_z[kMaxSeg];
+  int half_last[kMaxSeg];  // BATCH: the segment's last 8-complex slab has <= 4 valid k (its
+                           // second half is zero-fill and is skipped); 0 elsewhere
   int nseg;
   int n;                   // TRI: order N_G.  BATCH: number of output columns (N_G)
-  int m_valid;             // BATCH: valid output rows per atom (N_L)
+  int m_valid;             // BATCH: valid output rows per atom (N_L; 2 N_L for the stacked W = M Y)
+  int m_row;               // BATCH, optional: rows per atom of `out` (0: m_valid).  Output rows
+                           // i >= m_row go to out2 (row i - m_row): the stacked W_A / W_B split
   int tiles;               // TRI: tiles per dimension
   int tiles_total;         // TRI: lower tiles t(t+1)/2
   int band;                // TRI: tile-row band of the grouped tile order (>= 1)
@@ -31,6 +35,7 @@ struct alignas(64) CtnParams {
                            // window's engine holds columns [g0, n)); TMA coordinate = global - g0
   uint64_t pk0;            // TRI: global packed index of out[0] (the window's first packed element)
   double2* out;            // TRI: packed lower.  BATCH: column-major stacked buffer
+  double2* out2;           // BATCH, optional: second stacked buffer (rows i >= m_row)
   double* sk_ws;           // TRI stream-K: per-CTA partial-accumulator slots
   uint32_t* sk_flags;      // TRI stream-K: per-CTA publish flags (== epoch when the slot is ready)
   uint32_t epoch;          // TRI stream-K: unique per launch

@@ -19,6 +19,9 @@ namespace hsdla_b200 {
 // 32x16; BATCH 32x128 tiles, 8 consumer warps of 32x16.
 constexpr int kTriBM = 64;
 constexpr int kBatBM = 32, kBatBN = 128;
+// merged build: ONE BATCH launch W = M Y per atom over the stacked 2 N_L rows
+// (W_A; W_B), 24-row tiles (162 rows -> 7 tiles = 168, against 2 x 96 with 32-row tiles)
+constexpr int kBatWBM = 24;
 // stream-K partial-accumulator slot per CTA: 64 x 64 outputs x 3 sets (3M) doubles
 constexpr uint64_t kSkSlot = uint64_t(kTriBM) * kTriBM * 3;
 
@@ -34,6 +37,7 @@ void set_kernel_attributes();
 // contraction with arith HSDLA_B200_ARITH_3M / _4M on `s`.
 void launch_tri_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStream_t s);
 void launch_bat_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStream_t s);
+void launch_batw_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStream_t s);
 
 inline int chunks_of(uint64_t kcomplex) { return static_cast<int>((kcomplex + kChunkC - 1) / kChunkC); }
 // Tile-row band of the TRI tile order (ctn_contract.cuh tri_tile); HSDLA_B200_TRI_BAND
@@ -47,8 +51,10 @@ void launch_diag_scale(const double2* B, const double* u, double2* X, uint64_t K
 // Counter-based synthetic fill ~ U(lo, hi) (timing sweeps; not the reference generator).
 void launch_fill_uniform(double* p, uint64_t n, uint64_t seed, double lo, double hi, unsigned grid, cudaStream_t s);
 // Operator expansion from the lower triangles (see elementwise.cu).
+// wl != nullptr (merged algorithm): only the stacked left operand of W = M Y is written,
+// per atom [Paa | Tab] (k over A rows) then [Pab | Pbb] (k over B rows), 4 N_L^2 complex.
 void launch_expand_hermitian(const double2* taa, const double2* tbb, double2* paa, double2* pbb, int nl,
-                             uint64_t total, double bscale, const double2* tab, double2* pab, cudaStream_t s);
+                             uint64_t total, double bscale, const double2* tab, double2* wl, cudaStream_t s);
 // kernels::potrf for nb blocks (potrf.cuh); n_fail nullable.
 void launch_potrf_batched(const double2* taa, double2* q, int32_t* info, int nl, uint64_t nb, int* n_fail,
                           cudaStream_t s);

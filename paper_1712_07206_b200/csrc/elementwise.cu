@@ -43,11 +43,14 @@ static __global__ void fill_uniform_kernel(double* __restrict__ p, uint64_t n, u
 // conj(h(l,i)) for l > i).  The contraction computes P^H R, so
 //   P(k,i) = conj(T(i,k)) for k <= i,  T(k,i) for k > i
 // (= full(T) with the diagonal conjugated; identical for a real diagonal).
-//   Pbb[a] = bscale * P(T_BB[a]),  Paa[a] = P(T_AA[a])  (bscale 1/2; 1 for the merged algorithm)
+//   Pbb[a] = bscale * P(T_BB[a]),  Paa[a] = P(T_AA[a])  (bscale 1/2)
+// Merged algorithm (wl != nullptr): the stacked left operand of W = M Y per atom instead,
+//   wl[a] = [Paa | Tab] then [Pab | Pbb]  (column i of each N_L x 2 N_L half holds k = 0 .. N_L-1)
+// with Pab(k, i) = conj(T_AB(i, k)) (Pab^H B = T_AB B) and Pbb = full(T_BB) (bscale 1).
 static __global__ void expand_hermitian_kernel(const double2* __restrict__ taa, const double2* __restrict__ tbb,
                                         double2* __restrict__ paa, double2* __restrict__ pbb, int nl,
                                         uint64_t total, double bscale, const double2* __restrict__ tab,
-                                        double2* __restrict__ pab) {
+                                        double2* __restrict__ wl) {
   const uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= total) return;
   const uint64_t blk = static_cast<uint64_t>(nl) * nl;
@@ -61,16 +64,21 @@ static __global__ void expand_hermitian_kernel(const double2* __restrict__ taa, 
     vaa.y = -vaa.y;
     vbb.y = -vbb.y;
   }
-  paa[idx] = vaa;
-  // merged (pab != nullptr): B^H T_BB B stands for the reference's Z^H B + B^H Z share
+  if (!wl) {
+    paa[idx] = vaa;
+    pbb[idx] = make_double2(bscale * vbb.x, bscale * vbb.y);
+    return;
+  }
+  // merged: B^H T_BB B stands for the reference's Z^H B + B^H Z share
   // 1/2 B^H (T_BB + T_BB^H) B (hemm reads T_BB's diagonal as stored, kernels.cpp:152-167),
   // i.e. T_BB with its diagonal's imaginary part dropped
-  if (pab && k == i) vbb.y = 0.0;
-  pbb[idx] = make_double2(bscale * vbb.x, bscale * vbb.y);
-  if (pab) {  // Pab[a](k, i) = conj(T_AB[a](i, k)): Pab^H B = T_AB B
-    const double2 v = tab[a * blk + i + static_cast<uint64_t>(k) * nl];
-    pab[idx] = make_double2(v.x, -v.y);
-  }
+  if (k == i) vbb.y = 0.0;
+  const double2 v = tab[a * blk + i + static_cast<uint64_t>(k) * nl];
+  double2* w = wl + 4 * a * blk + k;
+  w[static_cast<uint64_t>(i) * nl] = vaa;                      // [Paa | .]
+  w[static_cast<uint64_t>(nl + i) * nl] = tab[idx];            // [. | Tab]
+  w[2 * blk + static_cast<uint64_t>(i) * nl] = make_double2(v.x, -v.y);  // [Pab | .]
+  w[2 * blk + static_cast<uint64_t>(nl + i) * nl] = make_double2(bscale * vbb.x, bscale * vbb.y);  // [. | Pbb]
 }
 
 // out[i] = sum_r in[r][i], ranks in order (bitwise deterministic); out may alias one of
@@ -106,10 +114,10 @@ void launch_fill_uniform(double* p, uint64_t n, uint64_t seed, double lo, double
 }
 
 void launch_expand_hermitian(const double2* taa, const double2* tbb, double2* paa, double2* pbb, int nl,
-                             uint64_t total, double bscale, const double2* tab, double2* pab, cudaStream_t s) {
+                             uint64_t total, double bscale, const double2* tab, double2* wl, cudaStream_t s) {
   if (!total) return;
   expand_hermitian_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(taa, tbb, paa, pbb, nl, total,
-                                                                                      bscale, tab, pab);
+                                                                                      bscale, tab, wl);
   HS_CUDA(cudaGetLastError());
 }
 

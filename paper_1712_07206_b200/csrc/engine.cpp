@@ -45,7 +45,7 @@ void engine_free(hsdla_b200_engine* e) {
   for (void* p : {e->lapw_scratch, (void*)e->info, (void*)e->n_fail, (void*)e->sk_ws, (void*)e->sk_flags,
                   (void*)e->Aset[0], (void*)e->Bset[0], (void*)e->Aset[1], (void*)e->Bset[1], (void*)e->X1,
                   (void*)e->X2, (void*)e->Tab, (void*)e->Taa, (void*)e->Tbb, (void*)e->Paa, (void*)e->Pbb,
-                  (void*)e->Pab, (void*)e->U, (void*)e->Hp, (void*)e->Sp})
+                  (void*)e->Wl, (void*)e->U, (void*)e->Hp, (void*)e->Sp})
     if (p) cudaFree(p);
   if (e->host_stage) cudaFreeHost(e->host_stage);
   release_file_view(e);
@@ -182,16 +182,22 @@ static void make_chunk(hsdla_b200_engine* e, int set, uint64_t a0, uint64_t a1, 
   // batched per-atom products over the held columns: operators {2nl, nl, nac} (row i in
   // dim 1, atom in dim 2), coefficient views {2nl, nac, ncol} (atom in dim 1, G in dim 2).
   const uint64_t blk = nl * nl;
-  CUtensorMap mTab, mPbb, mPaa, mPab, vA, vB;
+  CUtensorMap mTab, mPbb, mPaa, mW0, mW1, vA, vB;
   make_map(&mTab, e->Tab + a0 * blk, 2 * nl, nl, nac, 2 * nl, 2 * blk, kBatBM, 1);
   make_map(&mPbb, e->Pbb + a0 * blk, 2 * nl, nl, nac, 2 * nl, 2 * blk, kBatBM, 1);
   make_map(&mPaa, e->Paa + a0 * blk, 2 * nl, nl, nac, 2 * nl, 2 * blk, kBatBM, 1);
-  make_map(&mPab, e->Pab + a0 * blk, 2 * nl, nl, nac, 2 * nl, 2 * blk, kBatBM, 1);
+  // merged: the stacked left operand {2nl (k), 2nl (output row), nac}, atom stride 4 blk
+  make_map(&mW0, e->Wl + 4 * a0 * blk, 2 * nl, 2 * nl, nac, 2 * nl, 8 * blk, kBatWBM, 1);
+  make_map(&mW1, e->Wl + 4 * a0 * blk + 2 * blk, 2 * nl, 2 * nl, nac, 2 * nl, 8 * blk, kBatWBM, 1);
   make_map(&vA, e->A(set) + r0, 2 * nl, nac, ncol, 2 * nl, 2 * K, 1, kBatBN);
   make_map(&vB, e->B(set) + r0, 2 * nl, nac, ncol, 2 * nl, 2 * K, 1, kBatBN);
   const int bat_tx = static_cast<int>((ncol + kBatBN - 1) / kBatBN), bat_ty = static_cast<int>((nl + kBatBM - 1) / kBatBM);
   const uint64_t bat_tiles = static_cast<uint64_t>(bat_tx) * bat_ty * nac;
-  if (bat_tiles > static_cast<uint64_t>(INT32_MAX)) throw Fail{HSDLA_B200_SIZING_ERROR, "too many batched tiles"};
+  const int batw_ty = static_cast<int>((2 * nl + kBatWBM - 1) / kBatWBM);
+  const uint64_t batw_tiles = static_cast<uint64_t>(bat_tx) * batw_ty * nac;
+  if (batw_tiles > static_cast<uint64_t>(INT32_MAX)) throw Fail{HSDLA_B200_SIZING_ERROR, "too many batched tiles"};
+  // N_L mod 8 in [1, 4]: each segment's last k-slab is half zero-fill (skipped by the kernel)
+  const int half = nl % kChunkC >= 1 && nl % kChunkC <= kChunkC / 2;
   auto bat_base = [&](CtnParams& P, double2* out) {
     std::memset(&P, 0, sizeof(P));
     P.n = static_cast<int>(ncol);
@@ -211,6 +217,7 @@ static void make_chunk(hsdla_b200_engine* e, int set, uint64_t a0, uint64_t a1, 
   cp.z.L[1] = mPbb;
   cp.z.R[1] = vB;
   cp.z.kchunks[0] = cp.z.kchunks[1] = chunks_of(nl);
+  cp.z.half_last[0] = cp.z.half_last[1] = half;
   cp.z.r_row_z[0] = cp.z.r_row_z[1] = 1;
   cp.z.nseg = 2;
   cp.zf = cp.z;
@@ -221,19 +228,27 @@ static void make_chunk(hsdla_b200_engine* e, int set, uint64_t a0, uint64_t a1, 
   cp.x.L[0] = mPaa;
   cp.x.R[0] = vA;
   cp.x.kchunks[0] = chunks_of(nl);
+  cp.x.half_last[0] = half;
   cp.x.r_row_z[0] = 1;
   cp.x.nseg = 1;
-  // merged: W_A = T_AA A_a + T_AB B_a -> X1, W_B = T_AB^H A_a + T_BB B_a -> X2
-  bat_base(cp.wa, e->X1 + r0);
-  cp.wa.L[0] = mPaa;
-  cp.wa.R[0] = vA;
-  cp.wa.L[1] = mPab;
-  cp.wa.R[1] = vB;
-  cp.wa.kchunks[0] = cp.wa.kchunks[1] = chunks_of(nl);
-  cp.wa.r_row_z[0] = cp.wa.r_row_z[1] = 1;
-  cp.wa.nseg = 2;
-  cp.wb = cp.z;  // T_AB^H A_a + Pbb^H B_a with Pbb = full(T_BB) in a merged build
-  cp.wb.out = x2 + r0;
+  // merged: [W_A; W_B] = M_a [A_a; B_a] in ONE launch over 2 N_L output rows per atom:
+  // segment 0 (k over A_a) reads [Paa | Tab], segment 1 (k over B_a) [Pab | Pbb];
+  // rows < N_L (W_A) go to X1, the rest (W_B) to X2
+  bat_base(cp.w, e->X1 + r0);
+  cp.w.L[0] = mW0;
+  cp.w.R[0] = vA;
+  cp.w.L[1] = mW1;
+  cp.w.R[1] = vB;
+  cp.w.kchunks[0] = cp.w.kchunks[1] = chunks_of(nl);
+  cp.w.half_last[0] = cp.w.half_last[1] = half;
+  cp.w.r_row_z[0] = cp.w.r_row_z[1] = 1;
+  cp.w.nseg = 2;
+  cp.w.m_valid = static_cast<int>(2 * nl);
+  cp.w.m_row = static_cast<int>(nl);
+  cp.w.out2 = x2 + r0;
+  cp.w.bat_ty = batw_ty;
+  cp.w.bat_tiles = static_cast<int>(batw_tiles);
+  cp.grid_batw = dim3(static_cast<unsigned>(std::min<uint64_t>(batw_tiles, e->sms)));
   // persistent: one CTA per SM (the 384-thread CTA holds the whole register file)
   cp.grid_bat = dim3(static_cast<unsigned>(std::min<uint64_t>(bat_tiles, e->sms)));
 }
@@ -405,7 +420,7 @@ hsdla_b200_engine* engine_create(int device, const ShardSpec& sp) {
     dalloc(e.get(), &e->Tbb, sp.na * blk);
     dalloc(e.get(), &e->Paa, sp.na * blk);
     dalloc(e.get(), &e->Pbb, sp.na * blk);
-    dalloc(e.get(), &e->Pab, sp.na * blk);
+    dalloc(e.get(), &e->Wl, 4 * sp.na * blk);
     dalloc(e.get(), &e->U, e->K);
     dalloc(e.get(), &e->info, sp.na);
     dalloc(e.get(), &e->n_fail, 1);
@@ -699,7 +714,7 @@ void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool last, hsd
     const uint64_t total = nac * nl * nl, off = cp.a0 * nl * nl;
     const bool merged = algo == HSDLA_B200_ALGO_REFINED_MERGED;
     launch_expand_hermitian(e->Taa + off, e->Tbb + off, e->Paa + off, e->Pbb + off, static_cast<int>(nl), total,
-                            merged ? 1.0 : 0.5, e->Tab + off, merged ? e->Pab + off : nullptr, s);
+                            merged ? 1.0 : 0.5, e->Tab + off, merged ? e->Wl + 4 * off : nullptr, s);
     ++e->launches;
   };
   // operators uploaded on the copy stream (engine_upload_operators): wait before expanding
@@ -761,8 +776,8 @@ void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool last, hsd
   } else if (algo == HSDLA_B200_ALGO_REFINED_MERGED) {
     timed_op(e, HSDLA_B200_PHASE_Z_LOOP, [&] {
       expand_ops();
-      launch_bat(e, cp.wa, cp.grid_bat);
-      launch_bat(e, cp.wb, cp.grid_bat);
+      launch_batw_kernel(e->arith, cp.grid_batw, cp.w, e->stream);  // W_A and W_B
+      ++e->launches;
     });
     timed_op(e, HSDLA_B200_PHASE_HER2K, [&] { timed_h(cp.hm, true); });  // her2k + herkx merged
   } else {

@@ -11,7 +11,10 @@
 //   Tab     raw per-atom T_AB blocks (used as-is: Z = T_AB^H A is a CTN product)
 //   Pbb,Paa 1/2 full(T_BB) (full(T_BB) for the merged algorithm), full(T_AA) expanded
 //           from the LOWER triangles only
-//   Pab     T_AB^H per atom (merged algorithm: W_A = T_AA A + T_AB B)
+//   Wl      merged algorithm: the left operand of W = M Y per atom, 4 N_L^2 complex:
+//           [Paa | Tab] (N_L k over A_a's rows x 2 N_L output rows), then [Pab | Pbb]
+//           (k over B_a's rows) with Pab = T_AB^H, Pbb = full(T_BB); one BATCH launch
+//           writes W_A (rows < N_L) to X1 and W_B to X2
 //   Hp, Sp  the engine's column window [c0, c1) of packed-lower N_G x N_G storage:
 //           global packed indices [pk0, pk0 + npk) (LAPACK 'L' packing; halves D2H and
 //           NCCL bytes).  The whole triangle when the window is [0, N_G).
@@ -61,12 +64,13 @@ struct ChunkPlan {
   const double2* B = nullptr;
   // s: S; z: Z -> X1 (refined/original); zf: Z -> X2 (fused); x: Q^H A -> X1;
   // h: fused her2k+herkx; h2k: her2k over X1; hkx: herkx A^H X1; haa: original X2^H X1
-  // merged: wa: W_A = T_AA A + T_AB B -> X1; wb: W_B = T_AB^H A + T_BB B -> X2; hm: [A;B]^H [X1;X2]
-  CtnParams s, z, zf, x, h, h2k, hkx, haa, wa, wb, hm;
+  // merged: w: [W_A; W_B] = M Y (W_A = T_AA A + T_AB B -> X1, W_B = T_AB^H A + T_BB B -> X2,
+  // one launch); hm: [A;B]^H [X1;X2]
+  CtnParams s, z, zf, x, h, h2k, hkx, haa, w, hm;
   // the S contraction split by segment (first streamed chunk: A^H A starts on A's rows
   // while B, T, U are still on the wire; (UB)^H (UB) accumulates once they landed)
   CtnParams sA, sB;
-  dim3 grid_tri, grid_bat;
+  dim3 grid_tri, grid_bat, grid_batw;
 };
 
 struct OpTime {
@@ -107,7 +111,7 @@ struct hsdla_b200_engine {
   double2* Aset[2] = {};  // A/B sets (set 1: k-point batches)
   double2* Bset[2] = {};
   double2 *X1 = nullptr, *X2 = nullptr;
-  double2 *Tab = nullptr, *Taa = nullptr, *Tbb = nullptr, *Paa = nullptr, *Pbb = nullptr, *Pab = nullptr;
+  double2 *Tab = nullptr, *Taa = nullptr, *Tbb = nullptr, *Paa = nullptr, *Pbb = nullptr, *Wl = nullptr;
   double* U = nullptr;
   int32_t* info = nullptr;        // per-atom potrf result of the original algorithm (-1 = HPD)
   int* n_fail = nullptr;          // original algorithm: failed atoms so far in this build

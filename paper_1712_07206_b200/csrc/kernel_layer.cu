@@ -289,6 +289,7 @@ static void rect(Ctx& x, const double2* L, const double2* R, uint64_t m, uint64_
   make_map(&P.L[0], L, 2 * k, m, 1, 2 * k, 2 * k * m, kBatBM, 1);
   make_map(&P.R[0], R, 2 * k, 1, n, 2 * k, 2 * k, 1, kBatBN);
   P.kchunks[0] = chunks_of(k);
+  P.half_last[0] = k % kChunkC >= 1 && k % kChunkC <= kChunkC / 2;  // skip the zero half-slab
   P.r_row_z[0] = 1;
   P.nseg = 1;
   P.n = static_cast<int>(n);

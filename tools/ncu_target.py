@@ -1,6 +1,6 @@
 """Small, fixed workload for ncu captures (development helper): `builds` device-resident
 builds of a config (default algo merged), or `--lapw` setup passes.  Launch order per
-merged build: expand, diag_scale, S (TRI), W_A (BATCH), W_B (BATCH), H (TRI)."""
+merged build: diag_scale, S (TRI), expand, W = [W_A; W_B] (BATCH, 24-row tiles), H (TRI)."""
 import argparse
 import sys
 
