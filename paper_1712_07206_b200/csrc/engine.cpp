@@ -57,6 +57,7 @@ void engine_free(hsdla_b200_engine* e) {
     if (e->stage_buf[i]) cudaFreeHost(e->stage_buf[i]);
   }
   for (cudaEvent_t ev : e->ev_pool) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : e->tr_pool) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e->ev_chunk_up) cudaEventDestroy(ev);
   for (int q = 0; q < hsdla_b200_engine::kD2hPieces; ++q)
     for (cudaEvent_t ev : {e->ev_h_band[q], e->ev_h_red[q], e->ev_dl_h[q]})
@@ -427,6 +428,7 @@ hsdla_b200_engine* engine_create(int device, const ShardSpec& sp) {
     dalloc(e.get(), &e->Hp, e->cap_pk);
     dalloc(e.get(), &e->Sp, e->cap_pk);
     HS_CUDA(cudaDeviceGetAttribute(&e->sms, cudaDevAttrMultiProcessorCount, device));
+    if (const int cap = static_cast<int>(env_double("HSDLA_B200_SMS", 0))) e->sms = std::min(e->sms, cap);  // tuning
     dalloc(e.get(), &e->sk_ws, static_cast<uint64_t>(e->sms) * kSkSlot);
     dalloc(e.get(), &e->sk_flags, static_cast<uint64_t>(e->sms));
     HS_CUDA(cudaMemset(e->sk_flags, 0, e->sms * sizeof(uint32_t)));
@@ -555,7 +557,12 @@ static void upload_atoms_staged(hsdla_b200_engine* e, int set, const hsdla_b200_
                                 cudaMemcpyHostToDevice, s));
       continue;
     }
-    const uint64_t per = std::max<uint64_t>(1, kStageSlab / colb);
+    // pack pieces of ~1/div of the matrix (1 MB .. one slab): the DMA of piece i overlaps
+    // the packing of piece i+1
+    static const double div = std::max(1.0, env_double("HSDLA_B200_PIECE_DIV", 1.0));
+    const uint64_t piece = std::min<uint64_t>(kStageSlab, std::max<uint64_t>(uint64_t(1) << 20,
+                                              static_cast<uint64_t>(static_cast<double>(colb * cols) / div)));
+    const uint64_t per = std::max<uint64_t>(1, piece / colb);
     for (uint64_t j0 = 0; j0 < cols; j0 += per) {
       const uint64_t nc = std::min(per, cols - j0);
       int slot;
@@ -616,6 +623,19 @@ static cudaEvent_t next_event(hsdla_b200_engine* e) {
     e->ev_pool.push_back(ev);
   }
   return e->ev_pool[e->ev_used++];
+}
+
+// HSDLA_B200_TRACE: a timing event on stream s named `what` (device timeline of one call).
+void trace_mark(hsdla_b200_engine* e, cudaStream_t s, const std::string& what) {
+  if (!trace_on()) return;
+  if (e->tr_marks.size() == e->tr_pool.size()) {
+    cudaEvent_t ev;
+    HS_CUDA(cudaEventCreate(&ev));
+    e->tr_pool.push_back(ev);
+  }
+  cudaEvent_t ev = e->tr_pool[e->tr_marks.size()];
+  HS_CUDA(cudaEventRecord(ev, s));
+  e->tr_marks.push_back({what, ev});
 }
 
 // NVTX range names of the phase slots (include/hsdla_b200.h HSDLA_B200_PHASE_*).
@@ -685,7 +705,8 @@ void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool last, hsd
     // reduce of band q overlaps the compute of band q+1)
     // (only with >= 4 tile waves: smaller final launches would mostly be stream-K tails)
     const bool grouped = e->comm || !e->local_group.empty();
-    if (!(last && (e->band_final_h || grouped) && P.tiles_total >= 4 * e->sms)) {
+    static const double min_waves = env_double("HSDLA_B200_BAND_MIN_WAVES", 4.0);
+    if (!(last && (e->band_final_h || grouped) && P.tiles_total >= min_waves * e->sms)) {
       launch_tri(e, P, cp.grid_tri);
       return;
     }
@@ -732,6 +753,7 @@ void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool last, hsd
       if (kt) HS_CUDA(cudaEventRecord(kt->s1, s));
     });
     if (last) HS_CUDA(cudaEventRecord(e->ev_s_done, s));
+    if (last) trace_mark(e, s, "s_done");
   };
   auto timed_h = [&](CtnParams& P, bool final) {
     if (e->wait_before_h) HS_CUDA(cudaStreamWaitEvent(s, e->wait_before_h, 0));  // H storage reuse
@@ -776,8 +798,10 @@ void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool last, hsd
   } else if (algo == HSDLA_B200_ALGO_REFINED_MERGED) {
     timed_op(e, HSDLA_B200_PHASE_Z_LOOP, [&] {
       expand_ops();
+      trace_mark(e, s, "x");
       launch_batw_kernel(e->arith, cp.grid_batw, cp.w, e->stream);  // W_A and W_B
       ++e->launches;
+      trace_mark(e, s, "w");
     });
     timed_op(e, HSDLA_B200_PHASE_HER2K, [&] { timed_h(cp.hm, true); });  // her2k + herkx merged
   } else {
@@ -806,6 +830,7 @@ void begin_build(hsdla_b200_engine* e, int algo) {
   e->uploaded_streamed = false;
   e->ev_used = 0;
   e->ops.clear();
+  e->tr_marks.clear();
   e->built = true;
   e->banded = false;
   if (e->overlap_dl) e->band_final_h = true;  // (the one-shot drop-in sets and clears it itself)
@@ -838,6 +863,7 @@ void engine_build_streamed(hsdla_b200_engine* e, const hsdla_b200_problem* p, ui
   // the copy stream may only overwrite A/B/T/U once the previous build has consumed them
   HS_CUDA(cudaStreamWaitEvent(e->copy_stream, e->ev_end, 0));
   HS_CUDA(cudaEventRecord(e->ev_up0, e->copy_stream));
+  trace_mark(e, e->copy_stream, "up_start");
   const uint64_t ab_bytes = p->n_atoms * p->n_l * p->n_g * sizeof(double2);
   const bool pinned = is_pinned(p->A, ab_bytes) && is_pinned(p->B, ab_bytes);
   // pageable rows are packed into pinned slabs at ~60 GB/s (copy_nt) and DMA'd from there,
@@ -863,6 +889,7 @@ void engine_build_streamed(hsdla_b200_engine* e, const hsdla_b200_problem* p, ui
                    ops_pinned ? 7 : 3);
       if (!ops_pinned) upload_atoms_staged(e, 0, p, a0, plan[c].a0, plan[c].a1, e->copy_stream, 4);
       HS_CUDA(cudaEventRecord(e->ev_chunk_up[c], e->copy_stream));
+      trace_mark(e, e->copy_stream, "up" + std::to_string(c));
     }
   }
   for (size_t c = 0; c < plan.size(); ++c) {
@@ -881,10 +908,13 @@ void engine_build_streamed(hsdla_b200_engine* e, const hsdla_b200_problem* p, ui
       // already computes chunk c-1 (its phases were enqueued in the previous iteration)
       upload_atoms_staged(e, 0, p, a0, plan[c].a0, plan[c].a1, e->copy_stream, first_split ? 6 : 7);
       HS_CUDA(cudaEventRecord(e->ev_chunk_up[c], e->copy_stream));
+      trace_mark(e, e->copy_stream, "up" + std::to_string(c));
     }
     HS_CUDA(cudaStreamWaitEvent(e->stream, e->ev_chunk_up[c], 0));
     if (c == 0 && !first_split) HS_CUDA(cudaEventRecord(e->ev_begin, e->stream));
+    trace_mark(e, e->stream, "c" + std::to_string(c) + "_start");
     enqueue_chunk(e, plan[c], algo, c + 1 == plan.size(), nullptr, first_split);
+    trace_mark(e, e->stream, "c" + std::to_string(c) + "_end");
   }
   HS_CUDA(cudaEventRecord(e->ev_up1, e->copy_stream));
   HS_CUDA(cudaEventRecord(e->ev_end, e->stream));

@@ -179,6 +179,10 @@ struct hsdla_b200_engine {
   size_t fmap_len = 0;
   struct stat fmap_st {};
   double tr_pack_ms = 0, tr_wait_ms = 0;  // HSDLA_B200_TRACE: pageable staging accounting
+  // HSDLA_B200_TRACE: device timeline marks (timing events on the compute / copy streams),
+  // printed relative to the first mark by finish_download
+  std::vector<std::pair<std::string, cudaEvent_t>> tr_marks;
+  std::vector<cudaEvent_t> tr_pool;
   uint64_t tr_pack_bytes = 0;
   // roofline: events around the whole-build S and H contraction launches, harvested lazily
   static constexpr int kRing = 64;
@@ -243,6 +247,7 @@ void harvest(hsdla_b200_engine* e, hsdla_b200_engine::KTimer& t);
 // building blocks shared with the HSDL-file and LAPW front ends
 void begin_build(hsdla_b200_engine* e, int algo);
 void ensure_streamed_plans(hsdla_b200_engine* e);
+void trace_mark(hsdla_b200_engine* e, cudaStream_t s, const std::string& what);
 void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool last, hsdla_b200_engine::KTimer* kt,
                    bool s_rest = false);
 char* stage_acquire(hsdla_b200_engine* e, int& slot);

@@ -172,7 +172,8 @@ void unpack_lower(const double2* pk, double2* full, uint64_t n, uint64_t c0, uin
 
 // Unpack the global packed-lower index range [b0, b1) (it may start and end inside a
 // column) into the lower triangle of the n x n column-major matrix `full`; src holds
-// exactly those b1 - b0 elements.  Threads split the range by element count.
-void unpack_range(const double2* src, double2* full, uint64_t n, uint64_t b0, uint64_t b1);
+// exactly those b1 - b0 elements.  Threads split the range by element count.  release:
+// demote the source lines from the cores' private caches afterwards (host_pool.cpp).
+void unpack_range(const double2* src, double2* full, uint64_t n, uint64_t b0, uint64_t b1, bool release);
 
 }  // namespace hsdla_b200

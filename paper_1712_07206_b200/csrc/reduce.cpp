@@ -275,6 +275,7 @@ void enqueue_download(hsdla_b200_engine* e) {
   d.h.clear();
   const std::vector<Range> own = engine_owned(e);
   cudaStream_t cs = e->copy_stream;
+  trace_mark(e, cs, "dl_enq");
   HS_CUDA(cudaStreamWaitEvent(cs, e->reduced ? e->ev_s_red : e->ev_s_done, 0));
   for (const Range& o : own) {
     HS_CUDA(cudaMemcpyAsync(e->host_stage + e->cap_pk + (o.first - e->pk0), e->Sp + (o.first - e->pk0),
@@ -282,6 +283,7 @@ void enqueue_download(hsdla_b200_engine* e) {
     d.s.push_back({o.first, o.second, e->ev_dl_s});
   }
   HS_CUDA(cudaEventRecord(e->ev_dl_s, cs));
+  trace_mark(e, cs, "dl_s");
   if (!e->banded) HS_CUDA(cudaStreamWaitEvent(cs, e->reduced ? e->ev_reduce_end : e->ev_end, 0));
   for (int q = 0; q < hsdla_b200_engine::kD2hPieces; ++q) {
     // banded: piece q is final once band q is computed (one engine) or reduced (group)
@@ -295,6 +297,7 @@ void enqueue_download(hsdla_b200_engine* e) {
       d.h.push_back({b0, b1, e->ev_dl_h[q]});
     }
     HS_CUDA(cudaEventRecord(e->ev_dl_h[q], cs));
+    trace_mark(e, cs, "dl_h" + std::to_string(q));
   }
   d.pending = true;
 }
@@ -309,24 +312,51 @@ void finish_download(hsdla_b200_engine* e, double* H, double* S, std::chrono::st
     if (trace_on()) tr += std::string(" ") + what + "=" + std::to_string(ms()).substr(0, 6);
   };
   d.pending = false;
+  // a stage that fits the cores' L2s (16 x 2 MB on the measured host) stays cached after the
+  // unpack reads it unless demoted (host_pool.cpp); HSDLA_B200_STAGE_DEMOTE_MB overrides
+  static const double demote_mb = env_double("HSDLA_B200_STAGE_DEMOTE_MB", 48.0);
+  uint64_t stage_elems = 0;
+  for (const DlPiece& p : d.s) stage_elems += p.b1 - p.b0;
+  for (const DlPiece& p : d.h) stage_elems += p.b1 - p.b0;
+  const bool release = static_cast<double>(stage_elems) * sizeof(double2) < demote_mb * (1 << 20);
   HS_CUDA(cudaEventSynchronize(e->ev_dl_s));
   mark("s_landed");
   if (S)
     for (const DlPiece& p : d.s)
-      unpack_range(e->host_stage + e->cap_pk + (p.b0 - d.pk0), reinterpret_cast<double2*>(S), d.ng, p.b0, p.b1);
+      unpack_range(e->host_stage + e->cap_pk + (p.b0 - d.pk0), reinterpret_cast<double2*>(S), d.ng, p.b0, p.b1,
+                   release);
   mark("s_unpacked");
-  cudaEvent_t waited = nullptr;
-  for (const DlPiece& p : d.h) {
-    if (p.ready != waited) {
-      HS_CUDA(cudaEventSynchronize(p.ready));
-      waited = p.ready;
-      mark("h_landed");
-    }
-    if (H) unpack_range(e->host_stage + (p.b0 - d.pk0), reinterpret_cast<double2*>(H), d.ng, p.b0, p.b1);
+  // H piece by piece as the pieces land; consecutive pieces that have all landed by the
+  // time the first is waited for are unpacked in ONE pass over the host pool (an unbanded
+  // build's pieces all land together: one 16-thread unpack instead of eight small ones)
+  auto landed = [](cudaEvent_t ev) {
+    const cudaError_t r = cudaEventQuery(ev);
+    if (r == cudaSuccess) return true;
+    if (r != cudaErrorNotReady) HS_CUDA(r);
+    return false;
+  };
+  for (size_t i = 0; i < d.h.size();) {
+    HS_CUDA(cudaEventSynchronize(d.h[i].ready));
+    mark("h_landed");
+    size_t j = i + 1;
+    while (j < d.h.size() && d.h[j].b0 == d.h[j - 1].b1 && (d.h[j].ready == d.h[i].ready || landed(d.h[j].ready)))
+      ++j;
+    if (H)
+      unpack_range(e->host_stage + (d.h[i].b0 - d.pk0), reinterpret_cast<double2*>(H), d.ng, d.h[i].b0,
+                   d.h[j - 1].b1, release);
+    i = j;
   }
   HS_CUDA(cudaEventSynchronize(e->ev_dl_h[hsdla_b200_engine::kD2hPieces - 1]));
   mark("h_unpacked");
-  if (trace_on()) std::fprintf(stderr, "[hsdla_b200 trace] download (ms since call start):%s\n", tr.c_str());
+  if (trace_on()) {
+    std::fprintf(stderr, "[hsdla_b200 trace] download (ms since call start):%s\n", tr.c_str());
+    if (!e->tr_marks.empty()) {
+      std::string dv;
+      for (auto& m : e->tr_marks) dv += " " + m.first + "=" + std::to_string(ev_ms(e->tr_marks[0].second, m.second)).substr(0, 5);
+      std::fprintf(stderr, "[hsdla_b200 trace] device (ms since first mark):%s\n", dv.c_str());
+      e->tr_marks.clear();
+    }
+  }
 }
 
 void engine_download(hsdla_b200_engine* e, double* H, double* S) {
