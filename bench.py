@@ -332,14 +332,14 @@ def run_b200(args):
     dev = d.local
     torch.cuda.set_device(dev)
     na_total, nl, ng, desc = workload(args, P)
-    bounds = hb.shard_atoms(na_total, P)
-    a0, a1 = bounds[d.rank], bounds[d.rank + 1]
-    # this rank's atom shard of ONE problem (bit-identical rows of generate_problem(na_total, ...))
+    # this rank's row-balanced shard of ONE problem: the K rows split evenly, the rank holds the
+    # atoms its rows touch (bit-identical rows of generate_problem(na_total, ...))
+    a0, na_sh, r0, r1 = hb.shard_rows(na_total, nl, P)[d.rank]
     p = (hb.generate_problem(na_total, nl, ng, 1, 0) if P == 1 else
-         hb.generate_problem_shard(na_total, nl, ng, a0, a1, 1, 0))
+         hb.generate_problem_shard(na_total, nl, ng, a0, a0 + na_sh, 1, 0))
     na = p.n_atoms
     hb.set_default_arith(args.arith)  # kernel layer + any engine created below
-    eng = hb.Engine(dev, na, nl, ng)
+    eng = hb.Engine(dev, na, nl, ng, row_begin=r0, row_end=r1)
     eng.set_arith(args.arith)
     multi = P > 1 or args.force_comm
     if multi:

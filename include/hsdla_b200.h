@@ -251,6 +251,11 @@ int hsdla_b200_generate_problem_shard(uint64_t n_atoms, uint64_t n_l, uint64_t n
 /* Contiguous, count-balanced atom ranges for `parts` GPUs:
  * bounds[r] .. bounds[r+1] is shard r; bounds has parts+1 entries. */
 int hsdla_b200_shard_atoms(uint64_t n_atoms, int parts, uint64_t* bounds);
+/* Row-balanced shards (what the multi-GPU drop-in uses): the K = n_atoms n_l rows split into
+ * `parts` equal ranges; shard r is shards[4r .. 4r+3] = {atom_begin, n_atoms_local, row_begin,
+ * row_end} (rows local to the shard, hsdla_b200_shard).  Shards' partials sum to the full H, S
+ * (the sum over atoms of pipeline.cpp:296-324 regrouped by rows). */
+int hsdla_b200_shard_rows(uint64_t n_atoms, uint64_t n_l, int parts, uint64_t* shards);
 
 const char* hsdla_b200_last_error(void);
 int hsdla_b200_device_count(int* count);
@@ -279,6 +284,11 @@ typedef struct hsdla_b200_shard {
   uint64_t n_atoms_local, n_l, n_g;
   uint64_t col_begin, col_end;
   uint64_t n_g_capacity;
+  /* K-row range [row_begin, row_end) of the shard's n_atoms_local * n_l rows that its H/S
+   * contractions sum over (row_end 0: all rows).  A row-balanced grid (hsdla_b200_shard_rows)
+   * gives every GPU the same share of the contraction work; the range must start in the
+   * shard's first atom and end in its last (boundary atoms are held by two shards). */
+  uint64_t row_begin, row_end;
 } hsdla_b200_shard;
 int hsdla_b200_engine_create_shard(int device, const hsdla_b200_shard* shard, hsdla_b200_engine** out);
 /* Re-target the engine at N_G = n_g (whole window) within its capacity; HSDLA_B200_SIZING_ERROR

@@ -10,7 +10,7 @@ package is the host-side mirror of the reference interface.
 from .errors import CudaError, ConfigError, DimensionError, IoError, NcclError, SizingError  # noqa: F401
 from .pipeline import (Engine, FlopLedger, HSResult, PhaseTime, PipelineConfig, build_hs, build_hs_file,  # noqa: F401,E501
                        build_hs_kpoints, build_hs_original, group_reduce, build_hs_refined, device_count, flop_model, fp64_peak, host_register, host_unregister, mirror,
-                       nccl_unique_id, parse_strategy, potrf, problem_file_info, set_default_arith, shard_atoms, parse_variant, rel_frobenius_error_lower,
+                       nccl_unique_id, parse_strategy, potrf, problem_file_info, set_default_arith, shard_atoms, shard_rows, parse_variant, rel_frobenius_error_lower,
                        release_cache)
 from .problem import (Preset, ProblemInstance, empty_problem, find_preset, generate_problem, generate_problem_shard,  # noqa: F401
                       load_problem, presets, save_problem)

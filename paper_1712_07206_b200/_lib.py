@@ -40,6 +40,7 @@ EXPORTS = (
     "hsdla_b200_engine_set_download_overlap", "hsdla_b200_build_hs_kpoints",
     "hsdla_b200_engine_create_shard", "hsdla_b200_engine_reshape", "hsdla_b200_engine_set_reduce_mode",
     "hsdla_b200_group_reduce", "hsdla_b200_engine_owned", "hsdla_b200_generate_problem_shard",
+    "hsdla_b200_shard_rows",
 )
 
 
@@ -56,7 +57,8 @@ class Options(C.Structure):
 
 class Shard(C.Structure):
     _fields_ = [("n_atoms_local", C.c_uint64), ("n_l", C.c_uint64), ("n_g", C.c_uint64),
-                ("col_begin", C.c_uint64), ("col_end", C.c_uint64), ("n_g_capacity", C.c_uint64)]
+                ("col_begin", C.c_uint64), ("col_end", C.c_uint64), ("n_g_capacity", C.c_uint64),
+                ("row_begin", C.c_uint64), ("row_end", C.c_uint64)]
 
 
 class Stats(C.Structure):

@@ -3,7 +3,7 @@
 // callers (one process per GPU, e.g. torchrun) drive themselves.
 //
 // Multi-GPU grid of the one-shot calls: n_gpus = col_groups x atom_ranks engines.  Engine
-// (g, r) holds atom shard r (shard_atoms) and column window g (equal-work tile-column
+// (g, r) holds row shard r (shard_rows: an even split of the K rows) and column window g (equal-work tile-column
 // windows) of H and S.  The atom ranks of a window sum their partials (group_reduce:
 // NCCL over the window's GPUs, or a sum kernel for engines that share a device); windows
 // never exchange data.  col_groups = 1 is plain atom sharding with H, S replicated per GPU;
@@ -64,6 +64,25 @@ static std::vector<uint64_t> shard_atoms(uint64_t na, int parts) {
   return b;
 }
 
+// Row-balanced shards: the K = na nl rows split evenly (the H/S contractions, ~all of the
+// work, then take equal time on every GPU: 108 atoms over 8 GPUs is 1633-1634 rows each instead
+// of 14 vs 13 atoms).  Shard r holds the atoms its rows touch: {atom_begin, n_atoms_local,
+// row0, row1} with the row range local to its first atom.
+struct RowShard {
+  uint64_t a0, na, row0, row1;
+};
+static std::vector<RowShard> shard_rows(uint64_t na, uint64_t nl, int parts) {
+  const uint64_t K = na * nl;
+  if (static_cast<uint64_t>(parts) > K) throw Fail{HSDLA_B200_CONFIG_ERROR, "more shards than K rows"};
+  std::vector<RowShard> out(parts);
+  for (int r = 0; r < parts; ++r) {
+    const uint64_t k0 = K * r / parts, k1 = K * (r + 1) / parts;
+    const uint64_t a0 = k0 / nl, a1 = (k1 + nl - 1) / nl;
+    out[r] = {a0, a1 - a0, k0 - a0 * nl, k1 - a0 * nl};
+  }
+  return out;
+}
+
 // Column boundaries of `parts` windows of (about) equal lower-triangle work; interior
 // boundaries are multiples of 64 (the tile width), the last is ng.
 static std::vector<uint64_t> col_windows(uint64_t ng, int parts) {
@@ -88,7 +107,8 @@ static std::vector<uint64_t> col_windows(uint64_t ng, int parts) {
 // Device bytes of the largest engine of a pc x pa grid (window 0 holds every operand
 // column; the merged algorithm's four K x N_G stacks, its packed H, S and the operator blocks).
 static double grid_bytes(uint64_t na, uint64_t nl, uint64_t ng, int pc, int pa) {
-  const double na_r = std::ceil(static_cast<double>(na) / pa), K = na_r * nl;
+  // a row-balanced shard holds up to one atom more than na / pa (the atoms its rows touch)
+  const double na_r = std::min<double>(na, std::ceil(static_cast<double>(na) / pa) + (pa > 1)), K = na_r * nl;
   const double pk = static_cast<double>(ng) * (ng + 1) / 2 / pc;
   return 16.0 * (4.0 * K * ng + 2.0 * pk * 1.1 + 6.0 * na_r * nl * nl);
 }
@@ -148,7 +168,7 @@ static EngineSet* get_engines(const std::vector<int>& devs, uint64_t na, uint64_
   }
   g_cache.clear();  // one grid at a time keeps HBM free for the caller
   if (static_cast<uint64_t>(pa) > na) throw Fail{HSDLA_B200_CONFIG_ERROR, "more GPUs than atoms"};
-  const auto ab = shard_atoms(na, pa);
+  const auto rs = shard_rows(na, nl, pa);
   const auto cw = col_windows(ng, pc);
   auto make = [&](uint64_t cap) {
     auto set = std::make_unique<EngineSet>();
@@ -159,7 +179,9 @@ static EngineSet* get_engines(const std::vector<int>& devs, uint64_t na, uint64_
       set->groups.emplace_back();
       for (int r = 0; r < pa; ++r) {
         ShardSpec sp;
-        sp.na = ab[r + 1] - ab[r];
+        sp.na = rs[r].na;
+        sp.row0 = rs[r].row0;
+        sp.row1 = rs[r].row1;
         sp.nl = nl;
         sp.ng = ng;
         sp.c0 = cw[g];
@@ -169,7 +191,7 @@ static EngineSet* get_engines(const std::vector<int>& devs, uint64_t na, uint64_
         set->engines.push_back(e);
         e->rank = r;
         e->nranks = pa;
-        set->atom0.push_back(ab[r]);
+        set->atom0.push_back(rs[r].a0);
         set->groups.back().push_back(e);
       }
     }
@@ -451,6 +473,19 @@ int hsdla_b200_engine_create(int device, uint64_t na, uint64_t nl, uint64_t ng, 
     *out = engine_create(device, sp);
   });
 }
+int hsdla_b200_shard_rows(uint64_t n_atoms, uint64_t n_l, int parts, uint64_t* shards) {
+  return guarded([&] {
+    if (!shards || parts < 1 || n_l < 1) throw Fail{HSDLA_B200_CONFIG_ERROR, "shard_rows: parts and n_l must be >= 1"};
+    if (static_cast<uint64_t>(parts) > n_atoms) throw Fail{HSDLA_B200_CONFIG_ERROR, "more GPUs than atoms"};
+    const auto rs = shard_rows(n_atoms, n_l, parts);
+    for (int r = 0; r < parts; ++r) {
+      shards[4 * r] = rs[r].a0;
+      shards[4 * r + 1] = rs[r].na;
+      shards[4 * r + 2] = rs[r].row0;
+      shards[4 * r + 3] = rs[r].row1;
+    }
+  });
+}
 int hsdla_b200_engine_create_shard(int device, const hsdla_b200_shard* s, hsdla_b200_engine** out) {
   return guarded([&] {
     if (!out || !s) throw Fail{HSDLA_B200_DIMENSION_ERROR, "null shard / out"};
@@ -461,6 +496,8 @@ int hsdla_b200_engine_create_shard(int device, const hsdla_b200_shard* s, hsdla_
     sp.c0 = s->col_begin;
     sp.c1 = s->col_end;
     sp.ng_capacity = s->n_g_capacity;
+    sp.row0 = s->row_begin;
+    sp.row1 = s->row_end;
     if (sp.ng_capacity && sp.ng_capacity < sp.ng) throw Fail{HSDLA_B200_CONFIG_ERROR, "n_g_capacity < n_g"};
     *out = engine_create(device, sp);
   });

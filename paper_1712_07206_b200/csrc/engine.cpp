@@ -103,20 +103,24 @@ static void set_seg(CtnParams& P, int s, const CUtensorMap& L, const CUtensorMap
 // H and S (beta 0); later chunks accumulate (beta 1).
 static void make_chunk(hsdla_b200_engine* e, int set, uint64_t a0, uint64_t a1, bool first, ChunkPlan& cp) {
   const uint64_t K = e->K, ncol = e->ncol, nl = e->nl;
-  const uint64_t r0 = a0 * nl, Kc = (a1 - a0) * nl, nac = a1 - a0;
+  const uint64_t r0 = a0 * nl, nac = a1 - a0;
   cp.a0 = a0;
   cp.a1 = a1;
   cp.A = e->A(set);
   cp.B = e->B(set);
-  // K-stacked buffers restricted to rows [r0, r0+Kc): {2Kc, ncol, 1}, column stride 2K
+  // the contractions sum over this chunk's rows inside the engine's row range [row0, row1)
+  // (every atom of an engine touches the range, so tr1 > tr0)
+  const uint64_t tr0 = std::max(r0, e->row0), tr1 = std::min(a1 * nl, e->row1), Kc = tr1 - tr0;
+  if (tr1 <= tr0) throw Fail{HSDLA_B200_CONFIG_ERROR, "chunk outside the engine's row range"};
+  // K-stacked buffers restricted to rows [tr0, tr1): {2Kc, ncol, 1}, column stride 2K
   // X2 is allocated on first use by the fused / original algorithms (the refined
   // algorithm needs X1 only); until then its maps alias X1 and are never launched.
   double2* x2 = e->X2 ? e->X2 : e->X1;
   CUtensorMap mA, mB, mX1, mX2;
-  make_map(&mA, e->A(set) + r0, 2 * Kc, ncol, 1, 2 * K, 2 * K * ncol, kTriBM, 1);
-  make_map(&mB, e->B(set) + r0, 2 * Kc, ncol, 1, 2 * K, 2 * K * ncol, kTriBM, 1);
-  make_map(&mX1, e->X1 + r0, 2 * Kc, ncol, 1, 2 * K, 2 * K * ncol, kTriBM, 1);
-  make_map(&mX2, x2 + r0, 2 * Kc, ncol, 1, 2 * K, 2 * K * ncol, kTriBM, 1);
+  make_map(&mA, e->A(set) + tr0, 2 * Kc, ncol, 1, 2 * K, 2 * K * ncol, kTriBM, 1);
+  make_map(&mB, e->B(set) + tr0, 2 * Kc, ncol, 1, 2 * K, 2 * K * ncol, kTriBM, 1);
+  make_map(&mX1, e->X1 + tr0, 2 * Kc, ncol, 1, 2 * K, 2 * K * ncol, kTriBM, 1);
+  make_map(&mX2, x2 + tr0, 2 * Kc, ncol, 1, 2 * K, 2 * K * ncol, kTriBM, 1);
   const uint64_t T = tiles_of(e->ng);
   const bool all = whole(e);
   const uint64_t t0 = e->c0 / kTriBM, t1 = tiles_of(e->c1);
@@ -388,6 +392,12 @@ hsdla_b200_engine* engine_create(int device, const ShardSpec& sp) {
   e->na = sp.na;
   e->nl = sp.nl;
   e->K = sp.na * sp.nl;
+  e->row0 = sp.row0;
+  e->row1 = sp.row1 ? sp.row1 : e->K;
+  if (e->row0 >= e->row1 || e->row1 > e->K || e->row0 >= sp.nl || e->row1 + sp.nl <= e->K)
+    throw Fail{HSDLA_B200_CONFIG_ERROR, "row range [row0, row1) must lie in the shard and touch its first and last atom"};
+  e->own_a0 = (e->row0 + sp.nl - 1) / sp.nl;
+  e->own_a1 = (e->row1 + sp.nl - 1) / sp.nl;
   const bool all = sp.c0 == 0 && c1 == sp.ng;
   // capacity: a whole-window engine can be reshaped to any N_G up to ng_capacity
   const uint64_t cap_ng = all ? std::max(sp.ng, sp.ng_capacity) : sp.ng;
@@ -841,8 +851,9 @@ void engine_build(hsdla_b200_engine* e, int algo) {
   begin_build(e, algo);
   auto& kt = e->ring[e->builds++ % hsdla_b200_engine::kRing];
   harvest(e, kt);
-  kt.flops_h = (algo == HSDLA_B200_ALGO_REFINED_FUSED ? 12 : 8) * e->K * e->ng * e->ng;
-  kt.flops_s = 8 * e->K * e->ng * e->ng;
+  const uint64_t rows = e->row1 - e->row0;
+  kt.flops_h = (algo == HSDLA_B200_ALGO_REFINED_FUSED ? 12 : 8) * rows * e->ng * e->ng;
+  kt.flops_s = 8 * rows * e->ng * e->ng;
   if (!whole(e)) {  // a window's share of the triangle (executed tiles; ledger-style count)
     const double f = static_cast<double>(e->npk) / (static_cast<double>(e->ng) * (e->ng + 1) / 2);
     kt.flops_h = static_cast<uint64_t>(kt.flops_h * f);

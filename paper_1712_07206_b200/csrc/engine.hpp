@@ -101,6 +101,12 @@ struct hsdla_b200_engine {
   int device = 0;
   // ---- geometry ----
   uint64_t na = 0, nl = 0, K = 0;  // local atoms, K = na * nl
+  // K-row range [row0, row1) of the local stack that this engine's H/S contractions sum over
+  // (default [0, K)).  A row-balanced multi-GPU grid splits the global K rows evenly, so an
+  // engine holds every atom its rows touch (boundary atoms on two engines: their W / Z / X
+  // are computed on both, their rows contracted on one).  Atoms [own_a0, own_a1) are the ones
+  // whose first row is in range (each atom of the grid is owned once: the n_hpd count).
+  uint64_t row0 = 0, row1 = 0, own_a0 = 0, own_a1 = 0;
   uint64_t ng = 0;                 // N_G of the problem (global)
   uint64_t c0 = 0, c1 = 0;         // H/S column window [c0, c1)
   uint64_t ncol = 0;               // operand columns held: [c0, ng)
@@ -204,6 +210,7 @@ namespace hsdla_b200 {
 // Engine shard description (hsdla_b200_shard in the C-ABI, with defaults resolved).
 struct ShardSpec {
   uint64_t na = 0, nl = 0, ng = 0;
+  uint64_t row0 = 0, row1 = 0;   // contracted local K rows; row1 == 0: [0, na * nl)
   uint64_t c0 = 0, c1 = 0;       // column window; c1 == 0: [0, ng)
   uint64_t ng_capacity = 0;      // allocate for up to this N_G (0: ng)
 };
@@ -239,7 +246,7 @@ void finish_download(hsdla_b200_engine* e, double* H, double* S,
 void engine_download(hsdla_b200_engine* e, double* H, double* S);
 // Packed ranges of the current result this engine holds final values for.
 std::vector<std::pair<uint64_t, uint64_t>> engine_owned(const hsdla_b200_engine* e);
-uint64_t executed_flops(uint64_t na, uint64_t nl, uint64_t ng, int arith, int algo);
+uint64_t executed_flops(uint64_t na, uint64_t nl, uint64_t ng, int arith, int algo, uint64_t rows = 0);
 void flop_model(int variant, uint64_t na, uint64_t nl, uint64_t ng, uint64_t n_hpd, uint64_t* l);
 float ev_ms(cudaEvent_t a, cudaEvent_t b);
 void harvest(hsdla_b200_engine* e, hsdla_b200_engine::KTimer& t);

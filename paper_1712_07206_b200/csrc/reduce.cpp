@@ -184,16 +184,17 @@ void engine_reduce(hsdla_b200_engine* e, int root) {
   group_reduce({e}, e->red_mode, root);
 }
 
-uint64_t executed_flops(uint64_t na, uint64_t nl, uint64_t ng, int arith, int algo) {
+uint64_t executed_flops(uint64_t na, uint64_t nl, uint64_t ng, int arith, int algo, uint64_t rows) {
   // Real flops the GPU executes for a build.  The refined, fused and original algorithms
   // run lower-triangular contractions of 20 K N_G^2 + 24 N_A N_L^2 N_G complex-MAC flops at
   // 8 per MAC (the original's trmm on the zero upper half of L and its full gemm fold are
   // executed as the lower-only h_aa contraction); the merged one 16 K N_G^2 + 32 N_A N_L^2
   // N_G (two H segments, four per-atom products).  Plus 2 K N_G for diag_scale; the 3M
   // arithmetic executes 6 real flops per complex MAC.
-  const uint64_t K = na * nl;
-  const uint64_t cmac8 = algo == HSDLA_B200_ALGO_REFINED_MERGED ? 16 * K * ng * ng + 32 * na * nl * nl * ng
-                                                                : 20 * K * ng * ng + 24 * na * nl * nl * ng;
+  // rows: the contracted K rows (a row-balanced shard; 0: all na * nl)
+  const uint64_t K = na * nl, R = rows ? rows : K;
+  const uint64_t cmac8 = algo == HSDLA_B200_ALGO_REFINED_MERGED ? 16 * R * ng * ng + 32 * na * nl * nl * ng
+                                                                : 20 * R * ng * ng + 24 * na * nl * nl * ng;
   return (arith == HSDLA_B200_ARITH_3M ? cmac8 / 8 * 6 : cmac8) + 2 * K * ng;
 }
 
@@ -241,12 +242,14 @@ void engine_sync(hsdla_b200_engine* e, hsdla_b200_stats* st) {
   if (e->last_algo == HSDLA_B200_ALGO_ORIGINAL) {
     std::vector<int32_t> info(e->na);
     HS_CUDA(cudaMemcpy(info.data(), e->info, e->na * sizeof(int32_t), cudaMemcpyDeviceToHost));
-    e->n_hpd_last = static_cast<uint64_t>(std::count_if(info.begin(), info.end(), [](int32_t v) { return v < 0; }));
+    // the owned atoms only (a boundary atom of a row-balanced grid is factorised on two engines)
+    e->n_hpd_last = static_cast<uint64_t>(std::count_if(info.begin() + e->own_a0, info.begin() + e->own_a1,
+                                                        [](int32_t v) { return v < 0; }));
   } else {
-    e->n_hpd_last = e->na;
+    e->n_hpd_last = e->own_a1 - e->own_a0;
   }
   st->n_hpd = e->n_hpd_last;
-  st->executed_flops = executed_flops(e->na, e->nl, e->ng, e->arith, e->last_algo);
+  st->executed_flops = executed_flops(e->na, e->nl, e->ng, e->arith, e->last_algo, e->row1 - e->row0);
   for (const OpTime& op : e->ops) st->phase_seconds[op.phase] += ev_ms(op.b, op.e) * 1e-3;
   const cudaEvent_t last = e->reduced ? e->ev_reduce_end : e->ev_end;
   st->device_seconds = ev_ms(e->ev_begin, last) * 1e-3;

@@ -327,11 +327,14 @@ class Engine:
     """Device-resident engine for one shard on one GPU (C-ABI hsdla_b200_engine_*): n_atoms_local
     atoms (an atom shard) and the column window [col_begin, col_end) of H and S (col_end 0: n_g;
     2-D tiling: engines of different windows compute disjoint tile-column bands).  n_g_capacity
-    sizes a whole-window engine for reshape() to larger N_G without reallocation."""
+    sizes a whole-window engine for reshape() to larger N_G without reallocation.  [row_begin,
+    row_end) restricts the H/S contractions to those rows of the shard's K (a row-balanced
+    shard from shard_rows; row_end 0: all rows)."""
 
-    def __init__(self, device, n_atoms_local, n_l, n_g, col_begin=0, col_end=0, n_g_capacity=0):
+    def __init__(self, device, n_atoms_local, n_l, n_g, col_begin=0, col_end=0, n_g_capacity=0,
+                 row_begin=0, row_end=0):
         h = C.c_void_p()
-        sh = _lib.Shard(n_atoms_local, n_l, n_g, col_begin, col_end, n_g_capacity)
+        sh = _lib.Shard(n_atoms_local, n_l, n_g, col_begin, col_end, n_g_capacity, row_begin, row_end)
         check(_lib.lib().hsdla_b200_engine_create_shard(C.c_int(device), C.byref(sh), C.byref(h)), "engine_create")
         self.h = h
         self.n_g = n_g
@@ -483,6 +486,15 @@ def shard_atoms(n_atoms, parts):
     out = (C.c_uint64 * (parts + 1))()
     check(_lib.lib().hsdla_b200_shard_atoms(C.c_uint64(n_atoms), C.c_int(parts), out), "shard_atoms")
     return [int(x) for x in out]
+
+
+def shard_rows(n_atoms, n_l, parts):
+    """Row-balanced shards (the multi-GPU drop-in's partition): the K = n_atoms n_l rows split
+    evenly; a list of (atom_begin, n_atoms_local, row_begin, row_end) per part, rows local to the
+    shard (Engine(..., row_begin=, row_end=))."""
+    out = (C.c_uint64 * (4 * parts))()
+    check(_lib.lib().hsdla_b200_shard_rows(C.c_uint64(n_atoms), C.c_uint64(n_l), C.c_int(parts), out), "shard_rows")
+    return [tuple(int(x) for x in out[4 * r:4 * r + 4]) for r in range(parts)]
 
 
 def device_count():

@@ -29,9 +29,9 @@ def main():
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     dist.init_process_group("gloo")
     na, nl, ng = (int(x) for x in args.dims.split(","))
-    b = hb.shard_atoms(na, world)
-    p = hb.generate_problem_shard(na, nl, ng, b[rank], b[rank + 1], 1, 0)
-    e = hb.Engine(local, p.n_atoms, nl, ng)
+    a0, na_sh, r0, r1 = hb.shard_rows(na, nl, world)[rank]
+    p = hb.generate_problem_shard(na, nl, ng, a0, a0 + na_sh, 1, 0)
+    e = hb.Engine(local, p.n_atoms, nl, ng, row_begin=r0, row_end=r1)
     obj = [hb.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     e.set_comm(obj[0], world, rank)

@@ -75,6 +75,6 @@ def test_ctypes_structs_match_the_header_layout():
                                                       "mem_budget_gb"]
     assert C.sizeof(_lib.Options) == 40  # int, pad, ptr, 3 x int, pad, double
     assert [f for f, _ in _lib.Shard._fields_] == ["n_atoms_local", "n_l", "n_g", "col_begin", "col_end",
-                                                    "n_g_capacity"]
-    assert C.sizeof(_lib.Shard) == 48
+                                                    "n_g_capacity", "row_begin", "row_end"]
+    assert C.sizeof(_lib.Shard) == 64
 

@@ -92,3 +92,24 @@ def test_shard_atoms_partition():
             b = hb.shard_atoms(na, parts)
             sizes = np.diff(b)
             assert b[0] == 0 and b[-1] == na and sizes.min() >= 1 and sizes.max() - sizes.min() <= 1
+
+
+def test_shard_rows_partition():
+    """Row-balanced shards: the K = n_atoms n_l rows split evenly (sizes differ by <= 1), each
+    shard's row range lies in its atoms and touches the first and the last one, and the global
+    rows are covered exactly once."""
+    for na, nl in ((1, 7), (7, 25), (16, 49), (108, 121), (512, 121)):
+        K = na * nl
+        for parts in (1, 2, 3, 8):
+            if parts > na:
+                with pytest.raises(hb.ConfigError):
+                    hb.shard_rows(na, nl, parts)
+                continue
+            sh = hb.shard_rows(na, nl, parts)
+            covered, sizes = 0, []
+            for a0, n_loc, r0, r1 in sh:
+                assert 0 <= r0 < nl and n_loc * nl - nl < r1 <= n_loc * nl
+                assert a0 * nl + r0 == covered  # contiguous, no gap, no overlap
+                covered = a0 * nl + r1
+                sizes.append(r1 - r0)
+            assert covered == K and max(sizes) - min(sizes) <= 1

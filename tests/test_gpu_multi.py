@@ -142,6 +142,43 @@ def test_emulated_grid_group_reduce(restatement, mode, dims):
     assert rel(H, Hs) <= TOL and rel(S, Ss) <= TOL
 
 
+@pytest.mark.parametrize("algo", ["merged", "fused", "refined", "original"])
+def test_row_balanced_shards_sum_to_the_full_result(restatement, algo):
+    """Row-balanced shards (shard_rows: K = 7 x 25 rows over 3 engines on one device, boundary
+    atoms held by two engines, each engine contracting only its row range): the summed partials
+    equal the full result, and the original algorithm's potrf outcomes (an HPD-failing atom
+    among them) are counted once per atom."""
+    p = hb.generate_problem(7, 25, 333, 4, 3)
+    if algo == "original":
+        Hs, Ss, _, want_hpd = restatement.build_hs_original(p)
+    else:
+        (Hs, Ss, _), want_hpd = restatement.build_hs_refined(p), p.n_atoms
+    n = p.n_g
+    H = np.zeros((n, n), np.complex128, order="F")
+    S = np.zeros_like(H)
+    shards = hb.shard_rows(p.n_atoms, p.n_l, 3)
+    assert any(r0 > 0 for _, _, r0, _ in shards)  # genuinely mid-atom boundaries
+    n_hpd = 0
+    for a0, na, r0, r1 in shards:
+        e = hb.Engine(0, na, p.n_l, n, row_begin=r0, row_end=r1)
+        e.upload(p, a0)
+        e.build(algo)
+        Hp, Sp = e.download()
+        H += Hp
+        S += Sp
+        n_hpd += e.sync()["n_hpd"]
+        e.close()
+    assert rel(H, Hs) <= TOL and rel(S, Ss) <= TOL
+    assert n_hpd == want_hpd and (algo != "original" or want_hpd < p.n_atoms)
+
+
+def test_row_range_errors():
+    with pytest.raises(hb.ConfigError):
+        hb.Engine(0, 3, 10, 100, row_begin=10, row_end=25)  # starts past the first atom
+    with pytest.raises(hb.ConfigError):
+        hb.Engine(0, 3, 10, 100, row_begin=0, row_end=20)  # ends before the last atom
+
+
 @pytest.mark.parametrize("reduce", ["scatter", "root"])
 @pytest.mark.parametrize("grid", [(3, 1), (4, 2), (2, 2)], ids=["3x1", "2x2", "1x2"])
 def test_dropin_emulated_grid(restatement, grid, reduce):
