@@ -78,17 +78,19 @@ struct OpTime {
   cudaEvent_t b, e;
 };
 
-// A packed-lower index range [b0, b1) (global indices) copied to the host stage at
-// local offset b0 - pk0 and final once `ready` (on the copy stream) has completed.
+// A packed-lower index range [b0, b1) (global indices) of S (h == 0) or H (h == 1) copied to
+// the host stage at local offset b0 - pk0 (+ cap_pk for S) and final once `ready` (on the
+// copy stream) has completed.
 struct DlPiece {
+  int h;
   uint64_t b0, b1;
   cudaEvent_t ready;
 };
 // The download of one build, snapshotted at enqueue time (the engine may be reshaped
-// for the next k-point before the host unpacks this one).
+// for the next k-point before the host unpacks this one); pieces in landing order.
 struct Download {
   uint64_t ng = 0, pk0 = 0;
-  std::vector<DlPiece> s, h;
+  std::vector<DlPiece> seq;
   bool pending = false;
 };
 

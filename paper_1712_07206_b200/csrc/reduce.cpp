@@ -274,16 +274,15 @@ void enqueue_download(hsdla_b200_engine* e) {
   Download& d = e->dl;
   d.ng = e->ng;
   d.pk0 = e->pk0;
-  d.s.clear();
-  d.h.clear();
-  const std::vector<Range> own = engine_owned(e);
+  d.seq.clear();
   cudaStream_t cs = e->copy_stream;
   trace_mark(e, cs, "dl_enq");
+  const std::vector<Range> own = engine_owned(e);
   HS_CUDA(cudaStreamWaitEvent(cs, e->reduced ? e->ev_s_red : e->ev_s_done, 0));
   for (const Range& o : own) {
     HS_CUDA(cudaMemcpyAsync(e->host_stage + e->cap_pk + (o.first - e->pk0), e->Sp + (o.first - e->pk0),
                             (o.second - o.first) * sizeof(double2), cudaMemcpyDeviceToHost, cs));
-    d.s.push_back({o.first, o.second, e->ev_dl_s});
+    d.seq.push_back({0, o.first, o.second, e->ev_dl_s});
   }
   HS_CUDA(cudaEventRecord(e->ev_dl_s, cs));
   trace_mark(e, cs, "dl_s");
@@ -297,7 +296,7 @@ void enqueue_download(hsdla_b200_engine* e) {
       if (b1 <= b0) continue;
       HS_CUDA(cudaMemcpyAsync(e->host_stage + (b0 - e->pk0), e->Hp + (b0 - e->pk0), (b1 - b0) * sizeof(double2),
                               cudaMemcpyDeviceToHost, cs));
-      d.h.push_back({b0, b1, e->ev_dl_h[q]});
+      d.seq.push_back({1, b0, b1, e->ev_dl_h[q]});
     }
     HS_CUDA(cudaEventRecord(e->ev_dl_h[q], cs));
     trace_mark(e, cs, "dl_h" + std::to_string(q));
@@ -319,34 +318,37 @@ void finish_download(hsdla_b200_engine* e, double* H, double* S, std::chrono::st
   // unpack reads it unless demoted (host_pool.cpp); HSDLA_B200_STAGE_DEMOTE_MB overrides
   static const double demote_mb = env_double("HSDLA_B200_STAGE_DEMOTE_MB", 48.0);
   uint64_t stage_elems = 0;
-  for (const DlPiece& p : d.s) stage_elems += p.b1 - p.b0;
-  for (const DlPiece& p : d.h) stage_elems += p.b1 - p.b0;
+  for (const DlPiece& p : d.seq) stage_elems += p.b1 - p.b0;
   const bool release = static_cast<double>(stage_elems) * sizeof(double2) < demote_mb * (1 << 20);
-  HS_CUDA(cudaEventSynchronize(e->ev_dl_s));
-  mark("s_landed");
-  if (S)
-    for (const DlPiece& p : d.s)
-      unpack_range(e->host_stage + e->cap_pk + (p.b0 - d.pk0), reinterpret_cast<double2*>(S), d.ng, p.b0, p.b1,
-                   release);
-  mark("s_unpacked");
-  // H piece by piece as the pieces land; consecutive pieces that have all landed by the
-  // time the first is waited for are unpacked in ONE pass over the host pool (an unbanded
-  // build's pieces all land together: one 16-thread unpack instead of eight small ones)
+  // Pieces in landing order; consecutive pieces of the same matrix that are contiguous (either
+  // direction) and have all landed by the time the first is waited for are unpacked in ONE
+  // pass over the host pool (an unbanded build's eight H pieces land together: one 16-thread
+  // unpack instead of eight small ones)
   auto landed = [](cudaEvent_t ev) {
     const cudaError_t r = cudaEventQuery(ev);
     if (r == cudaSuccess) return true;
     if (r != cudaErrorNotReady) HS_CUDA(r);
     return false;
   };
-  for (size_t i = 0; i < d.h.size();) {
-    HS_CUDA(cudaEventSynchronize(d.h[i].ready));
-    mark("h_landed");
+  for (size_t i = 0; i < d.seq.size();) {
+    HS_CUDA(cudaEventSynchronize(d.seq[i].ready));
+    mark(d.seq[i].h ? "h_landed" : "s_landed");
+    uint64_t lo = d.seq[i].b0, hi = d.seq[i].b1;
     size_t j = i + 1;
-    while (j < d.h.size() && d.h[j].b0 == d.h[j - 1].b1 && (d.h[j].ready == d.h[i].ready || landed(d.h[j].ready)))
-      ++j;
-    if (H)
-      unpack_range(e->host_stage + (d.h[i].b0 - d.pk0), reinterpret_cast<double2*>(H), d.ng, d.h[i].b0,
-                   d.h[j - 1].b1, release);
+    for (; j < d.seq.size(); ++j) {
+      const DlPiece& q = d.seq[j];
+      if (q.h != d.seq[i].h || !(q.ready == d.seq[i].ready || landed(q.ready))) break;
+      if (q.b0 == hi)
+        hi = q.b1;
+      else if (q.b1 == lo)
+        lo = q.b0;
+      else
+        break;
+    }
+    double* dst = d.seq[i].h ? H : S;
+    if (dst)
+      unpack_range(e->host_stage + (d.seq[i].h ? 0 : e->cap_pk) + (lo - d.pk0), reinterpret_cast<double2*>(dst), d.ng,
+                   lo, hi, release);
     i = j;
   }
   HS_CUDA(cudaEventSynchronize(e->ev_dl_h[hsdla_b200_engine::kD2hPieces - 1]));
