@@ -569,7 +569,7 @@ static void upload_atoms_staged(hsdla_b200_engine* e, int set, const hsdla_b200_
     }
     // pack pieces of ~1/div of the matrix (1 MB .. one slab): the DMA of piece i overlaps
     // the packing of piece i+1
-    static const double div = std::max(1.0, env_double("HSDLA_B200_PIECE_DIV", 1.0));
+    static const double div = std::max(1.0, env_double("HSDLA_B200_PIECE_DIV", 4.0));
     const uint64_t piece = std::min<uint64_t>(kStageSlab, std::max<uint64_t>(uint64_t(1) << 20,
                                               static_cast<uint64_t>(static_cast<double>(colb * cols) / div)));
     const uint64_t per = std::max<uint64_t>(1, piece / colb);

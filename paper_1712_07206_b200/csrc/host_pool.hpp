@@ -150,11 +150,11 @@ inline void copy_nt(void* dst, const void* src, size_t bytes) {
 }
 
 // fn(i) for i in [0, n), in `parts` contiguous ranges on the host pool when the work
-// is large (>= 4 MB), else inline.
+// is large (>= 1 MB; >= 256 KB per part), else inline.
 template <class F>
 void par_for(uint64_t n, uint64_t bytes, F&& fn) {
   HostPool& pool = HostPool::get();
-  const uint64_t parts = bytes < (size_t(4) << 20) ? 1 : std::min<uint64_t>(pool.width(), n);
+  const uint64_t parts = bytes < (size_t(1) << 20) ? 1 : std::min<uint64_t>({pool.width(), n, bytes >> 18});
   if (parts <= 1) {
     for (uint64_t i = 0; i < n; ++i) fn(i);
     return;
