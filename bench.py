@@ -9,9 +9,10 @@ synthetic problem (generate_problem, seed 1: the reference generator, bit-identi
 Default workload = BASELINE.json configs[1] ("NaCl-like cell: 64 atoms, lmax=8, N_G~3000,
 single k-point on 1 B200") = (64, 81, 3000).
 
-Multi-GPU (torchrun, one process per GPU): ONE problem is atom-sharded over the N ranks
-(each rank generates only its shard, generate_problem_shard) and the partial packed H, S are
-summed with NCCL inside the timed region (the path's one exchange step):
+Multi-GPU (torchrun, one process per GPU): the K = N_A N_L rows of ONE problem are split
+evenly over the N ranks (shard_rows: each rank holds the atoms its rows touch and generates only
+those, generate_problem_shard) and the partial packed H, S are summed with NCCL inside the timed
+region (the path's one exchange step):
   --scaling weak   (default) the problem has 64 N atoms of config c2 -- fixed work per GPU;
   --scaling strong the config's own atom count split N ways (BASELINE configs[2..3]: c3 at
                    N = 1/2/4/8, c4 at N = 8) -- fixed total work.
@@ -452,14 +453,14 @@ def run_b200(args):
             "scaling": args.scaling if P > 1 else "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (generate_problem seed 1, bit-identical to the reference generator; each rank "
-                    "generates its own atom shard)",
+                    "generates the atoms of its K-row shard)",
             "config": {"workload": f"{args.config}: {desc}", "n_atoms": na_total, "n_atoms_per_gpu": na_total / P,
                        "n_l": nl, "n_g": ng, "algo": args.algo,
                        "arith": args.arith + (" (Gauss 3-multiplication complex products: 6 executed real "
                                               "flops per complex MAC, all FP64; value counts the reference "
                                               "ledger's 8)" if args.arith == "3m" else " (4 real DMMAs per "
                                               "complex MAC)"),
-                       "parallelism": f"atom-sharded x{P}" + (f" + NCCL {'reduce-scatter' if args.reduce == 'scatter' else 'reduce'}"
+                       "parallelism": f"K-row-sharded x{P}" + (f" + NCCL {'reduce-scatter' if args.reduce == 'scatter' else 'reduce'}"
                                                               f" of packed H,S (timed)" if multi else ""),
                        "l2": f"inputs A,B {2 * na * nl * ng * 16 / 1e6:.0f} MB per GPU > 126 MB L2 (no flush)"},
             "build_ms": ms,

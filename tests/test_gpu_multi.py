@@ -319,7 +319,7 @@ def test_multigpu_dropin_config1_full_vs_reference(reduce):
 
 
 def test_multigpu_dropin_config3_sampled(restatement):
-    """Config 3 (108 atoms, N_L 121, N_G 6000) atom-sharded over every GPU: principal-submatrix
+    """Config 3 (108 atoms, N_L 121, N_G 6000) K-row-sharded over every GPU: principal-submatrix
     sampling against the oracle on the J-sliced problem."""
     _need_gpus(2)
     P = hb.device_count()

@@ -43,6 +43,21 @@ def test_oracle_sph_bessel_vs_scipy(restatement, x):
     assert np.all(np.abs(j - ref)[big] / scale[big] < 1e-12)
 
 
+@pytest.mark.parametrize("n", [1, 2, 3, 4])
+@pytest.mark.parametrize("d", [-1e-6, -1e-9, 0.0, 1e-9, 1e-6])
+def test_oracle_sph_bessel_next_to_zeros_of_j0(restatement, n, d):
+    """x = n pi + d: j_0 vanishes there, so a downward recurrence normalised by j_0 alone loses
+    every digit (3e-4 relative at 2 pi + 1e-12); normalising by the larger of |j_0|, |j_1| keeps
+    the 1e-12 bar (the GPU kernel uses the same normalisation, lapw_setup.cuh)."""
+    x = n * np.pi + d
+    j = restatement.sph_bessel(13, x)
+    ref = sps.spherical_jn(np.arange(14), x)
+    big = np.abs(ref) > 1e-200
+    # j_0 itself is ~|d| / x next to its zero: compare it absolutely
+    assert abs(j[0] - ref[0]) <= 1e-15
+    assert np.all(np.abs(j - ref)[1:][big[1:]] / np.abs(ref[1:][big[1:]]) < 1e-12)
+
+
 def _matching_residual(s, A, B, a, lm, g):
     """|A u + B udot - c j_l(KR)| and |A u' + B udot' - c K j_l'(KR)| with scipy values."""
     l = int(np.floor(np.sqrt(lm)))
@@ -98,6 +113,28 @@ def test_gpu_coefficients_vs_oracle(restatement, dims):
     rel = lambda x, y: np.linalg.norm(x - y) / max(np.linalg.norm(y), 1e-300)
     assert rel(A, Ar) <= 1e-13 and rel(B, Br) <= 1e-13
     assert np.array_equal(U, Ur)
+
+
+@pytest.mark.gpu
+def test_gpu_coefficients_next_to_zeros_of_j0(restatement):
+    """Muffin-tin radii set so that |k+G| R_mt = pi + 1e-9 and 2 pi - 1e-9 for two G vectors (the
+    zeros of j_0, where the j_l recurrence needs the j_0 / j_1 normalisation): the GPU coefficients
+    equal the oracle's and satisfy the matching conditions with scipy's j_l there."""
+    s = hb.make_lapw_system(4, 8, 80, n_types=2, seed=7)
+    kn = np.linalg.norm(s.kpt + s.gvec, axis=1)
+    g1, g2 = 5, 41
+    s.rmt = np.array([(np.pi + 1e-9) / kn[g1], (2 * np.pi - 1e-9) / kn[g2]])
+    A, B, U = hb.lapw_coefficients(s)
+    Ar, Br, Ur = restatement.lapw_coefficients(s)
+    rel = lambda x, y: np.linalg.norm(x - y) / max(np.linalg.norm(y), 1e-300)
+    assert rel(A, Ar) <= 1e-13 and rel(B, Br) <= 1e-13
+    for g, t in ((g1, 0), (g2, 1)):
+        for a in range(s.n_atoms):
+            if s.atom_type[a] != t:
+                continue
+            for lm in range(s.n_l):
+                r1, r2, c = _matching_residual(s, A, B, a, lm, g)
+                assert r1 <= 1e-12 * max(c, 1e-3) + 1e-15 and r2 <= 1e-12 * max(c, 1e-3) + 1e-15, (g, a, lm)
 
 
 @pytest.mark.gpu
