@@ -350,7 +350,11 @@ void ensure_streamed_plans(hsdla_b200_engine* e) {
   const auto b = stream_bounds(e->na, e->nl, e->ncol, 50e9);
   e->streamed.resize(b.size() - 1);
   for (size_t c = 0; c + 1 < b.size(); ++c) make_chunk(e, 0, b[c], b[c + 1], c == 0, e->streamed[c]);
-  const auto bp = stream_bounds(e->na, e->nl, e->ncol, 20e9);
+  // host-packed feeds (pageable rows, HSDL files from the page cache) deliver ~44 GB/s at C2
+  // (pack and DMA pipelined): chunks grow more slowly so each upload still hides under the
+  // previous chunk's compute (tools/small_probe.py, C2 pageable: 4,6,10,15,29 atoms 20.8 ms
+  // per call against 21.4 with the page-locked plan 4,9,20,31)
+  const auto bp = stream_bounds(e->na, e->nl, e->ncol, env_double("HSDLA_B200_PAGEABLE_RATE", 35e9));
   e->streamed_pg.resize(bp.size() - 1);
   for (size_t c = 0; c + 1 < bp.size(); ++c) make_chunk(e, 0, bp[c], bp[c + 1], c == 0, e->streamed_pg[c]);
   while (e->ev_chunk_up.size() < std::max(e->streamed.size(), e->streamed_pg.size())) {
@@ -877,11 +881,10 @@ void engine_build_streamed(hsdla_b200_engine* e, const hsdla_b200_problem* p, ui
   trace_mark(e, e->copy_stream, "up_start");
   const uint64_t ab_bytes = p->n_atoms * p->n_l * p->n_g * sizeof(double2);
   const bool pinned = is_pinned(p->A, ab_bytes) && is_pinned(p->B, ab_bytes);
-  // pageable rows are packed into pinned slabs at ~60 GB/s (copy_nt) and DMA'd from there,
-  // a feed close to page-locked inputs, so both use the same plan (HSDLA_B200_PAGEABLE_PLAN=pg:
-  // the slower-feed plan the HSDL file path uses)
+  // pageable rows are packed into pinned slabs by the host pool and DMA'd from there: the
+  // host-packed plan (HSDLA_B200_PAGEABLE_PLAN=pinned: the page-locked one)
   const char* pgp = std::getenv("HSDLA_B200_PAGEABLE_PLAN");
-  auto& plan = pinned || !(pgp && std::strcmp(pgp, "pg") == 0) ? e->streamed : e->streamed_pg;
+  auto& plan = pinned || (pgp && std::strcmp(pgp, "pinned") == 0) ? e->streamed : e->streamed_pg;
   // The first chunk's S starts with its A^H A half as soon as A's rows landed, hiding part
   // of the one upload nothing can overlap (not for the original algorithm, whose first
   // phase needs B and T; HSDLA_B200_SPLIT_S=0 disables it for comparisons)

@@ -222,10 +222,10 @@ void engine_build_file(hsdla_b200_engine* e, const char* path, uint64_t a0, int 
   ensure_streamed_plans(e);
   HS_CUDA(cudaStreamWaitEvent(e->copy_stream, e->ev_end, 0));
   HS_CUDA(cudaEventRecord(e->ev_up0, e->copy_stream));
-  // the mapped file view feeds ~36-42 GB/s (copy_nt from the page cache), close to the
-  // page-locked feed; HSDLA_B200_FILE_PLAN=pg selects the slower-feed plan (pread fallback)
+  // the mapped file view feeds ~36-42 GB/s (copy_nt from the page cache): the host-packed
+  // plan; HSDLA_B200_FILE_PLAN=pinned selects the page-locked one
   const char* fpl = std::getenv("HSDLA_B200_FILE_PLAN");
-  auto& plan = fpl && std::strcmp(fpl, "pg") == 0 ? e->streamed_pg : e->streamed;
+  auto& plan = fpl && std::strcmp(fpl, "pinned") == 0 ? e->streamed : e->streamed_pg;
   for (size_t c = 0; c < plan.size(); ++c) {
     load_atoms_from_file(e, f.fd, h, a0, plan[c].a0, plan[c].a1, e->copy_stream);
     HS_CUDA(cudaEventRecord(e->ev_chunk_up[c], e->copy_stream));
