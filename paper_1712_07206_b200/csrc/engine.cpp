@@ -442,7 +442,6 @@ hsdla_b200_engine* engine_create(int device, const ShardSpec& sp) {
     dalloc(e.get(), &e->Hp, e->cap_pk);
     dalloc(e.get(), &e->Sp, e->cap_pk);
     HS_CUDA(cudaDeviceGetAttribute(&e->sms, cudaDevAttrMultiProcessorCount, device));
-    if (const int cap = static_cast<int>(env_double("HSDLA_B200_SMS", 0))) e->sms = std::min(e->sms, cap);  // tuning
     dalloc(e.get(), &e->sk_ws, static_cast<uint64_t>(e->sms) * kSkSlot);
     dalloc(e.get(), &e->sk_flags, static_cast<uint64_t>(e->sms));
     HS_CUDA(cudaMemset(e->sk_flags, 0, e->sms * sizeof(uint32_t)));
