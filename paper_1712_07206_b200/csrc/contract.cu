@@ -1,6 +1,7 @@
 // The contraction-engine instantiations (ctn_contract.cuh) and their host launchers.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 #include <string>
@@ -64,16 +65,59 @@ static decltype(&ctn_contract_kernel<kBatch, kBatBM, kBatBN, 1, 8, kBatStages>) 
     ctn_contract_kernel<kBatch, kBatBM, kBatBN, 1, 8, kBatStages, 1, 1>,
     ctn_contract_kernel<kBatch, kBatBM, kBatBN, 1, 8, kBatStages, 1, 0>};
 
+// diagonal tiles: their own launch with the warp remapping (ctn_contract.cuh kDiagRemap)
+static decltype(&ctn_contract_kernel<kTriDiag, kTriBM, kTriBM, 2, 4, kTriStages>) const diag_kernels[2] = {
+    ctn_contract_kernel<kTriDiag, kTriBM, kTriBM, 2, 4, kTriStages, 1, 1>,
+    ctn_contract_kernel<kTriDiag, kTriBM, kTriBM, 2, 4, kTriStages, 1, 0>};
+
 void set_kernel_attributes() {
   for (int a = 0; a < 2; ++a) {
     HS_CUDA(cudaFuncSetAttribute(tri_kernels[a], cudaFuncAttributeMaxDynamicSharedMemorySize, TriCfg::kSmemBytes));
+    HS_CUDA(cudaFuncSetAttribute(diag_kernels[a], cudaFuncAttributeMaxDynamicSharedMemorySize, TriCfg::kSmemBytes));
     HS_CUDA(cudaFuncSetAttribute(bat_kernels[a], cudaFuncAttributeMaxDynamicSharedMemorySize, BatCfg::kSmemBytes));
     HS_CUDA(cudaFuncSetAttribute(batw_kernels[a], cudaFuncAttributeMaxDynamicSharedMemorySize, BatWCfg::kSmemBytes));
   }
 }
 
+// One lower-triangular contraction = two launches on `s`: the strictly-lower tiles, then the
+// diagonal tiles (warp-remapped: a diagonal tile costs 10 / 16 of a full one); small triangles
+// one launch over every lower tile.  P describes the
+// whole set (tiles_total counts the diagonal); grid.x bounds both grids.  Each launch gets its
+// own stream-K flag generation (2 epoch, 2 epoch + 1).
 void launch_tri_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStream_t s) {
-  tri_kernels[arith]<<<grid, TriCfg::kThreads, TriCfg::kSmemBytes, s>>>(P);
+  int iters = 0;
+  for (int sg = 0; sg < P.nseg; ++sg) iters += P.kchunks[sg];
+  const int t0 = P.col_t1 > 0 ? P.col_t0 : 0, ndiag = P.col_t1 > 0 ? P.col_t1 - P.col_t0 : P.tiles;
+  const int nstrict = P.tiles_total - ndiag;
+  auto grid_of = [&](int tiles) {
+    return dim3(static_cast<unsigned>(std::max<long long>(1, std::min<long long>(grid.x, 1LL * tiles * iters))));
+  };
+  // A separate diagonal launch saves 6/16 of the diagonal tiles' work, ~0.375 x ndiag x iters
+  // k-slabs over the GPU, and costs a launch (~10 us): below ~8000 tile-slabs (C1: 16 x 196) the
+  // triangle runs as ONE launch over every lower tile (measured: C1 0.42 ms in one launch, 0.46 split;
+  // C2 17.96 -> 17.77 ms split)
+  static const double split_min = env_double("HSDLA_B200_DIAG_SPLIT_MIN", 8000);
+  if (1.0 * ndiag * iters < split_min) {
+    CtnParams q = P;
+    q.with_diag = 1;
+    q.epoch = 2 * P.epoch;
+    tri_kernels[arith]<<<grid_of(P.tiles_total), TriCfg::kThreads, TriCfg::kSmemBytes, s>>>(q);
+    HS_CUDA(cudaGetLastError());
+    return;
+  }
+  if (nstrict > 0) {
+    CtnParams q = P;
+    q.tiles_total = nstrict;
+    q.with_diag = 0;
+    q.epoch = 2 * P.epoch;
+    tri_kernels[arith]<<<grid_of(nstrict), TriCfg::kThreads, TriCfg::kSmemBytes, s>>>(q);
+    HS_CUDA(cudaGetLastError());
+  }
+  CtnParams d = P;
+  d.tiles_total = ndiag;
+  d.diag_t0 = t0;
+  d.epoch = 2 * P.epoch + 1;
+  diag_kernels[arith]<<<grid_of(ndiag), TriCfg::kThreads, TriCfg::kSmemBytes, s>>>(d);
   HS_CUDA(cudaGetLastError());
 }
 

@@ -34,6 +34,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "ctn_params.hpp"
 
 namespace hsdla_b200 {
@@ -116,11 +118,10 @@ __device__ __forceinline__ void tri_tile(int t, int tiles, int kBand, int& ti, i
   ti = r0 + c + u;
 }
 
-// Tile t of the lower tiles restricted to tile columns [c0, c1): the triangle of rows
-// c0 .. c1-1 first (row by row), then the full-width rows c1 .. (w = c1 - c0 tiles each).
-// A column band of tiles covers a contiguous range of packed-lower storage, so a
-// build's final H contraction can run band by band with each band's download
-// overlapping the next band's compute.
+// Tile t of the lower tiles (diagonal included) restricted to tile columns [c0, c1): the triangle
+// of rows c0 .. c1-1 first (row by row), then the full-width rows c1 .. (w = c1 - c0 tiles each).
+// A column band of tiles covers a contiguous range of packed-lower storage, so a build's final H
+// contraction can run band by band with each band's download overlapping the next band's compute.
 __device__ __forceinline__ void tri_tile_cols(int t, int c0, int c1, int& ti, int& tj) {
   const int w = c1 - c0, tri = w * (w + 1) / 2;
   if (t < tri) {
@@ -128,6 +129,29 @@ __device__ __forceinline__ void tri_tile_cols(int t, int c0, int c1, int& ti, in
     while ((r + 1) * (r + 2) / 2 <= t) ++r;
     while (r * (r + 1) / 2 > t) --r;
     ti = c0 + r;
+    tj = c0 + t - r * (r + 1) / 2;
+  } else {
+    const int u = t - tri;
+    ti = c1 + u / w;
+    tj = c0 + u % w;
+  }
+}
+
+// Tile t of the STRICTLY lower tiles (ti > tj) restricted to tile columns [c0, c1) (c1 == 0:
+// all T columns, grouped order of tri_tile): the triangle of rows c0+1 .. c1-1, then the full
+// rows c1 .. (w = c1 - c0 tiles each).  The diagonal tiles run in a launch of their own.
+__device__ __forceinline__ void tri_tile_strict(int t, int T, int c0, int c1, int kBand, int& ti, int& tj) {
+  if (c1 <= 0) {  // the whole triangle: the lower tiles of the (T-1)-grid, one row down
+    tri_tile(t, T - 1, kBand, ti, tj);
+    ++ti;
+    return;
+  }
+  const int w = c1 - c0, tri = w * (w - 1) / 2;
+  if (t < tri) {
+    int r = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);  // row r + 1 of the window triangle
+    while ((r + 1) * (r + 2) / 2 <= t) ++r;
+    while (r * (r + 1) / 2 > t) --r;
+    ti = c0 + 1 + r;
     tj = c0 + t - r * (r + 1) / 2;
   } else {
     const int u = t - tri;
@@ -230,6 +254,23 @@ __device__ __forceinline__ void consumer_bar(int nthreads) {
   asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
 
+// Fragment masks of a warp tile (bit mb * NB + nb: the 8 x 8 fragment (mb, nb) is computed).
+__host__ __device__ constexpr bool frag_on(unsigned m, int mb, int nb, int NB) { return (m >> (mb * NB + nb)) & 1u; }
+__host__ __device__ constexpr bool row_on(unsigned m, int mb, int NB) {
+  return ((m >> (mb * NB)) & ((1u << NB) - 1u)) != 0;
+}
+__host__ __device__ constexpr bool col_on(unsigned m, int nb, int MB, int NB) {
+  for (int mb = 0; mb < MB; ++mb)
+    if (frag_on(m, mb, nb, NB)) return true;
+  return false;
+}
+// Diagonal TRI tiles (64 x 64, 8 warps of 32 x 16): of the 8 x 8 fragments only the 36 on or below
+// the diagonal carry output.  Roles by warp tile (wm, wn): (1,0), (1,1) all 8 fragments; (0,0),
+// (1,2) the 7 with mb >= nb; (0,1), (1,3) the 3 with mb >= nb + 2; (0,2), (0,3) none.  The warps
+// are re-assigned so the two warps of each SM sub-partition (w, w + 4) carry 8 / 8 / 10 / 10
+// fragments instead of 7 / 15 / 3 / 11: the tile takes 10 / 16 of a full tile's DMMA time.
+constexpr unsigned kMaskFull = 0xFFu, kMaskTri7 = 0xFDu, kMaskTri3 = 0xD0u, kMaskNone = 0u;
+
 // G3M = 0: four real DMMAs per complex MAC (8 flops, plain FP64 rounding).
 // G3M = 1: Gauss's three-multiplication complex product (the ZGEMM3M scheme, 6 executed
 //   flops per complex MAC): per k, t1 += a_r b_r, t2 += a_i b_i, t3 += (a_r - a_i)(b_r + b_i),
@@ -269,13 +310,21 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES,
     if (s < P.nseg) iters += P.kchunks[s];
 
   // tile coordinates of a piece
+  constexpr bool kTriLike = MODE != kBatch;
   auto tile_origin = [&](int tile, int& row0, int& col0, int& atom) {
-    if (MODE == kTri) {
+    if (MODE == kTriDiag) {
+      row0 = col0 = (P.diag_t0 + tile) * BM;
+      atom = 0;
+    } else if (MODE == kTri) {
       int ti, tj;
-      if (P.col_t1 > 0)
-        tri_tile_cols(tile, P.col_t0, P.col_t1, ti, tj);
-      else
-        tri_tile(tile, P.tiles, P.band, ti, tj);
+      if (P.with_diag) {
+        if (P.col_t1 > 0)
+          tri_tile_cols(tile, P.col_t0, P.col_t1, ti, tj);
+        else
+          tri_tile(tile, P.tiles, P.band, ti, tj);
+      } else {
+        tri_tile_strict(tile, P.tiles, P.col_t0, P.col_t1, P.band, ti, tj);
+      }
       row0 = ti * BM;
       col0 = tj * BN;
       atom = 0;
@@ -300,8 +349,8 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES,
       TriSched sched(P.tiles_total, iters, gridDim.x, blockIdx.x);
       Piece pc;
       int bt = blockIdx.x;  // BATCH: tiles blockIdx.x, + gridDim.x, ...
-      bool have = MODE == kTri ? sched.next(pc) : bt < P.bat_tiles;
-      if (MODE != kTri) pc = Piece{bt, 0, iters, 0};
+      bool have = kTriLike ? sched.next(pc) : bt < P.bat_tiles;
+      if (!kTriLike) pc = Piece{bt, 0, iters, 0};
       int it = 0;
       while (have) {
         int row0, col0, atom;
@@ -322,7 +371,7 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES,
             uint8_t* sR = smem + slot * Cfg::kStageBytes + Cfg::kStageL + u * Cfg::kSubR;
             const int x = kc * 2 * kChunkC;
             // TRI: operand columns are held from global column g0 on (column windows)
-            const int lr = MODE == kTri ? row0 - P.g0 : row0, lc = MODE == kTri ? col0 - P.g0 : col0;
+            const int lr = kTriLike ? row0 - P.g0 : row0, lc = kTriLike ? col0 - P.g0 : col0;
             if (P.l_row_z[seg])
               tma_load_3d(sL, &P.L[seg], x, atom, lr, &full[slot]);
             else
@@ -334,7 +383,7 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES,
             ++kc;
           }
         }
-        if (MODE == kTri) {
+        if (kTriLike) {
           have = sched.next(pc);
         } else {
           bt += gridDim.x;
@@ -349,27 +398,38 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES,
   // ======================= DMMA consumers =================================
   if (PW == 4) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(Cfg::kConsumerRegs) : "memory");
   const int ctid = threadIdx.x;  // 0 .. NCT-1
-  const int wm = warp % WARPS_M;
-  const int wn = warp / WARPS_M;
   const int g = lane >> 2;
   const int q = lane & 3;
   const int pg = ((g & 1) << 2) | (g >> 1);  // smem row permutation (bank-conflict-free LDS.128)
+  constexpr bool kDiagRemap = MODE == kTriDiag && WARPS_M == 2 && WARPS_N == 4 && MB == 4 && NB == 2;
 
   uint32_t offL[MB], offR[NB], offK[2];
-#pragma unroll
-  for (int mb = 0; mb < MB; ++mb) offL[mb] = (wm * Cfg::kWM + 8 * mb + pg) * 128;
-#pragma unroll
-  for (int nb = 0; nb < NB; ++nb) offR[nb] = Cfg::kStageL + (wn * Cfg::kWN + 8 * nb + pg) * 128;  // sub-slab 0
 #pragma unroll
   for (int kk = 0; kk < 2; ++kk) offK[kk] = ((4 * kk + q) ^ pg) << 4;
 
   TriSched sched(P.tiles_total, iters, gridDim.x, blockIdx.x);
   Piece pc;
   int bt = blockIdx.x;
-  bool have = MODE == kTri ? sched.next(pc) : bt < P.bat_tiles;
-  if (MODE != kTri) pc = Piece{bt, 0, iters, 0};
+  bool have = kTriLike ? sched.next(pc) : bt < P.bat_tiles;
+  if (!kTriLike) pc = Piece{bt, 0, iters, 0};
   int it = 0;
   while (have) {
+    // this tile's warp tile (wm, wn) and fragment role (0 all, 1 / 2 / 3: the diagonal-tile masks)
+    int wm = warp % WARPS_M, wn = warp / WARPS_M, role = 0;
+    if (kDiagRemap) {
+      {
+        // warp -> (wm, wn, role) = w0 (1,0,full) w1 (1,1,full) w2 (0,0,tri7) w3 (1,2,tri7)
+        // w4 (0,2,none) w5 (0,3,none) w6 (0,1,tri3) w7 (1,3,tri3); warps w and w + 4 share an SM
+        // sub-partition.  Bit-packed tables (an indexed constant array would live in local memory).
+        wm = (0x8Bu >> warp) & 1u;
+        wn = (0xDE84u >> (2 * warp)) & 3u;
+        role = (0xAF50u >> (2 * warp)) & 3u;
+      }
+    }
+#pragma unroll
+    for (int mb = 0; mb < MB; ++mb) offL[mb] = (wm * Cfg::kWM + 8 * mb + pg) * 128;
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) offR[nb] = Cfg::kStageL + (wn * Cfg::kWN + 8 * nb + pg) * 128;  // sub-slab 0
     double acc[MB][NB][2][NS];  // [mb][nb][e][re, im] or [t1, t2, t3]
 #pragma unroll
     for (int mb = 0; mb < MB; ++mb)
@@ -387,59 +447,6 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES,
       double2 a[MB], b[NB];
       double sa[G3M ? MB : 1], sb[G3M ? NB : 1];  // 3M: a_r - a_i, b_r + b_i
     };
-    auto load_frag = [&](Frag& f, const uint8_t* st, int u, int kk) {
-      const uint32_t base = smem_u32(st) + offK[kk];
-#pragma unroll
-      for (int mb = 0; mb < MB; ++mb) f.a[mb] = lds128(base + u * Cfg::kSubL + offL[mb]);
-#pragma unroll
-      for (int nb = 0; nb < NB; ++nb) f.b[nb] = lds128(base + u * Cfg::kSubR + offR[nb]);
-    };
-    // 3M operand sums, formed one step ahead of their use (off the DMMA issue path)
-    auto sum_frag = [&](Frag& f) {
-      if (G3M) {
-#pragma unroll
-        for (int mb = 0; mb < MB; ++mb) f.sa[mb] = f.a[mb].x - f.a[mb].y;
-#pragma unroll
-        for (int nb = 0; nb < NB; ++nb) f.sb[nb] = f.b[nb].x + f.b[nb].y;
-      }
-    };
-    auto mma_frag = [&](const Frag& f) {
-      if (G3M) {
-        // three independent sweeps (t3, t1, t2) so consecutive DMMAs never share an
-        // accumulator; the operand sums were formed one step ahead (sum_frag)
-#pragma unroll
-        for (int mb = 0; mb < MB; ++mb)
-#pragma unroll
-          for (int nb = 0; nb < NB; ++nb)
-            dmma(acc[mb][nb][0][NS - 1], acc[mb][nb][1][NS - 1], f.sa[mb], f.sb[nb]);
-#pragma unroll
-        for (int mb = 0; mb < MB; ++mb)
-#pragma unroll
-          for (int nb = 0; nb < NB; ++nb) dmma(acc[mb][nb][0][0], acc[mb][nb][1][0], f.a[mb].x, f.b[nb].x);
-#pragma unroll
-        for (int mb = 0; mb < MB; ++mb)
-#pragma unroll
-          for (int nb = 0; nb < NB; ++nb) dmma(acc[mb][nb][0][1], acc[mb][nb][1][1], f.a[mb].y, f.b[nb].y);
-        return;
-      }
-      // Four independent sweeps so consecutive DMMAs never share an accumulator.
-#pragma unroll
-      for (int mb = 0; mb < MB; ++mb)
-#pragma unroll
-        for (int nb = 0; nb < NB; ++nb) dmma(acc[mb][nb][0][0], acc[mb][nb][1][0], f.a[mb].x, f.b[nb].x);
-#pragma unroll
-      for (int mb = 0; mb < MB; ++mb)
-#pragma unroll
-        for (int nb = 0; nb < NB; ++nb) dmma(acc[mb][nb][0][1], acc[mb][nb][1][1], f.a[mb].x, f.b[nb].y);
-#pragma unroll
-      for (int mb = 0; mb < MB; ++mb)
-#pragma unroll
-        for (int nb = 0; nb < NB; ++nb) dmma(acc[mb][nb][0][0], acc[mb][nb][1][0], f.a[mb].y, f.b[nb].y);
-#pragma unroll
-      for (int mb = 0; mb < MB; ++mb)
-#pragma unroll
-        for (int nb = 0; nb < NB; ++nb) dmma(acc[mb][nb][0][1], acc[mb][nb][1][1], f.a[mb].y, -f.b[nb].x);
-    };
     // BATCH: k-slab c is the last of a segment whose length leaves <= 4 valid k in it
     auto half_pad = [&](int c) {
       bool h = false;
@@ -452,57 +459,138 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES,
         }
       return h;
     };
-    if (pc.k1 > pc.k0) {
-      Frag f0, f1;
-      {
-        const int slot = it % STAGES;
-        mbar_wait(&full[slot], (it / STAGES) & 1);
-        load_frag(f0, smem + slot * Cfg::kStageBytes, 0, 0);
-        sum_frag(f0);
-      }
-      for (int c = pc.k0; c < pc.k1; c += KSUB, ++it) {
-        const int n = min(KSUB, pc.k1 - c);
-        const int slot = it % STAGES;
-        const uint8_t* st = smem + slot * Cfg::kStageBytes;
-        if (MODE == kBatch && KSUB == 1 && half_pad(c)) {
-          // the segment's last slab holds <= 4 valid k: its second half (kk = 1) is TMA
-          // zero-fill, so only the first half's DMMAs issue (N_L = 81: 84 of 88 k per segment)
-          mma_frag(f0);
-          if (c + 1 < pc.k1) {
-            const int nslot = (it + 1) % STAGES;
-            mbar_wait(&full[nslot], ((it + 1) / STAGES) & 1);
-            load_frag(f0, smem + nslot * Cfg::kStageBytes, 0, 0);
-            sum_frag(f0);
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[slot]);
-          continue;
-        }
+    // The k-loop of one piece for fragment mask M (compile time: the loads, operand sums and
+    // DMMAs of fragments outside M are not emitted; a warp with no fragments still takes part in
+    // the stage handshake).
+    auto kloop = [&](auto maskc) {
+      constexpr unsigned M = decltype(maskc)::value;
+      auto load_frag = [&](Frag& f, const uint8_t* st, int u, int kk) {
+        const uint32_t base = smem_u32(st) + offK[kk];
 #pragma unroll
-        for (int u = 0; u < KSUB; ++u) {
-          if (u < n) {
-            load_frag(f1, st, u, 1);
+        for (int mb = 0; mb < MB; ++mb)
+          if (row_on(M, mb, NB)) f.a[mb] = lds128(base + u * Cfg::kSubL + offL[mb]);
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb)
+          if (col_on(M, nb, MB, NB)) f.b[nb] = lds128(base + u * Cfg::kSubR + offR[nb]);
+      };
+      // 3M operand sums, formed one step ahead of their use (off the DMMA issue path)
+      auto sum_frag = [&](Frag& f) {
+        if (G3M) {
+#pragma unroll
+          for (int mb = 0; mb < MB; ++mb)
+            if (row_on(M, mb, NB)) f.sa[mb] = f.a[mb].x - f.a[mb].y;
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb)
+            if (col_on(M, nb, MB, NB)) f.sb[nb] = f.b[nb].x + f.b[nb].y;
+        }
+      };
+      auto mma_frag = [&](const Frag& f) {
+        if (G3M) {
+          // three independent sweeps (t3, t1, t2) so consecutive DMMAs never share an
+          // accumulator; the operand sums were formed one step ahead (sum_frag)
+#pragma unroll
+          for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb)
+              if (frag_on(M, mb, nb, NB)) dmma(acc[mb][nb][0][NS - 1], acc[mb][nb][1][NS - 1], f.sa[mb], f.sb[nb]);
+#pragma unroll
+          for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb)
+              if (frag_on(M, mb, nb, NB)) dmma(acc[mb][nb][0][0], acc[mb][nb][1][0], f.a[mb].x, f.b[nb].x);
+#pragma unroll
+          for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb)
+              if (frag_on(M, mb, nb, NB)) dmma(acc[mb][nb][0][1], acc[mb][nb][1][1], f.a[mb].y, f.b[nb].y);
+          return;
+        }
+        // Four independent sweeps so consecutive DMMAs never share an accumulator.
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb)
+            if (frag_on(M, mb, nb, NB)) dmma(acc[mb][nb][0][0], acc[mb][nb][1][0], f.a[mb].x, f.b[nb].x);
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb)
+            if (frag_on(M, mb, nb, NB)) dmma(acc[mb][nb][0][1], acc[mb][nb][1][1], f.a[mb].x, f.b[nb].y);
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb)
+            if (frag_on(M, mb, nb, NB)) dmma(acc[mb][nb][0][0], acc[mb][nb][1][0], f.a[mb].y, f.b[nb].y);
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb)
+            if (frag_on(M, mb, nb, NB)) dmma(acc[mb][nb][0][1], acc[mb][nb][1][1], f.a[mb].y, -f.b[nb].x);
+      };
+      if (pc.k1 > pc.k0) {
+        Frag f0, f1;
+        {
+          const int slot = it % STAGES;
+          mbar_wait(&full[slot], (it / STAGES) & 1);
+          load_frag(f0, smem + slot * Cfg::kStageBytes, 0, 0);
+          sum_frag(f0);
+        }
+        for (int c = pc.k0; c < pc.k1; c += KSUB, ++it) {
+          const int n = min(KSUB, pc.k1 - c);
+          const int slot = it % STAGES;
+          const uint8_t* st = smem + slot * Cfg::kStageBytes;
+          if (MODE == kBatch && KSUB == 1 && half_pad(c)) {
+            // the segment's last slab holds <= 4 valid k: its second half (kk = 1) is TMA
+            // zero-fill, so only the first half's DMMAs issue (N_L = 81: 84 of 88 k per segment)
             mma_frag(f0);
-            sum_frag(f1);
-            // the next step's fragments: sub-slab u+1 of this stage, or the next stage
-            const bool more = u + 1 < n || c + KSUB < pc.k1;
-            if (u + 1 < n) {
-              load_frag(f0, st, u + 1, 0);
-            } else if (c + KSUB < pc.k1) {
+            if (c + 1 < pc.k1) {
               const int nslot = (it + 1) % STAGES;
               mbar_wait(&full[nslot], ((it + 1) / STAGES) & 1);
               load_frag(f0, smem + nslot * Cfg::kStageBytes, 0, 0);
+              sum_frag(f0);
             }
-            mma_frag(f1);
-            if (more) sum_frag(f0);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[slot]);
+            continue;
           }
+#pragma unroll
+          for (int u = 0; u < KSUB; ++u) {
+            if (u < n) {
+              load_frag(f1, st, u, 1);
+              mma_frag(f0);
+              sum_frag(f1);
+              // the next step's fragments: sub-slab u+1 of this stage, or the next stage
+              const bool more = u + 1 < n || c + KSUB < pc.k1;
+              if (u + 1 < n) {
+                load_frag(f0, st, u + 1, 0);
+              } else if (c + KSUB < pc.k1) {
+                const int nslot = (it + 1) % STAGES;
+                mbar_wait(&full[nslot], ((it + 1) / STAGES) & 1);
+                load_frag(f0, smem + nslot * Cfg::kStageBytes, 0, 0);
+              }
+              mma_frag(f1);
+              if (more) sum_frag(f0);
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[slot]);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);
       }
+    };
+    if constexpr (kDiagRemap) {
+      if (role == 0)
+        kloop(std::integral_constant<unsigned, kMaskFull>{});
+      else if (role == 1)
+        kloop(std::integral_constant<unsigned, kMaskTri7>{});
+      else if (role == 2)
+        kloop(std::integral_constant<unsigned, kMaskTri3>{});
+      else
+        kloop(std::integral_constant<unsigned, kMaskNone>{});
+    } else {
+      kloop(std::integral_constant<unsigned, (1u << (MB * NB)) - 1u>{});
     }
 
-    if (MODE == kTri && pc.kind == 2) {
+    if (kTriLike && pc.kind == 2) {
       // contributor: park the partial, publish the flag
       double* ws = P.sk_ws + static_cast<size_t>(blockIdx.x) * NACC * NCT;
 #pragma unroll
@@ -518,7 +606,7 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES,
       consumer_bar(NCT);
       if (ctid == 0) st_release_u32(P.sk_flags + blockIdx.x, P.epoch);
     } else {
-      if (MODE == kTri && pc.kind == 1) {
+      if (kTriLike && pc.kind == 1) {
         // owner: add the later pieces of this tile, in CTA order (deterministic)
         const long long tile_end = static_cast<long long>(pc.tile - sched.dp_tiles + 1) * sched.I;
         for (int b2 = blockIdx.x + 1; b2 < static_cast<int>(gridDim.x) && sched.start(b2) < tile_end; ++b2) {
@@ -542,12 +630,12 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES,
       int row0, col0, atom;
       tile_origin(pc.tile, row0, col0, atom);
       const double ar = P.alpha_re, ai = P.alpha_im, beta = P.beta;
-      const bool keep_di = MODE == kTri && P.keep_diag_imag != nullptr && *P.keep_diag_imag != 0;
+      const bool keep_di = kTriLike && P.keep_diag_imag != nullptr && *P.keep_diag_imag != 0;
       // destination of accumulator element (mb, nb, e); nullptr outside the output
       auto dst_of = [&](int mb, int nb, int e) -> double2* {
         const int i = row0 + wm * Cfg::kWM + 8 * mb + pg;
         const int j = col0 + wn * Cfg::kWN + 8 * nb + (e ? 4 + q : q);
-        if (MODE == kTri) return (i < P.n && j < P.n && i >= j) ? P.out + (packed_index(P.n, i, j) - P.pk0) : nullptr;
+        if (kTriLike) return (i < P.n && j < P.n && i >= j) ? P.out + (packed_index(P.n, i, j) - P.pk0) : nullptr;
         if (i >= P.m_valid || j >= P.n) return nullptr;
         const int mr = P.m_row ? P.m_row : P.m_valid;
         const bool hi = i >= mr;  // stacked W: rows [m_row, m_valid) are W_B's, in out2
@@ -597,7 +685,7 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES,
               const double xr = x[mb][nb][e].x, xi = x[mb][nb][e].y;
               double vr = ar * xr - ai * xi;
               double vi = ar * xi + ai * xr;
-              if (MODE == kTri && i == j && !keep_di) vi = 0.0;
+              if (kTriLike && i == j && !keep_di) vi = 0.0;
               if (beta != 0.0) {
                 vr += beta * old[u][nb][e].x;
                 vi += beta * old[u][nb][e].y;
@@ -608,7 +696,7 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES,
         }
       }
     }
-    if (MODE == kTri) {
+    if (kTriLike) {
       have = sched.next(pc);
     } else {
       bt += gridDim.x;

@@ -11,7 +11,9 @@ namespace hsdla_b200 {
 constexpr int kMaxSeg = 3;
 constexpr int kChunkC = 8;  // complex k per TMA slab (128 B rows)
 
-enum CtnMode { kTri = 0, kBatch = 1 };
+// kTri: the strictly-lower tiles of the triangle (or of a column window); kTriDiag: its diagonal
+// tiles (a launch of their own with a warp remapping, ctn_contract.cuh); kBatch: per-atom products.
+enum CtnMode { kTri = 0, kBatch = 1, kTriDiag = 2 };
 
 struct alignas(64) CtnParams {
   CUtensorMap L[kMaxSeg];  // left operands (conjugated), 3-D maps
@@ -31,6 +33,9 @@ struct alignas(64) CtnParams {
   int band;                // TRI: tile-row band of the grouped tile order (>= 1)
   int col_t0, col_t1;      // TRI, optional: only the lower tiles with col_t0 <= tj < col_t1
                            // (col_t1 == 0: the whole lower triangle); tiles_total = their count
+  int diag_t0;             // TRI diagonal launch: tile index of its first diagonal tile
+  int with_diag;           // TRI: 1 = this launch covers the diagonal tiles too (small triangles:
+                           // one launch; no warp remapping), 0 = strictly-lower tiles only
   int g0;                  // TRI: global column of the operands' first held column (a column
                            // window's engine holds columns [g0, n)); TMA coordinate = global - g0
   uint64_t pk0;            // TRI: global packed index of out[0] (the window's first packed element)

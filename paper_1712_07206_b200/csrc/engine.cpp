@@ -62,7 +62,7 @@ void engine_free(hsdla_b200_engine* e) {
   for (int q = 0; q < hsdla_b200_engine::kD2hPieces; ++q)
     for (cudaEvent_t ev : {e->ev_h_band[q], e->ev_h_red[q], e->ev_dl_h[q]})
       if (ev) cudaEventDestroy(ev);
-  for (cudaEvent_t ev : {e->ev_a0, e->ev_ops, e->ev_begin, e->ev_end, e->ev_s_done, e->ev_s_red, e->ev_reduce_end,
+  for (cudaEvent_t ev : {e->ev_a0, e->ev_ops, e->ev_cs_order, e->ev_begin, e->ev_end, e->ev_s_done, e->ev_s_red, e->ev_reduce_end,
                          e->ev_up0, e->ev_up1, e->ev_dl_s, e->ev_setup0, e->ev_setup1, e->ev_setup_mid})
     if (ev) cudaEventDestroy(ev);
   for (auto& t : e->ring)
@@ -77,7 +77,8 @@ void engine_free(hsdla_b200_engine* e) {
 static uint64_t tiles_of(uint64_t n) { return (n + kTriBM - 1) / kTriBM; }
 
 // Lower tiles of the engine's window: all t(t+1)/2, or for tile columns [t0, t1) the
-// triangle of rows t0..t1-1 plus the full-width rows t1..T-1 (ctn_contract.cuh tri_tile_cols).
+// triangle of rows t0..t1-1 plus the full-width rows t1..T-1 (ctn_contract.cuh tri_tile_strict
+// enumerates the strictly-lower ones, the diagonal tiles run in a launch of their own).
 static uint64_t window_tiles(uint64_t T, uint64_t t0, uint64_t t1) {
   const uint64_t w = t1 - t0;
   return w * (w + 1) / 2 + (T - t1) * w;
@@ -132,7 +133,7 @@ static void make_chunk(hsdla_b200_engine* e, int set, uint64_t a0, uint64_t a1, 
     P.n = static_cast<int>(e->ng);
     P.tiles = static_cast<int>(T);
     P.tiles_total = static_cast<int>(tri_tiles);
-    if (!all) {  // the window's tile columns (tri_tile_cols order)
+    if (!all) {  // the window's tile columns (tri_tile_strict order)
       P.col_t0 = static_cast<int>(t0);
       P.col_t1 = static_cast<int>(t1);
     }
@@ -419,7 +420,7 @@ hsdla_b200_engine* engine_create(int device, const ShardSpec& sp) {
     for (cudaEvent_t* ev : {&e->ev_begin, &e->ev_end, &e->ev_reduce_end, &e->ev_up0, &e->ev_up1, &e->ev_setup0,
                             &e->ev_setup1, &e->ev_setup_mid})
       HS_CUDA(cudaEventCreate(ev));
-    for (cudaEvent_t* ev : {&e->ev_s_done, &e->ev_s_red, &e->ev_dl_s, &e->ev_a0, &e->ev_ops})
+    for (cudaEvent_t* ev : {&e->ev_s_done, &e->ev_s_red, &e->ev_dl_s, &e->ev_a0, &e->ev_ops, &e->ev_cs_order})
       HS_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     for (int q = 0; q < hsdla_b200_engine::kD2hPieces; ++q)
       for (cudaEvent_t* ev : {&e->ev_h_band[q], &e->ev_h_red[q], &e->ev_dl_h[q]})
@@ -636,6 +637,11 @@ static cudaEvent_t next_event(hsdla_b200_engine* e) {
     e->ev_pool.push_back(ev);
   }
   return e->ev_pool[e->ev_used++];
+}
+
+void copy_after_compute(hsdla_b200_engine* e) {
+  HS_CUDA(cudaEventRecord(e->ev_cs_order, e->stream));
+  HS_CUDA(cudaStreamWaitEvent(e->copy_stream, e->ev_cs_order, 0));
 }
 
 // HSDLA_B200_TRACE: a timing event on stream s named `what` (device timeline of one call).
@@ -874,8 +880,9 @@ void engine_build_streamed(hsdla_b200_engine* e, const hsdla_b200_problem* p, ui
   check_problem(e, p, a0);
   begin_build(e, algo);
   ensure_streamed_plans(e);
-  // the copy stream may only overwrite A/B/T/U once the previous build has consumed them
-  HS_CUDA(cudaStreamWaitEvent(e->copy_stream, e->ev_end, 0));
+  // the copy stream may only overwrite A/B/T/U once the previous build has consumed them (and
+  // after any upload still in flight on the compute stream)
+  copy_after_compute(e);
   HS_CUDA(cudaEventRecord(e->ev_up0, e->copy_stream));
   trace_mark(e, e->copy_stream, "up_start");
   const uint64_t ab_bytes = p->n_atoms * p->n_l * p->n_g * sizeof(double2);

@@ -151,7 +151,8 @@ struct hsdla_b200_engine {
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr, ev_s_done = nullptr, ev_s_red = nullptr,
               ev_reduce_end = nullptr, ev_up0 = nullptr, ev_up1 = nullptr,
               ev_a0 = nullptr,   // the first streamed chunk's A rows landed
-              ev_ops = nullptr;  // operators uploaded on the copy stream (engine_upload_operators)
+              ev_ops = nullptr,  // operators uploaded on the copy stream (engine_upload_operators)
+              ev_cs_order = nullptr;  // copy_after_compute
   bool ops_pending = false;      // the next build must wait for ev_ops before expanding T
   static constexpr int kD2hPieces = 8;   // H downloads in column-range pieces, unpacked as each lands
   cudaEvent_t ev_h_band[kD2hPieces] = {};  // final H contraction finished tile-column band q
@@ -257,6 +258,9 @@ void harvest(hsdla_b200_engine* e, hsdla_b200_engine::KTimer& t);
 void begin_build(hsdla_b200_engine* e, int algo);
 void ensure_streamed_plans(hsdla_b200_engine* e);
 void trace_mark(hsdla_b200_engine* e, cudaStream_t s, const std::string& what);
+// The copy stream waits for everything enqueued on the compute stream so far (the previous
+// build, and uploads engine_upload issued there) before it overwrites the inputs.
+void copy_after_compute(hsdla_b200_engine* e);
 void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool last, hsdla_b200_engine::KTimer* kt,
                    bool s_rest = false);
 char* stage_acquire(hsdla_b200_engine* e, int& slot);

@@ -220,7 +220,7 @@ void engine_build_file(hsdla_b200_engine* e, const char* path, uint64_t a0, int 
   const HsdlHeader h = open_shard(f, path, e, a0);
   begin_build(e, algo);
   ensure_streamed_plans(e);
-  HS_CUDA(cudaStreamWaitEvent(e->copy_stream, e->ev_end, 0));
+  copy_after_compute(e);  // the previous build (and any upload on the compute stream) is done with A, B, T, U
   HS_CUDA(cudaEventRecord(e->ev_up0, e->copy_stream));
   // the mapped file view feeds ~36-42 GB/s (copy_nt from the page cache): the host-packed
   // plan; HSDLA_B200_FILE_PLAN=pinned selects the page-locked one

@@ -155,7 +155,10 @@ static void engine_upload_operators(hsdla_b200_engine* e, const double* taa, con
   // on the copy stream, so the next build's S contraction (which needs no operator) runs
   // while they travel; the build waits for ev_ops before its operator expansion
   cudaStream_t cs = e->copy_stream;
-  HS_CUDA(cudaStreamWaitEvent(cs, e->ev_end, 0));  // the previous build is done with T
+  // after everything already on the compute stream: the previous build (done with T) and any
+  // earlier upload into T (engine_upload copies on the compute stream; a pageable copy may still
+  // be in flight when it returns, and landing after this one would restore the old operators)
+  copy_after_compute(e);
   HS_CUDA(cudaMemcpyAsync(e->Taa, reinterpret_cast<const double2*>(taa) + a0 * blk, bytes, cudaMemcpyHostToDevice, cs));
   HS_CUDA(cudaMemcpyAsync(e->Tab, reinterpret_cast<const double2*>(tab) + a0 * blk, bytes, cudaMemcpyHostToDevice, cs));
   HS_CUDA(cudaMemcpyAsync(e->Tbb, reinterpret_cast<const double2*>(tbb) + a0 * blk, bytes, cudaMemcpyHostToDevice, cs));

@@ -32,8 +32,10 @@ __global__ void fill(double* p, size_t n, unsigned seed) {
 template <int BM, int WM, int WN, int ST, int MINB, int G3M = 0, int KSUB = 1>
 void run(const char* name, double2* A, double2* B, double2* out, uint64_t K, uint64_t ng, int nseg) {
   using Cfg = CtnCfg<kTri, BM, BM, WM, WN, ST, KSUB>;
-  auto kern = ctn_contract_kernel<kTri, BM, BM, WM, WN, ST, MINB, G3M, KSUB>;
+  auto kern = ctn_contract_kernel<kTri, BM, BM, WM, WN, ST, MINB, G3M, KSUB>;       // strictly-lower tiles
+  auto dkern = ctn_contract_kernel<kTriDiag, BM, BM, WM, WN, ST, MINB, G3M, KSUB>;  // diagonal tiles
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
+  cudaFuncSetAttribute(dkern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
   CtnParams P;
   memset(&P, 0, sizeof(P));
   CUtensorMap mA, mB;
@@ -48,7 +50,7 @@ void run(const char* name, double2* A, double2* B, double2* out, uint64_t K, uin
   P.n = (int)ng;
   int tiles = (int)((ng + BM - 1) / BM);
   P.tiles = tiles;
-  P.tiles_total = tiles * (tiles + 1) / 2;
+  P.tiles_total = tiles * (tiles - 1) / 2;  // kTri launch (with_diag 0): strictly lower; the kTriDiag launch: `tiles`
   P.band = 8;
   P.out = out;
   P.alpha_re = 1.0;
@@ -65,16 +67,24 @@ void run(const char* name, double2* A, double2* B, double2* out, uint64_t K, uin
   int grid = 148 * MINB;
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::kThreads, Cfg::kSmemBytes);
+  auto launch2 = [&] {
+    CtnParams d = P;
+    d.tiles_total = tiles;
+    d.diag_t0 = 0;
+    d.epoch = P.epoch | 0x40000000u;
+    kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes>>>(P);
+    dkern<<<grid, Cfg::kThreads, Cfg::kSmemBytes>>>(d);
+  };
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
   P.epoch = ++epoch;
-  kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes>>>(P);
+  launch2();
   cudaDeviceSynchronize();
   float best = 1e9;
   for (int r = 0; r < 5; ++r) {
     cudaEventRecord(e0);
     P.epoch = ++epoch;
-    kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes>>>(P);
+    launch2();
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
