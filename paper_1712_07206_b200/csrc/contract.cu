@@ -84,7 +84,7 @@ void set_kernel_attributes() {
 // one launch over every lower tile.  P describes the
 // whole set (tiles_total counts the diagonal); grid.x bounds both grids.  Each launch gets its
 // own stream-K flag generation (2 epoch, 2 epoch + 1).
-void launch_tri_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStream_t s) {
+int launch_tri_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStream_t s) {
   int iters = 0;
   for (int sg = 0; sg < P.nseg; ++sg) iters += P.kchunks[sg];
   const int t0 = P.col_t1 > 0 ? P.col_t0 : 0, ndiag = P.col_t1 > 0 ? P.col_t1 - P.col_t0 : P.tiles;
@@ -103,8 +103,9 @@ void launch_tri_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStre
     q.epoch = 2 * P.epoch;
     tri_kernels[arith]<<<grid_of(P.tiles_total), TriCfg::kThreads, TriCfg::kSmemBytes, s>>>(q);
     HS_CUDA(cudaGetLastError());
-    return;
+    return 1;
   }
+  int n = 1;
   if (nstrict > 0) {
     CtnParams q = P;
     q.tiles_total = nstrict;
@@ -112,6 +113,7 @@ void launch_tri_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStre
     q.epoch = 2 * P.epoch;
     tri_kernels[arith]<<<grid_of(nstrict), TriCfg::kThreads, TriCfg::kSmemBytes, s>>>(q);
     HS_CUDA(cudaGetLastError());
+    ++n;
   }
   CtnParams d = P;
   d.tiles_total = ndiag;
@@ -119,6 +121,7 @@ void launch_tri_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStre
   d.epoch = 2 * P.epoch + 1;
   diag_kernels[arith]<<<grid_of(ndiag), TriCfg::kThreads, TriCfg::kSmemBytes, s>>>(d);
   HS_CUDA(cudaGetLastError());
+  return n;
 }
 
 void launch_bat_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStream_t s) {

@@ -35,7 +35,8 @@ void make_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64
 void set_kernel_attributes();
 // Launch the TRI (lower-triangular, packed output) / BATCH (per-atom rectangular)
 // contraction with arith HSDLA_B200_ARITH_3M / _4M on `s`.
-void launch_tri_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStream_t s);
+// Returns the number of kernels launched (the strictly-lower and the diagonal launch, or one).
+int launch_tri_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStream_t s);
 void launch_bat_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStream_t s);
 void launch_batw_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStream_t s);
 

@@ -680,8 +680,7 @@ static void timed_op(hsdla_b200_engine* e, int phase, F&& body) {
 static void launch_tri(hsdla_b200_engine* e, const CtnParams& P, const dim3& grid) {
   CtnParams q = P;
   q.epoch = ++e->epoch;  // fresh stream-K flag generation per launch
-  launch_tri_kernel(e->arith, grid, q, e->stream);
-  ++e->launches;
+  e->launches += launch_tri_kernel(e->arith, grid, q, e->stream);
 }
 static void launch_bat(hsdla_b200_engine* e, const CtnParams& P, const dim3& grid) {
   launch_bat_kernel(e->arith, grid, P, e->stream);
