@@ -69,25 +69,32 @@ static decltype(&ctn_contract_kernel<kBatch, kBatBM, kBatBN, 1, 8, kBatStages>) 
 static decltype(&ctn_contract_kernel<kTriDiag, kTriBM, kTriBM, 2, 4, kTriStages>) const diag_kernels[2] = {
     ctn_contract_kernel<kTriDiag, kTriBM, kTriBM, 2, 4, kTriStages, 1, 1>,
     ctn_contract_kernel<kTriDiag, kTriBM, kTriBM, 2, 4, kTriStages, 1, 0>};
+// a ragged last tile row: its own launch with the row remapping (kRowRemap)
+static decltype(&ctn_contract_kernel<kTriRow, kTriBM, kTriBM, 2, 4, kTriStages>) const row_kernels[2] = {
+    ctn_contract_kernel<kTriRow, kTriBM, kTriBM, 2, 4, kTriStages, 1, 1>,
+    ctn_contract_kernel<kTriRow, kTriBM, kTriBM, 2, 4, kTriStages, 1, 0>};
 
 void set_kernel_attributes() {
   for (int a = 0; a < 2; ++a) {
     HS_CUDA(cudaFuncSetAttribute(tri_kernels[a], cudaFuncAttributeMaxDynamicSharedMemorySize, TriCfg::kSmemBytes));
     HS_CUDA(cudaFuncSetAttribute(diag_kernels[a], cudaFuncAttributeMaxDynamicSharedMemorySize, TriCfg::kSmemBytes));
+    HS_CUDA(cudaFuncSetAttribute(row_kernels[a], cudaFuncAttributeMaxDynamicSharedMemorySize, TriCfg::kSmemBytes));
     HS_CUDA(cudaFuncSetAttribute(bat_kernels[a], cudaFuncAttributeMaxDynamicSharedMemorySize, BatCfg::kSmemBytes));
     HS_CUDA(cudaFuncSetAttribute(batw_kernels[a], cudaFuncAttributeMaxDynamicSharedMemorySize, BatWCfg::kSmemBytes));
   }
 }
 
-// One lower-triangular contraction = two launches on `s`: the strictly-lower tiles, then the
-// diagonal tiles (warp-remapped: a diagonal tile costs 10 / 16 of a full one); small triangles
-// one launch over every lower tile.  P describes the
-// whole set (tiles_total counts the diagonal); grid.x bounds both grids.  Each launch gets its
-// own stream-K flag generation (2 epoch, 2 epoch + 1).
+// One lower-triangular contraction = up to three launches on `s`: the strictly-lower tiles, the
+// diagonal tiles (warp-remapped: a diagonal tile costs 10 / 16 of a full one) and, when N_G leaves
+// the last tile row with v <= 6 of its 8 fragment rows, that row's tiles (remapped so the valid
+// rows are spread over the SM sub-partitions: about v / 8 of a full row).  Small triangles run as
+// ONE launch over every lower tile.  P describes the whole set (tiles_total counts the diagonal);
+// grid.x bounds every grid.  Each launch gets its own stream-K flag generation (4 epoch + i).
 int launch_tri_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStream_t s) {
   int iters = 0;
   for (int sg = 0; sg < P.nseg; ++sg) iters += P.kchunks[sg];
-  const int t0 = P.col_t1 > 0 ? P.col_t0 : 0, ndiag = P.col_t1 > 0 ? P.col_t1 - P.col_t0 : P.tiles;
+  const int T = P.tiles;
+  const int t0 = P.col_t1 > 0 ? P.col_t0 : 0, ndiag = P.col_t1 > 0 ? P.col_t1 - P.col_t0 : T;
   const int nstrict = P.tiles_total - ndiag;
   auto grid_of = [&](int tiles) {
     return dim3(static_cast<unsigned>(std::max<long long>(1, std::min<long long>(grid.x, 1LL * tiles * iters))));
@@ -100,28 +107,47 @@ int launch_tri_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStrea
   if (1.0 * ndiag * iters < split_min) {
     CtnParams q = P;
     q.with_diag = 1;
-    q.epoch = 2 * P.epoch;
+    q.epoch = 4 * P.epoch;
     tri_kernels[arith]<<<grid_of(P.tiles_total), TriCfg::kThreads, TriCfg::kSmemBytes, s>>>(q);
     HS_CUDA(cudaGetLastError());
     return 1;
   }
-  int n = 1;
-  if (nstrict > 0) {
+  // the ragged last row: tiles (T-1, c) for c in [t0, min(t1, T-1)), v valid fragment rows
+  const int v = static_cast<int>((P.n - static_cast<long long>(T - 1) * kTriBM + 7) / 8);
+  const int c1 = P.col_t1 > 0 ? std::min(P.col_t1, T - 1) : T - 1;
+  const int nrow = T >= 2 && v <= 6 ? std::max(0, c1 - t0) : 0;
+  int n = 0;
+  if (nstrict - nrow > 0) {
     CtnParams q = P;
-    q.tiles_total = nstrict;
+    q.tiles_total = nstrict - nrow;
     q.with_diag = 0;
-    q.epoch = 2 * P.epoch;
-    tri_kernels[arith]<<<grid_of(nstrict), TriCfg::kThreads, TriCfg::kSmemBytes, s>>>(q);
+    // the whole triangle without its last row: the strictly-lower tiles of the (T-1)-grid (the
+    // grouped order interleaves the last rows, so the grid shrinks); a window's last row comes
+    // last in its enumeration, so the count alone excludes it
+    if (nrow > 0 && P.col_t1 <= 0) q.tiles = T - 1;
+    q.epoch = 4 * P.epoch;
+    tri_kernels[arith]<<<grid_of(q.tiles_total), TriCfg::kThreads, TriCfg::kSmemBytes, s>>>(q);
+    HS_CUDA(cudaGetLastError());
+    ++n;
+  }
+  if (nrow > 0) {
+    CtnParams r = P;
+    r.tiles_total = nrow;
+    r.row_ti = T - 1;
+    r.row_v = v;
+    r.diag_t0 = t0;
+    r.epoch = 4 * P.epoch + 2;
+    row_kernels[arith]<<<grid_of(nrow), TriCfg::kThreads, TriCfg::kSmemBytes, s>>>(r);
     HS_CUDA(cudaGetLastError());
     ++n;
   }
   CtnParams d = P;
   d.tiles_total = ndiag;
   d.diag_t0 = t0;
-  d.epoch = 2 * P.epoch + 1;
+  d.epoch = 4 * P.epoch + 1;
   diag_kernels[arith]<<<grid_of(ndiag), TriCfg::kThreads, TriCfg::kSmemBytes, s>>>(d);
   HS_CUDA(cudaGetLastError());
-  return n;
+  return n + 1;
 }
 
 void launch_bat_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStream_t s) {

@@ -315,6 +315,10 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES,
     if (MODE == kTriDiag) {
       row0 = col0 = (P.diag_t0 + tile) * BM;
       atom = 0;
+    } else if (MODE == kTriRow) {
+      row0 = P.row_ti * BM;
+      col0 = (P.diag_t0 + tile) * BN;
+      atom = 0;
     } else if (MODE == kTri) {
       int ti, tj;
       if (P.with_diag) {
@@ -402,6 +406,10 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES,
   const int q = lane & 3;
   const int pg = ((g & 1) << 2) | (g >> 1);  // smem row permutation (bank-conflict-free LDS.128)
   constexpr bool kDiagRemap = MODE == kTriDiag && WARPS_M == 2 && WARPS_N == 4 && MB == 4 && NB == 2;
+  // Ragged last tile row (rows 64 (T-1) .. N_G-1, v valid fragment rows of 8): warps w and w + 4
+  // (one SM sub-partition) take the two row halves of column block w % 4, so the sub-partitions
+  // share the valid rows evenly; each warp runs the k-loop of its first min(4, v - 4 wm) rows.
+  constexpr bool kRowRemap = MODE == kTriRow && WARPS_M == 2 && WARPS_N == 4 && MB == 4 && NB == 2;
 
   uint32_t offL[MB], offR[NB], offK[2];
 #pragma unroll
@@ -425,6 +433,12 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES,
         wn = (0xDE84u >> (2 * warp)) & 3u;
         role = (0xAF50u >> (2 * warp)) & 3u;
       }
+    }
+    if (kRowRemap) {
+      wm = warp >> 2;
+      wn = warp & 3;
+      const int rows = min(4, max(0, P.row_v - 4 * wm));
+      role = rows == 4 ? 0 : 4 + rows;  // 4: none, 5 / 6 / 7: the first 1 / 2 / 3 fragment rows
     }
 #pragma unroll
     for (int mb = 0; mb < MB; ++mb) offL[mb] = (wm * Cfg::kWM + 8 * mb + pg) * 128;
@@ -584,6 +598,17 @@ __global__ void __launch_bounds__(CtnCfg<MODE, BM, BN, WARPS_M, WARPS_N, STAGES,
         kloop(std::integral_constant<unsigned, kMaskTri7>{});
       else if (role == 2)
         kloop(std::integral_constant<unsigned, kMaskTri3>{});
+      else
+        kloop(std::integral_constant<unsigned, kMaskNone>{});
+    } else if constexpr (kRowRemap) {
+      if (role == 0)
+        kloop(std::integral_constant<unsigned, kMaskFull>{});
+      else if (role == 5)
+        kloop(std::integral_constant<unsigned, 0x03u>{});  // fragment row 0
+      else if (role == 6)
+        kloop(std::integral_constant<unsigned, 0x0Fu>{});  // rows 0-1
+      else if (role == 7)
+        kloop(std::integral_constant<unsigned, 0x3Fu>{});  // rows 0-2
       else
         kloop(std::integral_constant<unsigned, kMaskNone>{});
     } else {

@@ -13,7 +13,8 @@ constexpr int kChunkC = 8;  // complex k per TMA slab (128 B rows)
 
 // kTri: the strictly-lower tiles of the triangle (or of a column window); kTriDiag: its diagonal
 // tiles (a launch of their own with a warp remapping, ctn_contract.cuh); kBatch: per-atom products.
-enum CtnMode { kTri = 0, kBatch = 1, kTriDiag = 2 };
+// kTriRow: the last tile row when N_G leaves it ragged (a launch of its own, ctn_contract.cuh).
+enum CtnMode { kTri = 0, kBatch = 1, kTriDiag = 2, kTriRow = 3 };
 
 struct alignas(64) CtnParams {
   CUtensorMap L[kMaxSeg];  // left operands (conjugated), 3-D maps
@@ -33,7 +34,9 @@ struct alignas(64) CtnParams {
   int band;                // TRI: tile-row band of the grouped tile order (>= 1)
   int col_t0, col_t1;      // TRI, optional: only the lower tiles with col_t0 <= tj < col_t1
                            // (col_t1 == 0: the whole lower triangle); tiles_total = their count
-  int diag_t0;             // TRI diagonal launch: tile index of its first diagonal tile
+  int diag_t0;             // TRI diagonal launch: tile index of its first diagonal tile;
+                           // ragged-row launch: tile column of its first tile
+  int row_ti, row_v;       // ragged-row launch: the row's tile index, its valid 8-row fragment rows
   int with_diag;           // TRI: 1 = this launch covers the diagonal tiles too (small triangles:
                            // one launch; no warp remapping), 0 = strictly-lower tiles only
   int g0;                  // TRI: global column of the operands' first held column (a column
