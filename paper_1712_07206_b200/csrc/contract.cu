@@ -115,7 +115,11 @@ int launch_tri_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStrea
   // the ragged last row: tiles (T-1, c) for c in [t0, min(t1, T-1)), v valid fragment rows
   const int v = static_cast<int>((P.n - static_cast<long long>(T - 1) * kTriBM + 7) / 8);
   const int c1 = P.col_t1 > 0 ? std::min(P.col_t1, T - 1) : T - 1;
-  const int nrow = T >= 2 && v <= 6 ? std::max(0, c1 - t0) : 0;
+  // worth its launch when the skipped rows' work, nrow x iters x (8 - v) / 8 k-slabs over the GPU,
+  // exceeds ~15 us, and v <= 6 (C2's v = 7 measured 17.79 ms either way)
+  static const double row_min = env_double("HSDLA_B200_ROW_SPLIT_MIN", 24000);
+  const int nrow0 = T >= 2 && v <= 6 ? std::max(0, c1 - t0) : 0;
+  const int nrow = 1.0 * nrow0 * iters * (8 - v) >= row_min ? nrow0 : 0;
   int n = 0;
   if (nstrict - nrow > 0) {
     CtnParams q = P;
