@@ -103,7 +103,7 @@ int launch_tri_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStrea
   // k-slabs over the GPU, and costs a launch (~10 us): below ~8000 tile-slabs (C1: 16 x 196) the
   // triangle runs as ONE launch over every lower tile (measured: C1 0.42 ms in one launch, 0.46 split;
   // C2 17.96 -> 17.77 ms split)
-  static const double split_min = env_double("HSDLA_B200_DIAG_SPLIT_MIN", 8000);
+  const double split_min = env_double("HSDLA_B200_DIAG_SPLIT_MIN", 8000);  // read per call (tests vary it)
   if (1.0 * ndiag * iters < split_min) {
     CtnParams q = P;
     q.with_diag = 1;
@@ -117,7 +117,7 @@ int launch_tri_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStrea
   const int c1 = P.col_t1 > 0 ? std::min(P.col_t1, T - 1) : T - 1;
   // worth its launch when the skipped rows' work, nrow x iters x (8 - v) / 8 k-slabs over the GPU,
   // exceeds ~15 us, and v <= 6 (C2's v = 7 measured 17.79 ms either way)
-  static const double row_min = env_double("HSDLA_B200_ROW_SPLIT_MIN", 24000);
+  const double row_min = env_double("HSDLA_B200_ROW_SPLIT_MIN", 24000);
   const int nrow0 = T >= 2 && v <= 6 ? std::max(0, c1 - t0) : 0;
   const int nrow = 1.0 * nrow0 * iters * (8 - v) >= row_min ? nrow0 : 0;
   int n = 0;

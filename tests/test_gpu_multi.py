@@ -346,3 +346,39 @@ def test_multigpu_torchrun_engine_path(tmp_path, reduce):
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     z = np.load(out)
     assert z["err_h"] <= TOL and z["err_s"] <= TOL
+
+
+@pytest.mark.parametrize("split", ["always", "never"])
+def test_split_triangle_launches_in_windows_bands_and_kpoints(restatement, monkeypatch, split):
+    """The triangle as separate strictly-lower / diagonal / ragged-last-row launches (thresholds
+    forced to 0) or as one launch (thresholds huge), in every place a triangle is enumerated: whole
+    builds, column windows of an emulated 2 x 2 grid, the banded final H and k-point batches.
+    N_G = 2200 (35 tile columns: 630 lower tiles, enough for the banded final H) leaves the last
+    tile row with 24 of 64 rows (v = 3)."""
+    big = "1e18" if split == "never" else "0"
+    monkeypatch.setenv("HSDLA_B200_DIAG_SPLIT_MIN", big)
+    monkeypatch.setenv("HSDLA_B200_ROW_SPLIT_MIN", big)
+    p = hb.generate_problem(4, 16, 2200, 7, 1)
+    Hs, Ss, _ = restatement.build_hs_refined(p)
+    for algo in ("merged", "refined"):
+        r = hb.build_hs_refined(p, hb.PipelineConfig(algo=algo))
+        assert rel(r.H, Hs) <= TOL and rel(r.S, Ss) <= TOL, algo
+    r = hb.build_hs_refined(p, hb.PipelineConfig(n_gpus=4, device_ids=[0, 0, 0, 0], col_groups=2))
+    assert rel(r.H, Hs) <= TOL and rel(r.S, Ss) <= TOL
+    e = hb.Engine(0, p.n_atoms, p.n_l, p.n_g)
+    e.set_download_overlap(True)  # banded final H: 8 tile-column bands, each split or not
+    e.upload(p)
+    e.build()
+    H, S = e.download()
+    st = e.sync()
+    e.close()
+    assert rel(H, Hs) <= TOL and rel(S, Ss) <= TOL
+    assert st["kernel_launches"] == 12 if split == "never" else st["kernel_launches"] > 12  # 8 bands
+    kps = [hb.generate_problem(4, 16, 2200, 20 + k, 1) for k in range(2)]
+    got, _ = hb.build_hs_kpoints(p, [q.A for q in kps], [q.B for q in kps])
+    for (Hk, Sk), q in zip(got, kps):
+        pk = hb.generate_problem(4, 16, 2200, 7, 1)
+        pk.A, pk.B = q.A, q.B
+        Hq, Sq, _ = restatement.build_hs_refined(pk)
+        assert rel(Hk, Hq) <= TOL and rel(Sk, Sq) <= TOL
+    hb.release_cache()
