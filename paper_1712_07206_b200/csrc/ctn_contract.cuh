@@ -4,15 +4,19 @@
 //
 // The one engine behind every product of the refined H/S construction
 // (reference kernels.cpp:92-167 / pipeline.cpp:281-329):
-//   * TRI mode: lower-triangular N_G x N_G output written to packed-lower storage
+//   * TRI modes: lower-triangular N_G x N_G output written to packed-lower storage
 //     (ZHERK / ZHER2K / ZHERKX: herk_cols :104-117, her2k_cols :119-135,
-//     herkx_cols :137-150).  Tiles enumerate the t(t+1)/2 lower tiles
-//     (the idea of hybrid_dynamic.cpp:54-112), the strict upper triangle is never
-//     touched and diagonal imaginary parts are forced to 0 (kernels.cpp:112).
+//     herkx_cols :137-150).  Tiles enumerate the lower tiles (the idea of
+//     hybrid_dynamic.cpp:54-112); the strict upper triangle is never touched and
+//     diagonal imaginary parts are forced to 0 (kernels.cpp:112).  kTri covers the
+//     strictly-lower tiles (or every lower tile, `with_diag`), kTriDiag the diagonal
+//     tiles and kTriRow a ragged last tile row, each with its own warp assignment
+//     (launch_tri_kernel in contract.cu issues them).
 //   * BATCH mode (persistent: CTAs loop over column x row x atom tiles, so the next
-//     tile's TMA loads overlap the current tile's epilogue): per-atom rectangular products Z_a = T_AB^H A_a + 1/2 T_BB B_a and
-//     X_a = T_AA A_a (compute_z pipeline.cpp:176-185 and the hemm_loop
-//     :314-321) written straight into the stacked K x N_G buffers.
+//     tile's TMA loads overlap the current tile's epilogue): per-atom rectangular
+//     products Z_a = T_AB^H A_a + 1/2 T_BB B_a, X_a = T_AA A_a (compute_z
+//     pipeline.cpp:176-185 and the hemm_loop :314-321) and the merged algorithm's
+//     [W_A; W_B] = M_a Y_a, written straight into the stacked K x N_G buffers.
 //
 // B200 mapping (no tcgen05 kind::f64 exists; FP64 tensor work is warp-level DMMA):
 //   * one elected producer lane streams 128-byte k-slabs of both operands with
