@@ -259,20 +259,22 @@ static void make_chunk(hsdla_b200_engine* e, int set, uint64_t a0, uint64_t a1, 
   cp.grid_bat = dim3(static_cast<unsigned>(std::min<uint64_t>(bat_tiles, e->sms)));
 }
 
-// Streamed chunking for the host-buffer drop-in: whole-atom chunks growing
-// geometrically, so the exposed upload of the first chunk is short and later
-// (larger) uploads still finish before the previous chunk's phases do.  The growth
-// factor follows rho, the compute/upload time ratio of one atom:
-//   rho = (20 K N_G^2 / 34 TF/s) / (32 K N_G B / rate) = N_G * rate * 1.84e-14,
-// r = clamp(0.8 rho, 1, 4); the first chunk is the larger of N_A/16 and the head of an
-// 8-term geometric series summing to N_A; at most 8 chunks.  (The 34 TF/s is the 4M
-// fused rate; calibrating it to the merged 3M build's faster compute gives more,
-// smaller chunks, and every extra chunk costs ~0.2 ms at C2 in per-launch epilogues and
-// ramps: tools/stream_tune.py measured N_A/16 with this constant best for the merged
-// build, 20.5 ms per call at C2 against 20.8-23.8 for the other settings; C3 is flat.)  `rate` is the host->device
-// feed: ~50 GB/s for page-locked inputs (PCIe), ~20 GB/s for pageable inputs packed by
-// host threads or for page-cached HSDL files.  Small problems (< 64 MB of A+B): one chunk.
-static std::vector<uint64_t> stream_bounds(uint64_t na, uint64_t nl, uint64_t ng, double rate) {
+// Streamed chunking for the host-buffer drop-in: whole-atom chunks, chunk c+1's upload
+// overlapping chunk c's phases.  The plan minimises a model of the call's device timeline by
+// dynamic programming over the chunk boundaries (at most 8 chunks):
+//   chunk k of s_k atoms starts at max(end of chunk k-1, its upload done = u x atoms so far)
+//   and takes c x s_k + f,
+// with u = one atom's A and B rows at `rate` (host -> device feed: ~50 GB/s page-locked, ~35
+// GB/s effective for rows the host packs into pinned slabs or copies from the page cache),
+// c = one atom's share of the executed flops (merged 3M: S and H over the window's tiles, W)
+// at 33 TF/s, and f = a chunk's fixed cost (launch ramps and tails, the beta = 1 passes over the
+// packed H, S: 50 us + the window's packed bytes x 4 at 2 TB/s; ~0.2 ms at C2).  C2 pinned: the
+// plan 2,4,9,17,32 atoms ran 19.9 ms per call against 20.2 for the earlier geometric plan
+// 4,9,20,31 (tools/small_probe.py).  Small problems (< 4M A elements) stay one chunk: there the
+// copies slow the short kernels more than the overlap gains.
+static std::vector<uint64_t> stream_bounds(const hsdla_b200_engine* e, double rate, double fmul = 1.0,
+                                           uint64_t min_first = 1) {
+  const uint64_t na = e->na, nl = e->nl, ng = e->ng;
   std::vector<uint64_t> b{0};
   if (const char* plan = std::getenv("HSDLA_B200_STREAM_PLAN")) {  // explicit chunk sizes "4,9,19" (tuning)
     for (const char* c = plan; *c && b.back() < na;) {
@@ -288,18 +290,47 @@ static std::vector<uint64_t> stream_bounds(uint64_t na, uint64_t nl, uint64_t ng
     b.push_back(na);
     return b;
   }
-  const double rho = static_cast<double>(ng) * rate * env_double("HSDLA_B200_STREAM_C", 1.84e-14);
-  const double r = std::min(4.0, std::max(1.0, 0.8 * rho));
-  const double head = r > 1.0001 ? (r - 1.0) / (std::pow(r, 8.0) - 1.0) : 1.0 / 8.0;
-  double size = std::max(1.0, static_cast<double>(na) * std::max(env_double("HSDLA_B200_STREAM_FLOOR", 1.0 / 16.0), head));
-  while (b.back() < na) {
-    const uint64_t left = na - b.back();
-    uint64_t take = std::min<uint64_t>(left, static_cast<uint64_t>(std::llround(size)));
-    if (b.size() == 8 || left - take < take / 2) take = left;  // cap the count, no tiny last chunk
-    b.push_back(b.back() + std::max<uint64_t>(take, 1));
-    size *= r;
+  const double T = static_cast<double>(tiles_of(ng)), t0 = static_cast<double>(e->c0 / kTriBM),
+               t1 = static_cast<double>(tiles_of(e->c1));
+  const double tiles = (t1 - t0) * (t1 - t0 + 1) / 2 + (T - t1) * (t1 - t0);  // the window's lower tiles
+  const double rows = static_cast<double>(e->row1 - e->row0) / static_cast<double>(na);  // contracted rows per atom
+  // S and H: 2 segments of `rows` each over the window's tiles, 6 flops per complex MAC (3M)
+  const double flops = 2.0 * 2.0 * 8.0 * rows * tiles * kTriBM * kTriBM * 0.75 +
+                       32.0 * static_cast<double>(nl * nl * e->ncol) * 0.75;
+  const double u = 2.0 * static_cast<double>(nl * e->ncol) * 16.0 / rate;
+  const double c = flops / env_double("HSDLA_B200_STREAM_TFLOPS", 33e12);
+  const double f = fmul * (50e-6 + static_cast<double>(e->npk) * 64.0 / 2e12);
+  constexpr int kMaxChunks = 8;
+  const size_t n = na;
+  std::vector<double> best((kMaxChunks + 1) * (n + 1), 1e300);
+  std::vector<uint32_t> from((kMaxChunks + 1) * (n + 1), 0);
+  auto at = [&](int k, size_t m) { return static_cast<size_t>(k) * (n + 1) + m; };
+  best[at(0, 0)] = 0.0;
+  int kbest = 1;
+  for (int k = 1; k <= kMaxChunks; ++k) {
+    for (size_t m = 1; m <= n; ++m)
+      for (size_t p = 0; p < m; ++p) {  // chunk k covers atoms [p, m)
+        if (k == 1 && m < min_first && m < n) continue;
+        const double prev = best[at(k - 1, p)];
+        if (prev >= 1e299) continue;
+        const double t = std::max(prev, u * static_cast<double>(m)) + c * static_cast<double>(m - p) + f;
+        if (t < best[at(k, m)]) {
+          best[at(k, m)] = t;
+          from[at(k, m)] = static_cast<uint32_t>(p);
+        }
+      }
+    if (best[at(k, n)] < best[at(kbest, n)]) kbest = k;
   }
-  return b;
+  std::vector<uint64_t> cut(kbest + 1);
+  cut[kbest] = n;
+  for (int k = kbest; k > 0; --k) cut[k - 1] = from[at(k, cut[k])];
+  if (trace_on()) {
+    std::string pl;
+    for (int k = 0; k < kbest; ++k) pl += std::to_string(cut[k + 1] - cut[k]) + (k + 1 < kbest ? "," : "");
+    std::fprintf(stderr, "[hsdla_b200 trace] chunk plan at %.0f GB/s: %s (model %.2f ms)\n", rate / 1e9, pl.c_str(),
+                 best[at(kbest, n)] * 1e3);
+  }
+  return cut;
 }
 
 // Tile-column boundaries splitting the window's lower tiles into kD2hPieces bands
@@ -348,14 +379,16 @@ static void make_plans(hsdla_b200_engine* e) {
 
 void ensure_streamed_plans(hsdla_b200_engine* e) {
   if (!e->streamed_dirty) return;
-  const auto b = stream_bounds(e->na, e->nl, e->ncol, 50e9);
+  const auto b = stream_bounds(e, 50e9);
   e->streamed.resize(b.size() - 1);
   for (size_t c = 0; c + 1 < b.size(); ++c) make_chunk(e, 0, b[c], b[c + 1], c == 0, e->streamed[c]);
-  // host-packed feeds (pageable rows, HSDL files from the page cache) deliver ~44 GB/s at C2
-  // (pack and DMA pipelined): chunks grow more slowly so each upload still hides under the
-  // previous chunk's compute (tools/small_probe.py, C2 pageable: 4,6,10,15,29 atoms 20.8 ms
-  // per call against 21.4 with the page-locked plan 4,9,20,31)
-  const auto bp = stream_bounds(e->na, e->nl, e->ncol, env_double("HSDLA_B200_PAGEABLE_RATE", 35e9));
+  // host-packed feeds (pageable rows packed into the slabs, HSDL files copied from the page
+  // cache): ~35-44 GB/s, a chunk costs more (the host packs it before its launches are enqueued)
+  // and the first one is at least N_A/16 (tools/small_probe.py, pageable: C2 20.7 ms per call
+  // with 5,8,12,16,23 atoms against 20.9 for the earlier geometric 4,6,10,15,29; C3 180.0 against
+  // 184.6 ms)
+  const auto bp = stream_bounds(e, env_double("HSDLA_B200_PAGEABLE_RATE", 35e9), 2.0,
+                                static_cast<uint64_t>(std::ceil(e->na / 16.0)));
   e->streamed_pg.resize(bp.size() - 1);
   for (size_t c = 0; c + 1 < bp.size(); ++c) make_chunk(e, 0, bp[c], bp[c + 1], c == 0, e->streamed_pg[c]);
   while (e->ev_chunk_up.size() < std::max(e->streamed.size(), e->streamed_pg.size())) {

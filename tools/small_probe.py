@@ -15,7 +15,7 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1712_07206_b200 as hb  # noqa: E402
 
-CFG = {"c1": (16, 49, 1000), "s2": (16, 49, 2000), "s3": (32, 64, 1500), "c2": (64, 81, 3000)}
+CFG = {"c1": (16, 49, 1000), "s2": (16, 49, 2000), "s3": (32, 64, 1500), "c2": (64, 81, 3000), "c3": (108, 121, 6000)}
 
 
 def main():
