@@ -46,13 +46,17 @@ constexpr int kTriStages = 8;  // power of two: slot / phase are bit ops in the 
 using TriCfg = CtnCfg<kTri, kTriBM, kTriBM, 2, 4, kTriStages>;
 constexpr int kBatStages = 4;
 using BatCfg = CtnCfg<kBatch, kBatBM, kBatBN, 1, 8, kBatStages>;
-// the merged build's stacked W = M Y producer: 24-row tiles (2 N_L = 162 rows -> 168).
-// (Measured at C2: 1.18 ms per launch; 24 x 192 tiles with warp tiles 24 x 24: 1.15 ms; a
-// single producer warp, which ptxas still compiles against 168 registers since 9 warps put
-// 3 on one SM sub-partition: 1.19 ms, and 24 x 192 under it spills: 1.44 ms.)
+// the merged build's stacked W = M Y producer: 24-row tiles (2 N_L = 162 rows -> 168), 192 or 128
+// columns.  (Measured at C2: 1.15 ms per launch with 24 x 192 tiles (warp tiles 24 x 24), 1.18 ms
+// with 24 x 128; a single producer warp, which ptxas still compiles against 168 registers since 9
+// warps put 3 on one SM sub-partition: 1.19 ms, and 24 x 192 under it spills: 1.44 ms.)
 constexpr int kBatWStages = 8;
-using BatWCfg = CtnCfg<kBatch, kBatWBM, kBatBN, 1, 8, kBatWStages>;
-static decltype(&ctn_contract_kernel<kBatch, kBatWBM, kBatBN, 1, 8, kBatWStages>) const batw_kernels[2] = {
+using BatWCfg = CtnCfg<kBatch, kBatWBM, kBatWBN, 1, 8, kBatWStages>;
+static decltype(&ctn_contract_kernel<kBatch, kBatWBM, kBatWBN, 1, 8, kBatWStages>) const batw_kernels[2] = {
+    ctn_contract_kernel<kBatch, kBatWBM, kBatWBN, 1, 8, kBatWStages, 1, 1>,
+    ctn_contract_kernel<kBatch, kBatWBM, kBatWBN, 1, 8, kBatWStages, 1, 0>};
+using BatW128Cfg = CtnCfg<kBatch, kBatWBM, kBatBN, 1, 8, kBatWStages>;
+static decltype(&ctn_contract_kernel<kBatch, kBatWBM, kBatBN, 1, 8, kBatWStages>) const batw128_kernels[2] = {
     ctn_contract_kernel<kBatch, kBatWBM, kBatBN, 1, 8, kBatWStages, 1, 1>,
     ctn_contract_kernel<kBatch, kBatWBM, kBatBN, 1, 8, kBatWStages, 1, 0>};
 
@@ -81,6 +85,8 @@ void set_kernel_attributes() {
     HS_CUDA(cudaFuncSetAttribute(row_kernels[a], cudaFuncAttributeMaxDynamicSharedMemorySize, TriCfg::kSmemBytes));
     HS_CUDA(cudaFuncSetAttribute(bat_kernels[a], cudaFuncAttributeMaxDynamicSharedMemorySize, BatCfg::kSmemBytes));
     HS_CUDA(cudaFuncSetAttribute(batw_kernels[a], cudaFuncAttributeMaxDynamicSharedMemorySize, BatWCfg::kSmemBytes));
+    HS_CUDA(cudaFuncSetAttribute(batw128_kernels[a], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 BatW128Cfg::kSmemBytes));
   }
 }
 
@@ -159,8 +165,11 @@ void launch_bat_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStre
   HS_CUDA(cudaGetLastError());
 }
 
-void launch_batw_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStream_t s) {
-  batw_kernels[arith]<<<grid, BatWCfg::kThreads, BatWCfg::kSmemBytes, s>>>(P);
+void launch_batw_kernel(int arith, int bn, const dim3& grid, const CtnParams& P, cudaStream_t s) {
+  if (bn == kBatWBN)
+    batw_kernels[arith]<<<grid, BatWCfg::kThreads, BatWCfg::kSmemBytes, s>>>(P);
+  else
+    batw128_kernels[arith]<<<grid, BatW128Cfg::kThreads, BatW128Cfg::kSmemBytes, s>>>(P);
   HS_CUDA(cudaGetLastError());
 }
 

@@ -21,7 +21,7 @@ constexpr int kTriBM = 64;
 constexpr int kBatBM = 32, kBatBN = 128;
 // merged build: ONE BATCH launch W = M Y per atom over the stacked 2 N_L rows
 // (W_A; W_B), 24-row tiles (162 rows -> 7 tiles = 168, against 2 x 96 with 32-row tiles)
-constexpr int kBatWBM = 24;
+constexpr int kBatWBM = 24, kBatWBN = 192;  // (or kBatBN = 128 columns when that pads N_G less)
 // stream-K partial-accumulator slot per CTA: 64 x 64 outputs x 3 sets (3M) doubles
 constexpr uint64_t kSkSlot = uint64_t(kTriBM) * kTriBM * 3;
 
@@ -38,7 +38,8 @@ void set_kernel_attributes();
 // Returns the number of kernels launched (the strictly-lower and the diagonal launch, or one).
 int launch_tri_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStream_t s);
 void launch_bat_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStream_t s);
-void launch_batw_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStream_t s);
+// The W producer with bn = kBatWBN (warp tiles 24 x 24) or kBatBN (24 x 16) output columns per tile.
+void launch_batw_kernel(int arith, int bn, const dim3& grid, const CtnParams& P, cudaStream_t s);
 
 inline int chunks_of(uint64_t kcomplex) { return static_cast<int>((kcomplex + kChunkC - 1) / kChunkC); }
 // Tile-row band of the TRI tile order (ctn_contract.cuh tri_tile); HSDLA_B200_TRI_BAND

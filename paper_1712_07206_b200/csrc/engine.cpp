@@ -197,10 +197,18 @@ static void make_chunk(hsdla_b200_engine* e, int set, uint64_t a0, uint64_t a1, 
   make_map(&mW1, e->Wl + 4 * a0 * blk + 2 * blk, 2 * nl, 2 * nl, nac, 2 * nl, 8 * blk, kBatWBM, 1);
   make_map(&vA, e->A(set) + r0, 2 * nl, nac, ncol, 2 * nl, 2 * K, 1, kBatBN);
   make_map(&vB, e->B(set) + r0, 2 * nl, nac, ncol, 2 * nl, 2 * K, 1, kBatBN);
+  // the W launch's tile width: 192 columns (wider warp tiles: 1.15 against 1.18 ms at C2) unless
+  // 128 pads N_G less (N_G 1000: 1024 against 1152 columns)
+  const uint64_t pad192 = (ncol + kBatWBN - 1) / kBatWBN * kBatWBN, pad128 = (ncol + kBatBN - 1) / kBatBN * kBatBN;
+  cp.w_bn = pad192 <= pad128 + ncol / 64 ? kBatWBN : kBatBN;
+  CUtensorMap wA, wB;
+  make_map(&wA, e->A(set) + r0, 2 * nl, nac, ncol, 2 * nl, 2 * K, 1, cp.w_bn);
+  make_map(&wB, e->B(set) + r0, 2 * nl, nac, ncol, 2 * nl, 2 * K, 1, cp.w_bn);
   const int bat_tx = static_cast<int>((ncol + kBatBN - 1) / kBatBN), bat_ty = static_cast<int>((nl + kBatBM - 1) / kBatBM);
   const uint64_t bat_tiles = static_cast<uint64_t>(bat_tx) * bat_ty * nac;
   const int batw_ty = static_cast<int>((2 * nl + kBatWBM - 1) / kBatWBM);
-  const uint64_t batw_tiles = static_cast<uint64_t>(bat_tx) * batw_ty * nac;
+  const int batw_tx = static_cast<int>((ncol + cp.w_bn - 1) / cp.w_bn);
+  const uint64_t batw_tiles = static_cast<uint64_t>(batw_tx) * batw_ty * nac;
   if (batw_tiles > static_cast<uint64_t>(INT32_MAX)) throw Fail{HSDLA_B200_SIZING_ERROR, "too many batched tiles"};
   // N_L mod 8 in [1, 4]: each segment's last k-slab is half zero-fill (skipped by the kernel)
   const int half = nl % kChunkC >= 1 && nl % kChunkC <= kChunkC / 2;
@@ -242,9 +250,9 @@ static void make_chunk(hsdla_b200_engine* e, int set, uint64_t a0, uint64_t a1, 
   // rows < N_L (W_A) go to X1, the rest (W_B) to X2
   bat_base(cp.w, e->X1 + r0);
   cp.w.L[0] = mW0;
-  cp.w.R[0] = vA;
+  cp.w.R[0] = wA;
   cp.w.L[1] = mW1;
-  cp.w.R[1] = vB;
+  cp.w.R[1] = wB;
   cp.w.kchunks[0] = cp.w.kchunks[1] = chunks_of(nl);
   cp.w.half_last[0] = cp.w.half_last[1] = half;
   cp.w.r_row_z[0] = cp.w.r_row_z[1] = 1;
@@ -252,6 +260,7 @@ static void make_chunk(hsdla_b200_engine* e, int set, uint64_t a0, uint64_t a1, 
   cp.w.m_valid = static_cast<int>(2 * nl);
   cp.w.m_row = static_cast<int>(nl);
   cp.w.out2 = x2 + r0;
+  cp.w.bat_tx = batw_tx;
   cp.w.bat_ty = batw_ty;
   cp.w.bat_tiles = static_cast<int>(batw_tiles);
   cp.grid_batw = dim3(static_cast<unsigned>(std::min<uint64_t>(batw_tiles, e->sms)));
@@ -850,7 +859,7 @@ void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool last, hsd
     timed_op(e, HSDLA_B200_PHASE_Z_LOOP, [&] {
       expand_ops();
       trace_mark(e, s, "x");
-      launch_batw_kernel(e->arith, cp.grid_batw, cp.w, e->stream);  // W_A and W_B
+      launch_batw_kernel(e->arith, cp.w_bn, cp.grid_batw, cp.w, e->stream);  // W_A and W_B
       ++e->launches;
       trace_mark(e, s, "w");
     });

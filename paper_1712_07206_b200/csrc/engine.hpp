@@ -71,6 +71,7 @@ struct ChunkPlan {
   // while B, T, U are still on the wire; (UB)^H (UB) accumulates once they landed)
   CtnParams sA, sB;
   dim3 grid_tri, grid_bat, grid_batw;
+  int w_bn = 0;  // the W launch's tile width (kBatWBN or kBatBN)
 };
 
 struct OpTime {
