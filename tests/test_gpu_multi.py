@@ -382,3 +382,22 @@ def test_split_triangle_launches_in_windows_bands_and_kpoints(restatement, monke
         Hq, Sq, _ = restatement.build_hs_refined(pk)
         assert rel(Hk, Hq) <= TOL and rel(Sk, Sq) <= TOL
     hb.release_cache()
+
+
+@pytest.mark.parametrize("ng", [1, 63, 64, 65, 127, 130, 200, 257, 450])
+def test_split_triangle_launches_edge_sizes(restatement, monkeypatch, ng):
+    """Forced split launches at edge tile counts: one tile (no strictly-lower tiles), a last tile row
+    with 1..8 valid fragment rows, and the kernel layer's herk on the same sizes."""
+    from paper_1712_07206_b200 import kernels as K
+    monkeypatch.setenv("HSDLA_B200_DIAG_SPLIT_MIN", "0")
+    monkeypatch.setenv("HSDLA_B200_ROW_SPLIT_MIN", "0")
+    p = hb.generate_problem(3, 9, ng, 11, 1)
+    Hs, Ss, _ = restatement.build_hs_refined(p)
+    r = hb.build_hs_refined(p)
+    assert rel(r.H, Hs) <= TOL and rel(r.S, Ss) <= TOL
+    C = np.zeros((ng, ng), np.complex128, order="F")
+    K.herk(1.0, p.A, 0.0, C)
+    il = np.tril_indices(ng)
+    want = (p.A.conj().T @ p.A)[il]
+    assert np.linalg.norm(C[il] - want) <= 1e-12 * max(np.linalg.norm(want), 1e-300)
+    hb.release_cache()
