@@ -950,7 +950,7 @@ void engine_build_streamed(hsdla_b200_engine* e, const hsdla_b200_problem* p, ui
                    ops_pinned ? 7 : 3);
       if (!ops_pinned) upload_atoms_staged(e, 0, p, a0, plan[c].a0, plan[c].a1, e->copy_stream, 4);
       HS_CUDA(cudaEventRecord(e->ev_chunk_up[c], e->copy_stream));
-      trace_mark(e, e->copy_stream, "up" + std::to_string(c));
+      if (trace_on()) trace_mark(e, e->copy_stream, "up" + std::to_string(c));
     }
   }
   for (size_t c = 0; c < plan.size(); ++c) {
@@ -969,13 +969,13 @@ void engine_build_streamed(hsdla_b200_engine* e, const hsdla_b200_problem* p, ui
       // already computes chunk c-1 (its phases were enqueued in the previous iteration)
       upload_atoms_staged(e, 0, p, a0, plan[c].a0, plan[c].a1, e->copy_stream, first_split ? 6 : 7);
       HS_CUDA(cudaEventRecord(e->ev_chunk_up[c], e->copy_stream));
-      trace_mark(e, e->copy_stream, "up" + std::to_string(c));
+      if (trace_on()) trace_mark(e, e->copy_stream, "up" + std::to_string(c));
     }
     HS_CUDA(cudaStreamWaitEvent(e->stream, e->ev_chunk_up[c], 0));
     if (c == 0 && !first_split) HS_CUDA(cudaEventRecord(e->ev_begin, e->stream));
-    trace_mark(e, e->stream, "c" + std::to_string(c) + "_start");
+    if (trace_on()) trace_mark(e, e->stream, "c" + std::to_string(c) + "_start");
     enqueue_chunk(e, plan[c], algo, c + 1 == plan.size(), nullptr, first_split);
-    trace_mark(e, e->stream, "c" + std::to_string(c) + "_end");
+    if (trace_on()) trace_mark(e, e->stream, "c" + std::to_string(c) + "_end");
   }
   HS_CUDA(cudaEventRecord(e->ev_up1, e->copy_stream));
   HS_CUDA(cudaEventRecord(e->ev_end, e->stream));

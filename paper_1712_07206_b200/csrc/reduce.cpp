@@ -299,7 +299,7 @@ void enqueue_download(hsdla_b200_engine* e) {
       d.seq.push_back({1, b0, b1, e->ev_dl_h[q]});
     }
     HS_CUDA(cudaEventRecord(e->ev_dl_h[q], cs));
-    trace_mark(e, cs, "dl_h" + std::to_string(q));
+    if (trace_on()) trace_mark(e, cs, "dl_h" + std::to_string(q));
   }
   d.pending = true;
 }
