@@ -352,11 +352,14 @@ static std::vector<uint64_t> stream_bounds(const hsdla_b200_engine* e, double ra
 // full efficiency).
 static void make_pieces(hsdla_b200_engine* e) {
   const double kBandRatio = env_double("HSDLA_B200_BAND_RATIO", 1.0);
-  const int Q = hsdla_b200_engine::kD2hPieces;
   const long long T = static_cast<long long>(tiles_of(e->ng));
   const long long t0 = static_cast<long long>(e->c0 / kTriBM), t1 = static_cast<long long>(tiles_of(e->c1));
   long long total = 0;
   for (long long tj = t0; tj < t1; ++tj) total += T - tj;
+  // 8 bands from 4 tile waves on; smaller triangles 3 (C1, 0.9 waves: 1.32 -> 1.20 ms per pinned call;
+  // N_G 2000: 2.99 -> 2.86 ms; 2 and 4 bands measured in between)
+  const int Qd = total >= 4LL * e->sms ? hsdla_b200_engine::kD2hPieces : 3;
+  const int Q = std::max(1, std::min(hsdla_b200_engine::kD2hPieces, static_cast<int>(env_double("HSDLA_B200_BANDS", Qd))));
   double wsum = 0, w = 1;
   for (int q = 0; q < Q; ++q, w *= kBandRatio) wsum += w;
   e->piece_tiles[0] = static_cast<int>(t0);
@@ -369,7 +372,7 @@ static void make_pieces(hsdla_b200_engine* e) {
     while (tj < t1 && acc + (T - tj) <= target) acc += T - tj++;
     e->piece_tiles[q] = static_cast<int>(tj);
   }
-  e->piece_tiles[Q] = static_cast<int>(t1);
+  for (int q = Q; q <= hsdla_b200_engine::kD2hPieces; ++q) e->piece_tiles[q] = static_cast<int>(t1);
 }
 
 // The device-resident plans (set 0 and, when allocated, set 1); the streamed chunk
@@ -763,9 +766,9 @@ void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool last, hsd
     if (e->wait_before_h) HS_CUDA(cudaStreamWaitEvent(s, e->wait_before_h, 0));  // H storage reuse
     // bands: the one-shot drop-in (download overlaps) and every multi-rank build (the
     // reduce of band q overlaps the compute of band q+1)
-    // (only with >= 4 tile waves: smaller final launches would mostly be stream-K tails)
+    // (from half a tile wave on; below 4 waves in 3 bands, make_pieces)
     const bool grouped = e->comm || !e->local_group.empty();
-    static const double min_waves = env_double("HSDLA_B200_BAND_MIN_WAVES", 4.0);
+    static const double min_waves = env_double("HSDLA_B200_BAND_MIN_WAVES", 0.5);
     if (!(last && (e->band_final_h || grouped) && P.tiles_total >= min_waves * e->sms)) {
       launch_tri(e, P, cp.grid_tri);
       return;
