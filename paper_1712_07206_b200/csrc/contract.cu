@@ -102,6 +102,8 @@ int launch_tri_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStrea
   const int T = P.tiles;
   const int t0 = P.col_t1 > 0 ? P.col_t0 : 0, ndiag = P.col_t1 > 0 ? P.col_t1 - P.col_t0 : T;
   const int nstrict = P.tiles_total - ndiag;
+  // launch k (in issue order) stamps slot P.stamp + k * kStampWords
+  auto slot = [&](int k) { return P.stamp ? P.stamp + k * kStampWords : nullptr; };
   auto grid_of = [&](int tiles) {
     return dim3(static_cast<unsigned>(std::max<long long>(1, std::min<long long>(grid.x, 1LL * tiles * iters))));
   };
@@ -114,6 +116,7 @@ int launch_tri_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStrea
     CtnParams q = P;
     q.with_diag = 1;
     q.epoch = 4 * P.epoch;
+    q.stamp = slot(0);
     tri_kernels[arith]<<<grid_of(P.tiles_total), TriCfg::kThreads, TriCfg::kSmemBytes, s>>>(q);
     HS_CUDA(cudaGetLastError());
     return 1;
@@ -136,6 +139,7 @@ int launch_tri_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStrea
     // last in its enumeration, so the count alone excludes it
     if (nrow > 0 && P.col_t1 <= 0) q.tiles = T - 1;
     q.epoch = 4 * P.epoch;
+    q.stamp = slot(n);
     tri_kernels[arith]<<<grid_of(q.tiles_total), TriCfg::kThreads, TriCfg::kSmemBytes, s>>>(q);
     HS_CUDA(cudaGetLastError());
     ++n;
@@ -147,6 +151,7 @@ int launch_tri_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStrea
     r.row_v = v;
     r.diag_t0 = t0;
     r.epoch = 4 * P.epoch + 2;
+    r.stamp = slot(n);
     row_kernels[arith]<<<grid_of(nrow), TriCfg::kThreads, TriCfg::kSmemBytes, s>>>(r);
     HS_CUDA(cudaGetLastError());
     ++n;
@@ -155,6 +160,7 @@ int launch_tri_kernel(int arith, const dim3& grid, const CtnParams& P, cudaStrea
   d.tiles_total = ndiag;
   d.diag_t0 = t0;
   d.epoch = 4 * P.epoch + 1;
+  d.stamp = slot(n);
   diag_kernels[arith]<<<grid_of(ndiag), TriCfg::kThreads, TriCfg::kSmemBytes, s>>>(d);
   HS_CUDA(cudaGetLastError());
   return n + 1;

@@ -10,6 +10,7 @@ namespace hsdla_b200 {
 
 constexpr int kMaxSeg = 3;
 constexpr int kChunkC = 8;  // complex k per TMA slab (128 B rows)
+constexpr int kStampWords = 4;  // words per launch timestamp slot (stamp.cuh)
 
 // kTri: the strictly-lower tiles of the triangle (or of a column window); kTriDiag: its diagonal
 // tiles (a launch of their own with a warp remapping, ctn_contract.cuh); kBatch: per-atom products.
@@ -53,6 +54,8 @@ struct alignas(64) CtnParams {
   const int* keep_diag_imag;  // TRI, optional: when non-null and *keep_diag_imag != 0 the diagonal's
                               // imaginary part is kept (the original algorithm's full-gemm fold,
                               // pipeline.cpp:266-271, does not zero it); else forced to 0
+  unsigned long long* stamp;  // optional launch timestamp slot (stamp.cuh); launch_tri_kernel gives
+                              // its k-th kernel the slot stamp + k * kStampWords
   double alpha_re, alpha_im;
   double beta;             // real; 0 => C is never read
 };

@@ -3,6 +3,7 @@
 #include "common.hpp"
 #include "device.hpp"
 #include "potrf.cuh"
+#include "stamp.cuh"
 
 namespace hsdla_b200 {
 
@@ -13,13 +14,20 @@ namespace hsdla_b200 {
 // X = diag(u) B for rows [0, Kc) of a K-strided stack (kernels.cpp:438-450);
 // coalesced along K, columns strided over blockIdx.y.
 static __global__ void diag_scale_kernel(const double2* __restrict__ B, const double* __restrict__ u,
-                                  double2* __restrict__ X, uint64_t Kc, uint64_t ld, uint64_t ng) {
+                                  double2* __restrict__ X, uint64_t Kc, uint64_t ld, uint64_t ng,
+                                  unsigned long long* stamp) {
+  stamp_enter(stamp);
   const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= Kc) return;
-  const double s = u[k];
-  for (uint64_t j = blockIdx.y; j < ng; j += gridDim.y) {
-    const double2 b = B[k + j * ld];
-    X[k + j * ld] = make_double2(s * b.x, s * b.y);
+  if (k < Kc) {
+    const double s = u[k];
+    for (uint64_t j = blockIdx.y; j < ng; j += gridDim.y) {
+      const double2 b = B[k + j * ld];
+      X[k + j * ld] = make_double2(s * b.x, s * b.y);
+    }
+  }
+  if (stamp) {
+    __syncthreads();
+    if (threadIdx.x == 0) stamp_leave(stamp);
   }
 }
 
@@ -47,12 +55,26 @@ static __global__ void fill_uniform_kernel(double* __restrict__ p, uint64_t n, u
 // Merged algorithm (wl != nullptr): the stacked left operand of W = M Y per atom instead,
 //   wl[a] = [Paa | Tab] then [Pab | Pbb]  (column i of each N_L x 2 N_L half holds k = 0 .. N_L-1)
 // with Pab(k, i) = conj(T_AB(i, k)) (Pab^H B = T_AB B) and Pbb = full(T_BB) (bscale 1).
+static __device__ __forceinline__ void expand_one(const double2* __restrict__ taa, const double2* __restrict__ tbb,
+                                                  double2* __restrict__ paa, double2* __restrict__ pbb, int nl,
+                                                  double bscale, const double2* __restrict__ tab,
+                                                  double2* __restrict__ wl, uint64_t idx);
 static __global__ void expand_hermitian_kernel(const double2* __restrict__ taa, const double2* __restrict__ tbb,
                                         double2* __restrict__ paa, double2* __restrict__ pbb, int nl,
                                         uint64_t total, double bscale, const double2* __restrict__ tab,
-                                        double2* __restrict__ wl) {
+                                        double2* __restrict__ wl, unsigned long long* stamp) {
+  stamp_enter(stamp);
   const uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (idx >= total) return;
+  if (idx < total) expand_one(taa, tbb, paa, pbb, nl, bscale, tab, wl, idx);
+  if (stamp) {
+    __syncthreads();
+    if (threadIdx.x == 0) stamp_leave(stamp);
+  }
+}
+static __device__ __forceinline__ void expand_one(const double2* __restrict__ taa, const double2* __restrict__ tbb,
+                                                  double2* __restrict__ paa, double2* __restrict__ pbb, int nl,
+                                                  double bscale, const double2* __restrict__ tab,
+                                                  double2* __restrict__ wl, uint64_t idx) {
   const uint64_t blk = static_cast<uint64_t>(nl) * nl;
   const uint64_t a = idx / blk;
   const int r = static_cast<int>(idx - a * blk);
@@ -101,10 +123,10 @@ __global__ void sum_partials_kernel(double2* __restrict__ out, const SumIn in, i
 }
 
 void launch_diag_scale(const double2* B, const double* u, double2* X, uint64_t Kc, uint64_t ld, uint64_t ng,
-                       cudaStream_t s) {
+                       cudaStream_t s, unsigned long long* stamp) {
   if (!Kc || !ng) return;
   const dim3 g(static_cast<unsigned>((Kc + 255) / 256), static_cast<unsigned>(std::min<uint64_t>(ng, 2048)));
-  diag_scale_kernel<<<g, 256, 0, s>>>(B, u, X, Kc, ld, ng);
+  diag_scale_kernel<<<g, 256, 0, s>>>(B, u, X, Kc, ld, ng, stamp);
   HS_CUDA(cudaGetLastError());
 }
 
@@ -114,25 +136,26 @@ void launch_fill_uniform(double* p, uint64_t n, uint64_t seed, double lo, double
 }
 
 void launch_expand_hermitian(const double2* taa, const double2* tbb, double2* paa, double2* pbb, int nl,
-                             uint64_t total, double bscale, const double2* tab, double2* wl, cudaStream_t s) {
+                             uint64_t total, double bscale, const double2* tab, double2* wl, cudaStream_t s,
+                             unsigned long long* stamp) {
   if (!total) return;
   expand_hermitian_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(taa, tbb, paa, pbb, nl, total,
-                                                                                      bscale, tab, wl);
+                                                                                      bscale, tab, wl, stamp);
   HS_CUDA(cudaGetLastError());
 }
 
 void launch_potrf_batched(const double2* taa, double2* q, int32_t* info, int nl, uint64_t nb, int* n_fail,
-                          cudaStream_t s) {
+                          cudaStream_t s, unsigned long long* stamp) {
   if (!nb) return;
-  potrf_batched_kernel<<<static_cast<unsigned>(nb), 128, 0, s>>>(taa, q, info, nl, n_fail);
+  potrf_batched_kernel<<<static_cast<unsigned>(nb), 128, 0, s>>>(taa, q, info, nl, n_fail, stamp);
   HS_CUDA(cudaGetLastError());
 }
 
 void launch_select_left(const double2* X1, const double2* A, const int32_t* info, double2* X2, uint64_t Kc,
-                        uint64_t ld, uint64_t ng, int nl, cudaStream_t s) {
+                        uint64_t ld, uint64_t ng, int nl, cudaStream_t s, unsigned long long* stamp) {
   if (!Kc || !ng) return;
   const dim3 g(static_cast<unsigned>((Kc + 255) / 256), static_cast<unsigned>(std::min<uint64_t>(ng, 2048)));
-  select_left_kernel<<<g, 256, 0, s>>>(X1, A, info, X2, Kc, ld, ng, nl);
+  select_left_kernel<<<g, 256, 0, s>>>(X1, A, info, X2, Kc, ld, ng, nl, stamp);
   HS_CUDA(cudaGetLastError());
 }
 

@@ -45,7 +45,7 @@ void engine_free(hsdla_b200_engine* e) {
   for (void* p : {e->lapw_scratch, (void*)e->info, (void*)e->n_fail, (void*)e->sk_ws, (void*)e->sk_flags,
                   (void*)e->Aset[0], (void*)e->Bset[0], (void*)e->Aset[1], (void*)e->Bset[1], (void*)e->X1,
                   (void*)e->X2, (void*)e->Tab, (void*)e->Taa, (void*)e->Tbb, (void*)e->Paa, (void*)e->Pbb,
-                  (void*)e->Wl, (void*)e->U, (void*)e->Hp, (void*)e->Sp})
+                  (void*)e->Wl, (void*)e->U, (void*)e->Hp, (void*)e->Sp, (void*)e->d_stamp})
     if (p) cudaFree(p);
   if (e->host_stage) cudaFreeHost(e->host_stage);
   release_file_view(e);
@@ -56,13 +56,12 @@ void engine_free(hsdla_b200_engine* e) {
     if (e->stage_ev[i]) cudaEventDestroy(e->stage_ev[i]);
     if (e->stage_buf[i]) cudaFreeHost(e->stage_buf[i]);
   }
-  for (cudaEvent_t ev : e->ev_pool) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e->tr_pool) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e->ev_chunk_up) cudaEventDestroy(ev);
   for (int q = 0; q < hsdla_b200_engine::kD2hPieces; ++q)
     for (cudaEvent_t ev : {e->ev_h_band[q], e->ev_h_red[q], e->ev_dl_h[q]})
       if (ev) cudaEventDestroy(ev);
-  for (cudaEvent_t ev : {e->ev_a0, e->ev_ops, e->ev_cs_order, e->ev_begin, e->ev_end, e->ev_s_done, e->ev_s_red, e->ev_reduce_end,
+  for (cudaEvent_t ev : {e->ev_a0, e->ev_ops, e->ev_cs_order, e->ev_begin, e->ev_end, e->ev_end_t, e->ev_s_done, e->ev_s_red, e->ev_reduce_end,
                          e->ev_up0, e->ev_up1, e->ev_dl_s, e->ev_setup0, e->ev_setup1, e->ev_setup_mid})
     if (ev) cudaEventDestroy(ev);
   for (auto& t : e->ring)
@@ -462,10 +461,11 @@ hsdla_b200_engine* engine_create(int device, const ShardSpec& sp) {
     HS_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
     HS_CUDA(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
     HS_CUDA(cudaStreamCreateWithFlags(&e->comm_stream, cudaStreamNonBlocking));
-    for (cudaEvent_t* ev : {&e->ev_begin, &e->ev_end, &e->ev_reduce_end, &e->ev_up0, &e->ev_up1, &e->ev_setup0,
+    for (cudaEvent_t* ev : {&e->ev_begin, &e->ev_end_t, &e->ev_reduce_end, &e->ev_up0, &e->ev_up1, &e->ev_setup0,
                             &e->ev_setup1, &e->ev_setup_mid})
       HS_CUDA(cudaEventCreate(ev));
-    for (cudaEvent_t* ev : {&e->ev_s_done, &e->ev_s_red, &e->ev_dl_s, &e->ev_a0, &e->ev_ops, &e->ev_cs_order})
+    for (cudaEvent_t* ev : {&e->ev_end, &e->ev_s_done, &e->ev_s_red, &e->ev_dl_s, &e->ev_a0, &e->ev_ops,
+                            &e->ev_cs_order})
       HS_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     for (int q = 0; q < hsdla_b200_engine::kD2hPieces; ++q)
       for (cudaEvent_t* ev : {&e->ev_h_band[q], &e->ev_h_red[q], &e->ev_dl_h[q]})
@@ -491,6 +491,8 @@ hsdla_b200_engine* engine_create(int device, const ShardSpec& sp) {
     dalloc(e.get(), &e->sk_ws, static_cast<uint64_t>(e->sms) * kSkSlot);
     dalloc(e.get(), &e->sk_flags, static_cast<uint64_t>(e->sms));
     HS_CUDA(cudaMemset(e->sk_flags, 0, e->sms * sizeof(uint32_t)));
+    dalloc(e.get(), &e->d_stamp, static_cast<uint64_t>(hsdla_b200_engine::kMaxStamps) * kStampWords);
+    HS_CUDA(cudaMemset(e->d_stamp, 0, hsdla_b200_engine::kMaxStamps * kStampWords * sizeof(unsigned long long)));
     set_geometry(e.get(), sp.ng, sp.c0, c1);
   } catch (...) {
     engine_free(e.get());
@@ -675,13 +677,28 @@ void engine_upload(hsdla_b200_engine* e, const hsdla_b200_problem* p, uint64_t a
 }
 
 // ---- launches ---------------------------------------------------------------
-static cudaEvent_t next_event(hsdla_b200_engine* e) {
-  if (e->ev_used == e->ev_pool.size()) {
-    cudaEvent_t ev;
-    HS_CUDA(cudaEventCreate(&ev));
-    e->ev_pool.push_back(ev);
-  }
-  return e->ev_pool[e->ev_used++];
+// The next `n` launch timestamp slots (stamp.cuh), or nullptr (untimed launch) once the build
+// has used them all; take_stamp commits one slot, launches that may use up to n commit what they used.
+static unsigned long long* stamp_slots(hsdla_b200_engine* e, int n) {
+  return e->stamp_used + n <= hsdla_b200_engine::kMaxStamps ? e->d_stamp + e->stamp_used * kStampWords : nullptr;
+}
+static unsigned long long* take_stamp(hsdla_b200_engine* e) {
+  unsigned long long* p = stamp_slots(e, 1);
+  if (p) ++e->stamp_used;
+  return p;
+}
+
+// Build brackets.  ev_end orders the downloads after the build; the timing events exist for the
+// reduce's timeline only (a timing event on the compute stream costs 30-55 us while a copy is in
+// flight, stamp.cuh), so engines that never reduce with others skip them.
+static bool grouped(const hsdla_b200_engine* e) { return e->comm || !e->local_group.empty(); }
+void mark_build_begin(hsdla_b200_engine* e) {
+  e->marks_timed = grouped(e);
+  if (e->marks_timed) HS_CUDA(cudaEventRecord(e->ev_begin, e->stream));
+}
+void mark_build_end(hsdla_b200_engine* e) {
+  HS_CUDA(cudaEventRecord(e->ev_end, e->stream));
+  if (e->marks_timed) HS_CUDA(cudaEventRecord(e->ev_end_t, e->stream));
 }
 
 void copy_after_compute(hsdla_b200_engine* e) {
@@ -706,8 +723,8 @@ void trace_mark(hsdla_b200_engine* e, cudaStream_t s, const std::string& what) {
 static const char* const kPhaseNames[HSDLA_B200_N_PHASES] = {"s",         "z_loop",    "her2k",       "hemm_loop",
                                                              "herkx",     "chol_loop", "h_aa_update", "-"};
 
-// CUDA-event bracket of one phase op on the compute stream (plus an NVTX range
-// around its enqueue, for nsys / ncu --nvtx timelines).
+// One phase op on the compute stream: the launch timestamp slots its kernels take (plus an NVTX
+// range around its enqueue, for nsys / ncu --nvtx timelines).
 struct NvtxRange {
   explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
   ~NvtxRange() { nvtxRangePop(); }
@@ -715,20 +732,23 @@ struct NvtxRange {
 template <class F>
 static void timed_op(hsdla_b200_engine* e, int phase, F&& body) {
   NvtxRange range(kPhaseNames[phase]);
-  cudaEvent_t b = next_event(e), end = next_event(e);
-  HS_CUDA(cudaEventRecord(b, e->stream));
+  const int s0 = e->stamp_used;
   body();
-  HS_CUDA(cudaEventRecord(end, e->stream));
-  e->ops.push_back({phase, b, end});
+  e->ops.push_back({phase, s0, e->stamp_used});
 }
 
 static void launch_tri(hsdla_b200_engine* e, const CtnParams& P, const dim3& grid) {
   CtnParams q = P;
   q.epoch = ++e->epoch;  // fresh stream-K flag generation per launch
-  e->launches += launch_tri_kernel(e->arith, grid, q, e->stream);
+  q.stamp = stamp_slots(e, 3);  // up to 3 kernels (strictly-lower, ragged row, diagonal)
+  const int n = launch_tri_kernel(e->arith, grid, q, e->stream);
+  e->launches += n;
+  if (q.stamp) e->stamp_used += n;
 }
 static void launch_bat(hsdla_b200_engine* e, const CtnParams& P, const dim3& grid) {
-  launch_bat_kernel(e->arith, grid, P, e->stream);
+  CtnParams q = P;
+  q.stamp = take_stamp(e);
+  launch_bat_kernel(e->arith, grid, q, e->stream);
   ++e->launches;
 }
 
@@ -767,9 +787,8 @@ void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool last, hsd
     // bands: the one-shot drop-in (download overlaps) and every multi-rank build (the
     // reduce of band q overlaps the compute of band q+1)
     // (from half a tile wave on; below 4 waves in 3 bands, make_pieces)
-    const bool grouped = e->comm || !e->local_group.empty();
     static const double min_waves = env_double("HSDLA_B200_BAND_MIN_WAVES", 0.5);
-    if (!(last && (e->band_final_h || grouped) && P.tiles_total >= min_waves * e->sms)) {
+    if (!(last && (e->band_final_h || grouped(e)) && P.tiles_total >= min_waves * e->sms)) {
       launch_tri(e, P, cp.grid_tri);
       return;
     }
@@ -798,7 +817,8 @@ void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool last, hsd
     const uint64_t total = nac * nl * nl, off = cp.a0 * nl * nl;
     const bool merged = algo == HSDLA_B200_ALGO_REFINED_MERGED;
     launch_expand_hermitian(e->Taa + off, e->Tbb + off, e->Paa + off, e->Pbb + off, static_cast<int>(nl), total,
-                            merged ? 1.0 : 0.5, e->Tab + off, merged ? e->Wl + 4 * off : nullptr, s);
+                            merged ? 1.0 : 0.5, e->Tab + off, merged ? e->Wl + 4 * off : nullptr, s,
+                            take_stamp(e));
     ++e->launches;
   };
   // operators uploaded on the copy stream (engine_upload_operators): wait before expanding
@@ -809,7 +829,7 @@ void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool last, hsd
   auto phase_s = [&] {
     timed_op(e, HSDLA_B200_PHASE_S, [&] {
       if (e->wait_before_s) HS_CUDA(cudaStreamWaitEvent(s, e->wait_before_s, 0));
-      launch_diag_scale(cp.B + r0, e->U + r0, e->X1 + r0, Kc, e->K, ncol, s);
+      launch_diag_scale(cp.B + r0, e->U + r0, e->X1 + r0, Kc, e->K, ncol, s, take_stamp(e));
       ++e->launches;
       if (kt) HS_CUDA(cudaEventRecord(kt->s0, s));
       launch_tri(e, s_rest ? cp.sB : cp.s, cp.grid_tri);
@@ -837,11 +857,11 @@ void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool last, hsd
     timed_op(e, HSDLA_B200_PHASE_CHOL_LOOP, [&] {
       if (cp.a0 == 0) HS_CUDA(cudaMemsetAsync(e->n_fail, 0, sizeof(int), s));  // first chunk of the build
       launch_potrf_batched(e->Taa + cp.a0 * nl * nl, e->Paa + cp.a0 * nl * nl, e->info + cp.a0,
-                           static_cast<int>(nl), nac, e->n_fail, s);
+                           static_cast<int>(nl), nac, e->n_fail, s, take_stamp(e));
       ++e->launches;
       launch_bat(e, cp.x, cp.grid_bat);  // W_a = Q_a^H A_a: trmm (HPD) or hemm (failed)
       launch_select_left(e->X1 + r0, cp.A + r0, e->info + cp.a0, e->X2 + r0, Kc, e->K, ncol,
-                         static_cast<int>(nl), s);
+                         static_cast<int>(nl), s, take_stamp(e));
       ++e->launches;
     });
     timed_op(e, HSDLA_B200_PHASE_H_AA_UPDATE, [&] { final_h(cp.haa); });
@@ -862,7 +882,9 @@ void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool last, hsd
     timed_op(e, HSDLA_B200_PHASE_Z_LOOP, [&] {
       expand_ops();
       trace_mark(e, s, "x");
-      launch_batw_kernel(e->arith, cp.w_bn, cp.grid_batw, cp.w, e->stream);  // W_A and W_B
+      CtnParams w = cp.w;
+      w.stamp = take_stamp(e);
+      launch_batw_kernel(e->arith, cp.w_bn, cp.grid_batw, w, e->stream);  // W_A and W_B
       ++e->launches;
       trace_mark(e, s, "w");
     });
@@ -891,7 +913,8 @@ void begin_build(hsdla_b200_engine* e, int algo) {
   e->last_algo = algo;
   e->reduced = false;
   e->uploaded_streamed = false;
-  e->ev_used = 0;
+  e->stamp_used = 0;
+  e->marks_timed = false;
   e->ops.clear();
   e->tr_marks.clear();
   e->built = true;
@@ -912,10 +935,10 @@ void engine_build(hsdla_b200_engine* e, int algo) {
     kt.flops_h = static_cast<uint64_t>(kt.flops_h * f);
     kt.flops_s = static_cast<uint64_t>(kt.flops_s * f);
   }
-  HS_CUDA(cudaEventRecord(e->ev_begin, e->stream));
+  mark_build_begin(e);
   enqueue_chunk(e, e->whole[0], algo, true, &kt);
   e->ops_pending = false;
-  HS_CUDA(cudaEventRecord(e->ev_end, e->stream));
+  mark_build_end(e);
   kt.pending = true;
 }
 
@@ -964,7 +987,7 @@ void engine_build_streamed(hsdla_b200_engine* e, const hsdla_b200_problem* p, ui
         HS_CUDA(cudaEventRecord(e->ev_a0, e->copy_stream));
       }
       HS_CUDA(cudaStreamWaitEvent(e->stream, e->ev_a0, 0));
-      HS_CUDA(cudaEventRecord(e->ev_begin, e->stream));
+      mark_build_begin(e);
       enqueue_s_first(e, plan[c]);
     }
     if (!pinned) {
@@ -975,13 +998,13 @@ void engine_build_streamed(hsdla_b200_engine* e, const hsdla_b200_problem* p, ui
       if (trace_on()) trace_mark(e, e->copy_stream, "up" + std::to_string(c));
     }
     HS_CUDA(cudaStreamWaitEvent(e->stream, e->ev_chunk_up[c], 0));
-    if (c == 0 && !first_split) HS_CUDA(cudaEventRecord(e->ev_begin, e->stream));
+    if (c == 0 && !first_split) mark_build_begin(e);
     if (trace_on()) trace_mark(e, e->stream, "c" + std::to_string(c) + "_start");
     enqueue_chunk(e, plan[c], algo, c + 1 == plan.size(), nullptr, first_split);
     if (trace_on()) trace_mark(e, e->stream, "c" + std::to_string(c) + "_end");
   }
   HS_CUDA(cudaEventRecord(e->ev_up1, e->copy_stream));
-  HS_CUDA(cudaEventRecord(e->ev_end, e->stream));
+  mark_build_end(e);
   e->uploaded_streamed = true;
   if (trace_on() && !pinned) {
     std::fprintf(stderr, "[hsdla_b200 trace] pageable staging: packed %.0f MB in %.1f ms (%.1f GB/s), waited %.1f ms "
@@ -1083,7 +1106,7 @@ void engine_kpoints(hsdla_b200_engine* e, const hsdla_b200_problem* common, uint
     begin_build(e, algo);
     e->band_final_h = true;
     HS_CUDA(cudaStreamWaitEvent(e->stream, e->ev_kup[set], 0));
-    HS_CUDA(cudaEventRecord(e->ev_begin, e->stream));
+    mark_build_begin(e);
     // S and H storage: k-1's downloads (enqueued in the previous iteration) first
     e->wait_before_s = e->ev_dl_s;
     e->wait_before_h = e->ev_dl_h[hsdla_b200_engine::kD2hPieces - 1];
@@ -1097,7 +1120,7 @@ void engine_kpoints(hsdla_b200_engine* e, const hsdla_b200_problem* common, uint
     e->wait_before_s = e->wait_before_h = nullptr;
     e->band_final_h = false;
     HS_CUDA(cudaEventRecord(e->ev_kbuilt[set], e->stream));
-    HS_CUDA(cudaEventRecord(e->ev_end, e->stream));
+    mark_build_end(e);
     const double t_enq = trace_on() ? host_ms() : 0.0;
     if (k + 1 < nk) upload(k + 1);  // overlaps build k
     const double t_up = trace_on() ? host_ms() : 0.0;

@@ -76,7 +76,7 @@ struct ChunkPlan {
 
 struct OpTime {
   int phase;
-  cudaEvent_t b, e;
+  int s0, s1;  // the launch timestamp slots [s0, s1) of its kernels (stamp.cuh)
 };
 
 // A packed-lower index range [b0, b1) (global indices) of S (h == 0) or H (h == 1) copied to
@@ -146,10 +146,16 @@ struct hsdla_b200_engine {
   cudaEvent_t ev_kup[2] = {}, ev_kbuilt[2] = {};
   cudaEvent_t wait_before_s = nullptr, wait_before_h = nullptr;  // next enqueue_chunk waits (storage reuse)
   // per-build timing
-  std::vector<cudaEvent_t> ev_pool;
-  size_t ev_used = 0;
+  // launch timestamp slots of the current build (stamp.cuh): every kernel of a timed phase stamps
+  // one; engine_sync reads them back for the phase times and the device time
+  static constexpr int kMaxStamps = 1024;
+  unsigned long long* d_stamp = nullptr;
+  int stamp_used = 0;
   std::vector<hsdla_b200::OpTime> ops;
-  cudaEvent_t ev_begin = nullptr, ev_end = nullptr, ev_s_done = nullptr, ev_s_red = nullptr,
+  // ev_end: the build's end (ordering only).  ev_begin / ev_end_t: timing events around the build,
+  // recorded only by engines that reduce with others (their reduce is timed by events)
+  bool marks_timed = false;  // this build recorded ev_begin / ev_end_t (grouped when it began)
+  cudaEvent_t ev_begin = nullptr, ev_end = nullptr, ev_end_t = nullptr, ev_s_done = nullptr, ev_s_red = nullptr,
               ev_reduce_end = nullptr, ev_up0 = nullptr, ev_up1 = nullptr,
               ev_a0 = nullptr,   // the first streamed chunk's A rows landed
               ev_ops = nullptr,  // operators uploaded on the copy stream (engine_upload_operators)
@@ -262,6 +268,10 @@ void trace_mark(hsdla_b200_engine* e, cudaStream_t s, const std::string& what);
 // The copy stream waits for everything enqueued on the compute stream so far (the previous
 // build, and uploads engine_upload issued there) before it overwrites the inputs.
 void copy_after_compute(hsdla_b200_engine* e);
+// The build's begin / end marks on the compute stream (ev_end: ordering; timing events only
+// for engines that reduce with others).
+void mark_build_begin(hsdla_b200_engine* e);
+void mark_build_end(hsdla_b200_engine* e);
 void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool last, hsdla_b200_engine::KTimer* kt,
                    bool s_rest = false);
 char* stage_acquire(hsdla_b200_engine* e, int& slot);

@@ -230,11 +230,11 @@ void engine_build_file(hsdla_b200_engine* e, const char* path, uint64_t a0, int 
     load_atoms_from_file(e, f.fd, h, a0, plan[c].a0, plan[c].a1, e->copy_stream);
     HS_CUDA(cudaEventRecord(e->ev_chunk_up[c], e->copy_stream));
     HS_CUDA(cudaStreamWaitEvent(e->stream, e->ev_chunk_up[c], 0));
-    if (c == 0) HS_CUDA(cudaEventRecord(e->ev_begin, e->stream));
+    if (c == 0) mark_build_begin(e);
     enqueue_chunk(e, plan[c], algo, c + 1 == plan.size(), nullptr);
   }
   HS_CUDA(cudaEventRecord(e->ev_up1, e->copy_stream));
-  HS_CUDA(cudaEventRecord(e->ev_end, e->stream));
+  mark_build_end(e);
   e->uploaded_streamed = true;
 }
 

@@ -29,12 +29,16 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "stamp.cuh"
+
 namespace hsdla_b200 {
 
 // n_fail (nullable) counts the atoms that did not factorise.
 __global__ void __launch_bounds__(128) potrf_batched_kernel(const double2* __restrict__ taa, double2* __restrict__ q,
                                                             int32_t* __restrict__ info, int nl,
-                                                            int* __restrict__ n_fail = nullptr) {
+                                                            int* __restrict__ n_fail = nullptr,
+                                                            unsigned long long* stamp = nullptr) {
+  stamp_enter(stamp);
   const uint64_t blk = static_cast<uint64_t>(nl) * nl;
   const double2* T = taa + blockIdx.x * blk;
   double2* L = q + blockIdx.x * blk;
@@ -92,18 +96,28 @@ __global__ void __launch_bounds__(128) potrf_batched_kernel(const double2* __res
     info[blockIdx.x] = fail_at;
     if (fail_at >= 0 && n_fail) atomicAdd(n_fail, 1);
   }
+  if (stamp) {
+    __syncthreads();
+    if (threadIdx.x == 0) stamp_leave(stamp);
+  }
 }
 
 // X2[r, j] = info[atom(r)] < 0 ? X1[r, j] : A[r, j] for the rows [0, Kc) of a chunk
 // (pointers already offset to the chunk's first row; ld = K).
 __global__ void select_left_kernel(const double2* __restrict__ X1, const double2* __restrict__ A,
                                    const int32_t* __restrict__ info, double2* __restrict__ X2, uint64_t Kc,
-                                   uint64_t ld, uint64_t ng, int nl) {
+                                   uint64_t ld, uint64_t ng, int nl, unsigned long long* stamp = nullptr) {
+  stamp_enter(stamp);
   const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= Kc) return;
-  const bool hpd = info[k / nl] < 0;
-  const double2* src = hpd ? X1 : A;
-  for (uint64_t j = blockIdx.y; j < ng; j += gridDim.y) X2[k + j * ld] = src[k + j * ld];
+  if (k < Kc) {
+    const bool hpd = info[k / nl] < 0;
+    const double2* src = hpd ? X1 : A;
+    for (uint64_t j = blockIdx.y; j < ng; j += gridDim.y) X2[k + j * ld] = src[k + j * ld];
+  }
+  if (stamp) {
+    __syncthreads();
+    if (threadIdx.x == 0) stamp_leave(stamp);
+  }
 }
 
 }  // namespace hsdla_b200

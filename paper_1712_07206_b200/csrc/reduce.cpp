@@ -130,6 +130,12 @@ void group_reduce(const std::vector<hsdla_b200_engine*>& g, int mode, int root) 
       g[r]->rank = r;
     }
   }
+  // a group formed after its builds began: the reduce is timed from here (the builds' end)
+  for (hsdla_b200_engine* e : g)
+    if (!e->marks_timed) {
+      HS_CUDA(cudaSetDevice(e->device));
+      HS_CUDA(cudaEventRecord(e->ev_end_t, e->stream));
+    }
   const std::vector<Range> segs = segments(g[0]);
   const bool banded = g[0]->banded;
   auto run = [&](bool s_matrix) {
@@ -250,10 +256,24 @@ void engine_sync(hsdla_b200_engine* e, hsdla_b200_stats* st) {
   }
   st->n_hpd = e->n_hpd_last;
   st->executed_flops = executed_flops(e->na, e->nl, e->ng, e->arith, e->last_algo, e->row1 - e->row0);
-  for (const OpTime& op : e->ops) st->phase_seconds[op.phase] += ev_ms(op.b, op.e) * 1e-3;
-  const cudaEvent_t last = e->reduced ? e->ev_reduce_end : e->ev_end;
-  st->device_seconds = ev_ms(e->ev_begin, last) * 1e-3;
-  st->reduce_seconds = e->reduced ? ev_ms(e->ev_end, e->ev_reduce_end) * 1e-3 : 0.0;
+  // phase and device times from the launch timestamp slots (stamp.cuh): a phase op spans its
+  // first kernel's start to its last kernel's end; the build spans all of its kernels
+  std::vector<unsigned long long> ts(static_cast<size_t>(e->stamp_used) * kStampWords);
+  if (!ts.empty())
+    HS_CUDA(cudaMemcpy(ts.data(), e->d_stamp, ts.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  auto span = [&](int s0, int s1) {
+    unsigned long long t0 = ~0ull, t1 = 0;
+    for (int i = s0; i < s1; ++i) {
+      t0 = std::min(t0, ts[static_cast<size_t>(i) * kStampWords]);
+      t1 = std::max(t1, ts[static_cast<size_t>(i) * kStampWords + 1]);
+    }
+    return t1 > t0 ? static_cast<double>(t1 - t0) * 1e-9 : 0.0;
+  };
+  for (const OpTime& op : e->ops) st->phase_seconds[op.phase] += span(op.s0, op.s1);
+  // (the reduce tail after the build's end; a banded reduce can finish with the build)
+  st->reduce_seconds = e->reduced ? std::max(0.0, ev_ms(e->ev_end_t, e->ev_reduce_end) * 1e-3) : 0.0;
+  st->device_seconds = e->reduced && e->marks_timed ? ev_ms(e->ev_begin, e->ev_reduce_end) * 1e-3
+                                                    : span(0, e->stamp_used) + st->reduce_seconds;
   if (e->uploaded_streamed) st->h2d_seconds = ev_ms(e->ev_up0, e->ev_up1) * 1e-3;
   st->kernel_launches = e->launches;
 }

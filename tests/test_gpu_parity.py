@@ -544,3 +544,34 @@ def test_kpoint_batch_banded_final_h_storage_reuse():
             assert rel(H, want.H) <= 1e-13 and rel(S, want.S) <= 1e-13, k
     finally:
         hb.release_cache()
+
+
+@pytest.mark.parametrize("algo", ["merged", "refined", "original"])
+def test_phase_times_from_launch_stamps(algo):
+    """Phase and device times come from the kernels' own %globaltimer stamps (stamp.cuh), not
+    from CUDA timing events on the compute stream: every phase the algorithm runs is timed,
+    phases are disjoint (their sum stays within the device time) and the device time of a
+    device-resident build agrees with the host's wall clock around it."""
+    import time
+    p = hb.generate_problem(16, 49, 1000, 1, 0)
+    # streamed drop-in: copies overlap the kernels
+    r = hb.build_hs_original(p) if algo == "original" else hb.build_hs_refined(p, hb.PipelineConfig(algo=algo))
+    ph = r.stats["phase_seconds"]
+    ran = {"merged": ["s", "z_loop", "her2k"], "refined": ["s", "z_loop", "her2k", "hemm_loop", "herkx"],
+           "original": ["z_loop", "her2k", "s", "chol_loop", "h_aa_update"]}[algo]
+    for k in ran:
+        assert ph[k] > 0, (k, ph)
+    dev = r.stats["device_seconds"]
+    assert 0 < sum(ph.values()) <= dev * 1.001 + 1e-6, (ph, dev)
+    e = hb.Engine(0, 16, 49, 1000)
+    e.upload(p)
+    for _ in range(3):  # warm up
+        e.build(algo)
+        e.sync()
+    t = time.perf_counter()
+    e.build(algo)
+    st = e.sync()
+    wall = time.perf_counter() - t
+    e.close()
+    assert 0 < st["device_seconds"] <= wall, (st["device_seconds"], wall)
+    assert sum(st["phase_seconds"].values()) <= st["device_seconds"] * 1.001 + 1e-6
