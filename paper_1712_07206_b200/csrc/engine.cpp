@@ -936,7 +936,16 @@ void engine_build(hsdla_b200_engine* e, int algo) {
     kt.flops_s = static_cast<uint64_t>(kt.flops_s * f);
   }
   mark_build_begin(e);
-  enqueue_chunk(e, e->whole[0], algo, true, &kt);
+  // HSDLA_B200_CHUNKED_BUILD=1 (tuning): the device-resident inputs in the streamed drop-in's
+  // atom chunks (the chunking's own cost, without the uploads)
+  static const bool chunked = env_double("HSDLA_B200_CHUNKED_BUILD", 0) != 0;
+  if (chunked && whole(e)) {
+    ensure_streamed_plans(e);
+    for (size_t c = 0; c < e->streamed.size(); ++c)
+      enqueue_chunk(e, e->streamed[c], algo, c + 1 == e->streamed.size(), c + 1 == e->streamed.size() ? &kt : nullptr);
+  } else {
+    enqueue_chunk(e, e->whole[0], algo, true, &kt);
+  }
   e->ops_pending = false;
   mark_build_end(e);
   kt.pending = true;

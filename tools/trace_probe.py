@@ -25,8 +25,9 @@ for kind in kinds:
         t = time.perf_counter()
         r = hb.build_hs_refined(p, H=H, S=S)
         dt = time.perf_counter() - t
+        ph = " ".join(f"{k} {v * 1e3:.3f}" for k, v in r.stats["phase_seconds"].items() if v)
         print(f"{name} {kind} call {it}: wall {dt*1e3:.3f} ms ({led/dt/1e12:.2f} TF/s) device "
-              f"{r.stats['device_seconds']*1e3:.3f}", flush=True)
+              f"{r.stats['device_seconds']*1e3:.3f}; phases {ph}", flush=True)
     if kind == "pinned":
         for b in bufs:
             hb.host_unregister(b)

@@ -72,8 +72,9 @@ void run(const char* name, double2* A, double2* B, double2* out, uint64_t K, uin
     d.tiles_total = tiles;
     d.diag_t0 = 0;
     d.epoch = P.epoch | 0x40000000u;
-    kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes>>>(P);
-    dkern<<<grid, Cfg::kThreads, Cfg::kSmemBytes>>>(d);
+    static const char* only = getenv("TUNE_ONLY");  // "strict" | "diag": one of the two launches
+    if (!only || only[0] != 'd') kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes>>>(P);
+    if (!only || only[0] != 's') dkern<<<grid, Cfg::kThreads, Cfg::kSmemBytes>>>(d);
   };
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
