@@ -259,8 +259,11 @@ void engine_sync(hsdla_b200_engine* e, hsdla_b200_stats* st) {
   // phase and device times from the launch timestamp slots (stamp.cuh): a phase op spans its
   // first kernel's start to its last kernel's end; the build spans all of its kernels
   std::vector<unsigned long long> ts(static_cast<size_t>(e->stamp_used) * kStampWords);
-  if (!ts.empty())
-    HS_CUDA(cudaMemcpy(ts.data(), e->d_stamp, ts.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  if (!ts.empty()) {  // on the engine's own stream: no implicit sync with the legacy default stream
+    HS_CUDA(cudaMemcpyAsync(ts.data(), e->d_stamp, ts.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                            e->stream));
+    HS_CUDA(cudaStreamSynchronize(e->stream));
+  }
   auto span = [&](int s0, int s1) {
     unsigned long long t0 = ~0ull, t1 = 0;
     for (int i = s0; i < s1; ++i) {
