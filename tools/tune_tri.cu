@@ -101,6 +101,28 @@ void run(const char* name, double2* A, double2* B, double2* out, uint64_t K, uin
     if (ref3m.empty()) ref3m = h;
     for (size_t i = 0; i < h.size(); ++i) ndiff += h[i] != ref3m[i];
   }
+#ifdef HSDLA_EXP_TILE_CLOCK
+  {  // per-tile SM clocks of the last launch (tools/tile_clock.patch): whole tiles only
+    static long long h[148][64][4];
+    cudaMemcpyFromSymbol(h, g_tclk, sizeof(h));
+    double kl = 0, ep = 0, gap = 0;
+    int nt = 0, ng2 = 0;
+    for (int b = 0; b < 148; ++b)
+      for (int i = 0; i < 64; ++i) {
+        if (h[b][i][0] == 0 || h[b][i][2] < h[b][i][0]) break;
+        if (h[b][i][3] / 100000000LL != 0) continue;
+        kl += h[b][i][1] - h[b][i][0];
+        ep += h[b][i][2] - h[b][i][1];
+        ++nt;
+        if (i + 1 < 64 && h[b][i + 1][0] > h[b][i][2]) {
+          gap += h[b][i + 1][0] - h[b][i][2];
+          ++ng2;
+        }
+      }
+    printf("  per whole tile (%d tiles, %d k-slabs): k-loop %.0f clk, epilogue %.0f clk, gap %.0f clk\n", nt,
+           2 * (int)((K + 7) / 8), kl / nt, ep / nt, ng2 ? gap / ng2 : 0.0);
+  }
+#endif
   printf("%-34s occ %d grid %6d  %8.3f ms  %6.2f TF/s(ledger)  diff-vs-3M %zu  %s\n", name, occ, grid, best,
          flops / best / 1e9, ndiff, err ? cudaGetErrorString(err) : "");
 }
