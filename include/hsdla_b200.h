@@ -134,9 +134,12 @@ typedef struct hsdla_b200_options {
 /* Ledger key order: gemm, hemm, her2k, herk, scaling, herkx, potrf, trmm, total
  * (flop_ledger.hpp; values == pipeline::flop_model, pipeline.cpp:336-364). */
 typedef struct hsdla_b200_stats {
-  double phase_seconds[HSDLA_B200_N_PHASES]; /* device (CUDA-event) time per phase slot, max over GPUs */
+  double phase_seconds[HSDLA_B200_N_PHASES]; /* device time per phase slot, max over GPUs: from the
+                                                 kernels' own %globaltimer stamps (first kernel's
+                                                 start .. last kernel's end of each phase op) */
   double h2d_seconds;        /* host->device upload of A, B, T, U */
-  double device_seconds;     /* first phase start .. H,S reduced on the root GPU */
+  double device_seconds;     /* first kernel's start .. last kernel's end (launch stamps); with a
+                                multi-GPU reduce: CUDA events, first phase .. H,S reduced */
   double reduce_seconds;     /* NCCL reduce tail after the last contraction (0 on 1 GPU) */
   double d2h_seconds;        /* packed-triangle download + unpack into H, S */
   double total_seconds;      /* wall time of the call */

@@ -64,7 +64,8 @@ void run(const char* name, double2* A, double2* B, double2* out, uint64_t K, uin
   P.sk_ws = ws;
   P.sk_flags = flags;
   static uint32_t epoch = 0;
-  int grid = 148 * MINB;
+  const char* gs = getenv("TUNE_GRID");  // fewer persistent CTAs than SMs (memory-system probe)
+  int grid = gs ? atoi(gs) : 148 * MINB;
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::kThreads, Cfg::kSmemBytes);
   auto launch2 = [&] {
