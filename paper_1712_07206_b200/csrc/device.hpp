@@ -48,23 +48,24 @@ int tri_band();
 
 // ---- elementwise / batched helpers (elementwise.cu) ------------------------------
 // `stamp` (optional, every launcher): the launch timestamp slot of the engine's phase timing
-// (stamp.cuh).  The contraction launchers take it in CtnParams::stamp.
+// (stamp.cuh).  The contraction launchers take it in CtnParams::stamp.  These return whether they
+// launched (false for an empty range: the slot was not written).
 // X = diag(u) B for rows [0, Kc) of a K-strided stack (kernels.cpp:438-450).
-void launch_diag_scale(const double2* B, const double* u, double2* X, uint64_t Kc, uint64_t ld, uint64_t ng,
+bool launch_diag_scale(const double2* B, const double* u, double2* X, uint64_t Kc, uint64_t ld, uint64_t ng,
                        cudaStream_t s, unsigned long long* stamp = nullptr);
 // Counter-based synthetic fill ~ U(lo, hi) (timing sweeps; not the reference generator).
 void launch_fill_uniform(double* p, uint64_t n, uint64_t seed, double lo, double hi, unsigned grid, cudaStream_t s);
 // Operator expansion from the lower triangles (see elementwise.cu).
 // wl != nullptr (merged algorithm): only the stacked left operand of W = M Y is written,
 // per atom [Paa | Tab] (k over A rows) then [Pab | Pbb] (k over B rows), 4 N_L^2 complex.
-void launch_expand_hermitian(const double2* taa, const double2* tbb, double2* paa, double2* pbb, int nl,
+bool launch_expand_hermitian(const double2* taa, const double2* tbb, double2* paa, double2* pbb, int nl,
                              uint64_t total, double bscale, const double2* tab, double2* wl, cudaStream_t s,
                              unsigned long long* stamp = nullptr);
 // kernels::potrf for nb blocks (potrf.cuh); n_fail nullable.
-void launch_potrf_batched(const double2* taa, double2* q, int32_t* info, int nl, uint64_t nb, int* n_fail,
+bool launch_potrf_batched(const double2* taa, double2* q, int32_t* info, int nl, uint64_t nb, int* n_fail,
                           cudaStream_t s, unsigned long long* stamp = nullptr);
 // X2 = info < 0 ? X1 : A, rows [0, Kc) (potrf.cuh).
-void launch_select_left(const double2* X1, const double2* A, const int32_t* info, double2* X2, uint64_t Kc,
+bool launch_select_left(const double2* X1, const double2* A, const int32_t* info, double2* X2, uint64_t Kc,
                         uint64_t ld, uint64_t ng, int nl, cudaStream_t s, unsigned long long* stamp = nullptr);
 // out[i] = sum_r in[r][i] for i in [0, n) (r = 0 .. nin-1 in order; out may alias an input):
 // the owner's sum of the partial packed H/S of engines that share one device.

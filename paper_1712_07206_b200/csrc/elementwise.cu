@@ -122,12 +122,13 @@ __global__ void sum_partials_kernel(double2* __restrict__ out, const SumIn in, i
   }
 }
 
-void launch_diag_scale(const double2* B, const double* u, double2* X, uint64_t Kc, uint64_t ld, uint64_t ng,
+bool launch_diag_scale(const double2* B, const double* u, double2* X, uint64_t Kc, uint64_t ld, uint64_t ng,
                        cudaStream_t s, unsigned long long* stamp) {
-  if (!Kc || !ng) return;
+  if (!Kc || !ng) return false;
   const dim3 g(static_cast<unsigned>((Kc + 255) / 256), static_cast<unsigned>(std::min<uint64_t>(ng, 2048)));
   diag_scale_kernel<<<g, 256, 0, s>>>(B, u, X, Kc, ld, ng, stamp);
   HS_CUDA(cudaGetLastError());
+  return true;
 }
 
 void launch_fill_uniform(double* p, uint64_t n, uint64_t seed, double lo, double hi, unsigned grid, cudaStream_t s) {
@@ -135,28 +136,31 @@ void launch_fill_uniform(double* p, uint64_t n, uint64_t seed, double lo, double
   HS_CUDA(cudaGetLastError());
 }
 
-void launch_expand_hermitian(const double2* taa, const double2* tbb, double2* paa, double2* pbb, int nl,
+bool launch_expand_hermitian(const double2* taa, const double2* tbb, double2* paa, double2* pbb, int nl,
                              uint64_t total, double bscale, const double2* tab, double2* wl, cudaStream_t s,
                              unsigned long long* stamp) {
-  if (!total) return;
+  if (!total) return false;
   expand_hermitian_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(taa, tbb, paa, pbb, nl, total,
                                                                                       bscale, tab, wl, stamp);
   HS_CUDA(cudaGetLastError());
+  return true;
 }
 
-void launch_potrf_batched(const double2* taa, double2* q, int32_t* info, int nl, uint64_t nb, int* n_fail,
+bool launch_potrf_batched(const double2* taa, double2* q, int32_t* info, int nl, uint64_t nb, int* n_fail,
                           cudaStream_t s, unsigned long long* stamp) {
-  if (!nb) return;
+  if (!nb) return false;
   potrf_batched_kernel<<<static_cast<unsigned>(nb), 128, 0, s>>>(taa, q, info, nl, n_fail, stamp);
   HS_CUDA(cudaGetLastError());
+  return true;
 }
 
-void launch_select_left(const double2* X1, const double2* A, const int32_t* info, double2* X2, uint64_t Kc,
+bool launch_select_left(const double2* X1, const double2* A, const int32_t* info, double2* X2, uint64_t Kc,
                         uint64_t ld, uint64_t ng, int nl, cudaStream_t s, unsigned long long* stamp) {
-  if (!Kc || !ng) return;
+  if (!Kc || !ng) return false;
   const dim3 g(static_cast<unsigned>((Kc + 255) / 256), static_cast<unsigned>(std::min<uint64_t>(ng, 2048)));
   select_left_kernel<<<g, 256, 0, s>>>(X1, A, info, X2, Kc, ld, ng, nl, stamp);
   HS_CUDA(cudaGetLastError());
+  return true;
 }
 
 void launch_sum_partials(double2* out, const double2* const* in, int nin, uint64_t n, cudaStream_t s) {

@@ -687,6 +687,13 @@ static unsigned long long* take_stamp(hsdla_b200_engine* e) {
   if (p) ++e->stamp_used;
   return p;
 }
+// A launcher that may launch nothing (an empty range) takes a slot only when it launched, so no
+// slot keeps an earlier build's times.
+template <class F>
+static void stamped(hsdla_b200_engine* e, F&& launch) {
+  unsigned long long* p = stamp_slots(e, 1);
+  if (launch(p) && p) ++e->stamp_used;
+}
 
 // Build brackets.  ev_end orders the downloads after the build; the timing events exist for the
 // reduce's timeline only (a timing event on the compute stream costs 30-55 us while a copy is in
@@ -816,9 +823,11 @@ void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool last, hsd
     // operator expansion (lower triangles of T_AA, T_BB only) for this chunk's atoms
     const uint64_t total = nac * nl * nl, off = cp.a0 * nl * nl;
     const bool merged = algo == HSDLA_B200_ALGO_REFINED_MERGED;
-    launch_expand_hermitian(e->Taa + off, e->Tbb + off, e->Paa + off, e->Pbb + off, static_cast<int>(nl), total,
-                            merged ? 1.0 : 0.5, e->Tab + off, merged ? e->Wl + 4 * off : nullptr, s,
-                            take_stamp(e));
+    stamped(e, [&](unsigned long long* st) {
+      return launch_expand_hermitian(e->Taa + off, e->Tbb + off, e->Paa + off, e->Pbb + off, static_cast<int>(nl),
+                                     total, merged ? 1.0 : 0.5, e->Tab + off, merged ? e->Wl + 4 * off : nullptr, s,
+                                     st);
+    });
     ++e->launches;
   };
   // operators uploaded on the copy stream (engine_upload_operators): wait before expanding
@@ -829,7 +838,9 @@ void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool last, hsd
   auto phase_s = [&] {
     timed_op(e, HSDLA_B200_PHASE_S, [&] {
       if (e->wait_before_s) HS_CUDA(cudaStreamWaitEvent(s, e->wait_before_s, 0));
-      launch_diag_scale(cp.B + r0, e->U + r0, e->X1 + r0, Kc, e->K, ncol, s, take_stamp(e));
+      stamped(e, [&](unsigned long long* st) {
+        return launch_diag_scale(cp.B + r0, e->U + r0, e->X1 + r0, Kc, e->K, ncol, s, st);
+      });
       ++e->launches;
       if (kt) HS_CUDA(cudaEventRecord(kt->s0, s));
       launch_tri(e, s_rest ? cp.sB : cp.s, cp.grid_tri);
@@ -856,12 +867,16 @@ void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool last, hsd
     phase_s();
     timed_op(e, HSDLA_B200_PHASE_CHOL_LOOP, [&] {
       if (cp.a0 == 0) HS_CUDA(cudaMemsetAsync(e->n_fail, 0, sizeof(int), s));  // first chunk of the build
-      launch_potrf_batched(e->Taa + cp.a0 * nl * nl, e->Paa + cp.a0 * nl * nl, e->info + cp.a0,
-                           static_cast<int>(nl), nac, e->n_fail, s, take_stamp(e));
+      stamped(e, [&](unsigned long long* st) {
+        return launch_potrf_batched(e->Taa + cp.a0 * nl * nl, e->Paa + cp.a0 * nl * nl, e->info + cp.a0,
+                                    static_cast<int>(nl), nac, e->n_fail, s, st);
+      });
       ++e->launches;
       launch_bat(e, cp.x, cp.grid_bat);  // W_a = Q_a^H A_a: trmm (HPD) or hemm (failed)
-      launch_select_left(e->X1 + r0, cp.A + r0, e->info + cp.a0, e->X2 + r0, Kc, e->K, ncol,
-                         static_cast<int>(nl), s, take_stamp(e));
+      stamped(e, [&](unsigned long long* st) {
+        return launch_select_left(e->X1 + r0, cp.A + r0, e->info + cp.a0, e->X2 + r0, Kc, e->K, ncol,
+                                  static_cast<int>(nl), s, st);
+      });
       ++e->launches;
     });
     timed_op(e, HSDLA_B200_PHASE_H_AA_UPDATE, [&] { final_h(cp.haa); });
