@@ -1114,7 +1114,7 @@ void engine_kpoints(hsdla_b200_engine* e, const hsdla_b200_problem* common, uint
       p0.A = A[0];
       p0.B = B[0];
       p0.n_g = ng_of(0);
-      e->band_final_h = true;
+      e->band_final_h = nk == 1 || env_double("HSDLA_B200_KPOINT_BANDS", 0) != 0;
       try {
         engine_build_streamed(e, &p0, 0, algo);
       } catch (...) {
@@ -1128,7 +1128,9 @@ void engine_kpoints(hsdla_b200_engine* e, const hsdla_b200_problem* common, uint
       continue;
     }
     begin_build(e, algo);
-    e->band_final_h = true;
+    // only the last k-point's final H runs in bands: every earlier download overlaps the next
+    // build anyway, and the bands' launches cost ~1 % of a build
+    e->band_final_h = k + 1 == nk || env_double("HSDLA_B200_KPOINT_BANDS", 0) != 0;
     HS_CUDA(cudaStreamWaitEvent(e->stream, e->ev_kup[set], 0));
     mark_build_begin(e);
     // S and H storage: k-1's downloads (enqueued in the previous iteration) first
