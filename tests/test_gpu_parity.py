@@ -525,11 +525,14 @@ def test_kpoint_batch_matches_per_call_builds(pinned):
         hb.release_cache()
 
 
-def test_kpoint_batch_banded_final_h_storage_reuse():
-    """N_G = 2240 (35 tile columns, 630 lower tiles >= 4 x 148): every k-point's final H runs
-    band by band, and build k reuses the H, S storage while the banded D2H of k-1 is still in
-    flight (build k waits on k-1's last band download and on its S download).  Every k-point
-    equals its own per-call build."""
+@pytest.mark.parametrize("every_k", [False, True])
+def test_kpoint_batch_banded_final_h_storage_reuse(every_k, monkeypatch):
+    """N_G = 2240 (35 tile columns, 630 lower tiles >= 4 x 148): the last k-point's final H runs
+    band by band (HSDLA_B200_KPOINT_BANDS=1: every k-point's), and build k reuses the H, S storage
+    while the D2H of k-1 is still in flight (build k waits on k-1's last H piece download and on
+    its S download).  Every k-point equals its own per-call build."""
+    if every_k:
+        monkeypatch.setenv("HSDLA_B200_KPOINT_BANDS", "1")
     ng = 2240
     base = hb.generate_problem(6, 16, ng, 3, 1)
     kps = [hb.generate_problem(6, 16, ng, 20 + k, 1) for k in range(4)]
