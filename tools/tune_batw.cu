@@ -66,11 +66,11 @@ static void tile_report() {
 }
 #endif
 
-template <int BN, int PW = 4>
+template <int BN, int ST = 8, int KSUB = 1>
 static void run(uint64_t na, uint64_t nl, uint64_t ng) {
-  constexpr int BM = 24, ST = 8;
-  using Cfg = CtnCfg<kBatch, BM, BN, 1, 8, ST, 1, PW>;
-  auto kern = ctn_contract_kernel<kBatch, BM, BN, 1, 8, ST, 1, 1, 1, PW>;
+  constexpr int BM = 24, PW = 4;
+  using Cfg = CtnCfg<kBatch, BM, BN, 1, 8, ST, KSUB, PW>;
+  auto kern = ctn_contract_kernel<kBatch, BM, BN, 1, 8, ST, 1, 1, KSUB, PW>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
   const uint64_t K = na * nl, blk = nl * nl;
   double2 *A, *B, *Wl, *X1, *X2;
@@ -123,7 +123,8 @@ static void run(uint64_t na, uint64_t nl, uint64_t ng) {
   cudaError_t err = cudaGetLastError();
   // useful flops at 6 per complex MAC (3M): (2 N_L)^2 N_G per atom
   const double useful = 6.0 * 4.0 * nl * nl * ng * na;
-  printf("W 24x%d PW %d: %d tiles  %.3f ms  useful %.2f TF/s (%.3f of 37.0)  %s\n", BN, PW, P.bat_tiles, best,
+  printf("W 24x%d stages %d ksub %d: %d tiles  %.3f ms  useful %.2f TF/s (%.3f of 37.0)  %s\n", BN, ST, KSUB,
+         P.bat_tiles, best,
          useful / best / 1e9, useful / best / 1e9 / 37.0, err ? cudaGetErrorString(err) : "");
   {  // bitwise comparison against the first variant's output
     static std::vector<double> ref;
@@ -148,5 +149,11 @@ int main(int argc, char** argv) {
   printf("N_A %lu N_L %lu N_G %lu\n", na, nl, ng);
   run<192>(na, nl, ng);
   run<128>(na, nl, ng);
+  if (getenv("TUNE_VARIANTS")) {
+    run<192, 6>(na, nl, ng);
+    run<192, 7>(na, nl, ng);
+    run<192, 4, 2>(na, nl, ng);
+    run<128, 6, 2>(na, nl, ng);
+  }
   return 0;
 }
