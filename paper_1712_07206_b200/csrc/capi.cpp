@@ -291,6 +291,9 @@ static void one_shot(const hsdla_b200_options* o, uint64_t na, uint64_t nl, uint
   const int mode = o && (o->flags & HSDLA_B200_FLAG_REDUCE_ROOT) ? kReduceRoot : kReduceScatter;
   const std::vector<int> devs = devices_of(o);
   const int P = static_cast<int>(devs.size());
+  if (trace_on())
+    std::fprintf(stderr, "[hsdla_b200 trace] call start at %.3f ms (host clock)\n",
+                 std::chrono::duration<double, std::milli>(t0.time_since_epoch()).count());
   std::lock_guard<std::mutex> lk(g_cache_mu);
   const int pc = choose_col_groups(o, devs, na, nl, ng);
   EngineSet* set = get_engines(devs, na, nl, ng, pc);
