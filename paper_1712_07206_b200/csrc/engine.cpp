@@ -621,21 +621,22 @@ static void upload_atoms_staged(hsdla_b200_engine* e, int set, const hsdla_b200_
     // pack pieces of ~1/div of the matrix (1 MB .. one slab): the DMA of piece i overlaps
     // the packing of piece i+1
     static const double div = std::max(1.0, env_double("HSDLA_B200_PIECE_DIV", 4.0));
+    const size_t sp = slab_pitch(colb);  // each column's rows on a 4 KB boundary of the slab
     const uint64_t piece = std::min<uint64_t>(kStageSlab, std::max<uint64_t>(uint64_t(1) << 20,
-                                              static_cast<uint64_t>(static_cast<double>(colb * cols) / div)));
-    const uint64_t per = std::max<uint64_t>(1, piece / colb);
+                                              static_cast<uint64_t>(static_cast<double>(sp * cols) / div)));
+    const uint64_t per = std::max<uint64_t>(1, piece / sp);
     for (uint64_t j0 = 0; j0 < cols; j0 += per) {
       const uint64_t nc = std::min(per, cols - j0);
       int slot;
       char* b = stage_acquire(e, slot);
       const double t0 = trace_on() ? host_ms() : 0.0;
-      par_for(nc, nc * colb, [&](uint64_t j) { copy_nt(b + j * colb, src + (j0 + j) * Kg, colb); });
+      par_for(nc, nc * colb, [&](uint64_t j) { copy_nt(b + j * sp, src + (j0 + j) * Kg, colb); });
       _mm_sfence();  // the single-threaded case of par_for
       if (trace_on()) {
         e->tr_pack_ms += host_ms() - t0;
         e->tr_pack_bytes += nc * colb;
       }
-      HS_CUDA(cudaMemcpy2DAsync(dst + j0 * e->K, e->K * sizeof(double2), b, colb, colb, nc, cudaMemcpyHostToDevice,
+      HS_CUDA(cudaMemcpy2DAsync(dst + j0 * e->K, e->K * sizeof(double2), b, sp, colb, nc, cudaMemcpyHostToDevice,
                                 s));
       stage_release(e, slot, s);
     }

@@ -274,6 +274,10 @@ void mark_build_begin(hsdla_b200_engine* e);
 void mark_build_end(hsdla_b200_engine* e);
 void enqueue_chunk(hsdla_b200_engine* e, ChunkPlan& cp, int algo, bool last, hsdla_b200_engine::KTimer* kt,
                    bool s_rest = false);
+// Row pitch of a packed staging slab: each column's rows start on a 4 KB boundary.  A 2-D H2D
+// from rows packed back to back crosses host pages mid-row and runs at 22 / 40 GB/s for 2.6 /
+// 6.5 KB rows; 4 KB-aligned rows go at 53-55 (the link rate; tools/h2d_rows.cu).
+inline size_t slab_pitch(size_t colb) { return (colb + 4095) & ~size_t(4095); }
 char* stage_acquire(hsdla_b200_engine* e, int& slot);
 void stage_release(hsdla_b200_engine* e, int slot, cudaStream_t s);
 

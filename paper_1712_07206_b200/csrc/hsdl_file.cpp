@@ -79,7 +79,8 @@ int open_hsdl(const char* path) {
 
 // Read `n` pieces of `piece` bytes at offsets off0 + i*stride into dst (packed),
 // split over up to 8 threads.
-static void pread_pieces(int fd, char* dst, uint64_t off0, uint64_t stride, size_t piece, uint64_t n) {
+static void pread_pieces(int fd, char* dst, uint64_t off0, uint64_t stride, size_t piece, uint64_t n,
+                         size_t dpitch) {
   const uint64_t bytes = piece * n;
   const unsigned nt = bytes < (size_t(8) << 20) ? 1u : std::min<unsigned>(HostPool::get().width(), static_cast<unsigned>(n));
   std::vector<Fail> errs(nt);
@@ -87,10 +88,10 @@ static void pread_pieces(int fd, char* dst, uint64_t off0, uint64_t stride, size
   HostPool::get().run(nt, [&](uint64_t t) {
     const uint64_t i0 = n * t / nt, i1 = n * (t + 1) / nt;
     try {
-      if (stride == piece) {
+      if (stride == piece && dpitch == piece) {
         pread_all(fd, dst + i0 * piece, (i1 - i0) * piece, off0 + i0 * stride);
       } else {
-        for (uint64_t i = i0; i < i1; ++i) pread_all(fd, dst + i * piece, piece, off0 + i * stride);
+        for (uint64_t i = i0; i < i1; ++i) pread_all(fd, dst + i * dpitch, piece, off0 + i * stride);
       }
     } catch (const Fail& f) {
       errs[t] = f;
@@ -125,13 +126,14 @@ static const char* file_view(hsdla_b200_engine* e, int fd) {
 // pread_pieces through the file view when there is one: copy_nt from the mapped page cache
 // on the host pool (no syscall per piece)
 static void read_pieces(hsdla_b200_engine* e, const char* view, int fd, char* dst, uint64_t off0, uint64_t stride,
-                        size_t piece, uint64_t n) {
+                        size_t piece, uint64_t n, size_t dpitch = 0) {
+  if (!dpitch) dpitch = piece;
   if (!view) {
-    pread_pieces(fd, dst, off0, stride, piece, n);
+    pread_pieces(fd, dst, off0, stride, piece, n, dpitch);
     return;
   }
   if (n && off0 + (n - 1) * stride + piece > e->fmap_len) throw Fail{HSDLA_B200_IO_ERROR, "truncated problem file"};
-  par_for(n, n * piece, [&](uint64_t i) { copy_nt(dst + i * piece, view + off0 + i * stride, piece); });
+  par_for(n, n * piece, [&](uint64_t i) { copy_nt(dst + i * dpitch, view + off0 + i * stride, piece); });
   _mm_sfence();
 }
 
@@ -159,13 +161,14 @@ static void load_atoms_from_file(hsdla_b200_engine* e, int fd, const HsdlHeader&
         }
       continue;
     }
-    const uint64_t cols = std::max<uint64_t>(1, kStageSlab / colb);
+    const size_t sp = colb == Kf * 16 ? colb : slab_pitch(colb);  // 4 KB-aligned rows (engine.hpp)
+    const uint64_t cols = std::max<uint64_t>(1, kStageSlab / sp);
     for (uint64_t j0 = 0; j0 < ng; j0 += cols) {
       const uint64_t nc = std::min(cols, ng - j0);
       int slot;
       char* b = stage_acquire(e, slot);
-      read_pieces(e, view, fd, b, base + j0 * Kf * 16, Kf * 16, colb, nc);
-      HS_CUDA(cudaMemcpy2DAsync(dst + j0 * K, K * sizeof(double2), b, colb, colb, nc, cudaMemcpyHostToDevice, s));
+      read_pieces(e, view, fd, b, base + j0 * Kf * 16, Kf * 16, colb, nc, sp);
+      HS_CUDA(cudaMemcpy2DAsync(dst + j0 * K, K * sizeof(double2), b, sp, colb, nc, cudaMemcpyHostToDevice, s));
       stage_release(e, slot, s);
     }
   }
