@@ -1,7 +1,7 @@
 """k-point batch throughput (hsdla_b200_build_hs_kpoints) against per-call drop-in builds
 (development helper): n k-points of one cell, pinned and pageable coefficients.
 
-    python tools/kpoint_probe.py [c2|c3] [--nk 8]
+    python tools/kpoint_probe.py [c1|c2|c3] [--nk 8]
 """
 import argparse
 import os
@@ -13,7 +13,7 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1712_07206_b200 as hb  # noqa: E402
 
-CFG = {"c2": (64, 81, 3000), "c3": (108, 121, 6000)}
+CFG = {"c1": (16, 49, 1000), "c2": (64, 81, 3000), "c3": (108, 121, 6000)}
 ap = argparse.ArgumentParser()
 ap.add_argument("config", nargs="?", default="c2")
 ap.add_argument("--nk", type=int, default=8)
