@@ -48,6 +48,8 @@ void engine_free(hsdla_b200_engine* e) {
                   (void*)e->Wl, (void*)e->U, (void*)e->Hp, (void*)e->Sp, (void*)e->d_stamp})
     if (p) cudaFree(p);
   if (e->host_stage) cudaFreeHost(e->host_stage);
+  for (double2* st : e->host_stage_x)
+    if (st) cudaFreeHost(st);
   release_file_view(e);
   for (cudaEvent_t ev : {e->ev_kup[0], e->ev_kup[1], e->ev_kbuilt[0], e->ev_kbuilt[1]})
     if (ev) cudaEventDestroy(ev);
@@ -59,10 +61,10 @@ void engine_free(hsdla_b200_engine* e) {
   for (cudaEvent_t ev : e->tr_pool) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e->ev_chunk_up) cudaEventDestroy(ev);
   for (int q = 0; q < hsdla_b200_engine::kD2hPieces; ++q)
-    for (cudaEvent_t ev : {e->ev_h_band[q], e->ev_h_red[q], e->ev_dl_h[q]})
+    for (cudaEvent_t ev : {e->ev_h_band[q], e->ev_h_red[q], e->ev_dl_h[q], e->ev_dlx_h[0][q], e->ev_dlx_h[1][q]})
       if (ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : {e->ev_a0, e->ev_ops, e->ev_cs_order, e->ev_begin, e->ev_end, e->ev_end_t, e->ev_s_done, e->ev_s_red, e->ev_reduce_end,
-                         e->ev_up0, e->ev_up1, e->ev_dl_s, e->ev_setup0, e->ev_setup1, e->ev_setup_mid})
+                         e->ev_up0, e->ev_up1, e->ev_dl_s, e->ev_dlx_s[0], e->ev_dlx_s[1], e->ev_setup0, e->ev_setup1, e->ev_setup_mid})
     if (ev) cudaEventDestroy(ev);
   for (auto& t : e->ring)
     for (cudaEvent_t ev : {t.s0, t.s1, t.h0, t.h1})
@@ -1091,6 +1093,13 @@ void engine_kpoints(hsdla_b200_engine* e, const hsdla_b200_problem* common, uint
   for (uint64_t k = 0; k < nk; ++k)
     if (ng_of(k) < 1 || ng_of(k) > e->cap_cols) throw Fail{HSDLA_B200_SIZING_ERROR, "N_G(k) exceeds the engine capacity"};
   ensure_kpoints(e, algo);
+  // download slots in rotation: k-point k downloads into slot k % depth and the host unpacks
+  // k - depth + 1 after enqueueing build k and k's D2H.  Depth 3 keeps the next build queued
+  // on the GPU while the host unpacks (small cells: the host loop, not the GPU, set the pace
+  // at depth 2); large stages (> 256 MB pinned each) stay at 2, their builds hide the unpack.
+  static const double slot_mb = env_double("HSDLA_B200_KPOINT_SLOT_MB", 256.0);
+  const int depth = 2 * e->cap_pk * sizeof(double2) <= slot_mb * (1 << 20) ? hsdla_b200_engine::kDlSlots : 2;
+  auto slot_of = [&](uint64_t k) { return static_cast<int>(k % depth); };
   auto upload = [&](uint64_t k) {
     hsdla_b200_problem pk = *common;
     pk.A = A[k];
@@ -1134,9 +1143,10 @@ void engine_kpoints(hsdla_b200_engine* e, const hsdla_b200_problem* common, uint
     e->band_final_h = k + 1 == nk || env_double("HSDLA_B200_KPOINT_BANDS", 0) != 0;
     HS_CUDA(cudaStreamWaitEvent(e->stream, e->ev_kup[set], 0));
     mark_build_begin(e);
-    // S and H storage: k-1's downloads (enqueued in the previous iteration) first
-    e->wait_before_s = e->ev_dl_s;
-    e->wait_before_h = e->ev_dl_h[hsdla_b200_engine::kD2hPieces - 1];
+    // S and H storage: k-1's downloads (enqueued in the previous iteration, download slot
+    // (k-1) & 1) first
+    e->wait_before_s = download_done_s(e, slot_of(k - 1));
+    e->wait_before_h = download_done_h(e, slot_of(k - 1));
     try {
       enqueue_chunk(e, set ? e->whole2[0] : e->whole[0], algo, true, nullptr);
     } catch (...) {
@@ -1151,14 +1161,20 @@ void engine_kpoints(hsdla_b200_engine* e, const hsdla_b200_problem* common, uint
     const double t_enq = trace_on() ? host_ms() : 0.0;
     if (k + 1 < nk) upload(k + 1);  // overlaps build k
     const double t_up = trace_on() ? host_ms() : 0.0;
-    finish_download(e, H[k - 1], S[k - 1], std::chrono::steady_clock::now());  // overlaps build k
-    enqueue_download(e);
+    // k's D2H goes on the copy stream BEFORE the host unpacks an earlier k-point (another
+    // download slot), so it starts as soon as build k ends instead of after the unpack
+    enqueue_download(e, slot_of(k));
+    if (k + 1 >= static_cast<uint64_t>(depth)) {  // overlaps build k
+      const uint64_t j = k + 1 - depth;
+      finish_download(e, H[j], S[j], std::chrono::steady_clock::now(), slot_of(j));
+    }
     if (trace_on())
       std::fprintf(stderr, "[hsdla_b200 trace] k-point %llu: build enqueued %.2f, upload enqueued +%.2f, "
                    "previous download finished +%.2f ms\n", static_cast<unsigned long long>(k), t_enq,
                    t_up - t_enq, host_ms() - t_up);
   }
-  finish_download(e, H[nk - 1], S[nk - 1], std::chrono::steady_clock::now());
+  for (uint64_t j = nk + 1 > static_cast<uint64_t>(depth) ? nk + 1 - depth : 0; j < nk; ++j)
+    finish_download(e, H[j], S[j], std::chrono::steady_clock::now(), slot_of(j));
 }
 
 }  // namespace hsdla_b200

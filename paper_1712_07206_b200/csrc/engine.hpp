@@ -126,6 +126,7 @@ struct hsdla_b200_engine {
   int* n_fail = nullptr;          // original algorithm: failed atoms so far in this build
   double2 *Hp = nullptr, *Sp = nullptr;
   double2* host_stage = nullptr;  // pinned, 2 * cap_pk (H at [0, npk), S at [cap_pk, cap_pk + npk))
+  double2* host_stage_x[2] = {};  // download slots 1, 2 (k-point batches), same layout
   int sms = 148;                  // persistent TRI grid
   double* sk_ws = nullptr;        // stream-K workspace (sms slots x 64x64 complex)
   uint32_t* sk_flags = nullptr;
@@ -168,10 +169,16 @@ struct hsdla_b200_engine {
   bool band_final_h = false;               // this build runs its final H contraction band by band
   bool overlap_dl = false;                 // engine builds band their final H (a download follows)
   bool banded = false;                     // ... and the last build did
-  // download pieces: events recorded on the copy stream (S: up to 1, H: up to kD2hPieces)
+  // download pieces: events recorded on the copy stream (S: up to 1, H: up to kD2hPieces).
+  // Slot 0 serves every build; a k-point batch rotates over 2 or 3 slots (stage, events,
+  // record) so k's D2H is enqueued before the host unpacks an earlier k-point.
+  static constexpr int kDlSlots = 3;
   cudaEvent_t ev_dl_s = nullptr;
   cudaEvent_t ev_dl_h[kD2hPieces] = {};
   hsdla_b200::Download dl;                 // the enqueued, not yet unpacked download
+  cudaEvent_t ev_dlx_s[2] = {};            // slots 1, 2 (created with host_stage_x)
+  cudaEvent_t ev_dlx_h[2][kD2hPieces] = {};
+  hsdla_b200::Download dlx[2];
   std::vector<cudaEvent_t> ev_chunk_up;
   int last_algo = 0, launches = 0;
   int arith = HSDLA_B200_ARITH_3M;  // complex product scheme of the contractions
@@ -250,9 +257,13 @@ void group_reduce(const std::vector<hsdla_b200_engine*>& g, int mode, int root);
 void engine_sync(hsdla_b200_engine* e, hsdla_b200_stats* st);
 // Enqueue the D2H of the packed ranges this engine owns (all of them before a reduce),
 // then unpack them into the lower triangles of H, S (either may be null).
-void enqueue_download(hsdla_b200_engine* e);
+// slot 1, 2: the further stages / event sets of k-point batches.
+void enqueue_download(hsdla_b200_engine* e, int slot = 0);
 void finish_download(hsdla_b200_engine* e, double* H, double* S,
-                     std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now());
+                     std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), int slot = 0);
+// The last event of a slot's download (the next build reusing H / S storage waits on it).
+cudaEvent_t download_done_s(hsdla_b200_engine* e, int slot);
+cudaEvent_t download_done_h(hsdla_b200_engine* e, int slot);
 void engine_download(hsdla_b200_engine* e, double* H, double* S);
 // Packed ranges of the current result this engine holds final values for.
 std::vector<std::pair<uint64_t, uint64_t>> engine_owned(const hsdla_b200_engine* e);

@@ -281,9 +281,45 @@ void engine_sync(hsdla_b200_engine* e, hsdla_b200_stats* st) {
   st->kernel_launches = e->launches;
 }
 
-static void ensure_stage(hsdla_b200_engine* e) {
-  if (!e->host_stage)
-    HS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&e->host_stage), 2 * e->cap_pk * sizeof(double2)));
+// One download slot: its pinned stage, its copy-stream events and its record.
+struct DlSlot {
+  double2* stage;
+  cudaEvent_t ev_s;
+  cudaEvent_t* ev_h;
+  Download& d;
+};
+
+// Slot 0's stage is allocated on first use; slots 1 and 2 (k-point batches) get their stage
+// and events all-or-nothing on first use.
+static DlSlot dl_slot(hsdla_b200_engine* e, int slot) {
+  if (slot == 0) {
+    if (!e->host_stage)
+      HS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&e->host_stage), 2 * e->cap_pk * sizeof(double2)));
+    return {e->host_stage, e->ev_dl_s, e->ev_dl_h, e->dl};
+  }
+  const int x = slot - 1;
+  if (!e->host_stage_x[x]) {
+    double2* st = nullptr;
+    cudaEvent_t ev[1 + hsdla_b200_engine::kD2hPieces] = {};
+    try {
+      HS_CUDA(cudaMallocHost(reinterpret_cast<void**>(&st), 2 * e->cap_pk * sizeof(double2)));
+      for (cudaEvent_t& ev1 : ev) HS_CUDA(cudaEventCreateWithFlags(&ev1, cudaEventDisableTiming));
+    } catch (...) {
+      if (st) cudaFreeHost(st);
+      for (cudaEvent_t ev1 : ev)
+        if (ev1) cudaEventDestroy(ev1);
+      throw;
+    }
+    e->ev_dlx_s[x] = ev[0];
+    for (int q = 0; q < hsdla_b200_engine::kD2hPieces; ++q) e->ev_dlx_h[x][q] = ev[1 + q];
+    e->host_stage_x[x] = st;
+  }
+  return {e->host_stage_x[x], e->ev_dlx_s[x], e->ev_dlx_h[x], e->dlx[x]};
+}
+
+cudaEvent_t download_done_s(hsdla_b200_engine* e, int slot) { return slot ? e->ev_dlx_s[slot - 1] : e->ev_dl_s; }
+cudaEvent_t download_done_h(hsdla_b200_engine* e, int slot) {
+  return (slot ? e->ev_dlx_h[slot - 1] : e->ev_dl_h)[hsdla_b200_engine::kD2hPieces - 1];
 }
 
 // Enqueue the packed-triangle D2H of the ranges this engine owns on the copy stream: S
@@ -291,10 +327,10 @@ static void ensure_stage(hsdla_b200_engine* e) {
 // reduce when banded, else after the build / its reduce), each piece's event recorded so
 // the host unpacks piece q while q+1 is on the wire.  Every event is recorded every time
 // (the next k-point's build waits on the last one).
-void enqueue_download(hsdla_b200_engine* e) {
+void enqueue_download(hsdla_b200_engine* e, int slot) {
   HS_CUDA(cudaSetDevice(e->device));
-  ensure_stage(e);
-  Download& d = e->dl;
+  const DlSlot sl = dl_slot(e, slot);
+  Download& d = sl.d;
   d.ng = e->ng;
   d.pk0 = e->pk0;
   d.seq.clear();
@@ -303,11 +339,11 @@ void enqueue_download(hsdla_b200_engine* e) {
   const std::vector<Range> own = engine_owned(e);
   HS_CUDA(cudaStreamWaitEvent(cs, e->reduced ? e->ev_s_red : e->ev_s_done, 0));
   for (const Range& o : own) {
-    HS_CUDA(cudaMemcpyAsync(e->host_stage + e->cap_pk + (o.first - e->pk0), e->Sp + (o.first - e->pk0),
+    HS_CUDA(cudaMemcpyAsync(sl.stage + e->cap_pk + (o.first - e->pk0), e->Sp + (o.first - e->pk0),
                             (o.second - o.first) * sizeof(double2), cudaMemcpyDeviceToHost, cs));
-    d.seq.push_back({0, o.first, o.second, e->ev_dl_s});
+    d.seq.push_back({0, o.first, o.second, sl.ev_s});
   }
-  HS_CUDA(cudaEventRecord(e->ev_dl_s, cs));
+  HS_CUDA(cudaEventRecord(sl.ev_s, cs));
   trace_mark(e, cs, "dl_s");
   if (!e->banded) HS_CUDA(cudaStreamWaitEvent(cs, e->reduced ? e->ev_reduce_end : e->ev_end, 0));
   for (int q = 0; q < hsdla_b200_engine::kD2hPieces; ++q) {
@@ -317,19 +353,21 @@ void enqueue_download(hsdla_b200_engine* e) {
     for (const Range& o : own) {
       const uint64_t b0 = std::max(p0, o.first), b1 = std::min(p1, o.second);
       if (b1 <= b0) continue;
-      HS_CUDA(cudaMemcpyAsync(e->host_stage + (b0 - e->pk0), e->Hp + (b0 - e->pk0), (b1 - b0) * sizeof(double2),
+      HS_CUDA(cudaMemcpyAsync(sl.stage + (b0 - e->pk0), e->Hp + (b0 - e->pk0), (b1 - b0) * sizeof(double2),
                               cudaMemcpyDeviceToHost, cs));
-      d.seq.push_back({1, b0, b1, e->ev_dl_h[q]});
+      d.seq.push_back({1, b0, b1, sl.ev_h[q]});
     }
-    HS_CUDA(cudaEventRecord(e->ev_dl_h[q], cs));
+    HS_CUDA(cudaEventRecord(sl.ev_h[q], cs));
     if (trace_on()) trace_mark(e, cs, "dl_h" + std::to_string(q));
   }
   d.pending = true;
 }
 
 // Unpack S as soon as its bytes land (H may still be computing), then H piece by piece.
-void finish_download(hsdla_b200_engine* e, double* H, double* S, std::chrono::steady_clock::time_point t0) {
-  Download& d = e->dl;
+void finish_download(hsdla_b200_engine* e, double* H, double* S, std::chrono::steady_clock::time_point t0,
+                     int slot) {
+  const DlSlot sl = dl_slot(e, slot);
+  Download& d = sl.d;
   if (!d.pending) return;
   auto ms = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); };
   std::string tr;
@@ -370,17 +408,22 @@ void finish_download(hsdla_b200_engine* e, double* H, double* S, std::chrono::st
     }
     double* dst = d.seq[i].h ? H : S;
     if (dst)
-      unpack_range(e->host_stage + (d.seq[i].h ? 0 : e->cap_pk) + (lo - d.pk0), reinterpret_cast<double2*>(dst), d.ng,
+      unpack_range(sl.stage + (d.seq[i].h ? 0 : e->cap_pk) + (lo - d.pk0), reinterpret_cast<double2*>(dst), d.ng,
                    lo, hi, release);
     i = j;
   }
-  HS_CUDA(cudaEventSynchronize(e->ev_dl_h[hsdla_b200_engine::kD2hPieces - 1]));
+  HS_CUDA(cudaEventSynchronize(sl.ev_h[hsdla_b200_engine::kD2hPieces - 1]));
   mark("h_unpacked");
   if (trace_on()) {
     std::fprintf(stderr, "[hsdla_b200 trace] download (ms since call start):%s\n", tr.c_str());
     if (!e->tr_marks.empty()) {
+      // (a k-point batch has the next build's marks in flight by now: the trace waits for
+      // them, which serialises the batch while tracing)
       std::string dv;
-      for (auto& m : e->tr_marks) dv += " " + m.first + "=" + std::to_string(ev_ms(e->tr_marks[0].second, m.second)).substr(0, 5);
+      for (auto& m : e->tr_marks) {
+        HS_CUDA(cudaEventSynchronize(m.second));
+        dv += " " + m.first + "=" + std::to_string(ev_ms(e->tr_marks[0].second, m.second)).substr(0, 5);
+      }
       std::fprintf(stderr, "[hsdla_b200 trace] device (ms since first mark):%s\n", dv.c_str());
       e->tr_marks.clear();
     }
