@@ -1097,7 +1097,7 @@ void engine_kpoints(hsdla_b200_engine* e, const hsdla_b200_problem* common, uint
   // k - depth + 1 after enqueueing build k and k's D2H.  Depth 3 keeps the next build queued
   // on the GPU while the host unpacks (small cells: the host loop, not the GPU, set the pace
   // at depth 2); large stages (> 256 MB pinned each) stay at 2, their builds hide the unpack.
-  static const double slot_mb = env_double("HSDLA_B200_KPOINT_SLOT_MB", 256.0);
+  const double slot_mb = env_double("HSDLA_B200_KPOINT_SLOT_MB", 256.0);
   const int depth = 2 * e->cap_pk * sizeof(double2) <= slot_mb * (1 << 20) ? hsdla_b200_engine::kDlSlots : 2;
   auto slot_of = [&](uint64_t k) { return static_cast<int>(k % depth); };
   auto upload = [&](uint64_t k) {

@@ -525,17 +525,21 @@ def test_kpoint_batch_matches_per_call_builds(pinned):
         hb.release_cache()
 
 
-@pytest.mark.parametrize("every_k", [False, True])
-def test_kpoint_batch_banded_final_h_storage_reuse(every_k, monkeypatch):
+@pytest.mark.parametrize("every_k,slots", [(False, 3), (True, 3), (False, 2), (True, 2)])
+def test_kpoint_batch_banded_final_h_storage_reuse(every_k, slots, monkeypatch):
     """N_G = 2240 (35 tile columns, 630 lower tiles >= 4 x 148): the last k-point's final H runs
     band by band (HSDLA_B200_KPOINT_BANDS=1: every k-point's), and build k reuses the H, S storage
     while the D2H of k-1 is still in flight (build k waits on k-1's last H piece download and on
-    its S download).  Every k-point equals its own per-call build."""
+    its S download).  The downloads rotate over 3 host slots (the host unpacks k-2 while build k
+    runs) or, for stages above HSDLA_B200_KPOINT_SLOT_MB, 2.  Every k-point equals its own
+    per-call build."""
     if every_k:
         monkeypatch.setenv("HSDLA_B200_KPOINT_BANDS", "1")
+    if slots == 2:
+        monkeypatch.setenv("HSDLA_B200_KPOINT_SLOT_MB", "0")
     ng = 2240
     base = hb.generate_problem(6, 16, ng, 3, 1)
-    kps = [hb.generate_problem(6, 16, ng, 20 + k, 1) for k in range(4)]
+    kps = [hb.generate_problem(6, 16, ng, 20 + k, 1) for k in range(5)]
     As = [q.A for q in kps]
     Bs = [q.B for q in kps]
     try:
