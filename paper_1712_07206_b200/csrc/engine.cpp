@@ -600,6 +600,11 @@ static bool is_pinned(const void* p, size_t bytes) {
   return a0.type == cudaMemoryTypeHost && a1.type == cudaMemoryTypeHost;
 }
 
+static void stage_operator_blocks(hsdla_b200_engine* e, const hsdla_b200_problem* p, uint64_t a0, uint64_t b0,
+                                  uint64_t b1, cudaStream_t s);
+static void stage_u(hsdla_b200_engine* e, const hsdla_b200_problem* p, uint64_t a0, uint64_t b0, uint64_t b1,
+                    cudaStream_t s);
+
 // upload_atoms for PAGEABLE caller buffers: the rows of atoms [b0, b1) are packed by up
 // to 16 host threads into the engine's pinned staging slabs and copied from there
 // (a pageable cudaMemcpy is host-synchronous and single-threaded, ~10 GB/s).
@@ -644,9 +649,15 @@ static void upload_atoms_staged(hsdla_b200_engine* e, int set, const hsdla_b200_
     }
   }
   if (!(parts & 4)) return;
-  // operator blocks (T_AA, T_AB, T_BB per atom), then U, through the slabs: groups of
-  // atoms whose three blocks fit one slab (large chunks of large-N_L atoms need several)
-  const uint64_t blk = nl * nl, bb = blk * sizeof(double2);
+  stage_operator_blocks(e, p, a0, b0, b1, s);
+  stage_u(e, p, a0, b0, b1, s);
+}
+
+// The operator blocks (T_AA, T_AB, T_BB) of local atoms [b0, b1) through the slabs: groups of
+// atoms whose three blocks fit one slab (large chunks of large-N_L atoms need several).
+static void stage_operator_blocks(hsdla_b200_engine* e, const hsdla_b200_problem* p, uint64_t a0, uint64_t b0,
+                                  uint64_t b1, cudaStream_t s) {
+  const uint64_t nl = e->nl, blk = nl * nl, bb = blk * sizeof(double2);
   if (3 * bb > kStageSlab) throw Fail{HSDLA_B200_SIZING_ERROR, "operator blocks larger than the staging slab"};
   const uint64_t per = std::max<uint64_t>(1, kStageSlab / (3 * bb));
   const double* srcs[3] = {p->T_AA, p->T_AB, p->T_BB};
@@ -664,6 +675,12 @@ static void upload_atoms_staged(hsdla_b200_engine* e, int set, const hsdla_b200_
       HS_CUDA(cudaMemcpyAsync(dsts[m] + c0 * blk, b + m * tb, tb, cudaMemcpyHostToDevice, s));
     stage_release(e, slot, s);
   }
+}
+
+// U of local atoms [b0, b1) through a slab.
+static void stage_u(hsdla_b200_engine* e, const hsdla_b200_problem* p, uint64_t a0, uint64_t b0, uint64_t b1,
+                    cudaStream_t s) {
+  const uint64_t nl = e->nl, r0 = b0 * nl, rows = (b1 - b0) * nl, g0 = (a0 + b0) * nl;
   const size_t ub = rows * sizeof(double);
   if (ub > kStageSlab) throw Fail{HSDLA_B200_SIZING_ERROR, "U larger than the staging slab"};
   int slot;
@@ -998,12 +1015,22 @@ void engine_build_streamed(hsdla_b200_engine* e, const hsdla_b200_problem* p, ui
     const uint64_t blk_bytes = p->n_atoms * p->n_l * p->n_l * sizeof(double2);
     const bool ops_pinned = is_pinned(p->T_AA, blk_bytes) && is_pinned(p->T_AB, blk_bytes) &&
                             is_pinned(p->T_BB, blk_bytes) && is_pinned(p->U, p->n_atoms * p->n_l * sizeof(double));
+    // Unregistered operators: every atom's U goes up with chunk 0's rows (phase s needs it) and
+    // every atom's operator blocks right after them, staged ONCE through as few slabs as hold
+    // them; the expansions wait on ev_ops.  (Staged chunk by chunk, a later chunk's slab waited
+    // for a DMA queued behind the earlier chunks' A, B rows, blocking this host loop — and the
+    // first launch — for milliseconds: C2 22.0 ms per call.)
     for (size_t c = 0; c < plan.size(); ++c) {
       upload_atoms(e, 0, p, a0, plan[c].a0, plan[c].a1, e->copy_stream, c == 0 && split ? e->ev_a0 : nullptr,
                    ops_pinned ? 7 : 3);
-      if (!ops_pinned) upload_atoms_staged(e, 0, p, a0, plan[c].a0, plan[c].a1, e->copy_stream, 4);
+      if (c == 0 && !ops_pinned) stage_u(e, p, a0, 0, e->na, e->copy_stream);
       HS_CUDA(cudaEventRecord(e->ev_chunk_up[c], e->copy_stream));
       if (trace_on()) trace_mark(e, e->copy_stream, "up" + std::to_string(c));
+      if (c == 0 && !ops_pinned) {
+        stage_operator_blocks(e, p, a0, 0, e->na, e->copy_stream);
+        HS_CUDA(cudaEventRecord(e->ev_ops, e->copy_stream));
+        e->ops_pending = true;
+      }
     }
   }
   for (size_t c = 0; c < plan.size(); ++c) {
@@ -1032,6 +1059,7 @@ void engine_build_streamed(hsdla_b200_engine* e, const hsdla_b200_problem* p, ui
   }
   HS_CUDA(cudaEventRecord(e->ev_up1, e->copy_stream));
   mark_build_end(e);
+  e->ops_pending = false;  // every expansion of this build waited for them
   e->uploaded_streamed = true;
   if (trace_on() && !pinned) {
     std::fprintf(stderr, "[hsdla_b200 trace] pageable staging: packed %.0f MB in %.1f ms (%.1f GB/s), waited %.1f ms "

@@ -400,6 +400,33 @@ def test_pageable_and_pinned_inputs_agree_bitwise_with_multi_slab_operator_chunk
     assert rel(np.asfortranarray(a.S[np.ix_(J, J)]), Ss) <= TOL
 
 
+@pytest.mark.parametrize("algo", ["merged", "refined", "original"])
+def test_registered_rows_with_pageable_operators(algo, monkeypatch):
+    """A caller who page-locks A and B but not the operator blocks: the rows are copied straight
+    from the caller's buffers in the chunk plan, and every atom's T_AA, T_AB, T_BB and U go up
+    once, staged after the first chunk's rows (here 70 MB, two 64 MB slabs), with each
+    expansion waiting for them.  Bitwise equal to the build with everything registered."""
+    monkeypatch.setenv("HSDLA_B200_STREAM_PLAN", "20,100")
+    hb.release_cache()
+    p = hb.generate_problem(120, 121, 300, 6, 7)
+    run = (lambda: hb.build_hs_original(p)) if algo == "original" else \
+        (lambda: hb.build_hs_refined(p, hb.PipelineConfig(algo=algo)))
+    out = []
+    try:
+        for bufs in ([p.A, p.B], [p.A, p.B, p.T_AA, p.T_AB, p.T_BB, p.U]):
+            for b in bufs:
+                hb.host_register(b)
+            try:
+                out.append(run())
+            finally:
+                for b in bufs:
+                    hb.host_unregister(b)
+    finally:
+        hb.release_cache()
+    assert np.array_equal(out[0].H, out[1].H) and np.array_equal(out[0].S, out[1].S)
+    assert out[0].ledger.total() == out[1].ledger.total()
+
+
 def test_engine_download_overlap_matches_whole_build():
     """hsdla_b200_engine_set_download_overlap: the device-resident build bands its final H
     contraction (band downloads overlap the remaining bands); same H, S to rounding."""
